@@ -1,0 +1,132 @@
+"""Pins for oracle/static_near.py and oracle/precorrection.py (not gpu).
+
+The closed-form inner integrals are checked against brute-force quadrature
+(numpy Gauss-Legendre, with a Duffy-type split at the singular point), the
+assembled static entries against rigid-motion invariance and positivity, and
+the grouped precorrection against the dense definition W H_s P.
+"""
+import numpy as np
+import pytest
+
+import aimx_inputs as inp
+from oracle.mesh import build_rwg
+from oracle.precorrection import precorrection, precorrection_dense
+from oracle.static_near import static_pair_entries, triangle_potentials
+
+
+def _gl_tri(q):
+    """Product rule on the unit square, graded in u (geometric panels toward
+    u = 0) so that near-singular integrands at the apex are resolved."""
+    x, w = np.polynomial.legendre.leggauss(q)
+    edges = np.r_[0.0, np.logspace(-8, 0, 17)]
+    us, wus = [], []
+    for a, b in zip(edges[:-1], edges[1:]):
+        us.append(a + (b - a) * 0.5 * (x + 1))
+        wus.append((b - a) * 0.5 * w)
+    u = np.concatenate(us)
+    wu = np.concatenate(wus)
+    v = 0.5 * (x + 1)
+    wv = 0.5 * w
+    U, Vv = np.meshgrid(u, v, indexing="ij")
+    WU, WV = np.meshgrid(wu, wv, indexing="ij")
+    return U.ravel(), Vv.ravel(), (WU * WV).ravel()
+
+
+def _quad_potentials(r, v0, v1, v2, q=24):
+    """int 1/R and int (rho' - rho)/R over the triangle, by splitting it at the
+    projection of r into three sub-triangles whose apex is that point and using
+    the collapsed (Duffy) map lambda_apex = 1 - u (Jacobian (1 - u) cancels
+    1/R at the apex)."""
+    n = np.cross(v1 - v0, v2 - v0)
+    n /= np.linalg.norm(n)
+    d = np.dot(r - v0, n)
+    rho = r - d * n
+    U, Vv, W = _gl_tri(q)
+    I0 = 0.0
+    I1 = np.zeros(3)
+    for a, b in ((v0, v1), (v1, v2), (v2, v0)):
+        # sub-triangle (rho, a, b) with signed area (orientation w.r.t. n)
+        s_area = 0.5 * np.dot(np.cross(a - rho, b - rho), n)
+        # point = rho + u (a - rho) + u v (b - a): apex at u = 0, Jacobian u
+        P = rho + U[:, None] * (a - rho) + (U * Vv)[:, None] * (b - a)
+        R = np.linalg.norm(r - P, axis=1)
+        w = W * U * 2.0 * s_area
+        I0 += np.sum(w / R)
+        I1 += np.sum((w / R)[:, None] * (P - rho), axis=0)
+    return I0, I1
+
+
+TRI = (np.array([0.0, 0.0, 0.0]), np.array([1.0, 0.1, 0.0]), np.array([0.3, 0.9, 0.0]))
+
+
+@pytest.mark.parametrize("r", [
+    [0.4, 0.3, 0.0],      # in-plane, inside (singular)
+    [0.4, 0.3, 1e-3],     # just above the interior
+    [0.4, 0.3, -0.2],     # below
+    [2.5, 1.7, 0.9],      # far
+    [-0.5, -0.05, 0.0],   # in-plane on the extension of edge v0->v1's line
+    [1.0, 0.1, 0.3],      # above a vertex
+    [0.65, 0.5, 0.0],     # in-plane, exactly on edge v1->v2 (midpoint)
+])
+def test_triangle_potentials_vs_quadrature(r):
+    r = np.array(r)
+    v0, v1, v2 = TRI
+    I0, I1, rho = triangle_potentials(r[None], v0[None], v1[None], v2[None])
+    q0, q1 = _quad_potentials(r, v0, v1, v2)
+    assert I0[0] == pytest.approx(q0, rel=1e-9)
+    assert np.allclose(I1[0], q1, rtol=0, atol=1e-9 * np.abs(q1).max())
+
+
+def test_static_entries_rigid_motion_invariant_and_positive():
+    m = inp.make_mesh(1)
+    V, T = m.vertices, m.triangles
+    r = build_rwg(V, T)
+    rng = np.random.default_rng(5)
+    rows = rng.integers(0, r.n, 300)
+    cols = np.clip(rows + rng.integers(-20, 20, 300), 0, r.n - 1)
+    rows = np.r_[rows, np.arange(r.n)]
+    cols = np.r_[cols, np.arange(r.n)]
+    a1, p1 = static_pair_entries(V, T, r, rows, cols)
+    th = 0.7
+    Rz = np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1]])
+    Rx = np.array([[1, 0, 0], [0, np.cos(0.3), -np.sin(0.3)], [0, np.sin(0.3), np.cos(0.3)]])
+    V2 = V @ (Rx @ Rz).T + np.array([3.0, -1.0, 2.0])
+    a2, p2 = static_pair_entries(V2, T, r, rows, cols)
+    assert np.max(np.abs(a1 - a2)) <= 1e-10 * np.abs(a1).max()
+    assert np.max(np.abs(p1 - p2)) <= 1e-10 * np.abs(p1).max()
+    # L^A self terms (static kernel, coincident supports) are real and > 0
+    assert np.all(a1[-r.n:] > 0) and np.all(p1[-r.n:] > 0)
+
+
+def test_static_near_symmetric(cfg1_oracle):
+    op = cfg1_oracle
+    import scipy.sparse as sp
+    M = sp.csr_matrix((op.LA_NR, op.col, op.rowptr), shape=(op.N, op.N)).toarray()
+    assert np.array_equal(M, M.T)
+
+
+def test_far_pair_static_entry_vs_point_product():
+    # well separated supports: the entry tends to the product of moments / (4 pi R)
+    m = inp.make_mesh(1)
+    r = build_rwg(m.vertices, m.triangles)
+    V, T = m.vertices, m.triangles
+    a, p = static_pair_entries(V, T, r, np.array([0]), np.array([r.n - 1]))
+    # brute force: 7 x 7 points of both triangles (smooth integrand far away)
+    from oracle.direct import _points
+    pts, w, f, div = _points(V, T, r)
+    R = np.linalg.norm(pts[0].reshape(-1, 3)[:, None] - pts[-1].reshape(-1, 3)[None], axis=-1)
+    G = 1 / (4 * np.pi * R)
+    ww = np.outer(w[0].ravel(), w[-1].ravel())
+    fa = np.einsum("ic,jc->ij", f[0].reshape(-1, 3), f[-1].reshape(-1, 3))
+    ref_a = np.sum(ww * fa * G)
+    ref_p = np.sum(ww * np.outer(div[0].ravel(), div[-1].ravel()) * G)
+    assert a[0] == pytest.approx(ref_a, rel=1e-6)
+    assert p[0] == pytest.approx(ref_p, rel=1e-6)
+
+
+def test_precorrection_grouped_equals_dense_definition(cfg1_oracle):
+    op = cfg1_oracle
+    la, yr = precorrection(op.Lam, op.A, op.rowptr, op.col, op.order, op.grid.h)
+    la_d, yr_d = precorrection_dense(op.Lam, op.A, op.grid, op.rowptr, op.col)
+    assert np.max(np.abs(la - la_d)) <= 1e-12 * np.abs(la_d).max()
+    assert np.max(np.abs(yr - yr_d)) <= 1e-12 * np.abs(yr_d).max()
