@@ -1,0 +1,184 @@
+/*
+ * aimx.h -- C ABI of the B200-native AIMx matrix-vector product.
+ *
+ * Method: Sharma & Triverio, "AIMx: An Extended Adaptive Integral Method for
+ * the Fast Electromagnetic Modeling of Complex Structures" (arxiv 2009.02281).
+ * Citations "P:<line>" refer to that paper's LaTeX source with the
+ * equation label.  The library computes, for the EFIE of a PEC surface in free
+ * space (eq:EFIEdis P:179-181),
+ *
+ *     y = Z(k0) x = -j w mu0 ( L_A + k0^-2 L_phi ) x,
+ *     L   ~= L_s,NR - L_s,P + W H(k0) P                  (eq:LAIMx P:283)
+ *
+ * split as eq:EFIEAIMx: the sparse, frequency-independent near matrix
+ * L_s,NR and precorrection L_s,P = W H_s,NR P (eq:aimLPs P:276) are built ONCE
+ * with the static kernel G_s = 1/(4 pi r) (change (a)); the grid
+ * convolution H(k0) (eq:Hmn P:305, three-level Toeplitz) carries all
+ * frequency dependence, with the modified self term H^(m,m) = -j k0/(4 pi)
+ * (eq:Hmm P:335).  Its spectrum is H_hat_s (static, built once) + DFT(K_d(k0))
+ * (regenerated per frequency on the device).
+ *
+ * Conventions
+ * -----------
+ * - Every function returns an aimx_status; no C++ exception crosses the ABI.
+ * - All host arrays passed in are BORROWED for the duration of the call and
+ *   copied; the library never keeps a host pointer.
+ * - Device vectors x / y / X / Y are owned by the caller (e.g. torch tensors
+ *   via data_ptr()); they are contiguous complex numbers, interleaved
+ *   (re, im), complex64 (float2) for AIMX_C64 and complex128 (double2) for
+ *   AIMX_C128, in the EXTERNAL RWG order (ascending lexicographic vertex pair,
+ *   see aimx_get_rwg).  Input and output must not alias.
+ * - `stream` is a cudaStream_t passed as void*; NULL means the context's own
+ *   stream (the one given to aimx_setup).  Work is enqueued asynchronously:
+ *   no host synchronisation and no allocation happens in aimx_matvec /
+ *   aimx_matvec_parts / aimx_sweep.  A context owns one set of work buffers,
+ *   so calls on one context must not run concurrently on different streams
+ *   (the library orders them with events; it is not thread-safe).
+ * - Asynchronous CUDA faults surface as AIMX_E_CUDA on the next call.
+ * - Independent contexts are independent (one per GPU / process in the
+ *   multi-GPU frequency-sharded sweep).
+ */
+#ifndef AIMX_H
+#define AIMX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AIMX_OK = 0,
+  AIMX_E_INVALID_ARG = 1,  /* NULL pointer, size/precision mismatch, f <= 0 or not finite */
+  AIMX_E_MESH = 2,         /* index out of range, repeated vertex, zero-area triangle,
+                              edge in > 2 triangles, inconsistent orientation, no RWG */
+  AIMX_E_GRID = 3,         /* grid too small: a stencil does not fit, bad order/threshold */
+  AIMX_E_STATE = 4,        /* matvec before aimx_set_frequency */
+  AIMX_E_OOM = 5,          /* device or host allocation failed */
+  AIMX_E_CUDA = 6,         /* CUDA runtime error (message in aimx_last_error) */
+  AIMX_E_UNSUPPORTED = 7,  /* grid length with no compiled FFT kernel (see aimx.h notes) */
+  AIMX_E_INTERNAL = 8
+} aimx_status;
+
+typedef enum {
+  AIMX_C64 = 0,   /* complex64 storage and arithmetic on the hot path; setup in fp64 */
+  AIMX_C128 = 1   /* complex128 throughout */
+} aimx_prec;
+
+/* Triangle mesh: vertices [nv][3] in metres (row-major float64),
+ * triangles [nt][3] 0-based vertex indices (int32).  Triangles must be
+ * consistently oriented (closed surfaces: outward).  Interior edges (shared by
+ * exactly two triangles) carry the RWG unknowns; boundary edges none. */
+typedef struct {
+  int64_t nv;
+  const double* vertices;
+  int64_t nt;
+  const int32_t* triangles;
+} aimx_mesh_desc;
+
+/* AIM grid: n[3] = (N_x, N_y, N_z) unpadded points; order = stencil
+ * order n (n+1 points per axis), 1..3; near_cells = near-region
+ * threshold T in grid cells (pairs whose stencils are within T cells,
+ * Euclidean, are "near").  h <= 0 derives spacing and origin from the
+ * mesh bounding box (margin ceil(n/2) nodes, isotropic h =
+ * max_a ext_a / (N_a - 1 - 2 margin), origin = min - margin*h); otherwise h
+ * and origin[3] are used as given.  Supported FFT lengths: 2*N_a must be a
+ * power of two in [8, 1024]. */
+typedef struct {
+  int32_t n[3];
+  int32_t order;
+  int32_t near_cells;
+  double h;
+  double origin[3];
+} aimx_grid_desc;
+
+typedef struct aimx_ctx aimx_ctx;
+
+typedef struct {
+  int64_t num_unknowns;       /* N_b */
+  int64_t nnz;                /* near pairs */
+  int64_t occupied_nodes;     /* grid nodes carrying a non-zero projection weight */
+  int64_t occupied_lines;     /* x-lines (y, z) with an occupied node */
+  int64_t occupied_planes;    /* z planes with an occupied node */
+  int64_t device_bytes;       /* device memory owned by the context */
+  double setup_seconds;       /* wall time of aimx_setup */
+  int32_t n[3];
+  int32_t order;
+  double h;
+  double origin[3];
+} aimx_stats;
+
+/* S0 (the paper's "one-time static matrix-fill", tab:prof P:715): RWG basis,
+ * grid, stencil anchors, near-region map, projection weights, static near
+ * integrals L_s,NR (analytic inner, 7-point outer, symmetrised), precorrection
+ * L_s,P, C = L_s,NR - L_s,P (fp64, stored in `prec`), static spectrum H_hat_s.
+ * The only host->device copies of the context happen here.  `stream` becomes
+ * the context stream (NULL = legacy default stream).  On failure *out is NULL
+ * and aimx_last_setup_error() describes the cause. */
+aimx_status aimx_setup(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid,
+                       aimx_prec prec, int device, void* stream, aimx_ctx** out);
+
+/* S1: bind the frequency f (Hz): k0 = 2 pi f / c0; H_hat(k0) = H_hat_s +
+ * DFT3(K_d(k0)) with K_d = (e^{-j k0 r} - 1)/(4 pi r) (eq:hgfd P:231) and
+ * K_d(0) = -j k0/(4 pi) (eq:Hdmm P:331), generated on the device on the
+ * context stream.  Does not touch C or the weights (byte-identical across
+ * frequencies).  Idempotent.  f must be finite and > 0 (k0 = 0 rejected). */
+aimx_status aimx_set_frequency(aimx_ctx* ctx, double f_hz);
+
+/* S2-S5: y = Z(k0) x = -j w mu0 (y^A - k0^-2 y^rho) (eq:EFIEAIMx P:288), where
+ * y^A = W^(A) H P^(A) x + C_A x and y^rho = W^(phi) H P^(phi) x + C_rho x.
+ * x, y: device vectors of N_b complex numbers (see conventions). */
+aimx_status aimx_matvec(aimx_ctx* ctx, const void* x, void* y, void* stream);
+
+/* Parts, unscaled: yA = L_A x = y^A, yPhi = L_phi x = -y^rho (the divergence is
+ * moved to the testing function).  Either output may be NULL. */
+aimx_status aimx_matvec_parts(aimx_ctx* ctx, const void* x, void* yA, void* yPhi,
+                              void* stream);
+
+/* Frequency sweep: for i < nf, Y[i,:] = Z(f_hz[i]) X[i,:] (per frequency: S1
+ * then S2-S5).  f_hz is a HOST array; X, Y device arrays [nf][N_b] row-major.
+ * `batch` frequencies are processed per device batch (<= 0: library default).
+ * The context's bound frequency is restored afterwards if one was set. */
+aimx_status aimx_sweep(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* X,
+                       void* Y, int32_t batch, void* stream);
+
+/* The same sweep with X, Y in HOST memory (pinned or pageable): the library
+ * stages each batch host->device and the results device->host on `stream`
+ * and synchronises the stream before returning. */
+aimx_status aimx_sweep_host(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* X,
+                            void* Y, int32_t batch, void* stream);
+
+/* ---- introspection (parity tests; all host buffers, caller-allocated) ---- */
+int64_t aimx_num_unknowns(const aimx_ctx* ctx);
+aimx_status aimx_get_stats(const aimx_ctx* ctx, aimx_stats* out);
+/* edge_ab[N_b][2] (a < b), tri_pm[N_b][2] (T+, T-), free_pm[N_b][2] (p+, p-);
+ * any pointer may be NULL. */
+aimx_status aimx_get_rwg(const aimx_ctx* ctx, int32_t* edge_ab, int32_t* tri_pm,
+                         int32_t* free_pm);
+/* anchors[N_b][3]: lowest stencil node index per axis. */
+aimx_status aimx_get_anchors(const aimx_ctx* ctx, int32_t* anchors);
+/* Two-call: with rowptr == NULL and col == NULL only *nnz is written.
+ * rowptr[N_b+1] (int64), col[nnz] ascending per row. */
+aimx_status aimx_get_near_csr(const aimx_ctx* ctx, int64_t* rowptr, int32_t* col,
+                              int64_t* nnz);
+/* C_A = L^A_s,NR - L^A_s,P and C_rho = y^rho_s,NR - y^rho_s,P (fp64, CSR order);
+ * optional: the four constituent matrices (any pointer may be NULL). */
+aimx_status aimx_get_static(const aimx_ctx* ctx, double* CA, double* Crho,
+                            double* LA_NR, double* Yrho_NR, double* LA_P, double* Yrho_P);
+/* Projection weights (fp64) lam[N_b][4][(n+1)^3], channels (x, y, z, rho),
+ * node s = i + (n+1)(j + (n+1) k). */
+aimx_status aimx_get_weights(const aimx_ctx* ctx, double* lam);
+/* Spectrum octant, complex128 interleaved, index ((ky (N_x+1) + kx)(N_z+1) + kz):
+ * which = 0 static H_hat_s, 1 the bound H_hat(k0) (unnormalised DFT). */
+aimx_status aimx_get_spectrum(const aimx_ctx* ctx, int which, double* out);
+
+void aimx_destroy(aimx_ctx* ctx);
+const char* aimx_status_string(aimx_status s);
+const char* aimx_last_error(const aimx_ctx* ctx);
+const char* aimx_last_setup_error(void);
+const char* aimx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AIMX_H */

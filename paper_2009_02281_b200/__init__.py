@@ -1,0 +1,268 @@
+"""B200-native AIMx matrix-vector product (arxiv 2009.02281), Python binding.
+
+Thin ctypes marshalling over the C ABI in ``include/aimx.h`` (libaimx.so,
+hand-written sm_100a kernels).  Every step of the path runs in the library's
+kernels; PyTorch is used only for device memory and streams.  There is NO CPU
+fallback: if the shared library is missing or no CUDA device is present the
+calls raise.
+
+    op = AIMx(vertices, triangles, n=(16, 16, 4), prec="c128")
+    op.set_frequency(150e6)
+    y = op.matvec(x)               # x: complex torch tensor on cuda
+    yA, yPhi = op.matvec_parts(x)  # L_A x, L_phi x
+    Y = op.sweep(freqs, X)         # Y[i] = Z(f_i) X[i]
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+__all__ = ["AIMx", "AIMxError", "load_library", "library_path", "ABI_FUNCTIONS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+AIMX_C64, AIMX_C128 = 0, 1
+
+
+class AIMxError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"aimx status {status}: {msg}")
+        self.status = status
+
+
+class _Mesh(C.Structure):
+    _fields_ = [("nv", C.c_int64), ("vertices", C.POINTER(C.c_double)),
+                ("nt", C.c_int64), ("triangles", C.POINTER(C.c_int32))]
+
+
+class _Grid(C.Structure):
+    _fields_ = [("n", C.c_int32 * 3), ("order", C.c_int32), ("near_cells", C.c_int32),
+                ("h", C.c_double), ("origin", C.c_double * 3)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("num_unknowns", C.c_int64), ("nnz", C.c_int64), ("occupied_nodes", C.c_int64),
+                ("occupied_lines", C.c_int64), ("occupied_planes", C.c_int64),
+                ("device_bytes", C.c_int64), ("setup_seconds", C.c_double),
+                ("n", C.c_int32 * 3), ("order", C.c_int32), ("h", C.c_double),
+                ("origin", C.c_double * 3)]
+
+
+_P = C.c_void_p
+ABI_FUNCTIONS = {
+    "aimx_setup": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Grid), C.c_int, C.c_int, _P, C.POINTER(_P)]),
+    "aimx_set_frequency": (C.c_int, [_P, C.c_double]),
+    "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
+    "aimx_matvec_parts": (C.c_int, [_P, _P, _P, _P, _P]),
+    "aimx_sweep": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_int32, _P]),
+    "aimx_sweep_host": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_int32, _P]),
+    "aimx_num_unknowns": (C.c_int64, [_P]),
+    "aimx_get_stats": (C.c_int, [_P, C.POINTER(_Stats)]),
+    "aimx_get_rwg": (C.c_int, [_P, _P, _P, _P]),
+    "aimx_get_anchors": (C.c_int, [_P, _P]),
+    "aimx_get_near_csr": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int64)]),
+    "aimx_get_static": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "aimx_get_weights": (C.c_int, [_P, _P]),
+    "aimx_get_spectrum": (C.c_int, [_P, C.c_int, _P]),
+    "aimx_destroy": (None, [_P]),
+    "aimx_status_string": (C.c_char_p, [C.c_int]),
+    "aimx_last_error": (C.c_char_p, [_P]),
+    "aimx_last_setup_error": (C.c_char_p, []),
+    "aimx_version": (C.c_char_p, []),
+}
+
+
+def library_path() -> str:
+    return os.path.join(_HERE, "libaimx.so")
+
+
+def load_library():
+    """Load libaimx.so (built in-tree by ``python -m paper_2009_02281_b200.build``
+    or ``__graft_entry__.build()``).  Raises if it is missing."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = library_path()
+    if not os.path.exists(path):
+        raise ImportError(f"libaimx.so not built at {path}; run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, (res, args) in ABI_FUNCTIONS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _check(lib, st, ctx=None):
+    if st != 0:
+        msg = (lib.aimx_last_error(ctx) if ctx else lib.aimx_last_setup_error()) or b""
+        raise AIMxError(st, f"{lib.aimx_status_string(st).decode()}: {msg.decode()}")
+
+
+class AIMx:
+    """One AIMx operator context on one CUDA device (S0 setup in __init__)."""
+
+    def __init__(self, vertices, triangles, n, order: int = 2, near_cells: int = 2,
+                 h: float = 0.0, origin=(0.0, 0.0, 0.0), prec: str = "c64",
+                 device: int | None = None, stream=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("AIMx needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.prec = prec
+        self.cdtype = {"c64": torch.complex64, "c128": torch.complex128}[prec]
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        V = np.ascontiguousarray(vertices, dtype=np.float64)
+        T = np.ascontiguousarray(triangles, dtype=np.int32)
+        mesh = _Mesh(V.shape[0], V.ctypes.data_as(C.POINTER(C.c_double)),
+                     T.shape[0], T.ctypes.data_as(C.POINTER(C.c_int32)))
+        g = _Grid()
+        for a in range(3):
+            g.n[a] = int(n[a])
+            g.origin[a] = float(origin[a])
+        g.order, g.near_cells, g.h = int(order), int(near_cells), float(h)
+        with torch.cuda.device(self.device):
+            s = stream if stream is not None else torch.cuda.current_stream()
+            self._stream = s
+            ctx = _P()
+            st = self.lib.aimx_setup(C.byref(mesh), C.byref(g),
+                                     AIMX_C64 if prec == "c64" else AIMX_C128,
+                                     self.device, _P(s.cuda_stream), C.byref(ctx))
+        _check(self.lib, st)
+        self.ctx = ctx
+        self.N = int(self.lib.aimx_num_unknowns(ctx))
+        self.freq = None
+
+    # ----------------------------------------------------------- lifecycle
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.aimx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _s(self, stream):
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return _P(s.cuda_stream)
+
+    def _vec(self, x, shape):
+        torch = _torch()
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == self.cdtype
+                and x.is_contiguous() and tuple(x.shape) == shape):
+            raise ValueError(f"expected contiguous {self.cdtype} cuda tensor of shape {shape}")
+        return _P(x.data_ptr())
+
+    # ----------------------------------------------------------- hot path
+    def set_frequency(self, f_hz: float):
+        _check(self.lib, self.lib.aimx_set_frequency(self.ctx, float(f_hz)), self.ctx)
+        self.freq = float(f_hz)
+
+    def matvec(self, x, y=None, stream=None):
+        torch = _torch()
+        if y is None:
+            y = torch.empty(self.N, dtype=self.cdtype, device=x.device)
+        _check(self.lib, self.lib.aimx_matvec(self.ctx, self._vec(x, (self.N,)),
+                                              self._vec(y, (self.N,)), self._s(stream)), self.ctx)
+        return y
+
+    def matvec_parts(self, x, stream=None):
+        torch = _torch()
+        yA = torch.empty(self.N, dtype=self.cdtype, device=x.device)
+        yP = torch.empty(self.N, dtype=self.cdtype, device=x.device)
+        _check(self.lib, self.lib.aimx_matvec_parts(self.ctx, self._vec(x, (self.N,)),
+                                                    self._vec(yA, (self.N,)),
+                                                    self._vec(yP, (self.N,)), self._s(stream)),
+               self.ctx)
+        return yA, yP
+
+    def sweep(self, freqs, X, Y=None, batch: int = 0, stream=None):
+        torch = _torch()
+        f = np.ascontiguousarray(freqs, dtype=np.float64)
+        nf = f.shape[0]
+        if Y is None:
+            Y = torch.empty((nf, self.N), dtype=self.cdtype, device=X.device)
+        _check(self.lib, self.lib.aimx_sweep(self.ctx, nf, f.ctypes.data_as(C.POINTER(C.c_double)),
+                                             self._vec(X, (nf, self.N)), self._vec(Y, (nf, self.N)),
+                                             int(batch), self._s(stream)), self.ctx)
+        return Y
+
+    def sweep_host(self, freqs, X, Y, batch: int = 0, stream=None):
+        """X, Y: host (CPU) torch tensors [nf, N] (pinned for best speed)."""
+        torch = _torch()
+        f = np.ascontiguousarray(freqs, dtype=np.float64)
+        nf = f.shape[0]
+        for t in (X, Y):
+            if not (isinstance(t, torch.Tensor) and not t.is_cuda and t.dtype == self.cdtype
+                    and t.is_contiguous() and tuple(t.shape) == (nf, self.N)):
+                raise ValueError("sweep_host expects contiguous host tensors [nf, N]")
+        _check(self.lib, self.lib.aimx_sweep_host(self.ctx, nf, f.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  _P(X.data_ptr()), _P(Y.data_ptr()), int(batch),
+                                                  self._s(stream)), self.ctx)
+        return Y
+
+    # ----------------------------------------------------------- introspection
+    def stats(self) -> dict:
+        s = _Stats()
+        _check(self.lib, self.lib.aimx_get_stats(self.ctx, C.byref(s)), self.ctx)
+        return {"num_unknowns": s.num_unknowns, "nnz": s.nnz, "occupied_nodes": s.occupied_nodes,
+                "occupied_lines": s.occupied_lines, "occupied_planes": s.occupied_planes,
+                "device_bytes": s.device_bytes, "setup_seconds": s.setup_seconds,
+                "n": tuple(s.n), "order": s.order, "h": s.h, "origin": tuple(s.origin)}
+
+    def rwg(self):
+        ab = np.empty((self.N, 2), np.int32)
+        tpm = np.empty((self.N, 2), np.int32)
+        fpm = np.empty((self.N, 2), np.int32)
+        _check(self.lib, self.lib.aimx_get_rwg(self.ctx, _P(ab.ctypes.data), _P(tpm.ctypes.data),
+                                               _P(fpm.ctypes.data)), self.ctx)
+        return ab, tpm, fpm
+
+    def anchors(self):
+        a = np.empty((self.N, 3), np.int32)
+        _check(self.lib, self.lib.aimx_get_anchors(self.ctx, _P(a.ctypes.data)), self.ctx)
+        return a
+
+    def near_csr(self):
+        nnz = C.c_int64()
+        _check(self.lib, self.lib.aimx_get_near_csr(self.ctx, None, None, C.byref(nnz)), self.ctx)
+        rp = np.empty(self.N + 1, np.int64)
+        col = np.empty(nnz.value, np.int32)
+        _check(self.lib, self.lib.aimx_get_near_csr(self.ctx, _P(rp.ctypes.data), _P(col.ctypes.data),
+                                                    C.byref(nnz)), self.ctx)
+        return rp, col
+
+    def static(self):
+        nnz = C.c_int64()
+        _check(self.lib, self.lib.aimx_get_near_csr(self.ctx, None, None, C.byref(nnz)), self.ctx)
+        out = [np.empty(nnz.value) for _ in range(6)]
+        _check(self.lib, self.lib.aimx_get_static(self.ctx, *[_P(a.ctypes.data) for a in out]), self.ctx)
+        return dict(zip(["CA", "CR", "LA_NR", "YR_NR", "LA_P", "YR_P"], out))
+
+    def weights(self):
+        st = self.stats()
+        p3 = (st["order"] + 1) ** 3
+        lam = np.empty((self.N, 4, p3))
+        _check(self.lib, self.lib.aimx_get_weights(self.ctx, _P(lam.ctypes.data)), self.ctx)
+        return lam
+
+    def spectrum(self, which: int = 0):
+        st = self.stats()
+        nx, ny, nz = st["n"]
+        out = np.empty((ny + 1) * (nx + 1) * (nz + 1) * 2)
+        _check(self.lib, self.lib.aimx_get_spectrum(self.ctx, int(which), _P(out.ctypes.data)), self.ctx)
+        return out.view(np.complex128).reshape(ny + 1, nx + 1, nz + 1)

@@ -1,0 +1,275 @@
+// Host-side integer topology of the AIMx setup (S0): mesh validation, RWG
+// basis, AIM grid, stencil anchors, near-region CSR, occupied-node map.
+//
+// P:177-178 RWG basis on pairs of adjacent triangles; P:188 regular grid on the
+// bounding box; P:576 (n+1)^3 stencil; P:192 near-region entries.  Readings
+// R2-R5 of DESIGN.md (RWG order/sign, grid rule, anchor rule, near metric).
+// Compiled with -ffp-contract=off: the anchor arithmetic is one IEEE op at a
+// time so that anchors are reproducible bit for bit.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "aimx_internal.h"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace aimx {
+
+static void mesh_error(const std::string& m) { throw Error(AIMX_E_MESH, m); }
+static void grid_error(const std::string& m) { throw Error(AIMX_E_GRID, m); }
+
+static double tri_area2(const double* V, const int32_t* t) {
+  const double* a = V + 3 * (int64_t)t[0];
+  const double* b = V + 3 * (int64_t)t[1];
+  const double* c = V + 3 * (int64_t)t[2];
+  double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+  double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+  double n0 = e1[1] * e2[2] - e1[2] * e2[1];
+  double n1 = e1[2] * e2[0] - e1[0] * e2[2];
+  double n2 = e1[0] * e2[1] - e1[1] * e2[0];
+  return std::sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+}
+
+void build_topology(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, Topology& t) {
+  if (!mesh || !grid || !mesh->vertices || !mesh->triangles)
+    throw Error(AIMX_E_INVALID_ARG, "null mesh or grid descriptor");
+  if (mesh->nv <= 0 || mesh->nt <= 0) mesh_error("empty mesh");
+  if (mesh->nt > (int64_t)INT32_MAX / 3 || mesh->nv > (int64_t)INT32_MAX)
+    mesh_error("mesh too large for 32-bit indices");
+  t.nv = mesh->nv;
+  t.nt = mesh->nt;
+  t.V.assign(mesh->vertices, mesh->vertices + 3 * t.nv);
+  t.T.assign(mesh->triangles, mesh->triangles + 3 * t.nt);
+  for (int64_t i = 0; i < 3 * t.nv; ++i)
+    if (!std::isfinite(t.V[i])) mesh_error("non-finite vertex coordinate");
+  for (int64_t f = 0; f < t.nt; ++f) {
+    const int32_t* tr = &t.T[3 * f];
+    for (int k = 0; k < 3; ++k)
+      if (tr[k] < 0 || tr[k] >= t.nv) mesh_error("triangle index out of range");
+    if (tr[0] == tr[1] || tr[1] == tr[2] || tr[0] == tr[2]) mesh_error("triangle with repeated vertex");
+    if (!(tri_area2(t.V.data(), tr) > 0.0)) mesh_error("degenerate (zero-area) triangle");
+  }
+
+  // ---- RWG basis (reading R2) -----------------------------------------------
+  struct DEdge { int32_t lo, hi; uint8_t back; int32_t tri, free; };
+  std::vector<DEdge> de(3 * t.nt);
+  for (int64_t f = 0; f < t.nt; ++f) {
+    const int32_t* tr = &t.T[3 * f];
+    for (int k = 0; k < 3; ++k) {
+      int32_t u = tr[k], v = tr[(k + 1) % 3], w = tr[(k + 2) % 3];
+      de[3 * f + k] = {std::min(u, v), std::max(u, v), (uint8_t)(u < v ? 0 : 1), (int32_t)f, w};
+    }
+  }
+  std::sort(de.begin(), de.end(), [](const DEdge& a, const DEdge& b) {
+    if (a.lo != b.lo) return a.lo < b.lo;
+    if (a.hi != b.hi) return a.hi < b.hi;
+    if (a.back != b.back) return a.back < b.back;
+    return a.tri < b.tri;
+  });
+  for (size_t i = 0; i < de.size();) {
+    size_t j = i;
+    while (j < de.size() && de[j].lo == de[i].lo && de[j].hi == de[i].hi) ++j;
+    size_t cnt = j - i;
+    if (cnt > 2) mesh_error("non-manifold edge (more than two triangles)");
+    if (cnt == 2) {
+      if (de[i].back == de[i + 1].back) mesh_error("inconsistent triangle orientation");
+      t.ea.push_back(de[i].lo);
+      t.eb.push_back(de[i].hi);
+      t.tp.push_back(de[i].tri);       // a->b
+      t.pp.push_back(de[i].free);
+      t.tm.push_back(de[i + 1].tri);   // b->a
+      t.pm.push_back(de[i + 1].free);
+    }
+    i = j;
+  }
+  t.nb = (int64_t)t.ea.size();
+  if (t.nb == 0) mesh_error("mesh has no interior edge (no RWG unknowns)");
+
+  // ---- grid (reading R3) --------------------------------------------------------
+  t.order = grid->order;
+  t.near_cells = grid->near_cells;
+  if (t.order < 1 || t.order > 3) grid_error("stencil order must be 1..3");
+  if (t.near_cells < 0 || t.near_cells > 8) grid_error("near threshold must be 0..8 cells");
+  t.p = t.order + 1;
+  t.p3 = t.p * t.p * t.p;
+  for (int a = 0; a < 3; ++a) {
+    t.n[a] = grid->n[a];
+    if (t.n[a] < t.p) grid_error("grid has fewer points than the stencil");
+  }
+  if ((int64_t)t.n[0] * t.n[1] * t.n[2] > (int64_t)INT32_MAX / 64) grid_error("grid too large");
+  if (grid->h > 0.0) {
+    t.h = grid->h;
+    for (int a = 0; a < 3; ++a) t.origin[a] = grid->origin[a];
+  } else {
+    const int m = (t.order + 1) / 2;
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) { lo[a] = t.V[a]; hi[a] = t.V[a]; }
+    for (int64_t i = 0; i < t.nv; ++i)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], t.V[3 * i + a]);
+        hi[a] = std::max(hi[a], t.V[3 * i + a]);
+      }
+    double h = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      double ext = hi[a] - lo[a];
+      int span = t.n[a] - 1 - 2 * m;
+      if (ext > 0.0) {
+        if (span <= 0) grid_error("grid too small for the mesh extent");
+        h = std::max(h, ext / (double)span);
+      }
+    }
+    if (!(h > 0.0)) grid_error("zero-extent mesh");
+    t.h = h;
+    for (int a = 0; a < 3; ++a) t.origin[a] = lo[a] - (double)m * h;
+  }
+
+  // ---- stencil anchors (reading R4; no FMA contraction in this file) --------------
+  t.anchor.resize(3 * t.nb);
+  const int half = t.order / 2;
+  for (int64_t e = 0; e < t.nb; ++e) {
+    for (int a = 0; a < 3; ++a) {
+      double s1 = t.V[3 * (int64_t)t.ea[e] + a] + t.V[3 * (int64_t)t.eb[e] + a];
+      s1 = s1 * 2.0;
+      double s2 = t.V[3 * (int64_t)t.pp[e] + a] + t.V[3 * (int64_t)t.pm[e] + a];
+      double c = s1 + s2;
+      c = c / 6.0;
+      double u = (c - t.origin[a]) / t.h;
+      double A = (t.order % 2 == 0) ? std::floor(u + 0.5) - (double)half
+                                    : std::floor(u) - (double)((t.order - 1) / 2);
+      if (!(A >= 0.0) || A > (double)(t.n[a] - 1 - t.order))
+        grid_error("stencil does not fit in the grid (RWG " + std::to_string(e) + ")");
+      t.anchor[3 * e + a] = (int32_t)A;
+    }
+  }
+
+  // ---- near-region CSR (reading R5): bucket RWGs by anchor cell ---------------------
+  const int Nx = t.n[0], Ny = t.n[1], Nz = t.n[2];
+  const int64_t ncell = (int64_t)Nx * Ny * Nz;
+  std::vector<int32_t> cell_ptr(ncell + 1, 0), cell_rwg(t.nb);
+  for (int64_t e = 0; e < t.nb; ++e) {
+    int64_t c = t.anchor[3 * e] + (int64_t)Nx * (t.anchor[3 * e + 1] + (int64_t)Ny * t.anchor[3 * e + 2]);
+    cell_ptr[c + 1]++;
+  }
+  for (int64_t c = 0; c < ncell; ++c) cell_ptr[c + 1] += cell_ptr[c];
+  {
+    std::vector<int32_t> fill(cell_ptr.begin(), cell_ptr.end() - 1);
+    for (int64_t e = 0; e < t.nb; ++e) {
+      int64_t c = t.anchor[3 * e] + (int64_t)Nx * (t.anchor[3 * e + 1] + (int64_t)Ny * t.anchor[3 * e + 2]);
+      cell_rwg[fill[c]++] = (int32_t)e;   // ascending e within a cell
+    }
+  }
+  const int R = t.order + t.near_cells;
+  const int T2 = t.near_cells * t.near_cells;
+  const int nthreads =
+#ifdef _OPENMP
+      omp_get_max_threads();
+#else
+      1;
+#endif
+  // two passes over rows in contiguous chunks: count, then fill sorted columns
+  t.rowptr.assign(t.nb + 1, 0);
+  auto row_cols = [&](int64_t m, std::vector<int32_t>& out) {
+    out.clear();
+    const int32_t* Am = &t.anchor[3 * m];
+    for (int dz = -R; dz <= R; ++dz) {
+      int z = Am[2] + dz;
+      if (z < 0 || z >= Nz) continue;
+      int gz = std::max(0, std::abs(dz) - t.order);
+      for (int dy = -R; dy <= R; ++dy) {
+        int y = Am[1] + dy;
+        if (y < 0 || y >= Ny) continue;
+        int gy = std::max(0, std::abs(dy) - t.order);
+        for (int dx = -R; dx <= R; ++dx) {
+          int x = Am[0] + dx;
+          if (x < 0 || x >= Nx) continue;
+          int gx = std::max(0, std::abs(dx) - t.order);
+          if (gx * gx + gy * gy + gz * gz > T2) continue;
+          int64_t c = x + (int64_t)Nx * (y + (int64_t)Ny * z);
+          for (int32_t k = cell_ptr[c]; k < cell_ptr[c + 1]; ++k) out.push_back(cell_rwg[k]);
+        }
+      }
+    }
+    std::sort(out.begin(), out.end());
+  };
+#pragma omp parallel num_threads(nthreads)
+  {
+    std::vector<int32_t> buf;
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t m = 0; m < t.nb; ++m) {
+      row_cols(m, buf);
+      t.rowptr[m + 1] = (int64_t)buf.size();
+    }
+  }
+  for (int64_t m = 0; m < t.nb; ++m) t.rowptr[m + 1] += t.rowptr[m];
+  const int64_t nnz = t.rowptr[t.nb];
+  if (nnz > (int64_t)INT32_MAX) grid_error("near-region matrix exceeds 2^31 entries");
+  t.col.resize(nnz);
+#pragma omp parallel num_threads(nthreads)
+  {
+    std::vector<int32_t> buf;
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t m = 0; m < t.nb; ++m) {
+      row_cols(m, buf);
+      std::copy(buf.begin(), buf.end(), t.col.begin() + t.rowptr[m]);
+    }
+  }
+}
+
+void build_nodemap(const Topology& t, const std::vector<uint8_t>& nz_slot, NodeMap& m) {
+  const int Nx = t.n[0], Ny = t.n[1], Nz = t.n[2];
+  const int p = t.p, p3 = t.p3;
+  const int64_t ng = (int64_t)Nx * Ny * Nz;
+  std::vector<int32_t> cnt(ng + 1, 0);
+  auto node_of = [&](int64_t e, int s) -> int64_t {
+    int i = s % p, j = (s / p) % p, k = s / (p * p);
+    const int32_t* A = &t.anchor[3 * e];
+    return (A[0] + i) + (int64_t)Nx * ((A[1] + j) + (int64_t)Ny * (A[2] + k));
+  };
+  for (int64_t e = 0; e < t.nb; ++e)
+    for (int s = 0; s < p3; ++s)
+      if (nz_slot[e * p3 + s]) cnt[node_of(e, s) + 1]++;
+  for (int64_t q = 0; q < ng; ++q) cnt[q + 1] += cnt[q];
+  const int64_t nent = cnt[ng];
+  std::vector<int32_t> er(nent), es(nent);
+  {
+    std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t e = 0; e < t.nb; ++e)
+      for (int s = 0; s < p3; ++s)
+        if (nz_slot[e * p3 + s]) {
+          int64_t q = node_of(e, s);
+          er[fill[q]] = (int32_t)e;
+          es[fill[q]] = s;
+          fill[q]++;
+        }
+  }
+  m.node_lin.clear();
+  m.node_ptr.clear();
+  m.line_id.clear();
+  m.line_ptr.clear();
+  m.zplanes.clear();
+  m.line_occ.assign((size_t)Ny * Nz, 0);
+  m.node_ptr.push_back(0);
+  for (int64_t q = 0; q < ng; ++q) {
+    if (cnt[q + 1] == cnt[q]) continue;
+    int32_t line = (int32_t)(q / Nx);
+    if (m.line_id.empty() || m.line_id.back() != line) {
+      m.line_id.push_back(line);
+      m.line_ptr.push_back((int32_t)m.node_lin.size());
+      m.line_occ[line] = 1;
+      int z = line / Ny;
+      if (m.zplanes.empty() || m.zplanes.back() != z) m.zplanes.push_back(z);
+    }
+    m.node_lin.push_back((int32_t)q);
+    m.node_ptr.push_back(cnt[q + 1]);
+  }
+  m.line_ptr.push_back((int32_t)m.node_lin.size());
+  m.ent_rwg.swap(er);
+  m.ent_slot.swap(es);
+  (void)Nz;
+}
+
+}  // namespace aimx

@@ -1,0 +1,373 @@
+// Device-side static setup of AIMx (S0), all in fp64 on the B200:
+//   * per-RWG triangle geometry,
+//   * projection weights Lambda (moment matching == Lagrange interpolation,
+//     P:109-110) by collapsed Gauss-Legendre quadrature (exact for the
+//     polynomial integrand),
+//   * static near-region entries L_s,NR with G_s = 1/(4 pi r) (eq:Lmatdecomp2
+//     P:267, change (a) P:297): analytic inner potential integrals, 7-point
+//     outer rule, symmetrised (reading R9),
+//   * precorrection L_s,P = W H_s,NR P (eq:aimLPs P:276) with H_s(0) = 0
+//     (eq:Hsmm P:321), and C = L_s,NR - L_s,P.
+// The paper's own static fill is its "one-time static matrix-fill" (tab:prof
+// P:715); here it runs once per context on the GPU.
+#include <cmath>
+#include <vector>
+
+#include "aimx_internal.h"
+
+namespace aimx {
+
+namespace {
+
+__constant__ double c_gl_x[8];
+__constant__ double c_gl_w[8];
+__constant__ double c_hs_tab[512];   // 1/(4 pi h sqrt(q)), q = |delta|^2; [0] = 0
+
+// 7-point degree-5 rule (barycentric weights of v0, v1, v2; weights sum to 1)
+__device__ __forceinline__ void radon7(int q, double& b0, double& b1, double& b2, double& w) {
+  const double s15 = 3.872983346207417;  // sqrt(15)
+  const double a1 = (6.0 - s15) / 21.0, a2 = (6.0 + s15) / 21.0;
+  const double w1 = (155.0 - s15) / 1200.0, w2 = (155.0 + s15) / 1200.0;
+  switch (q) {
+    case 0: b0 = 1.0 / 3.0; b1 = 1.0 / 3.0; b2 = 1.0 / 3.0; w = 9.0 / 40.0; break;
+    case 1: b0 = a1; b1 = a1; b2 = 1.0 - 2.0 * a1; w = w1; break;
+    case 2: b0 = a1; b1 = 1.0 - 2.0 * a1; b2 = a1; w = w1; break;
+    case 3: b0 = 1.0 - 2.0 * a1; b1 = a1; b2 = a1; w = w1; break;
+    case 4: b0 = a2; b1 = a2; b2 = 1.0 - 2.0 * a2; w = w2; break;
+    case 5: b0 = a2; b1 = 1.0 - 2.0 * a2; b2 = a2; w = w2; break;
+    default: b0 = 1.0 - 2.0 * a2; b1 = a2; b2 = a2; w = w2; break;
+  }
+}
+
+struct Vec3 { double x, y, z; };
+__device__ __forceinline__ Vec3 v3(const double* p) { return {p[0], p[1], p[2]}; }
+__device__ __forceinline__ Vec3 operator+(Vec3 a, Vec3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ Vec3 operator-(Vec3 a, Vec3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ Vec3 operator*(double s, Vec3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ double dot(Vec3 a, Vec3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ Vec3 cross(Vec3 a, Vec3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ double norm(Vec3 a) { return sqrt(dot(a, a)); }
+
+// side record: v0 v1 v2 free (12), coef = sigma l/(2A), div = sigma l/A, area
+__global__ void k_rwg_sides(int nb, const double* __restrict__ V, const int32_t* __restrict__ T,
+                            const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                            const int32_t* __restrict__ tp, const int32_t* __restrict__ tm,
+                            const int32_t* __restrict__ pp, const int32_t* __restrict__ pm,
+                            double* __restrict__ side) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 2 * (int64_t)nb) return;
+  int e = (int)(i >> 1), sd = (int)(i & 1);
+  int tri = sd ? tm[e] : tp[e];
+  int fv = sd ? pm[e] : pp[e];
+  double* o = side + i * kSideStride;
+  Vec3 a = v3(V + 3 * (int64_t)T[3 * tri]), b = v3(V + 3 * (int64_t)T[3 * tri + 1]),
+       c = v3(V + 3 * (int64_t)T[3 * tri + 2]);
+  Vec3 f = v3(V + 3 * (int64_t)fv);
+  double area = 0.5 * norm(cross(b - a, c - a));
+  double len = norm(v3(V + 3 * (int64_t)eb[e]) - v3(V + 3 * (int64_t)ea[e]));
+  double sg = sd ? -1.0 : 1.0;
+  o[0] = a.x; o[1] = a.y; o[2] = a.z;
+  o[3] = b.x; o[4] = b.y; o[5] = b.z;
+  o[6] = c.x; o[7] = c.y; o[8] = c.z;
+  o[9] = f.x; o[10] = f.y; o[11] = f.z;
+  o[12] = sg * len / (2.0 * area);
+  o[13] = sg * len / area;
+  o[14] = area;
+  o[15] = 0.0;
+}
+
+// Lagrange basis on nodes t = 0..n
+__device__ __forceinline__ double lagrange(int order, int i, double t) {
+  double v = 1.0;
+  for (int j = 0; j <= order; ++j)
+    if (j != i) v *= (t - (double)j) / (double)(i - j);
+  return v;
+}
+
+// Thread per (rwg, slot s): Lambda^c_s = int f_c l_i l_j l_k dS, Lambda^rho_s = int div f (...)
+__global__ void k_weights(int nb, int order, int q, const double* __restrict__ side,
+                          const int32_t* __restrict__ anchor, double ox, double oy, double oz,
+                          double h, double* __restrict__ lam, uint8_t* __restrict__ nzflag) {
+  const int p = order + 1, p3 = p * p * p;
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nb * p3) return;
+  int e = (int)(idx / p3), s = (int)(idx % p3);
+  int si = s % p, sj = (s / p) % p, sk = s / (p * p);
+  double Ax = anchor[3 * e], Ay = anchor[3 * e + 1], Az = anchor[3 * e + 2];
+  double acc[4] = {0, 0, 0, 0};
+  for (int sd = 0; sd < 2; ++sd) {
+    const double* o = side + (2 * (int64_t)e + sd) * kSideStride;
+    Vec3 a = v3(o), b = v3(o + 3), c = v3(o + 6), f = v3(o + 9);
+    double coef = o[12], dv = o[13], area = o[14];
+    double sx = 0, sy = 0, sz = 0, sr = 0;
+    for (int iu = 0; iu < q; ++iu) {
+      double u = c_gl_x[iu];
+      for (int iv = 0; iv < q; ++iv) {
+        double v = c_gl_x[iv];
+        double l1 = u, l2 = v * (1.0 - u);
+        double w = c_gl_w[iu] * c_gl_w[iv] * (1.0 - u) * 2.0;   // sums to 1 over the triangle
+        Vec3 r = a + l1 * (b - a) + l2 * (c - a);
+        double tx = (r.x - ox) / h - Ax, ty = (r.y - oy) / h - Ay, tz = (r.z - oz) / h - Az;
+        double L = lagrange(order, si, tx) * lagrange(order, sj, ty) * lagrange(order, sk, tz) * w;
+        sx += L * (r.x - f.x);
+        sy += L * (r.y - f.y);
+        sz += L * (r.z - f.z);
+        sr += L;
+      }
+    }
+    acc[0] += area * coef * sx;
+    acc[1] += area * coef * sy;
+    acc[2] += area * coef * sz;
+    acc[3] += area * dv * sr;
+  }
+  double* out = lam + ((int64_t)e * p3 + s) * 4;
+  out[0] = acc[0]; out[1] = acc[1]; out[2] = acc[2]; out[3] = acc[3];
+  nzflag[idx] = (acc[0] != 0.0 || acc[1] != 0.0 || acc[2] != 0.0 || acc[3] != 0.0) ? 1 : 0;
+}
+
+// ln(R + s) without cancellation (s < 0: R + s = R0^2 / (R - s))
+__device__ __forceinline__ double logsum(double R, double s, double R0sq) {
+  return s >= 0.0 ? log(R + s) : log(R0sq / (R - s));
+}
+
+struct Frame {
+  Vec3 v[3];
+  Vec3 n;
+  Vec3 sh[3], mh[3];
+  double L[3];
+};
+
+__device__ __forceinline__ void make_frame(const double* o, Frame& F) {
+  F.v[0] = v3(o); F.v[1] = v3(o + 3); F.v[2] = v3(o + 6);
+  Vec3 nn = cross(F.v[1] - F.v[0], F.v[2] - F.v[0]);
+  F.n = (1.0 / norm(nn)) * nn;
+  for (int k = 0; k < 3; ++k) {
+    Vec3 ev = F.v[(k + 1) % 3] - F.v[k];
+    F.L[k] = norm(ev);
+    F.sh[k] = (1.0 / F.L[k]) * ev;
+    F.mh[k] = cross(F.sh[k], F.n);
+  }
+}
+
+// Closed-form I0 = int 1/R dS', I1 = int (rho' - rho)/R dS' over the flat source
+// triangle (Wilton et al. / Graglia form); same guards as the oracle's recipe.
+__device__ __forceinline__ void potentials(const Frame& F, Vec3 r, double& I0, Vec3& I1, Vec3& rho) {
+  double d = dot(r - F.v[0], F.n);
+  rho = r - d * F.n;
+  double ad = fabs(d);
+  I0 = 0.0;
+  I1 = {0.0, 0.0, 0.0};
+  for (int k = 0; k < 3; ++k) {
+    Vec3 va = F.v[k], vb = F.v[(k + 1) % 3];
+    double sm = dot(va - rho, F.sh[k]);
+    double sp = dot(vb - rho, F.sh[k]);
+    double t0 = dot(va - rho, F.mh[k]);
+    double R0sq = t0 * t0 + d * d;
+    double Rm = norm(r - va), Rp = norm(r - vb);
+    double lim = 1e-14 * F.L[k];
+    double f2 = 0.0;
+    if (R0sq > lim * lim) f2 = logsum(Rp, sp, R0sq) - logsum(Rm, sm, R0sq);
+    double beta = 0.0;
+    if (ad > 0.0) beta = atan(t0 * sp / (R0sq + ad * Rp)) - atan(t0 * sm / (R0sq + ad * Rm));
+    I0 += t0 * f2 - ad * beta;
+    double g = 0.5 * (R0sq * f2 + sp * Rp - sm * Rm);
+    I1 = I1 + g * F.mh[k];
+  }
+}
+
+// Warp per row m; lanes over the row's entries: unsymmetrised static entries,
+// outer integral over m's triangles, inner (analytic) over n's triangles.
+__global__ void k_static_near(int nb, const int64_t* __restrict__ rowptr,
+                              const int32_t* __restrict__ col, const double* __restrict__ side,
+                              double* __restrict__ LA, double* __restrict__ YR) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= nb) return;
+  const int m = (int)warp;
+  const double inv4pi = 1.0 / (4.0 * kPi);
+  for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
+    const int n = col[k];
+    double la = 0.0, yr = 0.0;
+    for (int sm = 0; sm < 2; ++sm) {
+      const double* om = side + (2 * (int64_t)m + sm) * kSideStride;
+      Vec3 a = v3(om), b = v3(om + 3), c = v3(om + 6), pm = v3(om + 9);
+      double coef_m = om[12], div_m = om[13], area_m = om[14];
+      for (int sn = 0; sn < 2; ++sn) {
+        const double* on = side + (2 * (int64_t)n + sn) * kSideStride;
+        Frame F;
+        make_frame(on, F);
+        Vec3 pn = v3(on + 9);
+        double coef_n = on[12], div_n = on[13];
+        double sA = 0.0, sR = 0.0;
+        for (int q = 0; q < 7; ++q) {
+          double b0, b1, b2, w;
+          radon7(q, b0, b1, b2, w);
+          Vec3 r = b0 * a + b1 * b + b2 * c;
+          double I0;
+          Vec3 I1, rho;
+          potentials(F, r, I0, I1, rho);
+          Vec3 inner = coef_n * (I1 + I0 * (rho - pn));
+          Vec3 fm = coef_m * (r - pm);
+          sA += w * area_m * dot(fm, inner);
+          sR += w * area_m * I0;
+        }
+        la += sA * inv4pi;
+        yr += div_m * div_n * sR * inv4pi;
+      }
+    }
+    LA[k] = la;
+    YR[k] = yr;
+  }
+}
+
+// Warp per row m: symmetrise (L + L^T)/2 via the transposed position, then the
+// precorrection L_s,P[m,n] = sum_c Lambda^c_m^T B_D Lambda^c_n, B_D[s,s'] =
+// H_s(s - s' - D), D = A_n - A_m, and C = L_s,NR - L_s,P.
+__global__ void k_precorrect(int nb, int order, const int64_t* __restrict__ rowptr,
+                             const int32_t* __restrict__ col, const int32_t* __restrict__ anchor,
+                             const double* __restrict__ lam, const double* __restrict__ LAun,
+                             const double* __restrict__ YRun, double* __restrict__ LA_NR,
+                             double* __restrict__ YR_NR, double* __restrict__ LA_P,
+                             double* __restrict__ YR_P, double* __restrict__ CA,
+                             double* __restrict__ CR) {
+  extern __shared__ double sh[];
+  const int p = order + 1, p3 = p * p * p;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  double* lm = sh + wib * (p3 * 4);
+  const bool active = warp < nb;
+  const int m = active ? (int)warp : 0;
+  for (int t = lane; t < p3 * 4; t += 32) lm[t] = active ? lam[(int64_t)m * p3 * 4 + t] : 0.0;
+  __syncwarp();
+  if (!active) return;
+  const int Amx = anchor[3 * m], Amy = anchor[3 * m + 1], Amz = anchor[3 * m + 2];
+  for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
+    const int n = col[k];
+    // transposed position: column m inside row n (columns ascending)
+    int64_t lo = rowptr[n], hi = rowptr[n + 1] - 1;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < m) lo = mid + 1; else hi = mid;
+    }
+    const int64_t kt = lo;
+    const double la_nr = 0.5 * (LAun[k] + LAun[kt]);
+    const double yr_nr = 0.5 * (YRun[k] + YRun[kt]);
+    const int Dx = anchor[3 * n] - Amx, Dy = anchor[3 * n + 1] - Amy, Dz = anchor[3 * n + 2] - Amz;
+    // per-axis squared offsets (i - i' - D)^2 for i - i' in [-n, n]
+    int sqx[7], sqy[7], sqz[7];
+    for (int d = -order; d <= order; ++d) {
+      sqx[d + order] = (d - Dx) * (d - Dx);
+      sqy[d + order] = (d - Dy) * (d - Dy);
+      sqz[d + order] = (d - Dz) * (d - Dz);
+    }
+    const double* ln = lam + (int64_t)n * p3 * 4;
+    double acc[4] = {0, 0, 0, 0};
+    for (int s2 = 0; s2 < p3; ++s2) {
+      const int i2 = s2 % p, j2 = (s2 / p) % p, k2 = s2 / (p * p);
+      double u0 = 0, u1 = 0, u2 = 0, u3 = 0;
+      for (int s1 = 0; s1 < p3; ++s1) {
+        const int i1 = s1 % p, j1 = (s1 / p) % p, k1 = s1 / (p * p);
+        const int qq = sqx[i1 - i2 + order] + sqy[j1 - j2 + order] + sqz[k1 - k2 + order];
+        const double hs = c_hs_tab[qq];
+        u0 += lm[s1 * 4 + 0] * hs;
+        u1 += lm[s1 * 4 + 1] * hs;
+        u2 += lm[s1 * 4 + 2] * hs;
+        u3 += lm[s1 * 4 + 3] * hs;
+      }
+      acc[0] += u0 * ln[s2 * 4 + 0];
+      acc[1] += u1 * ln[s2 * 4 + 1];
+      acc[2] += u2 * ln[s2 * 4 + 2];
+      acc[3] += u3 * ln[s2 * 4 + 3];
+    }
+    const double la_p = acc[0] + acc[1] + acc[2];
+    const double yr_p = acc[3];
+    LA_NR[k] = la_nr;
+    YR_NR[k] = yr_nr;
+    LA_P[k] = la_p;
+    YR_P[k] = yr_p;
+    CA[k] = la_nr - la_p;
+    CR[k] = yr_nr - yr_p;
+  }
+}
+
+void gauss_legendre(int q, double* x, double* w) {
+  // nodes/weights on [0, 1]
+  for (int i = 0; i < q; ++i) {
+    double z = std::cos(kPi * (i + 0.75) / (q + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= q; ++k) {
+        double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      double dp = q * (z * p1 - p0) / (z * z - 1.0);
+      double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) {
+        // recompute derivative at the converged root
+        p0 = 1.0; p1 = z;
+        for (int k = 2; k <= q; ++k) {
+          double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+          p0 = p1;
+          p1 = p2;
+        }
+        dp = q * (z * p1 - p0) / (z * z - 1.0);
+        x[i] = 0.5 * (1.0 - z);
+        w[i] = 1.0 / ((1.0 - z * z) * dp * dp);   // (2/((1-z^2) dp^2)) * 1/2
+        break;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void launch_rwg_sides(const Topology& t, SetupDev& d, cudaStream_t s) {
+  int64_t n = 2 * t.nb;
+  k_rwg_sides<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((int)t.nb, d.V, d.T, d.ea, d.eb, d.tp,
+                                                          d.tm, d.pp, d.pm, d.side);
+  AIMX_CHECK_LAUNCH();
+}
+
+void launch_weights(const Topology& t, SetupDev& d, cudaStream_t s, uint8_t* nzflag) {
+  const int q = (3 * t.order + 4) / 2;   // exact for degree 3n+1 after the collapse
+  double x[8], w[8];
+  gauss_legendre(q, x, w);
+  AIMX_CUDA(cudaMemcpyToSymbolAsync(c_gl_x, x, sizeof(double) * q, 0, cudaMemcpyHostToDevice, s));
+  AIMX_CUDA(cudaMemcpyToSymbolAsync(c_gl_w, w, sizeof(double) * q, 0, cudaMemcpyHostToDevice, s));
+  int64_t n = t.nb * (int64_t)t.p3;
+  k_weights<<<(unsigned)((n + 127) / 128), 128, 0, s>>>((int)t.nb, t.order, q, d.side, d.anchor,
+                                                        t.origin[0], t.origin[1], t.origin[2], t.h,
+                                                        d.lam, nzflag);
+  AIMX_CHECK_LAUNCH();
+}
+
+void launch_static_near(const Topology& t, SetupDev& d, cudaStream_t s) {
+  const int threads = 128;
+  int64_t blocks = (t.nb * 32 + threads - 1) / threads;
+  k_static_near<<<(unsigned)blocks, threads, 0, s>>>((int)t.nb, d.rowptr, d.col, d.side, d.LA_un,
+                                                     d.YR_un);
+  AIMX_CHECK_LAUNCH();
+}
+
+void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s) {
+  std::vector<double> tab(512, 0.0);
+  for (int qq = 1; qq < 512; ++qq) tab[qq] = 1.0 / (4.0 * kPi * t.h * std::sqrt((double)qq));
+  const int R = 2 * t.order + t.near_cells;
+  if (3 * R * R >= 512) throw Error(AIMX_E_GRID, "precorrection offset table too small");
+  AIMX_CUDA(cudaMemcpyToSymbolAsync(c_hs_tab, tab.data(), sizeof(double) * 512, 0,
+                                    cudaMemcpyHostToDevice, s));
+  const int threads = 128;
+  int64_t blocks = (t.nb * 32 + threads - 1) / threads;
+  size_t shm = (threads / 32) * t.p3 * 4 * sizeof(double);
+  k_precorrect<<<(unsigned)blocks, threads, shm, s>>>((int)t.nb, t.order, d.rowptr, d.col, d.anchor,
+                                                     d.lam, d.LA_un, d.YR_un, d.LA_NR, d.YR_NR,
+                                                     d.LA_P, d.YR_P, d.CA, d.CR);
+  AIMX_CHECK_LAUNCH();
+}
+
+}  // namespace aimx

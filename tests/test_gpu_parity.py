@@ -1,0 +1,178 @@
+"""GPU (CUDA, through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Bar (north_star): integer structures bit-exact; Z x, L_A x and
+L_phi x each within rel-L2 1e-11 (complex128 path) / 2e-5 (complex64 path).
+"""
+import numpy as np
+import pytest
+
+import aimx_inputs as inp
+from tests._parity import (TOL, check_structure, gpu_input_as_c128, make_gpu_op, rel_l2,
+                           to_gpu)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc1():
+    from oracle.aimx import from_config
+    return from_config(1)
+
+
+@pytest.fixture(scope="module", params=["c128", "c64"])
+def gpu1(request):
+    return make_gpu_op(inp.make_mesh(1), (16, 16, 4), request.param), request.param
+
+
+def test_cfg1_structures_bit_exact(gpu1, orc1):
+    op, prec = gpu1
+    check_structure(op, orc1)
+
+
+def test_cfg1_weights_and_static(gpu1, orc1):
+    op, prec = gpu1
+    lam = op.weights()
+    assert np.max(np.abs(lam - orc1.Lam)) <= 1e-14 * np.abs(orc1.Lam).max() * 10
+    s = op.static()
+    for key, ref in (("LA_NR", orc1.LA_NR), ("YR_NR", orc1.YR_NR), ("LA_P", orc1.LA_P),
+                     ("YR_P", orc1.YR_P), ("CA", orc1.CA), ("CR", orc1.CR)):
+        assert rel_l2(s[key], ref) <= 1e-12, key
+
+
+def test_cfg1_static_spectrum(gpu1, orc1):
+    op, prec = gpu1
+    Hs = op.spectrum(0)
+    Nx, Ny, Nz = orc1.grid.n
+    ref = orc1.Hs_hat[: Nz + 1, : Ny + 1, : Nx + 1]          # [kz, ky, kx]
+    ref = np.transpose(ref, (1, 2, 0))                      # -> [ky, kx, kz]
+    assert rel_l2(Hs, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("fi", [0, 1])
+def test_cfg1_matvec_parts_and_combined(gpu1, orc1, fi):
+    op, prec = gpu1
+    f = 150e6 if fi == 0 else 37.5e6
+    op.set_frequency(f)
+    orc1.set_frequency(f)
+    Hd = op.spectrum(1)
+    Nx, Ny, Nz = orc1.grid.n
+    ref = np.transpose(orc1.H_hat[: Nz + 1, : Ny + 1, : Nx + 1], (1, 2, 0))
+    assert rel_l2(Hd, ref) <= (1e-13 if prec == "c128" else 1e-6)
+    for i in range(3):
+        x = inp.rhs_vector(1, i, op.N)
+        xg = to_gpu(x, prec)
+        xo = gpu_input_as_c128(x, prec)
+        y = op.matvec(xg).cpu().numpy()
+        yA, yP = op.matvec_parts(xg)
+        yA, yP = yA.cpu().numpy(), yP.cpu().numpy()
+        oA, oR = orc1.parts(xo)
+        z = orc1.combine(oA, oR)
+        assert rel_l2(yA, oA) <= TOL[prec]
+        assert rel_l2(yP, -oR) <= TOL[prec]
+        assert rel_l2(y, z) <= TOL[prec]
+
+
+def test_cfg1_edge_cases(gpu1):
+    import torch
+    op, prec = gpu1
+    from paper_2009_02281_b200 import AIMxError
+    op.set_frequency(150e6)
+    z = torch.zeros(op.N, dtype=op.cdtype, device="cuda")
+    assert torch.count_nonzero(op.matvec(z)) == 0
+    x = to_gpu(inp.rhs_vector(1, 5, op.N), prec)
+    y1 = op.matvec(x).clone()
+    y2 = op.matvec(x).clone()
+    assert torch.equal(y1, y2)                   # deterministic, no atomics
+    a = 0.5 - 2.0j
+    ya = op.matvec((x * a).contiguous())
+    assert rel_l2(ya.cpu().numpy(), (y1 * a).cpu().numpy()) <= TOL[prec]
+    with pytest.raises(AIMxError):
+        op.set_frequency(0.0)
+    with pytest.raises(AIMxError):
+        op.set_frequency(float("nan"))
+    with pytest.raises(AIMxError):
+        op.matvec(x, x)                           # aliasing
+
+
+def test_matvec_before_frequency_is_state_error():
+    from paper_2009_02281_b200 import AIMxError
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), "c64")
+    x = to_gpu(np.ones(op.N), "c64")
+    with pytest.raises(AIMxError) as e:
+        op.matvec(x)
+    assert e.value.status == 4
+
+
+def test_setup_errors():
+    from paper_2009_02281_b200 import AIMxError
+    m = inp.make_mesh(1)
+    with pytest.raises(AIMxError) as e:           # grid too small for the stencil fit
+        make_gpu_op(m, (16, 16, 2), "c64")
+    assert e.value.status == 3
+    with pytest.raises(AIMxError) as e:           # FFT length 2*12 not compiled
+        make_gpu_op(m, (12, 16, 4), "c64")
+    assert e.value.status == 7
+    V = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0]], float)
+    bad = inp.Mesh(V, np.array([[0, 1, 2], [1, 2, 3]], np.int32))
+    with pytest.raises(AIMxError) as e:           # inconsistent orientation
+        make_gpu_op(bad, (8, 8, 4), "c64")
+    assert e.value.status == 2
+    deg = inp.Mesh(V, np.array([[0, 1, 1]], np.int32))
+    with pytest.raises(AIMxError) as e:
+        make_gpu_op(deg, (8, 8, 4), "c64")
+    assert e.value.status == 2
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_sweep_equals_matvec_loop_and_host_sweep(prec):
+    import torch
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), prec)
+    freqs = np.linspace(50e6, 300e6, 5)
+    X = np.stack([inp.rhs_vector(1, i, op.N) for i in range(5)])
+    Xg = to_gpu(X, prec)
+    Y = op.sweep(freqs, Xg).cpu()
+    for i, f in enumerate(freqs):
+        op.set_frequency(f)
+        yi = op.matvec(Xg[i].contiguous()).cpu()
+        assert torch.equal(yi, Y[i])
+    Xh = Xg.cpu().pin_memory()
+    Yh = torch.empty_like(Xh).pin_memory()
+    op.sweep_host(freqs, Xh, Yh, batch=2)
+    assert torch.equal(Yh, Y)
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_small_closed_mesh_ragged_grid(prec):
+    """Closed icosphere on a ragged non-cubic grid (several tiles + tails)."""
+    from oracle.aimx import AIMxOracle
+    m = inp.icosphere_mesh(2)
+    n = (16, 8, 32)
+    orc = AIMxOracle(m.vertices, m.triangles, n)
+    op = make_gpu_op(m, n, prec)
+    check_structure(op, orc)
+    for f in (30e6, 400e6):
+        op.set_frequency(f)
+        orc.set_frequency(f)
+        x = np.random.default_rng(3).standard_normal(op.N) * (1 + 0.5j)
+        xg = to_gpu(x, prec)
+        yA, yP = op.matvec_parts(xg)
+        oA, oR = orc.parts(gpu_input_as_c128(x, prec))
+        assert rel_l2(yA.cpu().numpy(), oA) <= TOL[prec]
+        assert rel_l2(yP.cpu().numpy(), -oR) <= TOL[prec]
+
+
+@pytest.mark.parametrize("order", [1, 3])
+def test_other_stencil_orders(order):
+    from oracle.aimx import AIMxOracle
+    m = inp.icosphere_mesh(2)
+    n = (16, 16, 16)
+    orc = AIMxOracle(m.vertices, m.triangles, n, order=order)
+    op = make_gpu_op(m, n, "c128", order=order)
+    check_structure(op, orc)
+    op.set_frequency(200e6)
+    orc.set_frequency(200e6)
+    x = np.random.default_rng(4).standard_normal(op.N) + 0j
+    yA, yP = op.matvec_parts(to_gpu(x, "c128"))
+    oA, oR = orc.parts(x)
+    assert rel_l2(yA.cpu().numpy(), oA) <= 1e-11
+    assert rel_l2(yP.cpu().numpy(), -oR) <= 1e-11
