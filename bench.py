@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""AIMx frequency-sweep benchmark on B200 (driver contract: one JSON line).
+
+Metric (BASELINE.json): "AIMx matvec/s and sweep freq-pts/s at 1/2/4/8 B200;
+HBM GB/s vs peak".  The headline `value` is sweep frequency points per second
+for the whole job; a "step" is one sweep of the rank's 100 frequency points of
+configs[1] (cfg2, two PEC strips, 20,028 RWG unknowns, grid 256x16x4, order 2,
+complex64): per point, the device-side spectrum regeneration (S1) and one AIMx
+matvec (S2-S5) -- every row of SURVEY.md section 8(a).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--prec c64|c128]
+    python bench.py --impl reference ...     # the fp64 CPU oracle, timed as is
+
+Multi-GPU (torchrun, one process per GPU): frequency points shard with no data
+collective (weak scaling: every rank sweeps 100 points of a 100*N-point band).
+The timed region is bracketed by barrier + synchronize; per-step device time is
+taken with CUDA events on the launching stream, L2 flushed (256 MB write)
+between steps, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import aimx_inputs as inp  # noqa: E402
+
+METRIC = "AIMx sweep freq-pts/s"
+UNIT = "freq-pts/s"
+STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
+KERNELS_PER_STAGE = {"spectrum": 4, "proj_xfft": 1, "yfwd": 1, "zconv": 1, "yinv": 1, "xinv": 1,
+                     "interp_near": 1}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="aimx", choices=["aimx", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--prec", default=None, choices=[None, "c64", "c128"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-freqs-per-step", type=int, default=2)
+    return ap.parse_args()
+
+
+def workload_desc(c: inp.Config, prec: str, nf: int) -> str:
+    n = c.grid_n
+    return (f"cfg{c.cfg} {c.name}: {c.expected_rwg} RWG, grid {n[0]}x{n[1]}x{n[2]} "
+            f"(padded {2*n[0]}x{2*n[1]}x{2*n[2]}), order {c.order}, near {c.near_cells} cells, "
+            f"{nf} freqs {c.freqs[0]/1e9:g}-{c.freqs[-1]/1e9:g} GHz per rank, {prec}")
+
+
+def env_dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def rank_freqs(c: inp.Config, rank: int, world: int):
+    nf = len(c.freqs)
+    g = np.linspace(c.freqs[0], c.freqs[-1], nf * world)
+    return g[rank * nf:(rank + 1) * nf], np.arange(rank * nf, (rank + 1) * nf)
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for k, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def stage_bytes(st: dict, prec: str) -> dict:
+    """Algorithmic (compulsory) bytes per launch of each stage, given this
+    implementation's pass structure."""
+    s = 8 if prec == "c64" else 16          # complex
+    r = s // 2                              # real
+    Nx, Ny, Nz = st["n"]
+    p3 = (st["order"] + 1) ** 3
+    nb, nnz = st["num_unknowns"], st["nnz"]
+    nocc, nl, nz_ = st["occupied_nodes"], st["occupied_lines"], st["occupied_planes"]
+    nent = st["projection_entries"]
+    noct = (Nx + 1) * (Ny + 1) * (Nz + 1)
+    row = 2 * Nx * 4 * s                    # one padded x-line, 4 channels
+    return {
+        "spectrum": 2 * noct * s,                                   # read H_hat_s, write H_hat
+        "proj_xfft": nent * (4 + 4 * r) + 8 * nocc + s * nb + nl * row,
+        "yfwd": nz_ * Ny * row + nz_ * 2 * Ny * row,
+        "zconv": 2 * nz_ * 2 * Ny * row + noct * s,
+        "yinv": nz_ * 2 * Ny * row + nl * row,
+        "xinv": nl * row + nl * Nx * 4 * s,
+        "interp_near": nb * p3 * 4 * r + 4 * nb + nocc * 4 * s + 4 * (nb + 1)
+                       + nnz * (4 + 2 * r) + 2 * s * nb,
+    }
+
+
+def ncu_traffic(cfg: int, prec: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    d = json.load(open(p))
+    return d.get(f"cfg{cfg}_{prec}", {})
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def oracle_sweep_rate(cfg: int, freqs, X, seconds: float, min_pts: int = 2):
+    """The fp64 oracle as it stands, on this host's cores: setup (untimed),
+    then sweep frequency points until ~`seconds` of work (>= min_pts)."""
+    from oracle.aimx import from_config
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    op = from_config(cfg, workers=cores)
+    t_setup = time.perf_counter() - t0
+    n, t = 0, 0.0
+    while n < len(freqs) and (n < min_pts or t < seconds):
+        a = time.perf_counter()
+        op.set_frequency(freqs[n])
+        op.matvec(X[n])
+        t += time.perf_counter() - a
+        n += 1
+    return {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"cfg{cfg}: oracle sweep of the first {n} of {len(freqs)} frequency points "
+                      f"({t:.1f} s; spectrum + matvec per point, fp64 NumPy/SciPy, scipy.fft "
+                      f"workers={cores}, scipy.sparse SpMV single-threaded); oracle setup "
+                      f"{t_setup:.1f} s with {cores} processes excluded like the GPU setup"}, op
+
+
+def run_reference(a):
+    rank, world, _ = env_dist()
+    if rank != 0:
+        return 0
+    c = inp.get_config(a.config)
+    prec = a.prec or c.precisions[0]
+    freqs, idx = rank_freqs(c, 0, 1)
+    from oracle.aimx import from_config
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    op = from_config(a.config, workers=cores)
+    t_setup = time.perf_counter() - t0
+    X = inp.rhs_matrix(a.config, op.N, idx)
+    per = a.ref_freqs_per_step
+    for w in range(a.warmup):
+        for i in range(per):
+            op.set_frequency(freqs[i])
+            op.matvec(X[i])
+    t = 0.0
+    for k in range(a.steps):
+        a0 = time.perf_counter()
+        for i in range(per):
+            j = (k * per + i) % len(freqs)
+            op.set_frequency(freqs[j])
+            op.matvec(X[j])
+        t += time.perf_counter() - a0
+    value = per * a.steps / t
+    sample = (f"each step = {per} of cfg{a.config}'s {len(freqs)} frequency points (spectrum + "
+              f"matvec each), fp64 oracle, {cores} host cores; oracle setup {t_setup:.1f} s excluded")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * t / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded meshes and complex-Gaussian x, aimx_inputs)",
+        "config": {"workload": workload_desc(c, "c128 (oracle)", len(freqs)), "config_index": a.config - 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_aimx(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2009_02281_b200 import AIMx
+
+    rank, world, local = env_dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = inp.get_config(a.config)
+    prec = a.prec or c.precisions[0]
+    mesh = inp.make_mesh(a.config)
+    op = AIMx(mesh.vertices, mesh.triangles, c.grid_n, order=c.order, near_cells=c.near_cells,
+              prec=prec)
+    st = op.stats()
+    freqs, idx = rank_freqs(c, rank, world)
+    nf = len(freqs)
+    cdt = torch.complex64 if prec == "c64" else torch.complex128
+    Xh = torch.from_numpy(inp.rhs_matrix(a.config, op.N, idx)).to(cdt)
+    X = Xh.cuda()
+    Y = torch.empty_like(X)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        flush.zero_()
+        op.sweep(freqs, X, Y)
+    torch.cuda.synchronize()
+    op.profile_enable(True)
+    barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
+    for k in range(a.steps):
+        flush.zero_()
+        evs[k][0].record()
+        op.sweep(freqs, X, Y)
+        evs[k][1].record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    prof = op.profile_read()
+    op.profile_enable(False)
+    total_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tmax = float(t.item())
+    value = nf * world * a.steps / (tmax / 1e3)
+
+    # matvec/s (secondary number: back-to-back matvecs at the first frequency)
+    op.set_frequency(freqs[0])
+    x0 = X[0].contiguous()
+    y0 = torch.empty_like(x0)
+    for _ in range(20):
+        op.matvec(x0, y0)
+    torch.cuda.synchronize()
+    nmv = 200
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(nmv):
+        op.matvec(x0, y0)
+    e1.record()
+    torch.cuda.synchronize()
+    mv_ms = e0.elapsed_time(e1) / nmv
+    mv = torch.tensor([mv_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(mv, op=dist.ReduceOp.MAX)
+    matvec_per_s = world * 1e3 / float(mv.item())
+
+    # end to end: the same sweep through the C ABI with HOST buffers (pinned)
+    Xp = Xh.pin_memory()
+    Yp = torch.empty_like(Xp).pin_memory()
+    op.sweep_host(freqs, Xp, Yp)
+    barrier()
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    for k in range(a.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        b0 = time.perf_counter()
+        op.sweep_host(freqs, Xp, Yp)          # synchronises its stream before returning
+        e2e_ms += 1e3 * (time.perf_counter() - b0)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = nf * world * a.steps / (float(te.item()) / 1e3)
+    vec_bytes = op.N * (8 if prec == "c64" else 16)
+
+    # roofline of the dominant stage
+    peak, peak_src = measured_peaks()
+    sb = stage_bytes(st, prec)
+    traffic = ncu_traffic(a.config, prec)
+    step_stage_ms = sum(ms for ms, n in prof.values())
+    stages = {}
+    for k in STAGES:
+        ms, n = prof[k]
+        if n == 0:
+            continue
+        avg = ms / n
+        stages[k] = {"ms_per_launch": avg, "launches": n, "bytes_per_launch": sb[k],
+                     "GBps": sb[k] / (avg * 1e-3) / 1e9, "share": ms / step_stage_ms}
+    dom = max(stages, key=lambda k: stages[k]["share"])
+    ach = stages[dom]["GBps"]
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic.get(dom), "kernel": dom, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": sb[dom]}
+    launches = sum(n * KERNELS_PER_STAGE[k] for k, (ms, n) in prof.items())
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            cpu, _ = oracle_sweep_rate(a.config, freqs, Xh.numpy().astype(np.complex128),
+                                       a.cpu_seconds)
+        except Exception as e:  # report, never fail the GPU number
+            cpu = {"value": None, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+                   "kind": "oracle", "sample": f"failed: {e!r}"}
+
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": tmax / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": prec,
+            "data": "synthetic (seeded meshes and complex-Gaussian x per frequency, aimx_inputs)",
+            "config": {"workload": workload_desc(c, prec, nf), "config_index": a.config - 1,
+                       "freq_pts_per_rank_per_step": nf, "parallelism": f"freq-shard x{world}",
+                       "l2": "flushed between timed steps (256 MB write); inputs resident in HBM",
+                       "setup_seconds": st["setup_seconds"]},
+            "matvec_per_s": matvec_per_s,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nf * vec_bytes,
+                    "d2h_bytes_per_step": nf * vec_bytes},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "stages": stages,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_aimx(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

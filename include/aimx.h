@@ -100,6 +100,7 @@ typedef struct {
   int64_t occupied_nodes;     /* grid nodes carrying a non-zero projection weight */
   int64_t occupied_lines;     /* x-lines (y, z) with an occupied node */
   int64_t occupied_planes;    /* z planes with an occupied node */
+  int64_t projection_entries; /* (RWG, node) pairs with a non-zero projection weight */
   int64_t device_bytes;       /* device memory owned by the context */
   double setup_seconds;       /* wall time of aimx_setup */
   int32_t n[3];
@@ -171,6 +172,17 @@ aimx_status aimx_get_weights(const aimx_ctx* ctx, double* lam);
 /* Spectrum octant, complex128 interleaved, index ((ky (N_x+1) + kx)(N_z+1) + kz):
  * which = 0 static H_hat_s, 1 the bound H_hat(k0) (unnormalised DFT). */
 aimx_status aimx_get_spectrum(const aimx_ctx* ctx, int which, double* out);
+
+/* ---- stage profiling (CUDA events recorded on the launching stream) ----
+ * Stages: 0 spectrum (S1: sample + 3 DCT passes), 1 proj_xfft (S2 + x fwd),
+ * 2 yfwd, 3 zconv (z fwd * H_hat * z inv), 4 yinv, 5 xinv, 6 interp_near
+ * (S4 + S5).  When enabled, every launch of a stage is bracketed by a pair of
+ * events; aimx_profile_read synchronises the context, adds up the elapsed
+ * device time per stage (ms) and the number of bracketed launches since the
+ * previous read, and resets them.  Arrays have AIMX_NUM_STAGES entries. */
+#define AIMX_NUM_STAGES 7
+aimx_status aimx_profile_enable(aimx_ctx* ctx, int on);
+aimx_status aimx_profile_read(aimx_ctx* ctx, double* ms, int64_t* launches);
 
 void aimx_destroy(aimx_ctx* ctx);
 const char* aimx_status_string(aimx_status s);

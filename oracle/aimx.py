@@ -33,7 +33,7 @@ from .static_near import static_near_matrices, static_pair_entries
 
 class AIMxOracle:
     def __init__(self, V, T, n, order: int = 2, near_cells: int = 2,
-                 grid: Grid | None = None, static: bool = True):
+                 grid: Grid | None = None, static: bool = True, workers: int = 1):
         self.V = np.asarray(V, np.float64)
         self.T = np.asarray(T, np.int64)
         self.rwg = build_rwg(self.V, self.T)
@@ -51,6 +51,7 @@ class AIMxOracle:
                                 shape=(Ng, N)) for c in range(4)]
         self.Hs_hat = conv.spectrum_static(self.grid.n, self.grid.h)
         self.CA = self.CR = None
+        self.workers = workers
         if static:
             self.build_static()
         self.k0 = None
@@ -61,8 +62,10 @@ class AIMxOracle:
 
     # ---------------------------------------------------------------- S0
     def build_static(self):
-        LA_NR, YR_NR = static_near_matrices(self.V, self.T, self.rwg, self.rowptr, self.col)
-        LA_P, YR_P = precorrection(self.Lam, self.A, self.rowptr, self.col, self.order, self.grid.h)
+        LA_NR, YR_NR = static_near_matrices(self.V, self.T, self.rwg, self.rowptr, self.col,
+                                            workers=self.workers)
+        LA_P, YR_P = precorrection(self.Lam, self.A, self.rowptr, self.col, self.order, self.grid.h,
+                                   workers=self.workers)
         self.LA_NR, self.YR_NR, self.LA_P, self.YR_P = LA_NR, YR_NR, LA_P, YR_P
         self.CA = LA_NR - LA_P
         self.CR = YR_NR - YR_P
@@ -154,9 +157,9 @@ def _precorr_row(op: AIMxOracle, m: int, cols):
     return la, yr
 
 
-def from_config(cfg: int, static: bool = True) -> AIMxOracle:
+def from_config(cfg: int, static: bool = True, workers: int = 1) -> AIMxOracle:
     import aimx_inputs as inp
     c = inp.get_config(cfg)
     mesh = inp.make_mesh(cfg)
     return AIMxOracle(mesh.vertices, mesh.triangles, c.grid_n, c.order, c.near_cells,
-                      static=static)
+                      static=static, workers=workers)

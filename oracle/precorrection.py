@@ -35,10 +35,8 @@ def H_s_block(D: np.ndarray, order: int, h: float) -> np.ndarray:
     return out
 
 
-def precorrection(Lam: np.ndarray, A: np.ndarray, rowptr, col, order: int, h: float):
-    """Returns (LA_P, Yrho_P) aligned with the CSR pattern."""
-    N = A.shape[0]
-    rows = np.repeat(np.arange(N), np.diff(rowptr))
+def precorrection_entries(Lam: np.ndarray, A: np.ndarray, rows, col, order: int, h: float):
+    """L^A_s,P and y^rho_s,P for the listed (row, col) pairs."""
     D = A[col] - A[rows]
     LA = np.zeros(col.shape[0])
     YR = np.zeros(col.shape[0])
@@ -57,6 +55,24 @@ def precorrection(Lam: np.ndarray, A: np.ndarray, rowptr, col, order: int, h: fl
         LA[idx] = t[:, 0] + t[:, 1] + t[:, 2]
         YR[idx] = t[:, 3]
     return LA, YR
+
+
+def _pc_job(args):
+    return precorrection_entries(*args)
+
+
+def precorrection(Lam: np.ndarray, A: np.ndarray, rowptr, col, order: int, h: float,
+                  workers: int = 1, chunk: int = 1000000):
+    """Returns (LA_P, Yrho_P) aligned with the CSR pattern."""
+    N = A.shape[0]
+    rows = np.repeat(np.arange(N), np.diff(rowptr))
+    if workers <= 1 or col.shape[0] <= chunk:
+        return precorrection_entries(Lam, A, rows, col, order, h)
+    import multiprocessing as mp
+    spans = [(s, min(col.shape[0], s + chunk)) for s in range(0, col.shape[0], chunk)]
+    with mp.get_context("fork").Pool(workers) as pool:
+        res = pool.map(_pc_job, [(Lam, A, rows[s:e], col[s:e], order, h) for s, e in spans])
+    return np.concatenate([r[0] for r in res]), np.concatenate([r[1] for r in res])
 
 
 def precorrection_dense(Lam: np.ndarray, A: np.ndarray, grid, rowptr, col):

@@ -131,16 +131,30 @@ def static_pair_entries(V, T, rwg: RWG, rows, cols):
     return LA, YR
 
 
-def static_near_matrices(V, T, rwg: RWG, rowptr, col, chunk: int = 200000):
+def _chunk_job(args):
+    V, T, rwg, rows, cols = args
+    return static_pair_entries(V, T, rwg, rows, cols)
+
+
+def static_near_matrices(V, T, rwg: RWG, rowptr, col, chunk: int = 200000, workers: int = 1):
     """Symmetrised L^A_s,NR and y^rho_s,NR on the near pattern, as CSR data
-    arrays aligned with (rowptr, col)."""
+    arrays aligned with (rowptr, col).  `workers` > 1 evaluates chunks of
+    pairs in a process pool (same per-pair arithmetic)."""
     N = rwg.n
     rows = np.repeat(np.arange(N), np.diff(rowptr))
     LA = np.empty(col.shape[0])
     YR = np.empty(col.shape[0])
-    for s in range(0, col.shape[0], chunk):
-        e = min(col.shape[0], s + chunk)
-        LA[s:e], YR[s:e] = static_pair_entries(V, T, rwg, rows[s:e], col[s:e])
+    spans = [(s, min(col.shape[0], s + chunk)) for s in range(0, col.shape[0], chunk)]
+    if workers > 1 and len(spans) > 1:
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        with ctx.Pool(workers) as pool:
+            res = pool.map(_chunk_job, [(V, T, rwg, rows[s:e], col[s:e]) for s, e in spans])
+        for (s, e), (a, r) in zip(spans, res):
+            LA[s:e], YR[s:e] = a, r
+    else:
+        for s, e in spans:
+            LA[s:e], YR[s:e] = static_pair_entries(V, T, rwg, rows[s:e], col[s:e])
     return symmetrize(rowptr, col, LA), symmetrize(rowptr, col, YR)
 
 

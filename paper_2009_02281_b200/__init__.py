@@ -46,7 +46,7 @@ class _Grid(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("num_unknowns", C.c_int64), ("nnz", C.c_int64), ("occupied_nodes", C.c_int64),
                 ("occupied_lines", C.c_int64), ("occupied_planes", C.c_int64),
-                ("device_bytes", C.c_int64), ("setup_seconds", C.c_double),
+                ("projection_entries", C.c_int64), ("device_bytes", C.c_int64), ("setup_seconds", C.c_double),
                 ("n", C.c_int32 * 3), ("order", C.c_int32), ("h", C.c_double),
                 ("origin", C.c_double * 3)]
 
@@ -67,6 +67,8 @@ ABI_FUNCTIONS = {
     "aimx_get_static": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "aimx_get_weights": (C.c_int, [_P, _P]),
     "aimx_get_spectrum": (C.c_int, [_P, C.c_int, _P]),
+    "aimx_profile_enable": (C.c_int, [_P, C.c_int]),
+    "aimx_profile_read": (C.c_int, [_P, _P, _P]),
     "aimx_destroy": (None, [_P]),
     "aimx_status_string": (C.c_char_p, [C.c_int]),
     "aimx_last_error": (C.c_char_p, [_P]),
@@ -221,8 +223,20 @@ class AIMx:
         _check(self.lib, self.lib.aimx_get_stats(self.ctx, C.byref(s)), self.ctx)
         return {"num_unknowns": s.num_unknowns, "nnz": s.nnz, "occupied_nodes": s.occupied_nodes,
                 "occupied_lines": s.occupied_lines, "occupied_planes": s.occupied_planes,
-                "device_bytes": s.device_bytes, "setup_seconds": s.setup_seconds,
+                "projection_entries": s.projection_entries, "device_bytes": s.device_bytes, "setup_seconds": s.setup_seconds,
                 "n": tuple(s.n), "order": s.order, "h": s.h, "origin": tuple(s.origin)}
+
+    STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
+
+    def profile_enable(self, on: bool = True):
+        _check(self.lib, self.lib.aimx_profile_enable(self.ctx, int(bool(on))), self.ctx)
+
+    def profile_read(self) -> dict:
+        ms = np.zeros(7)
+        n = np.zeros(7, np.int64)
+        _check(self.lib, self.lib.aimx_profile_read(self.ctx, _P(ms.ctypes.data), _P(n.ctypes.data)),
+               self.ctx)
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.STAGES)}
 
     def rwg(self):
         ab = np.empty((self.N, 2), np.int32)

@@ -152,6 +152,34 @@ struct HotDev {
   void* Hoct = nullptr;          // bound spectrum octant / M (compute precision)
 };
 
+// Per-stage CUDA-event timer (aimx_profile_*).
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  double ms[8] = {0};
+  int64_t n[8] = {0};
+  cudaEvent_t get();
+  void begin(int stage, cudaStream_t s, cudaEvent_t& a);
+  void end(int stage, cudaStream_t s, cudaEvent_t a);
+  void collect();
+  ~Profiler();
+};
+
+struct StageScope {
+  Profiler* p;
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  StageScope(Profiler* p_, int st, cudaStream_t s_) : p(p_), stage(st), s(s_) {
+    if (p && p->on) p->begin(stage, s, a);
+  }
+  ~StageScope() {
+    if (p && p->on) p->end(stage, s, a);
+  }
+};
+
 struct Combine {
   // y = alpha (yA - beta yR), alpha = -j w mu0 (purely imaginary), beta = k0^-2;
   // mode 0: combined into y0; mode 1: parts y0 = yA, y1 = -yR.
@@ -161,7 +189,9 @@ struct Combine {
 };
 
 bool fft_length_supported(int L);
-void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s);
-void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s);
+void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s,
+                    Profiler* prof);
+void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s,
+                    Profiler* prof);
 
 }  // namespace aimx

@@ -30,6 +30,7 @@ struct aimx_ctx {
   void* stage = nullptr;        // sweep_host staging
   int64_t stage_bytes = 0;
   double setup_seconds = 0;
+  Profiler prof;
   std::vector<void*> allocs;
   std::string last_error;
 };
@@ -247,6 +248,7 @@ void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
   const double k0 = 2.0 * kPi * f / kC0;
   const HotDev& h = c->hot;
   const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
+  StageScope sc(&c->prof, 0, s);
   if (c->prec == AIMX_C64)
     spectrum_dynamic_f32(c->sp, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)h.Hoct, s);
   else
@@ -262,8 +264,8 @@ void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaSt
   cb.alpha_im = -c->omega * kMu0;
   cb.beta = 1.0 / (c->k0 * c->k0);
   cb.mode = mode;
-  if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, s);
-  else hot_matvec_f64(c->hot, x, y0, y1, cb, s);
+  if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, s, &c->prof);
+  else hot_matvec_f64(c->hot, x, y0, y1, cb, s, &c->prof);
 }
 
 aimx_status fail(aimx_ctx* c, const Error& e) {
@@ -462,6 +464,7 @@ aimx_status aimx_get_stats(const aimx_ctx* c, aimx_stats* o) {
   o->occupied_nodes = (int64_t)c->nodes.node_lin.size();
   o->occupied_lines = (int64_t)c->nodes.line_id.size();
   o->occupied_planes = (int64_t)c->nodes.zplanes.size();
+  o->projection_entries = (int64_t)c->nodes.ent_rwg.size();
   o->device_bytes = c->dev_bytes;
   o->setup_seconds = c->setup_seconds;
   for (int a = 0; a < 3; ++a) { o->n[a] = c->topo.n[a]; o->origin[a] = c->topo.origin[a]; }
@@ -548,6 +551,29 @@ aimx_status aimx_get_spectrum(const aimx_ctx* cc, int which, double* out) {
       AIMX_CUDA(cudaMemcpy(out, c->hot.Hoct, n * sizeof(double2), cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < 2 * n; ++i) out[i] *= M;
     }
+  }
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_profile_enable(aimx_ctx* c, int on) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  AIMX_CUDA(cudaSetDevice(c->device));
+  c->prof.collect();
+  c->prof.on = on != 0;
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_profile_read(aimx_ctx* c, double* ms, int64_t* launches) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  AIMX_CUDA(cudaSetDevice(c->device));
+  c->prof.collect();
+  for (int i = 0; i < AIMX_NUM_STAGES; ++i) {
+    if (ms) ms[i] = c->prof.ms[i];
+    if (launches) launches[i] = c->prof.n[i];
+    c->prof.ms[i] = 0;
+    c->prof.n[i] = 0;
   }
   AIMX_API_END(c)
 }

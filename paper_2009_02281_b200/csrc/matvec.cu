@@ -467,17 +467,21 @@ void run_z(const HotDev& h, cudaStream_t s) {
   }
 
 template <typename T>
-void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s) {
+void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s,
+                Profiler* prof) {
   using T2 = typename CT<T>::T2;
   const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz;
-  AIMX_SWITCH_L(Lx, (run_x_fwd<T, L>(h, x, s)));
-  AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, s)));
-  AIMX_SWITCH_L(Lz, (run_z<T, L>(h, s)));
-  AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, s)));
-  AIMX_SWITCH_L(Lx, (run_x_inv<T, L>(h, s)));
-  unsigned g = (unsigned)(((int64_t)h.nb * 32 + 255) / 256);
-  k_interp_near<T><<<g, 256, 0, s>>>(h, (const T2*)x, (T2*)y0, (T2*)y1, c);
-  AIMX_CHECK_LAUNCH();
+  { StageScope sc(prof, 1, s); AIMX_SWITCH_L(Lx, (run_x_fwd<T, L>(h, x, s))); }
+  { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, s))); }
+  { StageScope sc(prof, 3, s); AIMX_SWITCH_L(Lz, (run_z<T, L>(h, s))); }
+  { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, s))); }
+  { StageScope sc(prof, 5, s); AIMX_SWITCH_L(Lx, (run_x_inv<T, L>(h, s))); }
+  {
+    StageScope sc(prof, 6, s);
+    unsigned g = (unsigned)(((int64_t)h.nb * 32 + 255) / 256);
+    k_interp_near<T><<<g, 256, 0, s>>>(h, (const T2*)x, (T2*)y0, (T2*)y1, c);
+    AIMX_CHECK_LAUNCH();
+  }
 }
 
 }  // namespace
@@ -486,11 +490,51 @@ bool fft_length_supported(int L) {
   return L >= 8 && L <= 1024 && (L & (L - 1)) == 0;
 }
 
-void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s) {
-  hot_matvec<float>(h, x, y0, y1, c, s);
+void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s,
+                    Profiler* prof) {
+  hot_matvec<float>(h, x, y0, y1, c, s, prof);
 }
-void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s) {
-  hot_matvec<double>(h, x, y0, y1, c, s);
+void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s,
+                    Profiler* prof) {
+  hot_matvec<double>(h, x, y0, y1, c, s, prof);
+}
+
+cudaEvent_t Profiler::get() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  AIMX_CUDA(cudaEventCreate(&e));
+  return e;
+}
+void Profiler::begin(int stage, cudaStream_t s, cudaEvent_t& a) {
+  (void)stage;
+  a = get();
+  AIMX_CUDA(cudaEventRecord(a, s));
+}
+void Profiler::end(int stage, cudaStream_t s, cudaEvent_t a) {
+  cudaEvent_t b = get();
+  AIMX_CUDA(cudaEventRecord(b, s));
+  pending.push_back({stage, a, b});
+  if (pending.size() > 16384) collect();
+}
+void Profiler::collect() {
+  for (auto& r : pending) {
+    AIMX_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    AIMX_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.stage] += t;
+    n[r.stage] += 1;
+    pool.push_back(r.a);
+    pool.push_back(r.b);
+  }
+  pending.clear();
+}
+Profiler::~Profiler() {
+  for (auto& r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : pool) cudaEventDestroy(e);
 }
 
 }  // namespace aimx

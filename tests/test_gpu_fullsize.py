@@ -1,0 +1,64 @@
+"""Full-size parity at BASELINE.json's configs, in bench.py's launch
+configuration: integer structures bit-exact over the WHOLE problem; static
+matrices and outputs on seeded sampled rows that the oracle computes one by one
+(the grid part of the oracle runs on the full grid)."""
+import numpy as np
+import pytest
+
+import aimx_inputs as inp
+from tests._parity import TOL, check_structure, gpu_input_as_c128, make_gpu_op, rel_l2, to_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _fullsize(cfg, prec, freqs, nrows):
+    from oracle.aimx import from_config
+    c = inp.get_config(cfg)
+    orc = from_config(cfg, static=False)
+    op = make_gpu_op(inp.make_mesh(cfg), c.grid_n, prec)
+    check_structure(op, orc)
+    lam = op.weights()
+    assert np.max(np.abs(lam - orc.Lam)) <= 1e-13 * np.abs(orc.Lam).max()
+    rng = np.random.default_rng(cfg)
+    rows = np.sort(rng.choice(op.N, nrows, replace=False))
+    st = op.static()
+    sr = orc.static_rows(rows)
+    for m, (cols, ca, cr) in zip(rows, sr):
+        sl = slice(orc.rowptr[m], orc.rowptr[m + 1])
+        assert rel_l2(st["CA"][sl], ca) <= 1e-12
+        assert rel_l2(st["CR"][sl], cr) <= 1e-12
+    for fi, f in enumerate(freqs):
+        op.set_frequency(f)
+        orc.set_frequency(f)
+        x = inp.rhs_vector(cfg, fi, op.N)
+        xg = to_gpu(x, prec)
+        y = op.matvec(xg).cpu().numpy()
+        yA, yP = op.matvec_parts(xg)
+        a, r, z = orc.matvec_rows(gpu_input_as_c128(x, prec), rows)
+        assert rel_l2(yA.cpu().numpy()[rows], a) <= TOL[prec]
+        assert rel_l2(yP.cpu().numpy()[rows], -r) <= TOL[prec]
+        assert rel_l2(y[rows], z) <= TOL[prec]
+    return op
+
+
+def test_cfg2_fullsize_c64():
+    c = inp.get_config(2)
+    _fullsize(2, "c64", [c.freqs[0], c.freqs[-1]], 48)
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_cfg3_fullsize(prec):
+    c = inp.get_config(3)
+    _fullsize(3, prec, [c.freqs[0], c.freqs[-1]], 24)
+
+
+def test_cfg2_sweep_matches_per_frequency_matvecs():
+    import torch
+    c = inp.get_config(2)
+    op = make_gpu_op(inp.make_mesh(2), c.grid_n, "c64")
+    freqs = c.freqs[:8]
+    X = to_gpu(np.stack([inp.rhs_vector(2, i, op.N) for i in range(8)]), "c64")
+    Y = op.sweep(freqs, X)
+    for i, f in enumerate(freqs):
+        op.set_frequency(f)
+        assert torch.equal(op.matvec(X[i].contiguous()), Y[i])
