@@ -102,6 +102,7 @@ typedef struct {
   int64_t occupied_planes;    /* z planes with an occupied node */
   int64_t projection_entries; /* (RWG, node) pairs with a non-zero projection weight */
   int64_t device_bytes;       /* device memory owned by the context */
+  int64_t batch_slots;        /* frequency points per device batch (aimx_sweep) */
   double setup_seconds;       /* wall time of aimx_setup */
   int32_t n[3];
   int32_t order;
@@ -138,8 +139,13 @@ aimx_status aimx_matvec_parts(aimx_ctx* ctx, const void* x, void* yA, void* yPhi
 
 /* Frequency sweep: for i < nf, Y[i,:] = Z(f_hz[i]) X[i,:] (per frequency: S1
  * then S2-S5).  f_hz is a HOST array; X, Y device arrays [nf][N_b] row-major.
- * `batch` frequencies are processed per device batch (<= 0: library default).
- * The context's bound frequency is restored afterwards if one was set. */
+ * Frequencies run in device batches of `batch` points (<= 0 or more than the
+ * context's batch slots: all slots; slots are chosen at setup from the grid
+ * size, at most 16, environment variable AIMX_BATCH overrides): the spectra of
+ * a batch are generated together and one batched matvec reads the near matrix
+ * and the weights once for all of its right-hand sides.  Results do not depend
+ * on the batch size (fixed-order reductions, no atomics).  The context's bound
+ * frequency is restored afterwards if one was set. */
 aimx_status aimx_sweep(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* X,
                        void* Y, int32_t batch, void* stream);
 
@@ -169,7 +175,7 @@ aimx_status aimx_get_static(const aimx_ctx* ctx, double* CA, double* Crho,
 /* Projection weights (fp64) lam[N_b][4][(n+1)^3], channels (x, y, z, rho),
  * node s = i + (n+1)(j + (n+1) k). */
 aimx_status aimx_get_weights(const aimx_ctx* ctx, double* lam);
-/* Spectrum octant, complex128 interleaved, index ((ky (N_x+1) + kx)(N_z+1) + kz):
+/* Spectrum octant, complex128 interleaved, index ((ky (N_z+1) + kz)(N_x+1) + kx):
  * which = 0 static H_hat_s, 1 the bound H_hat(k0) (unnormalised DFT). */
 aimx_status aimx_get_spectrum(const aimx_ctx* ctx, int which, double* out);
 

@@ -46,7 +46,8 @@ class _Grid(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("num_unknowns", C.c_int64), ("nnz", C.c_int64), ("occupied_nodes", C.c_int64),
                 ("occupied_lines", C.c_int64), ("occupied_planes", C.c_int64),
-                ("projection_entries", C.c_int64), ("device_bytes", C.c_int64), ("setup_seconds", C.c_double),
+                ("projection_entries", C.c_int64), ("device_bytes", C.c_int64), ("batch_slots", C.c_int64),
+                ("setup_seconds", C.c_double),
                 ("n", C.c_int32 * 3), ("order", C.c_int32), ("h", C.c_double),
                 ("origin", C.c_double * 3)]
 
@@ -223,7 +224,8 @@ class AIMx:
         _check(self.lib, self.lib.aimx_get_stats(self.ctx, C.byref(s)), self.ctx)
         return {"num_unknowns": s.num_unknowns, "nnz": s.nnz, "occupied_nodes": s.occupied_nodes,
                 "occupied_lines": s.occupied_lines, "occupied_planes": s.occupied_planes,
-                "projection_entries": s.projection_entries, "device_bytes": s.device_bytes, "setup_seconds": s.setup_seconds,
+                "projection_entries": s.projection_entries, "device_bytes": s.device_bytes,
+                "batch_slots": s.batch_slots, "setup_seconds": s.setup_seconds,
                 "n": tuple(s.n), "order": s.order, "h": s.h, "origin": tuple(s.origin)}
 
     STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
@@ -279,4 +281,4 @@ class AIMx:
         nx, ny, nz = st["n"]
         out = np.empty((ny + 1) * (nx + 1) * (nz + 1) * 2)
         _check(self.lib, self.lib.aimx_get_spectrum(self.ctx, int(which), _P(out.ctypes.data)), self.ctx)
-        return out.view(np.complex128).reshape(ny + 1, nx + 1, nz + 1)
+        return out.view(np.complex128).reshape(ny + 1, nz + 1, nx + 1)

@@ -53,6 +53,7 @@ void build_topology(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, Topo
 struct NodeMap {
   std::vector<int32_t> node_lin;   // [nocc] linear grid index, ascending
   std::vector<int32_t> node_ptr;   // [nocc+1]
+  std::vector<int32_t> node_line;  // [nocc] index into line_id
   std::vector<int32_t> ent_rwg;    // [nent]
   std::vector<int32_t> ent_slot;   // [nent] stencil slot s
   std::vector<int32_t> line_id;    // [nlines] y + Ny z, ascending
@@ -94,64 +95,34 @@ void launch_weights(const Topology& t, SetupDev& d, cudaStream_t s, uint8_t* nzf
 void launch_static_near(const Topology& t, SetupDev& d, cudaStream_t s);
 void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 
+// ---------------------------------------------------------------- batching
+constexpr int kMaxBatch = 16;
+
 // ---------------------------------------------------------------- spectrum
+// Octant layout (all spectra): index ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.
 struct SpectrumPlan {
-  int Nx, Ny, Nz;
-  int64_t noct;               // (Nx+1)(Ny+1)(Nz+1)
-  double h;
-  double* cosx = nullptr;     // DCT-I matrices [(N+1)][(N+1)] per axis (fp64)
-  double* cosy = nullptr;
-  double* cosz = nullptr;
-  float* cosx_f = nullptr;    // fp32 copies for the c64 per-frequency path
-  float* cosy_f = nullptr;
-  float* cosz_f = nullptr;
-  void* work0 = nullptr;      // octant work buffers (complex, compute precision)
+  int Nx = 0, Ny = 0, Nz = 0;
+  int64_t noct = 0;           // (Nx+1)(Ny+1)(Nz+1)
+  double h = 0;
+  int batch = 0;              // work buffers hold `batch` octants
+  void* tw64[3] = {nullptr, nullptr, nullptr};   // fp64 twiddles, L = 2N per axis
+  void* tw32[3] = {nullptr, nullptr, nullptr};   // fp32 twiddles
+  void* work0 = nullptr;      // [batch][noct] complex (double2-sized)
   void* work1 = nullptr;
 };
 
-void spectrum_plan_init(SpectrumPlan& sp, cudaStream_t s);
+void spectrum_plan_init(SpectrumPlan& sp, int batch, cudaStream_t s);
 void spectrum_plan_free(SpectrumPlan& sp);
 // H_hat octant (unnormalised) of the static kernel, fp64.
 void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s);
-// Per-frequency: out = scale * (Hs + DCT3(K_d(k0))) in precision T.
-void spectrum_dynamic_f32(SpectrumPlan& sp, double k0, const float2* Hs, float scale, float2* out,
-                          cudaStream_t s);
-void spectrum_dynamic_f64(SpectrumPlan& sp, double k0, const double2* Hs, double scale,
-                          double2* out, cudaStream_t s);
+// Per-frequency, B frequencies: out[b] = scale * (Hs + DFT3(K_d(k0[b]))) in the
+// compute precision (out stride noct).
+void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
+                          float2* out, cudaStream_t s);
+void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs,
+                          double scale, double2* out, cudaStream_t s);
 
-// ---------------------------------------------------------------- hot path
-struct HotDev {
-  // grid geometry
-  int Nx, Ny, Nz, p, p3;
-  int nb, nocc, nlines, nzocc;
-  int64_t nnz;
-  // stencil / weights
-  int32_t* rwg_base = nullptr;   // [nb] linear index of the stencil anchor node
-  void* lam = nullptr;           // [nb][p3] real4 (x,y,z,rho), compute precision
-  int32_t* node_lin = nullptr;
-  int32_t* node_ptr = nullptr;
-  int32_t* ent_rwg = nullptr;
-  void* ent_w = nullptr;         // [nent] real4
-  int32_t* line_id = nullptr;
-  int32_t* line_ptr = nullptr;
-  int32_t* zplanes = nullptr;
-  uint8_t* line_occ = nullptr;
-  // near matrix (CSR, int32 offsets)
-  int32_t* rowptr = nullptr;
-  int32_t* col = nullptr;
-  void* cval = nullptr;          // [nnz] real2 (C_A, C_rho)
-  // grid buffers (complex, 4 channels innermost)
-  void* bufA = nullptr;          // [Nz][Ny][2Nx][4]
-  void* bufB = nullptr;          // [Nz][2Ny][2Nx][4]
-  void* bufC = nullptr;          // [Nz][Ny][2Nx][4]
-  void* phi = nullptr;           // [Nz][Ny][Nx][4]
-  // twiddles exp(-2 pi i m / L) for L = 2Nx, 2Ny, 2Nz (compute precision)
-  void* twx = nullptr;
-  void* twy = nullptr;
-  void* twz = nullptr;
-  void* Hoct = nullptr;          // bound spectrum octant / M (compute precision)
-};
-
+// ---------------------------------------------------------------- profiler
 // Per-stage CUDA-event timer (aimx_profile_*).
 struct Profiler {
   bool on = false;
@@ -180,18 +151,58 @@ struct StageScope {
   }
 };
 
+// ---------------------------------------------------------------- hot path
+struct HotDev {
+  // grid geometry
+  int Nx = 0, Ny = 0, Nz = 0, p = 0, p3 = 0;
+  int nb = 0, nocc = 0, nlines = 0, nzocc = 0;
+  int G = 8;                     // lanes per node in the projection gather
+  int twy = 4, twz = 4;          // tile widths (complex elements) of the y / z passes
+  int64_t nnz = 0;
+  int batch = 0;                 // batch slots allocated
+  // per-batch-slot strides (complex elements)
+  int64_t sS = 0, sA = 0, sB = 0, sP = 0, sH = 0;
+  // stencil / weights
+  int32_t* rwg_base = nullptr;   // [nb] linear index of the stencil anchor node
+  void* lam = nullptr;           // [nb][p3] real4 (x,y,z,rho), compute precision
+  int32_t* node_lin = nullptr;   // [nocc]
+  int32_t* node_line = nullptr;  // [nocc] index of the node's line in line_id
+  int32_t* node_ptr = nullptr;   // [nocc+1]
+  int32_t* ent_rwg = nullptr;    // [nent]
+  void* ent_w = nullptr;         // [nent] real4
+  int32_t* line_id = nullptr;    // [nlines] y + Ny z
+  int32_t* zplanes = nullptr;    // [nzocc]
+  uint8_t* line_occ = nullptr;   // [Ny*Nz]
+  // near matrix (CSR, int32 offsets)
+  int32_t* rowptr = nullptr;
+  int32_t* col = nullptr;
+  void* cval = nullptr;          // [nnz] real2 (C_A, C_rho)
+  // grid buffers (complex, 4 channels innermost), `batch` slots each
+  void* S = nullptr;             // [nlines][Nx][4] gathered grid sources
+  void* bufA = nullptr;          // [Nz][Ny][2Nx][4]
+  void* bufB = nullptr;          // [Nz][2Ny][2Nx][4]
+  void* bufC = nullptr;          // [Nz][Ny][2Nx][4]
+  void* phi = nullptr;           // [Nz][Ny][Nx][4]
+  void* twx = nullptr;           // exp(-2 pi i m / L), L = 2Nx, 2Ny, 2Nz (compute precision)
+  void* twy_tab = nullptr;
+  void* twz_tab = nullptr;
+  void* Hoct = nullptr;          // [batch][noct] bound spectra / M (compute precision)
+};
+
+// Per-launch batch arguments (by value).
 struct Combine {
-  // y = alpha (yA - beta yR), alpha = -j w mu0 (purely imaginary), beta = k0^-2;
-  // mode 0: combined into y0; mode 1: parts y0 = yA, y1 = -yR.
-  double alpha_im;
-  double beta;
-  int mode;
+  int B = 1;                     // frequency points in this launch (<= batch slots)
+  int mode = 0;                  // 0: y = alpha (yA - beta yR); 1: parts y0 = yA, y1 = -yR
+  int64_t xstride = 0, ystride = 0;   // complex elements between batch vectors
+  double alpha_im[kMaxBatch];    // alpha = j * alpha_im = -j w mu0
+  double beta[kMaxBatch];        // k0^-2
 };
 
 bool fft_length_supported(int L);
-void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s,
-                    Profiler* prof);
-void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, Combine c, cudaStream_t s,
-                    Profiler* prof);
+int pick_tile(int L, int rowwidth, bool f32);
+void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
+                    cudaStream_t s, Profiler* prof);
+void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
+                    cudaStream_t s, Profiler* prof);
 
 }  // namespace aimx

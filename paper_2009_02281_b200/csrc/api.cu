@@ -1,7 +1,9 @@
 // C ABI of the AIMx B200 library (include/aimx.h): context lifecycle, setup
 // orchestration (host topology -> device fp64 static fill -> hot-path data),
 // frequency binding, matvec / sweep entry points and introspection.
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -176,10 +178,10 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   h.rwg_base = dupload(c, base);
   h.node_lin = dupload(c, m.node_lin);
   h.node_ptr = dupload(c, m.node_ptr);
+  h.node_line = dupload(c, m.node_line);
   h.ent_rwg = dupload(c, m.ent_rwg);
   int32_t* ent_slot = dupload(c, m.ent_slot);
   h.line_id = dupload(c, m.line_id);
-  h.line_ptr = dupload(c, m.line_ptr);
   h.zplanes = dupload(c, m.zplanes);
   h.line_occ = dupload(c, m.line_occ);
   std::vector<int32_t> rp32(nb + 1);
@@ -208,24 +210,41 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     k_pack_c<double2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, d.CA, d.CR, (double2*)h.cval);
   }
   AIMX_CHECK_LAUNCH();
+  // ---- batch slots and grid buffers
+  const int64_t nS = (int64_t)h.nlines * h.Nx * 4;
   const int64_t nA = (int64_t)h.Nz * h.Ny * 2 * h.Nx * 4;
   const int64_t nB = (int64_t)h.Nz * 2 * h.Ny * 2 * h.Nx * 4;
   const int64_t nP = ng * 4;
-  h.bufA = dalloc<char>(c, nA * (int64_t)cs);
-  h.bufB = dalloc<char>(c, nB * (int64_t)cs);
-  h.bufC = dalloc<char>(c, nA * (int64_t)cs);
-  h.phi = dalloc<char>(c, nP * (int64_t)cs);
-  AIMX_CUDA(cudaMemsetAsync(h.bufA, 0, nA * cs, c->stream));
-  AIMX_CUDA(cudaMemsetAsync(h.bufB, 0, nB * cs, c->stream));
-  AIMX_CUDA(cudaMemsetAsync(h.bufC, 0, nA * cs, c->stream));
-  AIMX_CUDA(cudaMemsetAsync(h.phi, 0, nP * cs, c->stream));
+  const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
+  const int64_t per_freq = (int64_t)cs * (nS + 2 * nA + nB + nP + noct) + 2 * (int64_t)sizeof(double2) * noct;
+  int slots = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)(1536ll << 20) / per_freq));
+  if (const char* e = std::getenv("AIMX_BATCH")) slots = std::max(1, std::min(kMaxBatch, std::atoi(e)));
+  h.batch = slots;
+  h.sS = nS; h.sA = nA; h.sB = nB; h.sP = nP; h.sH = noct;
+  h.S = dalloc<char>(c, nS * slots * (int64_t)cs);
+  h.bufA = dalloc<char>(c, nA * slots * (int64_t)cs);
+  h.bufB = dalloc<char>(c, nB * slots * (int64_t)cs);
+  h.bufC = dalloc<char>(c, nA * slots * (int64_t)cs);
+  h.phi = dalloc<char>(c, nP * slots * (int64_t)cs);
+  AIMX_CUDA(cudaMemsetAsync(h.S, 0, nS * slots * cs, c->stream));
+  AIMX_CUDA(cudaMemsetAsync(h.bufA, 0, nA * slots * cs, c->stream));
+  AIMX_CUDA(cudaMemsetAsync(h.bufB, 0, nB * slots * cs, c->stream));
+  AIMX_CUDA(cudaMemsetAsync(h.bufC, 0, nA * slots * cs, c->stream));
+  AIMX_CUDA(cudaMemsetAsync(h.phi, 0, nP * slots * cs, c->stream));
   h.twx = make_twiddles(c, 2 * h.Nx);
-  h.twy = make_twiddles(c, 2 * h.Ny);
-  h.twz = make_twiddles(c, 2 * h.Nz);
+  h.twy_tab = make_twiddles(c, 2 * h.Ny);
+  h.twz_tab = make_twiddles(c, 2 * h.Nz);
+  h.twy = pick_tile(2 * h.Ny, 8 * h.Nx, f32);
+  h.twz = pick_tile(2 * h.Nz, 8 * h.Nx, f32);
+  {
+    const double avg = h.nocc > 0 ? (double)nent / h.nocc : 1.0;
+    int G = 4;
+    while (G < 32 && G < avg) G *= 2;
+    h.G = G;
+  }
   // ---- static spectrum
   c->sp.Nx = h.Nx; c->sp.Ny = h.Ny; c->sp.Nz = h.Nz; c->sp.h = t.h;
-  spectrum_plan_init(c->sp, c->stream);
-  const int64_t noct = c->sp.noct;
+  spectrum_plan_init(c->sp, slots, c->stream);
   c->Hs = dalloc<double2>(c, noct);
   spectrum_static(c->sp, c->Hs, c->stream);
   if (f32) {
@@ -235,7 +254,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   } else {
     c->Hs_T = c->Hs;
   }
-  h.Hoct = dalloc<char>(c, noct * (int64_t)cs);
+  h.Hoct = dalloc<char>(c, noct * slots * (int64_t)cs);
   dfree(c, d.LA_un, nnz * sizeof(double));
   dfree(c, d.YR_un, nnz * sizeof(double));
   AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_spec, cudaEventDisableTiming));
@@ -243,29 +262,56 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
 }
 
-void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
-  if (!(f > 0.0) || !std::isfinite(f)) throw Error(AIMX_E_INVALID_ARG, "frequency must be finite and > 0");
-  const double k0 = 2.0 * kPi * f / kC0;
+// S1 for B frequency points into spectrum slots 0..B-1.
+void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s) {
+  double k0[kMaxBatch];
+  for (int b = 0; b < B; ++b) {
+    if (!(f[b] > 0.0) || !std::isfinite(f[b])) throw Error(AIMX_E_INVALID_ARG, "frequency must be finite and > 0");
+    k0[b] = 2.0 * kPi * f[b] / kC0;
+  }
   const HotDev& h = c->hot;
   const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
   StageScope sc(&c->prof, 0, s);
   if (c->prec == AIMX_C64)
-    spectrum_dynamic_f32(c->sp, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)h.Hoct, s);
+    spectrum_dynamic_f32(c->sp, B, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)h.Hoct, s);
   else
-    spectrum_dynamic_f64(c->sp, k0, c->Hs, 1.0 / M, (double2*)h.Hoct, s);
+    spectrum_dynamic_f64(c->sp, B, k0, c->Hs, 1.0 / M, (double2*)h.Hoct, s);
+}
+
+void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
+  spectra(c, 1, &f, s);
   c->f = f;
-  c->k0 = k0;
+  c->k0 = 2.0 * kPi * f / kC0;
   c->omega = 2.0 * kPi * f;
   c->freq_set = true;
 }
 
-void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaStream_t s) {
+Combine make_combine(int B, const double* f, int mode, int64_t nb) {
   Combine cb;
-  cb.alpha_im = -c->omega * kMu0;
-  cb.beta = 1.0 / (c->k0 * c->k0);
+  cb.B = B;
   cb.mode = mode;
+  cb.xstride = nb;
+  cb.ystride = nb;
+  for (int b = 0; b < B; ++b) {
+    const double k0 = 2.0 * kPi * f[b] / kC0;
+    cb.alpha_im[b] = -2.0 * kPi * f[b] * kMu0;
+    cb.beta[b] = 1.0 / (k0 * k0);
+  }
+  return cb;
+}
+
+void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaStream_t s) {
+  Combine cb = make_combine(1, &c->f, mode, c->hot.nb);
   if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, s, &c->prof);
   else hot_matvec_f64(c->hot, x, y0, y1, cb, s, &c->prof);
+}
+
+// B frequency points: spectra into slots, then one batched matvec.
+void run_batch(aimx_ctx* c, int B, const double* f, const void* X, void* Y, cudaStream_t s) {
+  spectra(c, B, f, s);
+  Combine cb = make_combine(B, f, 0, c->hot.nb);
+  if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, X, Y, nullptr, cb, s, &c->prof);
+  else hot_matvec_f64(c->hot, X, Y, nullptr, cb, s, &c->prof);
 }
 
 aimx_status fail(aimx_ctx* c, const Error& e) {
@@ -379,20 +425,24 @@ aimx_status aimx_matvec_parts(aimx_ctx* c, const void* x, void* yA, void* yPhi, 
   return matvec_common(c, x, yA, yPhi, 1, stream);
 }
 
-static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, char* Y,
+static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, char* Y, int B,
                        cudaStream_t s) {
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
-  for (int64_t i = 0; i < nf; ++i) {
-    bind_frequency(c, f[i], s);
-    run_matvec(c, X + i * vb, Y + i * vb, nullptr, 0, s);
+  for (int64_t i = 0; i < nf; i += B) {
+    const int nb_ = (int)std::min<int64_t>(B, nf - i);
+    run_batch(c, nb_, f + i, X + i * vb, Y + i * vb, s);
   }
+}
+
+static int sweep_batch(const aimx_ctx* c, int32_t batch) {
+  int B = batch > 0 ? batch : c->hot.batch;
+  return std::max(1, std::min(B, c->hot.batch));
 }
 
 aimx_status aimx_sweep(aimx_ctx* c, int64_t nf, const double* f_hz, const void* X, void* Y,
                        int32_t batch, void* stream) {
   if (!c) return AIMX_E_INVALID_ARG;
   AIMX_API_BEGIN
-  (void)batch;
   if (nf < 0 || (nf > 0 && (!f_hz || !X || !Y))) throw Error(AIMX_E_INVALID_ARG, "bad sweep arguments");
   for (int64_t i = 0; i < nf; ++i)
     if (!(f_hz[i] > 0.0) || !std::isfinite(f_hz[i])) throw Error(AIMX_E_INVALID_ARG, "bad frequency");
@@ -405,7 +455,7 @@ aimx_status aimx_sweep(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
   }
-  sweep_impl(c, nf, f_hz, (const char*)X, (char*)Y, s);
+  sweep_impl(c, nf, f_hz, (const char*)X, (char*)Y, sweep_batch(c, batch), s);
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
   AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
@@ -424,7 +474,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  const int64_t B = batch > 0 ? batch : 16;
+  const int64_t B = sweep_batch(c, batch);
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   const int64_t need = 2 * B * (int64_t)vb;
   if (c->stage_bytes < need) {
@@ -444,7 +494,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   for (int64_t i0 = 0; i0 < nf; i0 += B) {
     const int64_t nb_ = std::min(B, nf - i0);
     AIMX_CUDA(cudaMemcpyAsync(dX, (const char*)X + i0 * vb, nb_ * vb, cudaMemcpyHostToDevice, s));
-    sweep_impl(c, nb_, f_hz + i0, dX, dY, s);
+    sweep_impl(c, nb_, f_hz + i0, dX, dY, (int)B, s);
     AIMX_CUDA(cudaMemcpyAsync((char*)Y + i0 * vb, dY, nb_ * vb, cudaMemcpyDeviceToHost, s));
   }
   if (had) bind_frequency(c, f0, s);
@@ -466,6 +516,7 @@ aimx_status aimx_get_stats(const aimx_ctx* c, aimx_stats* o) {
   o->occupied_planes = (int64_t)c->nodes.zplanes.size();
   o->projection_entries = (int64_t)c->nodes.ent_rwg.size();
   o->device_bytes = c->dev_bytes;
+  o->batch_slots = c->hot.batch;
   o->setup_seconds = c->setup_seconds;
   for (int a = 0; a < 3; ++a) { o->n[a] = c->topo.n[a]; o->origin[a] = c->topo.origin[a]; }
   o->order = c->topo.order;

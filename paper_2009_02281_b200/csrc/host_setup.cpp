@@ -248,6 +248,7 @@ void build_nodemap(const Topology& t, const std::vector<uint8_t>& nz_slot, NodeM
   }
   m.node_lin.clear();
   m.node_ptr.clear();
+  m.node_line.clear();
   m.line_id.clear();
   m.line_ptr.clear();
   m.zplanes.clear();
@@ -264,6 +265,7 @@ void build_nodemap(const Topology& t, const std::vector<uint8_t>& nz_slot, NodeM
       if (m.zplanes.empty() || m.zplanes.back() != z) m.zplanes.push_back(z);
     }
     m.node_lin.push_back((int32_t)q);
+    m.node_line.push_back((int32_t)m.line_id.size() - 1);
     m.node_ptr.push_back(cnt[q + 1]);
   }
   m.line_ptr.push_back((int32_t)m.node_lin.size());

@@ -44,7 +44,7 @@ def test_cfg1_static_spectrum(gpu1, orc1):
     Hs = op.spectrum(0)
     Nx, Ny, Nz = orc1.grid.n
     ref = orc1.Hs_hat[: Nz + 1, : Ny + 1, : Nx + 1]          # [kz, ky, kx]
-    ref = np.transpose(ref, (1, 2, 0))                      # -> [ky, kx, kz]
+    ref = np.transpose(ref, (1, 0, 2))                      # -> [ky, kz, kx]
     assert rel_l2(Hs, ref) <= 1e-13
 
 
@@ -56,7 +56,7 @@ def test_cfg1_matvec_parts_and_combined(gpu1, orc1, fi):
     orc1.set_frequency(f)
     Hd = op.spectrum(1)
     Nx, Ny, Nz = orc1.grid.n
-    ref = np.transpose(orc1.H_hat[: Nz + 1, : Ny + 1, : Nx + 1], (1, 2, 0))
+    ref = np.transpose(orc1.H_hat[: Nz + 1, : Ny + 1, : Nx + 1], (1, 0, 2))
     assert rel_l2(Hd, ref) <= (1e-13 if prec == "c128" else 1e-6)
     for i in range(3):
         x = inp.rhs_vector(1, i, op.N)
@@ -176,3 +176,15 @@ def test_other_stencil_orders(order):
     oA, oR = orc.parts(x)
     assert rel_l2(yA.cpu().numpy(), oA) <= 1e-11
     assert rel_l2(yP.cpu().numpy(), -oR) <= 1e-11
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_sweep_results_independent_of_batch_size(prec):
+    import torch
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), prec)
+    assert op.stats()["batch_slots"] >= 4
+    freqs = np.linspace(20e6, 400e6, 11)
+    X = to_gpu(np.stack([inp.rhs_vector(1, i, op.N) for i in range(11)]), prec)
+    ref = op.sweep(freqs, X, batch=1).clone()
+    for b in (2, 3, 4, 16):
+        assert torch.equal(op.sweep(freqs, X, batch=b), ref)
