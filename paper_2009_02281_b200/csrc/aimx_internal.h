@@ -187,6 +187,7 @@ struct HotDev {
   void* twy_tab = nullptr;
   void* twz_tab = nullptr;
   void* Hoct = nullptr;          // [batch][noct] bound spectra / M (compute precision)
+  void* xt = nullptr;            // [nb][16] batch-interleaved right-hand sides (near SpMM)
 };
 
 // Per-launch batch arguments (by value).

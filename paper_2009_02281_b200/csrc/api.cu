@@ -255,6 +255,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     c->Hs_T = c->Hs;
   }
   h.Hoct = dalloc<char>(c, noct * slots * (int64_t)cs);
+  h.xt = dalloc<char>(c, (int64_t)nb * kMaxBatch * (int64_t)cs);
   dfree(c, d.LA_un, nnz * sizeof(double));
   dfree(c, d.YR_un, nnz * sizeof(double));
   AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_spec, cudaEventDisableTiming));

@@ -132,9 +132,25 @@ __device__ __forceinline__ void smem_fft(T2*& src, T2*& dst, int nlines, const T
   fft_stages<T2, L, INV, 1>(src, dst, nlines, tw, addr);
 }
 
+// Asynchronous global -> shared element copy (LDGSTS), many in flight per
+// thread without register staging; complete with cp_async_wait_all().
+template <typename T2>
+__device__ __forceinline__ void cp_async(T2* sdst, const T2* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  if constexpr (sizeof(T2) == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+  }
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <typename T2>
 __device__ __forceinline__ void load_tw(T2* s_tw, const T2* __restrict__ g_tw, int L) {
-  for (int i = threadIdx.x; i < L; i += blockDim.x) s_tw[i] = g_tw[i];
+  for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async(s_tw + i, g_tw + i);
 }
 
 #define AIMX_SWITCH_L(Lv, CALL)                                        \

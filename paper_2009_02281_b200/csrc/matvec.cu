@@ -89,10 +89,15 @@ __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
   const int Nx = h.Nx;
   load_tw(tw, (const T2*)h.twx, L);
   const T2* __restrict__ in = (const T2*)h.S + b * h.sS + (int64_t)l0 * Nx * 4;
-  for (int i = threadIdx.x; i < nrows * L * 4; i += blockDim.x) {
-    const int r = i / (L * 4), e = i - r * (L * 4);
-    b0[r * RS + e] = (e < Nx * 4) ? in[(int64_t)r * Nx * 4 + e] : mk<T2>(0, 0);
+  for (int i = threadIdx.x; i < nrows * Nx * 4; i += blockDim.x) {
+    const int r = i / (Nx * 4), e = i - r * (Nx * 4);
+    cp_async(b0 + r * RS + e, in + i);
   }
+  for (int i = threadIdx.x; i < nrows * (L - Nx) * 4; i += blockDim.x) {
+    const int r = i / ((L - Nx) * 4), e = Nx * 4 + i - r * ((L - Nx) * 4);
+    b0[r * RS + e] = mk<T2>(0, 0);
+  }
+  cp_async_wait_all();
   __syncthreads();
   T2* src = b0;
   T2* dst = b1;
@@ -120,10 +125,12 @@ __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
   const int Ny = h.Ny;
   load_tw(tw, (const T2*)h.twy_tab, L);
   const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + (int64_t)z * Ny * W + x0;
-  for (int i = threadIdx.x; i < L * TW; i += blockDim.x) {
+  for (int i = threadIdx.x; i < Ny * TW; i += blockDim.x) {
     const int y = i / TW, w = i - y * TW;
-    b0[i] = (y < Ny) ? in[(int64_t)y * W + w] : mk<T2>(0, 0);
+    cp_async(b0 + i, in + (int64_t)y * W + w);
   }
+  for (int i = Ny * TW + threadIdx.x; i < L * TW; i += blockDim.x) b0[i] = mk<T2>(0, 0);
+  cp_async_wait_all();
   __syncthreads();
   T2* src = b0;
   T2* dst = b1;
@@ -151,14 +158,18 @@ __global__ void __launch_bounds__(256) k_zconv(HotDev h) {
   const int Ny2 = 2 * h.Ny;
   const int64_t zs = (int64_t)Ny2 * W;   // z stride in bufB
   load_tw(tw, (const T2*)h.twz_tab, L);
-  for (int i = threadIdx.x; i < L * TW; i += blockDim.x) b0[i] = mk<T2>(0, 0);
+  if (h.nzocc < h.Nz)
+    for (int i = threadIdx.x; i < L * TW; i += blockDim.x) b0[i] = mk<T2>(0, 0);
+  else
+    for (int i = h.Nz * TW + threadIdx.x; i < L * TW; i += blockDim.x) b0[i] = mk<T2>(0, 0);
   __syncthreads();
   T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)ky * W + x0;
   for (int i = threadIdx.x; i < h.nzocc * TW; i += blockDim.x) {
     const int zi = i / TW, w = i - zi * TW;
     const int z = h.zplanes[zi];
-    b0[z * TW + w] = g[z * zs + w];
+    cp_async(b0 + z * TW + w, g + z * zs + w);
   }
+  cp_async_wait_all();
   __syncthreads();
   T2* src = b0;
   T2* dst = b1;
@@ -202,8 +213,9 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
   const T2* __restrict__ in = (const T2*)h.bufB + b * h.sB + (int64_t)z * L * W + x0;
   for (int i = threadIdx.x; i < L * TW; i += blockDim.x) {
     const int y = i / TW, w = i - y * TW;
-    b0[i] = in[(int64_t)y * W + w];
+    cp_async(b0 + i, in + (int64_t)y * W + w);
   }
+  cp_async_wait_all();
   __syncthreads();
   T2* src = b0;
   T2* dst = b1;
@@ -231,10 +243,11 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   const int nrows = min(ROWS, h.nlines - l0);
   load_tw(tw, (const T2*)h.twx, L);
   const T2* __restrict__ in = (const T2*)h.bufC + b * h.sA;
-  for (int r = 0; r < nrows; ++r) {
-    const int64_t base = (int64_t)h.line_id[l0 + r] * L * 4;
-    for (int i = threadIdx.x; i < L * 4; i += blockDim.x) b0[r * RS + i] = in[base + i];
+  for (int i = threadIdx.x; i < nrows * L * 4; i += blockDim.x) {
+    const int r = i / (L * 4), e = i - r * (L * 4);
+    cp_async(b0 + r * RS + e, in + (int64_t)h.line_id[l0 + r] * L * 4 + e);
   }
+  cp_async_wait_all();
   __syncthreads();
   T2* src = b0;
   T2* dst = b1;
@@ -292,16 +305,18 @@ __global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT
   }
   const T2* __restrict__ cv = (const T2*)h.cval;
   const int kb = h.rowptr[m], ke = h.rowptr[m + 1];
+  // x for the near rows: batch-interleaved xt[n * BB + b] (BB > 1) or x itself
   for (int kk = kb + lane; kk < ke; kk += 32) {
     const int n = h.col[kk];
     const T2 c = cv[kk];
+    const T2* __restrict__ xr = x + (int64_t)n * BB;
+    T2 xv[BB];
+#pragma unroll
+    for (int b = 0; b < BB; ++b) xv[b] = xr[b];
 #pragma unroll
     for (int b = 0; b < BB; ++b) {
-      if (b < B) {
-        const T2 xv = x[b * cb.xstride + n];
-        aA[b].x += c.x * xv.x; aA[b].y += c.x * xv.y;
-        aR[b].x += c.y * xv.x; aR[b].y += c.y * xv.y;
-      }
+      aA[b].x += c.x * xv[b].x; aA[b].y += c.x * xv[b].y;
+      aR[b].x += c.y * xv[b].x; aR[b].y += c.y * xv[b].y;
     }
   }
   using R = decltype(T2::x);
@@ -385,11 +400,30 @@ void run_z(const HotDev& h, int B, cudaStream_t s) {
   AIMX_CHECK_LAUNCH();
 }
 
+// xt[n * BB + b] = x[b * xstride + n] (zero for b >= B)
+template <typename T>
+__global__ void k_interleave(int nb, int B, int BB, const typename CT<T>::T2* __restrict__ x,
+                             int64_t xstride, typename CT<T>::T2* __restrict__ xt) {
+  using T2 = typename CT<T>::T2;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * BB) return;
+  const int n = (int)(i / BB), b = (int)(i - (int64_t)n * BB);
+  xt[i] = b < B ? x[b * xstride + n] : mk<T2>(0, 0);
+}
+
 template <typename T>
 void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   const unsigned g = (unsigned)(((int64_t)h.nb * 32 + 255) / 256);
   const T2* xx = (const T2*)x;
+  if (c.B > 1) {
+    const int BB = c.B <= 2 ? 2 : (c.B <= 4 ? 4 : (c.B <= 8 ? 8 : 16));
+    const int64_t n = (int64_t)h.nb * BB;
+    k_interleave<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.nb, c.B, BB, xx, c.xstride,
+                                                                (T2*)h.xt);
+    AIMX_CHECK_LAUNCH();
+    xx = (const T2*)h.xt;
+  }
   if (c.B <= 1) k_interp_near<T, 1><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);
   else if (c.B <= 2) k_interp_near<T, 2><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);
   else if (c.B <= 4) k_interp_near<T, 4><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);

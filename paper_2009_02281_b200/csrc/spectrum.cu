@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(256) k_even_rows(int64_t nlines, int64_t noct,
   const T2* __restrict__ src = in + boff + l0 * N1;
   for (int t = threadIdx.x; t < nl * N1; t += blockDim.x) {
     const int r = t / N1, i = t - r * N1;
-    b0[r * RS + i] = src[t];
+    cp_async(b0 + r * RS + i, src + t);
   }
+  cp_async_wait_all();
   __syncthreads();
   for (int t = threadIdx.x; t < nl * (L - N1); t += blockDim.x) {
     const int r = t / (L - N1), i = N1 + (t - r * (L - N1));
@@ -123,8 +124,10 @@ __global__ void __launch_bounds__(256) k_even_cols(int64_t inner, int TW, int64_
   const int64_t base = boff + o * N1 * inner + u0;
   for (int t = threadIdx.x; t < N1 * TW; t += blockDim.x) {
     const int i = t / TW, w = t - i * TW;
-    b0[t] = (w < nu) ? in[base + (int64_t)i * inner + w] : mk<T2>(0, 0);
+    if (w < nu) cp_async(b0 + t, in + base + (int64_t)i * inner + w);
+    else b0[t] = mk<T2>(0, 0);
   }
+  cp_async_wait_all();
   __syncthreads();
   for (int t = threadIdx.x; t < (L - N1) * TW; t += blockDim.x) {
     const int i = N1 + t / TW, w = t % TW;
