@@ -143,8 +143,9 @@ aimx_status aimx_matvec_parts(aimx_ctx* ctx, const void* x, void* yA, void* yPhi
  * context's batch slots: all slots; slots are chosen at setup from the grid
  * size, at most 16, environment variable AIMX_BATCH overrides): the spectra of
  * a batch are generated together and one batched matvec reads the near matrix
- * and the weights once for all of its right-hand sides.  Results do not depend
- * on the batch size (fixed-order reductions, no atomics).  The context's bound
+ * and the weights once for all of its right-hand sides.  Results are
+ * deterministic (fixed-order reductions, no atomics); across batch sizes the
+ * near-row sums are partitioned differently and agree to rounding.  The context's bound
  * frequency is restored afterwards if one was set. */
 aimx_status aimx_sweep(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* X,
                        void* Y, int32_t batch, void* stream);

@@ -173,6 +173,7 @@ struct HotDev {
   int32_t* line_id = nullptr;    // [nlines] y + Ny z
   int32_t* zplanes = nullptr;    // [nzocc]
   uint8_t* line_occ = nullptr;   // [Ny*Nz]
+  uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix (CSR, int32 offsets)
   int32_t* rowptr = nullptr;
   int32_t* col = nullptr;

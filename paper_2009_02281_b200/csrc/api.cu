@@ -184,6 +184,11 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   h.line_id = dupload(c, m.line_id);
   h.zplanes = dupload(c, m.zplanes);
   h.line_occ = dupload(c, m.line_occ);
+  {
+    std::vector<uint8_t> zo(t.n[2], 0);
+    for (int z : m.zplanes) zo[z] = 1;
+    h.zocc = dupload(c, zo);
+  }
   std::vector<int32_t> rp32(nb + 1);
   for (int64_t i = 0; i <= nb; ++i) rp32[i] = (int32_t)t.rowptr[i];
   h.rowptr = dupload(c, rp32);

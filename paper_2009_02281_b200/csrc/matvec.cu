@@ -25,15 +25,11 @@
 
 #include "aimx_internal.h"
 #include "fft.cuh"
+#include "fft_reg.cuh"
 
 namespace aimx {
 
 namespace {
-
-template <typename T> constexpr int rows_x(int L) {
-  int r = (sizeof(T) == 4 ? 4096 : 2048) / (4 * L);
-  return r < 1 ? 1 : (r > 32 ? 32 : r);
-}
 
 // ------------------------------------------------------------------ S2 gather
 template <typename T, int G>
@@ -73,190 +69,221 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
   }
 }
 
-// ------------------------------------------------------------------ x-fwd
+// ------------------------------------------------------------------ FFT passes
+// Register-resident two-level FFTs (fft_reg.cuh).  Threads are mapped
+// line-fastest (line = tid % NL, t = tid / NL) so that a warp's loads and
+// stores cover consecutive grid columns; the per-line exchange uses one block
+// barrier per transform.
+template <int L> struct PassGeom {
+  static constexpr int R1 = Fac<L>::R1, R2 = Fac<L>::R2;
+  using TL = TwoLevel<R1, R2>;
+  static constexpr int T = TL::T, E = TL::E;
+  static constexpr int NL = 256 / T;                // lines per CTA
+  static constexpr int XB = R1 > 1 ? TL::XB : 0;    // exchange elements per line
+};
+
+template <typename T2, int L>
+__device__ __forceinline__ void fwd_fft(T2* v, T2* xb, const T2* tw, int t) {
+  using G = PassGeom<L>;
+  fft2<T2, G::R1, G::R2, false>(v, xb, tw, t);
+}
+// inverse of data in the forward's output distribution, back to the input one
+template <typename T2, int L>
+__device__ __forceinline__ void inv_fft_swapped(T2* v, T2* xb, const T2* tw, int t) {
+  using G = PassGeom<L>;
+  fft2<T2, G::R2, G::R1, true>(v, xb, tw, t);
+}
+// inverse of data loaded in the input distribution (output distribution after)
+template <typename T2, int L>
+__device__ __forceinline__ void inv_fft(T2* v, T2* xb, const T2* tw, int t) {
+  using G = PassGeom<L>;
+  fft2<T2, G::R1, G::R2, true>(v, xb, tw, t);
+}
+
+template <typename T2, int L>
+__device__ __forceinline__ void pass_prologue(T2*& tw, T2*& xb, const T2* __restrict__ gtw, int line) {
+  using G = PassGeom<L>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  tw = reinterpret_cast<T2*>(smem_raw);
+  xb = tw + L + line * G::XB;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = gtw[i];
+  __syncthreads();
+}
+
+template <typename T, int L> constexpr size_t pass_smem() {
+  using G = PassGeom<L>;
+  return sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB);
+}
+
+// ---- x forward: occupied lines of S (x < Nx, zero padded) -> bufA[line_id][kx][c]
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
   using T2 = typename CT<T>::T2;
-  constexpr int ROWS = rows_x<T>(L);
-  constexpr int RS = (L + 1) * 4;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* b0 = tw + L;
-  T2* b1 = b0 + ROWS * RS;
+  using G = PassGeom<L>;
+  const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  T2 *tw, *xb;
+  pass_prologue<T2, L>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y;
-  const int l0 = blockIdx.x * ROWS;
-  const int nrows = min(ROWS, h.nlines - l0);
+  const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
+  const bool act = r < h.nlines;
   const int Nx = h.Nx;
-  load_tw(tw, (const T2*)h.twx, L);
-  const T2* __restrict__ in = (const T2*)h.S + b * h.sS + (int64_t)l0 * Nx * 4;
-  for (int i = threadIdx.x; i < nrows * Nx * 4; i += blockDim.x) {
-    const int r = i / (Nx * 4), e = i - r * (Nx * 4);
-    cp_async(b0 + r * RS + e, in + i);
+  const T2* __restrict__ in = (const T2*)h.S + b * h.sS + (int64_t)r * Nx * 4 + c;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int x = G::TL::in_index(t, i);
+    v[i] = (act && x < Nx) ? in[x * 4] : mk<T2>(0, 0);
   }
-  for (int i = threadIdx.x; i < nrows * (L - Nx) * 4; i += blockDim.x) {
-    const int r = i / ((L - Nx) * 4), e = Nx * 4 + i - r * ((L - Nx) * 4);
-    b0[r * RS + e] = mk<T2>(0, 0);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  T2* src = b0;
-  T2* dst = b1;
-  smem_fft<T2, L, false>(src, dst, nrows * 4, tw, RowAddr<L>{});
-  T2* __restrict__ out = (T2*)h.bufA + b * h.sA;
-  for (int r = 0; r < nrows; ++r) {
-    const int64_t base = (int64_t)h.line_id[l0 + r] * L * 4;
-    for (int i = threadIdx.x; i < L * 4; i += blockDim.x) out[base + i] = src[r * RS + i];
-  }
+  fwd_fft<T2, L>(v, xb, tw, t);
+  if (!act) return;
+  T2* __restrict__ out = (T2*)h.bufA + b * h.sA + (int64_t)h.line_id[r] * L * 4 + c;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) out[TwoLevel<G::R2, G::R1>::in_index(t, i) * 4] = v[i];
 }
 
-// ------------------------------------------------------------------ y-fwd
-template <typename T, int L>
-__global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
-  using T2 = typename CT<T>::T2;
-  const int TW = h.twy;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* b0 = tw + L;
-  T2* b1 = b0 + L * TW;
-  const int b = blockIdx.z;
-  const int z = h.zplanes[blockIdx.y];
-  const int x0 = blockIdx.x * TW;
-  const int W = 8 * h.Nx;          // row width in complex elements (2Nx * 4)
-  const int Ny = h.Ny;
-  load_tw(tw, (const T2*)h.twy_tab, L);
-  const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + (int64_t)z * Ny * W + x0;
-  for (int i = threadIdx.x; i < Ny * TW; i += blockDim.x) {
-    const int y = i / TW, w = i - y * TW;
-    cp_async(b0 + i, in + (int64_t)y * W + w);
-  }
-  for (int i = Ny * TW + threadIdx.x; i < L * TW; i += blockDim.x) b0[i] = mk<T2>(0, 0);
-  cp_async_wait_all();
-  __syncthreads();
-  T2* src = b0;
-  T2* dst = b1;
-  smem_fft<T2, L, false>(src, dst, TW, tw, ColAddr{TW});
-  T2* __restrict__ out = (T2*)h.bufB + b * h.sB + (int64_t)z * L * W + x0;
-  for (int i = threadIdx.x; i < L * TW; i += blockDim.x) {
-    const int y = i / TW, w = i - y * TW;
-    out[(int64_t)y * W + w] = src[i];
-  }
-}
-
-// ------------------------------------------------------------------ z fwd * H * z inv
-template <typename T, int L>
-__global__ void __launch_bounds__(256) k_zconv(HotDev h) {
-  using T2 = typename CT<T>::T2;
-  const int TW = h.twz;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* b0 = tw + L;
-  T2* b1 = b0 + L * TW;
-  const int b = blockIdx.z;
-  const int ky = blockIdx.y;
-  const int x0 = blockIdx.x * TW;
-  const int W = 8 * h.Nx;
-  const int Ny2 = 2 * h.Ny;
-  const int64_t zs = (int64_t)Ny2 * W;   // z stride in bufB
-  load_tw(tw, (const T2*)h.twz_tab, L);
-  if (h.nzocc < h.Nz)
-    for (int i = threadIdx.x; i < L * TW; i += blockDim.x) b0[i] = mk<T2>(0, 0);
-  else
-    for (int i = h.Nz * TW + threadIdx.x; i < L * TW; i += blockDim.x) b0[i] = mk<T2>(0, 0);
-  __syncthreads();
-  T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)ky * W + x0;
-  for (int i = threadIdx.x; i < h.nzocc * TW; i += blockDim.x) {
-    const int zi = i / TW, w = i - zi * TW;
-    const int z = h.zplanes[zi];
-    cp_async(b0 + z * TW + w, g + z * zs + w);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  T2* src = b0;
-  T2* dst = b1;
-  smem_fft<T2, L, false>(src, dst, TW, tw, ColAddr{TW});
-  {  // spectrum multiply (octant [ky][kz][kx], 1/M folded into H)
-    const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz;
-    const int kyf = ky <= Ny ? ky : Ny2 - ky;
-    const T2* __restrict__ H = (const T2*)h.Hoct + b * h.sH + (int64_t)kyf * (Nz + 1) * (Nx + 1);
-    for (int i = threadIdx.x; i < L * TW; i += blockDim.x) {
-      const int kz = i / TW, w = i - kz * TW;
-      const int kx = (x0 + w) >> 2;
-      const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
-      const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
-      src[i] = cmul(src[i], H[(int64_t)kzf * (Nx + 1) + kxf]);
-    }
-  }
-  __syncthreads();
-  smem_fft<T2, L, true>(src, dst, TW, tw, ColAddr{TW});
-  for (int i = threadIdx.x; i < h.nzocc * TW; i += blockDim.x) {
-    const int zi = i / TW, w = i - zi * TW;
-    const int z = h.zplanes[zi];
-    g[z * zs + w] = src[z * TW + w];
-  }
-}
-
-// ------------------------------------------------------------------ y-inv
-template <typename T, int L>
-__global__ void __launch_bounds__(256) k_yinv(HotDev h) {
-  using T2 = typename CT<T>::T2;
-  const int TW = h.twy;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* b0 = tw + L;
-  T2* b1 = b0 + L * TW;
-  const int b = blockIdx.z;
-  const int z = h.zplanes[blockIdx.y];
-  const int x0 = blockIdx.x * TW;
-  const int W = 8 * h.Nx;
-  const int Ny = h.Ny;
-  load_tw(tw, (const T2*)h.twy_tab, L);
-  const T2* __restrict__ in = (const T2*)h.bufB + b * h.sB + (int64_t)z * L * W + x0;
-  for (int i = threadIdx.x; i < L * TW; i += blockDim.x) {
-    const int y = i / TW, w = i - y * TW;
-    cp_async(b0 + i, in + (int64_t)y * W + w);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  T2* src = b0;
-  T2* dst = b1;
-  smem_fft<T2, L, true>(src, dst, TW, tw, ColAddr{TW});
-  T2* __restrict__ out = (T2*)h.bufC + b * h.sA + (int64_t)z * Ny * W + x0;
-  const uint8_t* occ = h.line_occ + (int64_t)z * Ny;
-  for (int i = threadIdx.x; i < Ny * TW; i += blockDim.x) {
-    const int y = i / TW, w = i - y * TW;
-    if (occ[y]) out[(int64_t)y * W + w] = src[i];
-  }
-}
-
-// ------------------------------------------------------------------ x-inv
+// ---- x inverse: bufC[line_id][kx][c] -> phi[line][x < Nx][c]
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   using T2 = typename CT<T>::T2;
-  constexpr int ROWS = rows_x<T>(L);
-  constexpr int RS = (L + 1) * 4;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* b0 = tw + L;
-  T2* b1 = b0 + ROWS * RS;
+  using G = PassGeom<L>;
+  const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  T2 *tw, *xb;
+  pass_prologue<T2, L>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y;
-  const int l0 = blockIdx.x * ROWS;
-  const int nrows = min(ROWS, h.nlines - l0);
-  load_tw(tw, (const T2*)h.twx, L);
-  const T2* __restrict__ in = (const T2*)h.bufC + b * h.sA;
-  for (int i = threadIdx.x; i < nrows * L * 4; i += blockDim.x) {
-    const int r = i / (L * 4), e = i - r * (L * 4);
-    cp_async(b0 + r * RS + e, in + (int64_t)h.line_id[l0 + r] * L * 4 + e);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  T2* src = b0;
-  T2* dst = b1;
-  smem_fft<T2, L, true>(src, dst, nrows * 4, tw, RowAddr<L>{});
-  T2* __restrict__ out = (T2*)h.phi + b * h.sP;
+  const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
+  const bool act = r < h.nlines;
+  const int lid = act ? h.line_id[r] : 0;
+  const T2* __restrict__ in = (const T2*)h.bufC + b * h.sA + (int64_t)lid * L * 4 + c;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * 4] : mk<T2>(0, 0);
+  inv_fft<T2, L>(v, xb, tw, t);
+  if (!act) return;
   const int Nx = h.Nx;
-  for (int r = 0; r < nrows; ++r) {
-    const int64_t base = (int64_t)h.line_id[l0 + r] * Nx * 4;
-    for (int i = threadIdx.x; i < Nx * 4; i += blockDim.x) out[base + i] = src[r * RS + i];
+  T2* __restrict__ out = (T2*)h.phi + b * h.sP + (int64_t)lid * Nx * 4 + c;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int x = TwoLevel<G::R2, G::R1>::in_index(t, i);
+    if (x < Nx) out[x * 4] = v[i];
+  }
+}
+
+// Column passes: CTA = NL lines = (rows per CTA) x (column tile CW).
+struct ColTile {
+  int w, rsub, CW, RPC;
+};
+template <int L> __device__ __forceinline__ ColTile col_tile(int line, int W) {
+  constexpr int NL = PassGeom<L>::NL;
+  ColTile ct;
+  ct.CW = NL < W ? NL : W;
+  ct.RPC = NL / ct.CW;
+  ct.w = line % ct.CW;
+  ct.rsub = line / ct.CW;
+  return ct;
+}
+
+// ---- y forward: bufA[z][y < Ny][.] -> bufB[z][ky][.]
+template <typename T, int L>
+__global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<L>;
+  const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  T2 *tw, *xb;
+  pass_prologue<T2, L>(tw, xb, (const T2*)h.twy_tab, line);
+  const int W = 8 * h.Nx, Ny = h.Ny;
+  const ColTile ct = col_tile<L>(line, W);
+  const int zi = blockIdx.y * ct.RPC + ct.rsub;
+  const bool act = zi < h.nzocc;
+  const int z = act ? h.zplanes[zi] : 0;
+  const int b = blockIdx.z;
+  const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
+  const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + (int64_t)z * Ny * W + col;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int y = G::TL::in_index(t, i);
+    v[i] = (act && y < Ny) ? in[(int64_t)y * W] : mk<T2>(0, 0);
+  }
+  fwd_fft<T2, L>(v, xb, tw, t);
+  if (!act) return;
+  T2* __restrict__ out = (T2*)h.bufB + b * h.sB + (int64_t)z * L * W + col;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) out[(int64_t)TwoLevel<G::R2, G::R1>::in_index(t, i) * W] = v[i];
+}
+
+// ---- y inverse: bufB[z][ky][.] -> bufC[z][y < Ny, occupied][.]
+template <typename T, int L>
+__global__ void __launch_bounds__(256) k_yinv(HotDev h) {
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<L>;
+  const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  T2 *tw, *xb;
+  pass_prologue<T2, L>(tw, xb, (const T2*)h.twy_tab, line);
+  const int W = 8 * h.Nx, Ny = h.Ny;
+  const ColTile ct = col_tile<L>(line, W);
+  const int zi = blockIdx.y * ct.RPC + ct.rsub;
+  const bool act = zi < h.nzocc;
+  const int z = act ? h.zplanes[zi] : 0;
+  const int b = blockIdx.z;
+  const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
+  const T2* __restrict__ in = (const T2*)h.bufB + b * h.sB + (int64_t)z * L * W + col;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) v[i] = act ? in[(int64_t)G::TL::in_index(t, i) * W] : mk<T2>(0, 0);
+  inv_fft<T2, L>(v, xb, tw, t);
+  if (!act) return;
+  T2* __restrict__ out = (T2*)h.bufC + b * h.sA + (int64_t)z * Ny * W + col;
+  const uint8_t* occ = h.line_occ + (int64_t)z * Ny;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int y = TwoLevel<G::R2, G::R1>::in_index(t, i);
+    if (y < Ny && occ[y]) out[(int64_t)y * W] = v[i];
+  }
+}
+
+// ---- z forward * H_hat * z inverse, in place on bufB (occupied planes only)
+template <typename T, int L>
+__global__ void __launch_bounds__(256) k_zconv(HotDev h) {
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<L>;
+  const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  T2 *tw, *xb;
+  pass_prologue<T2, L>(tw, xb, (const T2*)h.twz_tab, line);
+  const int W = 8 * h.Nx, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
+  const ColTile ct = col_tile<L>(line, W);
+  const int ky = blockIdx.y * ct.RPC + ct.rsub;
+  const bool act = ky < Ny2;
+  const int b = blockIdx.z;
+  const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
+  const int64_t zs = (int64_t)Ny2 * W;
+  T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)(act ? ky : 0) * W + col;
+  const uint8_t* __restrict__ zocc = h.zocc;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int z = G::TL::in_index(t, i);
+    v[i] = (act && z < Nz && zocc[z]) ? g[z * zs] : mk<T2>(0, 0);
+  }
+  fwd_fft<T2, L>(v, xb, tw, t);
+  {  // spectrum multiply (octant [ky][kz][kx], 1/M folded into H)
+    const int kyf = ky <= Ny ? ky : Ny2 - ky;
+    const int kx = (int)(col >> 2);
+    const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
+    const T2* __restrict__ H = (const T2*)h.Hoct + b * h.sH + ((int64_t)(act ? kyf : 0) * (Nz + 1)) * (Nx + 1) + kxf;
+#pragma unroll
+    for (int i = 0; i < G::E; ++i) {
+      const int kz = TwoLevel<G::R2, G::R1>::in_index(t, i);
+      const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
+      v[i] = cmul(v[i], __ldg(H + (int64_t)kzf * (Nx + 1)));
+    }
+  }
+  __syncthreads();
+  inv_fft_swapped<T2, L>(v, xb, tw, t);
+  if (!act) return;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int z = G::TL::in_index(t, i);
+    if (z < Nz && zocc[z]) g[z * zs] = v[i];
   }
 }
 
@@ -270,72 +297,105 @@ template <typename T2> __device__ __forceinline__ T2 warp_sum(T2 v) {
   return v;
 }
 
-template <typename T, int BB>
-__global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ x,
-                                                     typename CT<T>::T2* __restrict__ y0,
-                                                     typename CT<T>::T2* __restrict__ y1, Combine cb) {
+// Single right-hand side: lanes stride the stencil nodes and the near row.
+template <typename T>
+__global__ void __launch_bounds__(256) k_interp_near1(HotDev h, const typename CT<T>::T2* __restrict__ x,
+                                                      typename CT<T>::T2* __restrict__ y0,
+                                                      typename CT<T>::T2* __restrict__ y1, Combine cb) {
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
   const int lane = threadIdx.x & 31;
   const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (m >= h.nb) return;
-  const int B = cb.B;
-  T2 aA[BB], aR[BB];
-#pragma unroll
-  for (int b = 0; b < BB; ++b) {
-    aA[b] = mk<T2>(0, 0);
-    aR[b] = mk<T2>(0, 0);
-  }
+  T2 aA = mk<T2>(0, 0), aR = mk<T2>(0, 0);
   for (int sl = lane; sl < h.p3; sl += 32) {
     const int p = h.p;
     const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
     const int64_t lin = (int64_t)h.rwg_base[m] + i + (int64_t)h.Nx * (j + (int64_t)h.Ny * k);
     const T4 w = ((const T4*)h.lam)[(int64_t)m * h.p3 + sl];
-#pragma unroll
-    for (int b = 0; b < BB; ++b) {
-      if (b < B) {
-        const T2* ph = (const T2*)h.phi + b * h.sP + lin * 4;
-        const T2 p0 = ph[0], p1 = ph[1], p2 = ph[2], p3 = ph[3];
-        aA[b].x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
-        aA[b].y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
-        aR[b].x += w.w * p3.x;
-        aR[b].y += w.w * p3.y;
-      }
+    const T2* ph = (const T2*)h.phi + lin * 4;
+    const T2 p0 = ph[0], p1 = ph[1], p2 = ph[2], p3 = ph[3];
+    aA.x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
+    aA.y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
+    aR.x += w.w * p3.x;
+    aR.y += w.w * p3.y;
+  }
+  const T2* __restrict__ cv = (const T2*)h.cval;
+  const int kb = h.rowptr[m], ke = h.rowptr[m + 1];
+#pragma unroll 4
+  for (int kk = kb + lane; kk < ke; kk += 32) {
+    const int n = h.col[kk];
+    const T2 c = cv[kk];
+    const T2 xv = x[n];
+    aA.x += c.x * xv.x; aA.y += c.x * xv.y;
+    aR.x += c.y * xv.x; aR.y += c.y * xv.y;
+  }
+  aA = warp_sum(aA);
+  aR = warp_sum(aR);
+  if (lane == 0) {
+    using R = decltype(T2::x);
+    if (cb.mode == 0) {
+      const R al = (R)cb.alpha_im[0], be = (R)cb.beta[0];
+      const R ux = aA.x - be * aR.x, uy = aA.y - be * aR.y;
+      y0[m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
+    } else {
+      if (y0) y0[m] = aA;
+      if (y1) y1[m] = mk<T2>(-aR.x, -aR.y);
+    }
+  }
+}
+
+// BB right-hand sides (batch-interleaved xt[n * BB + b]): lane = (group g,
+// column b); the 32/BB groups stride the stencil nodes and the near row, the
+// BB lanes of a group read one contiguous x row per near entry.
+template <typename T, int BB>
+__global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
+                                                     typename CT<T>::T2* __restrict__ y0, Combine cb) {
+  using T2 = typename CT<T>::T2;
+  using T4 = typename CT<T>::T4;
+  constexpr int NG = 32 / BB;
+  const int lane = threadIdx.x & 31;
+  const int b = lane % BB, g = lane / BB;
+  const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (m >= h.nb) return;
+  const bool live = b < cb.B;
+  T2 aA = mk<T2>(0, 0), aR = mk<T2>(0, 0);
+  for (int sl = g; sl < h.p3; sl += NG) {
+    const int p = h.p;
+    const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
+    const int64_t lin = (int64_t)h.rwg_base[m] + i + (int64_t)h.Nx * (j + (int64_t)h.Ny * k);
+    const T4 w = ((const T4*)h.lam)[(int64_t)m * h.p3 + sl];
+    if (live) {
+      const T2* ph = (const T2*)h.phi + b * h.sP + lin * 4;
+      const T2 p0 = ph[0], p1 = ph[1], p2 = ph[2], p3 = ph[3];
+      aA.x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
+      aA.y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
+      aR.x += w.w * p3.x;
+      aR.y += w.w * p3.y;
     }
   }
   const T2* __restrict__ cv = (const T2*)h.cval;
   const int kb = h.rowptr[m], ke = h.rowptr[m + 1];
-  // x for the near rows: batch-interleaved xt[n * BB + b] (BB > 1) or x itself
-  for (int kk = kb + lane; kk < ke; kk += 32) {
+#pragma unroll 4
+  for (int kk = kb + g; kk < ke; kk += NG) {
     const int n = h.col[kk];
     const T2 c = cv[kk];
-    const T2* __restrict__ xr = x + (int64_t)n * BB;
-    T2 xv[BB];
-#pragma unroll
-    for (int b = 0; b < BB; ++b) xv[b] = xr[b];
-#pragma unroll
-    for (int b = 0; b < BB; ++b) {
-      aA[b].x += c.x * xv[b].x; aA[b].y += c.x * xv[b].y;
-      aR[b].x += c.y * xv[b].x; aR[b].y += c.y * xv[b].y;
-    }
+    const T2 xv = xt[(int64_t)n * BB + b];
+    aA.x += c.x * xv.x; aA.y += c.x * xv.y;
+    aR.x += c.y * xv.x; aR.y += c.y * xv.y;
   }
-  using R = decltype(T2::x);
 #pragma unroll
-  for (int b = 0; b < BB; ++b) {
-    if (b < B) {
-      const T2 sA = warp_sum(aA[b]);
-      const T2 sR = warp_sum(aR[b]);
-      if (lane == 0) {
-        if (cb.mode == 0) {
-          const R al = (R)cb.alpha_im[b], be = (R)cb.beta[b];
-          const R ux = sA.x - be * sR.x, uy = sA.y - be * sR.y;
-          y0[b * cb.ystride + m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
-        } else {
-          if (y0) y0[b * cb.ystride + m] = sA;
-          if (y1) y1[b * cb.ystride + m] = mk<T2>(-sR.x, -sR.y);
-        }
-      }
-    }
+  for (int o = BB; o < 32; o <<= 1) {
+    aA.x += __shfl_xor_sync(0xffffffffu, aA.x, o);
+    aA.y += __shfl_xor_sync(0xffffffffu, aA.y, o);
+    aR.x += __shfl_xor_sync(0xffffffffu, aR.x, o);
+    aR.y += __shfl_xor_sync(0xffffffffu, aR.y, o);
+  }
+  if (g == 0 && live) {
+    using R = decltype(T2::x);
+    const R al = (R)cb.alpha_im[b], be = (R)cb.beta[b];
+    const R ux = aA.x - be * aR.x, uy = aA.y - be * aR.y;
+    y0[b * cb.ystride + m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
   }
 }
 
@@ -361,10 +421,9 @@ void run_gather(const HotDev& h, const void* x, int64_t xstride, int B, cudaStre
 
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
-  using T2 = typename CT<T>::T2;
-  constexpr int ROWS = rows_x<T>(L);
-  const size_t sm = sizeof(T2) * (L + 2 * ROWS * (L + 1) * 4);
-  dim3 g((unsigned)((h.nlines + ROWS - 1) / ROWS), (unsigned)B);
+  constexpr size_t sm = pass_smem<T, L>();
+  constexpr int RPC = PassGeom<L>::NL / 4;
+  dim3 g((unsigned)((h.nlines + RPC - 1) / RPC), (unsigned)B);
   if (!inv) {
     set_smem(k_xfwd<T, L>, sm);
     k_xfwd<T, L><<<g, 256, sm, s>>>(h);
@@ -375,11 +434,17 @@ void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   AIMX_CHECK_LAUNCH();
 }
 
+template <int L> dim3 col_grid(int W, int rows, int B) {
+  constexpr int NL = PassGeom<L>::NL;
+  const int CW = NL < W ? NL : W;
+  const int RPC = NL / CW;
+  return dim3((unsigned)(W / CW), (unsigned)((rows + RPC - 1) / RPC), (unsigned)B);
+}
+
 template <typename T, int L>
 void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
-  using T2 = typename CT<T>::T2;
-  const size_t sm = sizeof(T2) * (L + 2 * (size_t)L * h.twy);
-  dim3 g((unsigned)(8 * h.Nx / h.twy), (unsigned)h.nzocc, (unsigned)B);
+  constexpr size_t sm = pass_smem<T, L>();
+  dim3 g = col_grid<L>(8 * h.Nx, h.nzocc, B);
   if (!inv) {
     set_smem(k_yfwd<T, L>, sm);
     k_yfwd<T, L><<<g, 256, sm, s>>>(h);
@@ -392,10 +457,9 @@ void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
 
 template <typename T, int L>
 void run_z(const HotDev& h, int B, cudaStream_t s) {
-  using T2 = typename CT<T>::T2;
-  const size_t sm = sizeof(T2) * (L + 2 * (size_t)L * h.twz);
+  constexpr size_t sm = pass_smem<T, L>();
   set_smem(k_zconv<T, L>, sm);
-  dim3 g((unsigned)(8 * h.Nx / h.twz), (unsigned)(2 * h.Ny), (unsigned)B);
+  dim3 g = col_grid<L>(8 * h.Nx, 2 * h.Ny, B);
   k_zconv<T, L><<<g, 256, sm, s>>>(h);
   AIMX_CHECK_LAUNCH();
 }
@@ -415,20 +479,24 @@ template <typename T>
 void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   const unsigned g = (unsigned)(((int64_t)h.nb * 32 + 255) / 256);
-  const T2* xx = (const T2*)x;
-  if (c.B > 1) {
-    const int BB = c.B <= 2 ? 2 : (c.B <= 4 ? 4 : (c.B <= 8 ? 8 : 16));
-    const int64_t n = (int64_t)h.nb * BB;
-    k_interleave<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.nb, c.B, BB, xx, c.xstride,
-                                                                (T2*)h.xt);
+  if (c.B == 1) {
+    k_interp_near1<T><<<g, 256, 0, s>>>(h, (const T2*)x, (T2*)y0, (T2*)y1, c);
     AIMX_CHECK_LAUNCH();
-    xx = (const T2*)h.xt;
+    return;
   }
-  if (c.B <= 1) k_interp_near<T, 1><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);
-  else if (c.B <= 2) k_interp_near<T, 2><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);
-  else if (c.B <= 4) k_interp_near<T, 4><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);
-  else if (c.B <= 8) k_interp_near<T, 8><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);
-  else k_interp_near<T, 16><<<g, 256, 0, s>>>(h, xx, (T2*)y0, (T2*)y1, c);
+  if (c.mode != 0) throw Error(AIMX_E_INTERNAL, "batched parts not supported");
+  const int BB = c.B <= 2 ? 2 : (c.B <= 4 ? 4 : (c.B <= 8 ? 8 : 16));
+  const int64_t n = (int64_t)h.nb * BB;
+  k_interleave<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.nb, c.B, BB, (const T2*)x, c.xstride,
+                                                              (T2*)h.xt);
+  AIMX_CHECK_LAUNCH();
+  const T2* xt = (const T2*)h.xt;
+  switch (BB) {
+    case 2: k_interp_near<T, 2><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
+    case 4: k_interp_near<T, 4><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
+    case 8: k_interp_near<T, 8><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
+    default: k_interp_near<T, 16><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
+  }
   AIMX_CHECK_LAUNCH();
 }
 

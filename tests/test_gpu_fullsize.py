@@ -61,4 +61,4 @@ def test_cfg2_sweep_matches_per_frequency_matvecs():
     Y = op.sweep(freqs, X)
     for i, f in enumerate(freqs):
         op.set_frequency(f)
-        assert torch.equal(op.matvec(X[i].contiguous()), Y[i])
+        assert rel_l2(op.matvec(X[i].contiguous()).cpu().numpy(), Y[i].cpu().numpy()) <= 1e-6

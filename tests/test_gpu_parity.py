@@ -131,14 +131,15 @@ def test_sweep_equals_matvec_loop_and_host_sweep(prec):
     X = np.stack([inp.rhs_vector(1, i, op.N) for i in range(5)])
     Xg = to_gpu(X, prec)
     Y = op.sweep(freqs, Xg).cpu()
+    tol = 1e-6 if prec == "c64" else 1e-14
     for i, f in enumerate(freqs):
         op.set_frequency(f)
         yi = op.matvec(Xg[i].contiguous()).cpu()
-        assert torch.equal(yi, Y[i])
+        assert rel_l2(yi.numpy(), Y[i].numpy()) <= tol
     Xh = Xg.cpu().pin_memory()
     Yh = torch.empty_like(Xh).pin_memory()
     op.sweep_host(freqs, Xh, Yh, batch=2)
-    assert torch.equal(Yh, Y)
+    assert torch.equal(Yh, op.sweep(freqs, Xg, batch=2).cpu())
 
 
 @pytest.mark.parametrize("prec", ["c64", "c128"])
@@ -180,11 +181,16 @@ def test_other_stencil_orders(order):
 
 @pytest.mark.parametrize("prec", ["c64", "c128"])
 def test_sweep_results_independent_of_batch_size(prec):
+    """Deterministic (bitwise) for a fixed batch size; across batch sizes the
+    near-row reduction is partitioned differently, so results agree to rounding."""
     import torch
     op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), prec)
     assert op.stats()["batch_slots"] >= 4
     freqs = np.linspace(20e6, 400e6, 11)
     X = to_gpu(np.stack([inp.rhs_vector(1, i, op.N) for i in range(11)]), prec)
     ref = op.sweep(freqs, X, batch=1).clone()
+    tol = 1e-6 if prec == "c64" else 1e-14
     for b in (2, 3, 4, 16):
-        assert torch.equal(op.sweep(freqs, X, batch=b), ref)
+        y = op.sweep(freqs, X, batch=b).clone()
+        assert torch.equal(op.sweep(freqs, X, batch=b), y)
+        assert rel_l2(y.cpu().numpy(), ref.cpu().numpy()) <= tol
