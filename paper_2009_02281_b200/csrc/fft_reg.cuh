@@ -179,6 +179,10 @@ template <typename T2, int R1, int R2, bool INV>
 __device__ __forceinline__ void fft2(T2* v, T2* xb, const T2* tw, int t) {
   using TL = TwoLevel<R1, R2>;
   constexpr int T = TL::T, A = R1 / T, C = R2 / T;
+  if constexpr (R2 == 1) {   // one thread holds the whole line in natural order
+    dftr<T2, R1, INV>(v);
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < A; ++a) dftr<T2, R2, INV>(v + a * R2);
   if constexpr (R1 > 1) {

@@ -74,35 +74,39 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
 // line-fastest (line = tid % NL, t = tid / NL) so that a warp's loads and
 // stores cover consecutive grid columns; the per-line exchange uses one block
 // barrier per transform.
-template <int L> struct PassGeom {
+template <typename S, int L> struct PassGeom {
   static constexpr int R1 = Fac<L>::R1, R2 = Fac<L>::R2;
   using TL = TwoLevel<R1, R2>;
   static constexpr int T = TL::T, E = TL::E;
-  static constexpr int NL = 256 / T;                // lines per CTA
-  static constexpr int XB = R1 > 1 ? TL::XB : 0;    // exchange elements per line
+  // per-line exchange stride: bank-spread so that the lines and threads of a
+  // warp hit distinct 8-byte slots (stride = 1 mod 16, or 4 mod 16 when a
+  // warp holds 8 lines x 4 threads)
+  static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? 4 : 1) : 0;
+  static constexpr size_t BYTES256 = sizeof(typename CT<S>::T2) * (size_t)(256 / T) * XB;
+  static constexpr int NT = BYTES256 > 200 * 1024 ? 128 : 256;   // threads per CTA
+  static constexpr int NL = NT / T;                               // lines per CTA
 };
 
 template <typename T2, int L>
 __device__ __forceinline__ void fwd_fft(T2* v, T2* xb, const T2* tw, int t) {
-  using G = PassGeom<L>;
-  fft2<T2, G::R1, G::R2, false>(v, xb, tw, t);
+  fft2<T2, Fac<L>::R1, Fac<L>::R2, false>(v, xb, tw, t);
 }
 // inverse of data in the forward's output distribution, back to the input one
 template <typename T2, int L>
 __device__ __forceinline__ void inv_fft_swapped(T2* v, T2* xb, const T2* tw, int t) {
-  using G = PassGeom<L>;
-  fft2<T2, G::R2, G::R1, true>(v, xb, tw, t);
+  fft2<T2, Fac<L>::R2, Fac<L>::R1, true>(v, xb, tw, t);
 }
 // inverse of data loaded in the input distribution (output distribution after)
 template <typename T2, int L>
 __device__ __forceinline__ void inv_fft(T2* v, T2* xb, const T2* tw, int t) {
-  using G = PassGeom<L>;
-  fft2<T2, G::R1, G::R2, true>(v, xb, tw, t);
+  fft2<T2, Fac<L>::R1, Fac<L>::R2, true>(v, xb, tw, t);
 }
 
-template <typename T2, int L>
-__device__ __forceinline__ void pass_prologue(T2*& tw, T2*& xb, const T2* __restrict__ gtw, int line) {
-  using G = PassGeom<L>;
+template <typename T, int L>
+__device__ __forceinline__ void pass_prologue(typename CT<T>::T2*& tw, typename CT<T>::T2*& xb,
+                                              const typename CT<T>::T2* __restrict__ gtw, int line) {
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<T, L>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   tw = reinterpret_cast<T2*>(smem_raw);
   xb = tw + L + line * G::XB;
@@ -111,7 +115,7 @@ __device__ __forceinline__ void pass_prologue(T2*& tw, T2*& xb, const T2* __rest
 }
 
 template <typename T, int L> constexpr size_t pass_smem() {
-  using G = PassGeom<L>;
+  using G = PassGeom<T, L>;
   return sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB);
 }
 
@@ -119,10 +123,10 @@ template <typename T, int L> constexpr size_t pass_smem() {
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<L>;
+  using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T2, L>(tw, xb, (const T2*)h.twx, line);
+  pass_prologue<T, L>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y;
   const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
   const bool act = r < h.nlines;
@@ -145,10 +149,10 @@ __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<L>;
+  using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T2, L>(tw, xb, (const T2*)h.twx, line);
+  pass_prologue<T, L>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y;
   const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
   const bool act = r < h.nlines;
@@ -172,8 +176,8 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
 struct ColTile {
   int w, rsub, CW, RPC;
 };
-template <int L> __device__ __forceinline__ ColTile col_tile(int line, int W) {
-  constexpr int NL = PassGeom<L>::NL;
+template <typename T, int L> __device__ __forceinline__ ColTile col_tile(int line, int W) {
+  constexpr int NL = PassGeom<T, L>::NL;
   ColTile ct;
   ct.CW = NL < W ? NL : W;
   ct.RPC = NL / ct.CW;
@@ -186,12 +190,12 @@ template <int L> __device__ __forceinline__ ColTile col_tile(int line, int W) {
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<L>;
+  using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T2, L>(tw, xb, (const T2*)h.twy_tab, line);
+  pass_prologue<T, L>(tw, xb, (const T2*)h.twy_tab, line);
   const int W = 8 * h.Nx, Ny = h.Ny;
-  const ColTile ct = col_tile<L>(line, W);
+  const ColTile ct = col_tile<T, L>(line, W);
   const int zi = blockIdx.y * ct.RPC + ct.rsub;
   const bool act = zi < h.nzocc;
   const int z = act ? h.zplanes[zi] : 0;
@@ -215,12 +219,12 @@ __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<L>;
+  using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T2, L>(tw, xb, (const T2*)h.twy_tab, line);
+  pass_prologue<T, L>(tw, xb, (const T2*)h.twy_tab, line);
   const int W = 8 * h.Nx, Ny = h.Ny;
-  const ColTile ct = col_tile<L>(line, W);
+  const ColTile ct = col_tile<T, L>(line, W);
   const int zi = blockIdx.y * ct.RPC + ct.rsub;
   const bool act = zi < h.nzocc;
   const int z = act ? h.zplanes[zi] : 0;
@@ -245,12 +249,12 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_zconv(HotDev h) {
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<L>;
+  using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T2, L>(tw, xb, (const T2*)h.twz_tab, line);
+  pass_prologue<T, L>(tw, xb, (const T2*)h.twz_tab, line);
   const int W = 8 * h.Nx, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
-  const ColTile ct = col_tile<L>(line, W);
+  const ColTile ct = col_tile<T, L>(line, W);
   const int ky = blockIdx.y * ct.RPC + ct.rsub;
   const bool act = ky < Ny2;
   const int b = blockIdx.z;
@@ -422,20 +426,20 @@ void run_gather(const HotDev& h, const void* x, int64_t xstride, int B, cudaStre
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>();
-  constexpr int RPC = PassGeom<L>::NL / 4;
+  constexpr int RPC = PassGeom<T, L>::NL / 4;
   dim3 g((unsigned)((h.nlines + RPC - 1) / RPC), (unsigned)B);
   if (!inv) {
     set_smem(k_xfwd<T, L>, sm);
-    k_xfwd<T, L><<<g, 256, sm, s>>>(h);
+    k_xfwd<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
   } else {
     set_smem(k_xinv<T, L>, sm);
-    k_xinv<T, L><<<g, 256, sm, s>>>(h);
+    k_xinv<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
   }
   AIMX_CHECK_LAUNCH();
 }
 
-template <int L> dim3 col_grid(int W, int rows, int B) {
-  constexpr int NL = PassGeom<L>::NL;
+template <typename T, int L> dim3 col_grid(int W, int rows, int B) {
+  constexpr int NL = PassGeom<T, L>::NL;
   const int CW = NL < W ? NL : W;
   const int RPC = NL / CW;
   return dim3((unsigned)(W / CW), (unsigned)((rows + RPC - 1) / RPC), (unsigned)B);
@@ -444,13 +448,13 @@ template <int L> dim3 col_grid(int W, int rows, int B) {
 template <typename T, int L>
 void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>();
-  dim3 g = col_grid<L>(8 * h.Nx, h.nzocc, B);
+  dim3 g = col_grid<T, L>(8 * h.Nx, h.nzocc, B);
   if (!inv) {
     set_smem(k_yfwd<T, L>, sm);
-    k_yfwd<T, L><<<g, 256, sm, s>>>(h);
+    k_yfwd<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
   } else {
     set_smem(k_yinv<T, L>, sm);
-    k_yinv<T, L><<<g, 256, sm, s>>>(h);
+    k_yinv<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
   }
   AIMX_CHECK_LAUNCH();
 }
@@ -459,8 +463,8 @@ template <typename T, int L>
 void run_z(const HotDev& h, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>();
   set_smem(k_zconv<T, L>, sm);
-  dim3 g = col_grid<L>(8 * h.Nx, 2 * h.Ny, B);
-  k_zconv<T, L><<<g, 256, sm, s>>>(h);
+  dim3 g = col_grid<T, L>(8 * h.Nx, 2 * h.Ny, B);
+  k_zconv<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
   AIMX_CHECK_LAUNCH();
 }
 
