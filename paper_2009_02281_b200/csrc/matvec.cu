@@ -134,9 +134,9 @@ __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
   const T2* __restrict__ in = (const T2*)h.S + b * h.sS + (int64_t)r * Nx * 4 + c;
   T2 v[G::E];
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) {
+  for (int i = 0; i < G::E; ++i) {   // x < Nx = L/2  <=>  n2 < R2/2
     const int x = G::TL::in_index(t, i);
-    v[i] = (act && x < Nx) ? in[x * 4] : mk<T2>(0, 0);
+    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * 4] : mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
@@ -164,11 +164,12 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   inv_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   const int Nx = h.Nx;
-  T2* __restrict__ out = (T2*)h.phi + b * h.sP + (int64_t)lid * Nx * 4 + c;
+  const int64_t ns = (int64_t)h.batch * 4;   // node stride (batch-interleaved phi)
+  T2* __restrict__ out = (T2*)h.phi + (int64_t)b * 4 + c + (int64_t)lid * Nx * ns;
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) {
+  for (int i = 0; i < G::E; ++i) {   // x < Nx  <=>  k1 < R1/2 in D(R2,R1)
     const int x = TwoLevel<G::R2, G::R1>::in_index(t, i);
-    if (x < Nx) out[x * 4] = v[i];
+    if (i % G::R1 < (G::R1 + 1) / 2 && x < Nx) out[x * ns] = v[i];
   }
 }
 
@@ -204,9 +205,9 @@ __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
   const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + (int64_t)z * Ny * W + col;
   T2 v[G::E];
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) {
+  for (int i = 0; i < G::E; ++i) {   // y < Ny = L/2  <=>  n2 < R2/2
     const int y = G::TL::in_index(t, i);
-    v[i] = (act && y < Ny) ? in[(int64_t)y * W] : mk<T2>(0, 0);
+    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[(int64_t)y * W] : mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
@@ -239,18 +240,19 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
   T2* __restrict__ out = (T2*)h.bufC + b * h.sA + (int64_t)z * Ny * W + col;
   const uint8_t* occ = h.line_occ + (int64_t)z * Ny;
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) {
+  for (int i = 0; i < G::E; ++i) {   // y < Ny  <=>  k1 < R1/2 in D(R2,R1)
     const int y = TwoLevel<G::R2, G::R1>::in_index(t, i);
-    if (y < Ny && occ[y]) out[(int64_t)y * W] = v[i];
+    if (i % G::R1 < (G::R1 + 1) / 2 && y < Ny && occ[y]) out[(int64_t)y * W] = v[i];
   }
 }
 
 // ---- z forward * H_hat * z inverse, in place on bufB (occupied planes only)
-template <typename T, int L>
+template <typename T, int L, bool FULLZ>
 __global__ void __launch_bounds__(256) k_zconv(HotDev h) {
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  __builtin_assume(t < G::T);
   T2 *tw, *xb;
   pass_prologue<T, L>(tw, xb, (const T2*)h.twz_tab, line);
   const int W = 8 * h.Nx, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
@@ -262,11 +264,13 @@ __global__ void __launch_bounds__(256) k_zconv(HotDev h) {
   const int64_t zs = (int64_t)Ny2 * W;
   T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)(act ? ky : 0) * W + col;
   const uint8_t* __restrict__ zocc = h.zocc;
+  // input distribution D(R1,R2): z = t + T a + R1 n2 < Nz = L/2  <=>  n2 < R2/2
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {
     const int z = G::TL::in_index(t, i);
-    v[i] = (act && z < Nz && zocc[z]) ? g[z * zs] : mk<T2>(0, 0);
+    if (i % G::R2 < G::R2 / 2) v[i] = (act && (FULLZ || zocc[z])) ? g[z * zs] : mk<T2>(0, 0);
+    else v[i] = mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   {  // spectrum multiply (octant [ky][kz][kx], 1/M folded into H)
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(256) k_zconv(HotDev h) {
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {
     const int z = G::TL::in_index(t, i);
-    if (z < Nz && zocc[z]) g[z * zs] = v[i];
+    if (i % G::R2 < G::R2 / 2 && (FULLZ || zocc[z])) g[z * zs] = v[i];
   }
 }
 
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(256) k_interp_near1(HotDev h, const typename C
     const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
     const int64_t lin = (int64_t)h.rwg_base[m] + i + (int64_t)h.Nx * (j + (int64_t)h.Ny * k);
     const T4 w = ((const T4*)h.lam)[(int64_t)m * h.p3 + sl];
-    const T2* ph = (const T2*)h.phi + lin * 4;
+    const T2* ph = (const T2*)h.phi + lin * h.batch * 4;
     const T2 p0 = ph[0], p1 = ph[1], p2 = ph[2], p3 = ph[3];
     aA.x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
     aA.y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
@@ -349,33 +353,55 @@ __global__ void __launch_bounds__(256) k_interp_near1(HotDev h, const typename C
   }
 }
 
-// BB right-hand sides (batch-interleaved xt[n * BB + b]): lane = (group g,
-// column b); the 32/BB groups stride the stencil nodes and the near row, the
-// BB lanes of a group read one contiguous x row per near entry.
+// BB right-hand sides (batch-interleaved xt[n * BB + b], phi[(lin * slots + b)
+// * 4 + c]): lane = (group g, columns b0..b0+V-1) with V complex per 16-byte
+// load; the 32/(BB/V) groups stride the stencil nodes and the near row, the
+// lanes of a group read one contiguous x row per near entry.
+template <typename T2, int V> struct VecT;
+template <> struct VecT<float2, 2> { using type = float4; };
+template <> struct VecT<double2, 1> { using type = double2; };
+
 template <typename T, int BB>
 __global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      typename CT<T>::T2* __restrict__ y0, Combine cb) {
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
-  constexpr int NG = 32 / BB;
+  constexpr int V = sizeof(T2) == 8 ? 2 : 1;       // complex per 16-byte load
+  constexpr int LG = BB / V;                         // lanes per group
+  constexpr int NG = 32 / LG;                        // groups per warp
+  using VT = typename VecT<T2, V>::type;
   const int lane = threadIdx.x & 31;
-  const int b = lane % BB, g = lane / BB;
+  const int b0 = (lane % LG) * V, g = lane / LG;
   const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (m >= h.nb) return;
-  const bool live = b < cb.B;
-  T2 aA = mk<T2>(0, 0), aR = mk<T2>(0, 0);
+  T2 aA[V], aR[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) { aA[v] = mk<T2>(0, 0); aR[v] = mk<T2>(0, 0); }
+  const int64_t ns = (int64_t)h.batch * 4;
   for (int sl = g; sl < h.p3; sl += NG) {
     const int p = h.p;
     const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
     const int64_t lin = (int64_t)h.rwg_base[m] + i + (int64_t)h.Nx * (j + (int64_t)h.Ny * k);
     const T4 w = ((const T4*)h.lam)[(int64_t)m * h.p3 + sl];
-    if (live) {
-      const T2* ph = (const T2*)h.phi + b * h.sP + lin * 4;
-      const T2 p0 = ph[0], p1 = ph[1], p2 = ph[2], p3 = ph[3];
-      aA.x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
-      aA.y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
-      aR.x += w.w * p3.x;
-      aR.y += w.w * p3.y;
+    const VT* ph = (const VT*)((const T2*)h.phi + lin * ns + (int64_t)b0 * 4);
+    T2 pv[4 * V];
+#pragma unroll
+    for (int q = 0; q < 4 * V / V; ++q) {
+      const VT u = ph[q];
+      if constexpr (V == 2) {
+        pv[2 * q] = mk<T2>(u.x, u.y);
+        pv[2 * q + 1] = mk<T2>(u.z, u.w);
+      } else {
+        pv[q] = u;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const T2 p0 = pv[4 * v], p1 = pv[4 * v + 1], p2 = pv[4 * v + 2], p3 = pv[4 * v + 3];
+      aA[v].x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
+      aA[v].y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
+      aR[v].x += w.w * p3.x;
+      aR[v].y += w.w * p3.y;
     }
   }
   const T2* __restrict__ cv = (const T2*)h.cval;
@@ -384,22 +410,41 @@ __global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT
   for (int kk = kb + g; kk < ke; kk += NG) {
     const int n = h.col[kk];
     const T2 c = cv[kk];
-    const T2 xv = xt[(int64_t)n * BB + b];
-    aA.x += c.x * xv.x; aA.y += c.x * xv.y;
-    aR.x += c.y * xv.x; aR.y += c.y * xv.y;
+    const VT u = *(const VT*)(xt + (int64_t)n * BB + b0);
+    T2 xv[V];
+    if constexpr (V == 2) {
+      xv[0] = mk<T2>(u.x, u.y);
+      xv[1] = mk<T2>(u.z, u.w);
+    } else {
+      xv[0] = u;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      aA[v].x += c.x * xv[v].x; aA[v].y += c.x * xv[v].y;
+      aR[v].x += c.y * xv[v].x; aR[v].y += c.y * xv[v].y;
+    }
   }
 #pragma unroll
-  for (int o = BB; o < 32; o <<= 1) {
-    aA.x += __shfl_xor_sync(0xffffffffu, aA.x, o);
-    aA.y += __shfl_xor_sync(0xffffffffu, aA.y, o);
-    aR.x += __shfl_xor_sync(0xffffffffu, aR.x, o);
-    aR.y += __shfl_xor_sync(0xffffffffu, aR.y, o);
+  for (int o = LG; o < 32; o <<= 1) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      aA[v].x += __shfl_xor_sync(0xffffffffu, aA[v].x, o);
+      aA[v].y += __shfl_xor_sync(0xffffffffu, aA[v].y, o);
+      aR[v].x += __shfl_xor_sync(0xffffffffu, aR[v].x, o);
+      aR[v].y += __shfl_xor_sync(0xffffffffu, aR[v].y, o);
+    }
   }
-  if (g == 0 && live) {
+  if (g == 0) {
     using R = decltype(T2::x);
-    const R al = (R)cb.alpha_im[b], be = (R)cb.beta[b];
-    const R ux = aA.x - be * aR.x, uy = aA.y - be * aR.y;
-    y0[b * cb.ystride + m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int b = b0 + v;
+      if (b < cb.B) {
+        const R al = (R)cb.alpha_im[b], be = (R)cb.beta[b];
+        const R ux = aA[v].x - be * aR[v].x, uy = aA[v].y - be * aR[v].y;
+        y0[b * cb.ystride + m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
+      }
+    }
   }
 }
 
@@ -462,9 +507,14 @@ void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
 template <typename T, int L>
 void run_z(const HotDev& h, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>();
-  set_smem(k_zconv<T, L>, sm);
   dim3 g = col_grid<T, L>(8 * h.Nx, 2 * h.Ny, B);
-  k_zconv<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+  if (h.nzocc == h.Nz) {
+    set_smem(k_zconv<T, L, true>, sm);
+    k_zconv<T, L, true><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+  } else {
+    set_smem(k_zconv<T, L, false>, sm);
+    k_zconv<T, L, false><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+  }
   AIMX_CHECK_LAUNCH();
 }
 

@@ -21,6 +21,7 @@
 
 #include "aimx_internal.h"
 #include "fft.cuh"
+#include "fft_reg.cuh"
 
 namespace aimx {
 
@@ -61,92 +62,74 @@ __global__ void k_sample(int Nx, int Ny, int Nz, int64_t noct, double h, K0s k0s
   out[(int64_t)b * noct + idx] = mk<T2>((T)re, (T)im);
 }
 
-// Row mode: lines contiguous (x axis), line l element i at l*n1 + i.
-template <typename T, int L>
-__global__ void __launch_bounds__(256) k_even_rows(int64_t nlines, int64_t noct,
-                                                   const typename CT<T>::T2* __restrict__ in,
-                                                   typename CT<T>::T2* __restrict__ out,
-                                                   const typename CT<T>::T2* __restrict__ twg) {
-  using T2 = typename CT<T>::T2;
-  constexpr int N1 = L / 2 + 1;
-  constexpr int R = (4096 / L) < 1 ? 1 : (4096 / L);
-  constexpr int RS = L + 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* b0 = tw + L;
-  T2* b1 = b0 + R * RS;
-  const int64_t l0 = (int64_t)blockIdx.x * R;
-  const int nl = (int)min((int64_t)R, nlines - l0);
-  const int64_t boff = (int64_t)blockIdx.y * noct;
-  load_tw(tw, twg, L);
-  const T2* __restrict__ src = in + boff + l0 * N1;
-  for (int t = threadIdx.x; t < nl * N1; t += blockDim.x) {
-    const int r = t / N1, i = t - r * N1;
-    cp_async(b0 + r * RS + i, src + t);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  for (int t = threadIdx.x; t < nl * (L - N1); t += blockDim.x) {
-    const int r = t / (L - N1), i = N1 + (t - r * (L - N1));
-    b0[r * RS + i] = b0[r * RS + (L - i)];
-  }
-  __syncthreads();
-  T2* s0 = b0;
-  T2* s1 = b1;
-  struct A { __device__ int operator()(int line, int idx) const { return line * RS + idx; } };
-  smem_fft<T2, L, false>(s0, s1, nl, tw, A{});
-  T2* __restrict__ dst = out + boff + l0 * N1;
-  for (int t = threadIdx.x; t < nl * N1; t += blockDim.x) {
-    const int r = t / N1, i = t - r * N1;
-    dst[t] = s0[r * RS + i];
-  }
-}
+// Even-extension transform of lines of N1 = L/2 + 1 octant samples with the
+// register engine (fft_reg.cuh): slot n of the length-L line holds
+// v[n <= L/2 ? n : L - n]; only the outputs k <= L/2 are stored.
+// Row mode (contiguous lines, x axis): line-major thread mapping so a warp
+// reads consecutive samples; column mode (strided lines): line-fastest
+// mapping, lines = consecutive u.  Optional epilogue out = scale (v + add).
+template <typename S, int L> struct EvGeom {
+  static constexpr int R1 = Fac<L>::R1, R2 = Fac<L>::R2;
+  using TL = TwoLevel<R1, R2>;
+  static constexpr int T = TL::T, E = TL::E;
+  static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? 4 : 1) : 0;
+  static constexpr size_t BYTES256 = sizeof(typename CT<S>::T2) * (size_t)(256 / T) * XB;
+  static constexpr int NT = BYTES256 > 200 * 1024 ? 128 : 256;
+  static constexpr int NL = NT / T;
+};
 
-// Column mode: element (o, i, u) at (o n1 + i) inner + u; tile of TW u's.
-// Optional epilogue: out = scale * (v + add[idx]).
-template <typename T, int L>
-__global__ void __launch_bounds__(256) k_even_cols(int64_t inner, int TW, int64_t noct,
-                                                   const typename CT<T>::T2* __restrict__ in,
-                                                   typename CT<T>::T2* __restrict__ out,
-                                                   const typename CT<T>::T2* __restrict__ twg,
-                                                   const typename CT<T>::T2* __restrict__ add, T scale) {
+template <typename T, int L, bool ROW>
+__global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int64_t noct,
+                                              const typename CT<T>::T2* __restrict__ in,
+                                              typename CT<T>::T2* __restrict__ out,
+                                              const typename CT<T>::T2* __restrict__ twg,
+                                              const typename CT<T>::T2* __restrict__ add, T scale) {
   using T2 = typename CT<T>::T2;
+  using G = EvGeom<T, L>;
   constexpr int N1 = L / 2 + 1;
+  const int line = ROW ? threadIdx.x / G::T : threadIdx.x % G::NL;
+  const int t = ROW ? threadIdx.x % G::T : threadIdx.x / G::NL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* b0 = tw + L;
-  T2* b1 = b0 + L * TW;
-  const int64_t u0 = (int64_t)blockIdx.x * TW;
-  const int nu = (int)min((int64_t)TW, inner - u0);
-  const int64_t o = blockIdx.y;
+  T2* xb = tw + L + line * G::XB;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = twg[i];
+  __syncthreads();
   const int64_t boff = (int64_t)blockIdx.z * noct;
-  load_tw(tw, twg, L);
-  const int64_t base = boff + o * N1 * inner + u0;
-  for (int t = threadIdx.x; t < N1 * TW; t += blockDim.x) {
-    const int i = t / TW, w = t - i * TW;
-    if (w < nu) cp_async(b0 + t, in + base + (int64_t)i * inner + w);
-    else b0[t] = mk<T2>(0, 0);
+  // line -> base offset and element stride
+  int64_t base, stride;
+  bool act;
+  if (ROW) {
+    const int64_t lg = (int64_t)blockIdx.x * G::NL + line;
+    act = lg < nlines;
+    base = boff + (act ? lg : 0) * N1;
+    stride = 1;
+  } else {
+    const int64_t u = (int64_t)blockIdx.x * G::NL + line;
+    act = u < inner;
+    base = boff + (int64_t)blockIdx.y * N1 * inner + (act ? u : 0);
+    stride = inner;
   }
-  cp_async_wait_all();
-  __syncthreads();
-  for (int t = threadIdx.x; t < (L - N1) * TW; t += blockDim.x) {
-    const int i = N1 + t / TW, w = t % TW;
-    b0[i * TW + w] = b0[(L - i) * TW + w];
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    int n = G::TL::in_index(t, i);
+    n = n <= L / 2 ? n : L - n;
+    v[i] = act ? in[base + n * stride] : mk<T2>(0, 0);
   }
-  __syncthreads();
-  T2* s0 = b0;
-  T2* s1 = b1;
-  smem_fft<T2, L, false>(s0, s1, TW, tw, ColAddr{TW});
-  for (int t = threadIdx.x; t < N1 * TW; t += blockDim.x) {
-    const int i = t / TW, w = t - i * TW;
-    if (w >= nu) continue;
-    const int64_t g = base + (int64_t)i * inner + w;
-    T2 v = s0[t];
-    if (add) {
-      const T2 a = add[g - boff];
-      v = mk<T2>(scale * (v.x + a.x), scale * (v.y + a.y));
+  fft2<T2, G::R1, G::R2, false>(v, xb, tw, t);
+  if (!act) return;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int k = TwoLevel<G::R2, G::R1>::in_index(t, i);
+    if (k <= L / 2) {
+      const int64_t gi = base + k * stride;
+      T2 r = v[i];
+      if (add) {
+        const T2 a = add[gi - boff];
+        r = mk<T2>(scale * (r.x + a.x), scale * (r.y + a.y));
+      }
+      out[gi] = r;
     }
-    out[g] = v;
   }
 }
 
@@ -160,11 +143,12 @@ void even_rows(int L, int64_t nlines, int64_t noct, int B, const void* in, void*
                cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   AIMX_SWITCH_L(L, ({
-    constexpr int R = (4096 / L) < 1 ? 1 : (4096 / L);
-    size_t sm = sizeof(T2) * (L + 2 * R * (L + 1));
-    set_smem(k_even_rows<T, L>, sm);
-    dim3 g((unsigned)((nlines + R - 1) / R), (unsigned)B);
-    k_even_rows<T, L><<<g, 256, sm, s>>>(nlines, noct, (const T2*)in, (T2*)out, (const T2*)tw);
+    using G = EvGeom<T, L>;
+    const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+    set_smem(k_even<T, L, true>, sm);
+    dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
+    k_even<T, L, true><<<g, G::NT, sm, s>>>(nlines, 1, noct, (const T2*)in, (T2*)out, (const T2*)tw,
+                                            nullptr, (T)1);
   }));
   AIMX_CHECK_LAUNCH();
 }
@@ -173,14 +157,13 @@ template <typename T>
 void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const void* in, void* out,
                const void* tw, const void* add, T scale, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
-  int TW = (int)(sizeof(T) == 4 ? 4096 : 2048) / L;
-  TW = TW < 4 ? 4 : (TW > 256 ? 256 : TW);
   AIMX_SWITCH_L(L, ({
-    size_t sm = sizeof(T2) * (L + 2 * (size_t)L * TW);
-    set_smem(k_even_cols<T, L>, sm);
-    dim3 g((unsigned)((inner + TW - 1) / TW), (unsigned)outer, (unsigned)B);
-    k_even_cols<T, L><<<g, 256, sm, s>>>(inner, TW, noct, (const T2*)in, (T2*)out, (const T2*)tw,
-                                         (const T2*)add, scale);
+    using G = EvGeom<T, L>;
+    const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+    set_smem(k_even<T, L, false>, sm);
+    dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
+    k_even<T, L, false><<<g, G::NT, sm, s>>>(0, inner, noct, (const T2*)in, (T2*)out, (const T2*)tw,
+                                             (const T2*)add, scale);
   }));
   AIMX_CHECK_LAUNCH();
 }
