@@ -186,10 +186,12 @@ aimx_status aimx_get_spectrum(const aimx_ctx* ctx, int which, double* out);
  * (S4 + S5).  When enabled, every launch of a stage is bracketed by a pair of
  * events; aimx_profile_read synchronises the context, adds up the elapsed
  * device time per stage (ms) and the number of bracketed launches since the
- * previous read, and resets them.  Arrays have AIMX_NUM_STAGES entries. */
+ * previous read, and resets them.  Arrays have AIMX_NUM_STAGES entries.
+ * *kernels (optional) receives the number of kernels this thread launched
+ * through the library since the last aimx_profile_enable / aimx_profile_read. */
 #define AIMX_NUM_STAGES 7
 aimx_status aimx_profile_enable(aimx_ctx* ctx, int on);
-aimx_status aimx_profile_read(aimx_ctx* ctx, double* ms, int64_t* launches);
+aimx_status aimx_profile_read(aimx_ctx* ctx, double* ms, int64_t* launches, int64_t* kernels);
 
 void aimx_destroy(aimx_ctx* ctx);
 const char* aimx_status_string(aimx_status s);

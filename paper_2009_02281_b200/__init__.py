@@ -69,7 +69,7 @@ ABI_FUNCTIONS = {
     "aimx_get_weights": (C.c_int, [_P, _P]),
     "aimx_get_spectrum": (C.c_int, [_P, C.c_int, _P]),
     "aimx_profile_enable": (C.c_int, [_P, C.c_int]),
-    "aimx_profile_read": (C.c_int, [_P, _P, _P]),
+    "aimx_profile_read": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int64)]),
     "aimx_destroy": (None, [_P]),
     "aimx_status_string": (C.c_char_p, [C.c_int]),
     "aimx_last_error": (C.c_char_p, [_P]),
@@ -234,11 +234,16 @@ class AIMx:
         _check(self.lib, self.lib.aimx_profile_enable(self.ctx, int(bool(on))), self.ctx)
 
     def profile_read(self) -> dict:
+        """{stage: (device ms, bracketed launches)} plus "kernels": total kernel
+        launches since profile_enable / the previous read."""
         ms = np.zeros(7)
         n = np.zeros(7, np.int64)
-        _check(self.lib, self.lib.aimx_profile_read(self.ctx, _P(ms.ctypes.data), _P(n.ctypes.data)),
-               self.ctx)
-        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.STAGES)}
+        k = C.c_int64()
+        _check(self.lib, self.lib.aimx_profile_read(self.ctx, _P(ms.ctypes.data), _P(n.ctypes.data),
+                                                    C.byref(k)), self.ctx)
+        out = {s: (float(ms[i]), int(n[i])) for i, s in enumerate(self.STAGES)}
+        out["kernels"] = int(k.value)
+        return out
 
     def rwg(self):
         ab = np.empty((self.N, 2), np.int32)

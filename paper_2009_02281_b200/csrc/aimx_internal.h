@@ -26,7 +26,14 @@ struct Error : std::runtime_error {
     }                                                                                \
   } while (0)
 
-#define AIMX_CHECK_LAUNCH() AIMX_CUDA(cudaGetLastError())
+// Every kernel launch is followed by AIMX_CHECK_LAUNCH(), which also counts it
+// (aimx_profile_read reports the count).
+int64_t& launch_counter();
+#define AIMX_CHECK_LAUNCH()            \
+  do {                                 \
+    ++::aimx::launch_counter();        \
+    AIMX_CUDA(cudaGetLastError());     \
+  } while (0)
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kC0 = 299792458.0;          // m/s (exact)

@@ -37,6 +37,13 @@ struct aimx_ctx {
   std::string last_error;
 };
 
+namespace aimx {
+int64_t& launch_counter() {
+  static thread_local int64_t n = 0;
+  return n;
+}
+}  // namespace aimx
+
 namespace {
 
 thread_local std::string g_setup_error;
@@ -618,14 +625,17 @@ aimx_status aimx_profile_enable(aimx_ctx* c, int on) {
   AIMX_CUDA(cudaSetDevice(c->device));
   c->prof.collect();
   c->prof.on = on != 0;
+  launch_counter() = 0;
   AIMX_API_END(c)
 }
 
-aimx_status aimx_profile_read(aimx_ctx* c, double* ms, int64_t* launches) {
+aimx_status aimx_profile_read(aimx_ctx* c, double* ms, int64_t* launches, int64_t* kernels) {
   if (!c) return AIMX_E_INVALID_ARG;
   AIMX_API_BEGIN
   AIMX_CUDA(cudaSetDevice(c->device));
   c->prof.collect();
+  if (kernels) *kernels = launch_counter();
+  launch_counter() = 0;
   for (int i = 0; i < AIMX_NUM_STAGES; ++i) {
     if (ms) ms[i] = c->prof.ms[i];
     if (launches) launches[i] = c->prof.n[i];

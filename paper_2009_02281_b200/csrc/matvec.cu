@@ -22,6 +22,7 @@
 // Pruning (exact, reading R12): lines/planes with no occupied node are never
 // transformed; their data are identically zero and are never read as input.
 #include <algorithm>
+#include <type_traits>
 
 #include "aimx_internal.h"
 #include "fft.cuh"
@@ -66,6 +67,69 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
   if (act && gl == 0) {
     T2* dst = (T2*)h.S + b * h.sS + ((int64_t)h.node_line[q] * h.Nx + h.node_lin[q] % h.Nx) * 4;
     dst[0] = a0; dst[1] = a1; dst[2] = a2; dst[3] = a3;
+  }
+}
+
+// S2 for BB right-hand sides at once (batch-interleaved xt[n * BB + b]):
+// warp per occupied node, groups of BB/V lanes stride its entries (each entry's
+// weights and RWG index read once for all columns), lanes cover columns.
+template <typename T, int BB>
+__global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
+                                                  int B) {
+  using T2 = typename CT<T>::T2;
+  using T4 = typename CT<T>::T4;
+  constexpr int V = sizeof(T2) == 8 ? 2 : 1;
+  constexpr int LG = BB / V, NG = 32 / LG;
+  using VT = typename std::conditional<V == 2, float4, double2>::type;
+  const int lane = threadIdx.x & 31;
+  const int b0 = (lane % LG) * V, g = lane / LG;
+  const int q = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (q >= h.nocc) return;
+  T2 a[V][4];
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a[v][c] = mk<T2>(0, 0);
+  const T4* __restrict__ ew = (const T4*)h.ent_w;
+  const int e1 = h.node_ptr[q + 1];
+#pragma unroll 4
+  for (int e = h.node_ptr[q] + g; e < e1; e += NG) {
+    const T4 w = ew[e];
+    const VT u = *(const VT*)(xt + (int64_t)h.ent_rwg[e] * BB + b0);
+    T2 xv[V];
+    if constexpr (V == 2) {
+      xv[0] = mk<T2>(u.x, u.y);
+      xv[1] = mk<T2>(u.z, u.w);
+    } else {
+      xv[0] = u;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      a[v][0].x += w.x * xv[v].x; a[v][0].y += w.x * xv[v].y;
+      a[v][1].x += w.y * xv[v].x; a[v][1].y += w.y * xv[v].y;
+      a[v][2].x += w.z * xv[v].x; a[v][2].y += w.z * xv[v].y;
+      a[v][3].x += w.w * xv[v].x; a[v][3].y += w.w * xv[v].y;
+    }
+  }
+#pragma unroll
+  for (int o = LG; o < 32; o <<= 1)
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        a[v][c].x += __shfl_xor_sync(0xffffffffu, a[v][c].x, o);
+        a[v][c].y += __shfl_xor_sync(0xffffffffu, a[v][c].y, o);
+      }
+  if (g == 0) {
+    const int64_t off = ((int64_t)h.node_line[q] * h.Nx + h.node_lin[q] % h.Nx) * 4;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int b = b0 + v;
+      if (b < B) {
+        T2* dst = (T2*)h.S + b * h.sS + off;
+        dst[0] = a[v][0]; dst[1] = a[v][1]; dst[2] = a[v][2]; dst[3] = a[v][3];
+      }
+    }
   }
 }
 
@@ -248,7 +312,7 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
 
 // ---- z forward * H_hat * z inverse, in place on bufB (occupied planes only)
 template <typename T, int L, bool FULLZ>
-__global__ void __launch_bounds__(256) k_zconv(HotDev h) {
+__global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_zconv(HotDev h) {
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
@@ -529,6 +593,33 @@ __global__ void k_interleave(int nb, int B, int BB, const typename CT<T>::T2* __
   xt[i] = b < B ? x[b * xstride + n] : mk<T2>(0, 0);
 }
 
+template <int BB> constexpr int bucket_ok() { return BB; }
+inline int batch_bucket(int B) { return B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : (B <= 8 ? 8 : 16))); }
+
+template <typename T>
+void run_interleave(const HotDev& h, const void* x, const Combine& c, cudaStream_t s) {
+  using T2 = typename CT<T>::T2;
+  const int BB = batch_bucket(c.B);
+  const int64_t n = (int64_t)h.nb * BB;
+  k_interleave<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.nb, c.B, BB, (const T2*)x, c.xstride,
+                                                              (T2*)h.xt);
+  AIMX_CHECK_LAUNCH();
+}
+
+template <typename T>
+void run_gather_b(const HotDev& h, int B, cudaStream_t s) {
+  using T2 = typename CT<T>::T2;
+  const unsigned g = (unsigned)(((int64_t)h.nocc * 32 + 255) / 256);
+  const T2* xt = (const T2*)h.xt;
+  switch (batch_bucket(B)) {
+    case 2: k_gather_b<T, 2><<<g, 256, 0, s>>>(h, xt, B); break;
+    case 4: k_gather_b<T, 4><<<g, 256, 0, s>>>(h, xt, B); break;
+    case 8: k_gather_b<T, 8><<<g, 256, 0, s>>>(h, xt, B); break;
+    default: k_gather_b<T, 16><<<g, 256, 0, s>>>(h, xt, B); break;
+  }
+  AIMX_CHECK_LAUNCH();
+}
+
 template <typename T>
 void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
@@ -539,13 +630,8 @@ void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combin
     return;
   }
   if (c.mode != 0) throw Error(AIMX_E_INTERNAL, "batched parts not supported");
-  const int BB = c.B <= 2 ? 2 : (c.B <= 4 ? 4 : (c.B <= 8 ? 8 : 16));
-  const int64_t n = (int64_t)h.nb * BB;
-  k_interleave<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.nb, c.B, BB, (const T2*)x, c.xstride,
-                                                              (T2*)h.xt);
-  AIMX_CHECK_LAUNCH();
-  const T2* xt = (const T2*)h.xt;
-  switch (BB) {
+  const T2* xt = (const T2*)h.xt;   // interleaved by run_interleave earlier in the matvec
+  switch (batch_bucket(c.B)) {
     case 2: k_interp_near<T, 2><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
     case 4: k_interp_near<T, 4><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
     case 8: k_interp_near<T, 8><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
@@ -561,7 +647,12 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
   const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz, B = c.B;
   {
     StageScope sc(prof, 1, s);
-    run_gather<T>(h, x, c.xstride, B, s);
+    if (B == 1) {
+      run_gather<T>(h, x, c.xstride, B, s);
+    } else {
+      run_interleave<T>(h, x, c, s);
+      run_gather_b<T>(h, B, s);
+    }
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, B, s)));
   }
   { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, B, s))); }

@@ -54,6 +54,7 @@ for cfg in [int(x) for x in a.configs.split(",")]:
         e1.record()
         torch.cuda.synchronize()
         prof = op.profile_read()
+        kern = prof.pop("kernels")
         op.profile_enable(False)
         # unprofiled back-to-back matvecs
         op.set_frequency(c.freqs[0])
@@ -69,7 +70,8 @@ for cfg in [int(x) for x in a.configs.split(",")]:
                       "MB": sb[k] / 1e6} for k, (ms, n) in prof.items()}
         print(json.dumps({"cfg": cfg, "prec": prec, "setup_s": tset, "stats": st,
                           "ms_per_freq_pt_profiled": e0.elapsed_time(e1) / a.iters,
-                          "ms_per_matvec": e2.elapsed_time(e3) / a.iters, "stages": stages}),
+                          "ms_per_matvec": e2.elapsed_time(e3) / a.iters, "kernels_per_freq_pt": kern / a.iters,
+                          "stages": stages}),
               flush=True)
         op.close()
         del op
