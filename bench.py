@@ -75,44 +75,66 @@ def rank_freqs(c: inp.Config, rank: int, world: int):
     return g[rank * nf:(rank + 1) * nf], np.arange(rank * nf, (rank + 1) * nf)
 
 
+def max_over_ranks(x: float, device="cuda") -> float:
+    """Max of a per-rank scalar over the job (identity at world size 1)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # --------------------------------------------------------------------------- clocks
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and clock-event reasons DURING the timed region via NVML
+    (every ~2 ms in a thread; the timed region of a cfg2 sweep is short), with
+    the nvidia-smi query of B200_PROFILING.md as fallback."""
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake_slowdown": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
     def __init__(self, gpu: int):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import threading
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop_ev = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[gpu]) if vis else gpu
+            self.h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = nv
+            self.mx.append(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
         except Exception:
-            self.p = None
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        bits = {k: getattr(nv, v, 0) for k, v in self.REASONS.items()}
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in bits.items():
+                    if bit and (r & bit):
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self.stop_ev.wait(0.002)
 
     def stop(self) -> dict:
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.flush()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
-        os.unlink(self.f.name)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            r = [x.strip() for x in r]
-            try:
-                sm.append(float(r[1]))
-                mx.append(float(r[2]))
-            except (ValueError, IndexError):
-                continue
-            for k, v in zip(names, r[5:9]):
-                if v.lower() == "active":
-                    reasons.add(k)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_ev.set()
+        self.t.join()
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "NVML, ~2 ms polling during the timed steps"}
 
 
 def measured_peaks():
@@ -270,10 +292,7 @@ def run_aimx(a):
     kernels_timed = prof.pop("kernels")
     op.profile_enable(False)
     total_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tmax = float(t.item())
+    tmax = max_over_ranks(total_ms)
     value = nf * world * a.steps / (tmax / 1e3)
 
     # matvec/s (secondary number: back-to-back matvecs at the first frequency)
@@ -291,10 +310,7 @@ def run_aimx(a):
     e1.record()
     torch.cuda.synchronize()
     mv_ms = e0.elapsed_time(e1) / nmv
-    mv = torch.tensor([mv_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(mv, op=dist.ReduceOp.MAX)
-    matvec_per_s = world * 1e3 / float(mv.item())
+    matvec_per_s = world * 1e3 / max_over_ranks(mv_ms)
 
     # end to end: the same sweep through the C ABI with HOST buffers (pinned)
     Xp = Xh.pin_memory()
@@ -309,10 +325,7 @@ def run_aimx(a):
         b0 = time.perf_counter()
         op.sweep_host(freqs, Xp, Yp)          # synchronises its stream before returning
         e2e_ms += 1e3 * (time.perf_counter() - b0)
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = nf * world * a.steps / (float(te.item()) / 1e3)
+    e2e_value = nf * world * a.steps / (max_over_ranks(e2e_ms) / 1e3)
     vec_bytes = op.N * (8 if prec == "c64" else 16)
 
     # roofline of the dominant stage
