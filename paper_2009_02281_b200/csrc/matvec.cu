@@ -91,11 +91,24 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
 #pragma unroll
     for (int c = 0; c < 4; ++c) a[v][c] = mk<T2>(0, 0);
   const T4* __restrict__ ew = (const T4*)h.ent_w;
-  const int e1 = h.node_ptr[q + 1];
-#pragma unroll 4
-  for (int e = h.node_ptr[q] + g; e < e1; e += NG) {
-    const T4 w = ew[e];
-    const VT u = *(const VT*)(xt + (int64_t)h.ent_rwg[e] * BB + b0);
+  const int e0 = h.node_ptr[q], e1 = h.node_ptr[q + 1];
+  for (int base = e0; base < e1; base += 32) {
+    // 32 entries loaded coalesced, then handed to the groups by shuffles
+    const int ee = base + lane;
+    const bool ok = ee < e1;
+    const int myr = ok ? h.ent_rwg[ee] : 0;
+    const T4 myw = ok ? ew[ee] : T4{0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 32; j += NG) {
+    const int src = j + g;
+    if (base + j >= e1) break;
+    T4 w;
+    w.x = __shfl_sync(0xffffffffu, myw.x, src);
+    w.y = __shfl_sync(0xffffffffu, myw.y, src);
+    w.z = __shfl_sync(0xffffffffu, myw.z, src);
+    w.w = __shfl_sync(0xffffffffu, myw.w, src);
+    const int rr = __shfl_sync(0xffffffffu, myr, src);
+    const VT u = *(const VT*)(xt + (int64_t)rr * BB + b0);
     T2 xv[V];
     if constexpr (V == 2) {
       xv[0] = mk<T2>(u.x, u.y);
@@ -109,6 +122,7 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
       a[v][1].x += w.y * xv[v].x; a[v][1].y += w.y * xv[v].y;
       a[v][2].x += w.z * xv[v].x; a[v][2].y += w.z * xv[v].y;
       a[v][3].x += w.w * xv[v].x; a[v][3].y += w.w * xv[v].y;
+    }
     }
   }
 #pragma unroll
@@ -317,13 +331,31 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   __builtin_assume(t < G::T);
-  T2 *tw, *xb;
-  pass_prologue<T, L>(tw, xb, (const T2*)h.twz_tab, line);
   const int W = 8 * h.Nx, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
   const ColTile ct = col_tile<T, L>(line, W);
+  const int b = blockIdx.z;
+  // prefetch this CTA's spectrum slab [rsub][kz][kx - kx0] into shared memory
+  // (cp.async, overlaps the column loads and the forward transform)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* hs = reinterpret_cast<T2*>(smem_raw) + L + (size_t)G::NL * G::XB;
+  const int nkx = ct.CW / 4, kx0 = (blockIdx.x * ct.CW) / 4;
+  {
+    const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
+    const int n = ct.RPC * L * nkx;
+    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      const int r = idx / (L * nkx), kz = (idx / nkx) % L, kxl = idx % nkx;
+      const int kyy = blockIdx.y * ct.RPC + r;
+      const int kyf = kyy <= Ny ? kyy : Ny2 - kyy;
+      const int kx = kx0 + kxl;
+      const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
+      const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
+      if (kyy < Ny2) cp_async(hs + idx, Hb + ((int64_t)kyf * (Nz + 1) + kzf) * (Nx + 1) + kxf);
+    }
+  }
+  T2 *tw, *xb;
+  pass_prologue<T, L>(tw, xb, (const T2*)h.twz_tab, line);
   const int ky = blockIdx.y * ct.RPC + ct.rsub;
   const bool act = ky < Ny2;
-  const int b = blockIdx.z;
   const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
   const int64_t zs = (int64_t)Ny2 * W;
   T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)(act ? ky : 0) * W + col;
@@ -337,19 +369,16 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
     else v[i] = mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
-  {  // spectrum multiply (octant [ky][kz][kx], 1/M folded into H)
-    const int kyf = ky <= Ny ? ky : Ny2 - ky;
-    const int kx = (int)(col >> 2);
-    const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
-    const T2* __restrict__ H = (const T2*)h.Hoct + b * h.sH + ((int64_t)(act ? kyf : 0) * (Nz + 1)) * (Nx + 1) + kxf;
+  cp_async_wait_all();
+  __syncthreads();
+  {  // spectrum multiply (slab in shared memory, 1/M folded into H)
+    const T2* hl = hs + (size_t)ct.rsub * L * nkx + (ct.w >> 2);
 #pragma unroll
     for (int i = 0; i < G::E; ++i) {
       const int kz = TwoLevel<G::R2, G::R1>::in_index(t, i);
-      const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
-      v[i] = cmul(v[i], __ldg(H + (int64_t)kzf * (Nx + 1)));
+      v[i] = cmul(v[i], hl[kz * nkx]);
     }
   }
-  __syncthreads();
   inv_fft_swapped<T2, L>(v, xb, tw, t);
   if (!act) return;
 #pragma unroll
@@ -468,24 +497,36 @@ __global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT
       aR[v].y += w.w * p3.y;
     }
   }
+  // near row: the warp loads 32 entries (col, C) coalesced per chunk, then
+  // each group takes every NG-th of them via shuffles, so the chunk's x-row
+  // loads are independent and issue back to back.
   const T2* __restrict__ cv = (const T2*)h.cval;
   const int kb = h.rowptr[m], ke = h.rowptr[m + 1];
-#pragma unroll 4
-  for (int kk = kb + g; kk < ke; kk += NG) {
-    const int n = h.col[kk];
-    const T2 c = cv[kk];
-    const VT u = *(const VT*)(xt + (int64_t)n * BB + b0);
-    T2 xv[V];
-    if constexpr (V == 2) {
-      xv[0] = mk<T2>(u.x, u.y);
-      xv[1] = mk<T2>(u.z, u.w);
-    } else {
-      xv[0] = u;
-    }
+  for (int base = kb; base < ke; base += 32) {
+    const int kk = base + lane;
+    const bool ok = kk < ke;
+    const int mycol = ok ? h.col[kk] : 0;
+    const T2 myc = ok ? cv[kk] : mk<T2>(0, 0);
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      aA[v].x += c.x * xv[v].x; aA[v].y += c.x * xv[v].y;
-      aR[v].x += c.y * xv[v].x; aR[v].y += c.y * xv[v].y;
+    for (int j = 0; j < 32; j += NG) {
+      const int src = j + g;
+      const int n = __shfl_sync(0xffffffffu, mycol, src);
+      T2 c;
+      c.x = __shfl_sync(0xffffffffu, myc.x, src);
+      c.y = __shfl_sync(0xffffffffu, myc.y, src);
+      const VT u = *(const VT*)(xt + (int64_t)n * BB + b0);   // entries past the row: c = 0
+      T2 xv[V];
+      if constexpr (V == 2) {
+        xv[0] = mk<T2>(u.x, u.y);
+        xv[1] = mk<T2>(u.z, u.w);
+      } else {
+        xv[0] = u;
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        aA[v].x += c.x * xv[v].x; aA[v].y += c.x * xv[v].y;
+        aR[v].x += c.y * xv[v].x; aR[v].y += c.y * xv[v].y;
+      }
     }
   }
 #pragma unroll
@@ -570,7 +611,8 @@ void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
 
 template <typename T, int L>
 void run_z(const HotDev& h, int B, cudaStream_t s) {
-  constexpr size_t sm = pass_smem<T, L>();
+  // + spectrum slab: NL lines x L / 4 complex (RPC * L * CW / 4)
+  constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
   dim3 g = col_grid<T, L>(8 * h.Nx, 2 * h.Ny, B);
   if (h.nzocc == h.Nz) {
     set_smem(k_zconv<T, L, true>, sm);
