@@ -231,6 +231,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   const int64_t per_freq = (int64_t)cs * (nS + 2 * nA + nB + nP + noct) + 2 * (int64_t)sizeof(double2) * noct;
   int slots = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)(1536ll << 20) / per_freq));
   if (const char* e = std::getenv("AIMX_BATCH")) slots = std::max(1, std::min(kMaxBatch, std::atoi(e)));
+  while (slots & (slots - 1)) slots &= slots - 1;   // power of two (batch buckets never exceed it)
   h.batch = slots;
   h.sS = nS; h.sA = nA; h.sB = nB; h.sP = nP; h.sH = noct;
   h.S = dalloc<char>(c, nS * slots * (int64_t)cs);
