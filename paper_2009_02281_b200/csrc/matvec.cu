@@ -448,78 +448,111 @@ __global__ void __launch_bounds__(256) k_interp_near1(HotDev h, const typename C
   }
 }
 
-// BB right-hand sides.  Lanes are (column b, re/im component): lane l reads
-// real number l of a 2*BB-real row, so every x row (xt[n][BB], batch-
-// interleaved) and every potential row (phi[node][channel][slot]) is ONE
-// coalesced load of 8*BB (c64) bytes.  32/(2 BB) entries are processed per
-// instruction.  The near entries (col, C_A, C_rho) of each 32-entry chunk are
-// staged through a per-warp shared buffer and read back as broadcasts.
+// BB right-hand sides (batch-interleaved xt[n * BB + b], phi[(lin * slots + b)
+// * 4 + c]): lane = (group g, columns b0..b0+V-1) with V complex per 16-byte
+// load; the 32/(BB/V) groups stride the stencil nodes and the near row, the
+// lanes of a group read one contiguous x row per near entry.
+template <typename T2, int V> struct VecT;
+template <> struct VecT<float2, 2> { using type = float4; };
+template <> struct VecT<double2, 1> { using type = double2; };
+
 template <typename T, int BB>
 __global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      typename CT<T>::T2* __restrict__ y0, Combine cb) {
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
-  constexpr int LPN = 2 * BB;           // lanes per entry
-  constexpr int NPI = 32 / LPN;         // entries per instruction
-  struct Ent { int col; T ca, cr; };
-  __shared__ Ent sent[8][32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int sub = lane / LPN, lb = lane % LPN;   // lb = 2 b + component
+  constexpr int V = sizeof(T2) == 8 ? 2 : 1;       // complex per 16-byte load
+  constexpr int LG = BB / V;                         // lanes per group
+  constexpr int NG = 32 / LG;                        // groups per warp
+  using VT = typename VecT<T2, V>::type;
+  const int lane = threadIdx.x & 31;
+  const int b0 = (lane % LG) * V, g = lane / LG;
   const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (m >= h.nb) return;
-  const T* __restrict__ xr = (const T*)xt;
-  const T* __restrict__ pr = (const T*)h.phi;
-  const int pb2 = 2 * h.batch;          // reals per (node, channel)
-  T aA = 0, aR = 0;
-  for (int sl = sub; sl < h.p3; sl += NPI) {
+  T2 aA[V], aR[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) { aA[v] = mk<T2>(0, 0); aR[v] = mk<T2>(0, 0); }
+  const int64_t ns = (int64_t)h.batch * 4;
+  for (int sl = g; sl < h.p3; sl += NG) {
     const int p = h.p;
     const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
     const int64_t lin = (int64_t)h.rwg_base[m] + i + (int64_t)h.Nx * (j + (int64_t)h.Ny * k);
     const T4 w = ((const T4*)h.lam)[(int64_t)m * h.p3 + sl];
-    const T* ph = pr + lin * 4 * pb2 + lb;
-    aA += w.x * ph[0] + w.y * ph[pb2] + w.z * ph[2 * pb2];
-    aR += w.w * ph[3 * pb2];
+    // phi[node][channel][slot]: a group's lanes read one contiguous channel row
+    const T2* phn = (const T2*)h.phi + lin * ns + b0;
+    T2 pv[4 * V];   // pv[4 v + c] = channel c of column b0 + v
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const VT u = *(const VT*)(phn + (int64_t)c * h.batch);
+      if constexpr (V == 2) {
+        pv[c] = mk<T2>(u.x, u.y);
+        pv[4 + c] = mk<T2>(u.z, u.w);
+      } else {
+        pv[c] = u;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const T2 p0 = pv[4 * v], p1 = pv[4 * v + 1], p2 = pv[4 * v + 2], p3 = pv[4 * v + 3];
+      aA[v].x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
+      aA[v].y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
+      aR[v].x += w.w * p3.x;
+      aR[v].y += w.w * p3.y;
+    }
   }
+  // near row: the warp loads 32 entries (col, C) coalesced per chunk, then
+  // each group takes every NG-th of them via shuffles, so the chunk's x-row
+  // loads are independent and issue back to back.
   const T2* __restrict__ cv = (const T2*)h.cval;
   const int kb = h.rowptr[m], ke = h.rowptr[m + 1];
-  Ent* se = sent[wib];
   for (int base = kb; base < ke; base += 32) {
     const int kk = base + lane;
-    Ent e;
-    if (kk < ke) {
-      const T2 c = cv[kk];
-      e.col = h.col[kk];
-      e.ca = c.x;
-      e.cr = c.y;
-    } else {
-      e.col = 0;
-      e.ca = 0;
-      e.cr = 0;
-    }
-    __syncwarp();
-    se[lane] = e;
-    __syncwarp();
-#pragma unroll 8
-    for (int jj = 0; jj < 32; jj += NPI) {
-      const Ent en = se[jj + sub];
-      const T xv = xr[(int64_t)en.col * LPN + lb];
-      aA += en.ca * xv;
-      aR += en.cr * xv;
+    const bool ok = kk < ke;
+    const int mycol = ok ? h.col[kk] : 0;
+    const T2 myc = ok ? cv[kk] : mk<T2>(0, 0);
+#pragma unroll
+    for (int j = 0; j < 32; j += NG) {
+      const int src = j + g;
+      const int n = __shfl_sync(0xffffffffu, mycol, src);
+      T2 c;
+      c.x = __shfl_sync(0xffffffffu, myc.x, src);
+      c.y = __shfl_sync(0xffffffffu, myc.y, src);
+      const VT u = *(const VT*)(xt + (int64_t)n * BB + b0);   // entries past the row: c = 0
+      T2 xv[V];
+      if constexpr (V == 2) {
+        xv[0] = mk<T2>(u.x, u.y);
+        xv[1] = mk<T2>(u.z, u.w);
+      } else {
+        xv[0] = u;
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        aA[v].x += c.x * xv[v].x; aA[v].y += c.x * xv[v].y;
+        aR[v].x += c.y * xv[v].x; aR[v].y += c.y * xv[v].y;
+      }
     }
   }
 #pragma unroll
-  for (int o = LPN; o < 32; o <<= 1) {
-    aA += __shfl_xor_sync(0xffffffffu, aA, o);
-    aR += __shfl_xor_sync(0xffffffffu, aR, o);
+  for (int o = LG; o < 32; o <<= 1) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      aA[v].x += __shfl_xor_sync(0xffffffffu, aA[v].x, o);
+      aA[v].y += __shfl_xor_sync(0xffffffffu, aA[v].y, o);
+      aR[v].x += __shfl_xor_sync(0xffffffffu, aR[v].x, o);
+      aR[v].y += __shfl_xor_sync(0xffffffffu, aR[v].y, o);
+    }
   }
-  // lanes (b, re) and (b, im) exchange to form the complex result
-  const T oA = __shfl_xor_sync(0xffffffffu, aA, 1);
-  const T oR = __shfl_xor_sync(0xffffffffu, aR, 1);
-  const int b = lb >> 1;
-  if (sub == 0 && (lb & 1) == 0 && b < cb.B) {
-    const T al = (T)cb.alpha_im[b], be = (T)cb.beta[b];
-    const T ux = aA - be * aR, uy = oA - be * oR;
-    y0[b * cb.ystride + m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
+  if (g == 0) {
+    using R = decltype(T2::x);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int b = b0 + v;
+      if (b < cb.B) {
+        const R al = (R)cb.alpha_im[b], be = (R)cb.beta[b];
+        const R ux = aA[v].x - be * aR[v].x, uy = aA[v].y - be * aR[v].y;
+        y0[b * cb.ystride + m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
+      }
+    }
   }
 }
 
