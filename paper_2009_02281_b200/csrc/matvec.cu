@@ -517,7 +517,12 @@ __global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT
       T2 c;
       c.x = __shfl_sync(0xffffffffu, myc.x, src);
       c.y = __shfl_sync(0xffffffffu, myc.y, src);
-      const VT u = *(const VT*)(xt + (int64_t)n * BB + b0);   // entries past the row: c = 0
+      // one load instruction per group: each touches a single 8*BB-byte row
+      // (a multi-line load costs ~2 L1 cycles per line, a single-line one 1)
+      VT u;
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg)
+        if (g == gg) u = *(const VT*)(xt + (int64_t)n * BB + b0);   // entries past the row: c = 0
       T2 xv[V];
       if constexpr (V == 2) {
         xv[0] = mk<T2>(u.x, u.y);

@@ -78,12 +78,45 @@ template <typename S, int L> struct EvGeom {
   static constexpr int NL = NT / T;
 };
 
-template <typename T, int L, bool ROW>
+// Kernel sample K(h |(i, j, l)|) of octant point (i = x, j = y, l = z); 0 on
+// wrap slots; K_s (STATIC) or K_d(k0) in fp64, rounded to T.
+template <typename T, bool STATIC>
+__device__ __forceinline__ typename CT<T>::T2 ksample(int i, int j, int l, int Nx, int Ny, int Nz,
+                                                      double h, double k0) {
+  using T2 = typename CT<T>::T2;
+  double re = 0.0, im = 0.0;
+  if (i < Nx && j < Ny && l < Nz) {
+    const int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
+    const double inv4pi = 1.0 / (4.0 * kPi);
+    if (STATIC) {
+      if (q > 0) re = inv4pi / (h * sqrt((double)q));
+    } else if (q == 0) {
+      im = -k0 * inv4pi;
+    } else {
+      const double r = h * sqrt((double)q);
+      double s, c;
+      sincos(0.5 * k0 * r, &s, &c);
+      re = -2.0 * s * s * inv4pi / r;
+      im = -2.0 * s * c * inv4pi / r;   // sin(x) = 2 sin(x/2) cos(x/2)
+    }
+  }
+  return mk<T2>((T)re, (T)im);
+}
+
+struct SampleArgs {
+  int Nx, Ny, Nz;
+  double h;
+  double k0[kMaxBatch];
+};
+
+// MODE 0: read `in`; MODE 1: generate dynamic samples K_d (row pass only).
+template <typename T, int L, bool ROW, int MODE = 0>
 __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int64_t noct,
                                               const typename CT<T>::T2* __restrict__ in,
                                               typename CT<T>::T2* __restrict__ out,
                                               const typename CT<T>::T2* __restrict__ twg,
-                                              const typename CT<T>::T2* __restrict__ add, T scale) {
+                                              const typename CT<T>::T2* __restrict__ add, T scale,
+                                              SampleArgs sa) {
   using T2 = typename CT<T>::T2;
   using G = EvGeom<T, L>;
   constexpr int N1 = L / 2 + 1;
@@ -110,11 +143,23 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
     stride = inner;
   }
   T2 v[G::E];
+  if (MODE == 1) {   // row pass over x: line lg = j (Nz+1) + l, element n = i
+    const int64_t lg = (int64_t)blockIdx.x * G::NL + line;
+    const int jj = (int)(lg / (sa.Nz + 1)), ll = (int)(lg % (sa.Nz + 1));
+    const double k0 = sa.k0[blockIdx.z];
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) {
-    int n = G::TL::in_index(t, i);
-    n = n <= L / 2 ? n : L - n;
-    v[i] = act ? in[base + n * stride] : mk<T2>(0, 0);
+    for (int i = 0; i < G::E; ++i) {
+      int n = G::TL::in_index(t, i);
+      n = n <= L / 2 ? n : L - n;
+      v[i] = act ? ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0) : mk<T2>(0, 0);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < G::E; ++i) {
+      int n = G::TL::in_index(t, i);
+      n = n <= L / 2 ? n : L - n;
+      v[i] = act ? in[base + n * stride] : mk<T2>(0, 0);
+    }
   }
   fft2<T2, G::R1, G::R2, false>(v, xb, tw, t);
   if (!act) return;
@@ -140,15 +185,23 @@ template <class K> void set_smem(K kernel, size_t bytes) {
 
 template <typename T>
 void even_rows(int L, int64_t nlines, int64_t noct, int B, const void* in, void* out, const void* tw,
-               cudaStream_t s) {
+               cudaStream_t s, const SampleArgs* gen = nullptr) {
   using T2 = typename CT<T>::T2;
+  SampleArgs sa{};
+  if (gen) sa = *gen;
   AIMX_SWITCH_L(L, ({
     using G = EvGeom<T, L>;
     const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
-    set_smem(k_even<T, L, true>, sm);
     dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
-    k_even<T, L, true><<<g, G::NT, sm, s>>>(nlines, 1, noct, (const T2*)in, (T2*)out, (const T2*)tw,
-                                            nullptr, (T)1);
+    if (gen) {
+      set_smem(k_even<T, L, true, 1>, sm);
+      k_even<T, L, true, 1><<<g, G::NT, sm, s>>>(nlines, 1, noct, nullptr, (T2*)out, (const T2*)tw,
+                                                 nullptr, (T)1, sa);
+    } else {
+      set_smem(k_even<T, L, true>, sm);
+      k_even<T, L, true><<<g, G::NT, sm, s>>>(nlines, 1, noct, (const T2*)in, (T2*)out, (const T2*)tw,
+                                              nullptr, (T)1, sa);
+    }
   }));
   AIMX_CHECK_LAUNCH();
 }
@@ -163,7 +216,7 @@ void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const v
     set_smem(k_even<T, L, false>, sm);
     dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
     k_even<T, L, false><<<g, G::NT, sm, s>>>(0, inner, noct, (const T2*)in, (T2*)out, (const T2*)tw,
-                                             (const T2*)add, scale);
+                                             (const T2*)add, scale, SampleArgs{});
   }));
   AIMX_CHECK_LAUNCH();
 }
@@ -171,9 +224,9 @@ void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const v
 // 3-D even-extension transform on the octant [B][y][z][x]: x rows, z cols, y cols.
 template <typename T>
 void dct3(SpectrumPlan& sp, int B, void** tw, void* a, void* b, void* out, const void* add, T scale,
-          cudaStream_t s) {
+          cudaStream_t s, const SampleArgs* gen = nullptr) {
   const int64_t nx = sp.Nx + 1, ny = sp.Ny + 1, nz = sp.Nz + 1, no = sp.noct;
-  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s);
+  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s, gen);
   even_cols<T>(2 * sp.Nz, ny, nx, no, B, b, a, tw[2], nullptr, (T)1, s);
   even_cols<T>(2 * sp.Ny, 1, nz * nx, no, B, a, out, tw[1], add, scale, s);
 }
@@ -228,23 +281,17 @@ void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s) {
 void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
                           float2* out, cudaStream_t s) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  K0s k{};
-  for (int b = 0; b < B; ++b) k.v[b] = k0[b];
-  k_sample<float, false><<<dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), 256, 0, s>>>(
-      sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (float2*)sp.work0);
-  AIMX_CHECK_LAUNCH();
-  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s);
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
+  for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
+  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s, &sa);
 }
 
 void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs,
                           double scale, double2* out, cudaStream_t s) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  K0s k{};
-  for (int b = 0; b < B; ++b) k.v[b] = k0[b];
-  k_sample<double, false><<<dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), 256, 0, s>>>(
-      sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (double2*)sp.work0);
-  AIMX_CHECK_LAUNCH();
-  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s);
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
+  for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
+  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s, &sa);
 }
 
 }  // namespace aimx
