@@ -108,6 +108,9 @@ typedef struct {
   int32_t order;
   double h;
   double origin[3];
+  int32_t near_group_rows;    /* R: rows per group of the near matrix's row-group layout */
+  int32_t near_row_order;     /* 0: rows ordered by anchor linear index, 1: by anchor Morton code */
+  int64_t near_union;         /* stored (column, group) entries; fill = nnz / (near_union * R) */
 } aimx_stats;
 
 /* S0 (the paper's "one-time static matrix-fill", tab:prof P:715): RWG basis,

@@ -49,7 +49,8 @@ class _Stats(C.Structure):
                 ("projection_entries", C.c_int64), ("device_bytes", C.c_int64), ("batch_slots", C.c_int64),
                 ("setup_seconds", C.c_double),
                 ("n", C.c_int32 * 3), ("order", C.c_int32), ("h", C.c_double),
-                ("origin", C.c_double * 3)]
+                ("origin", C.c_double * 3), ("near_group_rows", C.c_int32), ("near_row_order", C.c_int32),
+                ("near_union", C.c_int64)]
 
 
 _P = C.c_void_p
@@ -226,7 +227,9 @@ class AIMx:
                 "occupied_lines": s.occupied_lines, "occupied_planes": s.occupied_planes,
                 "projection_entries": s.projection_entries, "device_bytes": s.device_bytes,
                 "batch_slots": s.batch_slots, "setup_seconds": s.setup_seconds,
-                "n": tuple(s.n), "order": s.order, "h": s.h, "origin": tuple(s.origin)}
+                "n": tuple(s.n), "order": s.order, "h": s.h, "origin": tuple(s.origin),
+                "near_group_rows": s.near_group_rows, "near_row_order": s.near_row_order,
+                "near_union": s.near_union}
 
     STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
 

@@ -71,6 +71,33 @@ struct NodeMap {
 
 void build_nodemap(const Topology& t, const std::vector<uint8_t>& nz_slot, NodeMap& m);
 
+// Near matrix in row-group form (host_setup.cpp build_near_groups): groups of
+// R spatially ordered rows sharing one sorted column union.
+struct NearGroups {
+  int R = 8;
+  int order_kind = 0;              // 0: anchor linear index, 1: anchor Morton code
+  int64_t ngrp = 0;
+  std::vector<int32_t> rows;       // [ngrp][R] external row ids, -1 = padding
+  std::vector<int64_t> ptr;        // [ngrp+1] into ucol
+  std::vector<int32_t> ucol;       // [U] union columns (external ids), ascending per group
+  std::vector<int64_t> slot;       // [nnz] CSR entry k -> value slot u*R + r
+  std::vector<int64_t> wptr;       // [ngrp+1] into wnode
+  std::vector<int32_t> wnode;      // [Uw] union of the rows' stencil nodes (linear grid index)
+  std::vector<int64_t> wslot;      // [nb][p3] weight slot (w*R + r), -1 = exactly zero weight
+};
+
+void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, NearGroups& g);
+
+// Work list of the S4+S5 kernel: chunks {group, flags, begin, count} (flags:
+// bit0 = near (C) chunk, else interpolation (W) chunk; bit1 first, bit2 last
+// chunk of its group) and contiguous chunk ranges per CTA (whole groups).
+struct NearChunks {
+  std::vector<int32_t> chunks;     // [nchunk][4]
+  std::vector<int32_t> cta_ptr;    // [ncta+1]
+  int ncta = 0;
+};
+void build_near_chunks(const NearGroups& g, int chw, int chc, int ncta, NearChunks& ck);
+
 // ---------------------------------------------------------------- device setup (fp64)
 struct SetupDev {
   double* V = nullptr;        // [nv][3]
@@ -171,7 +198,6 @@ struct HotDev {
   int64_t sS = 0, sA = 0, sB = 0, sP = 0, sH = 0;
   // stencil / weights
   int32_t* rwg_base = nullptr;   // [nb] linear index of the stencil anchor node
-  void* lam = nullptr;           // [nb][p3] real4 (x,y,z,rho), compute precision
   int32_t* node_lin = nullptr;   // [nocc]
   int32_t* node_line = nullptr;  // [nocc] index of the node's line in line_id
   int32_t* node_ptr = nullptr;   // [nocc+1]
@@ -181,10 +207,17 @@ struct HotDev {
   int32_t* zplanes = nullptr;    // [nzocc]
   uint8_t* line_occ = nullptr;   // [Ny*Nz]
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
-  // near matrix (CSR, int32 offsets)
-  int32_t* rowptr = nullptr;
-  int32_t* col = nullptr;
-  void* cval = nullptr;          // [nnz] real2 (C_A, C_rho)
+  // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)
+  int R = 8;                     // rows per group
+  int ngrp = 0;
+  int32_t* grp_rows = nullptr;   // [ngrp][R]
+  int32_t* ucol = nullptr;       // [U]
+  void* gval = nullptr;          // [U][R] real2 (C_A, C_rho), zero where not near
+  int32_t* wnode = nullptr;      // [Uw] stencil-node unions (linear grid index)
+  void* wval = nullptr;          // [Uw][R] real4 weights (x, y, z, rho), zero off-stencil
+  int32_t* chunks = nullptr;     // [nchunk][4] NearChunks work list
+  int32_t* cta_ptr = nullptr;    // [near_ctas+1]
+  int near_ctas = 0;
   // grid buffers (complex, 4 channels innermost), `batch` slots each
   void* S = nullptr;             // [nlines][Nx][4] gathered grid sources
   void* bufA = nullptr;          // [Nz][Ny][2Nx][4]

@@ -32,6 +32,8 @@ struct aimx_ctx {
   void* stage = nullptr;        // sweep_host staging
   int64_t stage_bytes = 0;
   double setup_seconds = 0;
+  int near_R = 0, near_order = 0;
+  int64_t near_union = 0;
   Profiler prof;
   std::vector<void*> allocs;
   std::string last_error;
@@ -76,13 +78,15 @@ P* dupload(aimx_ctx* c, const std::vector<P>& v) {
 }
 
 // ---- small conversion kernels ------------------------------------------------------
+// weight (rwg, slot) i -> its row-group slot (exactly-zero weights have none)
 template <typename T4>
-__global__ void k_lam_to(int64_t n, const double* __restrict__ lam, T4* __restrict__ out) {
+__global__ void k_lam_to(int64_t n, const int64_t* __restrict__ slot, const double* __restrict__ lam,
+                         T4* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || slot[i] < 0) return;
   T4 v;
   v.x = lam[4 * i]; v.y = lam[4 * i + 1]; v.z = lam[4 * i + 2]; v.w = lam[4 * i + 3];
-  out[i] = v;
+  out[slot[i]] = v;
 }
 template <typename T4>
 __global__ void k_ent_w(int64_t n, int p3, const int32_t* __restrict__ er, const int32_t* __restrict__ es,
@@ -94,15 +98,16 @@ __global__ void k_ent_w(int64_t n, int p3, const int32_t* __restrict__ er, const
   v.x = l[0]; v.y = l[1]; v.z = l[2]; v.w = l[3];
   out[i] = v;
 }
+// CSR entry k of (C_A, C_rho) -> its row-group value slot
 template <typename T2>
-__global__ void k_pack_c(int64_t n, const double* __restrict__ CA, const double* __restrict__ CR,
-                         T2* __restrict__ out) {
+__global__ void k_pack_c(int64_t n, const int64_t* __restrict__ slot, const double* __restrict__ CA,
+                         const double* __restrict__ CR, T2* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   T2 v;
   v.x = CA[i];
   v.y = CR[i];
-  out[i] = v;
+  out[slot[i]] = v;
 }
 __global__ void k_d2f(int64_t n, const double2* __restrict__ a, float2* __restrict__ b) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -196,30 +201,56 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     for (int z : m.zplanes) zo[z] = 1;
     h.zocc = dupload(c, zo);
   }
-  std::vector<int32_t> rp32(nb + 1);
-  for (int64_t i = 0; i <= nb; ++i) rp32[i] = (int32_t)t.rowptr[i];
-  h.rowptr = dupload(c, rp32);
-  h.col = d.col;
+  // near matrix in row-group form (host ordering and unions; values scattered on device)
+  NearGroups grp;
+  build_near_groups(t, nz, grp);
+  if (grp.ptr.back() > (int64_t)INT32_MAX || grp.wptr.back() > (int64_t)INT32_MAX)
+    throw Error(AIMX_E_GRID, "near matrix too large");
+  h.R = grp.R;
+  h.ngrp = (int)grp.ngrp;
+  h.grp_rows = dupload(c, grp.rows);
+  h.ucol = dupload(c, grp.ucol);
+  h.wnode = dupload(c, grp.wnode);
+  int64_t* gslot = dupload(c, grp.slot);
+  int64_t* wslot = dupload(c, grp.wslot);
+  const int64_t nU = grp.ptr.back(), nUw = grp.wptr.back();
+  {
+    int nsm = 148;
+    AIMX_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    NearChunks ck;
+    const bool f32p = c->prec == AIMX_C64;
+    build_near_chunks(grp, f32p ? 16 : 8, f32p ? 64 : 32, 3 * nsm, ck);
+    h.chunks = dupload(c, ck.chunks);
+    h.cta_ptr = dupload(c, ck.cta_ptr);
+    h.near_ctas = ck.ncta;
+  }
+  c->near_R = grp.R;
+  c->near_order = grp.order_kind;
+  c->near_union = nU;
   const int64_t nent = (int64_t)m.ent_rwg.size();
   const int64_t ng = (int64_t)h.Nx * h.Ny * h.Nz;
   const bool f32 = c->prec == AIMX_C64;
   const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
   if (f32) {
-    h.lam = dalloc<float4>(c, nb * p3);
+    h.wval = dalloc<float4>(c, nUw * grp.R);
+    AIMX_CUDA(cudaMemsetAsync(h.wval, 0, nUw * grp.R * sizeof(float4), c->stream));
     h.ent_w = dalloc<float4>(c, nent);
-    h.cval = dalloc<float2>(c, nnz);
-    k_lam_to<float4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, d.lam, (float4*)h.lam);
+    h.gval = dalloc<float2>(c, nU * grp.R);
+    AIMX_CUDA(cudaMemsetAsync(h.gval, 0, nU * grp.R * sizeof(float2), c->stream));
+    k_lam_to<float4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (float4*)h.wval);
     k_ent_w<float4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)p3, h.ent_rwg, ent_slot, d.lam,
                                                       (float4*)h.ent_w);
-    k_pack_c<float2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, d.CA, d.CR, (float2*)h.cval);
+    k_pack_c<float2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (float2*)h.gval);
   } else {
-    h.lam = dalloc<double4>(c, nb * p3);
+    h.wval = dalloc<double4>(c, nUw * grp.R);
+    AIMX_CUDA(cudaMemsetAsync(h.wval, 0, nUw * grp.R * sizeof(double4), c->stream));
     h.ent_w = dalloc<double4>(c, nent);
-    h.cval = dalloc<double2>(c, nnz);
-    k_lam_to<double4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, d.lam, (double4*)h.lam);
+    h.gval = dalloc<double2>(c, nU * grp.R);
+    AIMX_CUDA(cudaMemsetAsync(h.gval, 0, nU * grp.R * sizeof(double2), c->stream));
+    k_lam_to<double4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (double4*)h.wval);
     k_ent_w<double4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)p3, h.ent_rwg, ent_slot, d.lam,
                                                        (double4*)h.ent_w);
-    k_pack_c<double2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, d.CA, d.CR, (double2*)h.cval);
+    k_pack_c<double2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (double2*)h.gval);
   }
   AIMX_CHECK_LAUNCH();
   // ---- batch slots and grid buffers
@@ -238,7 +269,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   h.bufA = dalloc<char>(c, nA * slots * (int64_t)cs);
   h.bufB = dalloc<char>(c, nB * slots * (int64_t)cs);
   h.bufC = dalloc<char>(c, nA * slots * (int64_t)cs);
-  h.phi = dalloc<char>(c, nP * slots * (int64_t)cs);
+  h.phi = dalloc<char>(c, nP * slots * (int64_t)cs + 64);   // + 64: 16-byte row blocks may overhang
   AIMX_CUDA(cudaMemsetAsync(h.S, 0, nS * slots * cs, c->stream));
   AIMX_CUDA(cudaMemsetAsync(h.bufA, 0, nA * slots * cs, c->stream));
   AIMX_CUDA(cudaMemsetAsync(h.bufB, 0, nB * slots * cs, c->stream));
@@ -268,7 +299,10 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     c->Hs_T = c->Hs;
   }
   h.Hoct = dalloc<char>(c, noct * slots * (int64_t)cs);
-  h.xt = dalloc<char>(c, (int64_t)nb * kMaxBatch * (int64_t)cs);
+  h.xt = dalloc<char>(c, (int64_t)nb * kMaxBatch * (int64_t)cs + 64);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  dfree(c, gslot, nnz * (int64_t)sizeof(int64_t));
+  dfree(c, wslot, nb * p3 * (int64_t)sizeof(int64_t));
   dfree(c, d.LA_un, nnz * sizeof(double));
   dfree(c, d.YR_un, nnz * sizeof(double));
   AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_spec, cudaEventDisableTiming));
@@ -302,6 +336,7 @@ void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
 
 Combine make_combine(int B, const double* f, int mode, int64_t nb) {
   Combine cb;
+  for (int b = 0; b < kMaxBatch; ++b) cb.alpha_im[b] = cb.beta[b] = 0.0;
   cb.B = B;
   cb.mode = mode;
   cb.xstride = nb;
@@ -535,6 +570,9 @@ aimx_status aimx_get_stats(const aimx_ctx* c, aimx_stats* o) {
   for (int a = 0; a < 3; ++a) { o->n[a] = c->topo.n[a]; o->origin[a] = c->topo.origin[a]; }
   o->order = c->topo.order;
   o->h = c->topo.h;
+  o->near_group_rows = c->near_R;
+  o->near_row_order = c->near_order;
+  o->near_union = c->near_union;
   return AIMX_OK;
 }
 

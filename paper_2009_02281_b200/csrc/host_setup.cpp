@@ -8,6 +8,7 @@
 // time so that anchors are reproducible bit for bit.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -272,6 +273,211 @@ void build_nodemap(const Topology& t, const std::vector<uint8_t>& nz_slot, NodeM
   m.ent_rwg.swap(er);
   m.ent_slot.swap(es);
   (void)Nz;
+}
+
+}  // namespace aimx
+
+namespace aimx {
+
+// ---- near matrix in row-group form (hot-path layout of C) ----
+// Rows (testing RWGs) are ordered spatially by their stencil anchor and cut
+// into groups of R consecutive rows.  A group stores the sorted union of its
+// rows' near columns once; each union entry carries R (C_A, C_rho) pairs, zero
+// where the pair (row, column) is not near.  A column's x values are then read
+// once for R rows.  Near-ness depends only on the anchors (reading R5), so rows
+// with close anchors have nearly equal column sets.
+
+static uint32_t spread3(uint32_t v) {   // 10 bits -> every third bit
+  v &= 0x3ff;
+  v = (v | (v << 16)) & 0x030000ff;
+  v = (v | (v << 8)) & 0x0300f00f;
+  v = (v | (v << 4)) & 0x030c30c3;
+  v = (v | (v << 2)) & 0x09249249;
+  return v;
+}
+
+static std::vector<int32_t> row_order(const Topology& t, int kind) {
+  const int64_t nb = t.nb;
+  std::vector<int64_t> key(nb);
+  for (int64_t e = 0; e < nb; ++e) {
+    const int32_t* A = &t.anchor[3 * e];
+    key[e] = kind == 0 ? (int64_t)A[0] + (int64_t)t.n[0] * ((int64_t)A[1] + (int64_t)t.n[1] * A[2])
+                       : (int64_t)(spread3(A[0]) | (spread3(A[1]) << 1) | (spread3(A[2]) << 2));
+  }
+  std::vector<int32_t> p(nb);
+  std::iota(p.begin(), p.end(), 0);
+  std::stable_sort(p.begin(), p.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+  return p;
+}
+
+static void group_union(const Topology& t, const std::vector<int32_t>& p, int64_t g, int R,
+                        std::vector<int32_t>& u) {
+  u.clear();
+  const int64_t nb = t.nb;
+  for (int r = 0; r < R; ++r) {
+    const int64_t i = g * R + r;
+    if (i >= nb) break;
+    const int32_t m = p[i];
+    u.insert(u.end(), t.col.begin() + t.rowptr[m], t.col.begin() + t.rowptr[m + 1]);
+  }
+  std::sort(u.begin(), u.end());
+  u.erase(std::unique(u.begin(), u.end()), u.end());
+}
+
+void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, NearGroups& ng) {
+  const int64_t nb = t.nb;
+  // candidate (ordering, R): union sizes estimated on a sample of groups, cost
+  // model = HBM bytes + FMA issue + x-row loads of a 16-column c64 SpMM
+  int best_kind = 0, best_R = 8;
+  double best = 1e300;
+  const char* eR = std::getenv("AIMX_NEAR_R");
+  const char* eK = std::getenv("AIMX_NEAR_ORDER");
+  std::vector<int32_t> perm[2] = {row_order(t, 0), row_order(t, 1)};
+  for (int kind = 0; kind < 2; ++kind) {
+    if (eK && std::atoi(eK) != kind) continue;
+    for (int R : {4, 8}) {
+      if (eR && std::atoi(eR) != R) continue;
+      const int64_t ngrp = (nb + R - 1) / R;
+      const int64_t stride = std::max<int64_t>(1, ngrp / 4096);
+      int64_t U = 0, ns = 0;
+#pragma omp parallel reduction(+ : U, ns)
+      {
+        std::vector<int32_t> u;
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t g = 0; g < ngrp; g += stride) {
+          group_union(t, perm[kind], g, R, u);
+          U += (int64_t)u.size();
+          ns += 1;
+        }
+      }
+      const double Ue = (double)U * (double)ngrp / (double)std::max<int64_t>(ns, 1);
+      const double cost = Ue * (4.0 + 8.0 * R) / 6.0 + Ue * R * 48.0 / 18.0 + Ue * 128.0 / 18.0;
+      if (cost < best) { best = cost; best_kind = kind; best_R = R; }
+    }
+  }
+  const int R = best_R;
+  const std::vector<int32_t>& p = perm[best_kind];
+  const int64_t ngrp = (nb + R - 1) / R;
+  const int Nx = t.n[0], Ny = t.n[1], pp = t.p, p3 = t.p3;
+  ng.R = R;
+  ng.order_kind = best_kind;
+  ng.ngrp = ngrp;
+  ng.rows.assign(ngrp * R, -1);
+  for (int64_t i = 0; i < nb; ++i) ng.rows[i] = p[i];
+  // stencil node (linear grid index) of slot s of RWG e
+  auto node_of = [&](int64_t e, int sl) -> int32_t {
+    const int32_t* A = &t.anchor[3 * e];
+    return (A[0] + sl % pp) + Nx * ((A[1] + (sl / pp) % pp) + Ny * (A[2] + sl / (pp * pp)));
+  };
+  auto w_union = [&](int64_t g, std::vector<int32_t>& u) {
+    u.clear();
+    for (int r = 0; r < R; ++r) {
+      const int64_t i = g * R + r;
+      if (i >= nb) break;
+      const int32_t m = p[i];
+      for (int sl = 0; sl < p3; ++sl)
+        if (nz_slot[(int64_t)m * p3 + sl]) u.push_back(node_of(m, sl));
+    }
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+  };
+  ng.ptr.assign(ngrp + 1, 0);
+  ng.wptr.assign(ngrp + 1, 0);
+#pragma omp parallel
+  {
+    std::vector<int32_t> u;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t g = 0; g < ngrp; ++g) {
+      group_union(t, p, g, R, u);
+      ng.ptr[g + 1] = (int64_t)u.size();
+      w_union(g, u);
+      ng.wptr[g + 1] = (int64_t)u.size();
+    }
+  }
+  // unions padded to a multiple of 4 entries (16-byte aligned index blocks;
+  // padding entries carry zero coefficients)
+  for (int64_t g = 0; g < ngrp; ++g) {
+    ng.ptr[g + 1] = ng.ptr[g] + ((ng.ptr[g + 1] + 3) & ~(int64_t)3);
+    ng.wptr[g + 1] = ng.wptr[g] + ((ng.wptr[g + 1] + 3) & ~(int64_t)3);
+  }
+  const int64_t U = ng.ptr[ngrp], Uw = ng.wptr[ngrp];
+  if (U * R > (int64_t)INT32_MAX * 4) throw Error(AIMX_E_GRID, "near matrix too large for the row-group layout");
+  ng.ucol.resize(U);
+  ng.slot.resize(t.rowptr[nb]);
+  ng.wnode.resize(Uw);
+  ng.wslot.assign(nb * p3, -1);
+#pragma omp parallel
+  {
+    std::vector<int32_t> u;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t g = 0; g < ngrp; ++g) {
+      group_union(t, p, g, R, u);
+      const int64_t u0 = ng.ptr[g];
+      std::copy(u.begin(), u.end(), ng.ucol.begin() + u0);
+      std::fill(ng.ucol.begin() + u0 + (int64_t)u.size(), ng.ucol.begin() + ng.ptr[g + 1], u.empty() ? 0 : u[0]);
+      for (int r = 0; r < R; ++r) {
+        const int64_t i = g * R + r;
+        if (i >= nb) break;
+        const int32_t m = p[i];
+        size_t pos = 0;
+        for (int64_t k = t.rowptr[m]; k < t.rowptr[m + 1]; ++k) {   // both sorted: two pointers
+          while (u[pos] != t.col[k]) ++pos;
+          ng.slot[k] = (u0 + (int64_t)pos) * R + r;
+        }
+      }
+      w_union(g, u);
+      const int64_t w0 = ng.wptr[g];
+      std::copy(u.begin(), u.end(), ng.wnode.begin() + w0);
+      std::fill(ng.wnode.begin() + w0 + (int64_t)u.size(), ng.wnode.begin() + ng.wptr[g + 1], u.empty() ? 0 : u[0]);
+      for (int r = 0; r < R; ++r) {
+        const int64_t i = g * R + r;
+        if (i >= nb) break;
+        const int32_t m = p[i];
+        for (int sl = 0; sl < p3; ++sl)
+          if (nz_slot[(int64_t)m * p3 + sl]) {
+            const int64_t pos = std::lower_bound(u.begin(), u.end(), node_of(m, sl)) - u.begin();
+            ng.wslot[(int64_t)m * p3 + sl] = (w0 + pos) * R + r;
+          }
+      }
+    }
+  }
+}
+
+void build_near_chunks(const NearGroups& ng, int chw, int chc, int ncta, NearChunks& ck) {
+  // chunk list in group order: the group's W (interpolation) chunks, then its
+  // C (near) chunks; every group gets at least one chunk (its epilogue).
+  ck.chunks.clear();
+  std::vector<int64_t> gfirst(ng.ngrp + 1);
+  std::vector<double> cost(ng.ngrp);
+  for (int64_t g = 0; g < ng.ngrp; ++g) {
+    gfirst[g] = (int64_t)ck.chunks.size() / 4;
+    const int64_t n0 = ck.chunks.size();
+    for (int kind = 0; kind < 2; ++kind) {
+      const int64_t b = kind ? ng.ptr[g] : ng.wptr[g], e = kind ? ng.ptr[g + 1] : ng.wptr[g + 1];
+      const int ch = kind ? chc : chw;
+      for (int64_t u = b; u < e; u += ch) {
+        ck.chunks.insert(ck.chunks.end(), {(int32_t)g, kind, (int32_t)u, (int32_t)std::min<int64_t>(ch, e - u)});
+      }
+    }
+    if ((int64_t)ck.chunks.size() == n0) ck.chunks.insert(ck.chunks.end(), {(int32_t)g, 1, 0, 0});
+    ck.chunks[n0 + 1] |= 2;                          // first chunk of the group
+    ck.chunks[ck.chunks.size() - 3] |= 4;            // last chunk of the group
+    cost[g] = 4.0 * (ng.wptr[g + 1] - ng.wptr[g]) + (ng.ptr[g + 1] - ng.ptr[g]) + 32.0;
+  }
+  gfirst[ng.ngrp] = (int64_t)ck.chunks.size() / 4;
+  // contiguous group ranges per CTA, balanced by cost
+  ncta = (int)std::max<int64_t>(1, std::min<int64_t>(ncta, ng.ngrp));
+  double total = 0;
+  for (double c : cost) total += c;
+  ck.cta_ptr.assign(ncta + 1, 0);
+  int64_t g = 0;
+  double acc = 0;
+  for (int k = 0; k < ncta; ++k) {
+    const double target = total * (k + 1) / ncta;
+    while (g < ng.ngrp && (acc + 0.5 * cost[g] <= target || k == ncta - 1)) acc += cost[g++];
+    ck.cta_ptr[k + 1] = (int32_t)gfirst[g];
+  }
+  ck.ncta = ncta;
 }
 
 }  // namespace aimx

@@ -390,175 +390,334 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
 }
 
 // ------------------------------------------------------------------ S4 + S5
-template <typename T2> __device__ __forceinline__ T2 warp_sum(T2 v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
-  }
-  return v;
-}
-
-// Single right-hand side: lanes stride the stencil nodes and the near row.
-template <typename T>
-__global__ void __launch_bounds__(256) k_interp_near1(HotDev h, const typename CT<T>::T2* __restrict__ x,
-                                                      typename CT<T>::T2* __restrict__ y0,
-                                                      typename CT<T>::T2* __restrict__ y1, Combine cb) {
-  using T2 = typename CT<T>::T2;
-  using T4 = typename CT<T>::T4;
-  const int lane = threadIdx.x & 31;
-  const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (m >= h.nb) return;
-  T2 aA = mk<T2>(0, 0), aR = mk<T2>(0, 0);
-  for (int sl = lane; sl < h.p3; sl += 32) {
-    const int p = h.p;
-    const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
-    const int64_t lin = (int64_t)h.rwg_base[m] + i + (int64_t)h.Nx * (j + (int64_t)h.Ny * k);
-    const T4 w = ((const T4*)h.lam)[(int64_t)m * h.p3 + sl];
-    const T2* ph = (const T2*)h.phi + lin * h.batch * 4;   // [node][channel][slot], slot 0
-    const int pb = h.batch;
-    const T2 p0 = ph[0], p1 = ph[pb], p2 = ph[2 * pb], p3 = ph[3 * pb];
-    aA.x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
-    aA.y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
-    aR.x += w.w * p3.x;
-    aR.y += w.w * p3.y;
-  }
-  const T2* __restrict__ cv = (const T2*)h.cval;
-  const int kb = h.rowptr[m], ke = h.rowptr[m + 1];
-#pragma unroll 4
-  for (int kk = kb + lane; kk < ke; kk += 32) {
-    const int n = h.col[kk];
-    const T2 c = cv[kk];
-    const T2 xv = x[n];
-    aA.x += c.x * xv.x; aA.y += c.x * xv.y;
-    aR.x += c.y * xv.x; aR.y += c.y * xv.y;
-  }
-  aA = warp_sum(aA);
-  aR = warp_sum(aR);
-  if (lane == 0) {
-    using R = decltype(T2::x);
-    if (cb.mode == 0) {
-      const R al = (R)cb.alpha_im[0], be = (R)cb.beta[0];
-      const R ux = aA.x - be * aR.x, uy = aA.y - be * aR.y;
-      y0[m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
-    } else {
-      if (y0) y0[m] = aA;
-      if (y1) y1[m] = mk<T2>(-aR.x, -aR.y);
-    }
-  }
-}
-
-// BB right-hand sides (batch-interleaved xt[n * BB + b], phi[(lin * slots + b)
-// * 4 + c]): lane = (group g, columns b0..b0+V-1) with V complex per 16-byte
-// load; the 32/(BB/V) groups stride the stencil nodes and the near row, the
-// lanes of a group read one contiguous x row per near entry.
+// Row groups (NearGroups): R spatially ordered testing functions share one
+// sorted union of their stencil nodes (interpolation W = P^T) and one
+// sorted union of their near columns (C = L_s,NR - L_s,P, eq:LAIMx P:283);
+// each union entry carries R coefficient tuples, so a potential row (4
+// channels x BB columns) or an x row (BB columns) is read once for R rows.
+//
+// One CTA walks a contiguous range of whole groups as a stream of chunks
+// (NearChunks): per group its W (interpolation) chunks, then its C (near)
+// chunks.  The dense coefficient blocks -- the HBM stream -- are moved by the
+// TMA bulk-copy engine into a ring of D+1 shared-memory stages, D chunks ahead,
+// completion tracked by one mbarrier per stage; the row indices (two D ahead)
+// and chunk descriptors (three D ahead) ride on the same barriers.  The
+// gathered rows -- x rows (C) and potential rows (W), L2-resident -- are
+// loaded straight into registers one chunk ahead (ping-pong register buffers),
+// so their latency overlaps the previous chunk's arithmetic.  Lanes: group g of
+// LG lanes covers V columns per lane (16-byte loads); the NLG lane groups of
+// the CTA stride the chunk's entries.  At a group's last chunk the partial sums
+// are reduced in a fixed order (shuffles within the warp, then shared memory)
+// and combined: y = -j w mu0 (y^A - k0^-2 y^rho) (eq:EFIEAIMx P:288), or the
+// unscaled parts y^A and -y^rho (PARTS).
 template <typename T2, int V> struct VecT;
+template <> struct VecT<float2, 1> { using type = float2; };
 template <> struct VecT<float2, 2> { using type = float4; };
 template <> struct VecT<double2, 1> { using type = double2; };
 
-template <typename T, int BB>
-__global__ void __launch_bounds__(256) k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
-                                                     typename CT<T>::T2* __restrict__ y0, Combine cb) {
+// acc += s * x for a complex x and a real s: one packed FFMA2 (fma.rn.f32x2,
+// sm_100) in fp32 with s broadcast, two DFMA in fp64.
+__device__ __forceinline__ unsigned long long f2_as_u64(const float2& v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 u64_as_f2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ float2 fma2(const float2& a, const float2& b, const float2& c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)), "l"(f2_as_u64(c)));
+  return u64_as_f2(r);
+}
+__device__ __forceinline__ void axpy(float2& acc, float s, const float2& x) { acc = fma2(make_float2(s, s), x, acc); }
+__device__ __forceinline__ void axpy(double2& acc, double s, const double2& x) {
+  acc.x = fma(s, x.x, acc.x);
+  acc.y = fma(s, x.y, acc.y);
+}
+
+template <typename T, int R, int BB, bool PARTS> struct NearCfg {
+  using T2 = typename CT<T>::T2;
+  static constexpr int NT = 128;                      // threads per CTA
+  static constexpr int S = (int)sizeof(T2);           // complex bytes
+  static constexpr int CHC = 512 / S, CHW = 128 / S;  // entries per C / W chunk
+  static constexpr int COEFB = CHC * R * S;           // stage bytes (C: R pairs; W: R real4 = 2 S per entry)
+  static constexpr int D = 3;                         // pipeline depth (chunks)
+  static constexpr int NDS = D + 1, NIS = 2 * D, NDD = 3 * D + 1;   // stage / index / descriptor slots
+  static constexpr int V = (S == 8 && BB >= 2) ? 2 : 1;
+  static constexpr int LG = BB / V, NG = 32 / LG, NLG = (NT / 32) * NG;
+  static constexpr int NPC = (CHC + NLG - 1) / NLG;   // C entries per lane group per chunk (<= 4)
+  static constexpr bool WACT = CHW <= NLG;            // W: one entry per lane group
+  static_assert(NPC <= 4 && WACT, "row prefetch buffer holds 4 loads");
+  static constexpr int NA = (PARTS ? 2 : 1) * R * V;  // complex accumulators: [part][r][v]
+  static constexpr int NV = 2 * NA;                   // as reals
+  // partial sums: per lane (NG > 4) or, after a shuffle reduction over the
+  // warp's NG lane groups, per (warp, lane of group 0)
+  static constexpr bool SHFL = NG <= 4;
+  static constexpr size_t REDB = (size_t)(SHFL ? (NT / 32) * LG : NT) * (NV + 1) * sizeof(T);
+  static constexpr size_t OFF_RED = (size_t)NDS * COEFB;
+  static constexpr size_t OFF_IDX = (OFF_RED + REDB + 15) / 16 * 16;
+  static constexpr size_t OFF_DESC = OFF_IDX + (size_t)NIS * CHC * 4;
+  static constexpr size_t OFF_BAR = OFF_DESC + NDD * 16;
+  static constexpr size_t SMEM = OFF_BAR + NDS * 8;
+};
+
+// ---- mbarrier + bulk-copy (TMA engine) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// global -> shared bulk copy (bytes: multiple of 16, both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <typename T2, int V>
+__device__ __forceinline__ void unpack(const typename VecT<T2, V>::type& u, T2* out) {
+  if constexpr (V == 2) {
+    out[0] = mk<T2>(u.x, u.y);
+    out[1] = mk<T2>(u.z, u.w);
+  } else {
+    out[0] = u;
+  }
+}
+
+template <typename T, int R, int BB, bool PARTS>
+__global__ void __launch_bounds__(128) k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
+                                                     typename CT<T>::T2* __restrict__ y0,
+                                                     typename CT<T>::T2* __restrict__ y1, Combine cb) {
+  using K = NearCfg<T, R, BB, PARTS>;
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
-  constexpr int V = sizeof(T2) == 8 ? 2 : 1;       // complex per 16-byte load
-  constexpr int LG = BB / V;                         // lanes per group
-  constexpr int NG = 32 / LG;                        // groups per warp
-  using VT = typename VecT<T2, V>::type;
-  const int lane = threadIdx.x & 31;
-  const int b0 = (lane % LG) * V, g = lane / LG;
-  const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (m >= h.nb) return;
-  T2 aA[V], aR[V];
+  using VT = typename VecT<T2, K::V>::type;
+  constexpr int NT = K::NT, V = K::V, LG = K::LG, NG = K::NG, NLG = K::NLG, NV = K::NV, NA = K::NA;
+  constexpr int D = K::D, CHC = K::CHC, NPC = K::NPC;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* const sdata = smem;                                         // [NDS][COEFB]
+  T* const red = reinterpret_cast<T*>(smem + K::OFF_RED);                    // partial sums
+  int* const sidx = reinterpret_cast<int*>(smem + K::OFF_IDX);               // [NIS][CHC]
+  int4* const sdesc = reinterpret_cast<int4*>(smem + K::OFF_DESC);           // [NDD]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);      // [NDS]
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  const int b0 = (lane % LG) * V, g = lane / LG, lgid = wib * NG + g;
+  const int c0 = h.cta_ptr[blockIdx.x], nch = h.cta_ptr[blockIdx.x + 1] - c0;
+  if (nch <= 0) return;
+  const int4* __restrict__ chunks = reinterpret_cast<const int4*>(h.chunks) + c0;
+  const int64_t ns = (int64_t)h.batch * 4;        // phi node stride (complex): [node][channel][slot]
+  const T2* __restrict__ phi = (const T2*)h.phi + b0;
+  const T2* __restrict__ xr = xt + b0;
+  T be[V];
 #pragma unroll
-  for (int v = 0; v < V; ++v) { aA[v] = mk<T2>(0, 0); aR[v] = mk<T2>(0, 0); }
-  const int64_t ns = (int64_t)h.batch * 4;
-  for (int sl = g; sl < h.p3; sl += NG) {
-    const int p = h.p;
-    const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
-    const int64_t lin = (int64_t)h.rwg_base[m] + i + (int64_t)h.Nx * (j + (int64_t)h.Ny * k);
-    const T4 w = ((const T4*)h.lam)[(int64_t)m * h.p3 + sl];
-    // phi[node][channel][slot]: a group's lanes read one contiguous channel row
-    const T2* phn = (const T2*)h.phi + lin * ns + b0;
-    T2 pv[4 * V];   // pv[4 v + c] = channel c of column b0 + v
+  for (int v = 0; v < V; ++v) be[v] = PARTS ? T(0) : (T)cb.beta[b0 + v];   // 0 for b >= B
+  T2 acc[NA];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const VT u = *(const VT*)(phn + (int64_t)c * h.batch);
-      if constexpr (V == 2) {
-        pv[c] = mk<T2>(u.x, u.y);
-        pv[4 + c] = mk<T2>(u.z, u.w);
+  for (int i = 0; i < NA; ++i) acc[i] = mk<T2>(0, 0);
+  const T2 nbe2 = mk<T2>(-be[0], V == 2 ? -be[V - 1] : T(0));   // (-beta_b0, -beta_b0+1)
+
+  auto get_desc = [&](int j) -> int4 { return j < nch ? sdesc[j % K::NDD] : make_int4(0, 0, 0, 0); };
+  // bulk copies of chunk j's coefficient block (stage j % NDS), plus chunk
+  // ji's row indices and chunk jd's descriptor, all on bar[j % NDS]
+  auto issue = [&](int j, int ji, int jd) {
+    if (tid != 0 || j >= nch) return;
+    const int4 d = get_desc(j);
+    uint64_t* bj = bar + j % K::NDS;
+    const uint32_t cbytes = (uint32_t)d.w * R * ((d.y & 1) ? K::S : 2 * K::S);
+    const int4 di = get_desc(ji);
+    const uint32_t ibytes = ji < nch ? (uint32_t)di.w * 4 : 0;
+    const uint32_t dbytes = jd < nch ? 16 : 0;
+    mbar_arrive_expect_tx(bj, cbytes + ibytes + dbytes);
+    if (cbytes)
+      bulk_g2s(sdata + (j % K::NDS) * K::COEFB,
+               (d.y & 1) ? (const char*)h.gval + (int64_t)d.z * R * K::S
+                         : (const char*)h.wval + (int64_t)d.z * R * 2 * K::S,
+               cbytes, bj);
+    if (ibytes) bulk_g2s(sidx + (ji % K::NIS) * CHC, ((di.y & 1) ? h.ucol : h.wnode) + di.z, ibytes, bj);
+    if (dbytes) bulk_g2s(sdesc + jd % K::NDD, chunks + jd, 16, bj);
+  };
+  // gathered rows of chunk j into registers: C: x rows of entries
+  // lgid + i NLG (i < NPC); W: the 4 channel rows of entry lgid
+  auto load_rows = [&](int j, VT* buf) {
+    const int4 d = get_desc(j);
+    const int* ix = sidx + (j % K::NIS) * CHC;
+    if (d.y & 1) {
+#pragma unroll
+      for (int i = 0; i < NPC; ++i) {
+        const int e = lgid + i * NLG;
+        if (e < d.w) buf[i] = __ldg((const VT*)(xr + (int64_t)ix[e] * BB));
+      }
+    } else if (lgid < d.w) {
+      const T2* pr = phi + (int64_t)ix[lgid] * ns;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) buf[c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
+    }
+  };
+  auto compute = [&](int k, const VT* buf) {
+    const int4 d = get_desc(k);
+    const unsigned char* stg = sdata + (k % K::NDS) * K::COEFB;
+    if (d.y & 1) {   // near correction: pairs [e][R]
+      const T2* __restrict__ cf = (const T2*)stg;
+#pragma unroll
+      for (int i = 0; i < NPC; ++i) {
+        const int e = lgid + i * NLG;
+        if (e >= d.w) break;
+        T2 xv[V];
+        unpack<T2, V>(buf[i], xv);
+        T2 cv[R];
+        if constexpr (K::S == 8) {
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) {
+            const float4 f = reinterpret_cast<const float4*>(cf + e * R)[q];
+            cv[2 * q] = mk<T2>(f.x, f.y);
+            cv[2 * q + 1] = mk<T2>(f.z, f.w);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) cv[r] = cf[e * R + r];
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if constexpr (PARTS) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              axpy(acc[r * V + v], cv[r].x, xv[v]);
+              axpy(acc[(R + r) * V + v], cv[r].y, xv[v]);
+            }
+          } else if constexpr (K::S == 8 && V == 2) {
+            // (ce_0, ce_1) = C_A - beta_b C_rho for both columns: one FFMA2
+            const T2 ce = fma2(nbe2, mk<T2>(cv[r].y, cv[r].y), mk<T2>(cv[r].x, cv[r].x));
+            axpy(acc[r * V], ce.x, xv[0]);
+            axpy(acc[r * V + 1], ce.y, xv[1]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) axpy(acc[r * V + v], cv[r].x - be[v] * cv[r].y, xv[v]);
+          }
+        }
+      }
+    } else if (lgid < d.w) {   // interpolation: weights [e][R] real4
+      const T4* __restrict__ wf = (const T4*)stg + lgid * R;
+      T2 pv[4][V];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) unpack<T2, V>(buf[c], pv[c]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const T4 w = wf[r];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          T2& a = acc[r * V + v];
+          axpy(a, w.x, pv[0][v]);
+          axpy(a, w.y, pv[1][v]);
+          axpy(a, w.z, pv[2][v]);
+          if constexpr (PARTS) axpy(acc[(R + r) * V + v], w.w, pv[3][v]);
+          else axpy(a, -be[v] * w.w, pv[3][v]);
+        }
+      }
+    }
+    if (d.y & 4) {   // last chunk of group d.x: fixed-order reduction + combine
+      int nsrc;      // partial-sum rows per output lane
+      if constexpr (K::SHFL) {
+#pragma unroll
+        for (int o = LG; o < 32; o <<= 1)
+#pragma unroll
+          for (int i = 0; i < NA; ++i) {
+            acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, o);
+            acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, o);
+          }
+        if (g == 0)
+#pragma unroll
+          for (int i = 0; i < NA; ++i) {
+            red[(wib * LG + lane) * (NV + 1) + 2 * i] = acc[i].x;
+            red[(wib * LG + lane) * (NV + 1) + 2 * i + 1] = acc[i].y;
+          }
+        nsrc = NT / 32;
       } else {
-        pv[c] = u;
-      }
-    }
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const T2 p0 = pv[4 * v], p1 = pv[4 * v + 1], p2 = pv[4 * v + 2], p3 = pv[4 * v + 3];
-      aA[v].x += w.x * p0.x + w.y * p1.x + w.z * p2.x;
-      aA[v].y += w.x * p0.y + w.y * p1.y + w.z * p2.y;
-      aR[v].x += w.w * p3.x;
-      aR[v].y += w.w * p3.y;
-    }
-  }
-  // near row: the warp loads 32 entries (col, C) coalesced per chunk, then
-  // each group takes every NG-th of them via shuffles, so the chunk's x-row
-  // loads are independent and issue back to back.
-  const T2* __restrict__ cv = (const T2*)h.cval;
-  const int kb = h.rowptr[m], ke = h.rowptr[m + 1];
-  for (int base = kb; base < ke; base += 32) {
-    const int kk = base + lane;
-    const bool ok = kk < ke;
-    const int mycol = ok ? h.col[kk] : 0;
-    const T2 myc = ok ? cv[kk] : mk<T2>(0, 0);
-#pragma unroll
-    for (int j = 0; j < 32; j += NG) {
-      const int src = j + g;
-      const int n = __shfl_sync(0xffffffffu, mycol, src);
-      T2 c;
-      c.x = __shfl_sync(0xffffffffu, myc.x, src);
-      c.y = __shfl_sync(0xffffffffu, myc.y, src);
-      // one load instruction per group: each touches a single 8*BB-byte row
-      // (a multi-line load costs ~2 L1 cycles per line, a single-line one 1)
-      VT u;
-#pragma unroll
-      for (int gg = 0; gg < NG; ++gg)
-        if (g == gg) u = *(const VT*)(xt + (int64_t)n * BB + b0);   // entries past the row: c = 0
-      T2 xv[V];
-      if constexpr (V == 2) {
-        xv[0] = mk<T2>(u.x, u.y);
-        xv[1] = mk<T2>(u.z, u.w);
-      } else {
-        xv[0] = u;
+        for (int i = 0; i < NA; ++i) {
+          red[tid * (NV + 1) + 2 * i] = acc[i].x;
+          red[tid * (NV + 1) + 2 * i + 1] = acc[i].y;
+        }
+        nsrc = NLG;
       }
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        aA[v].x += c.x * xv[v].x; aA[v].y += c.x * xv[v].y;
-        aR[v].x += c.y * xv[v].x; aR[v].y += c.y * xv[v].y;
+      for (int i = 0; i < NA; ++i) acc[i] = mk<T2>(0, 0);
+      __syncthreads();
+      const int32_t* gr = h.grp_rows + (int64_t)d.x * R;
+      for (int o = tid; o < LG * NV; o += NT) {
+        const int lb = o / NV, i = o % NV;
+        T sum = T(0);
+        // source row j of output lane lb: SHFL: warp j's lane lb; else lane group j
+        for (int j = 0; j < nsrc; ++j) {
+          const int row = K::SHFL ? j * LG + lb : (j / NG) * 32 + (j % NG) * LG + lb;
+          sum += red[row * (NV + 1) + i];
+        }
+        const int comp = i & 1, v = (i >> 1) % V, r = (i / (2 * V)) % R, part = i / (2 * V * R);
+        const int m = gr[r];
+        if (m < 0) continue;
+        if constexpr (PARTS) {
+          T2* y = part ? y1 : y0;
+          if (y) reinterpret_cast<T*>(y + m)[comp] = part ? -sum : sum;
+        } else {
+          const int b = lb * V + v;
+          if (b < cb.B) {   // (j alpha) u: re = -alpha u.im, im = alpha u.re
+            const T al = (T)cb.alpha_im[b];
+            T* yy = reinterpret_cast<T*>(y0 + (int64_t)b * cb.ystride + m);
+            if (comp == 0) yy[1] = al * sum;
+            else yy[0] = -al * sum;
+          }
+        }
       }
     }
+  };
+
+  // prologue: barriers; descriptors 0..3D-1 and indices 0..2D-1 by plain
+  // loads; coefficients 0..D-1 in flight; rows of chunk 0 in registers
+  if (tid < K::NDS) mbar_init(bar + tid, 1);
+  if (tid < 3 * D && tid < nch) sdesc[tid] = chunks[tid];
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  for (int j = 0; j < 2 * D && j < nch; ++j) {
+    const int4 d = sdesc[j];
+    const int* src = ((d.y & 1) ? h.ucol : h.wnode) + d.z;
+    for (int e = tid; e < d.w; e += NT) sidx[j * CHC + e] = src[e];
   }
-#pragma unroll
-  for (int o = LG; o < 32; o <<= 1) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      aA[v].x += __shfl_xor_sync(0xffffffffu, aA[v].x, o);
-      aA[v].y += __shfl_xor_sync(0xffffffffu, aA[v].y, o);
-      aR[v].x += __shfl_xor_sync(0xffffffffu, aR[v].x, o);
-      aR[v].y += __shfl_xor_sync(0xffffffffu, aR[v].y, o);
-    }
+  __syncthreads();
+  for (int j = 0; j < D; ++j) issue(j, nch, nch);
+  VT bufA[4], bufB[4];
+  load_rows(0, bufA);
+
+  // iteration k: coefficients(k) landed (with idx(k+D), desc(k+2D)); issue
+  // bulk copies for k+D; rows of k+1 into the other register buffer; compute k
+  auto step = [&](int k, const VT* cur, VT* nxt) {
+    mbar_wait(bar + k % K::NDS, (uint32_t)(k / K::NDS) & 1u);
+    issue(k + D, k + 2 * D, k + 3 * D);
+    if (k + 1 < nch) load_rows(k + 1, nxt);
+    compute(k, cur);
+    __syncthreads();   // stage k % NDS is refilled at iteration k + 1
+  };
+  int k = 0;
+  for (; k + 1 < nch; k += 2) {
+    step(k, bufA, bufB);
+    step(k + 1, bufB, bufA);
   }
-  if (g == 0) {
-    using R = decltype(T2::x);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int b = b0 + v;
-      if (b < cb.B) {
-        const R al = (R)cb.alpha_im[b], be = (R)cb.beta[b];
-        const R ux = aA[v].x - be * aR[v].x, uy = aA[v].y - be * aR[v].y;
-        y0[b * cb.ystride + m] = mk<T2>(-al * uy, al * ux);   // (j alpha) * u
-      }
-    }
-  }
+  if (k < nch) step(k, bufA, bufB);
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -670,24 +829,37 @@ void run_gather_b(const HotDev& h, int B, cudaStream_t s) {
   AIMX_CHECK_LAUNCH();
 }
 
-template <typename T>
-void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
+template <typename T, int R, int BB, bool PARTS>
+void launch_interp(const HotDev& h, const void* xt, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
-  const unsigned g = (unsigned)(((int64_t)h.nb * 32 + 255) / 256);
-  if (c.B == 1) {
-    k_interp_near1<T><<<g, 256, 0, s>>>(h, (const T2*)x, (T2*)y0, (T2*)y1, c);
-    AIMX_CHECK_LAUNCH();
+  using K = NearCfg<T, R, BB, PARTS>;
+  set_smem(k_interp_near<T, R, BB, PARTS>, K::SMEM);
+  k_interp_near<T, R, BB, PARTS><<<(unsigned)h.near_ctas, K::NT, K::SMEM, s>>>(h, (const T2*)xt, (T2*)y0,
+                                                                                 (T2*)y1, c);
+  AIMX_CHECK_LAUNCH();
+}
+
+template <typename T, int R>
+void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
+  (void)x;
+  if (c.B == 1) {   // single column, staged in xt by run_interleave
+    if (c.mode == 1) launch_interp<T, R, 1, true>(h, h.xt, y0, y1, c, s);
+    else launch_interp<T, R, 1, false>(h, h.xt, y0, y1, c, s);
     return;
   }
   if (c.mode != 0) throw Error(AIMX_E_INTERNAL, "batched parts not supported");
-  const T2* xt = (const T2*)h.xt;   // interleaved by run_interleave earlier in the matvec
-  switch (batch_bucket(c.B)) {
-    case 2: k_interp_near<T, 2><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
-    case 4: k_interp_near<T, 4><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
-    case 8: k_interp_near<T, 8><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
-    default: k_interp_near<T, 16><<<g, 256, 0, s>>>(h, xt, (T2*)y0, c); break;
+  switch (batch_bucket(c.B)) {   // xt: interleaved by run_interleave earlier in the matvec
+    case 2: launch_interp<T, R, 2, false>(h, h.xt, y0, y1, c, s); break;
+    case 4: launch_interp<T, R, 4, false>(h, h.xt, y0, y1, c, s); break;
+    case 8: launch_interp<T, R, 8, false>(h, h.xt, y0, y1, c, s); break;
+    default: launch_interp<T, R, 16, false>(h, h.xt, y0, y1, c, s); break;
   }
-  AIMX_CHECK_LAUNCH();
+}
+
+template <typename T>
+void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
+  if (h.R == 4) run_interp_r<T, 4>(h, x, y0, y1, c, s);
+  else run_interp_r<T, 8>(h, x, y0, y1, c, s);
 }
 
 template <typename T>
@@ -697,12 +869,9 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
   const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz, B = c.B;
   {
     StageScope sc(prof, 1, s);
-    if (B == 1) {
-      run_gather<T>(h, x, c.xstride, B, s);
-    } else {
-      run_interleave<T>(h, x, c, s);
-      run_gather_b<T>(h, B, s);
-    }
+    run_interleave<T>(h, x, c, s);   // xt: 16-byte aligned staging copy for the S4+S5 kernel
+    if (B == 1) run_gather<T>(h, x, c.xstride, B, s);
+    else run_gather_b<T>(h, B, s);
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, B, s)));
   }
   { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, B, s))); }

@@ -194,3 +194,35 @@ def test_sweep_results_independent_of_batch_size(prec):
         y = op.sweep(freqs, X, batch=b).clone()
         assert torch.equal(op.sweep(freqs, X, batch=b), y)
         assert rel_l2(y.cpu().numpy(), ref.cpu().numpy()) <= tol
+
+
+@pytest.mark.parametrize("R,order", [(4, 0), (4, 1), (8, 0), (8, 1)])
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_near_row_group_layouts(R, order, prec, monkeypatch):
+    """Every row-group layout of the near matrix (R rows per group, anchor
+    linear or Morton row order) against the oracle: parts at one column, and
+    a batched sweep (16-column SpMM bucket) per frequency."""
+    from oracle.aimx import AIMxOracle
+    monkeypatch.setenv("AIMX_NEAR_R", str(R))
+    monkeypatch.setenv("AIMX_NEAR_ORDER", str(order))
+    m = inp.icosphere_mesh(2)
+    n = (16, 8, 32)
+    orc = AIMxOracle(m.vertices, m.triangles, n)
+    op = make_gpu_op(m, n, prec)
+    st = op.stats()
+    assert st["near_group_rows"] == R and st["near_row_order"] == order
+    assert st["nnz"] <= st["near_union"] * R
+    x = np.random.default_rng(5).standard_normal(op.N) * (0.3 - 1j)
+    op.set_frequency(250e6)
+    orc.set_frequency(250e6)
+    yA, yP = op.matvec_parts(to_gpu(x, prec))
+    oA, oR = orc.parts(gpu_input_as_c128(x, prec))
+    assert rel_l2(yA.cpu().numpy(), oA) <= TOL[prec]
+    assert rel_l2(yP.cpu().numpy(), -oR) <= TOL[prec]
+    freqs = np.linspace(40e6, 500e6, 11)
+    X = np.stack([inp.rhs_vector(1, i, op.N) for i in range(11)])
+    Y = op.sweep(freqs, to_gpu(X, prec), batch=11).cpu().numpy()
+    for i, f in enumerate(freqs):
+        orc.set_frequency(f)
+        z = orc.matvec(gpu_input_as_c128(X[i], prec))
+        assert rel_l2(Y[i], z) <= TOL[prec]
