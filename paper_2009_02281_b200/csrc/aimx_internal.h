@@ -132,6 +132,9 @@ void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 // ---------------------------------------------------------------- batching
 constexpr int kMaxBatch = 16;
 
+// CTAs per SM of the S4+S5 kernel (its register budget, __launch_bounds__)
+constexpr int near_ctas_per_sm(bool f32, bool single) { return f32 ? (single ? 8 : 6) : 4; }
+
 // ---------------------------------------------------------------- spectrum
 // Octant layout (all spectra): index ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.
 struct SpectrumPlan {
@@ -216,8 +219,10 @@ struct HotDev {
   int32_t* wnode = nullptr;      // [Uw] stencil-node unions (linear grid index)
   void* wval = nullptr;          // [Uw][R] real4 weights (x, y, z, rho), zero off-stencil
   int32_t* chunks = nullptr;     // [nchunk][4] NearChunks work list
-  int32_t* cta_ptr = nullptr;    // [near_ctas+1]
+  int32_t* cta_ptr = nullptr;    // [near_ctas+1] whole-group chunk ranges per CTA (batched launches)
   int near_ctas = 0;
+  int32_t* cta_ptr1 = nullptr;   // [near_ctas1+1] the same for single-column launches
+  int near_ctas1 = 0;
   // grid buffers (complex, 4 channels innermost), `batch` slots each
   void* S = nullptr;             // [nlines][Nx][4] gathered grid sources
   void* bufA = nullptr;          // [Nz][Ny][2Nx][4]

@@ -219,10 +219,14 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     AIMX_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
     NearChunks ck;
     const bool f32p = c->prec == AIMX_C64;
-    build_near_chunks(grp, f32p ? 16 : 8, f32p ? 64 : 32, 3 * nsm, ck);
+    const int chw = f32p ? 16 : 8, chc = f32p ? 64 : 32;
+    build_near_chunks(grp, chw, chc, near_ctas_per_sm(f32p, false) * nsm, ck);
     h.chunks = dupload(c, ck.chunks);
     h.cta_ptr = dupload(c, ck.cta_ptr);
     h.near_ctas = ck.ncta;
+    build_near_chunks(grp, chw, chc, near_ctas_per_sm(f32p, true) * nsm, ck);
+    h.cta_ptr1 = dupload(c, ck.cta_ptr);
+    h.near_ctas1 = ck.ncta;
   }
   c->near_R = grp.R;
   c->near_order = grp.order_kind;

@@ -502,7 +502,8 @@ __device__ __forceinline__ void unpack(const typename VecT<T2, V>::type& u, T2* 
 }
 
 template <typename T, int R, int BB, bool PARTS>
-__global__ void __launch_bounds__(128) k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
+__global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1))
+    k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      typename CT<T>::T2* __restrict__ y0,
                                                      typename CT<T>::T2* __restrict__ y1, Combine cb) {
   using K = NearCfg<T, R, BB, PARTS>;
@@ -519,7 +520,8 @@ __global__ void __launch_bounds__(128) k_interp_near(HotDev h, const typename CT
   uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);      // [NDS]
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int b0 = (lane % LG) * V, g = lane / LG, lgid = wib * NG + g;
-  const int c0 = h.cta_ptr[blockIdx.x], nch = h.cta_ptr[blockIdx.x + 1] - c0;
+  const int32_t* __restrict__ cta_ptr = BB == 1 ? h.cta_ptr1 : h.cta_ptr;
+  const int c0 = cta_ptr[blockIdx.x], nch = cta_ptr[blockIdx.x + 1] - c0;
   if (nch <= 0) return;
   const int4* __restrict__ chunks = reinterpret_cast<const int4*>(h.chunks) + c0;
   const int64_t ns = (int64_t)h.batch * 4;        // phi node stride (complex): [node][channel][slot]
@@ -834,7 +836,7 @@ void launch_interp(const HotDev& h, const void* xt, void* y0, void* y1, const Co
   using T2 = typename CT<T>::T2;
   using K = NearCfg<T, R, BB, PARTS>;
   set_smem(k_interp_near<T, R, BB, PARTS>, K::SMEM);
-  k_interp_near<T, R, BB, PARTS><<<(unsigned)h.near_ctas, K::NT, K::SMEM, s>>>(h, (const T2*)xt, (T2*)y0,
+  k_interp_near<T, R, BB, PARTS><<<(unsigned)(BB == 1 ? h.near_ctas1 : h.near_ctas), K::NT, K::SMEM, s>>>(h, (const T2*)xt, (T2*)y0,
                                                                                  (T2*)y1, c);
   AIMX_CHECK_LAUNCH();
 }

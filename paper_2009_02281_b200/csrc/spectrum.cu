@@ -29,7 +29,11 @@ namespace {
 
 struct K0s { double v[kMaxBatch]; };
 
-// sample[b][(j (Nz+1) + l)(Nx+1) + i] = K(h sqrt(i^2 + j^2 + l^2)), 0 on wrap slots
+// sample[b][(j (Nz+1) + l)(Nx+1) + i] = K(h sqrt(i^2 + j^2 + l^2)), 0 on wrap slots.
+// fp64 (T = double, and the static kernel): K_d with the cancellation-free
+// half-angle form (reading R11).  fp32 results (T = float): the phase
+// k0 r / 2 is formed and reduced modulo 2 pi in fp64, then sin / cos of the
+// reduced angle in fp32 -- the sample is rounded to fp32 either way.
 template <typename T, bool STATIC>
 __global__ void k_sample(int Nx, int Ny, int Nz, int64_t noct, double h, K0s k0s,
                          typename CT<T>::T2* __restrict__ out) {
@@ -42,24 +46,30 @@ __global__ void k_sample(int Nx, int Ny, int Nz, int64_t noct, double h, K0s k0s
   int64_t r2 = idx / (Nx + 1);
   int l = (int)(r2 % (Nz + 1));
   int j = (int)(r2 / (Nz + 1));
-  double re = 0.0, im = 0.0;
+  T2 res = mk<T2>(0, 0);
   if (i < Nx && j < Ny && l < Nz) {
     int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
     const double inv4pi = 1.0 / (4.0 * kPi);
     if (STATIC) {
-      if (q > 0) re = inv4pi / (h * sqrt((double)q));
+      if (q > 0) res = mk<T2>((T)(inv4pi / (h * sqrt((double)q))), (T)0);
     } else if (q == 0) {
-      im = -k0 * inv4pi;
-    } else {
+      res = mk<T2>((T)0, (T)(-k0 * inv4pi));
+    } else if (sizeof(T) == 8) {
       double r = h * sqrt((double)q);
-      double x = k0 * r;
       double s, c;
-      sincos(0.5 * x, &s, &c);
-      re = -2.0 * s * s * inv4pi / r;
-      im = -2.0 * s * c * inv4pi / r;   // sin(x) = 2 sin(x/2) cos(x/2)
+      sincos(0.5 * k0 * r, &s, &c);
+      res = mk<T2>((T)(-2.0 * s * s * inv4pi / r), (T)(-2.0 * s * c * inv4pi / r));   // sin x = 2 sin(x/2) cos(x/2)
+    } else {
+      const double r = h * sqrt((double)q);
+      const double u = 0.25 * k0 * r / kPi;             // (k0 r / 2) / (2 pi)
+      const float red = (float)(u - rint(u));           // in [-1/2, 1/2] turns
+      float s, c;
+      sincospif(2.0f * red, &s, &c);
+      const float a = (float)(inv4pi / r);
+      res = mk<T2>((T)(-2.0f * s * s * a), (T)(-2.0f * s * c * a));
     }
   }
-  out[(int64_t)b * noct + idx] = mk<T2>((T)re, (T)im);
+  out[(int64_t)b * noct + idx] = res;
 }
 
 // Even-extension transform of lines of N1 = L/2 + 1 octant samples with the
@@ -68,13 +78,14 @@ __global__ void k_sample(int Nx, int Ny, int Nz, int64_t noct, double h, K0s k0s
 // Row mode (contiguous lines, x axis): line-major thread mapping so a warp
 // reads consecutive samples; column mode (strided lines): line-fastest
 // mapping, lines = consecutive u.  Optional epilogue out = scale (v + add).
-template <typename S, int L> struct EvGeom {
+template <typename S, int L, bool SMALL = false> struct EvGeom {
   static constexpr int R1 = Fac<L>::R1, R2 = Fac<L>::R2;
   using TL = TwoLevel<R1, R2>;
   static constexpr int T = TL::T, E = TL::E;
   static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? 4 : 1) : 0;
   static constexpr size_t BYTES256 = sizeof(typename CT<S>::T2) * (size_t)(256 / T) * XB;
-  static constexpr int NT = BYTES256 > 200 * 1024 ? 128 : 256;
+  // SMALL: 64-thread CTAs when there are few lines (more CTAs in flight)
+  static constexpr int NT = SMALL ? (T > 64 ? T : 64) : (BYTES256 > 200 * 1024 ? 128 : 256);
   static constexpr int NL = NT / T;
 };
 
@@ -110,7 +121,7 @@ struct SampleArgs {
 };
 
 // MODE 0: read `in`; MODE 1: generate dynamic samples K_d (row pass only).
-template <typename T, int L, bool ROW, int MODE = 0>
+template <typename T, int L, bool ROW, int MODE = 0, bool SMALL = false>
 __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int64_t noct,
                                               const typename CT<T>::T2* __restrict__ in,
                                               typename CT<T>::T2* __restrict__ out,
@@ -118,7 +129,7 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
                                               const typename CT<T>::T2* __restrict__ add, T scale,
                                               SampleArgs sa) {
   using T2 = typename CT<T>::T2;
-  using G = EvGeom<T, L>;
+  using G = EvGeom<T, L, SMALL>;
   constexpr int N1 = L / 2 + 1;
   const int line = ROW ? threadIdx.x / G::T : threadIdx.x % G::NL;
   const int t = ROW ? threadIdx.x % G::T : threadIdx.x / G::NL;
@@ -183,24 +194,28 @@ template <class K> void set_smem(K kernel, size_t bytes) {
     AIMX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+// CTAs of a pass with the default geometry; below two waves use SMALL CTAs
+template <typename T, int L> bool use_small(int64_t ctas_default) { return ctas_default < 2 * 148; }
+
 template <typename T>
 void even_rows(int L, int64_t nlines, int64_t noct, int B, const void* in, void* out, const void* tw,
-               cudaStream_t s, const SampleArgs* gen = nullptr) {
+               cudaStream_t s) {
   using T2 = typename CT<T>::T2;
-  SampleArgs sa{};
-  if (gen) sa = *gen;
   AIMX_SWITCH_L(L, ({
-    using G = EvGeom<T, L>;
-    const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
-    dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
-    if (gen) {
-      set_smem(k_even<T, L, true, 1>, sm);
-      k_even<T, L, true, 1><<<g, G::NT, sm, s>>>(nlines, 1, noct, nullptr, (T2*)out, (const T2*)tw,
-                                                 nullptr, (T)1, sa);
+    if (use_small<T, L>((nlines + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * B)) {
+      using G = EvGeom<T, L, true>;
+      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+      dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
+      set_smem(k_even<T, L, true, 0, true>, sm);
+      k_even<T, L, true, 0, true><<<g, G::NT, sm, s>>>(nlines, 1, noct, (const T2*)in, (T2*)out,
+                                                       (const T2*)tw, nullptr, (T)1, SampleArgs{});
     } else {
+      using G = EvGeom<T, L>;
+      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+      dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
       set_smem(k_even<T, L, true>, sm);
       k_even<T, L, true><<<g, G::NT, sm, s>>>(nlines, 1, noct, (const T2*)in, (T2*)out, (const T2*)tw,
-                                              nullptr, (T)1, sa);
+                                              nullptr, (T)1, SampleArgs{});
     }
   }));
   AIMX_CHECK_LAUNCH();
@@ -211,12 +226,21 @@ void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const v
                const void* tw, const void* add, T scale, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   AIMX_SWITCH_L(L, ({
-    using G = EvGeom<T, L>;
-    const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
-    set_smem(k_even<T, L, false>, sm);
-    dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
-    k_even<T, L, false><<<g, G::NT, sm, s>>>(0, inner, noct, (const T2*)in, (T2*)out, (const T2*)tw,
-                                             (const T2*)add, scale, SampleArgs{});
+    if (use_small<T, L>((inner + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * outer * B)) {
+      using G = EvGeom<T, L, true>;
+      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+      set_smem(k_even<T, L, false, 0, true>, sm);
+      dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
+      k_even<T, L, false, 0, true><<<g, G::NT, sm, s>>>(0, inner, noct, (const T2*)in, (T2*)out,
+                                                        (const T2*)tw, (const T2*)add, scale, SampleArgs{});
+    } else {
+      using G = EvGeom<T, L>;
+      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+      set_smem(k_even<T, L, false>, sm);
+      dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
+      k_even<T, L, false><<<g, G::NT, sm, s>>>(0, inner, noct, (const T2*)in, (T2*)out, (const T2*)tw,
+                                               (const T2*)add, scale, SampleArgs{});
+    }
   }));
   AIMX_CHECK_LAUNCH();
 }
@@ -224,9 +248,9 @@ void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const v
 // 3-D even-extension transform on the octant [B][y][z][x]: x rows, z cols, y cols.
 template <typename T>
 void dct3(SpectrumPlan& sp, int B, void** tw, void* a, void* b, void* out, const void* add, T scale,
-          cudaStream_t s, const SampleArgs* gen = nullptr) {
+          cudaStream_t s) {
   const int64_t nx = sp.Nx + 1, ny = sp.Ny + 1, nz = sp.Nz + 1, no = sp.noct;
-  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s, gen);
+  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s);
   even_cols<T>(2 * sp.Nz, ny, nx, no, B, b, a, tw[2], nullptr, (T)1, s);
   even_cols<T>(2 * sp.Ny, 1, nz * nx, no, B, a, out, tw[1], add, scale, s);
 }
@@ -281,17 +305,23 @@ void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s) {
 void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
                           float2* out, cudaStream_t s) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
-  for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
-  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s, &sa);
+  K0s k{};
+  for (int b = 0; b < B; ++b) k.v[b] = k0[b];
+  k_sample<float, false><<<dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), 256, 0, s>>>(
+      sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (float2*)sp.work0);
+  AIMX_CHECK_LAUNCH();
+  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s);
 }
 
-void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs,
-                          double scale, double2* out, cudaStream_t s) {
+void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs, double scale,
+                          double2* out, cudaStream_t s) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
-  for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
-  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s, &sa);
+  K0s k{};
+  for (int b = 0; b < B; ++b) k.v[b] = k0[b];
+  k_sample<double, false><<<dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), 256, 0, s>>>(
+      sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (double2*)sp.work0);
+  AIMX_CHECK_LAUNCH();
+  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s);
 }
 
 }  // namespace aimx
