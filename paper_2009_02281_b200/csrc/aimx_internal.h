@@ -88,15 +88,24 @@ struct NearGroups {
 
 void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, NearGroups& g);
 
-// Work list of the S4+S5 kernel: chunks {group, flags, begin, count} (flags:
-// bit0 = near (C) chunk, else interpolation (W) chunk; bit1 first, bit2 last
-// chunk of its group) and contiguous chunk ranges per CTA (whole groups).
+// Work list of the S4+S5 kernel: chunks {group, flags, payload offset / 16,
+// count} (flags: bit0 = near (C) chunk, else interpolation (W) chunk; bit1
+// first, bit2 last chunk of its group).  Chunk c's payload, moved by ONE bulk
+// copy: [count coefficient tuples (C: R (C_A, C_rho) pairs; W: R real4
+// weights) | count row indices, 16-byte padded | descriptor of chunk c + kNearD].
+constexpr int kNearD = 2;          // S4+S5 pipeline depth (chunks in flight)
 struct NearChunks {
   std::vector<int32_t> chunks;     // [nchunk][4]
-  std::vector<int32_t> cta_ptr;    // [ncta+1]
-  int ncta = 0;
+  std::vector<unsigned char> payload;
+  std::vector<int64_t> uoff_c;     // [U] payload byte offset of union entry u's C pairs
+  std::vector<int64_t> uoff_w;     // [Uw] ... of the W weights
+  std::vector<int64_t> gfirst;     // [ngrp+1] first chunk of each group
+  std::vector<double> cost;        // [ngrp] work estimate
 };
-void build_near_chunks(const NearGroups& g, int chw, int chc, int ncta, NearChunks& ck);
+// cs = bytes of one complex (= one real pair) in the compute precision
+void build_near_chunks(const NearGroups& g, int chw, int chc, int cs, NearChunks& ck);
+// chunk ranges (whole groups) per CTA
+std::vector<int32_t> near_partition(const NearChunks& ck, int64_t ngrp, int ncta);
 
 // ---------------------------------------------------------------- device setup (fp64)
 struct SetupDev {
@@ -133,7 +142,7 @@ void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 constexpr int kMaxBatch = 16;
 
 // CTAs per SM of the S4+S5 kernel (its register budget, __launch_bounds__)
-constexpr int near_ctas_per_sm(bool f32, bool single) { return f32 ? (single ? 8 : 6) : 4; }
+constexpr int near_ctas_per_sm(bool f32, bool single) { return f32 ? (single ? 5 : 6) : 4; }
 
 // ---------------------------------------------------------------- spectrum
 // Octant layout (all spectra): index ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.
@@ -214,15 +223,14 @@ struct HotDev {
   int R = 8;                     // rows per group
   int ngrp = 0;
   int32_t* grp_rows = nullptr;   // [ngrp][R]
-  int32_t* ucol = nullptr;       // [U]
-  void* gval = nullptr;          // [U][R] real2 (C_A, C_rho), zero where not near
-  int32_t* wnode = nullptr;      // [Uw] stencil-node unions (linear grid index)
-  void* wval = nullptr;          // [Uw][R] real4 weights (x, y, z, rho), zero off-stencil
+  unsigned char* payload = nullptr;   // NearChunks payloads: C pairs / W weights (zero where
+                                      // not near / off-stencil), row indices, next descriptors
   int32_t* chunks = nullptr;     // [nchunk][4] NearChunks work list
   int32_t* cta_ptr = nullptr;    // [near_ctas+1] whole-group chunk ranges per CTA (batched launches)
   int near_ctas = 0;
   int32_t* cta_ptr1 = nullptr;   // [near_ctas1+1] the same for single-column launches
   int near_ctas1 = 0;
+  int dbg = 0;                   // experiments only (AIMX_DEBUG_NEAR)
   // grid buffers (complex, 4 channels innermost), `batch` slots each
   void* S = nullptr;             // [nlines][Nx][4] gathered grid sources
   void* bufA = nullptr;          // [Nz][Ny][2Nx][4]

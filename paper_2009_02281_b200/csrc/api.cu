@@ -79,14 +79,15 @@ P* dupload(aimx_ctx* c, const std::vector<P>& v) {
 
 // ---- small conversion kernels ------------------------------------------------------
 // weight (rwg, slot) i -> its row-group slot (exactly-zero weights have none)
+// weight (rwg, slot) i -> byte offset slot[i] of the near payload (exactly-zero weights have none)
 template <typename T4>
-__global__ void k_lam_to(int64_t n, const int64_t* __restrict__ slot, const double* __restrict__ lam,
-                         T4* __restrict__ out) {
+__global__ void k_lam_to(int64_t n, const int64_t* __restrict__ slot, const double* __restrict__ lam, T4*,
+                         unsigned char* __restrict__ payload) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n || slot[i] < 0) return;
   T4 v;
   v.x = lam[4 * i]; v.y = lam[4 * i + 1]; v.z = lam[4 * i + 2]; v.w = lam[4 * i + 3];
-  out[slot[i]] = v;
+  *reinterpret_cast<T4*>(payload + slot[i]) = v;
 }
 template <typename T4>
 __global__ void k_ent_w(int64_t n, int p3, const int32_t* __restrict__ er, const int32_t* __restrict__ es,
@@ -98,16 +99,16 @@ __global__ void k_ent_w(int64_t n, int p3, const int32_t* __restrict__ er, const
   v.x = l[0]; v.y = l[1]; v.z = l[2]; v.w = l[3];
   out[i] = v;
 }
-// CSR entry k of (C_A, C_rho) -> its row-group value slot
+// CSR entry k of (C_A, C_rho) -> byte offset slot[k] of the near payload
 template <typename T2>
 __global__ void k_pack_c(int64_t n, const int64_t* __restrict__ slot, const double* __restrict__ CA,
-                         const double* __restrict__ CR, T2* __restrict__ out) {
+                         const double* __restrict__ CR, T2*, unsigned char* __restrict__ payload) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   T2 v;
   v.x = CA[i];
   v.y = CR[i];
-  out[slot[i]] = v;
+  *reinterpret_cast<T2*>(payload + slot[i]) = v;
 }
 __global__ void k_d2f(int64_t n, const double2* __restrict__ a, float2* __restrict__ b) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -209,24 +210,31 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   h.R = grp.R;
   h.ngrp = (int)grp.ngrp;
   h.grp_rows = dupload(c, grp.rows);
-  h.ucol = dupload(c, grp.ucol);
-  h.wnode = dupload(c, grp.wnode);
-  int64_t* gslot = dupload(c, grp.slot);
-  int64_t* wslot = dupload(c, grp.wslot);
   const int64_t nU = grp.ptr.back(), nUw = grp.wptr.back();
+  int64_t* gslot = nullptr;
+  int64_t* wslot = nullptr;
   {
     int nsm = 148;
     AIMX_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
     NearChunks ck;
     const bool f32p = c->prec == AIMX_C64;
-    const int chw = f32p ? 16 : 8, chc = f32p ? 64 : 32;
-    build_near_chunks(grp, chw, chc, near_ctas_per_sm(f32p, false) * nsm, ck);
+    const int cs = f32p ? 8 : 16;
+    build_near_chunks(grp, f32p ? 32 : 16, f32p ? 128 : 64, cs, ck);
+    // value slot (u R + r) -> payload byte offset
+    for (auto& v : grp.slot) v = ck.uoff_c[v / grp.R] + (v % grp.R) * cs;
+    for (auto& v : grp.wslot)
+      if (v >= 0) v = ck.uoff_w[v / grp.R] + (v % grp.R) * 2 * cs;
+    gslot = dupload(c, grp.slot);
+    wslot = dupload(c, grp.wslot);
+    h.payload = dupload(c, ck.payload);
     h.chunks = dupload(c, ck.chunks);
-    h.cta_ptr = dupload(c, ck.cta_ptr);
-    h.near_ctas = ck.ncta;
-    build_near_chunks(grp, chw, chc, near_ctas_per_sm(f32p, true) * nsm, ck);
-    h.cta_ptr1 = dupload(c, ck.cta_ptr);
-    h.near_ctas1 = ck.ncta;
+    std::vector<int32_t> cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32p, false) * nsm);
+    h.cta_ptr = dupload(c, cp);
+    h.near_ctas = (int)cp.size() - 1;
+    cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32p, true) * nsm);
+    h.cta_ptr1 = dupload(c, cp);
+    h.near_ctas1 = (int)cp.size() - 1;
+    if (const char* e = std::getenv("AIMX_DEBUG_NEAR")) h.dbg = std::atoi(e);
   }
   c->near_R = grp.R;
   c->near_order = grp.order_kind;
@@ -236,25 +244,17 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   const bool f32 = c->prec == AIMX_C64;
   const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
   if (f32) {
-    h.wval = dalloc<float4>(c, nUw * grp.R);
-    AIMX_CUDA(cudaMemsetAsync(h.wval, 0, nUw * grp.R * sizeof(float4), c->stream));
     h.ent_w = dalloc<float4>(c, nent);
-    h.gval = dalloc<float2>(c, nU * grp.R);
-    AIMX_CUDA(cudaMemsetAsync(h.gval, 0, nU * grp.R * sizeof(float2), c->stream));
-    k_lam_to<float4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (float4*)h.wval);
+    k_lam_to<float4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (float4*)nullptr, h.payload);
     k_ent_w<float4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)p3, h.ent_rwg, ent_slot, d.lam,
                                                       (float4*)h.ent_w);
-    k_pack_c<float2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (float2*)h.gval);
+    k_pack_c<float2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (float2*)nullptr, h.payload);
   } else {
-    h.wval = dalloc<double4>(c, nUw * grp.R);
-    AIMX_CUDA(cudaMemsetAsync(h.wval, 0, nUw * grp.R * sizeof(double4), c->stream));
     h.ent_w = dalloc<double4>(c, nent);
-    h.gval = dalloc<double2>(c, nU * grp.R);
-    AIMX_CUDA(cudaMemsetAsync(h.gval, 0, nU * grp.R * sizeof(double2), c->stream));
-    k_lam_to<double4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (double4*)h.wval);
+    k_lam_to<double4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (double4*)nullptr, h.payload);
     k_ent_w<double4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)p3, h.ent_rwg, ent_slot, d.lam,
                                                        (double4*)h.ent_w);
-    k_pack_c<double2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (double2*)h.gval);
+    k_pack_c<double2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (double2*)nullptr, h.payload);
   }
   AIMX_CHECK_LAUNCH();
   // ---- batch slots and grid buffers

@@ -443,41 +443,79 @@ void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, N
   }
 }
 
-void build_near_chunks(const NearGroups& ng, int chw, int chc, int ncta, NearChunks& ck) {
+void build_near_chunks(const NearGroups& ng, int chw, int chc, int cs, NearChunks& ck) {
   // chunk list in group order: the group's W (interpolation) chunks, then its
   // C (near) chunks; every group gets at least one chunk (its epilogue).
+  const int R = ng.R;
   ck.chunks.clear();
-  std::vector<int64_t> gfirst(ng.ngrp + 1);
-  std::vector<double> cost(ng.ngrp);
+  ck.gfirst.assign(ng.ngrp + 1, 0);
+  ck.cost.assign(ng.ngrp, 0.0);
+  ck.uoff_c.assign(ng.ptr[ng.ngrp], 0);
+  ck.uoff_w.assign(ng.wptr[ng.ngrp], 0);
+  int64_t off = 0;   // payload bytes so far
+  std::vector<int64_t> poff;
+  auto pad16 = [](int64_t x) { return (x + 15) & ~(int64_t)15; };
   for (int64_t g = 0; g < ng.ngrp; ++g) {
-    gfirst[g] = (int64_t)ck.chunks.size() / 4;
+    ck.gfirst[g] = (int64_t)ck.chunks.size() / 4;
     const int64_t n0 = ck.chunks.size();
     for (int kind = 0; kind < 2; ++kind) {
       const int64_t b = kind ? ng.ptr[g] : ng.wptr[g], e = kind ? ng.ptr[g + 1] : ng.wptr[g + 1];
       const int ch = kind ? chc : chw;
+      const int eb = R * (kind ? cs : 2 * cs);   // coefficient bytes per entry
       for (int64_t u = b; u < e; u += ch) {
-        ck.chunks.insert(ck.chunks.end(), {(int32_t)g, kind, (int32_t)u, (int32_t)std::min<int64_t>(ch, e - u)});
+        const int64_t n = std::min<int64_t>(ch, e - u);
+        for (int64_t i = 0; i < n; ++i) (kind ? ck.uoff_c : ck.uoff_w)[u + i] = off + i * eb;
+        ck.chunks.insert(ck.chunks.end(), {(int32_t)g, kind, (int32_t)u, (int32_t)n});
+        poff.push_back(off);
+        off += n * eb + pad16(4 * n) + 16;
       }
     }
-    if ((int64_t)ck.chunks.size() == n0) ck.chunks.insert(ck.chunks.end(), {(int32_t)g, 1, 0, 0});
+    if ((int64_t)ck.chunks.size() == n0) {
+      ck.chunks.insert(ck.chunks.end(), {(int32_t)g, 1, 0, 0});
+      poff.push_back(off);
+      off += 16;
+    }
     ck.chunks[n0 + 1] |= 2;                          // first chunk of the group
     ck.chunks[ck.chunks.size() - 3] |= 4;            // last chunk of the group
-    cost[g] = 4.0 * (ng.wptr[g + 1] - ng.wptr[g]) + (ng.ptr[g + 1] - ng.ptr[g]) + 32.0;
+    ck.cost[g] = 4.0 * (ng.wptr[g + 1] - ng.wptr[g]) + (ng.ptr[g + 1] - ng.ptr[g]) + 32.0;
   }
-  gfirst[ng.ngrp] = (int64_t)ck.chunks.size() / 4;
+  ck.gfirst[ng.ngrp] = (int64_t)ck.chunks.size() / 4;
+  if (off / 16 > (int64_t)INT32_MAX) throw Error(AIMX_E_GRID, "near matrix payload too large");
+  // payload: per chunk [coefficients | row indices (16-byte padded) | descriptor of chunk + kNearD]
+  const int64_t nchunk = (int64_t)ck.chunks.size() / 4;
+  ck.payload.assign(off, 0);
+  for (int64_t c = 0; c < nchunk; ++c) {
+    const int32_t* d = &ck.chunks[4 * c];
+    const int kind = d[1] & 1;
+    const int64_t n = d[3];
+    const int eb = R * (kind ? cs : 2 * cs);
+    unsigned char* p = ck.payload.data() + poff[c] + n * eb;
+    const int32_t* src = (kind ? ng.ucol.data() : ng.wnode.data()) + d[2];
+    std::memcpy(p, src, 4 * n);
+    p += pad16(4 * n);
+    if (c + kNearD < nchunk) {
+      int32_t nd[4] = {ck.chunks[4 * (c + kNearD)], ck.chunks[4 * (c + kNearD) + 1],
+                       (int32_t)(poff[c + kNearD] / 16), ck.chunks[4 * (c + kNearD) + 3]};
+      std::memcpy(p, nd, 16);
+    }
+  }
+  for (int64_t c = 0; c < nchunk; ++c) ck.chunks[4 * c + 2] = (int32_t)(poff[c] / 16);
+}
+
+std::vector<int32_t> near_partition(const NearChunks& ck, int64_t ngrp, int ncta) {
   // contiguous group ranges per CTA, balanced by cost
-  ncta = (int)std::max<int64_t>(1, std::min<int64_t>(ncta, ng.ngrp));
+  ncta = (int)std::max<int64_t>(1, std::min<int64_t>(ncta, ngrp));
   double total = 0;
-  for (double c : cost) total += c;
-  ck.cta_ptr.assign(ncta + 1, 0);
+  for (double c : ck.cost) total += c;
+  std::vector<int32_t> cta_ptr(ncta + 1, 0);
   int64_t g = 0;
   double acc = 0;
   for (int k = 0; k < ncta; ++k) {
     const double target = total * (k + 1) / ncta;
-    while (g < ng.ngrp && (acc + 0.5 * cost[g] <= target || k == ncta - 1)) acc += cost[g++];
-    ck.cta_ptr[k + 1] = (int32_t)gfirst[g];
+    while (g < ngrp && (acc + 0.5 * ck.cost[g] <= target || k == ncta - 1)) acc += ck.cost[g++];
+    cta_ptr[k + 1] = (int32_t)ck.gfirst[g];
   }
-  ck.ncta = ncta;
+  return cta_ptr;
 }
 
 }  // namespace aimx

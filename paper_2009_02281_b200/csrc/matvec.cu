@@ -442,24 +442,24 @@ template <typename T, int R, int BB, bool PARTS> struct NearCfg {
   using T2 = typename CT<T>::T2;
   static constexpr int NT = 128;                      // threads per CTA
   static constexpr int S = (int)sizeof(T2);           // complex bytes
-  static constexpr int CHC = 512 / S, CHW = 128 / S;  // entries per C / W chunk
-  static constexpr int COEFB = CHC * R * S;           // stage bytes (C: R pairs; W: R real4 = 2 S per entry)
-  static constexpr int D = 3;                         // pipeline depth (chunks)
-  static constexpr int NDS = D + 1, NIS = 2 * D, NDD = 3 * D + 1;   // stage / index / descriptor slots
+  static constexpr int CHC = 1024 / S, CHW = 256 / S; // entries per C / W chunk
+  static constexpr int COEFB = CHC * R * S;           // coefficient bytes (C: R pairs; W: R real4 = 2 S per entry)
+  static constexpr int STB = COEFB + CHC * 4 + 16;    // stage: one chunk payload (NearChunks)
+  static constexpr int D = kNearD;                    // pipeline depth (chunks)
+  static constexpr int NDS = D + 1, NDD = D + 1;      // stage / descriptor slots
   static constexpr int V = (S == 8 && BB >= 2) ? 2 : 1;
   static constexpr int LG = BB / V, NG = 32 / LG, NLG = (NT / 32) * NG;
-  static constexpr int NPC = (CHC + NLG - 1) / NLG;   // C entries per lane group per chunk (<= 4)
-  static constexpr bool WACT = CHW <= NLG;            // W: one entry per lane group
-  static_assert(NPC <= 4 && WACT, "row prefetch buffer holds 4 loads");
+  static constexpr int NPC = (CHC + NLG - 1) / NLG;   // C entries per lane group per chunk
+  static constexpr int NPW = (CHW + NLG - 1) / NLG;   // W entries per lane group per chunk
+  static constexpr int NBUF = NPC > 4 * NPW ? NPC : 4 * NPW;   // row loads in flight per lane
   static constexpr int NA = (PARTS ? 2 : 1) * R * V;  // complex accumulators: [part][r][v]
   static constexpr int NV = 2 * NA;                   // as reals
   // partial sums: per lane (NG > 4) or, after a shuffle reduction over the
   // warp's NG lane groups, per (warp, lane of group 0)
   static constexpr bool SHFL = NG <= 4;
   static constexpr size_t REDB = (size_t)(SHFL ? (NT / 32) * LG : NT) * (NV + 1) * sizeof(T);
-  static constexpr size_t OFF_RED = (size_t)NDS * COEFB;
-  static constexpr size_t OFF_IDX = (OFF_RED + REDB + 15) / 16 * 16;
-  static constexpr size_t OFF_DESC = OFF_IDX + (size_t)NIS * CHC * 4;
+  static constexpr size_t OFF_RED = (size_t)NDS * STB;
+  static constexpr size_t OFF_DESC = (OFF_RED + REDB + 15) / 16 * 16;
   static constexpr size_t OFF_BAR = OFF_DESC + NDD * 16;
   static constexpr size_t SMEM = OFF_BAR + NDS * 8;
 };
@@ -513,9 +513,8 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
   constexpr int NT = K::NT, V = K::V, LG = K::LG, NG = K::NG, NLG = K::NLG, NV = K::NV, NA = K::NA;
   constexpr int D = K::D, CHC = K::CHC, NPC = K::NPC;
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned char* const sdata = smem;                                         // [NDS][COEFB]
+  unsigned char* const sdata = smem;                                         // [NDS][STB]
   T* const red = reinterpret_cast<T*>(smem + K::OFF_RED);                    // partial sums
-  int* const sidx = reinterpret_cast<int*>(smem + K::OFF_IDX);               // [NIS][CHC]
   int4* const sdesc = reinterpret_cast<int4*>(smem + K::OFF_DESC);           // [NDD]
   uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);      // [NDS]
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
@@ -535,50 +534,60 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
   for (int i = 0; i < NA; ++i) acc[i] = mk<T2>(0, 0);
   const T2 nbe2 = mk<T2>(-be[0], V == 2 ? -be[V - 1] : T(0));   // (-beta_b0, -beta_b0+1)
 
-  auto get_desc = [&](int j) -> int4 { return j < nch ? sdesc[j % K::NDD] : make_int4(0, 0, 0, 0); };
-  // bulk copies of chunk j's coefficient block (stage j % NDS), plus chunk
-  // ji's row indices and chunk jd's descriptor, all on bar[j % NDS]
-  auto issue = [&](int j, int ji, int jd) {
-    if (tid != 0 || j >= nch) return;
-    const int4 d = get_desc(j);
+  // coefficient bytes of a chunk
+  auto coef_bytes = [&](const int4& d) -> int { return d.w * R * ((d.y & 1) ? K::S : 2 * K::S); };
+  // ONE bulk copy moves chunk j's payload (coefficients, row indices, the
+  // descriptor of chunk j + D) into stage j % NDS, completing on bar[j % NDS]
+  // (thread 0; d = chunk j's descriptor, recorded for the compute)
+  auto issue = [&](int j, const int4& d) {
     uint64_t* bj = bar + j % K::NDS;
-    const uint32_t cbytes = (uint32_t)d.w * R * ((d.y & 1) ? K::S : 2 * K::S);
-    const int4 di = get_desc(ji);
-    const uint32_t ibytes = ji < nch ? (uint32_t)di.w * 4 : 0;
-    const uint32_t dbytes = jd < nch ? 16 : 0;
-    mbar_arrive_expect_tx(bj, cbytes + ibytes + dbytes);
-    if (cbytes)
-      bulk_g2s(sdata + (j % K::NDS) * K::COEFB,
-               (d.y & 1) ? (const char*)h.gval + (int64_t)d.z * R * K::S
-                         : (const char*)h.wval + (int64_t)d.z * R * 2 * K::S,
-               cbytes, bj);
-    if (ibytes) bulk_g2s(sidx + (ji % K::NIS) * CHC, ((di.y & 1) ? h.ucol : h.wnode) + di.z, ibytes, bj);
-    if (dbytes) bulk_g2s(sdesc + jd % K::NDD, chunks + jd, 16, bj);
+    const uint32_t bytes = (uint32_t)(coef_bytes(d) + ((4 * d.w + 15) & ~15) + 16);
+    sdesc[j % K::NDD] = d;
+    mbar_arrive_expect_tx(bj, bytes);
+    bulk_g2s(sdata + (j % K::NDS) * K::STB, h.payload + (int64_t)d.z * 16, bytes, bj);
   };
-  // gathered rows of chunk j into registers: C: x rows of entries
-  // lgid + i NLG (i < NPC); W: the 4 channel rows of entry lgid
-  auto load_rows = [&](int j, VT* buf) {
-    const int4 d = get_desc(j);
-    const int* ix = sidx + (j % K::NIS) * CHC;
+
+  // prologue: barriers; descriptors 0..D-1 by plain loads; chunks 0..D-1 in flight
+  if (tid < K::NDS) mbar_init(bar + tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  if (tid == 0)
+    for (int j = 0; j < D && j < nch; ++j) issue(j, chunks[j]);
+  __syncthreads();
+
+  VT buf[K::NBUF];
+  for (int k = 0; k < nch; ++k) {
+    // chunk k's payload (with the descriptor of chunk k + D) has landed
+    mbar_wait(bar + k % K::NDS, (uint32_t)(k / K::NDS) & 1u);
+    const int4 d = sdesc[k % K::NDD];
+    const unsigned char* stg = sdata + (k % K::NDS) * K::STB;
+    const int* ix = reinterpret_cast<const int*>(stg + coef_bytes(d));
+    if (tid == 0 && k + D < nch)
+      issue(k + D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
+    // gathered rows into registers (all loads issued before any use): C: x rows
+    // of entries lgid + i NLG; W: the 4 channel rows of entries lgid + i NLG
     if (d.y & 1) {
 #pragma unroll
-      for (int i = 0; i < NPC; ++i) {
+      for (int i = 0; i < K::NPC; ++i) {
         const int e = lgid + i * NLG;
-        if (e < d.w) buf[i] = __ldg((const VT*)(xr + (int64_t)ix[e] * BB));
+        if (e < d.w) buf[i] = __ldg((const VT*)(xr + (int64_t)(h.dbg == 1 ? (e & 7) : ix[e]) * BB));
       }
-    } else if (lgid < d.w) {
-      const T2* pr = phi + (int64_t)ix[lgid] * ns;
+    } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) buf[c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
+      for (int i = 0; i < K::NPW; ++i) {
+        const int e = lgid + i * NLG;
+        if (e < d.w) {
+          const T2* pr = phi + (int64_t)ix[e] * ns;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) buf[4 * i + c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
+        }
+      }
     }
-  };
-  auto compute = [&](int k, const VT* buf) {
-    const int4 d = get_desc(k);
-    const unsigned char* stg = sdata + (k % K::NDS) * K::COEFB;
-    if (d.y & 1) {   // near correction: pairs [e][R]
+    if (h.dbg == 2) {
+    } else if (d.y & 1) {   // near correction: pairs [e][R]
       const T2* __restrict__ cf = (const T2*)stg;
 #pragma unroll
-      for (int i = 0; i < NPC; ++i) {
+      for (int i = 0; i < K::NPC; ++i) {
         const int e = lgid + i * NLG;
         if (e >= d.w) break;
         T2 xv[V];
@@ -614,11 +623,15 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
           }
         }
       }
-    } else if (lgid < d.w) {   // interpolation: weights [e][R] real4
-      const T4* __restrict__ wf = (const T4*)stg + lgid * R;
+    } else {         // interpolation: weights [e][R] real4
+#pragma unroll
+      for (int i = 0; i < K::NPW; ++i) {
+      const int e = lgid + i * NLG;
+      if (e >= d.w) break;
+      const T4* __restrict__ wf = (const T4*)stg + e * R;
       T2 pv[4][V];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) unpack<T2, V>(buf[c], pv[c]);
+      for (int c = 0; c < 4; ++c) unpack<T2, V>(buf[4 * i + c], pv[c]);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const T4 w = wf[r];
@@ -631,6 +644,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
           if constexpr (PARTS) axpy(acc[(R + r) * V + v], w.w, pv[3][v]);
           else axpy(a, -be[v] * w.w, pv[3][v]);
         }
+      }
       }
     }
     if (d.y & 4) {   // last chunk of group d.x: fixed-order reduction + combine
@@ -687,39 +701,8 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
         }
       }
     }
-  };
-
-  // prologue: barriers; descriptors 0..3D-1 and indices 0..2D-1 by plain
-  // loads; coefficients 0..D-1 in flight; rows of chunk 0 in registers
-  if (tid < K::NDS) mbar_init(bar + tid, 1);
-  if (tid < 3 * D && tid < nch) sdesc[tid] = chunks[tid];
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  __syncthreads();
-  for (int j = 0; j < 2 * D && j < nch; ++j) {
-    const int4 d = sdesc[j];
-    const int* src = ((d.y & 1) ? h.ucol : h.wnode) + d.z;
-    for (int e = tid; e < d.w; e += NT) sidx[j * CHC + e] = src[e];
+    __syncthreads();   // stage and descriptor slots of chunk k are refilled next
   }
-  __syncthreads();
-  for (int j = 0; j < D; ++j) issue(j, nch, nch);
-  VT bufA[4], bufB[4];
-  load_rows(0, bufA);
-
-  // iteration k: coefficients(k) landed (with idx(k+D), desc(k+2D)); issue
-  // bulk copies for k+D; rows of k+1 into the other register buffer; compute k
-  auto step = [&](int k, const VT* cur, VT* nxt) {
-    mbar_wait(bar + k % K::NDS, (uint32_t)(k / K::NDS) & 1u);
-    issue(k + D, k + 2 * D, k + 3 * D);
-    if (k + 1 < nch) load_rows(k + 1, nxt);
-    compute(k, cur);
-    __syncthreads();   // stage k % NDS is refilled at iteration k + 1
-  };
-  int k = 0;
-  for (; k + 1 < nch; k += 2) {
-    step(k, bufA, bufB);
-    step(k + 1, bufB, bufA);
-  }
-  if (k < nch) step(k, bufA, bufB);
 }
 
 // ------------------------------------------------------------------ dispatch
