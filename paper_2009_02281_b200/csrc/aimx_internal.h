@@ -93,7 +93,7 @@ void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, N
 // first, bit2 last chunk of its group).  Chunk c's payload, moved by ONE bulk
 // copy: [count coefficient tuples (C: R (C_A, C_rho) pairs; W: R real4
 // weights) | count row indices, 16-byte padded | descriptor of chunk c + kNearD].
-constexpr int kNearD = 2;          // S4+S5 pipeline depth (chunks in flight)
+constexpr int kNearD = 3;          // S4+S5 pipeline depth (chunks in flight)
 struct NearChunks {
   std::vector<int32_t> chunks;     // [nchunk][4]
   std::vector<unsigned char> payload;
@@ -142,7 +142,7 @@ void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 constexpr int kMaxBatch = 16;
 
 // CTAs per SM of the S4+S5 kernel (its register budget, __launch_bounds__)
-constexpr int near_ctas_per_sm(bool f32, bool single) { return f32 ? (single ? 5 : 6) : 4; }
+constexpr int near_ctas_per_sm(bool f32, bool single) { return f32 ? 5 : 4; }
 
 // ---------------------------------------------------------------- spectrum
 // Octant layout (all spectra): index ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.
@@ -230,7 +230,6 @@ struct HotDev {
   int near_ctas = 0;
   int32_t* cta_ptr1 = nullptr;   // [near_ctas1+1] the same for single-column launches
   int near_ctas1 = 0;
-  int dbg = 0;                   // experiments only (AIMX_DEBUG_NEAR)
   // grid buffers (complex, 4 channels innermost), `batch` slots each
   void* S = nullptr;             // [nlines][Nx][4] gathered grid sources
   void* bufA = nullptr;          // [Nz][Ny][2Nx][4]

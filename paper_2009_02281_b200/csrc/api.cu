@@ -234,7 +234,6 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32p, true) * nsm);
     h.cta_ptr1 = dupload(c, cp);
     h.near_ctas1 = (int)cp.size() - 1;
-    if (const char* e = std::getenv("AIMX_DEBUG_NEAR")) h.dbg = std::atoi(e);
   }
   c->near_R = grp.R;
   c->near_order = grp.order_kind;

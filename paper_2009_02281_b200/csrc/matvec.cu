@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
 #pragma unroll
       for (int i = 0; i < K::NPC; ++i) {
         const int e = lgid + i * NLG;
-        if (e < d.w) buf[i] = __ldg((const VT*)(xr + (int64_t)(h.dbg == 1 ? (e & 7) : ix[e]) * BB));
+        if (e < d.w) buf[i] = __ldg((const VT*)(xr + (int64_t)ix[e] * BB));
       }
     } else {
 #pragma unroll
@@ -583,8 +583,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
         }
       }
     }
-    if (h.dbg == 2) {
-    } else if (d.y & 1) {   // near correction: pairs [e][R]
+    if (d.y & 1) {   // near correction: pairs [e][R]
       const T2* __restrict__ cf = (const T2*)stg;
 #pragma unroll
       for (int i = 0; i < K::NPC; ++i) {
