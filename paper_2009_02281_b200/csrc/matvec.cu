@@ -389,6 +389,80 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
   }
 }
 
+// ---- fused y fwd -> (z fwd * H_hat * z inv) -> y inv for short y and z
+// transforms (2 N_y, 2 N_z <= 32): one CTA owns a tile of TW grid columns
+// (col = 4 kx + channel) and all (y, z) of them in shared memory, every line
+// transform is one thread's register DFT.  bufA[z][y < Ny][col] -> bufC[z][y
+// occupied][col]; the padded intermediate never leaves the SM.
+template <typename T, int LY, int LZ> struct YZGeom {
+  static constexpr int TW = 16;                          // columns per CTA
+  static constexpr int NT = 128;
+  static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (size_t)LZ * LY * TW;
+};
+
+template <typename T, int LY, int LZ>
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 4 : 2) k_yzconv(HotDev h) {
+  using T2 = typename CT<T>::T2;
+  using G = YZGeom<T, LY, LZ>;
+  constexpr int TW = G::TW, NT = G::NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* S = reinterpret_cast<T2*>(smem_raw);   // [z < LZ][ky < LY][TW]
+  const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, W = 8 * Nx;
+  const int b = blockIdx.y;
+  const int col0 = blockIdx.x * TW;
+  const T2* __restrict__ A = (const T2*)h.bufA + b * h.sA;
+  T2* __restrict__ C = (T2*)h.bufC + b * h.sA;
+  // phase 1: y forward of the z < Nz lines (zero for unoccupied planes)
+  for (int it = threadIdx.x; it < Nz * TW; it += NT) {
+    const int z = it / TW, w = it % TW;
+    T2 v[LY];
+    const bool occ = h.zocc[z];
+#pragma unroll
+    for (int y = 0; y < LY; ++y)
+      v[y] = (occ && y < Ny) ? A[((int64_t)z * Ny + y) * W + col0 + w] : mk<T2>(0, 0);
+    dftr<T2, LY, false>(v);
+#pragma unroll
+    for (int ky = 0; ky < LY; ++ky) S[(z * LY + ky) * TW + w] = v[ky];
+  }
+  __syncthreads();
+  // phase 2: z forward, spectrum multiply, z inverse (z < Nz kept)
+  const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
+  for (int it = threadIdx.x; it < LY * TW; it += NT) {
+    const int ky = it / TW, w = it % TW;
+    const int kx = (col0 + w) >> 2;
+    const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
+    const int kyf = ky <= Ny ? ky : 2 * Ny - ky;
+    T2 v[LZ];
+#pragma unroll
+    for (int z = 0; z < LZ; ++z) v[z] = z < Nz ? S[(z * LY + ky) * TW + w] : mk<T2>(0, 0);
+    dftr<T2, LZ, false>(v);
+    const T2* hl = Hb + (int64_t)kyf * (Nz + 1) * (Nx + 1) + kxf;
+#pragma unroll
+    for (int kz = 0; kz < LZ; ++kz) {
+      const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
+      v[kz] = cmul(v[kz], hl[(int64_t)kzf * (Nx + 1)]);
+    }
+    dftr<T2, LZ, true>(v);
+#pragma unroll
+    for (int z = 0; z < LZ; ++z)
+      if (z < Nz) S[(z * LY + ky) * TW + w] = v[z];
+  }
+  __syncthreads();
+  // phase 3: y inverse of the occupied planes, occupied lines stored
+  for (int it = threadIdx.x; it < Nz * TW; it += NT) {
+    const int z = it / TW, w = it % TW;
+    if (!h.zocc[z]) continue;
+    T2 v[LY];
+#pragma unroll
+    for (int ky = 0; ky < LY; ++ky) v[ky] = S[(z * LY + ky) * TW + w];
+    dftr<T2, LY, true>(v);
+    const uint8_t* occ = h.line_occ + (int64_t)z * Ny;
+#pragma unroll
+    for (int y = 0; y < LY; ++y)
+      if (y < Ny && occ[y]) C[((int64_t)z * Ny + y) * W + col0 + w] = v[y];
+  }
+}
+
 // ------------------------------------------------------------------ S4 + S5
 // Row groups (NearGroups): R spatially ordered testing functions share one
 // sorted union of their stencil nodes (interpolation W = P^T) and one
@@ -846,6 +920,33 @@ void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combin
   else run_interp_r<T, 8>(h, x, y0, y1, c, s);
 }
 
+// y fwd + z conv + y inv in one kernel when both transforms are short
+// (reported as stage 3, zconv)
+template <typename T, int LY, int LZ> void launch_yz(const HotDev& h, int B, cudaStream_t s) {
+  using G = YZGeom<T, LY, LZ>;
+  set_smem(k_yzconv<T, LY, LZ>, G::SMEM);
+  dim3 g((unsigned)(8 * h.Nx / G::TW), (unsigned)B);
+  k_yzconv<T, LY, LZ><<<g, G::NT, G::SMEM, s>>>(h);
+  AIMX_CHECK_LAUNCH();
+}
+template <typename T> bool run_yz_fused(const HotDev& h, int B, cudaStream_t s, Profiler* prof) {
+  const int Ly = 2 * h.Ny, Lz = 2 * h.Nz;
+  if (Ly > 32 || Lz > 32 || (8 * h.Nx) % YZGeom<T, 8, 8>::TW != 0 || Ly * Lz > 512) return false;
+  StageScope sc(prof, 3, s);
+  switch (Ly * 64 + Lz) {
+    case 8 * 64 + 8: launch_yz<T, 8, 8>(h, B, s); break;
+    case 16 * 64 + 8: launch_yz<T, 16, 8>(h, B, s); break;
+    case 32 * 64 + 8: launch_yz<T, 32, 8>(h, B, s); break;
+    case 8 * 64 + 16: launch_yz<T, 8, 16>(h, B, s); break;
+    case 16 * 64 + 16: launch_yz<T, 16, 16>(h, B, s); break;
+    case 32 * 64 + 16: launch_yz<T, 32, 16>(h, B, s); break;
+    case 8 * 64 + 32: launch_yz<T, 8, 32>(h, B, s); break;
+    case 16 * 64 + 32: launch_yz<T, 16, 32>(h, B, s); break;
+    default: return false;
+  }
+  return true;
+}
+
 template <typename T>
 void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
                 Profiler* prof) {
@@ -858,9 +959,11 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
     else run_gather_b<T>(h, B, s);
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, B, s)));
   }
-  { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, B, s))); }
-  { StageScope sc(prof, 3, s); AIMX_SWITCH_L(Lz, (run_z<T, L>(h, B, s))); }
-  { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, B, s))); }
+  if (!run_yz_fused<T>(h, B, s, prof)) {
+    { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, B, s))); }
+    { StageScope sc(prof, 3, s); AIMX_SWITCH_L(Lz, (run_z<T, L>(h, B, s))); }
+    { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, B, s))); }
+  }
   { StageScope sc(prof, 5, s); AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, B, s))); }
   { StageScope sc(prof, 6, s); run_interp<T>(h, x, y0, y1, c, s); }
 }
