@@ -196,6 +196,32 @@ aimx_status aimx_get_spectrum(const aimx_ctx* ctx, int which, double* out);
 aimx_status aimx_profile_enable(aimx_ctx* ctx, int on);
 aimx_status aimx_profile_read(aimx_ctx* ctx, double* ms, int64_t* launches, int64_t* kernels);
 
+/* ---- slab-decomposed FFT (multi-GPU for the largest grid) ----
+ * Host-only plan (no GPU needed): for `world` ranks, rank `rank` owns the
+ * unpadded grid rows y in [out[0], out[1]) (the RWGs whose stencil anchor row
+ * lies there: projection, x transforms, interpolation and near rows), needs
+ * potentials on rows [out[0], out[2]) (stencils reach `order` rows past the
+ * block) and transforms the padded kx slab [out[3], out[4]) along y and z.
+ * 2 N_x / world must be a power of two and N_y >= world (else UNSUPPORTED). */
+aimx_status aimx_slab_plan(const int32_t n[3], int32_t order, int32_t world, int32_t rank,
+                           int32_t out[6]);
+
+/* Slab-decomposed context.  nccl_id == NULL: EMULATION -- the `world` ranks
+ * all live in this context on one device and the two all-to-all exchanges of
+ * every matvec are device copies between them (same kernels, same exchange
+ * buffers as the NCCL path; for testing on one GPU).  nccl_id != NULL: this
+ * process is rank `rank` of `world`, one GPU each; nccl_id is the 128-byte
+ * ncclUniqueId from aimx_nccl_unique_id on rank 0, broadcast by the caller;
+ * the exchanges are grouped ncclSend/ncclRecv and the owned rows of y are
+ * summed over ranks with ncclAllReduce, so every rank returns the full y.
+ * matvec / matvec_parts / sweep / set_frequency then behave as for
+ * aimx_setup (x is replicated on every rank). */
+aimx_status aimx_setup_slab(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, aimx_prec prec,
+                            int device, int32_t rank, int32_t world, const uint8_t* nccl_id,
+                            void* stream, aimx_ctx** out);
+/* ncclGetUniqueId (NCCL loaded at run time; AIMX_E_UNSUPPORTED if absent). */
+aimx_status aimx_nccl_unique_id(uint8_t id[128]);
+
 void aimx_destroy(aimx_ctx* ctx);
 const char* aimx_status_string(aimx_status s);
 const char* aimx_last_error(const aimx_ctx* ctx);

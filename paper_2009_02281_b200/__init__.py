@@ -76,7 +76,28 @@ ABI_FUNCTIONS = {
     "aimx_last_error": (C.c_char_p, [_P]),
     "aimx_last_setup_error": (C.c_char_p, []),
     "aimx_version": (C.c_char_p, []),
+    "aimx_slab_plan": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P]),
+    "aimx_setup_slab": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Grid), C.c_int, C.c_int, C.c_int32,
+                                  C.c_int32, _P, _P, C.POINTER(_P)]),
+    "aimx_nccl_unique_id": (C.c_int, [_P]),
 }
+
+
+def slab_plan(n, order: int, world: int, rank: int) -> dict:
+    """Host-only slab decomposition of the grid (aimx_slab_plan; no GPU)."""
+    lib = load_library()
+    nn = (C.c_int32 * 3)(*[int(v) for v in n])
+    out = (C.c_int32 * 6)()
+    _check(lib, lib.aimx_slab_plan(C.cast(nn, _P), int(order), int(world), int(rank), C.cast(out, _P)))
+    return {"rows": (out[0], out[1]), "phi_rows": (out[0], out[2]), "kx": (out[3], out[4])}
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for aimx_setup_slab (call on rank 0, broadcast)."""
+    lib = load_library()
+    buf = (C.c_uint8 * 128)()
+    _check(lib, lib.aimx_nccl_unique_id(C.cast(buf, _P)))
+    return bytes(buf)
 
 
 def library_path() -> str:
@@ -118,7 +139,10 @@ class AIMx:
 
     def __init__(self, vertices, triangles, n, order: int = 2, near_cells: int = 2,
                  h: float = 0.0, origin=(0.0, 0.0, 0.0), prec: str = "c64",
-                 device: int | None = None, stream=None):
+                 device: int | None = None, stream=None, slab=None):
+        """slab: None (one GPU), ("emulate", world) (slab-decomposed FFT with
+        `world` ranks emulated on this GPU), or (rank, world, nccl_id) (this
+        process is one rank of the slab-decomposed FFT, NCCL)."""
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("AIMx needs a CUDA device (no CPU fallback)")
@@ -139,9 +163,19 @@ class AIMx:
             s = stream if stream is not None else torch.cuda.current_stream()
             self._stream = s
             ctx = _P()
-            st = self.lib.aimx_setup(C.byref(mesh), C.byref(g),
-                                     AIMX_C64 if prec == "c64" else AIMX_C128,
-                                     self.device, _P(s.cuda_stream), C.byref(ctx))
+            pc = AIMX_C64 if prec == "c64" else AIMX_C128
+            if slab is None:
+                st = self.lib.aimx_setup(C.byref(mesh), C.byref(g), pc, self.device,
+                                         _P(s.cuda_stream), C.byref(ctx))
+            elif slab[0] == "emulate":
+                st = self.lib.aimx_setup_slab(C.byref(mesh), C.byref(g), pc, self.device, 0,
+                                              int(slab[1]), None, _P(s.cuda_stream), C.byref(ctx))
+            else:
+                rank, world, nid = slab
+                idb = (C.c_uint8 * 128).from_buffer_copy(bytes(nid))
+                st = self.lib.aimx_setup_slab(C.byref(mesh), C.byref(g), pc, self.device, int(rank),
+                                              int(world), C.cast(idb, _P), _P(s.cuda_stream),
+                                              C.byref(ctx))
         _check(self.lib, st)
         self.ctx = ctx
         self.N = int(self.lib.aimx_num_unknowns(ctx))

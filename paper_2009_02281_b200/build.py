@@ -26,6 +26,22 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                  "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-Wall,-Wno-unknown-pragmas",
                  "-I" + os.path.join(ROOT, "include")]
 
+
+def _nccl_include():
+    """nccl.h of the NCCL torch loads (types only; the library dlopens NCCL)."""
+    try:
+        import nvidia.nccl as m
+        for base in list(getattr(m, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return ["-I" + inc]
+    except ImportError:
+        pass
+    return []
+
+
+COMMON = COMMON + _nccl_include()
+
 SOURCES = ["host_setup.cpp", "setup_kernels.cu", "spectrum.cu", "matvec.cu", "api.cu"]
 
 
@@ -62,7 +78,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
                 if p.returncode != 0:
                     raise RuntimeError(f"nvcc failed for {cmd[-3]}")
     if force or jobs or not os.path.exists(LIB):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-Xcompiler", "-fopenmp", "-lgomp"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-Xcompiler", "-fopenmp", "-lgomp", "-ldl"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or p.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)

@@ -29,10 +29,15 @@ struct Error : std::runtime_error {
 // Every kernel launch is followed by AIMX_CHECK_LAUNCH(), which also counts it
 // (aimx_profile_read reports the count).
 int64_t& launch_counter();
-#define AIMX_CHECK_LAUNCH()            \
-  do {                                 \
-    ++::aimx::launch_counter();        \
-    AIMX_CUDA(cudaGetLastError());     \
+#define AIMX_STR2(x) #x
+#define AIMX_STR(x) AIMX_STR2(x)
+#define AIMX_CHECK_LAUNCH()                                                                       \
+  do {                                                                                            \
+    ++::aimx::launch_counter();                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                          \
+    if (e_ != cudaSuccess)                                                                        \
+      throw ::aimx::Error(AIMX_E_CUDA, std::string("kernel launch at " __FILE__ ":" AIMX_STR(__LINE__) ": ") + \
+                                           cudaGetErrorString(e_));                              \
   } while (0)
 
 constexpr double kPi = 3.14159265358979323846;
@@ -86,7 +91,10 @@ struct NearGroups {
   std::vector<int64_t> wslot;      // [nb][p3] weight slot (w*R + r), -1 = exactly zero weight
 };
 
-void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, NearGroups& g);
+// rows: the testing functions grouped (empty = all); entries of other rows keep slot -1
+void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, NearGroups& g,
+                       const std::vector<int32_t>& rows = {});
+void nodemap_rows(const Topology& t, const NodeMap& full, int y0, int y1, NodeMap& m);
 
 // Work list of the S4+S5 kernel: chunks {group, flags, payload offset / 16,
 // count} (flags: bit0 = near (C) chunk, else interpolation (W) chunk; bit1
@@ -202,6 +210,9 @@ struct HotDev {
   // grid geometry
   int Nx = 0, Ny = 0, Nz = 0, p = 0, p3 = 0;
   int nb = 0, nocc = 0, nlines = 0, nzocc = 0;
+  int W = 0;                     // row width (complex) of the y / z passes: 8 Nx, or 4 x (kx slab width)
+  int kx0 = 0;                   // first kx of the column slab (slab-decomposed FFT), else 0
+  int32_t* phi_line = nullptr;   // [nlines] phi line (y + Ny z) of each x-inverse line; null: line_id
   int G = 8;                     // lanes per node in the projection gather
   int twy = 4, twz = 4;          // tile widths (complex elements) of the y / z passes
   int64_t nnz = 0;
@@ -243,6 +254,22 @@ struct HotDev {
   void* xt = nullptr;            // [nb][16] batch-interleaved right-hand sides (near SpMM)
 };
 
+// ---------------------------------------------------------------- slab-decomposed FFT
+// One rank of the y-slab / kx-slab decomposition (aimx_slab_plan): the
+// projection, x transforms and S4+S5 run on the rank's rows, the y / z
+// transforms on its kx slab; two all-to-all exchanges (NCCL, or device
+// copies between the virtual ranks of one process) re-partition the grid.
+struct SlabRank {
+  int rank = 0;
+  int y0 = 0, y1 = 0, yh1 = 0;   // owned rows [y0, y1); phi rows [y0, yh1)
+  int kx0 = 0, kx1 = 0;          // kx slab of the y / z passes
+  HotDev hr;                     // gather + x fwd on own rows (bufA: [Nz][y1-y0][2Nx][4]); S4+S5 of owned RWGs
+  HotDev hc;                     // y fwd / z conv / y inv on the kx slab ([Nz][Ny or 2Ny][4 (kx1-kx0)])
+  HotDev hx;                     // x inv of rows [y0, yh1) (bufC: [Nz][yh1-y0][2Nx][4]) -> phi
+  void* send = nullptr;          // exchange staging (both exchanges share it)
+  void* recv = nullptr;
+};
+
 // Per-launch batch arguments (by value).
 struct Combine {
   int B = 1;                     // frequency points in this launch (<= batch slots)
@@ -258,5 +285,16 @@ void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Co
                     cudaStream_t s, Profiler* prof);
 void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof);
+// Slab-decomposed hot path: every rank's S2-S5; the exchanges go through
+// `xchg` (step 0: rows -> kx slabs, step 1: kx slabs -> rows incl. halo).
+struct SlabExchange {
+  virtual void run(std::vector<SlabRank*>& ranks, int step, int B, size_t csize, cudaStream_t s) = 0;
+  virtual ~SlabExchange() {}
+};
+void slab_matvec(std::vector<SlabRank*>& ranks, int Ny, int Nz, int Nx, bool f32, SlabExchange& xchg,
+                 const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s, Profiler* prof);
+// block copy [d0][d1][d2][d3 complex] between strided layouts (strides in complex)
+void copy4(void* dst, const int64_t dstr[3], const void* src, const int64_t sstr[3], const int64_t dims[4],
+           size_t csize, cudaStream_t s);
 
 }  // namespace aimx

@@ -2,6 +2,7 @@
 // orchestration (host topology -> device fp64 static fill -> hot-path data),
 // frequency binding, matvec / sweep entry points and introspection.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -9,6 +10,11 @@
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <dlfcn.h>
+#include <memory>
+
+#include <nccl.h>   // types only: NCCL is loaded at run time (dlopen), see NcclApi
 
 #include "aimx_internal.h"
 
@@ -35,6 +41,16 @@ struct aimx_ctx {
   int near_R = 0, near_order = 0;
   int64_t near_union = 0;
   Profiler prof;
+  std::vector<uint8_t> nz;      // exactly-nonzero projection weights [N_b][p3]
+  // slab-decomposed FFT (aimx_setup_slab)
+  bool slab = false;
+  int world = 1, rank = 0;
+  std::vector<std::array<int, 5>> plans;   // per rank: y0, y1, yh1, kx0, kx1
+  std::vector<SlabRank> slabs;             // emulation: all ranks; NCCL: this rank
+  std::unique_ptr<SlabExchange> xchg;
+  void* comm = nullptr;                    // ncclComm_t
+  int slots = 0;
+  void* Hoct = nullptr;         // bound spectra [slots][noct], compute precision, scaled 1/M
   std::vector<void*> allocs;
   std::string last_error;
 };
@@ -104,7 +120,7 @@ template <typename T2>
 __global__ void k_pack_c(int64_t n, const int64_t* __restrict__ slot, const double* __restrict__ CA,
                          const double* __restrict__ CR, T2*, unsigned char* __restrict__ payload) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || slot[i] < 0) return;   // entries of rows outside this context's groups
   T2 v;
   v.x = CA[i];
   v.y = CR[i];
@@ -138,7 +154,8 @@ void* make_twiddles(aimx_ctx* c, int L) {
   return dupload(c, v);
 }
 
-void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid) {
+// ---- S0 common part: topology, fp64 static fill, weights, full node map
+void setup_static(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid) {
   Topology& t = c->topo;
   build_topology(mesh, grid, t);
   for (int a = 0; a < 3; ++a)
@@ -146,7 +163,6 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
       throw Error(AIMX_E_UNSUPPORTED, "2*N_a must be a power of two in [8, 1024]");
   const int64_t nb = t.nb, nnz = t.rowptr[nb], p3 = t.p3;
   SetupDev& d = c->sd;
-  // ---- upload topology
   d.V = dupload(c, t.V);
   d.T = dupload(c, t.T);
   d.ea = dupload(c, t.ea); d.eb = dupload(c, t.eb);
@@ -160,9 +176,8 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   uint8_t* nzf = dalloc<uint8_t>(c, nb * p3);
   launch_rwg_sides(t, d, c->stream);
   launch_weights(t, d, c->stream, nzf);
-  std::vector<uint8_t> nz((size_t)(nb * p3));
-  AIMX_CUDA(cudaMemcpyAsync(nz.data(), nzf, nz.size(), cudaMemcpyDeviceToHost, c->stream));
-  // ---- static near fill + precorrection (fp64)
+  c->nz.resize((size_t)(nb * p3));
+  AIMX_CUDA(cudaMemcpyAsync(c->nz.data(), nzf, c->nz.size(), cudaMemcpyDeviceToHost, c->stream));
   d.LA_un = dalloc<double>(c, nnz);
   d.YR_un = dalloc<double>(c, nnz);
   d.LA_NR = dalloc<double>(c, nnz);
@@ -174,143 +189,456 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   launch_static_near(t, d, c->stream);
   launch_precorrect(t, d, c->stream);
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
-  build_nodemap(t, nz, c->nodes);
-  // ---- hot-path data
-  HotDev& h = c->hot;
-  NodeMap& m = c->nodes;
+  build_nodemap(t, c->nz, c->nodes);
+  c->slots = 0;
+}
+
+// geometry common to every HotDev of the context
+void hot_common(aimx_ctx* c, HotDev& h) {
+  const Topology& t = c->topo;
   h.Nx = t.n[0]; h.Ny = t.n[1]; h.Nz = t.n[2];
+  h.W = 8 * h.Nx;
   h.p = t.p; h.p3 = t.p3;
-  h.nb = (int)nb;
-  h.nnz = nnz;
+  h.nb = (int)t.nb;
+  h.nnz = t.rowptr[t.nb];
+}
+
+// S2 gather structures of a node map (node-major projection entries)
+void build_gather(aimx_ctx* c, HotDev& h, const NodeMap& m) {
+  const Topology& t = c->topo;
   h.nocc = (int)m.node_lin.size();
   h.nlines = (int)m.line_id.size();
   h.nzocc = (int)m.zplanes.size();
-  std::vector<int32_t> base(nb);
-  for (int64_t e = 0; e < nb; ++e)
-    base[e] = t.anchor[3 * e] + t.n[0] * (t.anchor[3 * e + 1] + t.n[1] * t.anchor[3 * e + 2]);
-  h.rwg_base = dupload(c, base);
   h.node_lin = dupload(c, m.node_lin);
   h.node_ptr = dupload(c, m.node_ptr);
   h.node_line = dupload(c, m.node_line);
   h.ent_rwg = dupload(c, m.ent_rwg);
-  int32_t* ent_slot = dupload(c, m.ent_slot);
   h.line_id = dupload(c, m.line_id);
   h.zplanes = dupload(c, m.zplanes);
   h.line_occ = dupload(c, m.line_occ);
-  {
-    std::vector<uint8_t> zo(t.n[2], 0);
-    for (int z : m.zplanes) zo[z] = 1;
-    h.zocc = dupload(c, zo);
+  std::vector<uint8_t> zo(t.n[2], 0);
+  for (int z : m.zplanes) zo[z] = 1;
+  h.zocc = dupload(c, zo);
+  const int64_t nent = (int64_t)m.ent_rwg.size();
+  int32_t* ent_slot = dupload(c, m.ent_slot);
+  if (nent == 0) {   // a slab rank whose rows hold no occupied node
+    h.ent_w = dalloc<double4>(c, 1);
+  } else if (c->prec == AIMX_C64) {
+    h.ent_w = dalloc<float4>(c, nent);
+    k_ent_w<float4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)t.p3, h.ent_rwg, ent_slot, c->sd.lam,
+                                                      (float4*)h.ent_w);
+  } else {
+    h.ent_w = dalloc<double4>(c, nent);
+    k_ent_w<double4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)t.p3, h.ent_rwg, ent_slot, c->sd.lam,
+                                                       (double4*)h.ent_w);
   }
-  // near matrix in row-group form (host ordering and unions; values scattered on device)
+  if (nent > 0) AIMX_CHECK_LAUNCH();
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  dfree(c, ent_slot, nent * (int64_t)sizeof(int32_t));
+  const double avg = h.nocc > 0 ? (double)nent / h.nocc : 1.0;
+  int G = 4;
+  while (G < 32 && G < avg) G *= 2;
+  h.G = G;
+}
+
+// S4+S5 structures for the testing functions `rows` (empty: all)
+void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
+  const Topology& t = c->topo;
+  const int64_t nb = t.nb, nnz = t.rowptr[nb], p3 = t.p3;
+  std::vector<int32_t> base(nb);
+  for (int64_t e = 0; e < nb; ++e)
+    base[e] = t.anchor[3 * e] + t.n[0] * (t.anchor[3 * e + 1] + t.n[1] * t.anchor[3 * e + 2]);
+  h.rwg_base = dupload(c, base);
   NearGroups grp;
-  build_near_groups(t, nz, grp);
+  build_near_groups(t, c->nz, grp, rows);
   if (grp.ptr.back() > (int64_t)INT32_MAX || grp.wptr.back() > (int64_t)INT32_MAX)
     throw Error(AIMX_E_GRID, "near matrix too large");
   h.R = grp.R;
   h.ngrp = (int)grp.ngrp;
   h.grp_rows = dupload(c, grp.rows);
-  const int64_t nU = grp.ptr.back(), nUw = grp.wptr.back();
-  int64_t* gslot = nullptr;
-  int64_t* wslot = nullptr;
-  {
-    int nsm = 148;
-    AIMX_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-    NearChunks ck;
-    const bool f32p = c->prec == AIMX_C64;
-    const int cs = f32p ? 8 : 16;
-    build_near_chunks(grp, f32p ? 32 : 16, f32p ? 128 : 64, cs, ck);
-    // value slot (u R + r) -> payload byte offset
-    for (auto& v : grp.slot) v = ck.uoff_c[v / grp.R] + (v % grp.R) * cs;
-    for (auto& v : grp.wslot)
-      if (v >= 0) v = ck.uoff_w[v / grp.R] + (v % grp.R) * 2 * cs;
-    gslot = dupload(c, grp.slot);
-    wslot = dupload(c, grp.wslot);
-    h.payload = dupload(c, ck.payload);
-    h.chunks = dupload(c, ck.chunks);
-    std::vector<int32_t> cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32p, false) * nsm);
-    h.cta_ptr = dupload(c, cp);
-    h.near_ctas = (int)cp.size() - 1;
-    cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32p, true) * nsm);
-    h.cta_ptr1 = dupload(c, cp);
-    h.near_ctas1 = (int)cp.size() - 1;
-  }
-  c->near_R = grp.R;
-  c->near_order = grp.order_kind;
-  c->near_union = nU;
-  const int64_t nent = (int64_t)m.ent_rwg.size();
-  const int64_t ng = (int64_t)h.Nx * h.Ny * h.Nz;
+  int nsm = 148;
+  AIMX_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  NearChunks ck;
   const bool f32 = c->prec == AIMX_C64;
-  const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
+  const int cs = f32 ? 8 : 16;
+  build_near_chunks(grp, f32 ? 32 : 16, f32 ? 128 : 64, cs, ck);
+  // value slot (u R + r) -> payload byte offset
+  for (auto& v : grp.slot)
+    if (v >= 0) v = ck.uoff_c[v / grp.R] + (v % grp.R) * cs;
+  for (auto& v : grp.wslot)
+    if (v >= 0) v = ck.uoff_w[v / grp.R] + (v % grp.R) * 2 * cs;
+  int64_t* gslot = dupload(c, grp.slot);
+  int64_t* wslot = dupload(c, grp.wslot);
+  h.payload = dupload(c, ck.payload);
+  h.chunks = dupload(c, ck.chunks);
+  std::vector<int32_t> cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, false) * nsm);
+  h.cta_ptr = dupload(c, cp);
+  h.near_ctas = (int)cp.size() - 1;
+  cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, true) * nsm);
+  h.cta_ptr1 = dupload(c, cp);
+  h.near_ctas1 = (int)cp.size() - 1;
+  const SetupDev& d = c->sd;
   if (f32) {
-    h.ent_w = dalloc<float4>(c, nent);
     k_lam_to<float4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (float4*)nullptr, h.payload);
-    k_ent_w<float4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)p3, h.ent_rwg, ent_slot, d.lam,
-                                                      (float4*)h.ent_w);
     k_pack_c<float2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (float2*)nullptr, h.payload);
   } else {
-    h.ent_w = dalloc<double4>(c, nent);
     k_lam_to<double4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (double4*)nullptr, h.payload);
-    k_ent_w<double4><<<nblk(nent), 256, 0, c->stream>>>(nent, (int)p3, h.ent_rwg, ent_slot, d.lam,
-                                                       (double4*)h.ent_w);
     k_pack_c<double2><<<nblk(nnz), 256, 0, c->stream>>>(nnz, gslot, d.CA, d.CR, (double2*)nullptr, h.payload);
   }
   AIMX_CHECK_LAUNCH();
-  // ---- batch slots and grid buffers
-  const int64_t nS = (int64_t)h.nlines * h.Nx * 4;
-  const int64_t nA = (int64_t)h.Nz * h.Ny * 2 * h.Nx * 4;
-  const int64_t nB = (int64_t)h.Nz * 2 * h.Ny * 2 * h.Nx * 4;
-  const int64_t nP = ng * 4;
-  const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  dfree(c, gslot, nnz * (int64_t)sizeof(int64_t));
+  dfree(c, wslot, nb * p3 * (int64_t)sizeof(int64_t));
+  if (rows.empty() || c->near_R == 0) {
+    c->near_R = grp.R;
+    c->near_order = grp.order_kind;
+  }
+  c->near_union += grp.ptr.back();
+}
+
+// batch slots from the full-grid per-frequency footprint (<= 1.5 GB of buffers)
+int choose_slots(aimx_ctx* c) {
+  const Topology& t = c->topo;
+  const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
+  const int64_t Nx = t.n[0], Ny = t.n[1], Nz = t.n[2];
+  const int64_t nS = (int64_t)c->nodes.line_id.size() * Nx * 4;
+  const int64_t nA = Nz * Ny * 2 * Nx * 4, nB = Nz * 2 * Ny * 2 * Nx * 4, nP = Nx * Ny * Nz * 4;
+  const int64_t noct = (Nx + 1) * (Ny + 1) * (Nz + 1);
   const int64_t per_freq = (int64_t)cs * (nS + 2 * nA + nB + nP + noct) + 2 * (int64_t)sizeof(double2) * noct;
   int slots = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)(1536ll << 20) / per_freq));
   if (const char* e = std::getenv("AIMX_BATCH")) slots = std::max(1, std::min(kMaxBatch, std::atoi(e)));
   while (slots & (slots - 1)) slots &= slots - 1;   // power of two (batch buckets never exceed it)
-  h.batch = slots;
-  h.sS = nS; h.sA = nA; h.sB = nB; h.sP = nP; h.sH = noct;
-  h.S = dalloc<char>(c, nS * slots * (int64_t)cs);
-  h.bufA = dalloc<char>(c, nA * slots * (int64_t)cs);
-  h.bufB = dalloc<char>(c, nB * slots * (int64_t)cs);
-  h.bufC = dalloc<char>(c, nA * slots * (int64_t)cs);
-  h.phi = dalloc<char>(c, nP * slots * (int64_t)cs + 64);   // + 64: 16-byte row blocks may overhang
-  AIMX_CUDA(cudaMemsetAsync(h.S, 0, nS * slots * cs, c->stream));
-  AIMX_CUDA(cudaMemsetAsync(h.bufA, 0, nA * slots * cs, c->stream));
-  AIMX_CUDA(cudaMemsetAsync(h.bufB, 0, nB * slots * cs, c->stream));
-  AIMX_CUDA(cudaMemsetAsync(h.bufC, 0, nA * slots * cs, c->stream));
-  AIMX_CUDA(cudaMemsetAsync(h.phi, 0, nP * slots * cs, c->stream));
-  h.twx = make_twiddles(c, 2 * h.Nx);
-  h.twy_tab = make_twiddles(c, 2 * h.Ny);
-  h.twz_tab = make_twiddles(c, 2 * h.Nz);
-  h.twy = pick_tile(2 * h.Ny, 8 * h.Nx, f32);
-  h.twz = pick_tile(2 * h.Nz, 8 * h.Nx, f32);
-  {
-    const double avg = h.nocc > 0 ? (double)nent / h.nocc : 1.0;
-    int G = 4;
-    while (G < 32 && G < avg) G *= 2;
-    h.G = G;
-  }
-  // ---- static spectrum
-  c->sp.Nx = h.Nx; c->sp.Ny = h.Ny; c->sp.Nz = h.Nz; c->sp.h = t.h;
-  spectrum_plan_init(c->sp, slots, c->stream);
+  return slots;
+}
+
+template <typename P> P* zalloc(aimx_ctx* c, int64_t bytes) {
+  P* p = (P*)dalloc<char>(c, bytes);
+  AIMX_CUDA(cudaMemsetAsync(p, 0, bytes, c->stream));
+  return p;
+}
+
+// static spectrum (fp64, and its compute-precision copy) and the spectrum plan
+void setup_spectrum(aimx_ctx* c) {
+  const Topology& t = c->topo;
+  const int64_t noct = (int64_t)(t.n[0] + 1) * (t.n[1] + 1) * (t.n[2] + 1);
+  c->sp.Nx = t.n[0]; c->sp.Ny = t.n[1]; c->sp.Nz = t.n[2]; c->sp.h = t.h;
+  spectrum_plan_init(c->sp, c->slots, c->stream);
   c->Hs = dalloc<double2>(c, noct);
   spectrum_static(c->sp, c->Hs, c->stream);
-  if (f32) {
+  if (c->prec == AIMX_C64) {
     c->Hs_T = dalloc<float2>(c, noct);
     k_d2f<<<nblk(noct), 256, 0, c->stream>>>(noct, c->Hs, (float2*)c->Hs_T);
     AIMX_CHECK_LAUNCH();
   } else {
     c->Hs_T = c->Hs;
   }
-  h.Hoct = dalloc<char>(c, noct * slots * (int64_t)cs);
-  h.xt = dalloc<char>(c, (int64_t)nb * kMaxBatch * (int64_t)cs + 64);
+  const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
+  c->Hoct = dalloc<char>(c, noct * c->slots * (int64_t)cs);
+}
+
+void finish_setup(aimx_ctx* c) {
+  const Topology& t = c->topo;
+  const int64_t nnz = t.rowptr[t.nb];
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
-  dfree(c, gslot, nnz * (int64_t)sizeof(int64_t));
-  dfree(c, wslot, nb * p3 * (int64_t)sizeof(int64_t));
-  dfree(c, d.LA_un, nnz * sizeof(double));
-  dfree(c, d.YR_un, nnz * sizeof(double));
+  dfree(c, c->sd.LA_un, nnz * (int64_t)sizeof(double));
+  dfree(c, c->sd.YR_un, nnz * (int64_t)sizeof(double));
   AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_spec, cudaEventDisableTiming));
   AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_use, cudaEventDisableTiming));
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid) {
+  setup_static(c, mesh, grid);
+  const Topology& t = c->topo;
+  HotDev& h = c->hot;
+  hot_common(c, h);
+  build_gather(c, h, c->nodes);
+  build_near(c, h, {});
+  // ---- batch slots and grid buffers
+  const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
+  const int slots = c->slots = choose_slots(c);
+  const int64_t nS = (int64_t)h.nlines * h.Nx * 4;
+  const int64_t nA = (int64_t)h.Nz * h.Ny * 2 * h.Nx * 4;
+  const int64_t nB = (int64_t)h.Nz * 2 * h.Ny * 2 * h.Nx * 4;
+  const int64_t nP = (int64_t)h.Nx * h.Ny * h.Nz * 4;
+  const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
+  h.batch = slots;
+  h.sS = nS; h.sA = nA; h.sB = nB; h.sP = nP; h.sH = noct;
+  h.S = zalloc<char>(c, nS * slots * (int64_t)cs);
+  h.bufA = zalloc<char>(c, nA * slots * (int64_t)cs);
+  h.bufB = zalloc<char>(c, nB * slots * (int64_t)cs);
+  h.bufC = zalloc<char>(c, nA * slots * (int64_t)cs);
+  h.phi = zalloc<char>(c, nP * slots * (int64_t)cs + 64);
+  h.twx = make_twiddles(c, 2 * h.Nx);
+  h.twy_tab = make_twiddles(c, 2 * h.Ny);
+  h.twz_tab = make_twiddles(c, 2 * h.Nz);
+  setup_spectrum(c);
+  h.Hoct = c->Hoct;
+  h.xt = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
+  finish_setup(c);
+}
+
+// ---- NCCL, loaded at run time (the library itself does not link it)
+struct NcclApi {
+  void* lib = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    for (const char* n : names)
+      if ((api.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL)) != nullptr) break;
+    if (!api.lib) return;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(api.lib, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(api.lib, "ncclCommInitRank");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(api.lib, "ncclCommDestroy");
+    api.send = (decltype(api.send))dlsym(api.lib, "ncclSend");
+    api.recv = (decltype(api.recv))dlsym(api.lib, "ncclRecv");
+    api.groupStart = (decltype(api.groupStart))dlsym(api.lib, "ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))dlsym(api.lib, "ncclGroupEnd");
+    api.allReduce = (decltype(api.allReduce))dlsym(api.lib, "ncclAllReduce");
+    api.errorString = (decltype(api.errorString))dlsym(api.lib, "ncclGetErrorString");
+  });
+  if (!api.lib || !api.getUniqueId || !api.commInitRank || !api.send || !api.recv || !api.groupStart ||
+      !api.groupEnd || !api.allReduce)
+    throw Error(AIMX_E_UNSUPPORTED, "NCCL (libnccl.so.2) could not be loaded");
+  return api;
+}
+#define AIMX_NCCL(call)                                                                        \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess)                                                                     \
+      throw Error(AIMX_E_CUDA, std::string("NCCL: ") + (nccl().errorString ? nccl().errorString(r_) : "error")); \
+  } while (0)
+
+// Exchange geometry.  Step 0 (rows -> kx slabs): rank p sends rank q the
+// block [slot][z][y in p's rows][4 kx in q's slab] of its x-transformed rows;
+// q stores it in rows y0_p.. of its column buffer.  Step 1 (kx slabs -> rows):
+// rank q sends rank p the block [slot][z][y in [y0_p, yh1_p)][4 kx in q's slab]
+// of its y-inverse buffer; p stores it at kx0_q of its row buffer.
+struct XchgGeom {
+  const aimx_ctx* c;
+  int64_t Nz, Ny, Nx;
+  int64_t rows(int p, int step) const { const auto& q = c->plans[p]; return step == 0 ? q[1] - q[0] : q[2] - q[0]; }
+  int64_t W(int q) const { return 4 * (int64_t)(c->plans[q][4] - c->plans[q][3]); }
+  // complex per block from src to dst for B slots
+  int64_t block(int src, int dst, int step, int B) const {
+    return step == 0 ? B * Nz * rows(src, 0) * W(dst) : B * Nz * rows(dst, 1) * W(src);
+  }
+  int64_t send_off(int src, int dst, int step, int B) const {
+    int64_t o = 0;
+    for (int q = 0; q < dst; ++q) o += block(src, q, step, B);
+    return o;
+  }
+  int64_t recv_off(int dst, int src, int step, int B) const {
+    int64_t o = 0;
+    for (int p = 0; p < src; ++p) o += block(p, dst, step, B);
+    return o;
+  }
+  void pack(SlabRank& r, int dst, int step, int B, size_t cs, cudaStream_t s) const {
+    const int p = r.rank;
+    char* out = (char*)r.send + send_off(p, dst, step, B) * (int64_t)cs;
+    const int64_t Wd = W(dst), Wp = W(p);
+    if (step == 0) {   // from the row buffer (x-transformed rows) -> [B][Nz][rows_p][W_dst]
+      const int64_t rp = rows(p, 0);
+      const int64_t d[4] = {B, Nz, rp, Wd}, so[3] = {r.hr.sA, rp * 8 * Nx, 8 * Nx}, to[3] = {Nz * rp * Wd, rp * Wd, Wd};
+      copy4(out, to, (const char*)r.hr.bufA + 4 * (int64_t)c->plans[dst][3] * (int64_t)cs, so, d, cs, s);
+    } else {           // from the column buffer rows [y0_dst, yh1_dst) -> [B][Nz][rows_dst][W_p]
+      const int64_t rd = rows(dst, 1);
+      const int64_t d[4] = {B, Nz, rd, Wp}, so[3] = {r.hc.sA, Ny * Wp, Wp}, to[3] = {Nz * rd * Wp, rd * Wp, Wp};
+      copy4(out, to, (const char*)r.hc.bufC + (int64_t)c->plans[dst][0] * Wp * (int64_t)cs, so, d, cs, s);
+    }
+  }
+  void unpack(SlabRank& r, int src, int step, int B, size_t cs, cudaStream_t s) const {
+    const int q = r.rank;
+    const char* in = (const char*)r.recv + recv_off(q, src, step, B) * (int64_t)cs;
+    if (step == 0) {   // [B][Nz][rows_src][W_q] -> column buffer rows y0_src..
+      const int64_t rs = rows(src, 0), Wq = W(q);
+      const int64_t d[4] = {B, Nz, rs, Wq}, so[3] = {Nz * rs * Wq, rs * Wq, Wq}, to[3] = {r.hc.sA, Ny * Wq, Wq};
+      copy4((char*)r.hc.bufA + (int64_t)c->plans[src][0] * Wq * (int64_t)cs, to, in, so, d, cs, s);
+    } else {           // [B][Nz][rows_q][W_src] -> row buffer at kx0_src
+      const int64_t rq = rows(q, 1), Ws = W(src);
+      const int64_t d[4] = {B, Nz, rq, Ws}, so[3] = {Nz * rq * Ws, rq * Ws, Ws}, to[3] = {r.hx.sA, rq * 8 * Nx, 8 * Nx};
+      copy4((char*)r.hx.bufC + 4 * (int64_t)c->plans[src][3] * (int64_t)cs, to, in, so, d, cs, s);
+    }
+  }
+};
+
+// all ranks in this process: pack, device copies between the virtual ranks, unpack
+struct EmulatedExchange : SlabExchange {
+  XchgGeom g;
+  explicit EmulatedExchange(const XchgGeom& g_) : g(g_) {}
+  void run(std::vector<SlabRank*>& ranks, int step, int B, size_t cs, cudaStream_t s) override {
+    const int P = (int)ranks.size();
+    for (SlabRank* r : ranks)
+      for (int q = 0; q < P; ++q) g.pack(*r, q, step, B, cs, s);
+    for (SlabRank* src : ranks)
+      for (SlabRank* dst : ranks) {
+        const int64_t n = g.block(src->rank, dst->rank, step, B);
+        if (n > 0)
+          AIMX_CUDA(cudaMemcpyAsync((char*)dst->recv + g.recv_off(dst->rank, src->rank, step, B) * (int64_t)cs,
+                                    (const char*)src->send + g.send_off(src->rank, dst->rank, step, B) * (int64_t)cs,
+                                    n * cs, cudaMemcpyDeviceToDevice, s));
+      }
+    for (SlabRank* r : ranks)
+      for (int p = 0; p < P; ++p) g.unpack(*r, p, step, B, cs, s);
+  }
+};
+
+// this process is one rank: pack, grouped ncclSend / ncclRecv, unpack
+struct NcclExchange : SlabExchange {
+  XchgGeom g;
+  int world;
+  ncclComm_t comm;
+  NcclExchange(const XchgGeom& g_, int w, ncclComm_t cm) : g(g_), world(w), comm(cm) {}
+  void run(std::vector<SlabRank*>& ranks, int step, int B, size_t cs, cudaStream_t s) override {
+    SlabRank& r = *ranks[0];
+    for (int q = 0; q < world; ++q) g.pack(r, q, step, B, cs, s);
+    NcclApi& api = nccl();
+    AIMX_NCCL(api.groupStart());
+    for (int q = 0; q < world; ++q) {
+      const int64_t ns = g.block(r.rank, q, step, B) * (int64_t)cs, nr = g.block(q, r.rank, step, B) * (int64_t)cs;
+      if (ns > 0)
+        AIMX_NCCL(api.send((const char*)r.send + g.send_off(r.rank, q, step, B) * (int64_t)cs, (size_t)ns,
+                           ncclInt8, q, comm, s));
+      if (nr > 0)
+        AIMX_NCCL(api.recv((char*)r.recv + g.recv_off(r.rank, q, step, B) * (int64_t)cs, (size_t)nr, ncclInt8,
+                           q, comm, s));
+    }
+    AIMX_NCCL(api.groupEnd());
+    for (int p = 0; p < world; ++p) g.unpack(r, p, step, B, cs, s);
+  }
+};
+
+void do_setup_slab(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, int rank, int world,
+                   const uint8_t* nccl_id) {
+  setup_static(c, mesh, grid);
+  const Topology& t = c->topo;
+  const int Nx = t.n[0], Ny = t.n[1], Nz = t.n[2];
+  c->slab = true;
+  c->world = world;
+  c->rank = nccl_id ? rank : 0;
+  for (int r = 0; r < world; ++r) {
+    int32_t o[6];
+    aimx_status st = aimx_slab_plan(t.n, t.order, world, r, o);
+    if (st != AIMX_OK) throw Error(st, "slab plan: 2 N_x / world must be a power of two and N_y >= world");
+    c->plans.push_back({o[0], o[1], o[2], o[3], o[4]});
+  }
+  hot_common(c, c->hot);
+  const int slots = c->slots = choose_slots(c);
+  c->hot.batch = slots;
+  setup_spectrum(c);
+  const bool f32 = c->prec == AIMX_C64;
+  const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
+  const int64_t noct = (int64_t)(Nx + 1) * (Ny + 1) * (Nz + 1);
+  const NodeMap& full = c->nodes;
+  std::vector<uint8_t> zo(Nz, 0);
+  for (int z : full.zplanes) zo[z] = 1;
+  XchgGeom geo{c, Nz, Ny, Nx};
+  std::vector<int> mine;
+  if (nccl_id) mine.push_back(rank);
+  else for (int r = 0; r < world; ++r) mine.push_back(r);
+  c->slabs.resize(mine.size());
+  for (size_t i = 0; i < mine.size(); ++i) {
+    SlabRank& R = c->slabs[i];
+    const auto& pl = c->plans[mine[i]];
+    R.rank = mine[i];
+    R.y0 = pl[0]; R.y1 = pl[1]; R.yh1 = pl[2]; R.kx0 = pl[3]; R.kx1 = pl[4];
+    const int ny = R.y1 - R.y0, nyh = R.yh1 - R.y0, W = 4 * (R.kx1 - R.kx0);
+    // rows: gather + x fwd, S4+S5 of the RWGs anchored in the rows
+    HotDev& hr = R.hr;
+    hot_common(c, hr);
+    NodeMap m;
+    nodemap_rows(t, full, R.y0, R.y1, m);
+    build_gather(c, hr, m);
+    std::vector<int32_t> owned;
+    for (int64_t e = 0; e < t.nb; ++e)
+      if (t.anchor[3 * e + 1] >= R.y0 && t.anchor[3 * e + 1] < R.y1) owned.push_back((int32_t)e);
+    if (!owned.empty()) build_near(c, hr, owned);
+    hr.batch = slots;
+    hr.sS = (int64_t)hr.nlines * Nx * 4;
+    hr.sA = (int64_t)Nz * ny * 2 * Nx * 4;
+    hr.sP = (int64_t)Nx * Ny * Nz * 4;
+    hr.S = zalloc<char>(c, hr.sS * slots * (int64_t)cs + 64);
+    hr.bufA = zalloc<char>(c, hr.sA * slots * (int64_t)cs);
+    hr.phi = zalloc<char>(c, hr.sP * slots * (int64_t)cs + 64);
+    hr.twx = make_twiddles(c, 2 * Nx);
+    hr.xt = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
+    // kx slab: y / z passes over all (y, z)
+    HotDev& hc = R.hc;
+    hot_common(c, hc);
+    hc.W = W;
+    hc.kx0 = R.kx0;
+    hc.nzocc = (int)full.zplanes.size();
+    hc.zplanes = dupload(c, full.zplanes);
+    hc.zocc = dupload(c, zo);
+    hc.line_occ = dupload(c, full.line_occ);
+    hc.batch = slots;
+    hc.sA = (int64_t)Nz * Ny * W;
+    hc.sB = (int64_t)Nz * 2 * Ny * W;
+    hc.sH = noct;
+    hc.bufA = zalloc<char>(c, hc.sA * slots * (int64_t)cs);
+    hc.bufB = zalloc<char>(c, hc.sB * slots * (int64_t)cs);
+    hc.bufC = zalloc<char>(c, hc.sA * slots * (int64_t)cs);
+    hc.Hoct = c->Hoct;
+    hc.twy_tab = make_twiddles(c, 2 * Ny);
+    hc.twz_tab = make_twiddles(c, 2 * Nz);
+    // x inverse of rows [y0, yh1) into phi (global line numbering)
+    HotDev& hx = R.hx;
+    hot_common(c, hx);
+    std::vector<int32_t> lid, plid;
+    for (int32_t line : full.line_id) {
+      const int y = line % Ny, z = line / Ny;
+      if (y >= R.y0 && y < R.yh1) {
+        lid.push_back((y - R.y0) + nyh * z);
+        plid.push_back(line);
+      }
+    }
+    hx.nlines = (int)lid.size();
+    hx.line_id = dupload(c, lid);
+    hx.phi_line = dupload(c, plid);
+    hx.batch = slots;
+    hx.sA = (int64_t)Nz * nyh * 2 * Nx * 4;
+    hx.bufC = zalloc<char>(c, hx.sA * slots * (int64_t)cs);
+    hx.phi = hr.phi;
+    hx.twx = hr.twx;
+    // exchange staging: the larger of the two steps, send and receive
+    int64_t sn = 0, rn = 0;
+    for (int step = 0; step < 2; ++step) {
+      int64_t a = 0, b = 0;
+      for (int q = 0; q < world; ++q) {
+        a += geo.block(R.rank, q, step, slots);
+        b += geo.block(q, R.rank, step, slots);
+      }
+      sn = std::max(sn, a);
+      rn = std::max(rn, b);
+    }
+    R.send = dalloc<char>(c, sn * (int64_t)cs + 64);
+    R.recv = dalloc<char>(c, rn * (int64_t)cs + 64);
+  }
+  if (nccl_id) {
+    NcclApi& api = nccl();
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    AIMX_NCCL(api.commInitRank(&comm, world, id, rank));
+    c->comm = comm;
+    c->xchg.reset(new NcclExchange(geo, world, comm));
+  } else {
+    c->xchg.reset(new EmulatedExchange(geo));
+  }
+  finish_setup(c);
 }
 
 // S1 for B frequency points into spectrum slots 0..B-1.
@@ -324,9 +652,9 @@ void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s) {
   const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
   StageScope sc(&c->prof, 0, s);
   if (c->prec == AIMX_C64)
-    spectrum_dynamic_f32(c->sp, B, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)h.Hoct, s);
+    spectrum_dynamic_f32(c->sp, B, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)c->Hoct, s);
   else
-    spectrum_dynamic_f64(c->sp, B, k0, c->Hs, 1.0 / M, (double2*)h.Hoct, s);
+    spectrum_dynamic_f64(c->sp, B, k0, c->Hs, 1.0 / M, (double2*)c->Hoct, s);
 }
 
 void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
@@ -352,8 +680,32 @@ Combine make_combine(int B, const double* f, int mode, int64_t nb) {
   return cb;
 }
 
+// slab contexts: every rank's part; NCCL: owned rows summed over ranks
+void run_slab(aimx_ctx* c, const void* x, void* y0, void* y1, const Combine& cb, cudaStream_t s) {
+  const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
+  const size_t ybytes = (size_t)cb.B * c->hot.nb * cs;
+  if (c->comm) {   // rows owned elsewhere stay zero before the sum
+    if (y0) AIMX_CUDA(cudaMemsetAsync(y0, 0, ybytes, s));
+    if (y1) AIMX_CUDA(cudaMemsetAsync(y1, 0, ybytes, s));
+  }
+  std::vector<SlabRank*> rk;
+  for (auto& r : c->slabs) rk.push_back(&r);
+  slab_matvec(rk, c->topo.n[1], c->topo.n[2], c->topo.n[0], c->prec == AIMX_C64, *c->xchg, x, y0, y1, cb, s,
+              &c->prof);
+  if (c->comm) {
+    NcclApi& api = nccl();
+    const ncclDataType_t dt = c->prec == AIMX_C64 ? ncclFloat32 : ncclFloat64;
+    const size_t n = (size_t)cb.B * c->hot.nb * 2;
+    AIMX_NCCL(api.groupStart());
+    if (y0) AIMX_NCCL(api.allReduce(y0, y0, n, dt, ncclSum, (ncclComm_t)c->comm, s));
+    if (y1) AIMX_NCCL(api.allReduce(y1, y1, n, dt, ncclSum, (ncclComm_t)c->comm, s));
+    AIMX_NCCL(api.groupEnd());
+  }
+}
+
 void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaStream_t s) {
   Combine cb = make_combine(1, &c->f, mode, c->hot.nb);
+  if (c->slab) return run_slab(c, x, y0, y1, cb, s);
   if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, s, &c->prof);
   else hot_matvec_f64(c->hot, x, y0, y1, cb, s, &c->prof);
 }
@@ -362,6 +714,7 @@ void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaSt
 void run_batch(aimx_ctx* c, int B, const double* f, const void* X, void* Y, cudaStream_t s) {
   spectra(c, B, f, s);
   Combine cb = make_combine(B, f, 0, c->hot.nb);
+  if (c->slab) return run_slab(c, X, Y, nullptr, cb, s);
   if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, X, Y, nullptr, cb, s, &c->prof);
   else hot_matvec_f64(c->hot, X, Y, nullptr, cb, s, &c->prof);
 }
@@ -383,6 +736,12 @@ void destroy_impl(aimx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) {
+    try {
+      nccl().commDestroy((ncclComm_t)c->comm);
+    } catch (...) {
+    }
+  }
   for (void* p : c->allocs) if (p) cudaFree(p);
   spectrum_plan_free(c->sp);
   if (c->stage) cudaFree(c->stage);
@@ -439,6 +798,53 @@ aimx_status aimx_setup(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, a
     g_setup_error = e.what();
     destroy_impl(c);
     return AIMX_E_INTERNAL;
+  }
+}
+
+aimx_status aimx_setup_slab(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, aimx_prec prec, int device,
+                            int32_t rank, int32_t world, const uint8_t* nccl_id, void* stream, aimx_ctx** out) {
+  g_setup_error.clear();
+  if (!out) { g_setup_error = "out is NULL"; return AIMX_E_INVALID_ARG; }
+  *out = nullptr;
+  if (prec != AIMX_C64 && prec != AIMX_C128) { g_setup_error = "bad precision"; return AIMX_E_INVALID_ARG; }
+  if (world < 1 || rank < 0 || rank >= world) { g_setup_error = "bad rank / world"; return AIMX_E_INVALID_ARG; }
+  aimx_ctx* c = nullptr;
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    AIMX_CUDA(cudaSetDevice(device));
+    c = new aimx_ctx;
+    c->device = device;
+    c->prec = prec;
+    c->stream = (cudaStream_t)stream;
+    do_setup_slab(c, mesh, grid, rank, world, nccl_id);
+    c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = c;
+    return AIMX_OK;
+  } catch (const Error& e) {
+    g_setup_error = e.what();
+    destroy_impl(c);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_setup_error = "host allocation failed";
+    destroy_impl(c);
+    return AIMX_E_OOM;
+  } catch (const std::exception& e) {
+    g_setup_error = e.what();
+    destroy_impl(c);
+    return AIMX_E_INTERNAL;
+  }
+}
+
+aimx_status aimx_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return AIMX_E_INVALID_ARG;
+  try {
+    ncclUniqueId u;
+    AIMX_NCCL(nccl().getUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+    return AIMX_OK;
+  } catch (const Error& e) {
+    g_setup_error = e.what();
+    return e.code;
   }
 }
 
@@ -651,10 +1057,10 @@ aimx_status aimx_get_spectrum(const aimx_ctx* cc, int which, double* out) {
     const double M = 8.0 * (double)c->hot.Nx * c->hot.Ny * c->hot.Nz;
     if (c->prec == AIMX_C64) {
       std::vector<float2> tmp(n);
-      AIMX_CUDA(cudaMemcpy(tmp.data(), c->hot.Hoct, n * sizeof(float2), cudaMemcpyDeviceToHost));
+      AIMX_CUDA(cudaMemcpy(tmp.data(), c->Hoct, n * sizeof(float2), cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < n; ++i) { out[2 * i] = tmp[i].x * M; out[2 * i + 1] = tmp[i].y * M; }
     } else {
-      AIMX_CUDA(cudaMemcpy(out, c->hot.Hoct, n * sizeof(double2), cudaMemcpyDeviceToHost));
+      AIMX_CUDA(cudaMemcpy(out, c->Hoct, n * sizeof(double2), cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < 2 * n; ++i) out[i] *= M;
     }
   }

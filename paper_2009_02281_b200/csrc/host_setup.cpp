@@ -296,27 +296,31 @@ static uint32_t spread3(uint32_t v) {   // 10 bits -> every third bit
   return v;
 }
 
-static std::vector<int32_t> row_order(const Topology& t, int kind) {
-  const int64_t nb = t.nb;
-  std::vector<int64_t> key(nb);
-  for (int64_t e = 0; e < nb; ++e) {
-    const int32_t* A = &t.anchor[3 * e];
-    key[e] = kind == 0 ? (int64_t)A[0] + (int64_t)t.n[0] * ((int64_t)A[1] + (int64_t)t.n[1] * A[2])
-                       : (int64_t)(spread3(A[0]) | (spread3(A[1]) << 1) | (spread3(A[2]) << 2));
+// rows (a subset of the RWGs, all if `sub` is empty) ordered by anchor key
+static std::vector<int32_t> row_order(const Topology& t, int kind, const std::vector<int32_t>& sub) {
+  std::vector<int32_t> p;
+  if (sub.empty()) {
+    p.resize(t.nb);
+    std::iota(p.begin(), p.end(), 0);
+  } else {
+    p = sub;
   }
-  std::vector<int32_t> p(nb);
-  std::iota(p.begin(), p.end(), 0);
-  std::stable_sort(p.begin(), p.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+  auto key = [&](int32_t e) -> int64_t {
+    const int32_t* A = &t.anchor[3 * (int64_t)e];
+    return kind == 0 ? (int64_t)A[0] + (int64_t)t.n[0] * ((int64_t)A[1] + (int64_t)t.n[1] * A[2])
+                     : (int64_t)(spread3(A[0]) | (spread3(A[1]) << 1) | (spread3(A[2]) << 2));
+  };
+  std::stable_sort(p.begin(), p.end(), [&](int32_t a, int32_t b) { return key(a) < key(b); });
   return p;
 }
 
 static void group_union(const Topology& t, const std::vector<int32_t>& p, int64_t g, int R,
                         std::vector<int32_t>& u) {
   u.clear();
-  const int64_t nb = t.nb;
+  const int64_t nr = (int64_t)p.size();
   for (int r = 0; r < R; ++r) {
     const int64_t i = g * R + r;
-    if (i >= nb) break;
+    if (i >= nr) break;
     const int32_t m = p[i];
     u.insert(u.end(), t.col.begin() + t.rowptr[m], t.col.begin() + t.rowptr[m + 1]);
   }
@@ -324,15 +328,16 @@ static void group_union(const Topology& t, const std::vector<int32_t>& p, int64_
   u.erase(std::unique(u.begin(), u.end()), u.end());
 }
 
-void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, NearGroups& ng) {
-  const int64_t nb = t.nb;
+void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, NearGroups& ng,
+                       const std::vector<int32_t>& rows) {
+  const int64_t nb = rows.empty() ? t.nb : (int64_t)rows.size();   // rows in the groups
   // candidate (ordering, R): union sizes estimated on a sample of groups, cost
   // model = HBM bytes + FMA issue + x-row loads of a 16-column c64 SpMM
   int best_kind = 0, best_R = 8;
   double best = 1e300;
   const char* eR = std::getenv("AIMX_NEAR_R");
   const char* eK = std::getenv("AIMX_NEAR_ORDER");
-  std::vector<int32_t> perm[2] = {row_order(t, 0), row_order(t, 1)};
+  std::vector<int32_t> perm[2] = {row_order(t, 0, rows), row_order(t, 1, rows)};
   for (int kind = 0; kind < 2; ++kind) {
     if (eK && std::atoi(eK) != kind) continue;
     for (int R : {4, 8}) {
@@ -403,9 +408,9 @@ void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, N
   const int64_t U = ng.ptr[ngrp], Uw = ng.wptr[ngrp];
   if (U * R > (int64_t)INT32_MAX * 4) throw Error(AIMX_E_GRID, "near matrix too large for the row-group layout");
   ng.ucol.resize(U);
-  ng.slot.resize(t.rowptr[nb]);
+  ng.slot.assign(t.rowptr[t.nb], -1);
   ng.wnode.resize(Uw);
-  ng.wslot.assign(nb * p3, -1);
+  ng.wslot.assign(t.nb * p3, -1);
 #pragma omp parallel
   {
     std::vector<int32_t> u;
@@ -518,4 +523,53 @@ std::vector<int32_t> near_partition(const NearChunks& ck, int64_t ngrp, int ncta
   return cta_ptr;
 }
 
+
+// Nodes of rows [y0, y1) only, lines renumbered locally: (y - y0) + (y1 - y0) z.
+void nodemap_rows(const Topology& t, const NodeMap& full, int y0, int y1, NodeMap& m) {
+  const int Nx = t.n[0], Ny = t.n[1], Nz = t.n[2], ny = y1 - y0;
+  m = NodeMap{};
+  m.line_occ.assign((size_t)ny * Nz, 0);
+  m.node_ptr.push_back(0);
+  for (size_t q = 0; q < full.node_lin.size(); ++q) {
+    const int32_t lin = full.node_lin[q];
+    const int y = (lin / Nx) % Ny, z = lin / (Nx * Ny);
+    if (y < y0 || y >= y1) continue;
+    const int32_t line = (y - y0) + ny * z;
+    if (m.line_id.empty() || m.line_id.back() != line) {
+      m.line_id.push_back(line);
+      m.line_ptr.push_back((int32_t)m.node_lin.size());
+      m.line_occ[line] = 1;
+      if (m.zplanes.empty() || m.zplanes.back() != z) m.zplanes.push_back(z);
+    }
+    m.node_lin.push_back(lin);
+    m.node_line.push_back((int32_t)m.line_id.size() - 1);
+    for (int32_t e = full.node_ptr[q]; e < full.node_ptr[q + 1]; ++e) {
+      m.ent_rwg.push_back(full.ent_rwg[e]);
+      m.ent_slot.push_back(full.ent_slot[e]);
+    }
+    m.node_ptr.push_back((int32_t)m.ent_rwg.size());
+  }
+  m.line_ptr.push_back((int32_t)m.node_lin.size());
+}
+
 }  // namespace aimx
+
+extern "C" aimx_status aimx_slab_plan(const int32_t n[3], int32_t order, int32_t world, int32_t rank,
+                                      int32_t out[6]) {
+  if (!n || !out || world < 1 || rank < 0 || rank >= world || order < 1) return AIMX_E_INVALID_ARG;
+  const int Lx = 2 * n[0];
+  if (Lx % world != 0 || ((Lx / world) & (Lx / world - 1)) != 0) return AIMX_E_UNSUPPORTED;
+  if (n[1] < world) return AIMX_E_UNSUPPORTED;
+  // rows: contiguous near-equal blocks of the unpadded y axis; phi rows extend
+  // `order` rows past the block (stencils of RWGs anchored in it); kx: equal slabs
+  const int base = n[1] / world, rem = n[1] % world;
+  const int y0 = rank * base + (rank < rem ? rank : rem);
+  const int y1 = y0 + base + (rank < rem ? 1 : 0);
+  out[0] = y0;
+  out[1] = y1;
+  out[2] = y1 + order < n[1] ? y1 + order : n[1];
+  out[3] = rank * (Lx / world);
+  out[4] = (rank + 1) * (Lx / world);
+  out[5] = 0;
+  return AIMX_OK;
+}

@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   const int Nx = h.Nx;
   // phi layout [node][channel][slot] (slots = batch, complex)
   const int64_t ns = (int64_t)h.batch * 4;   // node stride
-  T2* __restrict__ out = (T2*)h.phi + (int64_t)c * h.batch + b + (int64_t)lid * Nx * ns;
+  const int plid = h.phi_line ? (act ? h.phi_line[r] : 0) : lid;   // line of phi (global grid)
+  T2* __restrict__ out = (T2*)h.phi + (int64_t)c * h.batch + b + (int64_t)plid * Nx * ns;
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {   // x < Nx  <=>  k1 < R1/2 in D(R2,R1)
     const int x = TwoLevel<G::R2, G::R1>::in_index(t, i);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
   pass_prologue<T, L>(tw, xb, (const T2*)h.twy_tab, line);
-  const int W = 8 * h.Nx, Ny = h.Ny;
+  const int W = h.W, Ny = h.Ny;
   const ColTile ct = col_tile<T, L>(line, W);
   const int zi = blockIdx.y * ct.RPC + ct.rsub;
   const bool act = zi < h.nzocc;
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
   pass_prologue<T, L>(tw, xb, (const T2*)h.twy_tab, line);
-  const int W = 8 * h.Nx, Ny = h.Ny;
+  const int W = h.W, Ny = h.Ny;
   const ColTile ct = col_tile<T, L>(line, W);
   const int zi = blockIdx.y * ct.RPC + ct.rsub;
   const bool act = zi < h.nzocc;
@@ -332,14 +333,14 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   __builtin_assume(t < G::T);
-  const int W = 8 * h.Nx, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
+  const int W = h.W, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
   const ColTile ct = col_tile<T, L>(line, W);
   const int b = blockIdx.z;
   // prefetch this CTA's spectrum slab [rsub][kz][kx - kx0] into shared memory
   // (cp.async, overlaps the column loads and the forward transform)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* hs = reinterpret_cast<T2*>(smem_raw) + L + (size_t)G::NL * G::XB;
-  const int nkx = ct.CW / 4, kx0 = (blockIdx.x * ct.CW) / 4;
+  const int nkx = ct.CW / 4, kx0 = h.kx0 + (blockIdx.x * ct.CW) / 4;   // kx0: column slab offset
   {
     const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
     const int n = ct.RPC * L * nkx;
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 4 : 2) k_yzconv(HotDev h
   constexpr int TW = G::TW, NT = G::NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* S = reinterpret_cast<T2*>(smem_raw);   // [z < LZ][ky < LY][TW]
-  const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, W = 8 * Nx;
+  const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, W = h.W;
   const int b = blockIdx.y;
   const int col0 = blockIdx.x * TW;
   const T2* __restrict__ A = (const T2*)h.bufA + b * h.sA;
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 4 : 2) k_yzconv(HotDev h
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
   for (int it = threadIdx.x; it < LY * TW; it += NT) {
     const int ky = it / TW, w = it % TW;
-    const int kx = (col0 + w) >> 2;
+    const int kx = h.kx0 + ((col0 + w) >> 2);
     const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
     const int kyf = ky <= Ny ? ky : 2 * Ny - ky;
     T2 v[LZ];
@@ -823,7 +824,7 @@ template <typename T, int L> dim3 col_grid(int W, int rows, int B) {
 template <typename T, int L>
 void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>();
-  dim3 g = col_grid<T, L>(8 * h.Nx, h.nzocc, B);
+  dim3 g = col_grid<T, L>(h.W, h.nzocc, B);
   if (!inv) {
     set_smem(k_yfwd<T, L>, sm);
     k_yfwd<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
@@ -838,7 +839,7 @@ template <typename T, int L>
 void run_z(const HotDev& h, int B, cudaStream_t s) {
   // + spectrum slab: NL lines x L / 4 complex (RPC * L * CW / 4)
   constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
-  dim3 g = col_grid<T, L>(8 * h.Nx, 2 * h.Ny, B);
+  dim3 g = col_grid<T, L>(h.W, 2 * h.Ny, B);
   if (h.nzocc == h.Nz) {
     set_smem(k_zconv<T, L, true>, sm);
     k_zconv<T, L, true><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
@@ -925,13 +926,13 @@ void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combin
 template <typename T, int LY, int LZ> void launch_yz(const HotDev& h, int B, cudaStream_t s) {
   using G = YZGeom<T, LY, LZ>;
   set_smem(k_yzconv<T, LY, LZ>, G::SMEM);
-  dim3 g((unsigned)(8 * h.Nx / G::TW), (unsigned)B);
+  dim3 g((unsigned)(h.W / G::TW), (unsigned)B);
   k_yzconv<T, LY, LZ><<<g, G::NT, G::SMEM, s>>>(h);
   AIMX_CHECK_LAUNCH();
 }
 template <typename T> bool run_yz_fused(const HotDev& h, int B, cudaStream_t s, Profiler* prof) {
   const int Ly = 2 * h.Ny, Lz = 2 * h.Nz;
-  if (Ly > 32 || Lz > 32 || (8 * h.Nx) % YZGeom<T, 8, 8>::TW != 0 || Ly * Lz > 512) return false;
+  if (Ly > 32 || Lz > 32 || h.W % YZGeom<T, 8, 8>::TW != 0 || Ly * Lz > 512) return false;
   StageScope sc(prof, 3, s);
   switch (Ly * 64 + Lz) {
     case 8 * 64 + 8: launch_yz<T, 8, 8>(h, B, s); break;
@@ -968,7 +969,84 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
   { StageScope sc(prof, 6, s); run_interp<T>(h, x, y0, y1, c, s); }
 }
 
+// ---- slab-decomposed hot path (SlabRank): per rank S2 + x fwd on its rows,
+// exchange 0 (rows -> kx slabs), y fwd / z conv / y inv on its kx slab,
+// exchange 1 (kx slabs -> rows incl. the `order`-row halo), x inv of its
+// rows, S4 + S5 for its testing functions.
+template <typename T>
+void slab_matvec_t(std::vector<SlabRank*>& ranks, int Nx, int Ny, int Nz, SlabExchange& xchg, const void* x,
+                   void* y0, void* y1, const Combine& c, cudaStream_t s, Profiler* prof) {
+  if (c.B < 1 || c.B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "bad batch");
+  const int Lx = 2 * Nx, Ly = 2 * Ny, Lz = 2 * Nz, B = c.B;
+  using T2 = typename CT<T>::T2;
+  {
+    StageScope sc(prof, 1, s);
+    for (SlabRank* r : ranks) {
+      run_interleave<T>(r->hr, x, c, s);
+      if (r->hr.nocc > 0) {   // a rank's rows may hold no occupied node
+        if (B == 1) run_gather<T>(r->hr, x, c.xstride, B, s);
+        else run_gather_b<T>(r->hr, B, s);
+      }
+      if (r->hr.nlines > 0) AIMX_SWITCH_L(Lx, (run_x<T, L>(r->hr, false, B, s)));
+    }
+    xchg.run(ranks, 0, B, sizeof(T2), s);
+  }
+  for (SlabRank* r : ranks) {
+    const HotDev& h = r->hc;
+    if (!run_yz_fused<T>(h, B, s, prof)) {
+      { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, B, s))); }
+      { StageScope sc(prof, 3, s); AIMX_SWITCH_L(Lz, (run_z<T, L>(h, B, s))); }
+      { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, B, s))); }
+    }
+  }
+  {
+    StageScope sc(prof, 5, s);
+    xchg.run(ranks, 1, B, sizeof(T2), s);
+    for (SlabRank* r : ranks)
+      if (r->hx.nlines > 0) AIMX_SWITCH_L(Lx, (run_x<T, L>(r->hx, true, B, s)));
+  }
+  {
+    StageScope sc(prof, 6, s);
+    for (SlabRank* r : ranks)
+      if (r->hr.ngrp > 0) run_interp<T>(r->hr, x, y0, y1, c, s);
+  }
+}
+
+// dst[i0][i1][i2][i3] = src[i0][i1][i2][i3] with per-axis strides (complex units)
+template <typename T2>
+__global__ void k_copy4(T2* __restrict__ dst, int64_t t0, int64_t t1, int64_t t2, const T2* __restrict__ src,
+                        int64_t s0, int64_t s1, int64_t s2, int64_t d1, int64_t d2, int64_t d3, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t i3 = i % d3;
+  int64_t r = i / d3;
+  const int64_t i2 = r % d2;
+  r /= d2;
+  const int64_t i1 = r % d1, i0 = r / d1;
+  dst[i0 * t0 + i1 * t1 + i2 * t2 + i3] = src[i0 * s0 + i1 * s1 + i2 * s2 + i3];
+}
+
 }  // namespace
+
+void slab_matvec(std::vector<SlabRank*>& ranks, int Ny, int Nz, int Nx, bool f32, SlabExchange& xchg,
+                 const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s, Profiler* prof) {
+  if (f32) slab_matvec_t<float>(ranks, Nx, Ny, Nz, xchg, x, y0, y1, c, s, prof);
+  else slab_matvec_t<double>(ranks, Nx, Ny, Nz, xchg, x, y0, y1, c, s, prof);
+}
+
+void copy4(void* dst, const int64_t t[3], const void* src, const int64_t st[3], const int64_t d[4], size_t csize,
+           cudaStream_t s) {
+  const int64_t n = d[0] * d[1] * d[2] * d[3];
+  if (n <= 0) return;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (csize == 8)
+    k_copy4<float2><<<g, 256, 0, s>>>((float2*)dst, t[0], t[1], t[2], (const float2*)src, st[0], st[1], st[2], d[1],
+                                     d[2], d[3], n);
+  else
+    k_copy4<double2><<<g, 256, 0, s>>>((double2*)dst, t[0], t[1], t[2], (const double2*)src, st[0], st[1], st[2],
+                                      d[1], d[2], d[3], n);
+  AIMX_CHECK_LAUNCH();
+}
 
 bool fft_length_supported(int L) { return L >= 8 && L <= 1024 && (L & (L - 1)) == 0; }
 

@@ -61,11 +61,11 @@ __global__ void k_sample(int Nx, int Ny, int Nz, int64_t noct, double h, K0s k0s
       res = mk<T2>((T)(-2.0 * s * s * inv4pi / r), (T)(-2.0 * s * c * inv4pi / r));   // sin x = 2 sin(x/2) cos(x/2)
     } else {
       const double r = h * sqrt((double)q);
-      const double u = 0.25 * k0 * r / kPi;             // (k0 r / 2) / (2 pi)
+      const double u = (0.25 / kPi) * (k0 * r);         // (k0 r / 2) / (2 pi)
       const float red = (float)(u - rint(u));           // in [-1/2, 1/2] turns
       float s, c;
       sincospif(2.0f * red, &s, &c);
-      const float a = (float)(inv4pi / r);
+      const float a = (float)inv4pi / (float)r;
       res = mk<T2>((T)(-2.0f * s * s * a), (T)(-2.0f * s * c * a));
     }
   }

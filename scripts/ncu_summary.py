@@ -93,8 +93,8 @@ def full(path, out, jpath=None, key=None):
 
 
 def stage_of(k):
-    for pat, st in (("k_interp_near", "interp_near"), ("k_zconv", "zconv"), ("k_yfwd", "yfwd"),
-                    ("k_yinv", "yinv"), ("k_xinv", "xinv")):
+    for pat, st in (("k_interp_near", "interp_near"), ("k_zconv", "zconv"), ("k_yzconv", "zconv"),
+                    ("k_yfwd", "yfwd"), ("k_yinv", "yinv"), ("k_xinv", "xinv")):
         if pat in k:
             return st
     return None
