@@ -145,9 +145,11 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def stage_bytes(st: dict, prec: str) -> dict:
+def stage_bytes(st: dict, prec: str, fused_yz: bool = False) -> dict:
     """Algorithmic (compulsory) bytes per launch of each stage, given this
-    implementation's pass structure (DESIGN.md "Roofline")."""
+    implementation's pass structure.  fused_yz: y fwd,
+    z conv and y inv run as one kernel (short y / z transforms), reported as
+    zconv: x-transformed rows in, y-inverse rows out, the spectrum."""
     s = 8 if prec == "c64" else 16          # complex
     r = s // 2                              # real
     Nx, Ny, Nz = st["n"]
@@ -161,7 +163,7 @@ def stage_bytes(st: dict, prec: str) -> dict:
         "spectrum": 2 * noct * s,                                   # read H_hat_s, write H_hat
         "proj_xfft": nent * (4 + 4 * r) + 8 * nocc + s * nb + nl * row,
         "yfwd": nz_ * Ny * row + nz_ * 2 * Ny * row,
-        "zconv": 2 * nz_ * 2 * Ny * row + noct * s,
+        "zconv": (nz_ * Ny * row + nl * row + noct * s) if fused_yz else (2 * nz_ * 2 * Ny * row + noct * s),
         "yinv": nz_ * 2 * Ny * row + nl * row,
         "xinv": nl * row + nl * Nx * 4 * s,
         "interp_near": nb * p3 * 4 * r + 4 * nb + nocc * 4 * s + 4 * (nb + 1)
@@ -330,7 +332,7 @@ def run_aimx(a):
 
     # roofline of the dominant stage
     peak, peak_src = measured_peaks()
-    sb = stage_bytes(st, prec)
+    sb = stage_bytes(st, prec, fused_yz=prof["yfwd"][1] == 0)
     traffic = ncu_traffic(a.config, prec)
     step_stage_ms = sum(ms for ms, n in prof.values())
     stages = {}

@@ -21,14 +21,62 @@ template <typename T2> __device__ __forceinline__ T2 mk(decltype(T2::x) a, declt
   r.y = b;
   return r;
 }
+// ---- packed fp32 pair arithmetic (sm_100: add/sub/mul/fma .f32x2 -> FADD2 /
+// FMUL2 / FFMA2; ptxas folds pair swaps, broadcasts and half negations into
+// the operand swizzles), used for every complex operation in fp32.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+  return up2(r);
+}
+
 template <typename T2> __device__ __forceinline__ T2 cadd(T2 a, T2 b) { return mk<T2>(a.x + b.x, a.y + b.y); }
 template <typename T2> __device__ __forceinline__ T2 csub(T2 a, T2 b) { return mk<T2>(a.x - b.x, a.y - b.y); }
 template <typename T2> __device__ __forceinline__ T2 cmul(T2 a, T2 b) {
   return mk<T2>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return sub2(a, b); }
+// a b = (a.x b.x - a.y b.y, a.y b.x + a.x b.y): FMUL2 + FFMA2
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return ffma2(make_float2(-a.y, a.x), make_float2(b.y, b.y), mul2(a, make_float2(b.x, b.x)));
+}
 // multiply by -j (forward) or +j (inverse)
 template <typename T2, bool INV> __device__ __forceinline__ T2 mulj(T2 a) {
   return INV ? mk<T2>(-a.y, a.x) : mk<T2>(a.y, -a.x);
+}
+// t +- (-+j) d (forward), t +- (+-j) d (inverse), one FFMA2 each (fp32)
+template <bool INV> __device__ __forceinline__ float2 add_mulj(float2 t, float2 d) {
+  return INV ? ffma2(make_float2(d.y, d.x), make_float2(-1.f, 1.f), t)
+             : ffma2(make_float2(d.y, d.x), make_float2(1.f, -1.f), t);
+}
+template <bool INV> __device__ __forceinline__ float2 sub_mulj(float2 t, float2 d) {
+  return add_mulj<!INV>(t, d);
 }
 
 template <typename T2, bool INV> __device__ __forceinline__ void dft2(T2* v) {
@@ -38,6 +86,14 @@ template <typename T2, bool INV> __device__ __forceinline__ void dft2(T2* v) {
 }
 template <typename T2, bool INV>
 __device__ __forceinline__ void dft4(T2& v0, T2& v1, T2& v2, T2& v3) {
+  if constexpr (sizeof(T2) == 8) {
+    const float2 t0 = add2(v0, v2), t1 = sub2(v0, v2), t2 = add2(v1, v3), d = sub2(v1, v3);
+    v0 = add2(t0, t2);
+    v2 = sub2(t0, t2);
+    v1 = add_mulj<INV>(t1, d);
+    v3 = sub_mulj<INV>(t1, d);
+    return;
+  }
   T2 t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = mulj<T2, INV>(csub(v1, v3));
   v0 = cadd(t0, t2);
   v2 = csub(t0, t2);
@@ -50,6 +106,25 @@ template <typename T2, bool INV> __device__ __forceinline__ void dft8(T2* v) {
   T2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
   dft4<T2, INV>(e0, e1, e2, e3);
   dft4<T2, INV>(o0, o1, o2, o3);
+  if constexpr (sizeof(T2) == 8) {
+    const float s = 0.70710678118654752440f;
+    // W8^1 o1 = s (o1.x + o1.y, o1.y - o1.x) (fwd), s (o1.x - o1.y, o1.x + o1.y) (inv)
+    const float2 u1 = INV ? ffma2(make_float2(o1.y, o1.x), make_float2(-1.f, 1.f), o1)
+                          : ffma2(make_float2(o1.y, o1.x), make_float2(1.f, -1.f), o1);
+    // W8^3 o3 = s (o3.y - o3.x, -o3.x - o3.y) (fwd), s (-o3.x - o3.y, o3.x - o3.y) (inv)
+    const float2 n3 = make_float2(-o3.x, -o3.y);
+    const float2 u3 = INV ? ffma2(make_float2(o3.y, o3.x), make_float2(-1.f, 1.f), n3)
+                          : ffma2(make_float2(o3.y, o3.x), make_float2(1.f, -1.f), n3);
+    v[0] = add2(e0, o0);
+    v[4] = sub2(e0, o0);
+    v[1] = ffma2(u1, make_float2(s, s), e1);
+    v[5] = ffma2(u1, make_float2(-s, -s), e1);
+    v[2] = add_mulj<INV>(e2, o2);
+    v[6] = sub_mulj<INV>(e2, o2);
+    v[3] = ffma2(u3, make_float2(s, s), e3);
+    v[7] = ffma2(u3, make_float2(-s, -s), e3);
+    return;
+  }
   const R s = (R)0.70710678118654752440;
   // W8^1 = (1 -+ j)/sqrt2, W8^2 = -+j, W8^3 = (-1 -+ j)/sqrt2
   T2 w1 = INV ? mk<T2>(s * (o1.x - o1.y), s * (o1.x + o1.y)) : mk<T2>(s * (o1.x + o1.y), s * (o1.y - o1.x));

@@ -344,8 +344,10 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
   {
     const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
     const int n = ct.RPC * L * nkx;
+    const int lgk = __ffs(nkx) - 1;   // nkx: power of two
     for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
-      const int r = idx / (L * nkx), kz = (idx / nkx) % L, kxl = idx % nkx;
+      const int kxl = idx & (nkx - 1), rest = idx >> lgk;
+      const int kz = rest % L, r = rest / L;   // L: compile-time power of two
       const int kyy = blockIdx.y * ct.RPC + r;
       const int kyf = kyy <= Ny ? kyy : Ny2 - kyy;
       const int kx = kx0 + kxl;

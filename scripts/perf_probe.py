@@ -66,8 +66,11 @@ for cfg in [int(x) for x in a.configs.split(",")]:
         e3.record()
         torch.cuda.synchronize()
         sb = stage_bytes(st, prec)
-        stages = {k: {"ms": ms / max(n, 1), "GBps": sb[k] / (ms / max(n, 1) * 1e-3) / 1e9,
-                      "MB": sb[k] / 1e6} for k, (ms, n) in prof.items()}
+        fused = prof["yfwd"][1] == 0
+        if fused:
+            sb["zconv"] = stage_bytes(st, prec, fused_yz=True)["zconv"]
+        stages = {k: {"ms": ms / n, "GBps": sb[k] / (ms / n * 1e-3) / 1e9,
+                      "MB": sb[k] / 1e6} for k, (ms, n) in prof.items() if n > 0}
         print(json.dumps({"cfg": cfg, "prec": prec, "setup_s": tset, "stats": st,
                           "ms_per_freq_pt_profiled": e0.elapsed_time(e1) / a.iters,
                           "ms_per_matvec": e2.elapsed_time(e3) / a.iters, "kernels_per_freq_pt": kern / a.iters,
