@@ -195,6 +195,11 @@ aimx_status aimx_get_spectrum(const aimx_ctx* ctx, int which, double* out);
 #define AIMX_NUM_STAGES 7
 aimx_status aimx_profile_enable(aimx_ctx* ctx, int on);
 aimx_status aimx_profile_read(aimx_ctx* ctx, double* ms, int64_t* launches, int64_t* kernels);
+/* Which stages are bracketed while profiling is on (bit i = stage i; default
+ * all).  Each bracket is a pair of events on the stream, which also ends the
+ * overlap of consecutive kernels' launches (programmatic dependent launch)
+ * at that point, so a timed run brackets only the stage it reports. */
+aimx_status aimx_profile_stages(aimx_ctx* ctx, int32_t mask);
 
 /* ---- slab-decomposed FFT (multi-GPU for the largest grid) ----
  * Host-only plan (no GPU needed): for `world` ranks, rank `rank` owns the

@@ -71,6 +71,7 @@ ABI_FUNCTIONS = {
     "aimx_get_spectrum": (C.c_int, [_P, C.c_int, _P]),
     "aimx_profile_enable": (C.c_int, [_P, C.c_int]),
     "aimx_profile_read": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int64)]),
+    "aimx_profile_stages": (C.c_int, [_P, C.c_int32]),
     "aimx_destroy": (None, [_P]),
     "aimx_status_string": (C.c_char_p, [C.c_int]),
     "aimx_last_error": (C.c_char_p, [_P]),
@@ -267,7 +268,10 @@ class AIMx:
 
     STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
 
-    def profile_enable(self, on: bool = True):
+    def profile_enable(self, on: bool = True, stages=None):
+        """stages: names (AIMx.STAGES) to bracket with events; None = all."""
+        mask = 0x7F if stages is None else sum(1 << self.STAGES.index(k) for k in stages)
+        _check(self.lib, self.lib.aimx_profile_stages(self.ctx, int(mask)), self.ctx)
         _check(self.lib, self.lib.aimx_profile_enable(self.ctx, int(bool(on))), self.ctx)
 
     def profile_read(self) -> dict:

@@ -40,6 +40,23 @@ int64_t& launch_counter();
                                            cudaGetErrorString(e_));                              \
   } while (0)
 
+// Launch with programmatic stream serialization (PDL, see fft.cuh pdl_wait).
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AIMX_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kC0 = 299792458.0;          // m/s (exact)
 constexpr double kMu0 = 1.25663706212e-6;    // H/m (CODATA 2018), reading R1
@@ -180,6 +197,7 @@ void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const doubl
 // Per-stage CUDA-event timer (aimx_profile_*).
 struct Profiler {
   bool on = false;
+  int mask = 0x7f;             // stages bracketed while on (bit i = stage i)
   std::vector<cudaEvent_t> pool;
   struct Rec { int stage; cudaEvent_t a, b; };
   std::vector<Rec> pending;
@@ -198,10 +216,10 @@ struct StageScope {
   cudaStream_t s;
   cudaEvent_t a = nullptr;
   StageScope(Profiler* p_, int st, cudaStream_t s_) : p(p_), stage(st), s(s_) {
-    if (p && p->on) p->begin(stage, s, a);
+    if (p && p->on && ((p->mask >> stage) & 1)) p->begin(stage, s, a);
   }
   ~StageScope() {
-    if (p && p->on) p->end(stage, s, a);
+    if (a) p->end(stage, s, a);
   }
 };
 

@@ -1077,6 +1077,12 @@ aimx_status aimx_profile_enable(aimx_ctx* c, int on) {
   AIMX_API_END(c)
 }
 
+aimx_status aimx_profile_stages(aimx_ctx* c, int32_t mask) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  c->prof.mask = mask & 0x7f;
+  return AIMX_OK;
+}
+
 aimx_status aimx_profile_read(aimx_ctx* c, double* ms, int64_t* launches, int64_t* kernels) {
   if (!c) return AIMX_E_INVALID_ARG;
   AIMX_API_BEGIN

@@ -11,6 +11,15 @@
 
 namespace aimx {
 
+// Programmatic dependent launch (PDL): hot-path kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization so that a kernel's launch
+// and prologue overlap the previous kernel's tail.  Every such kernel calls
+// pdl_wait() before its first access to data produced by earlier work (which
+// also keeps the ordering transitive), and pdl_trigger() to let the next
+// kernel launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 template <typename T> struct CT;
 template <> struct CT<float> { using T2 = float2; using T4 = float4; };
 template <> struct CT<double> { using T2 = double2; using T4 = double4; };

@@ -36,6 +36,8 @@ namespace {
 template <typename T, int G>
 __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::T2* __restrict__ x,
                                                 int64_t xstride) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
   const int b = blockIdx.y;
@@ -76,6 +78,8 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
 template <typename T, int BB>
 __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                   int B) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
   constexpr int V = sizeof(T2) == 8 ? 2 : 1;
@@ -200,6 +204,8 @@ template <typename T, int L> constexpr size_t pass_smem() {
 // ---- x forward: occupied lines of S (x < Nx, zero padded) -> bufA[line_id][kx][c]
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
@@ -226,6 +232,8 @@ __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
 // ---- x inverse: bufC[line_id][kx][c] -> phi[line][x < Nx][c]
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
@@ -270,6 +278,8 @@ template <typename T, int L> __device__ __forceinline__ ColTile col_tile(int lin
 // ---- y forward: bufA[z][y < Ny][.] -> bufB[z][ky][.]
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
@@ -299,6 +309,8 @@ __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
 // ---- y inverse: bufB[z][ky][.] -> bufC[z][y < Ny, occupied][.]
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
@@ -329,6 +341,8 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
 // ---- z forward * H_hat * z inverse, in place on bufB (occupied planes only)
 template <typename T, int L, bool FULLZ>
 __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_zconv(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
@@ -405,6 +419,8 @@ template <typename T, int LY, int LZ> struct YZGeom {
 
 template <typename T, int LY, int LZ>
 __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 4 : 2) k_yzconv(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = YZGeom<T, LY, LZ>;
   constexpr int TW = G::TW, NT = G::NT;
@@ -583,6 +599,8 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
     k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      typename CT<T>::T2* __restrict__ y0,
                                                      typename CT<T>::T2* __restrict__ y1, Combine cb) {
+  pdl_wait();
+  pdl_trigger();
   using K = NearCfg<T, R, BB, PARTS>;
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
@@ -793,10 +811,10 @@ void run_gather(const HotDev& h, const void* x, int64_t xstride, int B, cudaStre
   const int per = 256 / h.G;
   dim3 g((unsigned)((h.nocc + per - 1) / per), (unsigned)B);
   switch (h.G) {
-    case 4: k_gather<T, 4><<<g, 256, 0, s>>>(h, (const T2*)x, xstride); break;
-    case 8: k_gather<T, 8><<<g, 256, 0, s>>>(h, (const T2*)x, xstride); break;
-    case 16: k_gather<T, 16><<<g, 256, 0, s>>>(h, (const T2*)x, xstride); break;
-    default: k_gather<T, 32><<<g, 256, 0, s>>>(h, (const T2*)x, xstride); break;
+    case 4: launch_pdl(k_gather<T, 4>, dim3(g), dim3(256), 0, s, h, (const T2*)x, xstride); break;
+    case 8: launch_pdl(k_gather<T, 8>, dim3(g), dim3(256), 0, s, h, (const T2*)x, xstride); break;
+    case 16: launch_pdl(k_gather<T, 16>, dim3(g), dim3(256), 0, s, h, (const T2*)x, xstride); break;
+    default: launch_pdl(k_gather<T, 32>, dim3(g), dim3(256), 0, s, h, (const T2*)x, xstride); break;
   }
   AIMX_CHECK_LAUNCH();
 }
@@ -808,10 +826,10 @@ void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   dim3 g((unsigned)((h.nlines + RPC - 1) / RPC), (unsigned)B);
   if (!inv) {
     set_smem(k_xfwd<T, L>, sm);
-    k_xfwd<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+    launch_pdl(k_xfwd<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
   } else {
     set_smem(k_xinv<T, L>, sm);
-    k_xinv<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+    launch_pdl(k_xinv<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
   }
   AIMX_CHECK_LAUNCH();
 }
@@ -829,10 +847,10 @@ void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
   dim3 g = col_grid<T, L>(h.W, h.nzocc, B);
   if (!inv) {
     set_smem(k_yfwd<T, L>, sm);
-    k_yfwd<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+    launch_pdl(k_yfwd<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
   } else {
     set_smem(k_yinv<T, L>, sm);
-    k_yinv<T, L><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+    launch_pdl(k_yinv<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
   }
   AIMX_CHECK_LAUNCH();
 }
@@ -844,10 +862,10 @@ void run_z(const HotDev& h, int B, cudaStream_t s) {
   dim3 g = col_grid<T, L>(h.W, 2 * h.Ny, B);
   if (h.nzocc == h.Nz) {
     set_smem(k_zconv<T, L, true>, sm);
-    k_zconv<T, L, true><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+    launch_pdl(k_zconv<T, L, true>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
   } else {
     set_smem(k_zconv<T, L, false>, sm);
-    k_zconv<T, L, false><<<g, PassGeom<T, L>::NT, sm, s>>>(h);
+    launch_pdl(k_zconv<T, L, false>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
   }
   AIMX_CHECK_LAUNCH();
 }
@@ -856,6 +874,8 @@ void run_z(const HotDev& h, int B, cudaStream_t s) {
 template <typename T>
 __global__ void k_interleave(int nb, int B, int BB, const typename CT<T>::T2* __restrict__ x,
                              int64_t xstride, typename CT<T>::T2* __restrict__ xt) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)nb * BB) return;
@@ -871,7 +891,7 @@ void run_interleave(const HotDev& h, const void* x, const Combine& c, cudaStream
   using T2 = typename CT<T>::T2;
   const int BB = batch_bucket(c.B);
   const int64_t n = (int64_t)h.nb * BB;
-  k_interleave<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.nb, c.B, BB, (const T2*)x, c.xstride,
+  launch_pdl(k_interleave<T>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, h.nb, c.B, BB, (const T2*)x, c.xstride,
                                                               (T2*)h.xt);
   AIMX_CHECK_LAUNCH();
 }
@@ -882,10 +902,10 @@ void run_gather_b(const HotDev& h, int B, cudaStream_t s) {
   const unsigned g = (unsigned)(((int64_t)h.nocc * 32 + 255) / 256);
   const T2* xt = (const T2*)h.xt;
   switch (batch_bucket(B)) {
-    case 2: k_gather_b<T, 2><<<g, 256, 0, s>>>(h, xt, B); break;
-    case 4: k_gather_b<T, 4><<<g, 256, 0, s>>>(h, xt, B); break;
-    case 8: k_gather_b<T, 8><<<g, 256, 0, s>>>(h, xt, B); break;
-    default: k_gather_b<T, 16><<<g, 256, 0, s>>>(h, xt, B); break;
+    case 2: launch_pdl(k_gather_b<T, 2>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    case 4: launch_pdl(k_gather_b<T, 4>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    case 8: launch_pdl(k_gather_b<T, 8>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    default: launch_pdl(k_gather_b<T, 16>, dim3(g), dim3(256), 0, s, h, xt, B); break;
   }
   AIMX_CHECK_LAUNCH();
 }
@@ -895,7 +915,7 @@ void launch_interp(const HotDev& h, const void* xt, void* y0, void* y1, const Co
   using T2 = typename CT<T>::T2;
   using K = NearCfg<T, R, BB, PARTS>;
   set_smem(k_interp_near<T, R, BB, PARTS>, K::SMEM);
-  k_interp_near<T, R, BB, PARTS><<<(unsigned)(BB == 1 ? h.near_ctas1 : h.near_ctas), K::NT, K::SMEM, s>>>(h, (const T2*)xt, (T2*)y0,
+  launch_pdl(k_interp_near<T, R, BB, PARTS>, dim3((unsigned)(BB == 1 ? h.near_ctas1 : h.near_ctas)), dim3(K::NT), K::SMEM, s, h, (const T2*)xt, (T2*)y0,
                                                                                  (T2*)y1, c);
   AIMX_CHECK_LAUNCH();
 }
@@ -929,7 +949,7 @@ template <typename T, int LY, int LZ> void launch_yz(const HotDev& h, int B, cud
   using G = YZGeom<T, LY, LZ>;
   set_smem(k_yzconv<T, LY, LZ>, G::SMEM);
   dim3 g((unsigned)(h.W / G::TW), (unsigned)B);
-  k_yzconv<T, LY, LZ><<<g, G::NT, G::SMEM, s>>>(h);
+  launch_pdl(k_yzconv<T, LY, LZ>, dim3(g), dim3(G::NT), G::SMEM, s, h);
   AIMX_CHECK_LAUNCH();
 }
 template <typename T> bool run_yz_fused(const HotDev& h, int B, cudaStream_t s, Profiler* prof) {
@@ -1018,6 +1038,8 @@ void slab_matvec_t(std::vector<SlabRank*>& ranks, int Nx, int Ny, int Nz, SlabEx
 template <typename T2>
 __global__ void k_copy4(T2* __restrict__ dst, int64_t t0, int64_t t1, int64_t t2, const T2* __restrict__ src,
                         int64_t s0, int64_t s1, int64_t s2, int64_t d1, int64_t d2, int64_t d3, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t i3 = i % d3;
@@ -1042,10 +1064,10 @@ void copy4(void* dst, const int64_t t[3], const void* src, const int64_t st[3], 
   if (n <= 0) return;
   const unsigned g = (unsigned)((n + 255) / 256);
   if (csize == 8)
-    k_copy4<float2><<<g, 256, 0, s>>>((float2*)dst, t[0], t[1], t[2], (const float2*)src, st[0], st[1], st[2], d[1],
+    launch_pdl(k_copy4<float2>, dim3(g), dim3(256), 0, s, (float2*)dst, t[0], t[1], t[2], (const float2*)src, st[0], st[1], st[2], d[1],
                                      d[2], d[3], n);
   else
-    k_copy4<double2><<<g, 256, 0, s>>>((double2*)dst, t[0], t[1], t[2], (const double2*)src, st[0], st[1], st[2],
+    launch_pdl(k_copy4<double2>, dim3(g), dim3(256), 0, s, (double2*)dst, t[0], t[1], t[2], (const double2*)src, st[0], st[1], st[2],
                                       d[1], d[2], d[3], n);
   AIMX_CHECK_LAUNCH();
 }

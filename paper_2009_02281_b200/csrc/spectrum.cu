@@ -37,6 +37,8 @@ struct K0s { double v[kMaxBatch]; };
 template <typename T, bool STATIC>
 __global__ void k_sample(int Nx, int Ny, int Nz, int64_t noct, double h, K0s k0s,
                          typename CT<T>::T2* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   const int b = blockIdx.y;
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -128,6 +130,8 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
                                               const typename CT<T>::T2* __restrict__ twg,
                                               const typename CT<T>::T2* __restrict__ add, T scale,
                                               SampleArgs sa) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = EvGeom<T, L, SMALL>;
   constexpr int N1 = L / 2 + 1;
@@ -207,14 +211,14 @@ void even_rows(int L, int64_t nlines, int64_t noct, int B, const void* in, void*
       const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
       dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
       set_smem(k_even<T, L, true, 0, true>, sm);
-      k_even<T, L, true, 0, true><<<g, G::NT, sm, s>>>(nlines, 1, noct, (const T2*)in, (T2*)out,
+      launch_pdl(k_even<T, L, true, 0, true>, g, dim3(G::NT), sm, s, nlines, 1, noct, (const T2*)in, (T2*)out,
                                                        (const T2*)tw, nullptr, (T)1, SampleArgs{});
     } else {
       using G = EvGeom<T, L>;
       const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
       dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
       set_smem(k_even<T, L, true>, sm);
-      k_even<T, L, true><<<g, G::NT, sm, s>>>(nlines, 1, noct, (const T2*)in, (T2*)out, (const T2*)tw,
+      launch_pdl(k_even<T, L, true>, g, dim3(G::NT), sm, s, nlines, 1, noct, (const T2*)in, (T2*)out, (const T2*)tw,
                                               nullptr, (T)1, SampleArgs{});
     }
   }));
@@ -231,14 +235,14 @@ void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const v
       const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
       set_smem(k_even<T, L, false, 0, true>, sm);
       dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
-      k_even<T, L, false, 0, true><<<g, G::NT, sm, s>>>(0, inner, noct, (const T2*)in, (T2*)out,
+      launch_pdl(k_even<T, L, false, 0, true>, g, dim3(G::NT), sm, s, 0, inner, noct, (const T2*)in, (T2*)out,
                                                         (const T2*)tw, (const T2*)add, scale, SampleArgs{});
     } else {
       using G = EvGeom<T, L>;
       const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
       set_smem(k_even<T, L, false>, sm);
       dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
-      k_even<T, L, false><<<g, G::NT, sm, s>>>(0, inner, noct, (const T2*)in, (T2*)out, (const T2*)tw,
+      launch_pdl(k_even<T, L, false>, g, dim3(G::NT), sm, s, 0, inner, noct, (const T2*)in, (T2*)out, (const T2*)tw,
                                                (const T2*)add, scale, SampleArgs{});
     }
   }));
@@ -296,7 +300,7 @@ void spectrum_plan_free(SpectrumPlan& sp) {
 
 void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s) {
   K0s k{};
-  k_sample<double, true><<<dim3((unsigned)((sp.noct + 255) / 256), 1), 256, 0, s>>>(
+  launch_pdl(k_sample<double, true>, dim3((unsigned)((sp.noct + 255) / 256), 1), dim3(256), 0, s, 
       sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (double2*)sp.work0);
   AIMX_CHECK_LAUNCH();
   dct3<double>(sp, 1, sp.tw64, sp.work0, sp.work1, out, nullptr, 1.0, s);
@@ -307,7 +311,7 @@ void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
   K0s k{};
   for (int b = 0; b < B; ++b) k.v[b] = k0[b];
-  k_sample<float, false><<<dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), 256, 0, s>>>(
+  launch_pdl(k_sample<float, false>, dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), dim3(256), 0, s, 
       sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (float2*)sp.work0);
   AIMX_CHECK_LAUNCH();
   dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s);
@@ -318,7 +322,7 @@ void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const doubl
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
   K0s k{};
   for (int b = 0; b < B; ++b) k.v[b] = k0[b];
-  k_sample<double, false><<<dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), 256, 0, s>>>(
+  launch_pdl(k_sample<double, false>, dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), dim3(256), 0, s, 
       sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (double2*)sp.work0);
   AIMX_CHECK_LAUNCH();
   dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s);
