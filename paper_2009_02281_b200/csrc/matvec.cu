@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
 // line-fastest (line = tid % NL, t = tid / NL) so that a warp's loads and
 // stores cover consecutive grid columns; the per-line exchange uses one block
 // barrier per transform.
-template <typename S, int L> struct PassGeom {
+template <typename S, int L, bool SMALL = false> struct PassGeom {
   static constexpr int R1 = Fac<L>::R1, R2 = Fac<L>::R2;
   using TL = TwoLevel<R1, R2>;
   static constexpr int T = TL::T, E = TL::E;
@@ -165,7 +165,8 @@ template <typename S, int L> struct PassGeom {
   // warp holds 8 lines x 4 threads)
   static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? 4 : 1) : 0;
   static constexpr size_t BYTES256 = sizeof(typename CT<S>::T2) * (size_t)(256 / T) * XB;
-  static constexpr int NT = BYTES256 > 200 * 1024 ? 128 : 256;   // threads per CTA
+  // threads per CTA; SMALL: one x row (4 channel lines) per CTA when rows are few
+  static constexpr int NT = SMALL ? (4 * T > 64 ? 4 * T : 64) : (BYTES256 > 200 * 1024 ? 128 : 256);
   static constexpr int NL = NT / T;                               // lines per CTA
 };
 
@@ -184,11 +185,11 @@ __device__ __forceinline__ void inv_fft(T2* v, T2* xb, const T2* tw, int t) {
   fft2<T2, Fac<L>::R1, Fac<L>::R2, true>(v, xb, tw, t);
 }
 
-template <typename T, int L>
+template <typename T, int L, bool SMALL = false>
 __device__ __forceinline__ void pass_prologue(typename CT<T>::T2*& tw, typename CT<T>::T2*& xb,
                                               const typename CT<T>::T2* __restrict__ gtw, int line) {
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<T, L>;
+  using G = PassGeom<T, L, SMALL>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   tw = reinterpret_cast<T2*>(smem_raw);
   xb = tw + L + line * G::XB;
@@ -196,21 +197,21 @@ __device__ __forceinline__ void pass_prologue(typename CT<T>::T2*& tw, typename 
   __syncthreads();
 }
 
-template <typename T, int L> constexpr size_t pass_smem() {
-  using G = PassGeom<T, L>;
+template <typename T, int L, bool SMALL = false> constexpr size_t pass_smem() {
+  using G = PassGeom<T, L, SMALL>;
   return sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB);
 }
 
 // ---- x forward: occupied lines of S (x < Nx, zero padded) -> bufA[line_id][kx][c]
-template <typename T, int L>
+template <typename T, int L, bool SMALL>
 __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<T, L>;
+  using G = PassGeom<T, L, SMALL>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T, L>(tw, xb, (const T2*)h.twx, line);
+  pass_prologue<T, L, SMALL>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y;
   const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
   const bool act = r < h.nlines;
@@ -230,15 +231,15 @@ __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
 }
 
 // ---- x inverse: bufC[line_id][kx][c] -> phi[line][x < Nx][c]
-template <typename T, int L>
+template <typename T, int L, bool SMALL>
 __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<T, L>;
+  using G = PassGeom<T, L, SMALL>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T, L>(tw, xb, (const T2*)h.twx, line);
+  pass_prologue<T, L, SMALL>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y;
   const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
   const bool act = r < h.nlines;
@@ -412,9 +413,10 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
 // transform is one thread's register DFT.  bufA[z][y < Ny][col] -> bufC[z][y
 // occupied][col]; the padded intermediate never leaves the SM.
 template <typename T, int LY, int LZ> struct YZGeom {
-  static constexpr int TW = 16;                          // columns per CTA
+  static constexpr int TW = sizeof(T) == 4 ? 32 : 16;   // columns per CTA
   static constexpr int NT = 128;
-  static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (size_t)LZ * LY * TW;
+  // only z < N_z = LZ/2 is ever stored (inputs there, outputs cropped there)
+  static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (size_t)(LZ / 2) * LY * TW;
 };
 
 template <typename T, int LY, int LZ>
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 4 : 2) k_yzconv(HotDev h
   using G = YZGeom<T, LY, LZ>;
   constexpr int TW = G::TW, NT = G::NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* S = reinterpret_cast<T2*>(smem_raw);   // [z < LZ][ky < LY][TW]
+  T2* S = reinterpret_cast<T2*>(smem_raw);   // [z < Nz][ky < LY][TW]
   const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, W = h.W;
   const int b = blockIdx.y;
   const int col0 = blockIdx.x * TW;
@@ -819,19 +821,26 @@ void run_gather(const HotDev& h, const void* x, int64_t xstride, int B, cudaStre
   AIMX_CHECK_LAUNCH();
 }
 
-template <typename T, int L>
-void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
-  constexpr size_t sm = pass_smem<T, L>();
-  constexpr int RPC = PassGeom<T, L>::NL / 4;
+template <typename T, int L, bool SMALL>
+void run_x_geom(const HotDev& h, bool inv, int B, cudaStream_t s) {
+  constexpr size_t sm = pass_smem<T, L, SMALL>();
+  constexpr int RPC = PassGeom<T, L, SMALL>::NL / 4;
   dim3 g((unsigned)((h.nlines + RPC - 1) / RPC), (unsigned)B);
   if (!inv) {
-    set_smem(k_xfwd<T, L>, sm);
-    launch_pdl(k_xfwd<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
+    set_smem(k_xfwd<T, L, SMALL>, sm);
+    launch_pdl(k_xfwd<T, L, SMALL>, g, dim3(PassGeom<T, L, SMALL>::NT), sm, s, h);
   } else {
-    set_smem(k_xinv<T, L>, sm);
-    launch_pdl(k_xinv<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
+    set_smem(k_xinv<T, L, SMALL>, sm);
+    launch_pdl(k_xinv<T, L, SMALL>, g, dim3(PassGeom<T, L, SMALL>::NT), sm, s, h);
   }
   AIMX_CHECK_LAUNCH();
+}
+// x passes: below two waves of default CTAs, one x row per (smaller) CTA
+template <typename T, int L>
+void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
+  constexpr int RPC = PassGeom<T, L>::NL / 4;
+  if ((int64_t)(h.nlines + RPC - 1) / RPC * B < 2 * 148) run_x_geom<T, L, true>(h, inv, B, s);
+  else run_x_geom<T, L, false>(h, inv, B, s);
 }
 
 template <typename T, int L> dim3 col_grid(int W, int rows, int B) {
