@@ -105,12 +105,20 @@ __device__ __forceinline__ typename CT<T>::T2 ksample(int i, int j, int l, int N
       if (q > 0) re = inv4pi / (h * sqrt((double)q));
     } else if (q == 0) {
       im = -k0 * inv4pi;
-    } else {
+    } else if (sizeof(T) == 8) {
       const double r = h * sqrt((double)q);
       double s, c;
       sincos(0.5 * k0 * r, &s, &c);
       re = -2.0 * s * s * inv4pi / r;
       im = -2.0 * s * c * inv4pi / r;   // sin(x) = 2 sin(x/2) cos(x/2)
+    } else {   // fp32 result: phase formed and reduced in fp64, sin / cos in fp32
+      const double r = h * sqrt((double)q);
+      const double u = (0.25 / kPi) * (k0 * r);
+      const float red = (float)(u - rint(u));
+      float s, c;
+      sincospif(2.0f * red, &s, &c);
+      const float a = (float)inv4pi / (float)r;
+      return mk<T2>((T)(-2.0f * s * s * a), (T)(-2.0f * s * c * a));
     }
   }
   return mk<T2>((T)re, (T)im);
@@ -158,15 +166,29 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
     stride = inner;
   }
   T2 v[G::E];
-  if (MODE == 1) {   // row pass over x: line lg = j (Nz+1) + l, element n = i
+  if constexpr (MODE == 1) {   // row pass over x: line lg = j (Nz+1) + l, element n = i
     const int64_t lg = (int64_t)blockIdx.x * G::NL + line;
     const int jj = (int)(lg / (sa.Nz + 1)), ll = (int)(lg % (sa.Nz + 1));
     const double k0 = sa.k0[blockIdx.z];
+    if constexpr (G::XB >= N1) {
+      // each of the N1 samples once, staged in the line's exchange buffer
+      if (act)
+        for (int n = t; n < N1; n += G::T) xb[n] = ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0);
+      __syncthreads();
 #pragma unroll
-    for (int i = 0; i < G::E; ++i) {
-      int n = G::TL::in_index(t, i);
-      n = n <= L / 2 ? n : L - n;
-      v[i] = act ? ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0) : mk<T2>(0, 0);
+      for (int i = 0; i < G::E; ++i) {
+        int n = G::TL::in_index(t, i);
+        n = n <= L / 2 ? n : L - n;
+        v[i] = act ? xb[n] : mk<T2>(0, 0);
+      }
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int i = 0; i < G::E; ++i) {
+        int n = G::TL::in_index(t, i);
+        n = n <= L / 2 ? n : L - n;
+        v[i] = act ? ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0) : mk<T2>(0, 0);
+      }
     }
   } else {
 #pragma unroll
@@ -201,28 +223,35 @@ template <class K> void set_smem(K kernel, size_t bytes) {
 // CTAs of a pass with the default geometry; below two waves use SMALL CTAs
 template <typename T, int L> bool use_small(int64_t ctas_default) { return ctas_default < 2 * 148; }
 
+template <typename T, int L, bool SMALL>
+void even_rows_geom(int64_t nlines, int64_t noct, int B, const void* in, void* out, const void* tw, cudaStream_t s,
+                    const SampleArgs* gen) {
+  using T2 = typename CT<T>::T2;
+  using G = EvGeom<T, L, SMALL>;
+  const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+  dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
+  if (gen) {
+    set_smem(k_even<T, L, true, 1, SMALL>, sm);
+    launch_pdl(k_even<T, L, true, 1, SMALL>, g, dim3(G::NT), sm, s, nlines, (int64_t)1, noct, (const T2*)nullptr,
+               (T2*)out, (const T2*)tw, (const T2*)nullptr, (T)1, *gen);
+  } else {
+    set_smem(k_even<T, L, true, 0, SMALL>, sm);
+    launch_pdl(k_even<T, L, true, 0, SMALL>, g, dim3(G::NT), sm, s, nlines, (int64_t)1, noct, (const T2*)in,
+               (T2*)out, (const T2*)tw, (const T2*)nullptr, (T)1, SampleArgs{});
+  }
+  AIMX_CHECK_LAUNCH();
+}
+
+// x rows (contiguous lines); gen: the dynamic samples are generated in the pass
 template <typename T>
 void even_rows(int L, int64_t nlines, int64_t noct, int B, const void* in, void* out, const void* tw,
-               cudaStream_t s) {
-  using T2 = typename CT<T>::T2;
+               cudaStream_t s, const SampleArgs* gen = nullptr) {
   AIMX_SWITCH_L(L, ({
-    if (use_small<T, L>((nlines + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * B)) {
-      using G = EvGeom<T, L, true>;
-      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
-      dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
-      set_smem(k_even<T, L, true, 0, true>, sm);
-      launch_pdl(k_even<T, L, true, 0, true>, g, dim3(G::NT), sm, s, nlines, 1, noct, (const T2*)in, (T2*)out,
-                                                       (const T2*)tw, nullptr, (T)1, SampleArgs{});
-    } else {
-      using G = EvGeom<T, L>;
-      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
-      dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
-      set_smem(k_even<T, L, true>, sm);
-      launch_pdl(k_even<T, L, true>, g, dim3(G::NT), sm, s, nlines, 1, noct, (const T2*)in, (T2*)out, (const T2*)tw,
-                                              nullptr, (T)1, SampleArgs{});
-    }
+    if (use_small<T, L>((nlines + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * B))
+      even_rows_geom<T, L, true>(nlines, noct, B, in, out, tw, s, gen);
+    else
+      even_rows_geom<T, L, false>(nlines, noct, B, in, out, tw, s, gen);
   }));
-  AIMX_CHECK_LAUNCH();
 }
 
 template <typename T>
@@ -249,12 +278,86 @@ void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const v
   AIMX_CHECK_LAUNCH();
 }
 
+// z then y even-extension transforms of the octant for short z / y lengths
+// (2 N_z, 2 N_y <= 32): a CTA owns TW consecutive kx and all their (ky, kz)
+// in shared memory; each line transform is one thread's register DFT; the
+// epilogue out = scale (v + add) is fused.
+template <typename T, int LY, int LZ>
+__global__ void __launch_bounds__(128) k_evyz(int Nx, int Ny, int Nz, int64_t noct,
+                                              const typename CT<T>::T2* __restrict__ in,
+                                              typename CT<T>::T2* __restrict__ out,
+                                              const typename CT<T>::T2* __restrict__ add, T scale) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  constexpr int TW = 32, NT = 128;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* S = reinterpret_cast<T2*>(smem_raw);   // [ky <= Ny][kz <= Nz][TW]
+  const int nx1 = Nx + 1, ny1 = Ny + 1, nz1 = Nz + 1;
+  const int kx0 = blockIdx.x * TW;
+  const int64_t boff = (int64_t)blockIdx.y * noct;
+  for (int it = threadIdx.x; it < ny1 * nz1 * TW; it += NT) {
+    const int w = it % TW, r = it / TW, kx = kx0 + w;
+    S[it] = kx < nx1 ? in[boff + (int64_t)r * nx1 + kx] : mk<T2>(0, 0);
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < ny1 * TW; it += NT) {   // z: per (ky, column)
+    const int w = it % TW, ky = it / TW;
+    T2 v[LZ];
+#pragma unroll
+    for (int n = 0; n < LZ; ++n) v[n] = S[(ky * nz1 + (n <= LZ / 2 ? n : LZ - n)) * TW + w];
+    dftr<T2, LZ, false>(v);
+#pragma unroll
+    for (int k = 0; k <= LZ / 2; ++k) S[(ky * nz1 + k) * TW + w] = v[k];
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < nz1 * TW; it += NT) {   // y: per (kz, column), epilogue
+    const int w = it % TW, kz = it / TW, kx = kx0 + w;
+    if (kx >= nx1) continue;
+    T2 v[LY];
+#pragma unroll
+    for (int n = 0; n < LY; ++n) v[n] = S[((n <= LY / 2 ? n : LY - n) * nz1 + kz) * TW + w];
+    dftr<T2, LY, false>(v);
+#pragma unroll
+    for (int k = 0; k <= LY / 2; ++k) {
+      const int64_t gi = ((int64_t)k * nz1 + kz) * nx1 + kx;
+      const T2 a = add ? add[gi] : mk<T2>(0, 0);
+      out[boff + gi] = mk<T2>(scale * (v[k].x + a.x), scale * (v[k].y + a.y));
+    }
+  }
+}
+
+template <typename T, int LY, int LZ>
+void launch_evyz(const SpectrumPlan& sp, int B, const void* in, void* out, const void* add, T scale, cudaStream_t s) {
+  using T2 = typename CT<T>::T2;
+  const size_t sm = sizeof(T2) * (size_t)(sp.Ny + 1) * (sp.Nz + 1) * 32;
+  set_smem(k_evyz<T, LY, LZ>, sm);
+  launch_pdl(k_evyz<T, LY, LZ>, dim3((unsigned)((sp.Nx + 1 + 31) / 32), (unsigned)B), dim3(128), sm, s, sp.Nx,
+             sp.Ny, sp.Nz, sp.noct, (const T2*)in, (T2*)out, (const T2*)add, scale);
+  AIMX_CHECK_LAUNCH();
+}
+
+template <typename T>
+bool evyz(const SpectrumPlan& sp, int B, const void* in, void* out, const void* add, T scale, cudaStream_t s) {
+  switch (2 * sp.Ny * 64 + 2 * sp.Nz) {
+    case 8 * 64 + 8: launch_evyz<T, 8, 8>(sp, B, in, out, add, scale, s); return true;
+    case 16 * 64 + 8: launch_evyz<T, 16, 8>(sp, B, in, out, add, scale, s); return true;
+    case 32 * 64 + 8: launch_evyz<T, 32, 8>(sp, B, in, out, add, scale, s); return true;
+    case 8 * 64 + 16: launch_evyz<T, 8, 16>(sp, B, in, out, add, scale, s); return true;
+    case 16 * 64 + 16: launch_evyz<T, 16, 16>(sp, B, in, out, add, scale, s); return true;
+    case 32 * 64 + 16: launch_evyz<T, 32, 16>(sp, B, in, out, add, scale, s); return true;
+    case 16 * 64 + 32: launch_evyz<T, 16, 32>(sp, B, in, out, add, scale, s); return true;
+    default: return false;
+  }
+}
+
 // 3-D even-extension transform on the octant [B][y][z][x]: x rows, z cols, y cols.
 template <typename T>
 void dct3(SpectrumPlan& sp, int B, void** tw, void* a, void* b, void* out, const void* add, T scale,
-          cudaStream_t s) {
+          cudaStream_t s, const SampleArgs* gen = nullptr) {
   const int64_t nx = sp.Nx + 1, ny = sp.Ny + 1, nz = sp.Nz + 1, no = sp.noct;
-  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s);
+  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s, gen);
+  if (evyz<T>(sp, B, b, out, add, scale, s)) return;
   even_cols<T>(2 * sp.Nz, ny, nx, no, B, b, a, tw[2], nullptr, (T)1, s);
   even_cols<T>(2 * sp.Ny, 1, nz * nx, no, B, a, out, tw[1], add, scale, s);
 }
@@ -309,23 +412,19 @@ void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s) {
 void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
                           float2* out, cudaStream_t s) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  K0s k{};
-  for (int b = 0; b < B; ++b) k.v[b] = k0[b];
-  launch_pdl(k_sample<float, false>, dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), dim3(256), 0, s, 
-      sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (float2*)sp.work0);
-  AIMX_CHECK_LAUNCH();
-  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s);
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
+  for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
+  // K_d samples generated inside the x pass (each sample once per line)
+  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s, &sa);
 }
 
 void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs, double scale,
                           double2* out, cudaStream_t s) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  K0s k{};
-  for (int b = 0; b < B; ++b) k.v[b] = k0[b];
-  launch_pdl(k_sample<double, false>, dim3((unsigned)((sp.noct + 255) / 256), (unsigned)B), dim3(256), 0, s, 
-      sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (double2*)sp.work0);
-  AIMX_CHECK_LAUNCH();
-  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s);
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
+  for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
+  // K_d samples generated inside the x pass (each sample once per line)
+  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s, &sa);
 }
 
 }  // namespace aimx
