@@ -340,70 +340,100 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
 }
 
 // ---- z forward * H_hat * z inverse, in place on bufB (occupied planes only)
+// Each CTA walks ZROWS consecutive row sets (of RPC ky rows each) of its
+// column tile, so the twiddle table and the per-thread spectrum-slab offsets
+// are set up once; the slab of the next row set is prefetched with cp.async
+// while the current one is transformed.
+constexpr int ZROWS = 8;
 template <typename T, int L, bool FULLZ>
 __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_zconv(HotDev h) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
+  constexpr int NPF = G::E / 4;   // slab elements per thread: (RPC L CW/4) / NT
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   __builtin_assume(t < G::T);
   const int W = h.W, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
   const ColTile ct = col_tile<T, L>(line, W);
   const int b = blockIdx.z;
-  // prefetch this CTA's spectrum slab [rsub][kz][kx - kx0] into shared memory
-  // (cp.async, overlaps the column loads and the forward transform)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* hs = reinterpret_cast<T2*>(smem_raw) + L + (size_t)G::NL * G::XB;
+  T2* hs = reinterpret_cast<T2*>(smem_raw) + L + (size_t)G::NL * G::XB;   // [2][RPC][kz][kx - kx0]
   const int nkx = ct.CW / 4, kx0 = h.kx0 + (blockIdx.x * ct.CW) / 4;   // kx0: column slab offset
+  const int nslab = ct.RPC * L * nkx;
+  const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
+  const int64_t kystride = (int64_t)(Nz + 1) * (Nx + 1);
+  // this thread's slab elements: row-set-independent offset and row
+  int64_t poff[NPF];
+  int prow[NPF];
   {
-    const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
-    const int n = ct.RPC * L * nkx;
     const int lgk = __ffs(nkx) - 1;   // nkx: power of two
-    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NPF; ++k) {
+      const int idx = threadIdx.x + k * G::NT;
       const int kxl = idx & (nkx - 1), rest = idx >> lgk;
-      const int kz = rest % L, r = rest / L;   // L: compile-time power of two
-      const int kyy = blockIdx.y * ct.RPC + r;
-      const int kyf = kyy <= Ny ? kyy : Ny2 - kyy;
+      const int kz = rest % L;   // L: compile-time power of two
       const int kx = kx0 + kxl;
       const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
       const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
-      if (kyy < Ny2) cp_async(hs + idx, Hb + ((int64_t)kyf * (Nz + 1) + kzf) * (Nx + 1) + kxf);
+      poff[k] = (int64_t)kzf * (Nx + 1) + kxf;
+      prow[k] = rest / L;
     }
   }
+  auto prefetch = [&](int rs, int buf) {
+#pragma unroll
+    for (int k = 0; k < NPF; ++k) {
+      const int idx = threadIdx.x + k * G::NT;
+      const int kyy = rs * ct.RPC + prow[k];
+      const int kyf = kyy <= Ny ? kyy : Ny2 - kyy;
+      if (idx < nslab && kyy < Ny2) cp_async(hs + buf * nslab + idx, Hb + (int64_t)kyf * kystride + poff[k]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
   T2 *tw, *xb;
   pass_prologue<T, L>(tw, xb, (const T2*)h.twz_tab, line);
-  const int ky = blockIdx.y * ct.RPC + ct.rsub;
-  const bool act = ky < Ny2;
   const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
   const int64_t zs = (int64_t)Ny2 * W;
-  T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)(act ? ky : 0) * W + col;
   const uint8_t* __restrict__ zocc = h.zocc;
-  // input distribution D(R1,R2): z = t + T a + R1 n2 < Nz = L/2  <=>  n2 < R2/2
-  T2 v[G::E];
-#pragma unroll
-  for (int i = 0; i < G::E; ++i) {
-    const int z = G::TL::in_index(t, i);
-    if (i % G::R2 < G::R2 / 2) v[i] = (act && (FULLZ || zocc[z])) ? g[z * zs] : mk<T2>(0, 0);
-    else v[i] = mk<T2>(0, 0);
-  }
-  fwd_fft<T2, L>(v, xb, tw, t);
-  cp_async_wait_all();
-  __syncthreads();
-  {  // spectrum multiply (slab in shared memory, 1/M folded into H)
-    const T2* hl = hs + (size_t)ct.rsub * L * nkx + (ct.w >> 2);
+  const int rs0 = blockIdx.y * ZROWS;
+  prefetch(rs0, 0);
+  for (int it = 0; it < ZROWS; ++it) {
+    const int rs = rs0 + it;
+    if (rs * ct.RPC >= Ny2) break;   // uniform over the CTA
+    if (it + 1 < ZROWS && (rs + 1) * ct.RPC < Ny2) prefetch(rs + 1, (it + 1) & 1);
+    const int ky = rs * ct.RPC + ct.rsub;
+    const bool act = ky < Ny2;
+    T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)(act ? ky : 0) * W + col;
+    // input distribution D(R1,R2): z = t + T a + R1 n2 < Nz = L/2  <=>  n2 < R2/2
+    T2 v[G::E];
 #pragma unroll
     for (int i = 0; i < G::E; ++i) {
-      const int kz = TwoLevel<G::R2, G::R1>::in_index(t, i);
-      v[i] = cmul(v[i], hl[kz * nkx]);
+      const int z = G::TL::in_index(t, i);
+      if (i % G::R2 < G::R2 / 2) v[i] = (act && (FULLZ || zocc[z])) ? g[z * zs] : mk<T2>(0, 0);
+      else v[i] = mk<T2>(0, 0);
     }
-  }
-  inv_fft_swapped<T2, L>(v, xb, tw, t);
-  if (!act) return;
+    fwd_fft<T2, L>(v, xb, tw, t);
+    // this row set's slab has landed (the next one may still be in flight)
+    if (it + 1 < ZROWS && (rs + 1) * ct.RPC < Ny2) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    {  // spectrum multiply (slab in shared memory, 1/M folded into H)
+      const T2* hl = hs + (it & 1) * nslab + (size_t)ct.rsub * L * nkx + (ct.w >> 2);
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) {
-    const int z = G::TL::in_index(t, i);
-    if (i % G::R2 < G::R2 / 2 && (FULLZ || zocc[z])) g[z * zs] = v[i];
+      for (int i = 0; i < G::E; ++i) {
+        const int kz = TwoLevel<G::R2, G::R1>::in_index(t, i);
+        v[i] = cmul(v[i], hl[kz * nkx]);
+      }
+    }
+    inv_fft_swapped<T2, L>(v, xb, tw, t);
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < G::E; ++i) {
+        const int z = G::TL::in_index(t, i);
+        if (i % G::R2 < G::R2 / 2 && (FULLZ || zocc[z])) g[z * zs] = v[i];
+      }
+    }
+    __syncthreads();   // slab buffer (it & 1) is refilled two row sets later; xb reuse
   }
 }
 
@@ -866,9 +896,10 @@ void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
 
 template <typename T, int L>
 void run_z(const HotDev& h, int B, cudaStream_t s) {
-  // + spectrum slab: NL lines x L / 4 complex (RPC * L * CW / 4)
-  constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
+  // + two spectrum slabs: NL lines x L / 4 complex (RPC * L * CW / 4) each
+  constexpr size_t sm = pass_smem<T, L>() + 2 * sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
   dim3 g = col_grid<T, L>(h.W, 2 * h.Ny, B);
+  g.y = (g.y + ZROWS - 1) / ZROWS;   // row sets per CTA
   if (h.nzocc == h.Nz) {
     set_smem(k_zconv<T, L, true>, sm);
     launch_pdl(k_zconv<T, L, true>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
