@@ -231,6 +231,7 @@ struct HotDev {
   int W = 0;                     // row width (complex) of the y / z passes: 8 Nx, or 4 x (kx slab width)
   int kx0 = 0;                   // first kx of the column slab (slab-decomposed FFT), else 0
   int32_t* phi_line = nullptr;   // [nlines] phi line (y + Ny z) of each x-inverse line; null: line_id
+  const void* tmB = nullptr;     // HOST pointer to the CUtensorMap of bufB (k_zconv_tma), or null
   int G = 8;                     // lanes per node in the projection gather
   int twy = 4, twz = 4;          // tile widths (complex elements) of the y / z passes
   int64_t nnz = 0;
@@ -298,6 +299,8 @@ struct Combine {
 };
 
 bool fft_length_supported(int L);
+// bufB tensor map for the TMA z pass (out: 128-byte CUtensorMap); false if unavailable
+bool make_z_tensor_map(const HotDev& h, bool f32, void* out);
 int pick_tile(int L, int rowwidth, bool f32);
 void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof);

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <dlfcn.h>
 #include <memory>
 
@@ -52,6 +53,7 @@ struct aimx_ctx {
   int slots = 0;
   void* Hoct = nullptr;         // bound spectra [slots][noct], compute precision, scaled 1/M
   std::vector<void*> allocs;
+  std::vector<std::unique_ptr<CUtensorMap>> tmaps;   // tensor maps referenced by HotDev::tmB
   std::string last_error;
 };
 
@@ -296,6 +298,16 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   c->near_union += grp.ptr.back();
 }
 
+// TMA tensor map of a HotDev's bufB for the z pass (AIMX_NO_TMA=1 disables)
+void attach_z_map(aimx_ctx* c, HotDev& h) {
+  if (std::getenv("AIMX_NO_TMA")) return;
+  std::unique_ptr<CUtensorMap> m(new CUtensorMap);
+  if (make_z_tensor_map(h, c->prec == AIMX_C64, m.get())) {
+    h.tmB = m.get();
+    c->tmaps.push_back(std::move(m));
+  }
+}
+
 // batch slots from the full-grid per-frequency footprint (<= 1.5 GB of buffers)
 int choose_slots(aimx_ctx* c) {
   const Topology& t = c->topo;
@@ -372,6 +384,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   h.twx = make_twiddles(c, 2 * h.Nx);
   h.twy_tab = make_twiddles(c, 2 * h.Ny);
   h.twz_tab = make_twiddles(c, 2 * h.Nz);
+  attach_z_map(c, h);
   setup_spectrum(c);
   h.Hoct = c->Hoct;
   h.xt = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
@@ -594,6 +607,7 @@ void do_setup_slab(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc
     hc.Hoct = c->Hoct;
     hc.twy_tab = make_twiddles(c, 2 * Ny);
     hc.twz_tab = make_twiddles(c, 2 * Nz);
+    attach_z_map(c, hc);
     // x inverse of rows [y0, yh1) into phi (global line numbering)
     HotDev& hx = R.hx;
     hot_common(c, hx);

@@ -27,6 +27,7 @@
 #include "aimx_internal.h"
 #include "fft.cuh"
 #include "fft_reg.cuh"
+#include "tma.cuh"
 
 namespace aimx {
 
@@ -437,6 +438,126 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
   }
 }
 
+// ---- z conv with TMA (all z planes occupied, N_z <= 256, one ky row per
+// CTA step): per row set ONE tensor copy brings the CTA's [z < N_z][16 columns]
+// block into shared memory (mbarrier), double-buffered one row set ahead; the
+// results go back with one tensor store from the same buffer.  Loads and
+// stores never occupy registers, so the transforms of one row set overlap the
+// HBM traffic of the next.
+template <typename T, int L> struct ZTma {
+  using G = PassGeom<T, L>;
+  static constexpr int CW = G::NL;   // columns per CTA (one ky row per step)
+  static constexpr size_t OFF_HS = sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB);
+  static constexpr size_t HSB = sizeof(typename CT<T>::T2) * (size_t)L * CW / 4;   // one slab
+  static constexpr size_t OFF_IN = OFF_HS + 2 * HSB;
+  __host__ __device__ static size_t inb(int Nz) { return sizeof(typename CT<T>::T2) * (size_t)Nz * CW; }
+  __host__ __device__ static size_t smem(int Nz) { return OFF_IN + 2 * inb(Nz) + 16; }
+};
+
+template <typename T, int L>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_zconv_tma(HotDev h, const __grid_constant__ CUtensorMap tm) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<T, L>;
+  using Z = ZTma<T, L>;
+  constexpr int NPF = G::E / 4, CW = Z::CW, C0S = sizeof(T2) / 8;   // tensor elements per complex
+  const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  __builtin_assume(t < G::T);
+  const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
+  const int b = blockIdx.z;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][kz][kx - kx0]
+  T2* inb = reinterpret_cast<T2*>(smem_raw + Z::OFF_IN);                       // [2][z][CW]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Z::OFF_IN + 2 * Z::inb(Nz));
+  const int nkx = CW / 4, kx0 = h.kx0 + (blockIdx.x * CW) / 4;
+  const int nslab = L * nkx;
+  const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
+  const int64_t kystride = (int64_t)(Nz + 1) * (Nx + 1);
+  int64_t poff[NPF];
+  {
+    constexpr int LGK = CW == 64 ? 4 : (CW == 32 ? 3 : (CW == 16 ? 2 : (CW == 8 ? 1 : 0)));
+#pragma unroll
+    for (int k = 0; k < NPF; ++k) {
+      const int idx = threadIdx.x + k * G::NT;
+      const int kxl = idx & (nkx - 1), kz = (idx >> LGK) % L;
+      const int kx = kx0 + kxl;
+      const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
+      const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
+      poff[k] = (int64_t)kzf * (Nx + 1) + kxf;
+    }
+  }
+  auto prefetch = [&](int ky, int buf) {
+    const int kyf = ky <= Ny ? ky : Ny2 - ky;
+#pragma unroll
+    for (int k = 0; k < NPF; ++k) {
+      const int idx = threadIdx.x + k * G::NT;
+      if (idx < nslab) cp_async(hs + buf * nslab + idx, Hb + (int64_t)kyf * kystride + poff[k]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const int col0 = blockIdx.x * CW, rs0 = blockIdx.y * ZROWS;
+  const int nrs = min(ZROWS, Ny2 - rs0);
+  const uint32_t bytes = (uint32_t)Z::inb(Nz);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  T2 *tw, *xb;
+  pass_prologue<T, L>(tw, xb, (const T2*)h.twz_tab, line);   // includes a block barrier
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(bar, bytes);
+    tma_load4(inb, &tm, col0 * C0S, rs0, 0, b, bar);
+  }
+  prefetch(rs0, 0);
+  for (int it = 0; it < nrs; ++it) {
+    const int ky = rs0 + it, buf = it & 1;
+    T2* ib = inb + (size_t)buf * Nz * CW;
+    if (it + 1 < nrs) {
+      prefetch(ky + 1, buf ^ 1);
+      if (threadIdx.x == 0) {
+        bulk_wait_read0();   // the store of row set it-1 has read buffer buf^1
+        mbar_arrive_expect_tx(bar + (buf ^ 1), bytes);
+        tma_load4(inb + (size_t)(buf ^ 1) * Nz * CW, &tm, col0 * C0S, ky + 1, 0, b, bar + (buf ^ 1));
+      }
+    }
+    mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
+    // input distribution D(R1,R2): z = t + T a + R1 n2 < Nz = L/2  <=>  n2 < R2/2
+    T2 v[G::E];
+#pragma unroll
+    for (int i = 0; i < G::E; ++i) {
+      const int z = G::TL::in_index(t, i);
+      v[i] = (i % G::R2 < G::R2 / 2) ? ib[z * CW + line] : mk<T2>(0, 0);
+    }
+    fwd_fft<T2, L>(v, xb, tw, t);
+    if (it + 1 < nrs) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    {  // spectrum multiply (slab in shared memory, 1/M folded into H)
+      const T2* hl = hs + buf * nslab + (line >> 2);
+#pragma unroll
+      for (int i = 0; i < G::E; ++i) {
+        const int kz = TwoLevel<G::R2, G::R1>::in_index(t, i);
+        v[i] = cmul(v[i], hl[kz * nkx]);
+      }
+    }
+    inv_fft_swapped<T2, L>(v, xb, tw, t);
+#pragma unroll
+    for (int i = 0; i < G::E; ++i) {
+      const int z = G::TL::in_index(t, i);
+      if (i % G::R2 < G::R2 / 2) ib[z * CW + line] = v[i];
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store4(&tm, col0 * C0S, ky, 0, b, ib);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
 // ---- fused y fwd -> (z fwd * H_hat * z inv) -> y inv for short y and z
 // transforms (2 N_y, 2 N_z <= 32): one CTA owns a tile of TW grid columns
 // (col = 4 kx + channel) and all (y, z) of them in shared memory, every line
@@ -588,33 +709,6 @@ template <typename T, int R, int BB, bool PARTS> struct NearCfg {
   static constexpr size_t OFF_BAR = OFF_DESC + NDD * 16;
   static constexpr size_t SMEM = OFF_BAR + NDS * 8;
 };
-
-// ---- mbarrier + bulk-copy (TMA engine) helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-// global -> shared bulk copy (bytes: multiple of 16, both addresses 16-byte aligned)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 template <typename T2, int V>
 __device__ __forceinline__ void unpack(const typename VecT<T2, V>::type& u, T2* out) {
@@ -900,7 +994,13 @@ void run_z(const HotDev& h, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>() + 2 * sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
   dim3 g = col_grid<T, L>(h.W, 2 * h.Ny, B);
   g.y = (g.y + ZROWS - 1) / ZROWS;   // row sets per CTA
-  if (h.nzocc == h.Nz) {
+  if (h.tmB && h.nzocc == h.Nz && h.W >= PassGeom<T, L>::NL && h.Nz <= 256) {
+    using Z = ZTma<T, L>;
+    const size_t zs = Z::smem(h.Nz);
+    set_smem(k_zconv_tma<T, L>, zs);
+    dim3 gt((unsigned)(h.W / Z::CW), (unsigned)((2 * h.Ny + ZROWS - 1) / ZROWS), (unsigned)B);
+    launch_pdl(k_zconv_tma<T, L>, gt, dim3(PassGeom<T, L>::NT), zs, s, h, *(const CUtensorMap*)h.tmB);
+  } else if (h.nzocc == h.Nz) {
     set_smem(k_zconv<T, L, true>, sm);
     launch_pdl(k_zconv<T, L, true>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
   } else {
@@ -1110,6 +1210,38 @@ void copy4(void* dst, const int64_t t[3], const void* src, const int64_t st[3], 
     launch_pdl(k_copy4<double2>, dim3(g), dim3(256), 0, s, (double2*)dst, t[0], t[1], t[2], (const double2*)src, st[0], st[1], st[2],
                                       d[1], d[2], d[3], n);
   AIMX_CHECK_LAUNCH();
+}
+
+// Tensor map of bufB for k_zconv_tma: 4-D (column, ky, z, slot), box = the
+// z pass's column tile x 1 ky x all z.  Returns false if the driver entry
+// point is unavailable (the plain z pass is used then).
+bool make_z_tensor_map(const HotDev& h, bool f32, void* out) {
+  using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Enc enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    enc = (Enc)fn;
+  }
+  if (h.Nz > 256) return false;
+  int CW = 0;
+  AIMX_SWITCH_L(2 * h.Nz, (CW = f32 ? PassGeom<float, L>::NL : PassGeom<double, L>::NL));
+  if (h.W < CW) return false;
+  const cuuint64_t es = f32 ? 1 : 2;   // 8-byte tensor elements per complex
+  cuuint64_t dim[4] = {(cuuint64_t)h.W * es, (cuuint64_t)2 * h.Ny, (cuuint64_t)h.Nz, (cuuint64_t)h.batch};
+  cuuint64_t str[3] = {(cuuint64_t)h.W * 8 * es, (cuuint64_t)h.W * 8 * es * 2 * h.Ny,
+                       (cuuint64_t)h.W * 8 * es * 2 * h.Ny * h.Nz};
+  cuuint32_t box[4] = {(cuuint32_t)(CW * es), 1, (cuuint32_t)h.Nz, 1};
+  cuuint32_t est[4] = {1, 1, 1, 1};
+  CUresult r = enc((CUtensorMap*)out, f32 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                   h.bufB, dim, str, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 bool fft_length_supported(int L) { return L >= 8 && L <= 1024 && (L & (L - 1)) == 0; }
