@@ -164,10 +164,15 @@ void launch_static_near(const Topology& t, SetupDev& d, cudaStream_t s);
 void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 
 // ---------------------------------------------------------------- batching
-constexpr int kMaxBatch = 16;
+constexpr int kMaxBatch = 32;
 
 // CTAs per SM of the S4+S5 kernel (its register budget, __launch_bounds__)
 constexpr int near_ctas_per_sm(bool f32, bool single) { return f32 ? 5 : 4; }
+// S4+S5 chunk lengths (entries) in the payload: C chunks 1024 / s, W chunks
+// 256 / s, halved when the context holds 32 batch slots (the 32-column kernel
+// keeps the same registers per lane)
+constexpr int near_chc(bool f32, int slots) { return (f32 ? 128 : 64) / (slots >= 32 ? 2 : 1); }
+constexpr int near_chw(bool f32, int slots) { return (f32 ? 32 : 16) / (slots >= 32 ? 2 : 1); }
 
 // ---------------------------------------------------------------- spectrum
 // Octant layout (all spectra): index ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.

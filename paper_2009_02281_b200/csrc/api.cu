@@ -263,7 +263,8 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   NearChunks ck;
   const bool f32 = c->prec == AIMX_C64;
   const int cs = f32 ? 8 : 16;
-  build_near_chunks(grp, f32 ? 32 : 16, f32 ? 128 : 64, cs, ck);
+  if (c->slots <= 0) throw Error(AIMX_E_INTERNAL, "batch slots not chosen before the near layout");
+  build_near_chunks(grp, near_chw(f32, c->slots), near_chc(f32, c->slots), cs, ck);
   // value slot (u R + r) -> payload byte offset
   for (auto& v : grp.slot)
     if (v >= 0) v = ck.uoff_c[v / grp.R] + (v % grp.R) * cs;
@@ -364,11 +365,11 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   const Topology& t = c->topo;
   HotDev& h = c->hot;
   hot_common(c, h);
+  const int slots = c->slots = choose_slots(c);
   build_gather(c, h, c->nodes);
   build_near(c, h, {});
   // ---- batch slots and grid buffers
   const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
-  const int slots = c->slots = choose_slots(c);
   const int64_t nS = (int64_t)h.nlines * h.Nx * 4;
   const int64_t nA = (int64_t)h.Nz * h.Ny * 2 * h.Nx * 4;
   const int64_t nB = (int64_t)h.Nz * 2 * h.Ny * 2 * h.Nx * 4;
@@ -906,9 +907,12 @@ static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, 
   }
 }
 
-static int sweep_batch(const aimx_ctx* c, int32_t batch) {
-  int B = batch > 0 ? batch : c->hot.batch;
-  return std::max(1, std::min(B, c->hot.batch));
+// device batch of a sweep: the caller's, else the slots, balanced over the
+// number of batches the sweep needs (e.g. 100 points in 32 slots: 4 x 25)
+static int sweep_batch(const aimx_ctx* c, int32_t batch, int64_t nf) {
+  if (batch > 0) return std::max(1, std::min<int>(batch, c->hot.batch));
+  const int64_t S = c->hot.batch, nb = (nf + S - 1) / S;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(S, nb > 0 ? (nf + nb - 1) / nb : S));
 }
 
 aimx_status aimx_sweep(aimx_ctx* c, int64_t nf, const double* f_hz, const void* X, void* Y,
@@ -927,7 +931,7 @@ aimx_status aimx_sweep(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
   }
-  sweep_impl(c, nf, f_hz, (const char*)X, (char*)Y, sweep_batch(c, batch), s);
+  sweep_impl(c, nf, f_hz, (const char*)X, (char*)Y, sweep_batch(c, batch, nf), s);
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
   AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
@@ -946,7 +950,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  const int64_t B = sweep_batch(c, batch);
+  const int64_t B = sweep_batch(c, batch, nf);
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   const int64_t need = 2 * B * (int64_t)vb;
   if (c->stage_bytes < need) {

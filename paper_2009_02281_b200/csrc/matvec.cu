@@ -688,7 +688,8 @@ template <typename T, int R, int BB, bool PARTS> struct NearCfg {
   using T2 = typename CT<T>::T2;
   static constexpr int NT = 128;                      // threads per CTA
   static constexpr int S = (int)sizeof(T2);           // complex bytes
-  static constexpr int CHC = 1024 / S, CHW = 256 / S; // entries per C / W chunk
+  // entries per C / W chunk (at most; near_chc / near_chw, halved for 32 columns)
+  static constexpr int CHC = (BB >= 32 ? 512 : 1024) / S, CHW = (BB >= 32 ? 128 : 256) / S;
   static constexpr int COEFB = CHC * R * S;           // coefficient bytes (C: R pairs; W: R real4 = 2 S per entry)
   static constexpr int STB = COEFB + CHC * 4 + 16;    // stage: one chunk payload (NearChunks)
   static constexpr int D = kNearD;                    // pipeline depth (chunks)
@@ -1024,7 +1025,7 @@ __global__ void k_interleave(int nb, int B, int BB, const typename CT<T>::T2* __
 }
 
 template <int BB> constexpr int bucket_ok() { return BB; }
-inline int batch_bucket(int B) { return B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : (B <= 8 ? 8 : 16))); }
+inline int batch_bucket(int B) { return B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : (B <= 8 ? 8 : (B <= 16 ? 16 : 32)))); }
 
 template <typename T>
 void run_interleave(const HotDev& h, const void* x, const Combine& c, cudaStream_t s) {
@@ -1045,7 +1046,8 @@ void run_gather_b(const HotDev& h, int B, cudaStream_t s) {
     case 2: launch_pdl(k_gather_b<T, 2>, dim3(g), dim3(256), 0, s, h, xt, B); break;
     case 4: launch_pdl(k_gather_b<T, 4>, dim3(g), dim3(256), 0, s, h, xt, B); break;
     case 8: launch_pdl(k_gather_b<T, 8>, dim3(g), dim3(256), 0, s, h, xt, B); break;
-    default: launch_pdl(k_gather_b<T, 16>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    case 16: launch_pdl(k_gather_b<T, 16>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    default: launch_pdl(k_gather_b<T, 32>, dim3(g), dim3(256), 0, s, h, xt, B); break;
   }
   AIMX_CHECK_LAUNCH();
 }
@@ -1073,7 +1075,8 @@ void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Comb
     case 2: launch_interp<T, R, 2, false>(h, h.xt, y0, y1, c, s); break;
     case 4: launch_interp<T, R, 4, false>(h, h.xt, y0, y1, c, s); break;
     case 8: launch_interp<T, R, 8, false>(h, h.xt, y0, y1, c, s); break;
-    default: launch_interp<T, R, 16, false>(h, h.xt, y0, y1, c, s); break;
+    case 16: launch_interp<T, R, 16, false>(h, h.xt, y0, y1, c, s); break;
+    default: launch_interp<T, R, 32, false>(h, h.xt, y0, y1, c, s); break;
   }
 }
 

@@ -185,12 +185,12 @@ def test_sweep_results_independent_of_batch_size(prec):
     near-row reduction is partitioned differently, so results agree to rounding."""
     import torch
     op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), prec)
-    assert op.stats()["batch_slots"] >= 4
+    assert op.stats()["batch_slots"] >= 20
     freqs = np.linspace(20e6, 400e6, 11)
     X = to_gpu(np.stack([inp.rhs_vector(1, i, op.N) for i in range(11)]), prec)
     ref = op.sweep(freqs, X, batch=1).clone()
     tol = 1e-6 if prec == "c64" else 1e-14
-    for b in (2, 3, 4, 16):
+    for b in (2, 3, 4, 16, 11 + 9):
         y = op.sweep(freqs, X, batch=b).clone()
         assert torch.equal(op.sweep(freqs, X, batch=b), y)
         assert rel_l2(y.cpu().numpy(), ref.cpu().numpy()) <= tol
@@ -221,8 +221,14 @@ def test_near_row_group_layouts(R, order, prec, monkeypatch):
     assert rel_l2(yP.cpu().numpy(), -oR) <= TOL[prec]
     freqs = np.linspace(40e6, 500e6, 11)
     X = np.stack([inp.rhs_vector(1, i, op.N) for i in range(11)])
-    Y = op.sweep(freqs, to_gpu(X, prec), batch=11).cpu().numpy()
+    Y = op.sweep(freqs, to_gpu(X, prec), batch=11).cpu().numpy()       # 16-column kernels
     for i, f in enumerate(freqs):
         orc.set_frequency(f)
         z = orc.matvec(gpu_input_as_c128(X[i], prec))
         assert rel_l2(Y[i], z) <= TOL[prec]
+    freqs = np.linspace(40e6, 500e6, 21)
+    X = np.stack([inp.rhs_vector(1, i, op.N) for i in range(21)])
+    Y = op.sweep(freqs, to_gpu(X, prec), batch=21).cpu().numpy()       # 32-column kernels
+    for i in (0, 7, 20):
+        orc.set_frequency(freqs[i])
+        assert rel_l2(Y[i], orc.matvec(gpu_input_as_c128(X[i], prec))) <= TOL[prec]
