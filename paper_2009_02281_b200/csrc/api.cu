@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -36,6 +37,12 @@ struct aimx_ctx {
   bool freq_set = false;
   double f = 0, k0 = 0, omega = 0;
   cudaEvent_t ev_spec = nullptr, ev_use = nullptr;
+  // sweep pipeline: side stream for the next batch's spectra, double buffer
+  cudaStream_t s2 = nullptr;
+  void* HB[2] = {nullptr, nullptr};
+  cudaStream_t sc[2] = {nullptr, nullptr};   // host sweep copy streams (H2D, D2H)
+  std::vector<cudaEvent_t> ev_io;
+  cudaEvent_t ev_start = nullptr, ev_sp[2] = {nullptr, nullptr}, ev_mv[2] = {nullptr, nullptr};
   void* stage = nullptr;        // sweep_host staging
   int64_t stage_bytes = 0;
   double setup_seconds = 0;
@@ -388,6 +395,16 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   attach_z_map(c, h);
   setup_spectrum(c);
   h.Hoct = c->Hoct;
+  {
+    const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
+    for (int k = 0; k < 2; ++k) c->HB[k] = dalloc<char>(c, noct * slots * (int64_t)cs);
+    AIMX_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+    AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k) {
+      AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_sp[k], cudaEventDisableTiming));
+      AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_mv[k], cudaEventDisableTiming));
+    }
+  }
   h.xt = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
   finish_setup(c);
 }
@@ -657,7 +674,8 @@ void do_setup_slab(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc
 }
 
 // S1 for B frequency points into spectrum slots 0..B-1.
-void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s) {
+void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s, void* out = nullptr) {
+  if (!out) out = c->Hoct;
   double k0[kMaxBatch];
   for (int b = 0; b < B; ++b) {
     if (!(f[b] > 0.0) || !std::isfinite(f[b])) throw Error(AIMX_E_INVALID_ARG, "frequency must be finite and > 0");
@@ -667,9 +685,9 @@ void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s) {
   const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
   StageScope sc(&c->prof, 0, s);
   if (c->prec == AIMX_C64)
-    spectrum_dynamic_f32(c->sp, B, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)c->Hoct, s);
+    spectrum_dynamic_f32(c->sp, B, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)out, s);
   else
-    spectrum_dynamic_f64(c->sp, B, k0, c->Hs, 1.0 / M, (double2*)c->Hoct, s);
+    spectrum_dynamic_f64(c->sp, B, k0, c->Hs, 1.0 / M, (double2*)out, s);
 }
 
 void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
@@ -762,6 +780,18 @@ void destroy_impl(aimx_ctx* c) {
   if (c->stage) cudaFree(c->stage);
   if (c->ev_spec) cudaEventDestroy(c->ev_spec);
   if (c->ev_use) cudaEventDestroy(c->ev_use);
+  if (c->s2) {
+    cudaStreamSynchronize(c->s2);
+    cudaStreamDestroy(c->s2);
+  }
+  for (int k = 0; k < 2; ++k)
+    if (c->sc[k]) {
+      cudaStreamSynchronize(c->sc[k]);
+      cudaStreamDestroy(c->sc[k]);
+    }
+  for (cudaEvent_t e : c->ev_io) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_start, c->ev_sp[0], c->ev_sp[1], c->ev_mv[0], c->ev_mv[1]})
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -898,12 +928,44 @@ aimx_status aimx_matvec_parts(aimx_ctx* c, const void* x, void* yA, void* yPhi, 
   return matvec_common(c, x, yA, yPhi, 1, stream);
 }
 
+// Several device batches: the spectra of batch i+1 are generated on a side
+// stream (double-buffered) while batch i's matvec runs, so S1 overlaps S2-S5.
+// before(i) / after(i): hooks on the compute stream around device batch i
+// (the host sweep orders its copies with them).
 static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, char* Y, int B,
-                       cudaStream_t s) {
+                       cudaStream_t s, const std::function<void(int64_t)>& before = nullptr,
+                       const std::function<void(int64_t)>& after = nullptr) {
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
-  for (int64_t i = 0; i < nf; i += B) {
-    const int nb_ = (int)std::min<int64_t>(B, nf - i);
-    run_batch(c, nb_, f + i, X + i * vb, Y + i * vb, s);
+  if (c->slab || nf <= B || !c->s2) {
+    for (int64_t i = 0; i < nf; i += B) {
+      const int nb_ = (int)std::min<int64_t>(B, nf - i);
+      if (before) before(i / B);
+      run_batch(c, nb_, f + i, X + i * vb, Y + i * vb, s);
+      if (after) after(i / B);
+    }
+    return;
+  }
+  const int64_t nbat = (nf + B - 1) / B;
+  auto count = [&](int64_t i) { return (int)std::min<int64_t>(B, nf - i * B); };
+  AIMX_CUDA(cudaEventRecord(c->ev_start, s));
+  AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_start, 0));
+  auto spec = [&](int64_t i) {
+    if (i >= 2) AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_mv[i % 2], 0));   // matvec i-2 read this buffer
+    spectra(c, count(i), f + i * B, c->s2, c->HB[i % 2]);
+    AIMX_CUDA(cudaEventRecord(c->ev_sp[i % 2], c->s2));
+  };
+  spec(0);
+  for (int64_t i = 0; i < nbat; ++i) {
+    if (i + 1 < nbat) spec(i + 1);
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_sp[i % 2], 0));
+    if (before) before(i);
+    HotDev hh = c->hot;
+    hh.Hoct = c->HB[i % 2];
+    Combine cb = make_combine(count(i), f + i * B, 0, c->hot.nb);
+    if (c->prec == AIMX_C64) hot_matvec_f32(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
+    else hot_matvec_f64(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
+    AIMX_CUDA(cudaEventRecord(c->ev_mv[i % 2], s));
+    if (after) after(i);
   }
 }
 
@@ -952,7 +1014,11 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   cudaStream_t s = pick(c, stream);
   const int64_t B = sweep_batch(c, batch, nf);
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
-  const int64_t need = 2 * B * (int64_t)vb;
+  // staging: as many whole batches as fit in 1 GB (all of them for cfg1/cfg2), so
+  // the device batches pipeline; copies of the next chunk wait for this one
+  const int64_t fit = std::max<int64_t>(1, (int64_t)(1ll << 30) / (2 * (int64_t)vb) / B);
+  const int64_t CH = std::min<int64_t>((nf + B - 1) / B, fit) * B;
+  const int64_t need = 2 * CH * (int64_t)vb;
   if (c->stage_bytes < need) {
     if (c->stage) AIMX_CUDA(cudaFree(c->stage));
     c->stage = nullptr;
@@ -960,18 +1026,49 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
     c->stage_bytes = need;
   }
   char* dX = (char*)c->stage;
-  char* dY = dX + B * vb;
+  char* dY = dX + CH * vb;
   const bool had = c->freq_set;
   const double f0 = c->f;
   if (s != c->stream) {
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
   }
-  for (int64_t i0 = 0; i0 < nf; i0 += B) {
-    const int64_t nb_ = std::min(B, nf - i0);
-    AIMX_CUDA(cudaMemcpyAsync(dX, (const char*)X + i0 * vb, nb_ * vb, cudaMemcpyHostToDevice, s));
-    sweep_impl(c, nb_, f_hz + i0, dX, dY, (int)B, s);
-    AIMX_CUDA(cudaMemcpyAsync((char*)Y + i0 * vb, dY, nb_ * vb, cudaMemcpyDeviceToHost, s));
+  // per device batch: host->device copy on one copy stream, device->host on
+  // another, ordered with the batch's compute by events, so both directions
+  // overlap the other batches' compute
+  if (!c->sc[0]) {
+    for (int k = 0; k < 2; ++k) AIMX_CUDA(cudaStreamCreateWithFlags(&c->sc[k], cudaStreamNonBlocking));
+  }
+  const int64_t nbat_max = (CH + B - 1) / B;
+  while ((int64_t)c->ev_io.size() < 2 * nbat_max + 1) {
+    cudaEvent_t e;
+    AIMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ev_io.push_back(e);
+  }
+  for (int64_t i0 = 0; i0 < nf; i0 += CH) {
+    const int64_t nb_ = std::min(CH, nf - i0);
+    const int64_t nbat = (nb_ + B - 1) / B;
+    cudaEvent_t go = c->ev_io[2 * nbat_max];
+    AIMX_CUDA(cudaEventRecord(go, s));   // staging free: the previous chunk's work is done
+    AIMX_CUDA(cudaStreamWaitEvent(c->sc[0], go, 0));
+    AIMX_CUDA(cudaStreamWaitEvent(c->sc[1], go, 0));
+    for (int64_t i = 0; i < nbat; ++i) {
+      const int64_t n = std::min<int64_t>(B, nb_ - i * B);
+      AIMX_CUDA(cudaMemcpyAsync(dX + i * B * vb, (const char*)X + (i0 + i * B) * vb, n * vb,
+                                cudaMemcpyHostToDevice, c->sc[0]));
+      AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i], c->sc[0]));
+    }
+    auto before = [&](int64_t i) { AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_io[2 * i], 0)); };
+    auto after = [&](int64_t i) {
+      const int64_t n = std::min<int64_t>(B, nb_ - i * B);
+      AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i + 1], s));
+      AIMX_CUDA(cudaStreamWaitEvent(c->sc[1], c->ev_io[2 * i + 1], 0));
+      AIMX_CUDA(cudaMemcpyAsync((char*)Y + (i0 + i * B) * vb, dY + i * B * vb, n * vb, cudaMemcpyDeviceToHost,
+                                c->sc[1]));
+    };
+    sweep_impl(c, nb_, f_hz + i0, dX, dY, (int)B, s, before, after);
+    AIMX_CUDA(cudaEventRecord(go, c->sc[1]));
+    AIMX_CUDA(cudaStreamWaitEvent(s, go, 0));   // results are home before the next chunk / return
   }
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
