@@ -444,29 +444,39 @@ __global__ void __launch_bounds__(256, (L <= 256 && sizeof(T) == 4) ? 3 : 1) k_z
 // results go back with one tensor store from the same buffer.  Loads and
 // stores never occupy registers, so the transforms of one row set overlap the
 // HBM traffic of the next.
+// z-pass geometry of the TMA kernel: 16 lines (columns) per CTA in fp32, 8 in
+// fp64 (smaller CTAs, more of them resident)
+template <typename S, int L> struct ZGeom {
+  static constexpr int R1 = Fac<L>::R1, R2 = Fac<L>::R2;
+  using TL = TwoLevel<R1, R2>;
+  static constexpr int T = TL::T, E = TL::E;
+  static constexpr int XB = PassGeom<S, L>::XB;
+  static constexpr int NL = sizeof(S) == 4 ? 16 : 8, NT = NL * T;   // (measured on cfg3)
+};
 template <typename T, int L> struct ZTma {
-  using G = PassGeom<T, L>;
+  using G = ZGeom<T, L>;
   static constexpr int CW = G::NL;   // columns per CTA (one ky row per step)
   static constexpr size_t OFF_HS = sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB);
   static constexpr size_t HSB = sizeof(typename CT<T>::T2) * (size_t)L * CW / 4;   // one slab
-  static constexpr size_t OFF_IN = OFF_HS + 2 * HSB;
+  static constexpr size_t OFF_IN = (OFF_HS + 2 * HSB + 127) / 128 * 128;   // TMA: 128-byte aligned
   __host__ __device__ static size_t inb(int Nz) { return sizeof(typename CT<T>::T2) * (size_t)Nz * CW; }
-  __host__ __device__ static size_t smem(int Nz) { return OFF_IN + 2 * inb(Nz) + 16; }
+  __host__ __device__ static size_t smem(int Nz) { return OFF_IN + 2 * inb(Nz) + 16 + 128; }
 };
 
 template <typename T, int L>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_zconv_tma(HotDev h, const __grid_constant__ CUtensorMap tm) {
+__global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zconv_tma(HotDev h, const __grid_constant__ CUtensorMap tm) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
-  using G = PassGeom<T, L>;
+  using G = ZGeom<T, L>;
   using Z = ZTma<T, L>;
   constexpr int NPF = G::E / 4, CW = Z::CW, C0S = sizeof(T2) / 8;   // tensor elements per complex
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   __builtin_assume(t < G::T);
   const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
   const int b = blockIdx.z;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_dyn[];
+  unsigned char* smem_raw = (unsigned char*)(((uintptr_t)smem_dyn + 127) & ~(uintptr_t)127);
   T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][kz][kx - kx0]
   T2* inb = reinterpret_cast<T2*>(smem_raw + Z::OFF_IN);                       // [2][z][CW]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Z::OFF_IN + 2 * Z::inb(Nz));
@@ -504,8 +514,10 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_zconv_tma(HotDe
     mbar_init(bar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  T2 *tw, *xb;
-  pass_prologue<T, L>(tw, xb, (const T2*)h.twz_tab, line);   // includes a block barrier
+  T2* tw = reinterpret_cast<T2*>(smem_raw);
+  T2* xb = tw + L + line * G::XB;
+  for (int i = threadIdx.x; i < L; i += G::NT) tw[i] = ((const T2*)h.twz_tab)[i];
+  __syncthreads();
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(bar, bytes);
     tma_load4(inb, &tm, col0 * C0S, rs0, 0, b, bar);
@@ -995,12 +1007,12 @@ void run_z(const HotDev& h, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>() + 2 * sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
   dim3 g = col_grid<T, L>(h.W, 2 * h.Ny, B);
   g.y = (g.y + ZROWS - 1) / ZROWS;   // row sets per CTA
-  if (h.tmB && h.nzocc == h.Nz && h.W >= PassGeom<T, L>::NL && h.Nz <= 256) {
+  if (h.tmB && h.nzocc == h.Nz && h.W >= ZGeom<T, L>::NL && h.Nz <= 256) {
     using Z = ZTma<T, L>;
     const size_t zs = Z::smem(h.Nz);
     set_smem(k_zconv_tma<T, L>, zs);
     dim3 gt((unsigned)(h.W / Z::CW), (unsigned)((2 * h.Ny + ZROWS - 1) / ZROWS), (unsigned)B);
-    launch_pdl(k_zconv_tma<T, L>, gt, dim3(PassGeom<T, L>::NT), zs, s, h, *(const CUtensorMap*)h.tmB);
+    launch_pdl(k_zconv_tma<T, L>, gt, dim3(ZGeom<T, L>::NT), zs, s, h, *(const CUtensorMap*)h.tmB);
   } else if (h.nzocc == h.Nz) {
     set_smem(k_zconv<T, L, true>, sm);
     launch_pdl(k_zconv<T, L, true>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
@@ -1233,7 +1245,7 @@ bool make_z_tensor_map(const HotDev& h, bool f32, void* out) {
   }
   if (h.Nz > 256) return false;
   int CW = 0;
-  AIMX_SWITCH_L(2 * h.Nz, (CW = f32 ? PassGeom<float, L>::NL : PassGeom<double, L>::NL));
+  AIMX_SWITCH_L(2 * h.Nz, (CW = f32 ? ZGeom<float, L>::NL : ZGeom<double, L>::NL));
   if (h.W < CW) return false;
   const cuuint64_t es = f32 ? 1 : 2;   // 8-byte tensor elements per complex
   cuuint64_t dim[4] = {(cuuint64_t)h.W * es, (cuuint64_t)2 * h.Ny, (cuuint64_t)h.Nz, (cuuint64_t)h.batch};
