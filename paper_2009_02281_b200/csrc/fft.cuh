@@ -64,6 +64,13 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return up2(r);
 }
 
+// acc += s x for a complex x and a real s: one FFMA2 in fp32, two DFMA in fp64
+__device__ __forceinline__ void axpy(float2& acc, float s, const float2& x) { acc = ffma2(make_float2(s, s), x, acc); }
+__device__ __forceinline__ void axpy(double2& acc, double s, const double2& x) {
+  acc.x = fma(s, x.x, acc.x);
+  acc.y = fma(s, x.y, acc.y);
+}
+
 template <typename T2> __device__ __forceinline__ T2 cadd(T2 a, T2 b) { return mk<T2>(a.x + b.x, a.y + b.y); }
 template <typename T2> __device__ __forceinline__ T2 csub(T2 a, T2 b) { return mk<T2>(a.x - b.x, a.y - b.y); }
 template <typename T2> __device__ __forceinline__ T2 cmul(T2 a, T2 b) {

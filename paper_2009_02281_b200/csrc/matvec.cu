@@ -75,7 +75,10 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
 
 // S2 for BB right-hand sides at once (batch-interleaved xt[n * BB + b]):
 // warp per occupied node, groups of BB/V lanes stride its entries (each entry's
-// weights and RWG index read once for all columns), lanes cover columns.
+// weights and RWG index read once for all columns), lanes cover columns.  The
+// entries come in coalesced chunks of 32 (the next chunk's loaded while this
+// one is used); within a chunk each group issues its x-row loads 8 at a time
+// before the arithmetic (packed FFMA2 in fp32).
 template <typename T, int BB>
 __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                   int B) {
@@ -85,6 +88,8 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
   using T4 = typename CT<T>::T4;
   constexpr int V = sizeof(T2) == 8 ? 2 : 1;
   constexpr int LG = BB / V, NG = 32 / LG;
+  constexpr int PER = 32 / NG;             // entries of a chunk per group
+  constexpr int QB = PER < 8 ? PER : 8;    // loads in flight per batch
   using VT = typename std::conditional<V == 2, float4, double2>::type;
   const int lane = threadIdx.x & 31;
   const int b0 = (lane % LG) * V, g = lane / LG;
@@ -97,38 +102,54 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
     for (int c = 0; c < 4; ++c) a[v][c] = mk<T2>(0, 0);
   const T4* __restrict__ ew = (const T4*)h.ent_w;
   const int e0 = h.node_ptr[q], e1 = h.node_ptr[q + 1];
+  int myr = 0;
+  T4 myw{0, 0, 0, 0};
+  if (e0 + lane < e1) {
+    myr = h.ent_rwg[e0 + lane];
+    myw = ew[e0 + lane];
+  }
   for (int base = e0; base < e1; base += 32) {
-    // 32 entries loaded coalesced, then handed to the groups by shuffles
-    const int ee = base + lane;
-    const bool ok = ee < e1;
-    const int myr = ok ? h.ent_rwg[ee] : 0;
-    const T4 myw = ok ? ew[ee] : T4{0, 0, 0, 0};
-#pragma unroll
-    for (int j = 0; j < 32; j += NG) {
-    const int src = j + g;
-    if (base + j >= e1) break;
-    T4 w;
-    w.x = __shfl_sync(0xffffffffu, myw.x, src);
-    w.y = __shfl_sync(0xffffffffu, myw.y, src);
-    w.z = __shfl_sync(0xffffffffu, myw.z, src);
-    w.w = __shfl_sync(0xffffffffu, myw.w, src);
-    const int rr = __shfl_sync(0xffffffffu, myr, src);
-    const VT u = *(const VT*)(xt + (int64_t)rr * BB + b0);
-    T2 xv[V];
-    if constexpr (V == 2) {
-      xv[0] = mk<T2>(u.x, u.y);
-      xv[1] = mk<T2>(u.z, u.w);
-    } else {
-      xv[0] = u;
+    const int nx = base + 32 + lane;
+    int nr = 0;
+    T4 nw{0, 0, 0, 0};
+    if (nx < e1) {   // next chunk, in flight during this one
+      nr = h.ent_rwg[nx];
+      nw = ew[nx];
     }
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      a[v][0].x += w.x * xv[v].x; a[v][0].y += w.x * xv[v].y;
-      a[v][1].x += w.y * xv[v].x; a[v][1].y += w.y * xv[v].y;
-      a[v][2].x += w.z * xv[v].x; a[v][2].y += w.z * xv[v].y;
-      a[v][3].x += w.w * xv[v].x; a[v][3].y += w.w * xv[v].y;
+    for (int jb = 0; jb < PER; jb += QB) {
+      VT u[QB];
+      T4 w[QB];
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) {
+        const int src = (jb + qq) * NG + g;   // entries past the node carry zero weights
+        w[qq].x = __shfl_sync(0xffffffffu, myw.x, src);
+        w[qq].y = __shfl_sync(0xffffffffu, myw.y, src);
+        w[qq].z = __shfl_sync(0xffffffffu, myw.z, src);
+        w[qq].w = __shfl_sync(0xffffffffu, myw.w, src);
+        const int rr = __shfl_sync(0xffffffffu, myr, src);
+        u[qq] = *(const VT*)(xt + (int64_t)rr * BB + b0);
+      }
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) {
+        T2 xv[V];
+        if constexpr (V == 2) {
+          xv[0] = mk<T2>(u[qq].x, u[qq].y);
+          xv[1] = mk<T2>(u[qq].z, u[qq].w);
+        } else {
+          xv[0] = u[qq];
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          axpy(a[v][0], w[qq].x, xv[v]);
+          axpy(a[v][1], w[qq].y, xv[v]);
+          axpy(a[v][2], w[qq].z, xv[v]);
+          axpy(a[v][3], w[qq].w, xv[v]);
+        }
+      }
     }
-    }
+    myr = nr;
+    myw = nw;
   }
 #pragma unroll
   for (int o = LG; o < 32; o <<= 1)
@@ -673,29 +694,6 @@ template <> struct VecT<float2, 1> { using type = float2; };
 template <> struct VecT<float2, 2> { using type = float4; };
 template <> struct VecT<double2, 1> { using type = double2; };
 
-// acc += s * x for a complex x and a real s: one packed FFMA2 (fma.rn.f32x2,
-// sm_100) in fp32 with s broadcast, two DFMA in fp64.
-__device__ __forceinline__ unsigned long long f2_as_u64(const float2& v) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
-  return r;
-}
-__device__ __forceinline__ float2 u64_as_f2(unsigned long long r) {
-  float2 v;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-  return v;
-}
-__device__ __forceinline__ float2 fma2(const float2& a, const float2& b, const float2& c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)), "l"(f2_as_u64(c)));
-  return u64_as_f2(r);
-}
-__device__ __forceinline__ void axpy(float2& acc, float s, const float2& x) { acc = fma2(make_float2(s, s), x, acc); }
-__device__ __forceinline__ void axpy(double2& acc, double s, const double2& x) {
-  acc.x = fma(s, x.x, acc.x);
-  acc.y = fma(s, x.y, acc.y);
-}
-
 template <typename T, int R, int BB, bool PARTS> struct NearCfg {
   using T2 = typename CT<T>::T2;
   static constexpr int NT = 128;                      // threads per CTA
@@ -847,7 +845,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1)
             }
           } else if constexpr (K::S == 8 && V == 2) {
             // (ce_0, ce_1) = C_A - beta_b C_rho for both columns: one FFMA2
-            const T2 ce = fma2(nbe2, mk<T2>(cv[r].y, cv[r].y), mk<T2>(cv[r].x, cv[r].x));
+            const T2 ce = ffma2(nbe2, mk<T2>(cv[r].y, cv[r].y), mk<T2>(cv[r].x, cv[r].x));
             axpy(acc[r * V], ce.x, xv[0]);
             axpy(acc[r * V + 1], ce.y, xv[1]);
           } else {
