@@ -299,6 +299,7 @@ struct Combine {
   int B = 1;                     // frequency points in this launch (<= batch slots)
   int mode = 0;                  // 0: y = alpha (yA - beta yR); 1: parts y0 = yA, y1 = -yR
   int64_t xstride = 0, ystride = 0;   // complex elements between batch vectors
+  int xt_ready = 0;              // 1: h.xt already holds the interleaved columns (sweep pipeline)
   double alpha_im[kMaxBatch];    // alpha = j * alpha_im = -j w mu0
   double beta[kMaxBatch];        // k0^-2
 };
@@ -309,6 +310,9 @@ bool make_z_tensor_map(const HotDev& h, bool f32, void* out);
 int pick_tile(int L, int rowwidth, bool f32);
 void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof);
+// xt <- the batch-interleaved columns of x (Combine: B, xstride)
+void interleave_f32(const HotDev& h, const void* x, const Combine& c, cudaStream_t s);
+void interleave_f64(const HotDev& h, const void* x, const Combine& c, cudaStream_t s);
 void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof);
 // Slab-decomposed hot path: every rank's S2-S5; the exchanges go through

@@ -40,6 +40,7 @@ struct aimx_ctx {
   // sweep pipeline: side stream for the next batch's spectra, double buffer
   cudaStream_t s2 = nullptr;
   void* HB[2] = {nullptr, nullptr};
+  void* XT[2] = {nullptr, nullptr};            // interleaved columns of batches i, i+1
   cudaStream_t sc[2] = {nullptr, nullptr};   // host sweep copy streams (H2D, D2H)
   std::vector<cudaEvent_t> ev_io;
   cudaEvent_t ev_start = nullptr, ev_sp[2] = {nullptr, nullptr}, ev_mv[2] = {nullptr, nullptr};
@@ -398,6 +399,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   {
     const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
     for (int k = 0; k < 2; ++k) c->HB[k] = dalloc<char>(c, noct * slots * (int64_t)cs);
+    for (int k = 0; k < 2; ++k) c->XT[k] = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
     AIMX_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
     AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
@@ -934,7 +936,8 @@ aimx_status aimx_matvec_parts(aimx_ctx* c, const void* x, void* yA, void* yPhi, 
 // (the host sweep orders its copies with them).
 static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, char* Y, int B,
                        cudaStream_t s, const std::function<void(int64_t)>& before = nullptr,
-                       const std::function<void(int64_t)>& after = nullptr) {
+                       const std::function<void(int64_t)>& after = nullptr,
+                       const std::function<void(int64_t, cudaStream_t)>& before_side = nullptr) {
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   if (c->slab || nf <= B || !c->s2) {
     for (int64_t i = 0; i < nf; i += B) {
@@ -949,9 +952,17 @@ static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, 
   auto count = [&](int64_t i) { return (int)std::min<int64_t>(B, nf - i * B); };
   AIMX_CUDA(cudaEventRecord(c->ev_start, s));
   AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_start, 0));
+  // side stream, per batch: its spectra and its interleaved columns (xt),
+  // double-buffered; `before` (the host sweep's copy) gates the columns
   auto spec = [&](int64_t i) {
-    if (i >= 2) AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_mv[i % 2], 0));   // matvec i-2 read this buffer
+    if (i >= 2) AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_mv[i % 2], 0));   // matvec i-2 read these buffers
     spectra(c, count(i), f + i * B, c->s2, c->HB[i % 2]);
+    HotDev hh = c->hot;
+    hh.xt = c->XT[i % 2];
+    Combine cb = make_combine(count(i), f + i * B, 0, c->hot.nb);
+    if (before_side) before_side(i, c->s2);
+    if (c->prec == AIMX_C64) interleave_f32(hh, X + i * B * vb, cb, c->s2);
+    else interleave_f64(hh, X + i * B * vb, cb, c->s2);
     AIMX_CUDA(cudaEventRecord(c->ev_sp[i % 2], c->s2));
   };
   spec(0);
@@ -961,7 +972,9 @@ static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, 
     if (before) before(i);
     HotDev hh = c->hot;
     hh.Hoct = c->HB[i % 2];
+    hh.xt = c->XT[i % 2];
     Combine cb = make_combine(count(i), f + i * B, 0, c->hot.nb);
+    cb.xt_ready = 1;
     if (c->prec == AIMX_C64) hot_matvec_f32(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
     else hot_matvec_f64(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
     AIMX_CUDA(cudaEventRecord(c->ev_mv[i % 2], s));
@@ -1059,6 +1072,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
       AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i], c->sc[0]));
     }
     auto before = [&](int64_t i) { AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_io[2 * i], 0)); };
+    auto before_side = [&](int64_t i, cudaStream_t s2) { AIMX_CUDA(cudaStreamWaitEvent(s2, c->ev_io[2 * i], 0)); };
     auto after = [&](int64_t i) {
       const int64_t n = std::min<int64_t>(B, nb_ - i * B);
       AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i + 1], s));
@@ -1066,7 +1080,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
       AIMX_CUDA(cudaMemcpyAsync((char*)Y + (i0 + i * B) * vb, dY + i * B * vb, n * vb, cudaMemcpyDeviceToHost,
                                 c->sc[1]));
     };
-    sweep_impl(c, nb_, f_hz + i0, dX, dY, (int)B, s, before, after);
+    sweep_impl(c, nb_, f_hz + i0, dX, dY, (int)B, s, before, after, before_side);
     AIMX_CUDA(cudaEventRecord(go, c->sc[1]));
     AIMX_CUDA(cudaStreamWaitEvent(s, go, 0));   // results are home before the next chunk / return
   }

@@ -1130,7 +1130,7 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
   const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz, B = c.B;
   {
     StageScope sc(prof, 1, s);
-    run_interleave<T>(h, x, c, s);   // xt: 16-byte aligned staging copy for the S4+S5 kernel
+    if (!c.xt_ready) run_interleave<T>(h, x, c, s);   // xt: batch-interleaved columns (gather, S4+S5)
     if (B == 1) run_gather<T>(h, x, c.xstride, B, s);
     else run_gather_b<T>(h, B, s);
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, B, s)));
@@ -1271,6 +1271,12 @@ int pick_tile(int L, int rowwidth, bool f32) {
   return t;
 }
 
+void interleave_f32(const HotDev& h, const void* x, const Combine& c, cudaStream_t s) {
+  run_interleave<float>(h, x, c, s);
+}
+void interleave_f64(const HotDev& h, const void* x, const Combine& c, cudaStream_t s) {
+  run_interleave<double>(h, x, c, s);
+}
 void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof) {
   hot_matvec<float>(h, x, y0, y1, c, s, prof);
