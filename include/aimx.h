@@ -123,6 +123,18 @@ typedef struct {
 aimx_status aimx_setup(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid,
                        aimx_prec prec, int device, void* stream, aimx_ctx** out);
 
+/* Static-setup cache (P:905-906 suggests storing the
+ * frequency-independent near matrix to disk and reusing it across sweeps).
+ * aimx_save_static writes the fp64 static matrices (C_A, C_rho and their four
+ * constituents, CSR order), the projection weights and their exact-zero flags,
+ * keyed by a hash of the mesh arrays and the grid descriptor.
+ * aimx_setup_cached is aimx_setup that reads them instead of computing the
+ * static fill: the integer topology is rebuilt from `mesh` and must match the
+ * file (else AIMX_E_INVALID_ARG); results are bit-identical to aimx_setup. */
+aimx_status aimx_save_static(const aimx_ctx* ctx, const char* path);
+aimx_status aimx_setup_cached(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, aimx_prec prec,
+                              int device, const char* path, void* stream, aimx_ctx** out);
+
 /* S1: bind the frequency f (Hz): k0 = 2 pi f / c0; H_hat(k0) = H_hat_s +
  * DFT3(K_d(k0)) with K_d = (e^{-j k0 r} - 1)/(4 pi r) (eq:hgfd P:231) and
  * K_d(0) = -j k0/(4 pi) (eq:Hdmm P:331), generated on the device on the

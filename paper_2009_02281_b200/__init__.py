@@ -81,6 +81,9 @@ ABI_FUNCTIONS = {
     "aimx_setup_slab": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Grid), C.c_int, C.c_int, C.c_int32,
                                   C.c_int32, _P, _P, C.POINTER(_P)]),
     "aimx_nccl_unique_id": (C.c_int, [_P]),
+    "aimx_save_static": (C.c_int, [_P, C.c_char_p]),
+    "aimx_setup_cached": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Grid), C.c_int, C.c_int, C.c_char_p, _P,
+                                    C.POINTER(_P)]),
 }
 
 
@@ -140,10 +143,11 @@ class AIMx:
 
     def __init__(self, vertices, triangles, n, order: int = 2, near_cells: int = 2,
                  h: float = 0.0, origin=(0.0, 0.0, 0.0), prec: str = "c64",
-                 device: int | None = None, stream=None, slab=None):
+                 device: int | None = None, stream=None, slab=None, static_cache: str | None = None):
         """slab: None (one GPU), ("emulate", world) (slab-decomposed FFT with
         `world` ranks emulated on this GPU), or (rank, world, nccl_id) (this
-        process is one rank of the slab-decomposed FFT, NCCL)."""
+        process is one rank of the slab-decomposed FFT, NCCL).  static_cache: path of
+        an aimx_save_static file to load the static matrices from (one context)."""
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("AIMx needs a CUDA device (no CPU fallback)")
@@ -165,7 +169,10 @@ class AIMx:
             self._stream = s
             ctx = _P()
             pc = AIMX_C64 if prec == "c64" else AIMX_C128
-            if slab is None:
+            if slab is None and static_cache is not None:
+                st = self.lib.aimx_setup_cached(C.byref(mesh), C.byref(g), pc, self.device,
+                                                os.fsencode(static_cache), _P(s.cuda_stream), C.byref(ctx))
+            elif slab is None:
                 st = self.lib.aimx_setup(C.byref(mesh), C.byref(g), pc, self.device,
                                          _P(s.cuda_stream), C.byref(ctx))
             elif slab[0] == "emulate":
@@ -183,6 +190,10 @@ class AIMx:
         self.freq = None
 
     # ----------------------------------------------------------- lifecycle
+    def save_static(self, path: str):
+        """Write the static matrices (aimx_save_static) for AIMx(..., static_cache=path)."""
+        _check(self.lib, self.lib.aimx_save_static(self.ctx, os.fsencode(path)), self.ctx)
+
     def close(self):
         if getattr(self, "ctx", None):
             self.lib.aimx_destroy(self.ctx)

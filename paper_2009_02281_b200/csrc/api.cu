@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
 #include <functional>
 #include <mutex>
 #include <string>
@@ -51,6 +52,7 @@ struct aimx_ctx {
   int64_t near_union = 0;
   Profiler prof;
   std::vector<uint8_t> nz;      // exactly-nonzero projection weights [N_b][p3]
+  bool from_cache = false;      // S0 static matrices read from an aimx_save_static file
   // slab-decomposed FFT (aimx_setup_slab)
   bool slab = false;
   int world = 1, rank = 0;
@@ -165,9 +167,80 @@ void* make_twiddles(aimx_ctx* c, int L) {
 }
 
 // ---- S0 common part: topology, fp64 static fill, weights, full node map
-void setup_static(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid) {
+// ---- static-setup cache (the frequency-independent near matrix is
+// stored and reused across sweeps).  Key: FNV-1a of the mesh arrays and the
+// grid descriptor (h and origin after derivation); payload: the fp64 static
+// matrices in CSR order, the projection weights and their exact-zero flags.
+constexpr char kCacheMagic[8] = {'A', 'I', 'M', 'X', 'S', 'T', 'A', 'T'};
+constexpr int64_t kCacheVersion = 1;
+
+uint64_t static_key(const Topology& t) {
+  uint64_t hsh = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t i = 0; i < n; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+  };
+  mix(t.V.data(), t.V.size() * sizeof(double));
+  mix(t.T.data(), t.T.size() * sizeof(int32_t));
+  mix(t.n, sizeof(t.n));
+  mix(&t.order, sizeof(t.order));
+  mix(&t.near_cells, sizeof(t.near_cells));
+  mix(&t.h, sizeof(t.h));
+  mix(t.origin, sizeof(t.origin));
+  return hsh;
+}
+
+struct CacheHeader {
+  char magic[8];
+  int64_t version, key, nb, nnz, p3;
+};
+
+void setup_static(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid,
+                  const char* cache = nullptr) {
   Topology& t = c->topo;
   build_topology(mesh, grid, t);
+  if (cache) {   // the topology is rebuilt (cheap, integer) and must match the file
+    std::FILE* fp = std::fopen(cache, "rb");
+    if (!fp) throw Error(AIMX_E_INVALID_ARG, std::string("cannot open static cache ") + cache);
+    std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(fp, std::fclose);
+    CacheHeader hd;
+    if (std::fread(&hd, sizeof(hd), 1, fp) != 1 || std::memcmp(hd.magic, kCacheMagic, 8) != 0 ||
+        hd.version != kCacheVersion)
+      throw Error(AIMX_E_INVALID_ARG, "not an AIMx static cache (or another version)");
+    if ((uint64_t)hd.key != static_key(t) || hd.nb != t.nb || hd.nnz != t.rowptr[t.nb] || hd.p3 != t.p3)
+      throw Error(AIMX_E_INVALID_ARG, "static cache was written for another mesh or grid");
+    for (int a = 0; a < 3; ++a)
+      if (!fft_length_supported(2 * t.n[a]))
+        throw Error(AIMX_E_UNSUPPORTED, "2*N_a must be a power of two in [8, 1024]");
+    const int64_t nb = t.nb, nnz = t.rowptr[nb], p3 = t.p3;
+    SetupDev& d = c->sd;
+    d.anchor = dupload(c, t.anchor);
+    d.rowptr = dupload(c, t.rowptr);
+    d.col = dupload(c, t.col);
+    std::vector<double> buf((size_t)std::max<int64_t>(nnz, nb * p3 * 4));
+    auto read_up = [&](double*& dst, int64_t n) {
+      if (std::fread(buf.data(), sizeof(double), (size_t)n, fp) != (size_t)n)
+        throw Error(AIMX_E_INVALID_ARG, "static cache truncated");
+      dst = dalloc<double>(c, n);
+      AIMX_CUDA(cudaMemcpy(dst, buf.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    };
+    read_up(d.CA, nnz);
+    read_up(d.CR, nnz);
+    read_up(d.LA_NR, nnz);
+    read_up(d.YR_NR, nnz);
+    read_up(d.LA_P, nnz);
+    read_up(d.YR_P, nnz);
+    read_up(d.lam, nb * p3 * 4);
+    c->nz.resize((size_t)(nb * p3));
+    if (std::fread(c->nz.data(), 1, c->nz.size(), fp) != c->nz.size())
+      throw Error(AIMX_E_INVALID_ARG, "static cache truncated");
+    d.LA_un = dalloc<double>(c, 1);
+    d.YR_un = dalloc<double>(c, 1);
+    build_nodemap(t, c->nz, c->nodes);
+    c->slots = 0;
+    c->from_cache = true;
+    return;
+  }
   for (int a = 0; a < 3; ++a)
     if (!fft_length_supported(2 * t.n[a]))
       throw Error(AIMX_E_UNSUPPORTED, "2*N_a must be a power of two in [8, 1024]");
@@ -359,7 +432,7 @@ void setup_spectrum(aimx_ctx* c) {
 
 void finish_setup(aimx_ctx* c) {
   const Topology& t = c->topo;
-  const int64_t nnz = t.rowptr[t.nb];
+  const int64_t nnz = c->from_cache ? 1 : t.rowptr[t.nb];
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
   dfree(c, c->sd.LA_un, nnz * (int64_t)sizeof(double));
   dfree(c, c->sd.YR_un, nnz * (int64_t)sizeof(double));
@@ -368,8 +441,8 @@ void finish_setup(aimx_ctx* c) {
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
 }
 
-void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid) {
-  setup_static(c, mesh, grid);
+void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, const char* cache = nullptr) {
+  setup_static(c, mesh, grid, cache);
   const Topology& t = c->topo;
   HotDev& h = c->hot;
   hot_common(c, h);
@@ -880,6 +953,76 @@ aimx_status aimx_setup_slab(const aimx_mesh_desc* mesh, const aimx_grid_desc* gr
     destroy_impl(c);
     return AIMX_E_INTERNAL;
   }
+}
+
+aimx_status aimx_setup_cached(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, aimx_prec prec, int device,
+                              const char* path, void* stream, aimx_ctx** out) {
+  g_setup_error.clear();
+  if (!out || !path) { g_setup_error = "out or path is NULL"; return AIMX_E_INVALID_ARG; }
+  *out = nullptr;
+  if (prec != AIMX_C64 && prec != AIMX_C128) { g_setup_error = "bad precision"; return AIMX_E_INVALID_ARG; }
+  aimx_ctx* c = nullptr;
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    AIMX_CUDA(cudaSetDevice(device));
+    c = new aimx_ctx;
+    c->device = device;
+    c->prec = prec;
+    c->stream = (cudaStream_t)stream;
+    do_setup(c, mesh, grid, path);
+    c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = c;
+    return AIMX_OK;
+  } catch (const Error& e) {
+    g_setup_error = e.what();
+    destroy_impl(c);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_setup_error = "host allocation failed";
+    destroy_impl(c);
+    return AIMX_E_OOM;
+  } catch (const std::exception& e) {
+    g_setup_error = e.what();
+    destroy_impl(c);
+    return AIMX_E_INTERNAL;
+  }
+}
+
+aimx_status aimx_save_static(const aimx_ctx* cc, const char* path) {
+  aimx_ctx* c = const_cast<aimx_ctx*>(cc);
+  if (!c || !path) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  AIMX_CUDA(cudaSetDevice(c->device));
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  const Topology& t = c->topo;
+  const int64_t nb = t.nb, nnz = t.rowptr[nb], p3 = t.p3;
+  std::FILE* fp = std::fopen(path, "wb");
+  if (!fp) throw Error(AIMX_E_INVALID_ARG, std::string("cannot write ") + path);
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(fp, std::fclose);
+  CacheHeader hd;
+  std::memcpy(hd.magic, kCacheMagic, 8);
+  hd.version = kCacheVersion;
+  hd.key = (int64_t)static_key(t);
+  hd.nb = nb;
+  hd.nnz = nnz;
+  hd.p3 = p3;
+  bool ok = std::fwrite(&hd, sizeof(hd), 1, fp) == 1;
+  std::vector<double> buf((size_t)std::max<int64_t>(nnz, nb * p3 * 4));
+  auto put = [&](const double* src, int64_t n) {
+    AIMX_CUDA(cudaMemcpy(buf.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost));
+    ok = ok && std::fwrite(buf.data(), sizeof(double), (size_t)n, fp) == (size_t)n;
+  };
+  const SetupDev& d = c->sd;
+  put(d.CA, nnz);
+  put(d.CR, nnz);
+  put(d.LA_NR, nnz);
+  put(d.YR_NR, nnz);
+  put(d.LA_P, nnz);
+  put(d.YR_P, nnz);
+  put(d.lam, nb * p3 * 4);
+  ok = ok && std::fwrite(c->nz.data(), 1, c->nz.size(), fp) == c->nz.size();
+  if (!ok) throw Error(AIMX_E_INVALID_ARG, std::string("write failed: ") + path);
+  AIMX_API_END(c)
 }
 
 aimx_status aimx_nccl_unique_id(uint8_t id[128]) {

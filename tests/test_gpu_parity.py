@@ -232,3 +232,24 @@ def test_near_row_group_layouts(R, order, prec, monkeypatch):
     for i in (0, 7, 20):
         orc.set_frequency(freqs[i])
         assert rel_l2(Y[i], orc.matvec(gpu_input_as_c128(X[i], prec))) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_static_cache_roundtrip(prec, tmp_path):
+    """aimx_save_static / aimx_setup_cached: the cached context
+    reproduces the computed one bit for bit; a cache of another mesh is refused."""
+    import torch
+    from paper_2009_02281_b200 import AIMxError
+    m = inp.make_mesh(1)
+    op = make_gpu_op(m, (16, 16, 4), prec)
+    path = str(tmp_path / "cfg1.aimxstat")
+    op.save_static(path)
+    op2 = make_gpu_op(m, (16, 16, 4), prec, static_cache=path)
+    for k in ("CA", "CR", "LA_NR"):
+        assert np.array_equal(op.static()[k], op2.static()[k])
+    freqs = np.linspace(50e6, 300e6, 5)
+    X = to_gpu(np.stack([inp.rhs_vector(1, i, op.N) for i in range(5)]), prec)
+    assert torch.equal(op.sweep(freqs, X), op2.sweep(freqs, X))
+    other = inp.icosphere_mesh(2)
+    with pytest.raises(AIMxError):
+        make_gpu_op(other, (16, 8, 32), prec, static_cache=path)
