@@ -165,6 +165,22 @@ aimx_status aimx_matvec_parts(aimx_ctx* ctx, const void* x, void* yA, void* yPhi
 aimx_status aimx_sweep(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* X,
                        void* Y, int32_t batch, void* stream);
 
+/* Iterative solve: for i < nf, Z(f_hz[i]) X[i,:] = RHS[i,:]
+ * by restarted GMRES(restart) as the paper's sweep does (GMRES,
+ * relative residual `tol`, the paper uses 1e-4), right-preconditioned with the
+ * diagonal of the frequency-independent near matrix (M(k0) =
+ * diag(-j w mu0 (L^A_s,NR[m,m] + k0^-2 L^phi_s,NR[m,m]))), x0 = 0.
+ * Frequencies run in device batches (as aimx_sweep): each batch's spectra
+ * are generated once and all its columns iterate together, each with its own
+ * Krylov basis (Arnoldi by classical Gram-Schmidt applied twice, Givens on the
+ * host).  RHS, X: device [nf][N_b]; f_hz, iters (iterations used, may be
+ * NULL) and relres (final true residual ||RHS - Z X|| / ||RHS||, may be NULL)
+ * are HOST arrays.  maxiter bounds the iterations per batch.  One-GPU contexts
+ * only (AIMX_E_UNSUPPORTED for slab contexts).  Synchronises `stream` per
+ * iteration (the Hessenberg work is on the host). */
+aimx_status aimx_solve(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* RHS, void* X, double tol,
+                       int32_t restart, int32_t maxiter, int32_t* iters, double* relres, void* stream);
+
 /* The same sweep with X, Y in HOST memory (pinned or pageable): the library
  * stages each batch host->device and the results device->host on `stream`
  * and synchronises the stream before returning. */

@@ -82,6 +82,8 @@ ABI_FUNCTIONS = {
                                   C.c_int32, _P, _P, C.POINTER(_P)]),
     "aimx_nccl_unique_id": (C.c_int, [_P]),
     "aimx_save_static": (C.c_int, [_P, C.c_char_p]),
+    "aimx_solve": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_double, C.c_int32, C.c_int32,
+                             C.POINTER(C.c_int32), C.POINTER(C.c_double), _P]),
     "aimx_setup_cached": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Grid), C.c_int, C.c_int, C.c_char_p, _P,
                                     C.POINTER(_P)]),
 }
@@ -250,6 +252,23 @@ class AIMx:
                                              self._vec(X, (nf, self.N)), self._vec(Y, (nf, self.N)),
                                              int(batch), self._s(stream)), self.ctx)
         return Y
+
+    def solve(self, freqs, RHS, X=None, tol: float = 1e-4, restart: int = 30, maxiter: int = 1000,
+              stream=None):
+        """GMRES solve Z(f_i) X[i] = RHS[i] (aimx_solve); returns (X, iterations, relative residuals)."""
+        torch = _torch()
+        f = np.ascontiguousarray(freqs, dtype=np.float64)
+        nf = f.shape[0]
+        if X is None:
+            X = torch.empty((nf, self.N), dtype=self.cdtype, device=RHS.device)
+        its = np.zeros(nf, np.int32)
+        rr = np.zeros(nf, np.float64)
+        _check(self.lib, self.lib.aimx_solve(self.ctx, nf, f.ctypes.data_as(C.POINTER(C.c_double)),
+                                             self._vec(RHS, (nf, self.N)), self._vec(X, (nf, self.N)),
+                                             float(tol), int(restart), int(maxiter),
+                                             its.ctypes.data_as(C.POINTER(C.c_int32)),
+                                             rr.ctypes.data_as(C.POINTER(C.c_double)), self._s(stream)), self.ctx)
+        return X, its, rr
 
     def sweep_host(self, freqs, X, Y, batch: int = 0, stream=None):
         """X, Y: host (CPU) torch tensors [nf, N] (pinned for best speed)."""

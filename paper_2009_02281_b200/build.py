@@ -42,7 +42,7 @@ def _nccl_include():
 
 COMMON = COMMON + _nccl_include()
 
-SOURCES = ["host_setup.cpp", "setup_kernels.cu", "spectrum.cu", "matvec.cu", "api.cu"]
+SOURCES = ["host_setup.cpp", "setup_kernels.cu", "spectrum.cu", "matvec.cu", "solve.cu", "api.cu"]
 
 
 def _newer(src, obj, deps):

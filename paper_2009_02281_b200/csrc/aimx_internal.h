@@ -304,6 +304,21 @@ struct Combine {
   double beta[kMaxBatch];        // k0^-2
 };
 
+// ---- batched GMRES building blocks (solve.cu); B columns of N per block
+struct PcArgs {
+  double alpha_im[kMaxBatch];   // M_b = j alpha_im[b] (dA - beta[b] dR): the static diagonal preconditioner
+  double beta[kMaxBatch];
+};
+void gm_pc(bool f32, int B, int64_t N, const void* in, void* out, const double* dA, const double* dR, const PcArgs& pa,
+           bool accumulate, cudaStream_t s);
+void gm_dots(bool f32, int nv, int B, int64_t N, const void* V, int64_t vstride, const void* W, double2* out,
+             cudaStream_t s);
+void gm_lincomb(bool f32, int nv, int B, int64_t N, const void* V, int64_t vstride, const double2* coef, void* W,
+                bool assign, cudaStream_t s);
+void gm_colscale(bool f32, int B, int64_t N, const void* W, const double* sc, void* out, cudaStream_t s);
+void gm_sub(bool f32, int64_t n, const void* a, const void* b, void* out, cudaStream_t s);
+void gm_take(int64_t n, const int64_t* idx, const double* src, double* d, cudaStream_t s);
+
 bool fft_length_supported(int L);
 // bufB tensor map for the TMA z pass (out: 128-byte CUtensorMap); false if unavailable
 bool make_z_tensor_map(const HotDev& h, bool f32, void* out);

@@ -3,6 +3,7 @@
 // frequency binding, matvec / sweep entry points and introspection.
 #include <algorithm>
 #include <array>
+#include <complex>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -53,6 +54,11 @@ struct aimx_ctx {
   Profiler prof;
   std::vector<uint8_t> nz;      // exactly-nonzero projection weights [N_b][p3]
   bool from_cache = false;      // S0 static matrices read from an aimx_save_static file
+  // batched GMRES (aimx_solve): static self terms and lazily allocated workspace
+  double* dA = nullptr;         // L^A_s,NR[m,m]
+  double* dR = nullptr;         // y^rho_s,NR[m,m]
+  void* gm_ws = nullptr;
+  int64_t gm_ws_bytes = 0;
   // slab-decomposed FFT (aimx_setup_slab)
   bool slab = false;
   int world = 1, rank = 0;
@@ -390,6 +396,25 @@ void attach_z_map(aimx_ctx* c, HotDev& h) {
   }
 }
 
+// static self terms for the diagonal preconditioner
+void setup_self_terms(aimx_ctx* c) {
+  const Topology& t = c->topo;
+  std::vector<int64_t> di(t.nb);
+  for (int64_t m = 0; m < t.nb; ++m) {
+    di[m] = -1;
+    for (int64_t k = t.rowptr[m]; k < t.rowptr[m + 1]; ++k)
+      if (t.col[k] == m) di[m] = k;
+    if (di[m] < 0) throw Error(AIMX_E_INTERNAL, "near row without its diagonal");
+  }
+  int64_t* d_di = dupload(c, di);
+  c->dA = dalloc<double>(c, t.nb);
+  c->dR = dalloc<double>(c, t.nb);
+  gm_take(t.nb, d_di, c->sd.LA_NR, c->dA, c->stream);
+  gm_take(t.nb, d_di, c->sd.YR_NR, c->dR, c->stream);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  dfree(c, d_di, t.nb * (int64_t)sizeof(int64_t));
+}
+
 // batch slots from the full-grid per-frequency footprint (<= 1.5 GB of buffers)
 int choose_slots(aimx_ctx* c) {
   const Topology& t = c->topo;
@@ -481,6 +506,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     }
   }
   h.xt = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
+  setup_self_terms(c);
   finish_setup(c);
 }
 
@@ -853,6 +879,7 @@ void destroy_impl(aimx_ctx* c) {
   for (void* p : c->allocs) if (p) cudaFree(p);
   spectrum_plan_free(c->sp);
   if (c->stage) cudaFree(c->stage);
+  if (c->gm_ws) cudaFree(c->gm_ws);
   if (c->ev_spec) cudaEventDestroy(c->ev_spec);
   if (c->ev_use) cudaEventDestroy(c->ev_use);
   if (c->s2) {
@@ -1022,6 +1049,198 @@ aimx_status aimx_save_static(const aimx_ctx* cc, const char* path) {
   put(d.lam, nb * p3 * 4);
   ok = ok && std::fwrite(c->nz.data(), 1, c->nz.size(), fp) == c->nz.size();
   if (!ok) throw Error(AIMX_E_INVALID_ARG, std::string("write failed: ") + path);
+  AIMX_API_END(c)
+}
+
+// ---- batched GMRES (right-preconditioned, restarted)
+// One device batch of B frequencies iterates together; every column has its
+// own Arnoldi basis, Hessenberg matrix and Givens rotations (host, fp64).
+// Arnoldi: classical Gram-Schmidt applied twice (CGS2: two batched dot /
+// update sweeps per step instead of j dependent ones).
+static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, char* X, double tol, int m,
+                        int maxit, int32_t* iters, double* relres, cudaStream_t s) {
+  const bool f32 = c->prec == AIMX_C64;
+  const int64_t N = c->hot.nb;
+  const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
+  const int64_t blk = (int64_t)B * N;   // complex per [B][N] block
+  // workspace: V[m+1] blocks, W, U, R blocks; device scalars
+  const int64_t need = (int64_t)(m + 4) * blk * (int64_t)cs + (int64_t)(m + 2) * B * 16 * 2 + B * 8 * 2;
+  if (c->gm_ws_bytes < need) {
+    if (c->gm_ws) AIMX_CUDA(cudaFree(c->gm_ws));
+    c->gm_ws = nullptr;
+    AIMX_CUDA(cudaMalloc(&c->gm_ws, need));
+    c->gm_ws_bytes = need;
+  }
+  char* V = (char*)c->gm_ws;
+  char* W = V + (int64_t)(m + 1) * blk * cs;
+  char* U = W + blk * cs;
+  char* Rb = U + blk * cs;
+  double2* ddots = (double2*)(Rb + blk * cs);
+  double2* dcoef = ddots + (int64_t)(m + 2) * B;
+  double* dsc = (double*)(dcoef + (int64_t)(m + 2) * B);
+  std::vector<double2> hd((size_t)(m + 2) * B);
+  std::vector<double> hs(B);
+  spectra(c, B, f, s);
+  Combine cb = make_combine(B, f, 0, N);
+  PcArgs pa;
+  for (int b = 0; b < kMaxBatch; ++b) pa.alpha_im[b] = pa.beta[b] = 0.0;
+  for (int b = 0; b < B; ++b) {
+    pa.alpha_im[b] = cb.alpha_im[b];
+    pa.beta[b] = cb.beta[b];
+  }
+  auto matvec = [&](const void* in, void* out) {
+    if (f32) hot_matvec_f32(c->hot, in, out, nullptr, cb, s, &c->prof);
+    else hot_matvec_f64(c->hot, in, out, nullptr, cb, s, &c->prof);
+  };
+  auto norms = [&](const void* A, std::vector<double>& out) {   // ||A_b||
+    gm_dots(f32, 1, B, N, A, 0, A, ddots, s);
+    AIMX_CUDA(cudaMemcpyAsync(hd.data(), ddots, B * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    AIMX_CUDA(cudaStreamSynchronize(s));
+    out.resize(B);
+    for (int b = 0; b < B; ++b) out[b] = std::sqrt(std::max(0.0, hd[b].x));
+  };
+  auto colscale = [&](const void* A, const std::vector<double>& sc, void* out) {
+    AIMX_CUDA(cudaMemcpyAsync(dsc, sc.data(), B * sizeof(double), cudaMemcpyHostToDevice, s));
+    gm_colscale(f32, B, N, A, dsc, out, s);
+  };
+  using cd = std::complex<double>;
+  std::vector<double> bnorm, beta;
+  norms(RHS, bnorm);
+  AIMX_CUDA(cudaMemsetAsync(X, 0, blk * cs, s));
+  std::vector<int> it(B, 0), done(B, 0);
+  for (int b = 0; b < B; ++b)
+    if (bnorm[b] == 0.0) done[b] = 1;
+  AIMX_CUDA(cudaMemcpyAsync(Rb, RHS, blk * cs, cudaMemcpyDeviceToDevice, s));
+  int total = 0;
+  while (total < maxit) {
+    norms(Rb, beta);
+    bool all = true;
+    for (int b = 0; b < B; ++b) {
+      if (!done[b] && beta[b] <= tol * bnorm[b]) done[b] = 1;
+      all = all && done[b];
+    }
+    if (all) break;
+    std::vector<double> inv(B);
+    for (int b = 0; b < B; ++b) inv[b] = (done[b] || beta[b] == 0.0) ? 0.0 : 1.0 / beta[b];
+    colscale(Rb, inv, V);   // v_0
+    std::vector<std::vector<cd>> H(B, std::vector<cd>((size_t)(m + 1) * m, 0.0));
+    std::vector<std::vector<cd>> csn(B, std::vector<cd>(2 * m, 0.0)), g(B, std::vector<cd>(m + 1, 0.0));
+    std::vector<int> kb(B, 0), conv(B, 0);
+    for (int b = 0; b < B; ++b) g[b][0] = done[b] ? 0.0 : beta[b];
+    int j = 0;
+    for (; j < m && total < maxit; ++j, ++total) {
+      char* Vj = V + (int64_t)j * blk * cs;
+      gm_pc(f32, B, N, Vj, U, c->dA, c->dR, pa, false, s);
+      matvec(U, W);
+      // CGS2: h = V^H w ; w -= V h ; twice
+      for (int pass = 0; pass < 2; ++pass) {
+        gm_dots(f32, j + 1, B, N, V, blk, W, ddots, s);
+        AIMX_CUDA(cudaMemcpyAsync(hd.data(), ddots, (size_t)(j + 1) * B * sizeof(double2), cudaMemcpyDeviceToHost, s));
+        AIMX_CUDA(cudaStreamSynchronize(s));
+        for (int b = 0; b < B; ++b)
+          for (int i = 0; i <= j; ++i) H[b][(size_t)i * m + j] += cd(hd[(size_t)i * B + b].x, hd[(size_t)i * B + b].y);
+        gm_lincomb(f32, j + 1, B, N, V, blk, ddots, W, false, s);
+      }
+      std::vector<double> hn;
+      norms(W, hn);
+      std::vector<double> sc(B);
+      for (int b = 0; b < B; ++b) sc[b] = hn[b] > 0.0 ? 1.0 / hn[b] : 0.0;
+      colscale(W, sc, V + (int64_t)(j + 1) * blk * cs);
+      for (int b = 0; b < B; ++b) {
+        if (done[b] || conv[b]) continue;
+        cd* Hb = H[b].data();
+        Hb[(size_t)(j + 1) * m + j] = hn[b];
+        for (int i = 0; i < j; ++i) {   // previous rotations [[conj c, conj s], [-s, c]]
+          const cd ci = csn[b][2 * i], si = csn[b][2 * i + 1];
+          const cd t = std::conj(ci) * Hb[(size_t)i * m + j] + std::conj(si) * Hb[(size_t)(i + 1) * m + j];
+          Hb[(size_t)(i + 1) * m + j] = -si * Hb[(size_t)i * m + j] + ci * Hb[(size_t)(i + 1) * m + j];
+          Hb[(size_t)i * m + j] = t;
+        }
+        const cd a = Hb[(size_t)j * m + j], bb = Hb[(size_t)(j + 1) * m + j];
+        const double den = std::sqrt(std::norm(a) + std::norm(bb));
+        const cd cj = den != 0.0 ? a / den : cd(1.0), sj = den != 0.0 ? bb / den : cd(0.0);
+        csn[b][2 * j] = cj;
+        csn[b][2 * j + 1] = sj;
+        Hb[(size_t)j * m + j] = den;
+        Hb[(size_t)(j + 1) * m + j] = 0.0;
+        g[b][j + 1] = -sj * g[b][j];
+        g[b][j] = std::conj(cj) * g[b][j];
+        kb[b] = j + 1;
+        it[b] += 1;
+        if (std::abs(g[b][j + 1]) <= tol * bnorm[b]) conv[b] = 1;
+      }
+      bool cyc_done = true;
+      for (int b = 0; b < B; ++b) cyc_done = cyc_done && (done[b] || conv[b]);
+      if (cyc_done) {
+        ++total;
+        break;
+      }
+    }
+    // y = H^-1 g per column (back substitution), x += M^-1 V y
+    int kmax = 0;
+    for (int b = 0; b < B; ++b) kmax = std::max(kmax, done[b] ? 0 : kb[b]);
+    if (kmax > 0) {
+      std::vector<double2> coef((size_t)kmax * B, make_double2(0.0, 0.0));
+      for (int b = 0; b < B; ++b) {
+        if (done[b]) continue;
+        const int k = kb[b];
+        std::vector<cd> y(k);
+        for (int i = k - 1; i >= 0; --i) {
+          cd acc = g[b][i];
+          for (int l = i + 1; l < k; ++l) acc -= H[b][(size_t)i * m + l] * y[l];
+          y[i] = acc / H[b][(size_t)i * m + i];
+        }
+        for (int i = 0; i < k; ++i) coef[(size_t)i * B + b] = make_double2(y[i].real(), y[i].imag());
+      }
+      AIMX_CUDA(cudaMemcpyAsync(dcoef, coef.data(), coef.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+      gm_lincomb(f32, kmax, B, N, V, blk, dcoef, U, true, s);
+      gm_pc(f32, B, N, U, X, c->dA, c->dR, pa, true, s);
+    }
+    // true residual for the restart / the convergence test
+    matvec(X, W);
+    gm_sub(f32, blk, RHS, W, Rb, s);
+  }
+  std::vector<double> rn;
+  norms(Rb, rn);
+  for (int b = 0; b < B; ++b) {
+    if (iters) iters[b] = it[b];
+    if (relres) relres[b] = bnorm[b] > 0.0 ? rn[b] / bnorm[b] : 0.0;
+  }
+}
+
+static int sweep_batch(const aimx_ctx* c, int32_t batch, int64_t nf);
+
+aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* RHS, void* X, double tol,
+                       int32_t restart, int32_t maxiter, int32_t* iters, double* relres, void* stream) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (nf < 0 || (nf > 0 && (!f_hz || !RHS || !X)) || !(tol > 0.0) || restart < 1 || maxiter < 1)
+    throw Error(AIMX_E_INVALID_ARG, "bad solve arguments");
+  if (RHS == X) throw Error(AIMX_E_INVALID_ARG, "input and output alias");
+  if (c->slab || !c->dA) throw Error(AIMX_E_UNSUPPORTED, "aimx_solve needs a one-GPU context");
+  for (int64_t i = 0; i < nf; ++i)
+    if (!(f_hz[i] > 0.0) || !std::isfinite(f_hz[i])) throw Error(AIMX_E_INVALID_ARG, "bad frequency");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  cudaStream_t s = pick(c, stream);
+  if (s != c->stream) {
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
+  }
+  const bool had = c->freq_set;
+  const double f0 = c->f;
+  const int B = sweep_batch(c, 0, nf);
+  const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
+  for (int64_t i = 0; i < nf; i += B) {
+    const int nb_ = (int)std::min<int64_t>(B, nf - i);
+    solve_batch(c, nb_, f_hz + i, (const char*)RHS + i * vb, (char*)X + i * vb, tol, restart, maxiter,
+                iters ? iters + i : nullptr, relres ? relres + i : nullptr, s);
+  }
+  if (had) bind_frequency(c, f0, s);
+  else c->freq_set = false;
+  AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
+  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
   AIMX_API_END(c)
 }
 
