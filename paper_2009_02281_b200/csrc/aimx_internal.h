@@ -238,7 +238,6 @@ struct HotDev {
   int32_t* phi_line = nullptr;   // [nlines] phi line (y + Ny z) of each x-inverse line; null: line_id
   const void* tmB = nullptr;     // HOST pointer to the CUtensorMap of bufB (k_zconv_tma), or null
   int G = 8;                     // lanes per node in the projection gather
-  int twy = 4, twz = 4;          // tile widths (complex elements) of the y / z passes
   int64_t nnz = 0;
   int batch = 0;                 // batch slots allocated
   // per-batch-slot strides (complex elements)
@@ -322,7 +321,6 @@ void gm_take(int64_t n, const int64_t* idx, const double* src, double* d, cudaSt
 bool fft_length_supported(int L);
 // bufB tensor map for the TMA z pass (out: 128-byte CUtensorMap); false if unavailable
 bool make_z_tensor_map(const HotDev& h, bool f32, void* out);
-int pick_tile(int L, int rowwidth, bool f32);
 void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof);
 // xt <- the batch-interleaved columns of x (Combine: B, xstride)

@@ -1,10 +1,7 @@
-// Shared-memory Stockham FFT engine for the AIMx grid passes (sm_100a).
-//
-// A CTA transforms `nlines` lines of power-of-two length L held in shared
-// memory (ping-pong buffers), radix 8 -> 4 -> 2 stages, twiddle table
-// tw[m] = exp(-2 pi i m / L) in shared memory.  Line element (line, idx) is at
-// addr(line, idx); consecutive threads take consecutive lines so that the
-// column layout idx * TW + line is bank-conflict free on the loads.
+// Complex arithmetic and small DFT kernels for the AIMx grid passes (sm_100a):
+// packed fp32 pair instructions (FADD2 / FMUL2 / FFMA2), radix-2/4/8
+// butterflies in registers, cp.async helpers, PDL hooks.  The two-level
+// register FFT engine built on them is fft_reg.cuh.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -161,70 +158,8 @@ template <typename T2, int R, bool INV> __device__ __forceinline__ void dft(T2* 
   else dft8<T2, INV>(v);
 }
 
-// Column layout: element (line, idx) at idx * tw + line (tw = lines per tile).
-struct ColAddr {
-  int tw;
-  __device__ __forceinline__ int operator()(int line, int idx) const { return idx * tw + line; }
-};
-// Row layout, 4 channels innermost, rows padded by one node (bank spread).
-template <int L> struct RowAddr {
-  __device__ __forceinline__ int operator()(int line, int idx) const {
-    return (line >> 2) * ((L + 1) * 4) + idx * 4 + (line & 3);
-  }
-};
-
-// One Stockham stage src -> dst (Govindaraju et al. formulation):
-//   j in [0, L/R), k = j mod NS, v_r = src[j + r L/R] * w^(r k), w = e^{-+2 pi i/(NS R)},
-//   V = DFT_R(v), dst[(j - k) R + k + q NS] = V_q.
-template <typename T2, int L, int R, int NS, bool INV, class Addr>
-__device__ __forceinline__ void fft_stage(const T2* __restrict__ src, T2* __restrict__ dst, int nlines,
-                                          const T2* __restrict__ tw, Addr addr) {
-  constexpr int NB = L / R;
-  const int total = nlines * NB;
-  for (int t = threadIdx.x; t < total; t += blockDim.x) {
-    const int line = t % nlines;
-    const int j = t / nlines;
-    const int k = j % NS;
-    T2 v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = src[addr(line, j + r * NB)];
-    if (NS > 1) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        T2 w = tw[(r * k * (L / (NS * R))) & (L - 1)];
-        if (INV) w.y = -w.y;
-        v[r] = cmul(v[r], w);
-      }
-    }
-    dft<T2, R, INV>(v);
-    const int base = (j - k) * R + k;
-#pragma unroll
-    for (int r = 0; r < R; ++r) dst[addr(line, base + r * NS)] = v[r];
-  }
-}
-
-template <typename T2, int L, bool INV, int NS, class Addr>
-__device__ __forceinline__ void fft_stages(T2*& src, T2*& dst, int nlines, const T2* tw, Addr addr) {
-  if constexpr (NS < L) {
-    constexpr int REM = L / NS;
-    constexpr int R = (REM % 8 == 0) ? 8 : ((REM % 4 == 0) ? 4 : 2);
-    fft_stage<T2, L, R, NS, INV>(src, dst, nlines, tw, addr);
-    __syncthreads();
-    T2* t = src;
-    src = dst;
-    dst = t;
-    fft_stages<T2, L, INV, NS * R>(src, dst, nlines, tw, addr);
-  }
-}
-
-// In-place-by-swap FFT of `nlines` lines: the result ends in `src`.
-template <typename T2, int L, bool INV, class Addr>
-__device__ __forceinline__ void smem_fft(T2*& src, T2*& dst, int nlines, const T2* tw, Addr addr) {
-  fft_stages<T2, L, INV, 1>(src, dst, nlines, tw, addr);
-}
-
 // Asynchronous global -> shared element copy (LDGSTS), many in flight per
-// thread without register staging; complete with cp_async_wait_all().
+// thread without register staging; complete with cp.async.commit_group + wait_group.
 template <typename T2>
 __device__ __forceinline__ void cp_async(T2* sdst, const T2* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
@@ -233,10 +168,6 @@ __device__ __forceinline__ void cp_async(T2* sdst, const T2* gsrc) {
   } else {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
   }
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 template <typename T2>

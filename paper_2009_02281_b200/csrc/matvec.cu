@@ -1,20 +1,25 @@
 // The AIMx hot path on the B200 (S2-S5), batched over B frequency points:
 //
-//   k_gather      S2: projection P x as a gather over the transposed
-//                 (node-major) stencil CSR -- a group of G lanes per occupied
+//   k_interleave  the B right-hand sides batch-interleaved: xt[n][b]
+//   k_gather(_b)  S2: projection P x as a gather over the transposed
+//                 (node-major) stencil CSR -- a warp or lane group per occupied
 //                 grid node, fixed-order shuffle reduction, no atomics -- into
 //                 dense occupied x-lines S[line][x][4]
 //   k_xfwd        zero-padded forward FFT along x of the occupied lines
+//   k_yzconv      (short y and z) y fwd, z fwd * H_hat * z inv, y inv in one
+//                 kernel over shared-memory column tiles; otherwise:
 //   k_yfwd        forward FFT along y (input rows y < N_y, zero padded)
-//   k_zconv       forward FFT along z, times the spectrum H_hat (octant,
-//                 already scaled by 1/M), inverse FFT along z, cropped to z < N_z
+//   k_zconv(_tma) forward FFT along z, times the spectrum H_hat (octant,
+//                 already scaled by 1/M), inverse FFT along z, cropped to
+//                 z < N_z (TMA tensor copies when every z plane is occupied)
 //   k_yinv        inverse FFT along y, cropped to y < N_y (occupied lines only)
 //   k_xinv        inverse FFT along x, cropped to x < N_x -> potentials phi
-//   k_interp_near S4 + S5: warp per RWG (testing function): interpolation
-//                 W = P^T of the 4 potentials on its (n+1)^3 stencil, plus the
-//                 near-region row of C = L_s,NR - L_s,P (read once for all B
-//                 right-hand sides), plus the EFIE combine
+//   k_interp_near S4 + S5 on row groups (NearGroups): interpolation W = P^T of
+//                 the 4 potentials and the near correction C = L_s,NR - L_s,P,
+//                 coefficient stream by TMA bulk copies, then the EFIE combine
 //                 y = -j w mu0 (y^A - k0^-2 y^rho).
+// Every kernel is launched with programmatic dependent launch (fft.cuh).
+// The slab-decomposed variant (slab_matvec) runs the same kernels per rank.
 //
 // P:198-200 (W H P, "accelerated with FFTs", applied on the entire grid);
 // eq:LAIMx P:283; eq:EFIEAIMx P:288.  Grid data are complex, 4 channels
@@ -1259,17 +1264,6 @@ bool make_z_tensor_map(const HotDev& h, bool f32, void* out) {
 
 bool fft_length_supported(int L) { return L >= 8 && L <= 1024 && (L & (L - 1)) == 0; }
 
-// Tile width (complex elements per row segment) of the strided y / z passes:
-// about 4096 (fp32) / 2048 (fp64) elements per CTA, at least one 32-byte
-// sector per row, at most the row width 8 N_x.
-int pick_tile(int L, int rowwidth, bool f32) {
-  int t = (f32 ? 4096 : 2048) / L;
-  const int lo = f32 ? 4 : 2;
-  if (t < lo) t = lo;
-  if (t > 512) t = 512;
-  if (t > rowwidth) t = rowwidth;
-  return t;
-}
 
 void interleave_f32(const HotDev& h, const void* x, const Combine& c, cudaStream_t s) {
   run_interleave<float>(h, x, c, s);

@@ -8,13 +8,14 @@
 // and 0 on the wrap slot o = N_a.  K is even along every axis, so its 2N-point
 // DFT is even as well and only the octant k in [0, N]^3 is kept.  Each axis is
 // transformed by loading the N+1 octant samples of a line, rebuilding its even
-// extension v[2N - i] = v[i] in shared memory and running the same Stockham
-// FFT as the hot path (an exact DCT-I via FFT, O(N log N) per line, HBM-bound:
-// one read + one write of the octant per axis).  The static spectrum is built
-// once in fp64; per frequency the dynamic samples are computed in fp64 with the
-// cancellation-free half-angle form (reading R11), rounded to the compute
-// precision, transformed, added to H_hat_s and scaled by 1/M (the inverse-FFT
-// normalisation is folded into the spectrum).  B frequencies per launch.
+// extension v[2N - i] = v[i] and running the hot path's register FFT engine
+// (an exact DCT-I via FFT, O(N log N) per line).  The static spectrum is built
+// once in fp64.  Per frequency the dynamic samples are generated inside the x
+// pass, once per octant point (the cancellation-free half-angle form, reading
+// R11; fp64, or an fp64-reduced phase with fp32 sin/cos for c64), the z and y
+// passes follow (fused into one kernel for short z / y), and the last one adds
+// H_hat_s and scales by 1/M (the inverse-FFT normalisation is folded into the
+// spectrum).  B frequencies per launch.
 // Octant layout ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.
 #include <cmath>
 #include <vector>
@@ -27,51 +28,25 @@ namespace aimx {
 
 namespace {
 
-struct K0s { double v[kMaxBatch]; };
 
-// sample[b][(j (Nz+1) + l)(Nx+1) + i] = K(h sqrt(i^2 + j^2 + l^2)), 0 on wrap slots.
-// fp64 (T = double, and the static kernel): K_d with the cancellation-free
-// half-angle form (reading R11).  fp32 results (T = float): the phase
-// k0 r / 2 is formed and reduced modulo 2 pi in fp64, then sin / cos of the
-// reduced angle in fp32 -- the sample is rounded to fp32 either way.
-template <typename T, bool STATIC>
-__global__ void k_sample(int Nx, int Ny, int Nz, int64_t noct, double h, K0s k0s,
-                         typename CT<T>::T2* __restrict__ out) {
+// Static samples: sample[(j (Nz+1) + l)(Nx+1) + i] = K_s(h sqrt(i^2 + j^2 + l^2)),
+// K_s = 1/(4 pi r) (eq:hgfs P:227), K_s(0) = 0 (eq:Hsmm P:321), 0 on wrap
+// slots; fp64.  (The dynamic samples are generated inside the x pass, ksample.)
+__global__ void k_sample_static(int Nx, int Ny, int Nz, int64_t noct, double h, double2* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  using T2 = typename CT<T>::T2;
-  const int b = blockIdx.y;
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= noct) return;
-  const double k0 = k0s.v[b];
   int i = (int)(idx % (Nx + 1));
   int64_t r2 = idx / (Nx + 1);
   int l = (int)(r2 % (Nz + 1));
   int j = (int)(r2 / (Nz + 1));
-  T2 res = mk<T2>(0, 0);
+  double re = 0.0;
   if (i < Nx && j < Ny && l < Nz) {
     int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
-    const double inv4pi = 1.0 / (4.0 * kPi);
-    if (STATIC) {
-      if (q > 0) res = mk<T2>((T)(inv4pi / (h * sqrt((double)q))), (T)0);
-    } else if (q == 0) {
-      res = mk<T2>((T)0, (T)(-k0 * inv4pi));
-    } else if (sizeof(T) == 8) {
-      double r = h * sqrt((double)q);
-      double s, c;
-      sincos(0.5 * k0 * r, &s, &c);
-      res = mk<T2>((T)(-2.0 * s * s * inv4pi / r), (T)(-2.0 * s * c * inv4pi / r));   // sin x = 2 sin(x/2) cos(x/2)
-    } else {
-      const double r = h * sqrt((double)q);
-      const double u = (0.25 / kPi) * (k0 * r);         // (k0 r / 2) / (2 pi)
-      const float red = (float)(u - rint(u));           // in [-1/2, 1/2] turns
-      float s, c;
-      sincospif(2.0f * red, &s, &c);
-      const float a = (float)inv4pi / (float)r;
-      res = mk<T2>((T)(-2.0f * s * s * a), (T)(-2.0f * s * c * a));
-    }
+    if (q > 0) re = 1.0 / (4.0 * kPi) / (h * sqrt((double)q));
   }
-  out[(int64_t)b * noct + idx] = res;
+  out[idx] = make_double2(re, 0.0);
 }
 
 // Even-extension transform of lines of N1 = L/2 + 1 octant samples with the
@@ -402,9 +377,8 @@ void spectrum_plan_free(SpectrumPlan& sp) {
 }
 
 void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s) {
-  K0s k{};
-  launch_pdl(k_sample<double, true>, dim3((unsigned)((sp.noct + 255) / 256), 1), dim3(256), 0, s, 
-      sp.Nx, sp.Ny, sp.Nz, sp.noct, sp.h, k, (double2*)sp.work0);
+  launch_pdl(k_sample_static, dim3((unsigned)((sp.noct + 255) / 256)), dim3(256), 0, s, sp.Nx, sp.Ny, sp.Nz,
+             sp.noct, sp.h, (double2*)sp.work0);
   AIMX_CHECK_LAUNCH();
   dct3<double>(sp, 1, sp.tw64, sp.work0, sp.work1, out, nullptr, 1.0, s);
 }
