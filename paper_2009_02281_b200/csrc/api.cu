@@ -326,7 +326,7 @@ void build_gather(aimx_ctx* c, HotDev& h, const NodeMap& m) {
   dfree(c, ent_slot, nent * (int64_t)sizeof(int32_t));
   const double avg = h.nocc > 0 ? (double)nent / h.nocc : 1.0;
   int G = 4;
-  while (G < 32 && G < avg) G *= 2;
+  while (G < 32 && 2 * G < avg) G *= 2;   // about two entries per lane: the shuffle reduction stays a small share
   h.G = G;
 }
 
