@@ -22,7 +22,12 @@ label) step by step:
 * ``convolution``   3-level Toeplitz H(k0) applied by zero-padded FFT
                     (eq:Hmn P:305, eq:Hmm P:335)
 * ``aimx``          the AIMx EFIE matvec (eq:LAIMx P:283, eq:EFIEAIMx P:288)
-* ``direct``        dense direct-integration MoM (the paper's "direct" mode)
+* ``direct``        dense direct-integration MoM (the paper's "direct" mode),
+                    optionally with k0^2 G_lin integrated analytically
+* ``linear_term``   the linear-term modification: G_lin = -r/(8 pi),
+                    C_lin = L_lin - W H_lin P on overlapping pairs
+                    (eq:linterm P:363, eq:Lmatdecomplin P:386)
+* ``gmres``         restarted GMRES with the static diagonal preconditioner
 
 Every reading of a silent/ambiguous/garbled passage is listed in DESIGN.md
 ("Readings") with the AMB-n tag used in comments here.

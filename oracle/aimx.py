@@ -14,6 +14,8 @@ Step by step:
   S4  y^A = sum_{c=x,y,z} P_c^T phi_c ;  y^rho = P_rho^T phi_rho     (W = P^T)
   S5  y^A += C_A x ; y^rho += C_rho x ; Z x = -j w mu0 (y^A - k0^-2 y^rho)
 Parts: L_A x = y^A, L_phi x = -y^rho (AMB-13).
+Optional (set_linear_term): y^A += k0^2 C^A_lin x, y^rho +=
+k0^2 C^rho_lin x on overlapping pairs (linear_term).
 """
 from __future__ import annotations
 
@@ -55,6 +57,20 @@ class AIMxOracle:
         if static:
             self.build_static()
         self.k0 = None
+        self.lin = False
+        self.CAl_mat = self.CRl_mat = None
+
+    def set_linear_term(self, on: bool = True):
+        """treat k0^2 G_lin separately on overlapping pairs."""
+        from .linear_term import lin_correction
+        self.lin = bool(on)
+        if self.lin and self.CAl_mat is None:
+            rp, cl, ca, cr, _, _ = lin_correction(self.V, self.T, self.rwg, self.Lam, self.A, self.order,
+                                                  self.grid.h)
+            shape = (self.N, self.N)
+            self.lin_rowptr, self.lin_col, self.CAl, self.CRl = rp, cl, ca, cr
+            self.CAl_mat = sp.csr_matrix((ca, cl, rp), shape=shape)
+            self.CRl_mat = sp.csr_matrix((cr, cl, rp), shape=shape)
 
     @property
     def N(self) -> int:
@@ -115,7 +131,13 @@ class AIMxOracle:
         """(y^A, y^rho): L_A x = y^A, L_phi x = -y^rho."""
         x = np.asarray(x, np.complex128)
         yA, yR = self.grid_parts(x)
-        return yA + self.CA_mat @ x, yR + self.CR_mat @ x
+        yA = yA + self.CA_mat @ x
+        yR = yR + self.CR_mat @ x
+        if self.lin:
+            k2 = self.k0 * self.k0
+            yA = yA + k2 * (self.CAl_mat @ x)
+            yR = yR + k2 * (self.CRl_mat @ x)
+        return yA, yR
 
     def combine(self, yA, yR):
         return -1j * self.omega * MU0 * (yA - yR / (self.k0 * self.k0))
@@ -132,6 +154,10 @@ class AIMxOracle:
         for m, (cols, ca, cr) in zip(rows, self.static_rows(rows)):
             a = yA[m] + ca @ x[cols]
             r = yR[m] + cr @ x[cols]
+            if self.lin:
+                k2 = self.k0 * self.k0
+                a += k2 * (self.CAl_mat.getrow(m) @ x)[0]
+                r += k2 * (self.CRl_mat.getrow(m) @ x)[0]
             res.append((a, r))
         a = np.array([t[0] for t in res])
         r = np.array([t[1] for t in res])

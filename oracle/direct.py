@@ -11,6 +11,12 @@ with G = G_s + G_d (eq:hgfdecomp0 P:222): the singular static part uses the
 same analytic-inner recipe as static_near (every pair, symmetrised); the
 bounded dynamic part G_d (continuous, G_d(0) = -j k0/(4 pi)) uses the
 7 x 7 product rule.  Small meshes only (dense N x N).
+
+lin_split=True: G_d is split further into k0^2 G_lin (eq:linterm,
+non-smooth at r = 0; analytic inner integrals on every pair, linear_term) and
+the remainder G_d - k0^2 G_lin (its first non-smooth term is O(k0^4 r^3)),
+which keeps the 7 x 7 rule.  This is the tighter reference the modification's
+error is measured against (fig:selferrors P:643-646).
 """
 from __future__ import annotations
 
@@ -18,6 +24,7 @@ import numpy as np
 
 from .kernels import G_d, MU0
 from .mesh import RWG
+from .linear_term import G_lin, lin_dense
 from .static_near import RADON7_BARY, RADON7_W, static_pair_entries
 
 
@@ -43,12 +50,14 @@ def static_dense(V, T, rwg: RWG):
     return 0.5 * (LA + LA.T), 0.5 * (YR + YR.T)
 
 
-def dynamic_dense(V, T, rwg: RWG, k0: float):
+def dynamic_dense(V, T, rwg: RWG, k0: float, minus_lin: bool = False):
     pts, w, f, div = _points(V, T, rwg)
     N = rwg.n
     P = pts.reshape(-1, 3)
     R = np.linalg.norm(P[:, None, :] - P[None, :, :], axis=-1)
     Gd = G_d(k0, R)
+    if minus_lin:
+        Gd = Gd - k0 * k0 * G_lin(R)
     M = P.shape[0]
     owner = np.repeat(np.arange(N), 14)
     LA = np.zeros((N, N), dtype=np.complex128)
@@ -63,17 +72,24 @@ def dynamic_dense(V, T, rwg: RWG, k0: float):
 
 
 class DirectEFIE:
-    def __init__(self, V, T, rwg: RWG):
+    def __init__(self, V, T, rwg: RWG, lin_split: bool = False):
         self.V = np.asarray(V, np.float64)
         self.T = np.asarray(T, np.int64)
         self.rwg = rwg
+        self.lin_split = lin_split
         self.LA_s, self.YR_s = static_dense(self.V, self.T, rwg)
+        if lin_split:
+            self.LA_lin, self.YR_lin = lin_dense(self.V, self.T, rwg)
 
     def set_frequency(self, f_hz: float):
         from .kernels import wavenumber
         self.k0 = wavenumber(f_hz)
         self.omega = 2.0 * np.pi * f_hz
-        LAd, YRd = dynamic_dense(self.V, self.T, self.rwg, self.k0)
+        LAd, YRd = dynamic_dense(self.V, self.T, self.rwg, self.k0, minus_lin=self.lin_split)
         self.LA = self.LA_s + LAd
         self.YR = self.YR_s + YRd
+        if self.lin_split:
+            k2 = self.k0 * self.k0
+            self.LA = self.LA + k2 * self.LA_lin
+            self.YR = self.YR + k2 * self.YR_lin
         self.Z = -1j * self.omega * MU0 * (self.LA - self.YR / self.k0 ** 2)
