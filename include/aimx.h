@@ -142,6 +142,21 @@ aimx_status aimx_setup_cached(const aimx_mesh_desc* mesh, const aimx_grid_desc* 
  * frequencies).  Idempotent.  f must be finite and > 0 (k0 = 0 rejected). */
 aimx_status aimx_set_frequency(aimx_ctx* ctx, double f_hz);
 
+/* Linear-term accuracy modification (sec:methods:aimx:acc P:361-398):
+ * k0^2 G_lin, G_lin(r) = -r/(8 pi) (eq:linterm P:365), is integrated directly
+ * on the pairs whose supports share a triangle (at most 5 per row, "O(N)"
+ * P:396) and applied on the fly scaled by k0^2 (eq:Lmatdecomplin P:388):
+ *   y^A   += k0^2 C^A_lin x,   C^A_lin   = L^A_lin   - sum_c W^c H_lin P^c,
+ *   y^rho += k0^2 C^rho_lin x, C^rho_lin = y^rho_lin - W^rho H_lin P^rho,
+ * with H_lin(delta) = G_lin(h |delta|) (the grid operator itself is unchanged:
+ * its samples already contain k0^2 G_lin).  enable != 0 turns it on for every
+ * later matvec, sweep and solve of the context (the first call builds C_lin on
+ * the device, fp64, stored in `prec`; synchronises the context stream);
+ * enable == 0 turns it off.  Off by default (the paper's results do not use it,
+ * P:648).  aimx_get_linear_term reports the current state. */
+aimx_status aimx_set_linear_term(aimx_ctx* ctx, int enable);
+aimx_status aimx_get_linear_term(const aimx_ctx* ctx, int* enabled);
+
 /* S2-S5: y = Z(k0) x = -j w mu0 (y^A - k0^-2 y^rho) (eq:EFIEAIMx P:288), where
  * y^A = W^(A) H P^(A) x + C_A x and y^rho = W^(phi) H P^(phi) x + C_rho x.
  * x, y: device vectors of N_b complex numbers (see conventions). */
@@ -204,6 +219,11 @@ aimx_status aimx_get_near_csr(const aimx_ctx* ctx, int64_t* rowptr, int32_t* col
  * optional: the four constituent matrices (any pointer may be NULL). */
 aimx_status aimx_get_static(const aimx_ctx* ctx, double* CA, double* Crho,
                             double* LA_NR, double* Yrho_NR, double* LA_P, double* Yrho_P);
+/* Linear-term modification (aimx_set_linear_term; AIMX_E_STATE before its
+ * first enable): cols[N_b][5] overlapping columns (ascending, -1 padded) and
+ * C^A_lin, C^rho_lin [N_b][5] as stored (compute precision, widened to fp64).
+ * Any pointer may be NULL. */
+aimx_status aimx_get_linear_entries(const aimx_ctx* ctx, int32_t* cols, double* CA_lin, double* Crho_lin);
 /* Projection weights (fp64) lam[N_b][4][(n+1)^3], channels (x, y, z, rho),
  * node s = i + (n+1)(j + (n+1) k). */
 aimx_status aimx_get_weights(const aimx_ctx* ctx, double* lam);

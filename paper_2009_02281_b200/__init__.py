@@ -57,6 +57,8 @@ _P = C.c_void_p
 ABI_FUNCTIONS = {
     "aimx_setup": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Grid), C.c_int, C.c_int, _P, C.POINTER(_P)]),
     "aimx_set_frequency": (C.c_int, [_P, C.c_double]),
+    "aimx_set_linear_term": (C.c_int, [_P, C.c_int]),
+    "aimx_get_linear_term": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec_parts": (C.c_int, [_P, _P, _P, _P, _P]),
     "aimx_sweep": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_int32, _P]),
@@ -67,6 +69,7 @@ ABI_FUNCTIONS = {
     "aimx_get_anchors": (C.c_int, [_P, _P]),
     "aimx_get_near_csr": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int64)]),
     "aimx_get_static": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "aimx_get_linear_entries": (C.c_int, [_P, _P, _P, _P]),
     "aimx_get_weights": (C.c_int, [_P, _P]),
     "aimx_get_spectrum": (C.c_int, [_P, C.c_int, _P]),
     "aimx_profile_enable": (C.c_int, [_P, C.c_int]),
@@ -224,6 +227,17 @@ class AIMx:
         _check(self.lib, self.lib.aimx_set_frequency(self.ctx, float(f_hz)), self.ctx)
         self.freq = float(f_hz)
 
+    def set_linear_term(self, on: bool = True):
+        """Linear-term accuracy modification: k0^2 G_lin integrated
+        directly on overlapping pairs for every later matvec / sweep / solve."""
+        _check(self.lib, self.lib.aimx_set_linear_term(self.ctx, int(bool(on))), self.ctx)
+
+    @property
+    def linear_term(self) -> bool:
+        v = C.c_int()
+        _check(self.lib, self.lib.aimx_get_linear_term(self.ctx, C.byref(v)), self.ctx)
+        return bool(v.value)
+
     def matvec(self, x, y=None, stream=None):
         torch = _torch()
         if y is None:
@@ -344,6 +358,15 @@ class AIMx:
         out = [np.empty(nnz.value) for _ in range(6)]
         _check(self.lib, self.lib.aimx_get_static(self.ctx, *[_P(a.ctypes.data) for a in out]), self.ctx)
         return dict(zip(["CA", "CR", "LA_NR", "YR_NR", "LA_P", "YR_P"], out))
+
+    def linear_entries(self):
+        """(cols [N][5], C^A_lin [N][5], C^rho_lin [N][5]) of the linear-term modification."""
+        cols = np.empty((self.N, 5), np.int32)
+        ca = np.empty((self.N, 5))
+        cr = np.empty((self.N, 5))
+        _check(self.lib, self.lib.aimx_get_linear_entries(self.ctx, _P(cols.ctypes.data), _P(ca.ctypes.data),
+                                                          _P(cr.ctypes.data)), self.ctx)
+        return cols, ca, cr
 
     def weights(self):
         st = self.stats()

@@ -163,6 +163,19 @@ void launch_weights(const Topology& t, SetupDev& d, cudaStream_t s, uint8_t* nzf
 void launch_static_near(const Topology& t, SetupDev& d, cudaStream_t s);
 void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 
+// ---------------------------------------------------------------- linear-term modification
+// P:382-398 (sec:methods:aimx:acc): k0^2 G_lin, G_lin = -r/(8 pi) (eq:linterm
+// P:365), by direct integration on overlapping pairs only (supports share a
+// triangle, reading R21): at most kLinW columns per row.
+constexpr int kLinW = 5;
+// cols: [nb][kLinW] overlapping columns, ascending, -1 padded
+void build_overlap(const Topology& t, std::vector<int32_t>& cols);
+// C_lin = (L^A_lin - sum_c W^c H_lin P^c, y^rho_lin - W^rho H_lin P^rho) on the
+// pairs of `cols` (device, [nb][kLinW]), symmetrised entries, written as
+// real pairs in the compute precision (f32: float2, else double2) to out.
+void launch_lin_entries(const Topology& t, const SetupDev& d, const int32_t* cols, bool f32, void* out,
+                        cudaStream_t s);
+
 // ---------------------------------------------------------------- batching
 constexpr int kMaxBatch = 32;
 
@@ -275,6 +288,9 @@ struct HotDev {
   void* twz_tab = nullptr;
   void* Hoct = nullptr;          // [batch][noct] bound spectra / M (compute precision)
   void* xt = nullptr;            // [nb][16] batch-interleaved right-hand sides (near SpMM)
+  // linear-term modification; null lin_col = off
+  int32_t* lin_col = nullptr;    // [nb][kLinW] overlapping columns of the rows this HotDev tests, -1 padded
+  void* lin_c = nullptr;         // [nb][kLinW] (C^A_lin, C^rho_lin) real pairs, compute precision
 };
 
 // ---------------------------------------------------------------- slab-decomposed FFT
@@ -289,6 +305,8 @@ struct SlabRank {
   HotDev hr;                     // gather + x fwd on own rows (bufA: [Nz][y1-y0][2Nx][4]); S4+S5 of owned RWGs
   HotDev hc;                     // y fwd / z conv / y inv on the kx slab ([Nz][Ny or 2Ny][4 (kx1-kx0)])
   HotDev hx;                     // x inv of rows [y0, yh1) (bufC: [Nz][yh1-y0][2Nx][4]) -> phi
+  std::vector<int32_t> owned;    // RWGs whose S4+S5 rows this rank computes
+  int32_t* lin_col = nullptr;    // kLinW columns of the owned rows (others -1), when built
   void* send = nullptr;          // exchange staging (both exchanges share it)
   void* recv = nullptr;
 };

@@ -68,6 +68,10 @@ struct aimx_ctx {
   void* comm = nullptr;                    // ncclComm_t
   int slots = 0;
   void* Hoct = nullptr;         // bound spectra [slots][noct], compute precision, scaled 1/M
+  // linear-term modification (aimx_set_linear_term), built on first use
+  int32_t* lin_col = nullptr;   // [nb][kLinW] overlapping columns
+  void* lin_c = nullptr;        // [nb][kLinW] (C^A_lin, C^rho_lin), compute precision
+  bool lin_on = false;
   std::vector<void*> allocs;
   std::vector<std::unique_ptr<CUtensorMap>> tmaps;   // tensor maps referenced by HotDev::tmB
   std::string last_error;
@@ -694,7 +698,7 @@ void do_setup_slab(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc
     NodeMap m;
     nodemap_rows(t, full, R.y0, R.y1, m);
     build_gather(c, hr, m);
-    std::vector<int32_t> owned;
+    std::vector<int32_t>& owned = R.owned;
     for (int64_t e = 0; e < t.nb; ++e)
       if (t.anchor[3 * e + 1] >= R.y0 && t.anchor[3 * e + 1] < R.y1) owned.push_back((int32_t)e);
     if (!owned.empty()) build_near(c, hr, owned);
@@ -1268,6 +1272,58 @@ aimx_status aimx_set_frequency(aimx_ctx* c, double f_hz) {
   AIMX_API_END(c)
 }
 
+// C_lin on the overlapping pairs, once per context; the per-RWG
+// geometry records are rebuilt first when the static matrices came from a cache.
+static void build_linear(aimx_ctx* c) {
+  const Topology& t = c->topo;
+  SetupDev& d = c->sd;
+  if (!d.side) {
+    d.V = dupload(c, t.V);
+    d.T = dupload(c, t.T);
+    d.ea = dupload(c, t.ea); d.eb = dupload(c, t.eb);
+    d.tp = dupload(c, t.tp); d.tm = dupload(c, t.tm);
+    d.pp = dupload(c, t.pp); d.pm = dupload(c, t.pm);
+    d.side = dalloc<double>(c, 2 * t.nb * kSideStride);
+    launch_rwg_sides(t, d, c->stream);
+  }
+  std::vector<int32_t> cols;
+  build_overlap(t, cols);
+  c->lin_col = dupload(c, cols);
+  const bool f32 = c->prec == AIMX_C64;
+  c->lin_c = dalloc<char>(c, t.nb * kLinW * (int64_t)(f32 ? sizeof(float2) : sizeof(double2)));
+  launch_lin_entries(t, d, c->lin_col, f32, c->lin_c, c->stream);
+  for (SlabRank& r : c->slabs) {   // each rank applies the rows it tests
+    std::vector<int32_t> own((size_t)t.nb * kLinW, -1);
+    for (int32_t e : r.owned) std::copy(cols.begin() + (int64_t)e * kLinW, cols.begin() + (int64_t)(e + 1) * kLinW,
+                                        own.begin() + (int64_t)e * kLinW);
+    r.lin_col = dupload(c, own);
+  }
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+aimx_status aimx_set_linear_term(aimx_ctx* c, int enable) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  if (enable && !c->lin_col) build_linear(c);
+  c->lin_on = enable != 0;
+  c->hot.lin_col = c->lin_on ? c->lin_col : nullptr;
+  c->hot.lin_c = c->lin_c;
+  for (SlabRank& r : c->slabs) {
+    r.hr.lin_col = c->lin_on && !r.owned.empty() ? r.lin_col : nullptr;
+    r.hr.lin_c = c->lin_c;
+  }
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_get_linear_term(const aimx_ctx* c, int* enabled) {
+  if (!c || !enabled) return AIMX_E_INVALID_ARG;
+  *enabled = c->lin_on ? 1 : 0;
+  return AIMX_OK;
+}
+
 static aimx_status matvec_common(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, void* stream) {
   if (!c) return AIMX_E_INVALID_ARG;
   AIMX_API_BEGIN
@@ -1516,6 +1572,31 @@ aimx_status aimx_get_static(const aimx_ctx* cc, double* CA, double* Crho, double
   if (Yrho_NR) AIMX_CUDA(cudaMemcpy(Yrho_NR, c->sd.YR_NR, n, cudaMemcpyDeviceToHost));
   if (LA_P) AIMX_CUDA(cudaMemcpy(LA_P, c->sd.LA_P, n, cudaMemcpyDeviceToHost));
   if (Yrho_P) AIMX_CUDA(cudaMemcpy(Yrho_P, c->sd.YR_P, n, cudaMemcpyDeviceToHost));
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_get_linear_entries(const aimx_ctx* cc, int32_t* cols, double* CA_lin, double* Crho_lin) {
+  aimx_ctx* c = const_cast<aimx_ctx*>(cc);
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (!c->lin_col) throw Error(AIMX_E_STATE, "aimx_set_linear_term has not been enabled");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  const int64_t n = c->topo.nb * kLinW;
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  if (cols) AIMX_CUDA(cudaMemcpy(cols, c->lin_col, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  const bool f32 = c->prec == AIMX_C64;
+  std::vector<double> v((size_t)(2 * n));
+  if (f32) {
+    std::vector<float> tmp((size_t)(2 * n));
+    AIMX_CUDA(cudaMemcpy(tmp.data(), c->lin_c, tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    std::copy(tmp.begin(), tmp.end(), v.begin());
+  } else {
+    AIMX_CUDA(cudaMemcpy(v.data(), c->lin_c, v.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (CA_lin) CA_lin[i] = v[2 * i];
+    if (Crho_lin) Crho_lin[i] = v[2 * i + 1];
+  }
   AIMX_API_END(c)
 }
 

@@ -220,6 +220,31 @@ void build_topology(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, Topo
   }
 }
 
+// Overlapping pairs for the linear-term modification (reading R21):
+// n is listed in row m when the supports of f_m and f_n share a triangle.
+// A triangle carries at most 3 RWGs, so a row holds at most 1 + 2 + 2 columns.
+void build_overlap(const Topology& t, std::vector<int32_t>& cols) {
+  std::vector<int32_t> cnt(t.nt + 1, 0);
+  for (int64_t e = 0; e < t.nb; ++e) { ++cnt[t.tp[e] + 1]; ++cnt[t.tm[e] + 1]; }
+  for (int64_t i = 0; i < t.nt; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int32_t> by_tri(cnt[t.nt]), fill(cnt.begin(), cnt.end() - 1);
+  for (int64_t e = 0; e < t.nb; ++e) {
+    by_tri[fill[t.tp[e]]++] = (int32_t)e;
+    by_tri[fill[t.tm[e]]++] = (int32_t)e;
+  }
+  cols.assign((size_t)t.nb * kLinW, -1);
+  std::vector<int32_t> u;
+  for (int64_t e = 0; e < t.nb; ++e) {
+    u.clear();
+    for (int32_t tri : {t.tp[e], t.tm[e]})
+      for (int32_t k = cnt[tri]; k < cnt[tri + 1]; ++k) u.push_back(by_tri[k]);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    if ((int)u.size() > kLinW) throw Error(AIMX_E_MESH, "more than 3 RWG edges on a triangle");
+    std::copy(u.begin(), u.end(), cols.begin() + e * kLinW);
+  }
+}
+
 void build_nodemap(const Topology& t, const std::vector<uint8_t>& nz_slot, NodeMap& m) {
   const int Nx = t.n[0], Ny = t.n[1], Nz = t.n[2];
   const int p = t.p, p3 = t.p3;

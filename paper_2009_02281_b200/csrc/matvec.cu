@@ -1095,6 +1095,62 @@ void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Comb
   }
 }
 
+// Linear-term modification: y^A += k0^2 C^A_lin x, y^rho += k0^2
+// C^rho_lin x over the <= kLinW overlapping columns of each row, after S4+S5
+// (combined: y += j alpha (k0^2 C^A_lin x - C^rho_lin x); PARTS: y0 += k0^2
+// C^A_lin x, y1 -= k0^2 C^rho_lin x).  Thread per (row, column of the batch):
+// the batch-interleaved xt makes the x reads of a row's threads contiguous.
+template <typename T, bool PARTS>
+__global__ void k_lin(const int32_t* __restrict__ lcol, const typename CT<T>::T2* __restrict__ lc, int nb, int BB,
+                      const typename CT<T>::T2* __restrict__ xt, typename CT<T>::T2* __restrict__ y0,
+                      typename CT<T>::T2* __restrict__ y1, Combine cb) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * BB) return;
+  const int m = (int)(i / BB), b = (int)(i - (int64_t)m * BB);
+  if (b >= cb.B) return;
+  T2 sa = mk<T2>(0, 0), sr = mk<T2>(0, 0);
+#pragma unroll
+  for (int j = 0; j < kLinW; ++j) {
+    const int n = lcol[m * kLinW + j];
+    if (n < 0) continue;
+    const T2 c = lc[m * kLinW + j];
+    const T2 xv = xt[(int64_t)n * BB + b];
+    sa.x += c.x * xv.x; sa.y += c.x * xv.y;
+    sr.x += c.y * xv.x; sr.y += c.y * xv.y;
+  }
+  const T k2 = (T)(1.0 / cb.beta[b]);
+  if constexpr (PARTS) {
+    if (y0) { T2 v = y0[m]; v.x += k2 * sa.x; v.y += k2 * sa.y; y0[m] = v; }
+    if (y1) { T2 v = y1[m]; v.x -= k2 * sr.x; v.y -= k2 * sr.y; y1[m] = v; }
+  } else {
+    const T al = (T)cb.alpha_im[b];
+    const T ux = k2 * sa.x - sr.x, uy = k2 * sa.y - sr.y;
+    T2* y = y0 + (int64_t)b * cb.ystride + m;
+    T2 v = *y;
+    v.x -= al * uy;
+    v.y += al * ux;
+    *y = v;
+  }
+}
+
+template <typename T>
+void run_lin(const HotDev& h, void* y0, void* y1, const Combine& c, cudaStream_t s) {
+  using T2 = typename CT<T>::T2;
+  const int BB = batch_bucket(c.B);
+  const int64_t n = (int64_t)h.nb * BB;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (c.mode == 1)
+    launch_pdl(k_lin<T, true>, dim3(g), dim3(256), 0, s, (const int32_t*)h.lin_col, (const T2*)h.lin_c, h.nb, BB,
+               (const T2*)h.xt, (T2*)y0, (T2*)y1, c);
+  else
+    launch_pdl(k_lin<T, false>, dim3(g), dim3(256), 0, s, (const int32_t*)h.lin_col, (const T2*)h.lin_c, h.nb, BB,
+               (const T2*)h.xt, (T2*)y0, (T2*)y1, c);
+  AIMX_CHECK_LAUNCH();
+}
+
 template <typename T>
 void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   if (h.R == 4) run_interp_r<T, 4>(h, x, y0, y1, c, s);
@@ -1146,7 +1202,11 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
     { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, B, s))); }
   }
   { StageScope sc(prof, 5, s); AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, B, s))); }
-  { StageScope sc(prof, 6, s); run_interp<T>(h, x, y0, y1, c, s); }
+  {
+    StageScope sc(prof, 6, s);
+    run_interp<T>(h, x, y0, y1, c, s);
+    if (h.lin_col) run_lin<T>(h, y0, y1, c, s);
+  }
 }
 
 // ---- slab-decomposed hot path (SlabRank): per rank S2 + x fwd on its rows,
@@ -1188,7 +1248,10 @@ void slab_matvec_t(std::vector<SlabRank*>& ranks, int Nx, int Ny, int Nz, SlabEx
   {
     StageScope sc(prof, 6, s);
     for (SlabRank* r : ranks)
-      if (r->hr.ngrp > 0) run_interp<T>(r->hr, x, y0, y1, c, s);
+      if (r->hr.ngrp > 0) {
+        run_interp<T>(r->hr, x, y0, y1, c, s);
+        if (r->hr.lin_col) run_lin<T>(r->hr, y0, y1, c, s);
+      }
   }
 }
 

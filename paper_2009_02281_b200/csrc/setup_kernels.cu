@@ -7,7 +7,9 @@
 //     P:267, change (a) P:297): analytic inner potential integrals, 7-point
 //     outer rule, symmetrised (reading R9),
 //   * precorrection L_s,P = W H_s,NR P (eq:aimLPs P:276) with H_s(0) = 0
-//     (eq:Hsmm P:321), and C = L_s,NR - L_s,P.
+//     (eq:Hsmm P:321), and C = L_s,NR - L_s,P,
+//   * the linear-term modification's C_lin = L_lin - W H_lin P on overlapping
+//     pairs (analytic inner integrals of R and (rho' - rho) R).
 // The paper's own static fill is its "one-time static matrix-fill" (tab:prof
 // P:715); here it runs once per context on the GPU.
 #include <cmath>
@@ -293,6 +295,118 @@ __global__ void k_precorrect(int nb, int order, const int64_t* __restrict__ rowp
   }
 }
 
+// ---- linear-term modification: kernel G_lin = -R/(8 pi)
+// Closed forms over the flat source triangle (surface divergence theorem in
+// its plane, u = rho' - rho, R0^2 = t0^2 + d^2 per edge):
+//   J0 = int R dS'   = (d^2 I0 + sum_k t0_k int_k R ds) / 3
+//   J1 = int u R dS' = (1/3) sum_k m_k int_k R^3 ds
+//   int R ds   = [s R + R0^2 ln(s + R)] / 2
+//   int R^3 ds = s R^3 / 4 + 3 R0^2 s R / 8 + 3 R0^4 ln(s + R) / 8
+__device__ __forceinline__ void r_potentials(const Frame& F, Vec3 r, double& J0, Vec3& J1, Vec3& rho) {
+  double d = dot(r - F.v[0], F.n);
+  rho = r - d * F.n;
+  double ad = fabs(d);
+  double I0 = 0.0, S = 0.0;
+  J1 = {0.0, 0.0, 0.0};
+  for (int k = 0; k < 3; ++k) {
+    Vec3 va = F.v[k], vb = F.v[(k + 1) % 3];
+    double sm = dot(va - rho, F.sh[k]);
+    double sp = dot(vb - rho, F.sh[k]);
+    double t0 = dot(va - rho, F.mh[k]);
+    double R0sq = t0 * t0 + d * d;
+    double Rm = norm(r - va), Rp = norm(r - vb);
+    double lim = 1e-14 * F.L[k];
+    double f2 = 0.0;
+    if (R0sq > lim * lim) f2 = logsum(Rp, sp, R0sq) - logsum(Rm, sm, R0sq);
+    double beta = 0.0;
+    if (ad > 0.0) beta = atan(t0 * sp / (R0sq + ad * Rp)) - atan(t0 * sm / (R0sq + ad * Rm));
+    I0 += t0 * f2 - ad * beta;
+    double lin = sp * Rp - sm * Rm;
+    S += t0 * 0.5 * (lin + R0sq * f2);
+    double k3 = 0.25 * (sp * Rp * Rp * Rp - sm * Rm * Rm * Rm) + 0.375 * R0sq * lin + 0.375 * R0sq * R0sq * f2;
+    J1 = J1 + k3 * F.mh[k];
+  }
+  J0 = (d * d * I0 + S) / 3.0;
+  J1 = (1.0 / 3.0) * J1;
+}
+
+// Unsymmetrised (L^A_lin, y^rho_lin)[m, n]: outer 7-point rule on m, analytic inner on n.
+__device__ void lin_pair(const double* __restrict__ side, int m, int n, double& la, double& yr) {
+  la = 0.0;
+  yr = 0.0;
+  for (int sm = 0; sm < 2; ++sm) {
+    const double* om = side + (2 * (int64_t)m + sm) * kSideStride;
+    Vec3 a = v3(om), b = v3(om + 3), c = v3(om + 6), pm = v3(om + 9);
+    double coef_m = om[12], div_m = om[13], area_m = om[14];
+    for (int sn = 0; sn < 2; ++sn) {
+      const double* on = side + (2 * (int64_t)n + sn) * kSideStride;
+      Frame F;
+      make_frame(on, F);
+      Vec3 pn = v3(on + 9);
+      double coef_n = on[12], div_n = on[13];
+      double sA = 0.0, sR = 0.0;
+      for (int q = 0; q < 7; ++q) {
+        double b0, b1, b2, w;
+        radon7(q, b0, b1, b2, w);
+        Vec3 r = b0 * a + b1 * b + b2 * c;
+        double J0;
+        Vec3 J1, rho;
+        r_potentials(F, r, J0, J1, rho);
+        Vec3 inner = coef_n * (J1 + J0 * (rho - pn));
+        Vec3 fm = coef_m * (r - pm);
+        sA += w * area_m * dot(fm, inner);
+        sR += w * area_m * J0;
+      }
+      la += sA;
+      yr += div_m * div_n * sR;
+    }
+  }
+  const double g = -1.0 / (8.0 * kPi);
+  la *= g;
+  yr *= g;
+}
+
+// Thread per (row m, overlap slot j): symmetrised L_lin entry minus the grid's
+// share W H_lin P, H_lin(delta) = -h |delta| / (8 pi) (H_lin(0) = 0).
+template <typename T2>
+__global__ void k_lin_entries(int nb, int order, double h, const int32_t* __restrict__ cols,
+                              const int32_t* __restrict__ anchor, const double* __restrict__ side,
+                              const double* __restrict__ lam, T2* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * kLinW) return;
+  const int m = (int)(i / kLinW), n = cols[i];
+  if (n < 0) {
+    out[i] = T2{0, 0};
+    return;
+  }
+  double la1, yr1, la2, yr2;
+  lin_pair(side, m, n, la1, yr1);
+  lin_pair(side, n, m, la2, yr2);
+  const int p = order + 1, p3 = p * p * p;
+  const int Dx = anchor[3 * n] - anchor[3 * m], Dy = anchor[3 * n + 1] - anchor[3 * m + 1],
+            Dz = anchor[3 * n + 2] - anchor[3 * m + 2];
+  const double* lm = lam + (int64_t)m * p3 * 4;
+  const double* ln = lam + (int64_t)n * p3 * 4;
+  const double g = -h / (8.0 * kPi);
+  double pa = 0.0, pr = 0.0;
+  for (int s2 = 0; s2 < p3; ++s2) {
+    const int i2 = s2 % p, j2 = (s2 / p) % p, k2 = s2 / (p * p);
+    double u0 = 0, u1 = 0, u2 = 0, u3 = 0;
+    for (int s1 = 0; s1 < p3; ++s1) {
+      const int dx = s1 % p - i2 - Dx, dy = (s1 / p) % p - j2 - Dy, dz = s1 / (p * p) - k2 - Dz;
+      const double hl = g * sqrt((double)(dx * dx + dy * dy + dz * dz));
+      u0 += lm[s1 * 4 + 0] * hl;
+      u1 += lm[s1 * 4 + 1] * hl;
+      u2 += lm[s1 * 4 + 2] * hl;
+      u3 += lm[s1 * 4 + 3] * hl;
+    }
+    pa += u0 * ln[s2 * 4 + 0] + u1 * ln[s2 * 4 + 1] + u2 * ln[s2 * 4 + 2];
+    pr += u3 * ln[s2 * 4 + 3];
+  }
+  using R = decltype(T2{}.x);
+  out[i] = T2{(R)(0.5 * (la1 + la2) - pa), (R)(0.5 * (yr1 + yr2) - pr)};
+}
+
 void gauss_legendre(int q, double* x, double* w) {
   // nodes/weights on [0, 1]
   for (int i = 0; i < q; ++i) {
@@ -351,6 +465,18 @@ void launch_static_near(const Topology& t, SetupDev& d, cudaStream_t s) {
   int64_t blocks = (t.nb * 32 + threads - 1) / threads;
   k_static_near<<<(unsigned)blocks, threads, 0, s>>>((int)t.nb, d.rowptr, d.col, d.side, d.LA_un,
                                                      d.YR_un);
+  AIMX_CHECK_LAUNCH();
+}
+
+void launch_lin_entries(const Topology& t, const SetupDev& d, const int32_t* cols, bool f32, void* out,
+                        cudaStream_t s) {
+  const int64_t n = t.nb * (int64_t)kLinW;
+  const unsigned g = (unsigned)((n + 127) / 128);
+  if (f32)
+    k_lin_entries<float2><<<g, 128, 0, s>>>((int)t.nb, t.order, t.h, cols, d.anchor, d.side, d.lam, (float2*)out);
+  else
+    k_lin_entries<double2><<<g, 128, 0, s>>>((int)t.nb, t.order, t.h, cols, d.anchor, d.side, d.lam,
+                                             (double2*)out);
   AIMX_CHECK_LAUNCH();
 }
 
