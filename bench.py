@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--prec", default=None, choices=[None, "c64", "c128"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--linear-term", action="store_true",
+                    help="apply the linear-term accuracy modification (P:382-398; off in the paper's results)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-freqs-per-step", type=int, default=2)
     ap.add_argument("--mode", default="shard", choices=["shard", "slab"],
@@ -184,13 +186,15 @@ def ncu_traffic(cfg: int, prec: str):
 
 
 # --------------------------------------------------------------------------- CPU oracle
-def oracle_sweep_rate(cfg: int, freqs, X, seconds: float, min_pts: int = 2):
+def oracle_sweep_rate(cfg: int, freqs, X, seconds: float, min_pts: int = 2, lin: bool = False):
     """The fp64 oracle as it stands, on this host's cores: setup (untimed),
     then sweep frequency points until ~`seconds` of work (>= min_pts)."""
     from oracle.aimx import from_config
     cores = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
     op = from_config(cfg, workers=cores)
+    if lin:
+        op.set_linear_term(True)
     t_setup = time.perf_counter() - t0
     n, t = 0, 0.0
     while n < len(freqs) and (n < min_pts or t < seconds):
@@ -217,6 +221,8 @@ def run_reference(a):
     cores = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
     op = from_config(a.config, workers=cores)
+    if a.linear_term:
+        op.set_linear_term(True)
     t_setup = time.perf_counter() - t0
     X = inp.rhs_matrix(a.config, op.N, idx)
     per = a.ref_freqs_per_step
@@ -270,6 +276,8 @@ def run_aimx(a):
         slab = (rank, world, box[0])
     op = AIMx(mesh.vertices, mesh.triangles, c.grid_n, order=c.order, near_cells=c.near_cells,
               prec=prec, slab=slab)
+    if a.linear_term:
+        op.set_linear_term(True)
     st = op.stats()
     if a.mode == "slab":   # every rank takes part in every frequency point
         freqs, idx = c.freqs, np.arange(len(c.freqs))
@@ -382,7 +390,7 @@ def run_aimx(a):
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             cpu, _ = oracle_sweep_rate(a.config, freqs, Xh.numpy().astype(np.complex128),
-                                       a.cpu_seconds)
+                                       a.cpu_seconds, lin=a.linear_term)
         except Exception as e:  # report, never fail the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
                    "kind": "oracle", "sample": f"failed: {e!r}"}
@@ -397,7 +405,7 @@ def run_aimx(a):
                        "freq_pts_per_rank_per_step": nf,
                        "parallelism": f"slab-fft x{world}" if a.mode == "slab" else f"freq-shard x{world}",
                        "l2": "flushed between timed steps (256 MB write); inputs resident in HBM",
-                       "setup_seconds": st["setup_seconds"]},
+                       "setup_seconds": st["setup_seconds"], "linear_term": bool(a.linear_term)},
             "matvec_per_s": matvec_per_s,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nf * vec_bytes,
                     "d2h_bytes_per_step": nf * vec_bytes},
