@@ -365,10 +365,10 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   int64_t* wslot = dupload(c, grp.wslot);
   h.payload = dupload(c, ck.payload);
   h.chunks = dupload(c, ck.chunks);
-  std::vector<int32_t> cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, false) * nsm);
+  std::vector<int32_t> cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, false, grp.R) * nsm);
   h.cta_ptr = dupload(c, cp);
   h.near_ctas = (int)cp.size() - 1;
-  cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, true) * nsm);
+  cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, true, grp.R) * nsm);
   h.cta_ptr1 = dupload(c, cp);
   h.near_ctas1 = (int)cp.size() - 1;
   const SetupDev& d = c->sd;

@@ -365,8 +365,8 @@ void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, N
   std::vector<int32_t> perm[2] = {row_order(t, 0, rows), row_order(t, 1, rows)};
   for (int kind = 0; kind < 2; ++kind) {
     if (eK && std::atoi(eK) != kind) continue;
-    for (int R : {4, 8}) {
-      if (eR && std::atoi(eR) != R) continue;
+    for (int R : {4, 8, 16}) {
+      if (eR ? std::atoi(eR) != R : R == 16) continue;   // 16: opt-in (AIMX_NEAR_R=16)
       const int64_t ngrp = (nb + R - 1) / R;
       const int64_t stride = std::max<int64_t>(1, ngrp / 4096);
       int64_t U = 0, ns = 0;

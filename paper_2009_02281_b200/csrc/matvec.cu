@@ -737,7 +737,7 @@ __device__ __forceinline__ void unpack(const typename VecT<T2, V>::type& u, T2* 
 }
 
 template <typename T, int R, int BB, bool PARTS>
-__global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1))
+__global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1, R))
     k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      typename CT<T>::T2* __restrict__ y0,
                                                      typename CT<T>::T2* __restrict__ y1, Combine cb) {
@@ -1154,6 +1154,7 @@ void run_lin(const HotDev& h, void* y0, void* y1, const Combine& c, cudaStream_t
 template <typename T>
 void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   if (h.R == 4) run_interp_r<T, 4>(h, x, y0, y1, c, s);
+  else if (h.R == 16) run_interp_r<T, 16>(h, x, y0, y1, c, s);
   else run_interp_r<T, 8>(h, x, y0, y1, c, s);
 }
 

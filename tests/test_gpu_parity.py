@@ -196,7 +196,7 @@ def test_sweep_results_independent_of_batch_size(prec):
         assert rel_l2(y.cpu().numpy(), ref.cpu().numpy()) <= tol
 
 
-@pytest.mark.parametrize("R,order", [(4, 0), (4, 1), (8, 0), (8, 1)])
+@pytest.mark.parametrize("R,order", [(4, 0), (4, 1), (8, 0), (8, 1), (16, 0), (16, 1)])
 @pytest.mark.parametrize("prec", ["c64", "c128"])
 def test_near_row_group_layouts(R, order, prec, monkeypatch):
     """Every row-group layout of the near matrix (R rows per group, anchor
