@@ -186,6 +186,36 @@ def ncu_traffic(cfg: int, prec: str):
 
 
 # --------------------------------------------------------------------------- CPU oracle
+def cufft_conv_ms(n, cols: int, prec: str, reps: int = 10) -> float:
+    """Comparison point only (north star): the same zero-padded FFT
+    convolution (4 channels x `cols` columns, full 2N_a grid, spectrum
+    multiply, crop) with cuFFT through torch.fft, ms per call."""
+    import torch
+    Nx, Ny, Nz = n
+    dt = torch.complex64 if prec == "c64" else torch.complex128
+    g = torch.randn(4 * cols, Nz, Ny, Nx, dtype=dt, device="cuda")
+    H = torch.randn(2 * Nz, 2 * Ny, 2 * Nx, dtype=dt, device="cuda")
+    pad = torch.zeros(4 * cols, 2 * Nz, 2 * Ny, 2 * Nx, dtype=dt, device="cuda")
+
+    def run():
+        pad.zero_()
+        pad[:, :Nz, :Ny, :Nx] = g
+        G = torch.fft.fftn(pad, dim=(-3, -2, -1))
+        G *= H
+        return torch.fft.ifftn(G, dim=(-3, -2, -1))[:, :Nz, :Ny, :Nx].contiguous()
+
+    for _ in range(3):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def oracle_sweep_rate(cfg: int, freqs, X, seconds: float, min_pts: int = 2, lin: bool = False):
     """The fp64 oracle as it stands, on this host's cores: setup (untimed),
     then sweep frequency points until ~`seconds` of work (>= min_pts)."""
@@ -378,6 +408,21 @@ def run_aimx(a):
         avg = ms / n
         stages[k] = {"ms_per_launch": avg, "launches": n, "bytes_per_launch": sb[k],
                      "GBps": sb[k] / (avg * 1e-3) / 1e9, "share": ms / step_stage_ms}
+    # cuFFT comparison point (untimed): our S2 + S3 stages per device batch
+    # (projection gather included, pruned transforms) vs cuFFT on the full
+    # padded grid with the same columns
+    cols = int(np.ceil(nf / max(1, prof_all["proj_xfft"][1])))
+    ours = sum(prof_all[k][0] / prof_all[k][1] for k in ("proj_xfft", "yfwd", "zconv", "yinv", "xinv")
+               if prof_all[k][1] > 0)
+    try:
+        cu = cufft_conv_ms(c.grid_n, cols, prec)
+    except Exception as e:  # comparison only
+        cu = None
+        print(f"cufft comparison failed: {e!r}", file=sys.stderr)
+    fft_vs_cufft = {"columns": cols, "ours_ms_per_batch": ours, "cufft_ms_per_batch": cu,
+                    "note": "ours = S2 projection gather + x/y/z transforms with the spectrum multiply (pruned "
+                            "to occupied lines/planes); cuFFT = torch.fft fftn * H, ifftn, crop on the full "
+                            "padded grid (4 channels x columns), comparison point only"}
     dms, dn = prof[dom]
     ach = sb[dom] / (dms / dn * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
@@ -412,6 +457,7 @@ def run_aimx(a):
             "gpu_launches": launches,
             "roofline": roofline,
             "stages": stages,
+            "fft_conv_vs_cufft": fft_vs_cufft,
             "stages_note": "one extra untimed step with every stage bracketed by CUDA events",
             "cpu_baseline": cpu,
             "clocks": clocks,

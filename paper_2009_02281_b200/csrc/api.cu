@@ -365,7 +365,9 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   int64_t* wslot = dupload(c, grp.wslot);
   h.payload = dupload(c, ck.payload);
   h.chunks = dupload(c, ck.chunks);
-  std::vector<int32_t> cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, false, grp.R) * nsm);
+  double waves = 1.0;   // CTAs per resident slot (experiments: AIMX_NEAR_WAVES)
+  if (const char* e = std::getenv("AIMX_NEAR_WAVES")) waves = std::max(0.25, std::atof(e));
+  std::vector<int32_t> cp = near_partition(ck, grp.ngrp, (int)(waves * near_ctas_per_sm(f32, false, grp.R) * nsm));
   h.cta_ptr = dupload(c, cp);
   h.near_ctas = (int)cp.size() - 1;
   cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, true, grp.R) * nsm);

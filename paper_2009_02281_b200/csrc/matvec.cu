@@ -486,7 +486,9 @@ template <typename T, int L> struct ZTma {
   static constexpr size_t HSB = sizeof(typename CT<T>::T2) * (size_t)L * CW / 4;   // one slab
   static constexpr size_t OFF_IN = (OFF_HS + 2 * HSB + 127) / 128 * 128;   // TMA: 128-byte aligned
   __host__ __device__ static size_t inb(int Nz) { return sizeof(typename CT<T>::T2) * (size_t)Nz * CW; }
-  __host__ __device__ static size_t smem(int Nz) { return OFF_IN + 2 * inb(Nz) + 16 + 128; }
+  // input ring depth: 3 (two row sets in flight) when two CTAs still fit an SM
+  __host__ __device__ static int nbuf(int Nz) { return OFF_IN + 3 * inb(Nz) + 24 + 128 <= 112 * 1024 ? 3 : 2; }
+  __host__ __device__ static size_t smem(int Nz) { return OFF_IN + nbuf(Nz) * inb(Nz) + 24 + 128; }
 };
 
 template <typename T, int L>
@@ -504,8 +506,9 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   unsigned char* smem_raw = (unsigned char*)(((uintptr_t)smem_dyn + 127) & ~(uintptr_t)127);
   T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][kz][kx - kx0]
-  T2* inb = reinterpret_cast<T2*>(smem_raw + Z::OFF_IN);                       // [2][z][CW]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Z::OFF_IN + 2 * Z::inb(Nz));
+  const int NB = Z::nbuf(Nz);
+  T2* inb = reinterpret_cast<T2*>(smem_raw + Z::OFF_IN);                       // [NB][z][CW]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Z::OFF_IN + NB * Z::inb(Nz));
   const int nkx = CW / 4, kx0 = h.kx0 + (blockIdx.x * CW) / 4;
   const int nslab = L * nkx;
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
@@ -536,31 +539,30 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
   const int nrs = min(ZROWS, Ny2 - rs0);
   const uint32_t bytes = (uint32_t)Z::inb(Nz);
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+    for (int k = 0; k < NB; ++k) mbar_init(bar + k, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   T2* tw = reinterpret_cast<T2*>(smem_raw);
   T2* xb = tw + L + line * G::XB;
   for (int i = threadIdx.x; i < L; i += G::NT) tw[i] = ((const T2*)h.twz_tab)[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(bar, bytes);
-    tma_load4(inb, &tm, col0 * C0S, rs0, 0, b, bar);
-  }
+  if (threadIdx.x == 0)   // rows rs0 .. rs0 + NB - 2 in flight before the loop
+    for (int k = 0; k < NB - 1 && k < nrs; ++k) {
+      mbar_arrive_expect_tx(bar + k, bytes);
+      tma_load4(inb + (size_t)k * Nz * CW, &tm, col0 * C0S, rs0 + k, 0, b, bar + k);
+    }
   prefetch(rs0, 0);
   for (int it = 0; it < nrs; ++it) {
-    const int ky = rs0 + it, buf = it & 1;
-    T2* ib = inb + (size_t)buf * Nz * CW;
-    if (it + 1 < nrs) {
-      prefetch(ky + 1, buf ^ 1);
-      if (threadIdx.x == 0) {
-        bulk_wait_read0();   // the store of row set it-1 has read buffer buf^1
-        mbar_arrive_expect_tx(bar + (buf ^ 1), bytes);
-        tma_load4(inb + (size_t)(buf ^ 1) * Nz * CW, &tm, col0 * C0S, ky + 1, 0, b, bar + (buf ^ 1));
-      }
+    const int ky = rs0 + it, buf = it & 1, ring = it % NB;
+    T2* ib = inb + (size_t)ring * Nz * CW;
+    if (it + 1 < nrs) prefetch(ky + 1, buf ^ 1);
+    if (threadIdx.x == 0 && it + NB - 1 < nrs) {
+      const int nr = (it + NB - 1) % NB;   // = the ring slot of row set it-1
+      bulk_wait_read0();                   // whose store has read it
+      mbar_arrive_expect_tx(bar + nr, bytes);
+      tma_load4(inb + (size_t)nr * Nz * CW, &tm, col0 * C0S, ky + NB - 1, 0, b, bar + nr);
     }
-    mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
+    mbar_wait(bar + ring, (uint32_t)(it / NB) & 1u);
     // input distribution D(R1,R2): z = t + T a + R1 n2 < Nz = L/2  <=>  n2 < R2/2
     T2 v[G::E];
 #pragma unroll

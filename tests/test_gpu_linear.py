@@ -150,3 +150,22 @@ def test_linear_cfg2_fullsize_rows():
         orc.set_frequency(freqs[i])
         _, _, z = orc.matvec_rows(gpu_input_as_c128(X[i], "c64"), rows)
         assert rel_l2(Y[i][rows], z) <= TOL["c64"], i
+
+
+def test_linear_solve_cfg1(orc1):
+    """aimx_solve with the modification on solves the modified system: the
+    library's residual under the ORACLE's modified operator, and the solution
+    against the oracle GMRES on the same operator."""
+    from oracle.gmres import solve
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), "c128")
+    op.set_linear_term(True)
+    freqs = np.array([60e6, 240e6])
+    B = np.stack([inp.rhs_vector(1, 50 + i, op.N) for i in range(2)])
+    X, its, rr = op.solve(freqs, to_gpu(B, "c128"), tol=1e-9, restart=20, maxiter=3000)
+    X = X.cpu().numpy()
+    for i, f in enumerate(freqs):
+        x_o, _, _ = solve(orc1, f, B[i], tol=1e-12, restart=40, maxiter=5000)
+        orc1.set_frequency(f)
+        res = np.linalg.norm(B[i] - orc1.matvec(X[i])) / np.linalg.norm(B[i])
+        assert rr[i] <= 1e-9 * (1 + 1e-6) and res <= 1e-9
+        assert rel_l2(X[i], x_o) <= 1e-6
