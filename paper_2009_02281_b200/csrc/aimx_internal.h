@@ -343,6 +343,13 @@ void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Co
                     cudaStream_t s, Profiler* prof);
 // xt <- the batch-interleaved columns of x (Combine: B, xstride)
 void interleave_f32(const HotDev& h, const void* x, const Combine& c, cudaStream_t s);
+// the two halves of hot_matvec: S2 + S3 up to phi, and S4 + S5 from phi and xt
+void hot_grid_f32(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, Profiler* prof);
+void hot_grid_f64(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, Profiler* prof);
+void hot_near_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
+                  Profiler* prof);
+void hot_near_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
+                  Profiler* prof);
 void interleave_f64(const HotDev& h, const void* x, const Combine& c, cudaStream_t s);
 void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof);

@@ -46,6 +46,10 @@ struct aimx_ctx {
   cudaStream_t sc[2] = {nullptr, nullptr};   // host sweep copy streams (H2D, D2H)
   std::vector<cudaEvent_t> ev_io;
   cudaEvent_t ev_start = nullptr, ev_sp[2] = {nullptr, nullptr}, ev_mv[2] = {nullptr, nullptr};
+  // sweep pipeline, S4+S5 of batch i on s3 while the grid part of batch i+1 runs:
+  cudaStream_t s3 = nullptr;
+  cudaEvent_t ev_grid[2] = {nullptr, nullptr};
+  void* PHI[2] = {nullptr, nullptr};          // potentials of batches i, i+1
   void* stage = nullptr;        // sweep_host staging
   int64_t stage_bytes = 0;
   double setup_seconds = 0;
@@ -505,11 +509,15 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     for (int k = 0; k < 2; ++k) c->HB[k] = dalloc<char>(c, noct * slots * (int64_t)cs);
     for (int k = 0; k < 2; ++k) c->XT[k] = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
     AIMX_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+    AIMX_CUDA(cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking));
     AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
       AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_sp[k], cudaEventDisableTiming));
       AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_mv[k], cudaEventDisableTiming));
+      AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_grid[k], cudaEventDisableTiming));
     }
+    c->PHI[0] = h.phi;
+    c->PHI[1] = zalloc<char>(c, nP * slots * (int64_t)cs + 64);
   }
   h.xt = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
   setup_self_terms(c);
@@ -888,17 +896,18 @@ void destroy_impl(aimx_ctx* c) {
   if (c->gm_ws) cudaFree(c->gm_ws);
   if (c->ev_spec) cudaEventDestroy(c->ev_spec);
   if (c->ev_use) cudaEventDestroy(c->ev_use);
-  if (c->s2) {
-    cudaStreamSynchronize(c->s2);
-    cudaStreamDestroy(c->s2);
-  }
+  for (cudaStream_t q : {c->s2, c->s3})
+    if (q) {
+      cudaStreamSynchronize(q);
+      cudaStreamDestroy(q);
+    }
   for (int k = 0; k < 2; ++k)
     if (c->sc[k]) {
       cudaStreamSynchronize(c->sc[k]);
       cudaStreamDestroy(c->sc[k]);
     }
   for (cudaEvent_t e : c->ev_io) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_start, c->ev_sp[0], c->ev_sp[1], c->ev_mv[0], c->ev_mv[1]})
+  for (cudaEvent_t e : {c->ev_start, c->ev_sp[0], c->ev_sp[1], c->ev_mv[0], c->ev_mv[1], c->ev_grid[0], c->ev_grid[1]})
     if (e) cudaEventDestroy(e);
   delete c;
 }
@@ -1356,7 +1365,7 @@ aimx_status aimx_matvec_parts(aimx_ctx* c, const void* x, void* yA, void* yPhi, 
 // (the host sweep orders its copies with them).
 static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, char* Y, int B,
                        cudaStream_t s, const std::function<void(int64_t)>& before = nullptr,
-                       const std::function<void(int64_t)>& after = nullptr,
+                       const std::function<void(int64_t, cudaStream_t)>& after = nullptr,
                        const std::function<void(int64_t, cudaStream_t)>& before_side = nullptr) {
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   if (c->slab || nf <= B || !c->s2) {
@@ -1364,7 +1373,7 @@ static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, 
       const int nb_ = (int)std::min<int64_t>(B, nf - i);
       if (before) before(i / B);
       run_batch(c, nb_, f + i, X + i * vb, Y + i * vb, s);
-      if (after) after(i / B);
+      if (after) after(i / B, s);
     }
     return;
   }
@@ -1385,6 +1394,10 @@ static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, 
     else interleave_f64(hh, X + i * B * vb, cb, c->s2);
     AIMX_CUDA(cudaEventRecord(c->ev_sp[i % 2], c->s2));
   };
+  // overlap: the grid part of batch i+1 (stream s) runs while S4+S5 of batch
+  // i (stream s3) does; phi is double-buffered (PHI), xt and the spectra are
+  // (XT, HB), and spec(i+2) waits for S4+S5 of batch i (ev_mv)
+  const bool ov = c->s3 && !std::getenv("AIMX_NO_OVERLAP");
   spec(0);
   for (int64_t i = 0; i < nbat; ++i) {
     if (i + 1 < nbat) spec(i + 1);
@@ -1395,11 +1408,25 @@ static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, 
     hh.xt = c->XT[i % 2];
     Combine cb = make_combine(count(i), f + i * B, 0, c->hot.nb);
     cb.xt_ready = 1;
-    if (c->prec == AIMX_C64) hot_matvec_f32(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
-    else hot_matvec_f64(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
-    AIMX_CUDA(cudaEventRecord(c->ev_mv[i % 2], s));
-    if (after) after(i);
+    const bool f32 = c->prec == AIMX_C64;
+    if (!ov) {
+      if (f32) hot_matvec_f32(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
+      else hot_matvec_f64(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
+      AIMX_CUDA(cudaEventRecord(c->ev_mv[i % 2], s));
+      if (after) after(i, s);
+      continue;
+    }
+    hh.phi = c->PHI[i % 2];
+    if (f32) hot_grid_f32(hh, X + i * B * vb, cb, s, &c->prof);
+    else hot_grid_f64(hh, X + i * B * vb, cb, s, &c->prof);
+    AIMX_CUDA(cudaEventRecord(c->ev_grid[i % 2], s));
+    AIMX_CUDA(cudaStreamWaitEvent(c->s3, c->ev_grid[i % 2], 0));
+    if (f32) hot_near_f32(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, c->s3, &c->prof);
+    else hot_near_f64(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, c->s3, &c->prof);
+    AIMX_CUDA(cudaEventRecord(c->ev_mv[i % 2], c->s3));
+    if (after) after(i, c->s3);
   }
+  if (ov) AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_mv[(nbat - 1) % 2], 0));
 }
 
 // device batch of a sweep: the caller's, else the slots, balanced over the
@@ -1493,9 +1520,9 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
     }
     auto before = [&](int64_t i) { AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_io[2 * i], 0)); };
     auto before_side = [&](int64_t i, cudaStream_t s2) { AIMX_CUDA(cudaStreamWaitEvent(s2, c->ev_io[2 * i], 0)); };
-    auto after = [&](int64_t i) {
+    auto after = [&](int64_t i, cudaStream_t sy) {
       const int64_t n = std::min<int64_t>(B, nb_ - i * B);
-      AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i + 1], s));
+      AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i + 1], sy));
       AIMX_CUDA(cudaStreamWaitEvent(c->sc[1], c->ev_io[2 * i + 1], 0));
       AIMX_CUDA(cudaMemcpyAsync((char*)Y + (i0 + i * B) * vb, dY + i * B * vb, n * vb, cudaMemcpyDeviceToHost,
                                 c->sc[1]));

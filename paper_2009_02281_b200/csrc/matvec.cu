@@ -1187,9 +1187,9 @@ template <typename T> bool run_yz_fused(const HotDev& h, int B, cudaStream_t s, 
   return true;
 }
 
+// S2 + S3 (+ x inverse): the grid part of a matvec, up to the potentials phi
 template <typename T>
-void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
-                Profiler* prof) {
+void hot_grid(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, Profiler* prof) {
   if (c.B < 1 || c.B > h.batch || c.B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "bad batch");
   const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz, B = c.B;
   {
@@ -1205,11 +1205,22 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
     { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, B, s))); }
   }
   { StageScope sc(prof, 5, s); AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, B, s))); }
-  {
-    StageScope sc(prof, 6, s);
-    run_interp<T>(h, x, y0, y1, c, s);
-    if (h.lin_col) run_lin<T>(h, y0, y1, c, s);
-  }
+}
+
+// S4 + S5 (+ the linear-term correction): from phi and xt to y
+template <typename T>
+void hot_near(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
+              Profiler* prof) {
+  StageScope sc(prof, 6, s);
+  run_interp<T>(h, x, y0, y1, c, s);
+  if (h.lin_col) run_lin<T>(h, y0, y1, c, s);
+}
+
+template <typename T>
+void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
+                Profiler* prof) {
+  hot_grid<T>(h, x, c, s, prof);
+  hot_near<T>(h, x, y0, y1, c, s, prof);
 }
 
 // ---- slab-decomposed hot path (SlabRank): per rank S2 + x fwd on its rows,
@@ -1340,6 +1351,20 @@ void interleave_f64(const HotDev& h, const void* x, const Combine& c, cudaStream
 void hot_matvec_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof) {
   hot_matvec<float>(h, x, y0, y1, c, s, prof);
+}
+void hot_grid_f32(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, Profiler* prof) {
+  hot_grid<float>(h, x, c, s, prof);
+}
+void hot_grid_f64(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, Profiler* prof) {
+  hot_grid<double>(h, x, c, s, prof);
+}
+void hot_near_f32(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
+                  Profiler* prof) {
+  hot_near<float>(h, x, y0, y1, c, s, prof);
+}
+void hot_near_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
+                  Profiler* prof) {
+  hot_near<double>(h, x, y0, y1, c, s, prof);
 }
 void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof) {
