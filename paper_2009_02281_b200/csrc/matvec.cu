@@ -483,7 +483,9 @@ template <typename T, int L> struct ZTma {
   using G = ZGeom<T, L>;
   static constexpr int CW = G::NL;   // columns per CTA (one ky row per step)
   static constexpr size_t OFF_HS = sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB);
-  static constexpr size_t HSB = sizeof(typename CT<T>::T2) * (size_t)L * CW / 4;   // one slab
+  static constexpr int KZ = L / 2 + 1;   // stored kz (the octant; kz > L/2 mirrors on read)
+  static constexpr int NPF = (KZ * (CW / 4) + G::NT - 1) / G::NT;   // slab elements per thread
+  static constexpr size_t HSB = sizeof(typename CT<T>::T2) * (size_t)KZ * CW / 4;   // one slab
   static constexpr size_t OFF_IN = (OFF_HS + 2 * HSB + 127) / 128 * 128;   // TMA: 128-byte aligned
   __host__ __device__ static size_t inb(int Nz) { return sizeof(typename CT<T>::T2) * (size_t)Nz * CW; }
   // input ring depth: 3 (two row sets in flight) when two CTAs still fit an SM
@@ -498,19 +500,20 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
   using T2 = typename CT<T>::T2;
   using G = ZGeom<T, L>;
   using Z = ZTma<T, L>;
-  constexpr int NPF = G::E / 4, CW = Z::CW, C0S = sizeof(T2) / 8;   // tensor elements per complex
+  constexpr int NPF = Z::NPF, CW = Z::CW, C0S = sizeof(T2) / 8;   // tensor elements per complex
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   __builtin_assume(t < G::T);
   const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
   const int b = blockIdx.z;
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   unsigned char* smem_raw = (unsigned char*)(((uintptr_t)smem_dyn + 127) & ~(uintptr_t)127);
-  T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][kz][kx - kx0]
+  T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][kz <= Nz][kx - kx0]
   const int NB = Z::nbuf(Nz);
   T2* inb = reinterpret_cast<T2*>(smem_raw + Z::OFF_IN);                       // [NB][z][CW]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Z::OFF_IN + NB * Z::inb(Nz));
-  const int nkx = CW / 4, kx0 = h.kx0 + (blockIdx.x * CW) / 4;
-  const int nslab = L * nkx;
+  constexpr int nkx = CW / 4;
+  const int kx0 = h.kx0 + (blockIdx.x * CW) / 4;
+  constexpr int nslab = Z::KZ * nkx;   // the slab stores kz = 0..Nz (Nz = L/2 here)
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
   const int64_t kystride = (int64_t)(Nz + 1) * (Nx + 1);
   int64_t poff[NPF];
@@ -519,11 +522,10 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
 #pragma unroll
     for (int k = 0; k < NPF; ++k) {
       const int idx = threadIdx.x + k * G::NT;
-      const int kxl = idx & (nkx - 1), kz = (idx >> LGK) % L;
+      const int kxl = idx & (nkx - 1), kz = min(idx >> LGK, Nz);
       const int kx = kx0 + kxl;
       const int kxf = kx <= Nx ? kx : 2 * Nx - kx;
-      const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
-      poff[k] = (int64_t)kzf * (Nx + 1) + kxf;
+      poff[k] = (int64_t)kz * (Nx + 1) + kxf;
     }
   }
   auto prefetch = [&](int ky, int buf) {
@@ -579,7 +581,7 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
 #pragma unroll
       for (int i = 0; i < G::E; ++i) {
         const int kz = TwoLevel<G::R2, G::R1>::in_index(t, i);
-        v[i] = cmul(v[i], hl[kz * nkx]);
+        v[i] = cmul(v[i], hl[(kz <= L / 2 ? kz : L - kz) * nkx]);
       }
     }
     inv_fft_swapped<T2, L>(v, xb, tw, t);
