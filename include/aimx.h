@@ -169,9 +169,10 @@ aimx_status aimx_matvec_parts(aimx_ctx* ctx, const void* x, void* yA, void* yPhi
 
 /* Frequency sweep: for i < nf, Y[i,:] = Z(f_hz[i]) X[i,:] (per frequency: S1
  * then S2-S5).  f_hz is a HOST array; X, Y device arrays [nf][N_b] row-major.
- * Frequencies run in device batches of `batch` points (<= 0 or more than the
- * context's batch slots: all slots; slots are chosen at setup from the grid
- * size, at most 16, environment variable AIMX_BATCH overrides): the spectra of
+ * Frequencies run in device batches of `batch` points, the remainder last
+ * (<= 0 or more than the context's batch slots: all slots; slots are chosen at
+ * setup from the grid size, at most 32, environment variable AIMX_BATCH
+ * overrides): the spectra of
  * a batch are generated together and one batched matvec reads the near matrix
  * and the weights once for all of its right-hand sides.  Results are
  * deterministic (fixed-order reductions, no atomics); across batch sizes the
@@ -185,7 +186,8 @@ aimx_status aimx_sweep(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void
  * relative residual `tol`, the paper uses 1e-4), right-preconditioned with the
  * diagonal of the frequency-independent near matrix (M(k0) =
  * diag(-j w mu0 (L^A_s,NR[m,m] + k0^-2 L^phi_s,NR[m,m]))), x0 = 0.
- * Frequencies run in device batches (as aimx_sweep): each batch's spectra
+ * Frequencies run in device batches (the slots, balanced over the batches
+ * needed): each batch's spectra
  * are generated once and all its columns iterate together, each with its own
  * Krylov basis (Arnoldi by classical Gram-Schmidt applied twice, Givens on the
  * host).  RHS, X: device [nf][N_b]; f_hz, iters (iterations used, may be

@@ -1363,35 +1363,34 @@ aimx_status aimx_matvec_parts(aimx_ctx* c, const void* x, void* yA, void* yPhi, 
 // stream (double-buffered) while batch i's matvec runs, so S1 overlaps S2-S5.
 // before(i) / after(i): hooks on the compute stream around device batch i
 // (the host sweep orders its copies with them).
-static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, char* Y, int B,
+static void sweep_impl(aimx_ctx* c, const std::vector<int64_t>& off, const double* f, const char* X, char* Y,
                        cudaStream_t s, const std::function<void(int64_t)>& before = nullptr,
                        const std::function<void(int64_t, cudaStream_t)>& after = nullptr,
                        const std::function<void(int64_t, cudaStream_t)>& before_side = nullptr) {
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
-  if (c->slab || nf <= B || !c->s2) {
-    for (int64_t i = 0; i < nf; i += B) {
-      const int nb_ = (int)std::min<int64_t>(B, nf - i);
-      if (before) before(i / B);
-      run_batch(c, nb_, f + i, X + i * vb, Y + i * vb, s);
-      if (after) after(i / B, s);
+  const int64_t nbat = (int64_t)off.size() - 1;
+  auto count = [&](int64_t i) { return (int)(off[i + 1] - off[i]); };
+  if (c->slab || nbat < 2 || !c->s2) {
+    for (int64_t i = 0; i < nbat; ++i) {
+      if (before) before(i);
+      run_batch(c, count(i), f + off[i], X + off[i] * vb, Y + off[i] * vb, s);
+      if (after) after(i, s);
     }
     return;
   }
-  const int64_t nbat = (nf + B - 1) / B;
-  auto count = [&](int64_t i) { return (int)std::min<int64_t>(B, nf - i * B); };
   AIMX_CUDA(cudaEventRecord(c->ev_start, s));
   AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_start, 0));
   // side stream, per batch: its spectra and its interleaved columns (xt),
   // double-buffered; `before` (the host sweep's copy) gates the columns
   auto spec = [&](int64_t i) {
     if (i >= 2) AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_mv[i % 2], 0));   // matvec i-2 read these buffers
-    spectra(c, count(i), f + i * B, c->s2, c->HB[i % 2]);
+    spectra(c, count(i), f + off[i], c->s2, c->HB[i % 2]);
     HotDev hh = c->hot;
     hh.xt = c->XT[i % 2];
-    Combine cb = make_combine(count(i), f + i * B, 0, c->hot.nb);
+    Combine cb = make_combine(count(i), f + off[i], 0, c->hot.nb);
     if (before_side) before_side(i, c->s2);
-    if (c->prec == AIMX_C64) interleave_f32(hh, X + i * B * vb, cb, c->s2);
-    else interleave_f64(hh, X + i * B * vb, cb, c->s2);
+    if (c->prec == AIMX_C64) interleave_f32(hh, X + off[i] * vb, cb, c->s2);
+    else interleave_f64(hh, X + off[i] * vb, cb, c->s2);
     AIMX_CUDA(cudaEventRecord(c->ev_sp[i % 2], c->s2));
   };
   // overlap: the grid part of batch i+1 (stream s) runs while S4+S5 of batch
@@ -1406,23 +1405,23 @@ static void sweep_impl(aimx_ctx* c, int64_t nf, const double* f, const char* X, 
     HotDev hh = c->hot;
     hh.Hoct = c->HB[i % 2];
     hh.xt = c->XT[i % 2];
-    Combine cb = make_combine(count(i), f + i * B, 0, c->hot.nb);
+    Combine cb = make_combine(count(i), f + off[i], 0, c->hot.nb);
     cb.xt_ready = 1;
     const bool f32 = c->prec == AIMX_C64;
     if (!ov) {
-      if (f32) hot_matvec_f32(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
-      else hot_matvec_f64(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, s, &c->prof);
+      if (f32) hot_matvec_f32(hh, X + off[i] * vb, Y + off[i] * vb, nullptr, cb, s, &c->prof);
+      else hot_matvec_f64(hh, X + off[i] * vb, Y + off[i] * vb, nullptr, cb, s, &c->prof);
       AIMX_CUDA(cudaEventRecord(c->ev_mv[i % 2], s));
       if (after) after(i, s);
       continue;
     }
     hh.phi = c->PHI[i % 2];
-    if (f32) hot_grid_f32(hh, X + i * B * vb, cb, s, &c->prof);
-    else hot_grid_f64(hh, X + i * B * vb, cb, s, &c->prof);
+    if (f32) hot_grid_f32(hh, X + off[i] * vb, cb, s, &c->prof);
+    else hot_grid_f64(hh, X + off[i] * vb, cb, s, &c->prof);
     AIMX_CUDA(cudaEventRecord(c->ev_grid[i % 2], s));
     AIMX_CUDA(cudaStreamWaitEvent(c->s3, c->ev_grid[i % 2], 0));
-    if (f32) hot_near_f32(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, c->s3, &c->prof);
-    else hot_near_f64(hh, X + i * B * vb, Y + i * B * vb, nullptr, cb, c->s3, &c->prof);
+    if (f32) hot_near_f32(hh, X + off[i] * vb, Y + off[i] * vb, nullptr, cb, c->s3, &c->prof);
+    else hot_near_f64(hh, X + off[i] * vb, Y + off[i] * vb, nullptr, cb, c->s3, &c->prof);
     AIMX_CUDA(cudaEventRecord(c->ev_mv[i % 2], c->s3));
     if (after) after(i, c->s3);
   }
@@ -1435,6 +1434,27 @@ static int sweep_batch(const aimx_ctx* c, int32_t batch, int64_t nf) {
   if (batch > 0) return std::max(1, std::min<int>(batch, c->hot.batch));
   const int64_t S = c->hot.batch, nb = (nf + S - 1) / S;
   return (int)std::max<int64_t>(1, std::min<int64_t>(S, nb > 0 ? (nf + nb - 1) / nb : S));
+}
+
+// Batch offsets of a sweep (size nbat + 1): batches of the caller's size, else
+// full slots with the remainder last (a short last batch also shortens the
+// host sweep's final device->host copy); AIMX_SWEEP_PLAN="s0,s1,..." sets the
+// leading batch sizes (experiments).
+static std::vector<int64_t> sweep_plan(const aimx_ctx* c, int32_t batch, int64_t nf) {
+  const int64_t S = c->hot.batch;
+  const int64_t B = batch > 0 ? std::max<int64_t>(1, std::min<int64_t>(batch, S)) : S;
+  std::vector<int64_t> off{0};
+  if (batch <= 0)
+    if (const char* e = std::getenv("AIMX_SWEEP_PLAN")) {
+      for (const char* p = e; *p && off.back() < nf;) {
+        const int64_t v = std::max<int64_t>(1, std::min<int64_t>(S, std::atoll(p)));
+        off.push_back(std::min(nf, off.back() + v));
+        while (*p && *p != ',') ++p;
+        if (*p == ',') ++p;
+      }
+    }
+  while (off.back() < nf) off.push_back(std::min(nf, off.back() + B));
+  return off;
 }
 
 aimx_status aimx_sweep(aimx_ctx* c, int64_t nf, const double* f_hz, const void* X, void* Y,
@@ -1453,7 +1473,7 @@ aimx_status aimx_sweep(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
   }
-  sweep_impl(c, nf, f_hz, (const char*)X, (char*)Y, sweep_batch(c, batch, nf), s);
+  sweep_impl(c, sweep_plan(c, batch, nf), f_hz, (const char*)X, (char*)Y, s);
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
   AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
@@ -1472,13 +1492,22 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  const int64_t B = sweep_batch(c, batch, nf);
+  const std::vector<int64_t> plan = sweep_plan(c, batch, nf);
+  const int64_t nbat_all = (int64_t)plan.size() - 1;
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
-  // staging: as many whole batches as fit in 1 GB (all of them for cfg1/cfg2), so
+  // staging: chunks of whole batches within 1 GB (all of them for cfg1/cfg2), so
   // the device batches pipeline; copies of the next chunk wait for this one
-  const int64_t fit = std::max<int64_t>(1, (int64_t)(1ll << 30) / (2 * (int64_t)vb) / B);
-  const int64_t CH = std::min<int64_t>((nf + B - 1) / B, fit) * B;
-  const int64_t need = 2 * CH * (int64_t)vb;
+  const int64_t fit = std::max<int64_t>((int64_t)c->hot.batch, (int64_t)(1ll << 30) / (2 * (int64_t)vb));
+  std::vector<int64_t> cuts{0};   // chunk boundaries, as batch indices
+  for (int64_t i = 0; i < nbat_all; ++i)
+    if (plan[i + 1] - plan[cuts.back()] > fit) cuts.push_back(i);
+  cuts.push_back(nbat_all);
+  int64_t CH = 0, nbat_max = 0;
+  for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+    CH = std::max(CH, plan[cuts[k + 1]] - plan[cuts[k]]);
+    nbat_max = std::max(nbat_max, cuts[k + 1] - cuts[k]);
+  }
+  const int64_t need = 2 * std::max<int64_t>(CH, 1) * (int64_t)vb;
   if (c->stage_bytes < need) {
     if (c->stage) AIMX_CUDA(cudaFree(c->stage));
     c->stage = nullptr;
@@ -1499,35 +1528,34 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   if (!c->sc[0]) {
     for (int k = 0; k < 2; ++k) AIMX_CUDA(cudaStreamCreateWithFlags(&c->sc[k], cudaStreamNonBlocking));
   }
-  const int64_t nbat_max = (CH + B - 1) / B;
   while ((int64_t)c->ev_io.size() < 2 * nbat_max + 1) {
     cudaEvent_t e;
     AIMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->ev_io.push_back(e);
   }
-  for (int64_t i0 = 0; i0 < nf; i0 += CH) {
-    const int64_t nb_ = std::min(CH, nf - i0);
-    const int64_t nbat = (nb_ + B - 1) / B;
+  for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+    const int64_t i0 = plan[cuts[k]];
+    std::vector<int64_t> sub;   // the chunk's batch offsets, relative to i0
+    for (int64_t i = cuts[k]; i <= cuts[k + 1]; ++i) sub.push_back(plan[i] - i0);
+    const int64_t nbat = (int64_t)sub.size() - 1;
     cudaEvent_t go = c->ev_io[2 * nbat_max];
     AIMX_CUDA(cudaEventRecord(go, s));   // staging free: the previous chunk's work is done
     AIMX_CUDA(cudaStreamWaitEvent(c->sc[0], go, 0));
     AIMX_CUDA(cudaStreamWaitEvent(c->sc[1], go, 0));
     for (int64_t i = 0; i < nbat; ++i) {
-      const int64_t n = std::min<int64_t>(B, nb_ - i * B);
-      AIMX_CUDA(cudaMemcpyAsync(dX + i * B * vb, (const char*)X + (i0 + i * B) * vb, n * vb,
+      AIMX_CUDA(cudaMemcpyAsync(dX + sub[i] * vb, (const char*)X + (i0 + sub[i]) * vb, (sub[i + 1] - sub[i]) * vb,
                                 cudaMemcpyHostToDevice, c->sc[0]));
       AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i], c->sc[0]));
     }
     auto before = [&](int64_t i) { AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_io[2 * i], 0)); };
     auto before_side = [&](int64_t i, cudaStream_t s2) { AIMX_CUDA(cudaStreamWaitEvent(s2, c->ev_io[2 * i], 0)); };
     auto after = [&](int64_t i, cudaStream_t sy) {
-      const int64_t n = std::min<int64_t>(B, nb_ - i * B);
       AIMX_CUDA(cudaEventRecord(c->ev_io[2 * i + 1], sy));
       AIMX_CUDA(cudaStreamWaitEvent(c->sc[1], c->ev_io[2 * i + 1], 0));
-      AIMX_CUDA(cudaMemcpyAsync((char*)Y + (i0 + i * B) * vb, dY + i * B * vb, n * vb, cudaMemcpyDeviceToHost,
-                                c->sc[1]));
+      AIMX_CUDA(cudaMemcpyAsync((char*)Y + (i0 + sub[i]) * vb, dY + sub[i] * vb, (sub[i + 1] - sub[i]) * vb,
+                                cudaMemcpyDeviceToHost, c->sc[1]));
     };
-    sweep_impl(c, nb_, f_hz + i0, dX, dY, (int)B, s, before, after, before_side);
+    sweep_impl(c, sub, f_hz + i0, dX, dY, s, before, after, before_side);
     AIMX_CUDA(cudaEventRecord(go, c->sc[1]));
     AIMX_CUDA(cudaStreamWaitEvent(s, go, 0));   // results are home before the next chunk / return
   }

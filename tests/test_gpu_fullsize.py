@@ -64,19 +64,19 @@ def test_cfg2_sweep_matches_per_frequency_matvecs():
 
 
 def test_cfg2_bench_sweep_vs_oracle_rows():
-    """bench.py's launch configuration (cfg2, c64, the 100-point sweep in four
-    25-point device batches, 32-column kernels) against the oracle on seeded
-    sampled rows."""
+    """bench.py's launch configuration (cfg2, c64, the 100-point sweep in
+    device batches of 32, 32, 32 and 4 points, 32- and 4-column kernels)
+    against the oracle on seeded sampled rows."""
     from oracle.aimx import from_config
     c = inp.get_config(2)
     op = make_gpu_op(inp.make_mesh(2), c.grid_n, "c64")
-    assert op.stats()["batch_slots"] == 32      # 100 points -> 4 device batches of 25
+    assert op.stats()["batch_slots"] == 32      # 100 points -> device batches 32, 32, 32, 4
     orc = from_config(2, static=False)
     X = np.stack([inp.rhs_vector(2, i, op.N) for i in range(len(c.freqs))])
     Y = op.sweep(c.freqs, to_gpu(X, "c64")).cpu().numpy()
     rows = np.sort(np.random.default_rng(22).choice(op.N, 32, replace=False))
     sr = orc.static_rows(rows)                       # near rows, pair by pair (once)
-    for i in (0, 24, 25, 74, 99):    # first / last points of the 25-point batches
+    for i in (0, 31, 32, 95, 96, 99):    # first / last points of the batches
         orc.set_frequency(c.freqs[i])
         x = gpu_input_as_c128(X[i], "c64")
         gA, gR = orc.grid_parts(x)
