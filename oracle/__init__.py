@@ -28,6 +28,8 @@ label) step by step:
                     C_lin = L_lin - W H_lin P on overlapping pairs
                     (eq:linterm P:363, eq:Lmatdecomplin P:386)
 * ``gmres``         restarted GMRES with the static diagonal preconditioner
+* ``aim``           the conventional AIM (per-frequency near region and
+                    precorrection, eq:aimL P:190, eq:aimLP P:205)
 
 Every reading of a silent/ambiguous/garbled passage is listed in DESIGN.md
 ("Readings") with the AMB-n tag used in comments here.
