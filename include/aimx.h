@@ -157,6 +157,24 @@ aimx_status aimx_set_frequency(aimx_ctx* ctx, double f_hz);
 aimx_status aimx_set_linear_term(aimx_ctx* ctx, int enable);
 aimx_status aimx_get_linear_term(const aimx_ctx* ctx, int* enabled);
 
+/* Conventional AIM mode (sec:methods:aim P:186-210), the method AIMx is
+ * measured against: the near region is regenerated by direct integration at
+ * every frequency ("Both L_NR(k0) and L_P(k0) must be generated for each
+ * frequency").  With the same grid, weights and static matrices it is
+ * AIMx plus, on the near pattern,
+ *   D(k0) = L_d,NR(k0) - W H_d,NR(k0) P
+ * (L_d,NR by the 7 x 7 product rule with G_d = G - G_s, H_d the grid samples
+ * of G_d with H_d(0) = -j k0/(4 pi)), so near entries are direct integration
+ * and far entries the grid.  enable != 0: every later aimx_set_frequency (and
+ * each frequency of a sweep) runs that fill on the device (fp64, stored in
+ * `prec`), matvec / parts / sweep add D(k0) x; sweeps run frequency by
+ * frequency.  Exclusive with the linear-term modification (AIMX_E_INVALID_ARG);
+ * one-GPU contexts only; aimx_solve is AIMX_E_UNSUPPORTED while it is on.
+ * aimx_get_aim_entries: D_A, D_rho of the bound frequency as complex128 in CSR
+ * order ([nnz] interleaved re/im; AIMX_E_STATE when off or unbound). */
+aimx_status aimx_set_conventional(aimx_ctx* ctx, int enable);
+aimx_status aimx_get_aim_entries(const aimx_ctx* ctx, double* DA, double* Drho);
+
 /* S2-S5: y = Z(k0) x = -j w mu0 (y^A - k0^-2 y^rho) (eq:EFIEAIMx P:288), where
  * y^A = W^(A) H P^(A) x + C_A x and y^rho = W^(phi) H P^(phi) x + C_rho x.
  * x, y: device vectors of N_b complex numbers (see conventions). */

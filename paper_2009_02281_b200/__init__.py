@@ -59,6 +59,8 @@ ABI_FUNCTIONS = {
     "aimx_set_frequency": (C.c_int, [_P, C.c_double]),
     "aimx_set_linear_term": (C.c_int, [_P, C.c_int]),
     "aimx_get_linear_term": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "aimx_set_conventional": (C.c_int, [_P, C.c_int]),
+    "aimx_get_aim_entries": (C.c_int, [_P, _P, _P]),
     "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec_parts": (C.c_int, [_P, _P, _P, _P, _P]),
     "aimx_sweep": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_int32, _P]),
@@ -231,6 +233,20 @@ class AIMx:
         """Linear-term accuracy modification: k0^2 G_lin integrated
         directly on overlapping pairs for every later matvec / sweep / solve."""
         _check(self.lib, self.lib.aimx_set_linear_term(self.ctx, int(bool(on))), self.ctx)
+
+    def set_conventional(self, on: bool = True):
+        """Conventional AIM mode: the near region regenerated by
+        direct integration at every frequency (the method AIMx is compared with)."""
+        _check(self.lib, self.lib.aimx_set_conventional(self.ctx, int(bool(on))), self.ctx)
+
+    def aim_entries(self):
+        """(D_A, D_rho) complex128 [nnz] in CSR order, at the bound frequency."""
+        nnz = C.c_int64()
+        _check(self.lib, self.lib.aimx_get_near_csr(self.ctx, None, None, C.byref(nnz)), self.ctx)
+        da = np.empty(nnz.value, np.complex128)
+        dr = np.empty(nnz.value, np.complex128)
+        _check(self.lib, self.lib.aimx_get_aim_entries(self.ctx, _P(da.ctypes.data), _P(dr.ctypes.data)), self.ctx)
+        return da, dr
 
     @property
     def linear_term(self) -> bool:

@@ -163,6 +163,11 @@ void launch_weights(const Topology& t, SetupDev& d, cudaStream_t s, uint8_t* nzf
 void launch_static_near(const Topology& t, SetupDev& d, cudaStream_t s);
 void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 
+// ---------------------------------------------------------------- conventional AIM mode
+// D(k0) = L_d,NR(k0) - W H_d,NR(k0) P on the near CSR pattern (external
+// order), fp64 arithmetic, stored in the compute precision (float2 / double2).
+void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, void* DA, void* DR, cudaStream_t s);
+
 // ---------------------------------------------------------------- linear-term modification
 // P:382-398 (sec:methods:aimx:acc): k0^2 G_lin, G_lin = -r/(8 pi) (eq:linterm
 // P:365), by direct integration on overlapping pairs only (supports share a
@@ -320,6 +325,11 @@ struct Combine {
   double alpha_im[kMaxBatch];    // alpha = j * alpha_im = -j w mu0
   double beta[kMaxBatch];        // k0^-2
 };
+
+// y += D(k0) x on the CSR pattern: combined (y += j alpha (D_A x - beta D_R x)) or parts
+// (y0 += D_A x, y1 -= D_R x), one column
+void aim_spmv(bool f32, int64_t nb, const int64_t* rowptr, const int32_t* col, const void* DA, const void* DR,
+              const void* x, void* y0, void* y1, const Combine& cb, cudaStream_t s);
 
 // ---- batched GMRES building blocks (solve.cu); B columns of N per block
 struct PcArgs {

@@ -76,6 +76,10 @@ struct aimx_ctx {
   int32_t* lin_col = nullptr;   // [nb][kLinW] overlapping columns
   void* lin_c = nullptr;        // [nb][kLinW] (C^A_lin, C^rho_lin), compute precision
   bool lin_on = false;
+  // conventional AIM mode (aimx_set_conventional): D(k0) on the near pattern
+  bool aim_on = false;
+  void* aimDA = nullptr;        // [nnz] compute precision complex
+  void* aimDR = nullptr;
   std::vector<void*> allocs;
   std::vector<std::unique_ptr<CUtensorMap>> tmaps;   // tensor maps referenced by HotDev::tmB
   std::string last_error;
@@ -811,6 +815,8 @@ void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
   c->k0 = 2.0 * kPi * f / kC0;
   c->omega = 2.0 * kPi * f;
   c->freq_set = true;
+  if (c->aim_on)   // conventional AIM: the per-frequency near fill
+    launch_aim_fill(c->topo, c->sd, c->k0, c->prec == AIMX_C64, c->aimDA, c->aimDR, s);
 }
 
 Combine make_combine(int B, const double* f, int mode, int64_t nb) {
@@ -856,10 +862,20 @@ void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaSt
   if (c->slab) return run_slab(c, x, y0, y1, cb, s);
   if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, s, &c->prof);
   else hot_matvec_f64(c->hot, x, y0, y1, cb, s, &c->prof);
+  if (c->aim_on)
+    aim_spmv(c->prec == AIMX_C64, c->hot.nb, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, x, y0, y1, cb, s);
 }
 
 // B frequency points: spectra into slots, then one batched matvec.
 void run_batch(aimx_ctx* c, int B, const double* f, const void* X, void* Y, cudaStream_t s) {
+  if (c->aim_on) {   // conventional AIM: near fill + matvec per frequency
+    const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
+    for (int b = 0; b < B; ++b) {
+      bind_frequency(c, f[b], s);
+      run_matvec(c, (const char*)X + b * vb, (char*)Y + b * vb, nullptr, 0, s);
+    }
+    return;
+  }
   spectra(c, B, f, s);
   Combine cb = make_combine(B, f, 0, c->hot.nb);
   if (c->slab) return run_slab(c, X, Y, nullptr, cb, s);
@@ -1233,6 +1249,7 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
     throw Error(AIMX_E_INVALID_ARG, "bad solve arguments");
   if (RHS == X) throw Error(AIMX_E_INVALID_ARG, "input and output alias");
   if (c->slab || !c->dA) throw Error(AIMX_E_UNSUPPORTED, "aimx_solve needs a one-GPU context");
+  if (c->aim_on) throw Error(AIMX_E_UNSUPPORTED, "aimx_solve runs the AIMx operator (conventional AIM mode is on)");
   for (int64_t i = 0; i < nf; ++i)
     if (!(f_hz[i] > 0.0) || !std::isfinite(f_hz[i])) throw Error(AIMX_E_INVALID_ARG, "bad frequency");
   AIMX_CUDA(cudaSetDevice(c->device));
@@ -1285,7 +1302,7 @@ aimx_status aimx_set_frequency(aimx_ctx* c, double f_hz) {
 
 // C_lin on the overlapping pairs, once per context; the per-RWG
 // geometry records are rebuilt first when the static matrices came from a cache.
-static void build_linear(aimx_ctx* c) {
+static void ensure_side(aimx_ctx* c) {
   const Topology& t = c->topo;
   SetupDev& d = c->sd;
   if (!d.side) {
@@ -1297,6 +1314,12 @@ static void build_linear(aimx_ctx* c) {
     d.side = dalloc<double>(c, 2 * t.nb * kSideStride);
     launch_rwg_sides(t, d, c->stream);
   }
+}
+
+static void build_linear(aimx_ctx* c) {
+  const Topology& t = c->topo;
+  SetupDev& d = c->sd;
+  ensure_side(c);
   std::vector<int32_t> cols;
   build_overlap(t, cols);
   c->lin_col = dupload(c, cols);
@@ -1318,6 +1341,7 @@ aimx_status aimx_set_linear_term(aimx_ctx* c, int enable) {
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  if (enable && c->aim_on) throw Error(AIMX_E_INVALID_ARG, "the linear-term modification is an AIMx option (conventional AIM mode is on)");
   if (enable && !c->lin_col) build_linear(c);
   c->lin_on = enable != 0;
   c->hot.lin_col = c->lin_on ? c->lin_col : nullptr;
@@ -1325,6 +1349,53 @@ aimx_status aimx_set_linear_term(aimx_ctx* c, int enable) {
   for (SlabRank& r : c->slabs) {
     r.hr.lin_col = c->lin_on && !r.owned.empty() ? r.lin_col : nullptr;
     r.hr.lin_c = c->lin_c;
+  }
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_set_conventional(aimx_ctx* c, int enable) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  if (enable && c->slab) throw Error(AIMX_E_UNSUPPORTED, "conventional AIM mode: one-GPU contexts only");
+  if (enable && c->lin_on) throw Error(AIMX_E_INVALID_ARG, "turn the linear-term modification off first");
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  if (enable && !c->aimDA) {
+    ensure_side(c);
+    const int64_t nnz = c->topo.rowptr[c->topo.nb];
+    const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
+    c->aimDA = dalloc<char>(c, nnz * (int64_t)cs);
+    c->aimDR = dalloc<char>(c, nnz * (int64_t)cs);
+  }
+  c->aim_on = enable != 0;
+  if (c->aim_on && c->freq_set) {   // the bound frequency's near fill
+    AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
+    launch_aim_fill(c->topo, c->sd, c->k0, c->prec == AIMX_C64, c->aimDA, c->aimDR, c->stream);
+    AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
+  }
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_get_aim_entries(const aimx_ctx* cc, double* DA, double* DR) {
+  aimx_ctx* c = const_cast<aimx_ctx*>(cc);
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (!c->aim_on || !c->freq_set) throw Error(AIMX_E_STATE, "conventional AIM mode off or no frequency bound");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  const int64_t nnz = c->topo.rowptr[c->topo.nb];
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  for (int part = 0; part < 2; ++part) {
+    double* out = part ? DR : DA;
+    const void* src = part ? c->aimDR : c->aimDA;
+    if (!out) continue;
+    if (c->prec == AIMX_C64) {
+      std::vector<float> tmp((size_t)(2 * nnz));
+      AIMX_CUDA(cudaMemcpy(tmp.data(), src, tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+      std::copy(tmp.begin(), tmp.end(), out);
+    } else {
+      AIMX_CUDA(cudaMemcpy(out, src, (size_t)(2 * nnz) * sizeof(double), cudaMemcpyDeviceToHost));
+    }
   }
   AIMX_API_END(c)
 }
@@ -1370,7 +1441,7 @@ static void sweep_impl(aimx_ctx* c, const std::vector<int64_t>& off, const doubl
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   const int64_t nbat = (int64_t)off.size() - 1;
   auto count = [&](int64_t i) { return (int)(off[i + 1] - off[i]); };
-  if (c->slab || nbat < 2 || !c->s2) {
+  if (c->slab || nbat < 2 || !c->s2 || c->aim_on) {
     for (int64_t i = 0; i < nbat; ++i) {
       if (before) before(i);
       run_batch(c, count(i), f + off[i], X + off[i] * vb, Y + off[i] * vb, s);

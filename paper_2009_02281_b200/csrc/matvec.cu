@@ -1341,8 +1341,61 @@ bool make_z_tensor_map(const HotDev& h, bool f32, void* out) {
   return r == CUDA_SUCCESS;
 }
 
+// Conventional AIM mode: y += D(k0) x, warp per row over the
+// near CSR pattern (complex coefficients, one column); lanes stride the row,
+// a fixed-order shuffle reduction, then the combine of eq:EFIEAIMx.
+template <typename T>
+__global__ void k_aim_spmv(int64_t nb, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                           const typename CT<T>::T2* __restrict__ DA, const typename CT<T>::T2* __restrict__ DR,
+                           const typename CT<T>::T2* __restrict__ x, typename CT<T>::T2* __restrict__ y0,
+                           typename CT<T>::T2* __restrict__ y1, Combine cb) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  const int lane = threadIdx.x & 31;
+  const int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (m >= nb) return;
+  T2 sa = mk<T2>(0, 0), sr = mk<T2>(0, 0);
+  for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
+    const T2 xv = x[col[k]], a = DA[k], r = DR[k];
+    sa = cadd(sa, cmul(a, xv));
+    sr = cadd(sr, cmul(r, xv));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sa.x += __shfl_xor_sync(0xffffffffu, sa.x, o);
+    sa.y += __shfl_xor_sync(0xffffffffu, sa.y, o);
+    sr.x += __shfl_xor_sync(0xffffffffu, sr.x, o);
+    sr.y += __shfl_xor_sync(0xffffffffu, sr.y, o);
+  }
+  if (lane != 0) return;
+  if (cb.mode == 1) {
+    if (y0) { T2 v = y0[m]; v.x += sa.x; v.y += sa.y; y0[m] = v; }
+    if (y1) { T2 v = y1[m]; v.x -= sr.x; v.y -= sr.y; y1[m] = v; }
+  } else {   // y += j alpha (sa - beta sr)
+    const T al = (T)cb.alpha_im[0], be = (T)cb.beta[0];
+    const T ux = sa.x - be * sr.x, uy = sa.y - be * sr.y;
+    T2 v = y0[m];
+    v.x -= al * uy;
+    v.y += al * ux;
+    y0[m] = v;
+  }
+}
+
 bool fft_length_supported(int L) { return L >= 8 && L <= 1024 && (L & (L - 1)) == 0; }
 
+
+void aim_spmv(bool f32, int64_t nb, const int64_t* rowptr, const int32_t* col, const void* DA, const void* DR,
+              const void* x, void* y0, void* y1, const Combine& cb, cudaStream_t s) {
+  const unsigned g = (unsigned)((nb * 32 + 255) / 256);
+  if (f32)
+    launch_pdl(k_aim_spmv<float>, dim3(g), dim3(256), 0, s, nb, rowptr, col, (const float2*)DA, (const float2*)DR,
+               (const float2*)x, (float2*)y0, (float2*)y1, cb);
+  else
+    launch_pdl(k_aim_spmv<double>, dim3(g), dim3(256), 0, s, nb, rowptr, col, (const double2*)DA, (const double2*)DR,
+               (const double2*)x, (double2*)y0, (double2*)y1, cb);
+  AIMX_CHECK_LAUNCH();
+}
 
 void interleave_f32(const HotDev& h, const void* x, const Combine& c, cudaStream_t s) {
   run_interleave<float>(h, x, c, s);

@@ -407,6 +407,108 @@ __global__ void k_lin_entries(int nb, int order, double h, const int32_t* __rest
   out[i] = T2{(R)(0.5 * (la1 + la2) - pa), (R)(0.5 * (yr1 + yr2) - pr)};
 }
 
+// ---- conventional AIM: per-frequency near correction
+// D(k0) = L_d,NR(k0) - W H_d,NR(k0) P on the near pattern (reading R22).
+__constant__ double2 c_hd_tab[512];   // H_d(delta) = G_d(k0, h sqrt(q)), [0] = -j k0/(4 pi)
+
+// G_d(k0, R) = (e^{-j k0 R} - 1)/(4 pi R), cancellation-free; R = 0: -j k0/(4 pi)
+__device__ __forceinline__ double2 green_d(double k0, double R) {
+  if (R == 0.0) return make_double2(0.0, -k0 / (4.0 * kPi));
+  double sh, ch, s, c;
+  sincos(0.5 * k0 * R, &sh, &ch);
+  s = 2.0 * sh * ch;
+  (void)c;
+  const double inv = 1.0 / (4.0 * kPi * R);
+  return make_double2(-2.0 * sh * sh * inv, -s * inv);
+}
+
+// Warp per row m, lanes over its near entries: L_d by the 7 x 7 product rule
+// over the 2 x 2 triangle combinations (the direct reference's recipe), minus
+// sum_c Lambda^c_m^T B_D(k0) Lambda^c_n with B_D[s,s'] = H_d(s - s' - D).
+template <typename T2>
+__global__ void k_aim_fill(int nb, int order, double k0, const int64_t* __restrict__ rowptr,
+                           const int32_t* __restrict__ col, const int32_t* __restrict__ anchor,
+                           const double* __restrict__ side, const double* __restrict__ lam, T2* __restrict__ DA,
+                           T2* __restrict__ DR) {
+  extern __shared__ double sh[];
+  const int p = order + 1, p3 = p * p * p;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  double* lm = sh + wib * (p3 * 4);
+  const bool active = warp < nb;
+  const int m = active ? (int)warp : 0;
+  for (int t = lane; t < p3 * 4; t += 32) lm[t] = active ? lam[(int64_t)m * p3 * 4 + t] : 0.0;
+  __syncwarp();
+  if (!active) return;
+  const int Amx = anchor[3 * m], Amy = anchor[3 * m + 1], Amz = anchor[3 * m + 2];
+  for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
+    const int n = col[k];
+    double2 la = make_double2(0, 0), yr = make_double2(0, 0);
+    for (int sm = 0; sm < 2; ++sm) {
+      const double* om = side + (2 * (int64_t)m + sm) * kSideStride;
+      const Vec3 a = v3(om), b = v3(om + 3), c = v3(om + 6), pm = v3(om + 9);
+      const double coef_m = om[12], div_m = om[13], area_m = om[14];
+      for (int sn = 0; sn < 2; ++sn) {
+        const double* on = side + (2 * (int64_t)n + sn) * kSideStride;
+        const Vec3 a2 = v3(on), b2 = v3(on + 3), c2 = v3(on + 6), pn = v3(on + 9);
+        const double coef_n = on[12], div_n = on[13], area_n = on[14];
+        for (int q1 = 0; q1 < 7; ++q1) {
+          double b0, b1, bb2, w1;
+          radon7(q1, b0, b1, bb2, w1);
+          const Vec3 r = b0 * a + b1 * b + bb2 * c;
+          const Vec3 fm = coef_m * (r - pm);
+          double2 sa = make_double2(0, 0), sr = make_double2(0, 0);
+          for (int q2 = 0; q2 < 7; ++q2) {
+            double e0, e1, e2, w2;
+            radon7(q2, e0, e1, e2, w2);
+            const Vec3 r2 = e0 * a2 + e1 * b2 + e2 * c2;
+            const double2 g = green_d(k0, norm(r - r2));
+            const double wf = w2 * dot(fm, coef_n * (r2 - pn));
+            sa.x += wf * g.x; sa.y += wf * g.y;
+            sr.x += w2 * g.x; sr.y += w2 * g.y;
+          }
+          const double wm = w1 * area_m * area_n;
+          la.x += wm * sa.x; la.y += wm * sa.y;
+          const double wr = wm * div_m * div_n;
+          yr.x += wr * sr.x; yr.y += wr * sr.y;
+        }
+      }
+    }
+    const int Dx = anchor[3 * n] - Amx, Dy = anchor[3 * n + 1] - Amy, Dz = anchor[3 * n + 2] - Amz;
+    int sqx[7], sqy[7], sqz[7];
+    for (int d = -order; d <= order; ++d) {
+      sqx[d + order] = (d - Dx) * (d - Dx);
+      sqy[d + order] = (d - Dy) * (d - Dy);
+      sqz[d + order] = (d - Dz) * (d - Dz);
+    }
+    const double* ln = lam + (int64_t)n * p3 * 4;
+    double2 pa = make_double2(0, 0), pr = make_double2(0, 0);
+    for (int s2 = 0; s2 < p3; ++s2) {
+      const int i2 = s2 % p, j2 = (s2 / p) % p, k2 = s2 / (p * p);
+      double2 u[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+      for (int s1 = 0; s1 < p3; ++s1) {
+        const int i1 = s1 % p, j1 = (s1 / p) % p, k1 = s1 / (p * p);
+        const double2 hd = c_hd_tab[sqx[i1 - i2 + order] + sqy[j1 - j2 + order] + sqz[k1 - k2 + order]];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          u[ch].x += lm[s1 * 4 + ch] * hd.x;
+          u[ch].y += lm[s1 * 4 + ch] * hd.y;
+        }
+      }
+      for (int ch = 0; ch < 3; ++ch) {
+        pa.x += u[ch].x * ln[s2 * 4 + ch];
+        pa.y += u[ch].y * ln[s2 * 4 + ch];
+      }
+      pr.x += u[3].x * ln[s2 * 4 + 3];
+      pr.y += u[3].y * ln[s2 * 4 + 3];
+    }
+    using R = decltype(T2{}.x);
+    DA[k] = T2{(R)(la.x - pa.x), (R)(la.y - pa.y)};
+    DR[k] = T2{(R)(yr.x - pr.x), (R)(yr.y - pr.y)};
+  }
+}
+
 void gauss_legendre(int q, double* x, double* w) {
   // nodes/weights on [0, 1]
   for (int i = 0; i < q; ++i) {
@@ -477,6 +579,28 @@ void launch_lin_entries(const Topology& t, const SetupDev& d, const int32_t* col
   else
     k_lin_entries<double2><<<g, 128, 0, s>>>((int)t.nb, t.order, t.h, cols, d.anchor, d.side, d.lam,
                                              (double2*)out);
+  AIMX_CHECK_LAUNCH();
+}
+
+void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, void* DA, void* DR, cudaStream_t s) {
+  std::vector<double2> tab(512);
+  tab[0] = make_double2(0.0, -k0 / (4.0 * kPi));
+  for (int q = 1; q < 512; ++q) {
+    const double r = t.h * std::sqrt((double)q), sh = std::sin(0.5 * k0 * r);
+    tab[q] = make_double2(-2.0 * sh * sh / (4.0 * kPi * r), -std::sin(k0 * r) / (4.0 * kPi * r));
+  }
+  const int R = 2 * t.order + t.near_cells;
+  if (3 * R * R >= 512) throw Error(AIMX_E_GRID, "precorrection offset table too small");
+  AIMX_CUDA(cudaMemcpyToSymbolAsync(c_hd_tab, tab.data(), sizeof(double2) * 512, 0, cudaMemcpyHostToDevice, s));
+  const int threads = 128;
+  const int64_t blocks = (t.nb * 32 + threads - 1) / threads;
+  const size_t shm = (threads / 32) * t.p3 * 4 * sizeof(double);
+  if (f32)
+    k_aim_fill<float2><<<(unsigned)blocks, threads, shm, s>>>((int)t.nb, t.order, k0, d.rowptr, d.col, d.anchor,
+                                                               d.side, d.lam, (float2*)DA, (float2*)DR);
+  else
+    k_aim_fill<double2><<<(unsigned)blocks, threads, shm, s>>>((int)t.nb, t.order, k0, d.rowptr, d.col, d.anchor,
+                                                                d.side, d.lam, (double2*)DA, (double2*)DR);
   AIMX_CHECK_LAUNCH();
 }
 
