@@ -239,11 +239,13 @@ __global__ void k_precorrect(int nb, int order, const int64_t* __restrict__ rowp
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  double* lm = sh + wib * (p3 * 4);
+  double* hs_tab = sh;   // H_s table in shared memory (lanes read different offsets)
+  for (int t = threadIdx.x; t < 512; t += blockDim.x) hs_tab[t] = c_hs_tab[t];
+  double* lm = sh + 512 + wib * (p3 * 4);
   const bool active = warp < nb;
   const int m = active ? (int)warp : 0;
   for (int t = lane; t < p3 * 4; t += 32) lm[t] = active ? lam[(int64_t)m * p3 * 4 + t] : 0.0;
-  __syncwarp();
+  __syncthreads();
   if (!active) return;
   const int Amx = anchor[3 * m], Amy = anchor[3 * m + 1], Amz = anchor[3 * m + 2];
   for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
@@ -273,7 +275,7 @@ __global__ void k_precorrect(int nb, int order, const int64_t* __restrict__ rowp
       for (int s1 = 0; s1 < p3; ++s1) {
         const int i1 = s1 % p, j1 = (s1 / p) % p, k1 = s1 / (p * p);
         const int qq = sqx[i1 - i2 + order] + sqy[j1 - j2 + order] + sqz[k1 - k2 + order];
-        const double hs = c_hs_tab[qq];
+        const double hs = hs_tab[qq];
         u0 += lm[s1 * 4 + 0] * hs;
         u1 += lm[s1 * 4 + 1] * hs;
         u2 += lm[s1 * 4 + 2] * hs;
@@ -435,11 +437,15 @@ __global__ void k_aim_fill(int nb, int order, double k0, const int64_t* __restri
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  double* lm = sh + wib * (p3 * 4);
+  // H_d table in shared memory: the lanes of a warp read different offsets
+  // (the constant bank would serialise them)
+  double2* hd_tab = reinterpret_cast<double2*>(sh);
+  for (int t = threadIdx.x; t < 512; t += blockDim.x) hd_tab[t] = c_hd_tab[t];
+  double* lm = sh + 2 * 512 + wib * (p3 * 4);
   const bool active = warp < nb;
   const int m = active ? (int)warp : 0;
   for (int t = lane; t < p3 * 4; t += 32) lm[t] = active ? lam[(int64_t)m * p3 * 4 + t] : 0.0;
-  __syncwarp();
+  __syncthreads();
   if (!active) return;
   const int Amx = anchor[3 * m], Amy = anchor[3 * m + 1], Amz = anchor[3 * m + 2];
   for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
@@ -489,7 +495,7 @@ __global__ void k_aim_fill(int nb, int order, double k0, const int64_t* __restri
       double2 u[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
       for (int s1 = 0; s1 < p3; ++s1) {
         const int i1 = s1 % p, j1 = (s1 / p) % p, k1 = s1 / (p * p);
-        const double2 hd = c_hd_tab[sqx[i1 - i2 + order] + sqy[j1 - j2 + order] + sqz[k1 - k2 + order]];
+        const double2 hd = hd_tab[sqx[i1 - i2 + order] + sqy[j1 - j2 + order] + sqz[k1 - k2 + order]];
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
           u[ch].x += lm[s1 * 4 + ch] * hd.x;
@@ -594,7 +600,7 @@ void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, 
   AIMX_CUDA(cudaMemcpyToSymbolAsync(c_hd_tab, tab.data(), sizeof(double2) * 512, 0, cudaMemcpyHostToDevice, s));
   const int threads = 128;
   const int64_t blocks = (t.nb * 32 + threads - 1) / threads;
-  const size_t shm = (threads / 32) * t.p3 * 4 * sizeof(double);
+  const size_t shm = (2 * 512 + (threads / 32) * t.p3 * 4) * sizeof(double);
   if (f32)
     k_aim_fill<float2><<<(unsigned)blocks, threads, shm, s>>>((int)t.nb, t.order, k0, d.rowptr, d.col, d.anchor,
                                                                d.side, d.lam, (float2*)DA, (float2*)DR);
@@ -613,7 +619,7 @@ void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s) {
                                     cudaMemcpyHostToDevice, s));
   const int threads = 128;
   int64_t blocks = (t.nb * 32 + threads - 1) / threads;
-  size_t shm = (threads / 32) * t.p3 * 4 * sizeof(double);
+  size_t shm = (512 + (threads / 32) * t.p3 * 4) * sizeof(double);
   k_precorrect<<<(unsigned)blocks, threads, shm, s>>>((int)t.nb, t.order, d.rowptr, d.col, d.anchor,
                                                      d.lam, d.LA_un, d.YR_un, d.LA_NR, d.YR_NR,
                                                      d.LA_P, d.YR_P, d.CA, d.CR);
