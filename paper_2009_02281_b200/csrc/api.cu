@@ -512,8 +512,16 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
     for (int k = 0; k < 2; ++k) c->HB[k] = dalloc<char>(c, noct * slots * (int64_t)cs);
     for (int k = 0; k < 2; ++k) c->XT[k] = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
-    AIMX_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
-    AIMX_CUDA(cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking));
+    // stream priorities (experiments: AIMX_PRIO_S2 / AIMX_PRIO_S3, 0 = default, 1 = high, -1 = low)
+    int plo = 0, phi_ = 0;
+    AIMX_CUDA(cudaDeviceGetStreamPriorityRange(&plo, &phi_));
+    auto prio = [&](const char* env) {
+      const char* e = std::getenv(env);
+      const int v = e ? std::atoi(e) : 0;
+      return v > 0 ? phi_ : (v < 0 ? plo : 0);
+    };
+    AIMX_CUDA(cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking, prio("AIMX_PRIO_S2")));
+    AIMX_CUDA(cudaStreamCreateWithPriority(&c->s3, cudaStreamNonBlocking, prio("AIMX_PRIO_S3")));
     AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
       AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_sp[k], cudaEventDisableTiming));

@@ -52,6 +52,11 @@ def test_aim_cfg1(prec, orc1):
     for i, f in enumerate(freqs):
         aim.set_frequency(f)
         assert rel_l2(Y[i], aim.matvec(gpu_input_as_c128(X[i], prec))) <= TOL[prec]
+    import torch
+    Xh = torch.as_tensor(X).to(op.cdtype).pin_memory()
+    Yh = torch.empty_like(Xh).pin_memory()
+    op.sweep_host(freqs, Xh, Yh)
+    assert np.array_equal(Yh.numpy(), Y)
     # exclusions, and back to AIMx
     with pytest.raises(AIMxError):
         op.set_linear_term(True)

@@ -276,3 +276,21 @@ def test_sweep_overlapped_near_equals_serial(prec, monkeypatch):
             s = op.sweep(freqs, X, batch=b).clone()
             monkeypatch.delenv("AIMX_NO_OVERLAP")
             assert torch.equal(a, s) and torch.equal(Yh, a.cpu())
+
+
+def test_sweep_plan_shapes():
+    """Sweep batch plans (full slots, remainder last): one point, exactly the
+    slots, slots + 1 (a 1-point last batch), an explicit batch size; every
+    point equals the single-frequency matvec."""
+    import torch
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), "c128")
+    S = op.stats()["batch_slots"]
+    for nf, b in ((1, 0), (S, 0), (S + 1, 0), (S + 1, 7)):
+        freqs = np.linspace(50e6, 400e6, nf)
+        X = to_gpu(np.stack([inp.rhs_vector(1, 90 + i, op.N) for i in range(nf)]), "c128")
+        Y = op.sweep(freqs, X, batch=b).cpu().numpy()
+        for i in (0, nf - 1):
+            op.set_frequency(freqs[i])
+            assert rel_l2(op.matvec(X[i].contiguous()).cpu().numpy(), Y[i]) <= 1e-13
+    Y0 = op.sweep(np.zeros(0), torch.zeros(0, op.N, dtype=op.cdtype, device="cuda"))
+    assert Y0.shape[0] == 0
