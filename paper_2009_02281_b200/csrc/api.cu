@@ -76,6 +76,15 @@ struct aimx_ctx {
   int32_t* lin_col = nullptr;   // [nb][kLinW] overlapping columns
   void* lin_c = nullptr;        // [nb][kLinW] (C^A_lin, C^rho_lin), compute precision
   bool lin_on = false;
+  // CUDA graphs of single matvecs (run_matvec): keyed by buffers, mode and
+  // frequency, captured when a key repeats (GMRES-style reuse), at most 8
+  struct MvGraph {
+    const void* x; void* y0; void* y1; int mode; double f;
+    cudaGraphExec_t exec; int64_t launches;
+  };
+  std::vector<MvGraph> graphs;
+  MvGraph last_mv{nullptr, nullptr, nullptr, -1, 0.0, nullptr, 0};
+  cudaStream_t cap = nullptr;   // capture stream
   // conventional AIM mode (aimx_set_conventional): D(k0) on the near pattern
   bool aim_on = false;
   void* aimDA = nullptr;        // [nnz] compute precision complex
@@ -865,13 +874,56 @@ void run_slab(aimx_ctx* c, const void* x, void* y0, void* y1, const Combine& cb,
   }
 }
 
+void clear_graphs(aimx_ctx* c) {
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+  c->last_mv = {nullptr, nullptr, nullptr, -1, 0.0, nullptr, 0};
+}
+
 void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaStream_t s) {
   Combine cb = make_combine(1, &c->f, mode, c->hot.nb);
   if (c->slab) return run_slab(c, x, y0, y1, cb, s);
-  if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, s, &c->prof);
-  else hot_matvec_f64(c->hot, x, y0, y1, cb, s, &c->prof);
-  if (c->aim_on)
-    aim_spmv(c->prec == AIMX_C64, c->hot.nb, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, x, y0, y1, cb, s);
+  auto eager = [&](cudaStream_t q) {
+    if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, q, &c->prof);
+    else hot_matvec_f64(c->hot, x, y0, y1, cb, q, &c->prof);
+    if (c->aim_on)
+      aim_spmv(c->prec == AIMX_C64, c->hot.nb, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, x, y0, y1, cb, q);
+  };
+  if (c->prof.on || std::getenv("AIMX_NO_GRAPH")) return eager(s);
+  auto same = [&](const aimx_ctx::MvGraph& g) {
+    return g.x == x && g.y0 == y0 && g.y1 == y1 && g.mode == mode && g.f == c->f;
+  };
+  for (auto& g : c->graphs)
+    if (same(g)) {   // replay: the kernels' launch latencies go away
+      AIMX_CUDA(cudaGraphLaunch(g.exec, s));
+      launch_counter() += g.launches;
+      return;
+    }
+  const bool repeat = same(c->last_mv);
+  c->last_mv = {x, y0, y1, mode, c->f, nullptr, 0};
+  if (!repeat) return eager(s);
+  if (!c->cap) AIMX_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+  const int64_t n0 = launch_counter();
+  AIMX_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeRelaxed));
+  cudaGraph_t graph = nullptr;
+  try {
+    eager(c->cap);
+  } catch (...) {
+    cudaStreamEndCapture(c->cap, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  AIMX_CUDA(cudaStreamEndCapture(c->cap, &graph));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  AIMX_CUDA(e);
+  if (c->graphs.size() >= 8) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  c->graphs.push_back({x, y0, y1, mode, c->f, exec, launch_counter() - n0});
+  AIMX_CUDA(cudaGraphLaunch(exec, s));
 }
 
 // B frequency points: spectra into slots, then one batched matvec.
@@ -914,6 +966,8 @@ void destroy_impl(aimx_ctx* c) {
     } catch (...) {
     }
   }
+  clear_graphs(c);
+  if (c->cap) cudaStreamDestroy(c->cap);
   for (void* p : c->allocs) if (p) cudaFree(p);
   spectrum_plan_free(c->sp);
   if (c->stage) cudaFree(c->stage);
@@ -1351,6 +1405,7 @@ aimx_status aimx_set_linear_term(aimx_ctx* c, int enable) {
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
   if (enable && c->aim_on) throw Error(AIMX_E_INVALID_ARG, "the linear-term modification is an AIMx option (conventional AIM mode is on)");
   if (enable && !c->lin_col) build_linear(c);
+  clear_graphs(c);
   c->lin_on = enable != 0;
   c->hot.lin_col = c->lin_on ? c->lin_col : nullptr;
   c->hot.lin_c = c->lin_c;
@@ -1376,6 +1431,7 @@ aimx_status aimx_set_conventional(aimx_ctx* c, int enable) {
     c->aimDA = dalloc<char>(c, nnz * (int64_t)cs);
     c->aimDR = dalloc<char>(c, nnz * (int64_t)cs);
   }
+  clear_graphs(c);
   c->aim_on = enable != 0;
   if (c->aim_on && c->freq_set) {   // the bound frequency's near fill
     AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
