@@ -9,3 +9,4 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 600 python scripts/perf_probe.py --configs 1,2,3,5 --iters 30 > gpurun_out/probe.jsonl 2> gpurun_out/probe.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 NCU_COUNT=2 NCU_OUT=gpurun_out/prof_dom bash scripts/gpu_ncu.sh "k_interp_near" --cfg 2 --nf 25
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sweep.csv python scripts/ncu_target.py --cfg 2 --nf 100 > gpurun_out/ncu_sweep.log 2>&1; echo "ncu sweep rc=$?" >> gpurun_out/ncu_sweep.log

@@ -25,7 +25,11 @@ def short(name):
     return name[:70]
 
 
-def launches(path, out):
+SETUP = ("k_static_near", "k_precorrect", "k_weights", "k_rwg_sides", "k_lam_to", "k_pack_c", "k_ent_w",
+         "k_aim_fill", "k_lin_entries", "k_sample_static", "k_d2f", "k_self", "k_diag")
+
+
+def launches(path, out, hot=False):
     txt = open(path).read()
     start = txt.find('"ID"')
     rows = list(csv.reader(io.StringIO(txt[start:])))
@@ -39,12 +43,15 @@ def launches(path, out):
         unit = r[ix["Metric Unit"]]
         v = float(r[ix["Metric Value"]].replace(",", ""))
         k = short(r[ix["Kernel Name"]])
+        if hot and (not ("k_" in k) or any(x in k for x in SETUP)):
+            continue
         per[k][0] += 1
         per[k][1] += v
     tot = sum(v[1] for v in per.values())
     with open(out, "w") as f:
         f.write(f"# ncu launch list summary ({path})\n\n")
-        f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over the whole bench command\n")
+        f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over the whole command"
+                + (" -- the library's hot-path kernels only (setup kernels excluded)" if hot else "") + "\n")
         f.write("(cold-cache, serialised: compare SHARES, not absolute times).\n\n")
         f.write(f"| kernel | launches | total ({unit}) | share |\n|---|---|---|---|\n")
         for k, (n, v) in sorted(per.items(), key=lambda kv: -kv[1][1]):
@@ -102,7 +109,7 @@ def stage_of(k):
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        launches(sys.argv[2], sys.argv[3])
+        launches(sys.argv[2], sys.argv[3], hot="--hot" in sys.argv)
     else:
         jp = key = None
         if "--json" in sys.argv:
