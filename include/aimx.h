@@ -169,7 +169,8 @@ aimx_status aimx_get_linear_term(const aimx_ctx* ctx, int* enabled);
  * each frequency of a sweep) runs that fill on the device (fp64, stored in
  * `prec`), matvec / parts / sweep add D(k0) x; sweeps run frequency by
  * frequency.  Exclusive with the linear-term modification (AIMX_E_INVALID_ARG);
- * one-GPU contexts only; aimx_solve is AIMX_E_UNSUPPORTED while it is on.
+ * one-GPU contexts only; aimx_solve then runs one frequency at a time, each
+ * with its near fill (same static diagonal preconditioner).
  * aimx_get_aim_entries: D_A, D_rho of the bound frequency as complex128 in CSR
  * order ([nnz] interleaved re/im; AIMX_E_STATE when off or unbound). */
 aimx_status aimx_set_conventional(aimx_ctx* ctx, int enable);

@@ -63,6 +63,9 @@ struct aimx_ctx {
   double* dR = nullptr;         // y^rho_s,NR[m,m]
   void* gm_ws = nullptr;
   int64_t gm_ws_bytes = 0;
+  void* gm_host = nullptr;      // pinned Arnoldi-step values
+  cudaEvent_t ev_gm = nullptr;  // their copy has landed
+  size_t gm_host_bytes = 0;
   // slab-decomposed FFT (aimx_setup_slab)
   bool slab = false;
   int world = 1, rank = 0;
@@ -972,6 +975,8 @@ void destroy_impl(aimx_ctx* c) {
   spectrum_plan_free(c->sp);
   if (c->stage) cudaFree(c->stage);
   if (c->gm_ws) cudaFree(c->gm_ws);
+  if (c->gm_host) cudaFreeHost(c->gm_host);
+  if (c->ev_gm) cudaEventDestroy(c->ev_gm);
   if (c->ev_spec) cudaEventDestroy(c->ev_spec);
   if (c->ev_use) cudaEventDestroy(c->ev_use);
   for (cudaStream_t q : {c->s2, c->s3})
@@ -1157,7 +1162,7 @@ static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, ch
   const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
   const int64_t blk = (int64_t)B * N;   // complex per [B][N] block
   // workspace: V[m+1] blocks, W, U, R blocks; device scalars
-  const int64_t need = (int64_t)(m + 4) * blk * (int64_t)cs + (int64_t)(m + 2) * B * 16 * 2 + B * 8 * 2;
+  const int64_t need = (int64_t)(m + 4) * blk * (int64_t)cs + (int64_t)(m + 2) * B * 16 * 4 + B * 8 * 2;
   if (c->gm_ws_bytes < need) {
     if (c->gm_ws) AIMX_CUDA(cudaFree(c->gm_ws));
     c->gm_ws = nullptr;
@@ -1170,8 +1175,19 @@ static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, ch
   char* Rb = U + blk * cs;
   double2* ddots = (double2*)(Rb + blk * cs);
   double2* dcoef = ddots + (int64_t)(m + 2) * B;
-  double* dsc = (double*)(dcoef + (int64_t)(m + 2) * B);
+  double2* dit = dcoef + (int64_t)(m + 2) * B;   // one Arnoldi step: [h pass 1 | h pass 2 | |w|^2]
+  double* dsc = (double*)(dit + (int64_t)(2 * m + 4) * B);
   std::vector<double2> hd((size_t)(m + 2) * B);
+  // pinned host copy of dit: one synchronisation per Arnoldi step
+  const size_t hit_bytes = (size_t)(2 * m + 4) * B * sizeof(double2);
+  if (c->gm_host_bytes < hit_bytes) {
+    if (c->gm_host) AIMX_CUDA(cudaFreeHost(c->gm_host));
+    c->gm_host = nullptr;
+    AIMX_CUDA(cudaMallocHost(&c->gm_host, hit_bytes));
+    c->gm_host_bytes = hit_bytes;
+  }
+  double2* hit = (double2*)c->gm_host;
+  if (!c->ev_gm) AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_gm, cudaEventDisableTiming));
   std::vector<double> hs(B);
   spectra(c, B, f, s);
   Combine cb = make_combine(B, f, 0, N);
@@ -1181,9 +1197,14 @@ static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, ch
     pa.alpha_im[b] = cb.alpha_im[b];
     pa.beta[b] = cb.beta[b];
   }
+  if (c->aim_on) {   // conventional AIM: this frequency's near fill (one column per batch)
+    if (B != 1) throw Error(AIMX_E_INTERNAL, "conventional AIM solve runs one frequency per batch");
+    launch_aim_fill(c->topo, c->sd, 2.0 * kPi * f[0] / kC0, f32, c->aimDA, c->aimDR, s);
+  }
   auto matvec = [&](const void* in, void* out) {
     if (f32) hot_matvec_f32(c->hot, in, out, nullptr, cb, s, &c->prof);
     else hot_matvec_f64(c->hot, in, out, nullptr, cb, s, &c->prof);
+    if (c->aim_on) aim_spmv(f32, N, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, in, out, nullptr, cb, s);
   };
   auto norms = [&](const void* A, std::vector<double>& out) {   // ||A_b||
     gm_dots(f32, 1, B, N, A, 0, A, ddots, s);
@@ -1221,24 +1242,39 @@ static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, ch
     std::vector<int> kb(B, 0), conv(B, 0);
     for (int b = 0; b < B; ++b) g[b][0] = done[b] ? 0.0 : beta[b];
     int j = 0;
+    bool pre = false;   // the step's preconditioned matvec is already queued
     for (; j < m && total < maxit; ++j, ++total) {
       char* Vj = V + (int64_t)j * blk * cs;
-      gm_pc(f32, B, N, Vj, U, c->dA, c->dR, pa, false, s);
-      matvec(U, W);
-      // CGS2: h = V^H w ; w -= V h ; twice
-      for (int pass = 0; pass < 2; ++pass) {
-        gm_dots(f32, j + 1, B, N, V, blk, W, ddots, s);
-        AIMX_CUDA(cudaMemcpyAsync(hd.data(), ddots, (size_t)(j + 1) * B * sizeof(double2), cudaMemcpyDeviceToHost, s));
-        AIMX_CUDA(cudaStreamSynchronize(s));
-        for (int b = 0; b < B; ++b)
-          for (int i = 0; i <= j; ++i) H[b][(size_t)i * m + j] += cd(hd[(size_t)i * B + b].x, hd[(size_t)i * B + b].y);
-        gm_lincomb(f32, j + 1, B, N, V, blk, ddots, W, false, s);
+      if (!pre) {
+        gm_pc(f32, B, N, Vj, U, c->dA, c->dR, pa, false, s);
+        matvec(U, W);
       }
-      std::vector<double> hn;
-      norms(W, hn);
-      std::vector<double> sc(B);
-      for (int b = 0; b < B; ++b) sc[b] = hn[b] > 0.0 ? 1.0 / hn[b] : 0.0;
-      colscale(W, sc, V + (int64_t)(j + 1) * blk * cs);
+      pre = false;
+      // CGS2: h = V^H w ; w -= V h ; twice (coefficients stay on the device),
+      // then |w|^2 and v_{j+1} = w / |w| on the device; ONE copy + sync
+      const int64_t hs_ = (int64_t)(j + 1) * B;
+      for (int pass = 0; pass < 2; ++pass) {
+        gm_dots(f32, j + 1, B, N, V, blk, W, dit + pass * hs_, s);
+        gm_lincomb(f32, j + 1, B, N, V, blk, dit + pass * hs_, W, false, s);
+      }
+      gm_dots(f32, 1, B, N, W, 0, W, dit + 2 * hs_, s);
+      gm_colscale_rsqrt(f32, B, N, W, dit + 2 * hs_, V + (int64_t)(j + 1) * blk * cs, s);
+      AIMX_CUDA(cudaMemcpyAsync(hit, dit, (size_t)(2 * hs_ + B) * sizeof(double2), cudaMemcpyDeviceToHost, s));
+      AIMX_CUDA(cudaEventRecord(c->ev_gm, s));
+      // look ahead: the next step's M^-1 v_{j+1} and its matvec need nothing
+      // from the host, so they run while the host does this step's rotations
+      if (j + 1 < m && total + 1 < maxit) {
+        gm_pc(f32, B, N, V + (int64_t)(j + 1) * blk * cs, U, c->dA, c->dR, pa, false, s);
+        matvec(U, W);
+        pre = true;
+      }
+      AIMX_CUDA(cudaEventSynchronize(c->ev_gm));
+      for (int pass = 0; pass < 2; ++pass)
+        for (int b = 0; b < B; ++b)
+          for (int i = 0; i <= j; ++i)
+            H[b][(size_t)i * m + j] += cd(hit[pass * hs_ + (int64_t)i * B + b].x, hit[pass * hs_ + (int64_t)i * B + b].y);
+      std::vector<double> hn(B);
+      for (int b = 0; b < B; ++b) hn[b] = std::sqrt(std::max(0.0, hit[2 * hs_ + b].x));
       for (int b = 0; b < B; ++b) {
         if (done[b] || conv[b]) continue;
         cd* Hb = H[b].data();
@@ -1311,7 +1347,6 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
     throw Error(AIMX_E_INVALID_ARG, "bad solve arguments");
   if (RHS == X) throw Error(AIMX_E_INVALID_ARG, "input and output alias");
   if (c->slab || !c->dA) throw Error(AIMX_E_UNSUPPORTED, "aimx_solve needs a one-GPU context");
-  if (c->aim_on) throw Error(AIMX_E_UNSUPPORTED, "aimx_solve runs the AIMx operator (conventional AIM mode is on)");
   for (int64_t i = 0; i < nf; ++i)
     if (!(f_hz[i] > 0.0) || !std::isfinite(f_hz[i])) throw Error(AIMX_E_INVALID_ARG, "bad frequency");
   AIMX_CUDA(cudaSetDevice(c->device));
@@ -1323,7 +1358,7 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
   }
   const bool had = c->freq_set;
   const double f0 = c->f;
-  const int B = sweep_batch(c, 0, nf);
+  const int B = c->aim_on ? 1 : sweep_batch(c, 0, nf);   // conventional AIM: per-frequency near fill
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   for (int64_t i = 0; i < nf; i += B) {
     const int nb_ = (int)std::min<int64_t>(B, nf - i);

@@ -86,6 +86,19 @@ __global__ void k_colscale(int B, int64_t N, const T2* __restrict__ W, const dou
   out[i] = mk<T2>(f * w.x, f * w.y);
 }
 
+// out_b = W_b / sqrt(n_b.x) (0 where n_b.x = 0): the Arnoldi normalisation
+// with the norm left on the device
+template <typename T2>
+__global__ void k_colscale_rsqrt(int B, int64_t N, const T2* __restrict__ W, const double2* __restrict__ n2,
+                                 T2* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * N) return;
+  const double q = n2[i / N].x;
+  const double f = q > 0.0 ? 1.0 / sqrt(q) : 0.0;
+  const double2 w = to_d(W[i]);
+  out[i] = mk<T2>(f * w.x, f * w.y);
+}
+
 // out = a - b
 template <typename T2>
 __global__ void k_sub(int64_t n, const T2* __restrict__ a, const T2* __restrict__ b, T2* __restrict__ out) {
@@ -129,6 +142,11 @@ void gm_lincomb(bool f32, int nv, int B, int64_t N, const void* V, int64_t vstri
 void gm_colscale(bool f32, int B, int64_t N, const void* W, const double* sc, void* out, cudaStream_t s) {
   if (f32) k_colscale<float2><<<nb256(B * N), 256, 0, s>>>(B, N, (const float2*)W, sc, (float2*)out);
   else k_colscale<double2><<<nb256(B * N), 256, 0, s>>>(B, N, (const double2*)W, sc, (double2*)out);
+  AIMX_CHECK_LAUNCH();
+}
+void gm_colscale_rsqrt(bool f32, int B, int64_t N, const void* W, const double2* n2, void* out, cudaStream_t s) {
+  if (f32) k_colscale_rsqrt<float2><<<nb256(B * N), 256, 0, s>>>(B, N, (const float2*)W, n2, (float2*)out);
+  else k_colscale_rsqrt<double2><<<nb256(B * N), 256, 0, s>>>(B, N, (const double2*)W, n2, (double2*)out);
   AIMX_CHECK_LAUNCH();
 }
 void gm_sub(bool f32, int64_t n, const void* a, const void* b, void* out, cudaStream_t s) {

@@ -60,8 +60,17 @@ def test_aim_cfg1(prec, orc1):
     # exclusions, and back to AIMx
     with pytest.raises(AIMxError):
         op.set_linear_term(True)
-    with pytest.raises(AIMxError):
-        op.solve(freqs[:1], to_gpu(X[:1], prec))
+    # GMRES on the conventional-AIM system (one frequency at a time, each with
+    # its near fill): the residual under the ORACLE's AIM operator
+    Xs, its, rr = op.solve(freqs[:2], to_gpu(X[:2], prec), tol=1e-6 if prec == "c128" else 1e-4,
+                           restart=30, maxiter=3000)
+    Xs = Xs.cpu().numpy()
+    for i in range(2):
+        aim.set_frequency(freqs[i])
+        b = gpu_input_as_c128(X[i], prec)
+        res = np.linalg.norm(b - aim.matvec(Xs[i])) / np.linalg.norm(b)
+        assert rr[i] <= (1e-6 if prec == "c128" else 1e-4) * (1 + 1e-6)
+        assert res <= (1e-6 if prec == "c128" else 5e-4)
     op.set_conventional(False)
     op.set_frequency(150e6)
     assert np.array_equal(op.matvec(xg).cpu().numpy(), y_aimx)
