@@ -17,6 +17,8 @@ template <typename T2> __device__ __forceinline__ double2 to_d(const T2& v) { re
 template <typename T2>
 __global__ void k_pc(int B, int64_t N, const T2* __restrict__ in, T2* __restrict__ out, const double* __restrict__ dA,
                      const double* __restrict__ dR, PcArgs pa, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * N) return;
   const int b = (int)(i / N);
@@ -36,6 +38,8 @@ __global__ void k_pc(int B, int64_t N, const T2* __restrict__ in, T2* __restrict
 template <typename T2>
 __global__ void __launch_bounds__(256) k_dots(int64_t N, const T2* __restrict__ V, int64_t vstride,
                                               const T2* __restrict__ W, double2* __restrict__ out, int B) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x, b = blockIdx.y;
   const T2* a = V + v * vstride + (int64_t)b * N;
   const T2* w = W + (int64_t)b * N;
@@ -63,6 +67,8 @@ __global__ void __launch_bounds__(256) k_dots(int64_t N, const T2* __restrict__ 
 template <typename T2>
 __global__ void k_lincomb(int nv, int B, int64_t N, const T2* __restrict__ V, int64_t vstride,
                           const double2* __restrict__ coef, T2* __restrict__ W, int mode) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * N) return;
   const int b = (int)(i / N);
@@ -79,6 +85,8 @@ __global__ void k_lincomb(int nv, int B, int64_t N, const T2* __restrict__ V, in
 // out[b][n] = s[b] * W[b][n]
 template <typename T2>
 __global__ void k_colscale(int B, int64_t N, const T2* __restrict__ W, const double* __restrict__ s, T2* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * N) return;
   const double f = s[i / N];
@@ -91,6 +99,8 @@ __global__ void k_colscale(int B, int64_t N, const T2* __restrict__ W, const dou
 template <typename T2>
 __global__ void k_colscale_rsqrt(int B, int64_t N, const T2* __restrict__ W, const double2* __restrict__ n2,
                                  T2* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * N) return;
   const double q = n2[i / N].x;
@@ -102,6 +112,8 @@ __global__ void k_colscale_rsqrt(int B, int64_t N, const T2* __restrict__ W, con
 // out = a - b
 template <typename T2>
 __global__ void k_sub(int64_t n, const T2* __restrict__ a, const T2* __restrict__ b, T2* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   out[i] = mk<T2>(a[i].x - b[i].x, a[i].y - b[i].y);
@@ -109,6 +121,8 @@ __global__ void k_sub(int64_t n, const T2* __restrict__ a, const T2* __restrict_
 
 // d[m] = src[diag[m]]
 __global__ void k_take(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ src, double* __restrict__ d) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) d[i] = src[idx[i]];
 }
@@ -119,43 +133,43 @@ unsigned nb256(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 void gm_pc(bool f32, int B, int64_t N, const void* in, void* out, const double* dA, const double* dR, const PcArgs& pa,
            bool accumulate, cudaStream_t s) {
-  if (f32) k_pc<float2><<<nb256(B * N), 256, 0, s>>>(B, N, (const float2*)in, (float2*)out, dA, dR, pa, accumulate);
-  else k_pc<double2><<<nb256(B * N), 256, 0, s>>>(B, N, (const double2*)in, (double2*)out, dA, dR, pa, accumulate);
+  if (f32) launch_pdl(k_pc<float2>, dim3(nb256(B * N)), dim3(256), 0, s, B, N, (const float2*)in, (float2*)out, dA, dR, pa, accumulate);
+  else launch_pdl(k_pc<double2>, dim3(nb256(B * N)), dim3(256), 0, s, B, N, (const double2*)in, (double2*)out, dA, dR, pa, accumulate);
   AIMX_CHECK_LAUNCH();
 }
 void gm_dots(bool f32, int nv, int B, int64_t N, const void* V, int64_t vstride, const void* W, double2* out,
              cudaStream_t s) {
   if (nv <= 0) return;
   dim3 g((unsigned)nv, (unsigned)B);
-  if (f32) k_dots<float2><<<g, 256, 0, s>>>(N, (const float2*)V, vstride, (const float2*)W, out, B);
-  else k_dots<double2><<<g, 256, 0, s>>>(N, (const double2*)V, vstride, (const double2*)W, out, B);
+  if (f32) launch_pdl(k_dots<float2>, dim3(g), dim3(256), 0, s, N, (const float2*)V, vstride, (const float2*)W, out, B);
+  else launch_pdl(k_dots<double2>, dim3(g), dim3(256), 0, s, N, (const double2*)V, vstride, (const double2*)W, out, B);
   AIMX_CHECK_LAUNCH();
 }
 void gm_lincomb(bool f32, int nv, int B, int64_t N, const void* V, int64_t vstride, const double2* coef, void* W,
                 bool assign, cudaStream_t s) {
   if (f32)
-    k_lincomb<float2><<<nb256(B * N), 256, 0, s>>>(nv, B, N, (const float2*)V, vstride, coef, (float2*)W, assign);
+    launch_pdl(k_lincomb<float2>, dim3(nb256(B * N)), dim3(256), 0, s, nv, B, N, (const float2*)V, vstride, coef, (float2*)W, assign);
   else
-    k_lincomb<double2><<<nb256(B * N), 256, 0, s>>>(nv, B, N, (const double2*)V, vstride, coef, (double2*)W, assign);
+    launch_pdl(k_lincomb<double2>, dim3(nb256(B * N)), dim3(256), 0, s, nv, B, N, (const double2*)V, vstride, coef, (double2*)W, assign);
   AIMX_CHECK_LAUNCH();
 }
 void gm_colscale(bool f32, int B, int64_t N, const void* W, const double* sc, void* out, cudaStream_t s) {
-  if (f32) k_colscale<float2><<<nb256(B * N), 256, 0, s>>>(B, N, (const float2*)W, sc, (float2*)out);
-  else k_colscale<double2><<<nb256(B * N), 256, 0, s>>>(B, N, (const double2*)W, sc, (double2*)out);
+  if (f32) launch_pdl(k_colscale<float2>, dim3(nb256(B * N)), dim3(256), 0, s, B, N, (const float2*)W, sc, (float2*)out);
+  else launch_pdl(k_colscale<double2>, dim3(nb256(B * N)), dim3(256), 0, s, B, N, (const double2*)W, sc, (double2*)out);
   AIMX_CHECK_LAUNCH();
 }
 void gm_colscale_rsqrt(bool f32, int B, int64_t N, const void* W, const double2* n2, void* out, cudaStream_t s) {
-  if (f32) k_colscale_rsqrt<float2><<<nb256(B * N), 256, 0, s>>>(B, N, (const float2*)W, n2, (float2*)out);
-  else k_colscale_rsqrt<double2><<<nb256(B * N), 256, 0, s>>>(B, N, (const double2*)W, n2, (double2*)out);
+  if (f32) launch_pdl(k_colscale_rsqrt<float2>, dim3(nb256(B * N)), dim3(256), 0, s, B, N, (const float2*)W, n2, (float2*)out);
+  else launch_pdl(k_colscale_rsqrt<double2>, dim3(nb256(B * N)), dim3(256), 0, s, B, N, (const double2*)W, n2, (double2*)out);
   AIMX_CHECK_LAUNCH();
 }
 void gm_sub(bool f32, int64_t n, const void* a, const void* b, void* out, cudaStream_t s) {
-  if (f32) k_sub<float2><<<nb256(n), 256, 0, s>>>(n, (const float2*)a, (const float2*)b, (float2*)out);
-  else k_sub<double2><<<nb256(n), 256, 0, s>>>(n, (const double2*)a, (const double2*)b, (double2*)out);
+  if (f32) launch_pdl(k_sub<float2>, dim3(nb256(n)), dim3(256), 0, s, n, (const float2*)a, (const float2*)b, (float2*)out);
+  else launch_pdl(k_sub<double2>, dim3(nb256(n)), dim3(256), 0, s, n, (const double2*)a, (const double2*)b, (double2*)out);
   AIMX_CHECK_LAUNCH();
 }
 void gm_take(int64_t n, const int64_t* idx, const double* src, double* d, cudaStream_t s) {
-  k_take<<<nb256(n), 256, 0, s>>>(n, idx, src, d);
+  launch_pdl(k_take, dim3(nb256(n)), dim3(256), 0, s, n, idx, src, d);
   AIMX_CHECK_LAUNCH();
 }
 
