@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
   }
   for (int base = e0; base < e1; base += 32) {
     const int nx = base + 32 + lane;
+    const int cnt = e1 - base;   // entries left (the last chunk may be partial)
     int nr = 0;
     T4 nw{0, 0, 0, 0};
     if (nx < e1) {   // next chunk, in flight during this one
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
     }
 #pragma unroll
     for (int jb = 0; jb < PER; jb += QB) {
+      if (jb * NG >= cnt) break;   // warp-uniform: no entry of this batch exists
       VT u[QB];
       T4 w[QB];
 #pragma unroll
