@@ -28,6 +28,8 @@ label) step by step:
                     C_lin = L_lin - W H_lin P on overlapping pairs
                     (eq:linterm P:363, eq:Lmatdecomplin P:386)
 * ``gmres``         restarted GMRES with the static diagonal preconditioner
+* ``kop``           AIMx for the double-layer operator K (eq:opK P:408,
+                    eq:KAIMx P:457; NEXT #1 groundwork, oracle only)
 * ``aim``           the conventional AIM (per-frequency near region and
                     precorrection, eq:aimL P:190, eq:aimLP P:205)
 
@@ -36,5 +38,6 @@ Every reading of a silent/ambiguous/garbled passage is listed in DESIGN.md
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against closed forms, brute force, invariants or
-the paper's printed values.  Parity unpinned: none in this module set.
+the paper's printed values.  Parity unpinned: the SIGN of the residue term
+of ``kop`` (reading R24, exterior limit; nothing in the paper fixes it).
 """

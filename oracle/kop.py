@@ -1,0 +1,332 @@
+"""The double-layer operator K and its AIMx form (oracle).  TEST INFRASTRUCTURE ONLY.
+
+SURVEY 8(f) NEXT #1 groundwork: the oracle side of AIMx for K (the device
+side is not built this round).
+
+R25  the static PV entries use the analytic inner integral with the 7-point
+     outer rule, subdivided 8 x 8 on triangle pairs that touch (the inner
+     field is log-singular along a shared edge), and are symmetrised like the
+     L entries (R9): the exact PV part is symmetric.
+
+P:408  eq:opK        K[X](r) = int_S grad G(r - r') x X(r') dS'
+P:412  eq:ghgf       grad G = -rhat (1 + j k0 r) e^{-j k0 r} / (4 pi r^2),
+                     rhat = (r - r')/r
+P:429  eq:ghgftaylor grad G = -rhat/(4 pi) (1/r^2 - (-j k0)^2/2! - 2 (-j k0)^3 r/3! + ...)
+P:445  eq:ghgfs      grad G_s = -rhat / (4 pi r^2);  eq:ghgfd  grad G_d = grad G - grad G_s
+P:457  eq:KAIMx      K ~= K_s,NR - K_s,P + W^(K) H_grad(k0) P^(K)
+P:463  eq:gH00       self term of H_grad (reading R23)
+P:474  "direct integration ... in a principal value sense, while the
+       self-interactions ... are accounted for with an analytical residue term"
+
+Readings:
+ R23 (AMB-16)  eq:gH00 gives one scalar for a vector kernel; grad G_d has no
+               limit at r = 0 (its direction is rhat).  H_grad(0) = 0 per
+               Cartesian component (the odd symmetry of d_a G); the static
+               H_grad,s(0) = 0 likewise, so near pairs are unaffected.
+ R24           the discrete K (eq:CFIEdis P:424: "the discretized n x n x K
+               operator") tested with f_m, exterior limit:
+                 Kmat[m,n] = int f_m . (n x n x K[f_n])^+ dS
+                           = -int f_m . PV K[f_n] dS  +  1/2 int f_m . (n x f_n) dS
+               (f_m is tangential, so f_m . (n (n . v) - v) = -f_m . v; the
+               residue is n x H^+ = J/2 + n x PV K[J]).  n = outward normal
+               (vertex order).  The residue sign follows this exterior-limit
+               reading; nothing in the paper pins it (parity unpinned for the
+               residue's sign; every other part is pinned).
+
+AIMx for K, channel form: with the current channels g_b = P^b x (b = x, y, z),
+    Phi_c = sum_{a,b} eps_{cab} (H_grad,a (*) g_b),   y_K = -sum_c W^c Phi_c + (K_s,NR - K_s,P) x,
+H_grad,a(delta) = d_a G(k0, r) at r = h delta (the test node minus the source
+node), W = P^T.  Inner integrals of the static part in closed form:
+    int_T (r - r')/R^3 dS' = sum_i m_i f2_i + n sgn(d) Omega,
+with f2_i = ln((R_+ + s_+)/(R_- + s_-)) on edge i and Omega the solid angle
+of T seen from r (the beta sum of the 1/R potential, static_near); and
+(r - r') x (r' - p) = (r - r') x (r - p), so
+    int_T grad G_s(r - r') x c (r' - p) dS' = -(c / 4 pi) Q(r) x (r - p).
+Coplanar contributions vanish: the inner vector is then normal to the plane
+and f_m is tangential.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .kernels import FOUR_PI
+from .mesh import RWG
+from .static_near import RADON7_BARY, RADON7_W, _dot, _logsum, _rwg_triangles
+
+EPS3 = np.zeros((3, 3, 3))
+EPS3[0, 1, 2] = EPS3[1, 2, 0] = EPS3[2, 0, 1] = 1.0
+EPS3[0, 2, 1] = EPS3[2, 1, 0] = EPS3[1, 0, 2] = -1.0
+
+
+def grad_G(k0, rv):
+    """eq:ghgf: grad_r G(r - r') at rv = r - r' (array [..., 3]); 0 at rv = 0."""
+    rv = np.asarray(rv, np.float64)
+    r = np.linalg.norm(rv, axis=-1)
+    z = r == 0.0
+    rr = np.where(z, 1.0, r)
+    f = -(1.0 + 1j * k0 * rr) * np.exp(-1j * k0 * rr) / (FOUR_PI * rr ** 3)
+    return np.where(z[..., None], 0.0, f[..., None] * rv)
+
+
+def grad_G_s(rv):
+    """eq:ghgfs: -rhat/(4 pi r^2) = -rv/(4 pi r^3); 0 at rv = 0."""
+    rv = np.asarray(rv, np.float64)
+    r = np.linalg.norm(rv, axis=-1)
+    z = r == 0.0
+    rr = np.where(z, 1.0, r)
+    return np.where(z[..., None], 0.0, -rv / (FOUR_PI * rr[..., None] ** 3))
+
+
+def grad_G_d(k0, rv):
+    """eq:ghgfd, evaluated without cancellation:
+    grad G_d = -rv/(4 pi r^3) ((1 + j x) e^{-j x} - 1), x = k0 r, with
+    (1 + j x) e^{-j x} - 1 = (cos x + x sin x - 1) + j (x cos x - sin x);
+    0 at rv = 0 (R23)."""
+    rv = np.asarray(rv, np.float64)
+    r = np.linalg.norm(rv, axis=-1)
+    z = r == 0.0
+    rr = np.where(z, 1.0, r)
+    x = k0 * rr
+    s2 = np.sin(0.5 * x)
+    re = -2.0 * s2 * s2 + x * np.sin(x)                 # cos x - 1 + x sin x
+    small = x < 1e-2                                      # x cos x - sin x = -x^3/3 + x^5/30 - ...
+    im = np.where(small, -x ** 3 / 3.0 + x ** 5 / 30.0, x * np.cos(x) - np.sin(x))
+    f = -(re + 1j * im) / (FOUR_PI * rr ** 3)
+    return np.where(z[..., None], 0.0, f[..., None] * rv)
+
+
+def triangle_Q(r, v0, v1, v2):
+    """Q(r) = int_T (r - r')/R^3 dS' over the flat triangle (arrays [..., 3]);
+    principal value in the plane (d = 0)."""
+    e1 = v1 - v0
+    e2 = v2 - v0
+    nrm = np.cross(e1, e2)
+    nhat = nrm / np.linalg.norm(nrm, axis=-1, keepdims=True)
+    d = _dot(r - v0, nhat)
+    # a point in the plane up to rounding is IN the plane: the normal part
+    # jumps by +-2 pi across it and belongs to the residue, not the PV (R24)
+    scale = (np.linalg.norm(e1, axis=-1) + np.linalg.norm(e2, axis=-1))
+    d = np.where(np.abs(d) <= 1e-12 * scale, 0.0, d)
+    rho = r - d[..., None] * nhat
+    ad = np.abs(d)
+    Q = np.zeros(np.broadcast_shapes(r.shape, v0.shape))
+    omega = np.zeros(d.shape)
+    for va, vb in ((v0, v1), (v1, v2), (v2, v0)):
+        ev = vb - va
+        L = np.linalg.norm(ev, axis=-1)
+        shat = ev / L[..., None]
+        mhat = np.cross(shat, nhat)
+        sm = _dot(va - rho, shat)
+        sp_ = _dot(vb - rho, shat)
+        t0 = _dot(va - rho, mhat)
+        R0sq = t0 * t0 + d * d
+        Rm = np.linalg.norm(r - va, axis=-1)
+        Rp = np.linalg.norm(r - vb, axis=-1)
+        live = R0sq > (1e-14 * L) ** 2
+        f2 = np.where(live, _logsum(Rp, sp_, R0sq, live) - _logsum(Rm, sm, R0sq, live), 0.0)
+        hasd = ad > 0.0
+        den_p = np.where(hasd, R0sq + ad * Rp, 1.0)
+        den_m = np.where(hasd, R0sq + ad * Rm, 1.0)
+        beta = np.where(hasd, np.arctan(t0 * sp_ / den_p) - np.arctan(t0 * sm / den_m), 0.0)
+        Q = Q + mhat * f2[..., None]
+        omega = omega + beta
+    return Q + (np.sign(d) * omega)[..., None] * nhat
+
+
+def triangle_normals(V, T):
+    n = np.cross(V[T[:, 1]] - V[T[:, 0]], V[T[:, 2]] - V[T[:, 0]])
+    return n / np.linalg.norm(n, axis=1, keepdims=True)
+
+
+def residue_entries(V, T, rwg: RWG, rows, cols):
+    """1/2 int f_m . (n x f_n) dS over the triangles m and n share (R24);
+    exact for the linear integrand by the 7-point rule."""
+    V = np.asarray(V, np.float64)
+    T = np.asarray(T, np.int64)
+    verts, area, free, coef, div = _rwg_triangles(V, T, rwg)
+    tri = np.stack([rwg.tp, rwg.tm], axis=1)
+    nrm = triangle_normals(V, T)
+    out = np.zeros(len(rows))
+    for i, (m, n) in enumerate(zip(rows, cols)):
+        for sm in range(2):
+            for sn in range(2):
+                if tri[m, sm] != tri[n, sn]:
+                    continue
+                pts = RADON7_BARY @ verts[m, sm]
+                fm = coef[m, sm] * (pts - free[m, sm])
+                fn = coef[n, sn] * (pts - free[n, sn])
+                out[i] += 0.5 * area[m, sm] * np.sum(RADON7_W * _dot(fm, np.cross(nrm[tri[m, sm]], fn)))
+    return out
+
+
+def subdivided_rule(nsub: int):
+    """Barycentric points / weights (sum 1) of the 7-point rule on each of the
+    nsub^2 congruent sub-triangles of the reference triangle."""
+    pts, wts = [], []
+    for i in range(nsub):
+        for j in range(nsub - i):
+            corners = [((i, j), (i + 1, j), (i, j + 1))]
+            if i + j + 1 < nsub:
+                corners.append(((i + 1, j + 1), (i, j + 1), (i + 1, j)))
+            for c in corners:
+                B = np.array([[1.0 - (u + v) / nsub, u / nsub, v / nsub] for u, v in c])   # [3 corners, 3 bary]
+                pts.append(RADON7_BARY @ B)
+                wts.append(RADON7_W / nsub ** 2)
+    return np.concatenate(pts), np.concatenate(wts)
+
+
+def static_K_entries(V, T, rwg: RWG, rows, cols, nsub_touch: int = 8):
+    """PV part of K_s on the listed pairs: -int f_m . int grad G_s x f_n,
+    analytic inner (triangle_Q); outer 7-point rule, subdivided nsub_touch^2
+    times on triangle pairs that touch without coinciding (the inner field is
+    log-singular along a shared edge; reading R25)."""
+    V = np.asarray(V, np.float64)
+    T = np.asarray(T, np.int64)
+    verts, area, free, coef, div = _rwg_triangles(V, T, rwg)
+    tri = np.stack([rwg.tp, rwg.tm], axis=1)
+    rows = np.asarray(rows)
+    cols = np.asarray(cols)
+    K = np.zeros(rows.shape[0])
+    rules = {1: (RADON7_BARY, RADON7_W), nsub_touch: subdivided_rule(nsub_touch)}
+    for sm in range(2):
+        for sn in range(2):
+            tm_, tn_ = tri[rows, sm], tri[cols, sn]
+            touch = np.array([len(set(T[a]) & set(T[b])) > 0 for a, b in zip(tm_, tn_)]) & (tm_ != tn_)
+            for ns, sel in ((1, ~touch), (nsub_touch, touch)):
+                idx = np.flatnonzero(sel & (tm_ != tn_))   # coinciding triangles: PV part 0
+                if idx.size == 0:
+                    continue
+                bary, wb = rules[ns]
+                m, n = rows[idx], cols[idx]
+                rq = np.einsum("qk,pkc->pqc", bary, verts[m, sm])
+                wq = wb[None, :] * area[m, sm][:, None]
+                fm = coef[m, sm][:, None, None] * (rq - free[m, sm][:, None, :])
+                sv = verts[n, sn][:, None, :, :]
+                Q = triangle_Q(rq, sv[..., 0, :], sv[..., 1, :], sv[..., 2, :])
+                inner = -(coef[n, sn] / FOUR_PI)[:, None, None] * np.cross(Q, rq - free[n, sn][:, None, :])
+                K[idx] -= (wq * _dot(fm, inner)).sum(axis=1)
+    return K
+
+
+def _points(V, T, rwg):
+    from .direct import _points as pts
+    return pts(np.asarray(V, np.float64), np.asarray(T, np.int64), rwg)
+
+
+def dynamic_K_dense(V, T, rwg: RWG, k0: float):
+    """-int f_m . int grad G_d x f_n over all pairs, 7 x 7 product rule."""
+    pts, w, f, div = _points(V, T, rwg)
+    N = rwg.n
+    P = pts.reshape(N, 14, 3)
+    W = w.reshape(N, 14)
+    F = f.reshape(N, 14, 3)
+    K = np.zeros((N, N), np.complex128)
+    for m in range(N):
+        g = grad_G_d(k0, P[m][None, :, None, :] - P[:, None, :, :])      # [N, 14, 14, 3]
+        cr = np.cross(g, F[:, None, :, :])                                # grad G_d x f_n(r')
+        K[m] = -np.einsum("i,ic,nijc,nj->n", W[m], F[m], cr, W)
+    return K
+
+
+def static_K_dense(V, T, rwg: RWG):
+    """Symmetrised PV part of K_s over all pairs (the exact one is symmetric:
+    grad G_s is odd and a . (b x c) = -c . (b x a); reading R25)."""
+    N = rwg.n
+    m, n = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    K = static_K_entries(V, T, rwg, m.ravel(), n.ravel()).reshape(N, N)
+    return 0.5 * (K + K.T)
+
+
+class DirectK:
+    """Dense direct-integration Kmat (R24): static PV part analytic-inner,
+    dynamic part 7 x 7, plus the residue."""
+
+    def __init__(self, V, T, rwg: RWG):
+        self.V = np.asarray(V, np.float64)
+        self.T = np.asarray(T, np.int64)
+        self.rwg = rwg
+        N = rwg.n
+        self.Ks = static_K_dense(self.V, self.T, rwg)
+        m, n = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+        self.Res = residue_entries(self.V, self.T, rwg, m.ravel(), n.ravel()).reshape(N, N)
+
+    def set_frequency(self, k0: float):
+        self.k0 = k0
+        self.K = self.Ks + dynamic_K_dense(self.V, self.T, self.rwg, k0) + self.Res
+
+
+# ---------------------------------------------------------------- AIMx for K
+def gradient_kernel_samples(n: tuple, h: float, k0: float | None):
+    """H_grad,a on the padded grid [2Nz, 2Ny, 2Nx] (wrap slot 0, R10): d_a G at
+    r = h * offset (k0 None: the static kernel).  Returns [3, ...] (a = x, y, z)."""
+    offs = []
+    wrap = []
+    for N in (n[2], n[1], n[0]):
+        i = np.arange(2 * N)
+        offs.append(np.where(i < N, i, i - 2 * N))
+        wrap.append(i == N)
+    oz, oy, ox = np.meshgrid(*offs, indexing="ij")
+    wz, wy, wx = np.meshgrid(*wrap, indexing="ij")
+    rv = h * np.stack([ox, oy, oz], axis=-1).astype(np.float64)
+    g = grad_G_s(rv) if k0 is None else grad_G(k0, rv)
+    g[wz | wy | wx] = 0.0
+    return np.moveaxis(g, -1, 0)
+
+
+def grid_K(op, x, k0: float):
+    """-sum_c W^c sum_{a,b} eps_cab (H_grad,a (*) P^b x) on the op's grid."""
+    import scipy.fft as sfft
+    Nx, Ny, Nz = op.grid.n
+    g = np.stack([(op.P[b] @ x).reshape(Nz, Ny, Nx) for b in range(3)])
+    G = sfft.fftn(g, s=(2 * Nz, 2 * Ny, 2 * Nx), axes=(-3, -2, -1))
+    Hh = sfft.fftn(gradient_kernel_samples(op.grid.n, op.grid.h, k0), axes=(-3, -2, -1))
+    y = np.zeros(op.N, np.complex128)
+    for c in range(3):
+        acc = np.zeros_like(G[0])
+        for a in range(3):
+            for b in range(3):
+                if EPS3[c, a, b] != 0.0:
+                    acc += EPS3[c, a, b] * Hh[a] * G[b]
+        phi = sfft.ifftn(acc)[:Nz, :Ny, :Nx]
+        y -= op.P[c].T @ phi.ravel()
+    return y
+
+
+def K_precorrection_entries(Lam, A, rows, cols, order: int, h: float):
+    """K_s,P on the listed pairs: -sum_{c,a,b} eps_cab Lam^c_m B^a_D Lam^b_n,
+    B^a_D[s, s'] = d_a G_s(h (s - s' - D))."""
+    from .precorrection import stencil_offsets
+    off = stencil_offsets(order)
+    out = np.zeros(len(rows))
+    for i, (m, n) in enumerate(zip(rows, cols)):
+        D = A[n] - A[m]
+        delta = off[:, None, :] - off[None, :, :] - D[None, None, :]
+        B = grad_G_s(h * delta.astype(np.float64))                   # [p3, p3, 3]
+        t = 0.0
+        for c in range(3):
+            for a in range(3):
+                for b in range(3):
+                    if EPS3[c, a, b] != 0.0:
+                        t += EPS3[c, a, b] * Lam[m, c] @ B[..., a] @ Lam[n, b]
+        out[i] = -t
+    return out
+
+
+class AIMxK:
+    """eq:KAIMx on top of an AIMxOracle (same grid, weights, near pattern)."""
+
+    def __init__(self, op):
+        self.op = op
+        from .static_near import symmetrize
+        rows = np.repeat(np.arange(op.N), np.diff(op.rowptr))
+        ks = symmetrize(op.rowptr, op.col, static_K_entries(op.V, op.T, op.rwg, rows, op.col))
+        res = residue_entries(op.V, op.T, op.rwg, rows, op.col)
+        kp = K_precorrection_entries(op.Lam, op.A, rows, op.col, op.order, op.grid.h)
+        import scipy.sparse as sp
+        self.C = sp.csr_matrix((ks + res - kp, op.col, op.rowptr), shape=(op.N, op.N))
+
+    def matvec(self, x, k0: float):
+        x = np.asarray(x, np.complex128)
+        return self.C @ x + grid_K(self.op, x, k0)

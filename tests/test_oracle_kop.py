@@ -1,0 +1,161 @@
+"""Pins for oracle/kop.py (AIMx for the double-layer operator K, P:400-474;
+SURVEY 8(f) NEXT #1 groundwork, oracle only this round).
+
+* grad G against central differences of G (eq:ghgf) and the paper's Taylor
+  coefficients (eq:ghgftaylor); grad G_d against grad G - grad G_s;
+* the closed-form Q(r) = int (r - r')/R^3 against Duffy quadrature;
+* the static PV entries of far pairs against a 7 x 7 product rule, and the
+  symmetry of the exact PV part (the antisymmetric quadrature error shrinks
+  under refinement);
+* the residue term: antisymmetric, zero on the diagonal;
+* K_s,P against the dense definition with explicit grid matrices;
+* the grid convolution against the dense O(N_g^2) sum;
+* AIMx K against the dense direct K on a closed icosphere (rel-L2 <= 1e-2).
+"""
+import numpy as np
+import pytest
+
+import aimx_inputs as inp
+from oracle.kernels import G
+from oracle.kop import (EPS3, AIMxK, DirectK, K_precorrection_entries, grad_G, grad_G_d, grad_G_s, grid_K,
+                        residue_entries, static_K_entries, triangle_Q)
+
+
+@pytest.fixture(scope="module")
+def sph():
+    from oracle.aimx import AIMxOracle
+    m = inp.icosphere_mesh(1, radius=0.5)
+    return AIMxOracle(m.vertices, m.triangles, (8, 8, 8))
+
+
+def test_grad_G_vs_central_differences():
+    k0 = 3.0
+    rv = np.random.default_rng(0).standard_normal((6, 3)) * 0.4
+    e = 1e-6
+    fd = np.stack([(G(k0, np.linalg.norm(rv + e * np.eye(3)[a], axis=-1))
+                    - G(k0, np.linalg.norm(rv - e * np.eye(3)[a], axis=-1))) / (2 * e) for a in range(3)], -1)
+    assert np.abs(grad_G(k0, rv) - fd).max() <= 1e-8 * np.abs(fd).max()
+    assert np.abs(grad_G_d(k0, rv) - (grad_G(k0, rv) - grad_G_s(rv))).max() <= 1e-13 * np.abs(fd).max()
+
+
+@pytest.mark.parametrize("k0,r", [(2.0, 1e-2), (5.0, 3e-3)])
+def test_grad_G_taylor(k0, r):
+    # eq:ghgftaylor: grad G = -rhat/(4 pi) (1/r^2 - (-j k0)^2/2! - 2 (-j k0)^3 r/3! + O(r^2))
+    rhat = np.array([0.6, 0.0, 0.8])
+    g = grad_G(k0, r * rhat)
+    series = -(1 / r ** 2 - (-1j * k0) ** 2 / 2 - 2 * (-1j * k0) ** 3 * r / 6) / (4 * np.pi)
+    assert np.allclose(g, series * rhat, rtol=(k0 * r) ** 2, atol=0)
+    gd = grad_G_d(k0, r * rhat)                          # the frequency-dependent terms only
+    assert np.allclose(gd, (series + 1 / (4 * np.pi * r * r)) * rhat, rtol=(k0 * r) ** 2 * 10, atol=0)
+
+
+def _duffy(r, v0, v1, v2, f, q):
+    x, w = np.polynomial.legendre.leggauss(q)
+    x = 0.5 * (x + 1)
+    w = 0.5 * w
+    n = np.cross(v1 - v0, v2 - v0)
+    n /= np.linalg.norm(n)
+    rho = r - np.dot(r - v0, n) * n
+    tot = 0.0
+    for a, b in ((v0, v1), (v1, v2), (v2, v0)):
+        a2 = np.dot(np.cross(a - rho, b - rho), n)
+        U, Vv = np.meshgrid(x, x, indexing="ij")
+        W = np.outer(w, w) * U * a2
+        P = rho + U[..., None] * ((a - rho) + Vv[..., None] * (b - a))
+        tot = tot + np.tensordot(W, f(P, r), axes=([0, 1], [0, 1]))
+    return tot
+
+
+@pytest.mark.parametrize("r", [[0.4, 0.3, 0.5], [2.0, 1.0, 0.3], [0.4, 0.35, 0.05], [-0.5, 0.2, 0.01],
+                               [1.5, 1.5, 0.0]])
+def test_Q_vs_duffy(r):
+    v0, v1, v2 = np.array([0.0, 0, 0]), np.array([1.0, 0.1, 0]), np.array([0.3, 0.9, 0.05])
+    r = np.array(r)
+    q = triangle_Q(r[None], v0[None], v1[None], v2[None])[0]
+    ref = _duffy(r, v0, v1, v2, lambda P, x: (x - P) / np.linalg.norm(x - P, axis=-1)[..., None] ** 3, 200)
+    assert np.linalg.norm(q - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_static_far_pairs_vs_product_rule_and_symmetry(sph):
+    from oracle.direct import _points
+    op = sph
+    pts, w, f, div = _points(op.V, op.T, op.rwg)
+    P, W, F = pts.reshape(op.N, 14, 3), w.reshape(op.N, 14), f.reshape(op.N, 14, 3)
+
+    def prod(a, b):
+        g = grad_G_s(P[a][:, None, :] - P[b][None, :, :])
+        return -np.einsum("i,ic,ijc,j->", W[a], F[a], np.cross(g, F[b][None, :, :]), W[b])
+    far = [(0, 100), (7, 60), (30, 111)]
+    for a, b in far:
+        k = static_K_entries(op.V, op.T, op.rwg, [a, b], [b, a])
+        assert k[0] == pytest.approx(prod(a, b), rel=1e-4)
+        assert k[1] == pytest.approx(k[0], rel=1e-4)                 # symmetric
+    # touching pairs: the antisymmetric part is quadrature error; refinement shrinks it
+    N = op.N
+    rows = np.repeat(np.arange(N), np.diff(op.rowptr))
+    errs = []
+    for ns in (1, 8):
+        k = static_K_entries(op.V, op.T, op.rwg, rows, op.col, nsub_touch=ns)
+        from oracle.static_near import transpose_perm
+        kt = k[transpose_perm(op.rowptr, op.col)]
+        errs.append(np.linalg.norm(k - kt) / np.linalg.norm(k))
+    assert errs[1] < 0.3 * errs[0]
+
+
+def test_residue_antisymmetric(sph):
+    op = sph
+    N = op.N
+    m, n = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    R = residue_entries(op.V, op.T, op.rwg, m.ravel(), n.ravel()).reshape(N, N)
+    assert np.abs(R + R.T).max() <= 1e-14 * np.abs(R).max()
+    assert np.abs(np.diag(R)).max() <= 1e-14 * np.abs(R).max() and np.count_nonzero(R) > 0
+
+
+def test_K_precorrection_vs_dense_definition(sph):
+    op = sph
+    g = op.grid
+    idx = np.arange(g.ng)
+    ijk = np.stack([idx % g.n[0], (idx // g.n[0]) % g.n[1], idx // (g.n[0] * g.n[1])], axis=1)
+    Hg = grad_G_s(g.h * (ijk[:, None, :] - ijk[None, :, :]).astype(float))      # [Ng, Ng, 3]
+    Pd = [op.P[c].toarray() for c in range(3)]
+    M = np.zeros((op.N, op.N))
+    for c in range(3):
+        for a in range(3):
+            for b in range(3):
+                if EPS3[c, a, b]:
+                    M -= EPS3[c, a, b] * Pd[c].T @ Hg[..., a] @ Pd[b]
+    rows = np.repeat(np.arange(op.N), np.diff(op.rowptr))
+    kp = K_precorrection_entries(op.Lam, op.A, rows, op.col, op.order, g.h)
+    assert np.abs(kp - M[rows, op.col]).max() <= 1e-12 * np.abs(M).max()
+
+
+def test_grid_K_vs_dense_sum(sph):
+    op = sph
+    k0 = 2 * np.pi * 1.5e8 / 299792458.0
+    g = op.grid
+    idx = np.arange(g.ng)
+    ijk = np.stack([idx % g.n[0], (idx // g.n[0]) % g.n[1], idx // (g.n[0] * g.n[1])], axis=1)
+    Hg = grad_G(k0, g.h * (ijk[:, None, :] - ijk[None, :, :]).astype(float))
+    x = np.random.default_rng(1).standard_normal(op.N) * (1 + 0.5j)
+    Pd = [op.P[c].toarray() for c in range(3)]
+    y = np.zeros(op.N, complex)
+    for c in range(3):
+        for a in range(3):
+            for b in range(3):
+                if EPS3[c, a, b]:
+                    y -= EPS3[c, a, b] * Pd[c].T @ (Hg[..., a] @ (Pd[b] @ x))
+    yk = grid_K(op, x, k0)
+    assert np.linalg.norm(yk - y) <= 1e-12 * np.linalg.norm(y)
+
+
+def test_aimx_K_vs_direct(sph):
+    op = sph
+    d = DirectK(op.V, op.T, op.rwg)
+    ak = AIMxK(op)
+    rng = np.random.default_rng(4)
+    for f in (50e6, 150e6):
+        k0 = 2 * np.pi * f / 299792458.0
+        d.set_frequency(k0)
+        for _ in range(3):
+            x = rng.standard_normal(op.N) + 1j * rng.standard_normal(op.N)
+            assert np.linalg.norm(ak.matvec(x, k0) - d.K @ x) <= 1e-2 * np.linalg.norm(d.K @ x)
