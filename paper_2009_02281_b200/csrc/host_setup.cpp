@@ -381,7 +381,12 @@ void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, N
         }
       }
       const double Ue = (double)U * (double)ngrp / (double)std::max<int64_t>(ns, 1);
-      const double cost = Ue * (4.0 + 8.0 * R) / 6.0 + Ue * R * 48.0 / 18.0 + Ue * 128.0 / 18.0;
+      // Morton order keeps the gathered x / potential rows of a CTA's groups
+      // local in 2-D and 3-D, which the union size does not see: measured,
+      // it wins whenever its union is within ~4% (cfg3, cfg5), not at 5%
+      // (cfg2's strips)
+      const double cost = (Ue * (4.0 + 8.0 * R) / 6.0 + Ue * R * 48.0 / 18.0 + Ue * 128.0 / 18.0) *
+                          (kind == 1 ? 0.96 : 1.0);
       if (cost < best) { best = cost; best_kind = kind; best_R = R; }
     }
   }
