@@ -269,6 +269,7 @@ struct HotDev {
   void* ent_w = nullptr;         // [nent] real4
   int32_t* line_id = nullptr;    // [nlines] y + Ny z
   int32_t* zplanes = nullptr;    // [nzocc]
+  int zplane0 = 0;               // the first occupied z plane (the z pass's one-plane form)
   uint8_t* line_occ = nullptr;   // [Ny*Nz]
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)

@@ -328,6 +328,7 @@ void build_gather(aimx_ctx* c, HotDev& h, const NodeMap& m) {
   h.ent_rwg = dupload(c, m.ent_rwg);
   h.line_id = dupload(c, m.line_id);
   h.zplanes = dupload(c, m.zplanes);
+  h.zplane0 = m.zplanes.empty() ? 0 : m.zplanes[0];
   h.line_occ = dupload(c, m.line_occ);
   std::vector<uint8_t> zo(t.n[2], 0);
   for (int z : m.zplanes) zo[z] = 1;
@@ -752,6 +753,7 @@ void do_setup_slab(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc
     hc.kx0 = R.kx0;
     hc.nzocc = (int)full.zplanes.size();
     hc.zplanes = dupload(c, full.zplanes);
+    hc.zplane0 = full.zplanes.empty() ? 0 : full.zplanes[0];
     hc.zocc = dupload(c, zo);
     hc.line_occ = dupload(c, full.line_occ);
     hc.batch = slots;

@@ -1010,8 +1010,45 @@ void run_y(const HotDev& h, bool inv, int B, cudaStream_t s) {
   AIMX_CHECK_LAUNCH();
 }
 
+// ---- z conv with ONE occupied z plane z0 (planar meshes, e.g. cfg5): the
+// potentials are only needed on z0 (the inverse passes read occupied planes
+// only), and for a single non-zero input the z forward * H_hat * z inverse at
+// z0 collapses exactly to a multiply by the kernel's z-sum,
+//   phi(z0) = v(z0) * sum_{kz < 2N_z} H_hat(kz) / M
+//           = v(z0) * (H(0) + H(N_z) + 2 sum_{0 < kz < N_z} H(kz))   (octant, H even in kz).
+// One thread per (ky, kx) and its 4 channel columns, in place on bufB.
+template <typename T>
+__global__ void k_zconv_plane(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  const int W = h.W, Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny, W4 = W / 4;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)Ny2 * W4) return;
+  const int ky = (int)(i / W4), kxl = (int)(i - (int64_t)ky * W4);
+  const int b = blockIdx.y;
+  const int kx = h.kx0 + kxl;
+  const int kxf = kx <= Nx ? kx : 2 * Nx - kx, kyf = ky <= Ny ? ky : Ny2 - ky;
+  const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH + (int64_t)kyf * (Nz + 1) * (Nx + 1) + kxf;
+  T2 f = Hb[0];
+  T2 mid = mk<T2>(0, 0);
+  for (int kz = 1; kz < Nz; ++kz) mid = cadd(mid, Hb[(int64_t)kz * (Nx + 1)]);
+  const T2 last = Hb[(int64_t)Nz * (Nx + 1)];
+  f.x += last.x + 2 * mid.x;
+  f.y += last.y + 2 * mid.y;
+  T2* __restrict__ g = (T2*)h.bufB + b * h.sB + (int64_t)h.zplane0 * Ny2 * W + (int64_t)ky * W + 4 * kxl;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) g[c] = cmul(g[c], f);
+}
+
 template <typename T, int L>
 void run_z(const HotDev& h, int B, cudaStream_t s) {
+  if (h.nzocc == 1) {
+    const int64_t n = (int64_t)2 * h.Ny * (h.W / 4);
+    launch_pdl(k_zconv_plane<T>, dim3((unsigned)((n + 255) / 256), (unsigned)B), dim3(256), 0, s, h);
+    AIMX_CHECK_LAUNCH();
+    return;
+  }
   // + two spectrum slabs: NL lines x L / 4 complex (RPC * L * CW / 4) each
   constexpr size_t sm = pass_smem<T, L>() + 2 * sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
   dim3 g = col_grid<T, L>(h.W, 2 * h.Ny, B);

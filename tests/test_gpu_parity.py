@@ -323,3 +323,26 @@ def test_matvec_graph_replay_bit_identical(prec, monkeypatch):
             for o in outs:
                 for u, v in zip(o, ref):
                     assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+@pytest.mark.parametrize("world", [1, 2])
+def test_planar_single_plane_z_pass(prec, world):
+    """A planar mesh occupies ONE z plane; on a grid whose y transform is too
+    long for the fused y/z kernel the z pass takes its one-plane form (a
+    multiply by the kernel's z-sum).  Against the oracle, single context and
+    emulated slab ranks (kx-slab offsets)."""
+    from oracle.aimx import AIMxOracle
+    m = inp.make_mesh(1)
+    n = (16, 32, 4)
+    orc = AIMxOracle(m.vertices, m.triangles, n)
+    op = make_gpu_op(m, n, prec, slab=None if world == 1 else ("emulate", world))
+    assert op.stats()["occupied_planes"] == 1
+    for f in (150e6, 600e6):
+        op.set_frequency(f)
+        orc.set_frequency(f)
+        x = inp.rhs_vector(1, 8, op.N)
+        yA, yP = op.matvec_parts(to_gpu(x, prec))
+        oA, oR = orc.parts(gpu_input_as_c128(x, prec))
+        assert rel_l2(yA.cpu().numpy(), oA) <= TOL[prec]
+        assert rel_l2(yP.cpu().numpy(), -oR) <= TOL[prec]
