@@ -294,6 +294,39 @@ def grid_K(op, x, k0: float):
     return y
 
 
+def radial_F_samples(n: tuple, h: float, k0: float):
+    """F(r) = (1 + j k0 r) e^{-j k0 r} / (4 pi r^3) at r = h |offset| on the
+    padded grid (0 at offset 0 and on the wrap slots): grad G(r) = -r F(r)."""
+    from .convolution import padded_distances
+    r, wrap = padded_distances(n, h)
+    F = np.zeros(r.shape, np.complex128)
+    nz = (r > 0) & ~wrap
+    F[nz] = (1.0 + 1j * k0 * r[nz]) * np.exp(-1j * k0 * r[nz]) / (FOUR_PI * r[nz] ** 3)
+    return F
+
+
+def grid_K_radial(op, x, k0: float):
+    """The same grid operator as grid_K through the EVEN radial kernel F only:
+    with node coordinates s (in cells),
+        sum_{a,b} eps_cab (d_a G (*) J_b) = -h [ s x (F (*) J) - F (*) (s x J) ]_c,
+    because d_a G(h delta) = -h delta_a F(h |delta|) and
+    sum_s' (s - s')_a F(s - s') J(s') = s_a (F (*) J)(s) - (F (*) (s_a J))(s).
+    (the planned device form of NEXT #1.)"""
+    import scipy.fft as sfft
+    Nx, Ny, Nz = op.grid.n
+    J = np.stack([(op.P[b] @ x).reshape(Nz, Ny, Nx) for b in range(3)])
+    kz, ky, kx = np.meshgrid(np.arange(Nz), np.arange(Ny), np.arange(Nx), indexing="ij")
+    S = np.stack([kx, ky, kz]).astype(np.float64)                    # node coordinates s (x, y, z)
+    SxJ = np.cross(S, J, axis=0)
+    Fh = sfft.fftn(radial_F_samples(op.grid.n, op.grid.h, k0))
+
+    def conv(g):
+        G_ = sfft.fftn(g, s=(2 * Nz, 2 * Ny, 2 * Nx), axes=(-3, -2, -1))
+        return sfft.ifftn(G_ * Fh, axes=(-3, -2, -1))[..., :Nz, :Ny, :Nx]
+    Phi = -op.grid.h * (np.cross(S, conv(J), axis=0) - conv(SxJ))
+    return -sum(op.P[c].T @ Phi[c].ravel() for c in range(3))
+
+
 def K_precorrection_entries(Lam, A, rows, cols, order: int, h: float):
     """K_s,P on the listed pairs: -sum_{c,a,b} eps_cab Lam^c_m B^a_D Lam^b_n,
     B^a_D[s, s'] = d_a G_s(h (s - s' - D))."""

@@ -159,3 +159,15 @@ def test_aimx_K_vs_direct(sph):
         for _ in range(3):
             x = rng.standard_normal(op.N) + 1j * rng.standard_normal(op.N)
             assert np.linalg.norm(ak.matvec(x, k0) - d.K @ x) <= 1e-2 * np.linalg.norm(d.K @ x)
+
+
+def test_grid_K_through_the_radial_kernel(sph):
+    # the planned device form: the curl of the gradient-kernel
+    # convolution from two even-kernel convolutions, J and s x J
+    from oracle.kop import grid_K_radial
+    op = sph
+    x = np.random.default_rng(6).standard_normal(op.N) * (1 - 0.3j)
+    for f in (30e6, 300e6):
+        k0 = 2 * np.pi * f / 299792458.0
+        a, b = grid_K(op, x, k0), grid_K_radial(op, x, k0)
+        assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(a)
