@@ -245,6 +245,11 @@ aimx_status aimx_get_static(const aimx_ctx* ctx, double* CA, double* Crho,
  * C^A_lin, C^rho_lin [N_b][5] as stored (compute precision, widened to fp64).
  * Any pointer may be NULL. */
 aimx_status aimx_get_linear_entries(const aimx_ctx* ctx, int32_t* cols, double* CA_lin, double* Crho_lin);
+/* Double-layer operator K, static near part (SURVEY 8(f) NEXT #1 groundwork;
+ * sec:methods:K P:400-474, readings R23-R25): CK[nnz] (fp64, CSR order) =
+ * sym(K_s,PV) + 1/2 int f_m . (n x f_n) - K_s,P, computed on the device on
+ * demand (the K matvec itself is not built yet).  One-GPU contexts only. */
+aimx_status aimx_get_K_static(aimx_ctx* ctx, double* CK);
 /* Projection weights (fp64) lam[N_b][4][(n+1)^3], channels (x, y, z, rho),
  * node s = i + (n+1)(j + (n+1) k). */
 aimx_status aimx_get_weights(const aimx_ctx* ctx, double* lam);

@@ -168,6 +168,11 @@ void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 // order), fp64 arithmetic, stored in the compute precision (float2 / double2).
 void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, void* DA, void* DR, cudaStream_t s);
 
+// ---------------------------------------------------------------- double-layer operator K (NEXT #1)
+// C_K = sym(K_s,PV) + residue - K_s,P on the near CSR pattern (fp64; oracle/kop.py,
+// readings R23-R25).  Needs d.side, d.T, d.tp, d.tm.
+void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s);
+
 // ---------------------------------------------------------------- linear-term modification
 // P:382-398 (sec:methods:aimx:acc): k0^2 G_lin, G_lin = -r/(8 pi) (eq:linterm
 // P:365), by direct integration on overlapping pairs only (supports share a

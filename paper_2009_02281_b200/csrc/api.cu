@@ -1829,6 +1829,27 @@ aimx_status aimx_get_linear_entries(const aimx_ctx* cc, int32_t* cols, double* C
   AIMX_API_END(c)
 }
 
+aimx_status aimx_get_K_static(aimx_ctx* c, double* CK) {
+  if (!c || !CK) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (c->slab) throw Error(AIMX_E_UNSUPPORTED, "one-GPU contexts only");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  ensure_side(c);
+  if (!c->sd.T) {
+    c->sd.T = dupload(c, c->topo.T);
+  }
+  const int64_t nnz = c->topo.rowptr[c->topo.nb];
+  double* d = nullptr;
+  AIMX_CUDA(cudaMalloc(&d, (size_t)std::max<int64_t>(nnz, 1) * sizeof(double)));
+  std::unique_ptr<double, decltype(&cudaFree)> guard(d, &cudaFree);
+  launch_K_static(c->topo, c->sd, d, c->stream);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  AIMX_CUDA(cudaMemcpy(CK, d, (size_t)nnz * sizeof(double), cudaMemcpyDeviceToHost));
+  AIMX_API_END(c)
+}
+
 aimx_status aimx_get_weights(const aimx_ctx* cc, double* lam) {
   aimx_ctx* c = const_cast<aimx_ctx*>(cc);
   if (!c || !lam) return AIMX_E_INVALID_ARG;

@@ -515,6 +515,169 @@ __global__ void k_aim_fill(int nb, int order, double k0, const int64_t* __restri
   }
 }
 
+// ---- the double-layer operator K, static near part (
+// oracle/kop.py, readings R23-R25): C_K = sym(K_s,PV) + residue - K_s,P.
+// Q(r) = int_T (r - r')/R^3 dS' = sum_i m_i f2_i + n sgn(d) Omega (in-plane
+// points up to rounding are in-plane: the +-2 pi jump is the residue's).
+__device__ __forceinline__ Vec3 k_q(const Frame& F, Vec3 r) {
+  double d = dot(r - F.v[0], F.n);
+  if (fabs(d) <= 1e-12 * (F.L[0] + F.L[2])) d = 0.0;
+  const Vec3 rho = r - d * F.n;
+  const double ad = fabs(d);
+  Vec3 Q = {0.0, 0.0, 0.0};
+  double omega = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    Vec3 va = F.v[k], vb = F.v[(k + 1) % 3];
+    double sm = dot(va - rho, F.sh[k]);
+    double sp = dot(vb - rho, F.sh[k]);
+    double t0 = dot(va - rho, F.mh[k]);
+    double R0sq = t0 * t0 + d * d;
+    double Rm = norm(r - va), Rp = norm(r - vb);
+    double lim = 1e-14 * F.L[k];
+    double f2 = 0.0;
+    if (R0sq > lim * lim) f2 = logsum(Rp, sp, R0sq) - logsum(Rm, sm, R0sq);
+    if (ad > 0.0) omega += atan(t0 * sp / (R0sq + ad * Rp)) - atan(t0 * sm / (R0sq + ad * Rm));
+    Q = Q + f2 * F.mh[k];
+  }
+  const double sg = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0);
+  return Q + (sg * omega) * F.n;
+}
+
+// barycentric point q of the 7-point rule on sub-triangle t of an nsub x nsub
+// subdivision (t < nsub^2; weight = radon weight / nsub^2)
+__device__ __forceinline__ void sub_point(int nsub, int t, int q, double& b0, double& b1, double& b2, double& w) {
+  // sub-triangles enumerated as in oracle kop.subdivided_rule: for i, for j < nsub - i:
+  // the "up" triangle, then (if i + j + 1 < nsub) the "down" one
+  int i = 0, j = 0, down = 0, c = 0;
+  for (i = 0; i < nsub; ++i) {
+    for (j = 0; j < nsub - i; ++j) {
+      if (c == t) { down = 0; goto found; }
+      ++c;
+      if (i + j + 1 < nsub) {
+        if (c == t) { down = 1; goto found; }
+        ++c;
+      }
+    }
+  }
+found:
+  double u0, v0, u1, v1, u2, v2;
+  if (!down) { u0 = i; v0 = j; u1 = i + 1; v1 = j; u2 = i; v2 = j + 1; }
+  else { u0 = i + 1; v0 = j + 1; u1 = i; v1 = j + 1; u2 = i + 1; v2 = j; }
+  double c0, c1, c2, wq;
+  radon7(q, c0, c1, c2, wq);
+  const double u = (c0 * u0 + c1 * u1 + c2 * u2) / nsub, v = (c0 * v0 + c1 * v1 + c2 * v2) / nsub;
+  b0 = 1.0 - u - v;
+  b1 = u;
+  b2 = v;
+  w = wq / ((double)nsub * nsub);
+}
+
+// Warp per row m, lanes over its near entries: the unsymmetrised PV part of
+// K_s (outer rule subdivided 8 x 8 on touching triangle pairs) and the
+// residue 1/2 int f_m . (n x f_n) on shared triangles.
+__global__ void k_K_near_un(int nb, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                            const double* __restrict__ side, const int32_t* __restrict__ T,
+                            const int32_t* __restrict__ tp, const int32_t* __restrict__ tm,
+                            double* __restrict__ Kun, double* __restrict__ Res) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= nb) return;
+  const int m = (int)warp;
+  const double inv4pi = 1.0 / (4.0 * kPi);
+  for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
+    const int n = col[k];
+    double kv = 0.0, rv = 0.0;
+    for (int sm = 0; sm < 2; ++sm) {
+      const double* om = side + (2 * (int64_t)m + sm) * kSideStride;
+      const int trm = sm ? tm[m] : tp[m];
+      const Vec3 a = v3(om), b = v3(om + 3), c = v3(om + 6), pm = v3(om + 9);
+      const double coef_m = om[12], area_m = om[14];
+      for (int sn = 0; sn < 2; ++sn) {
+        const double* on = side + (2 * (int64_t)n + sn) * kSideStride;
+        const int trn = sn ? tm[n] : tp[n];
+        const Vec3 pn = v3(on + 9);
+        const double coef_n = on[12];
+        if (trm == trn) {   // residue on the shared triangle (7-point rule exact)
+          Vec3 nn = cross(b - a, c - a);
+          nn = (1.0 / norm(nn)) * nn;
+          for (int q = 0; q < 7; ++q) {
+            double b0, b1, b2, w;
+            radon7(q, b0, b1, b2, w);
+            const Vec3 r = b0 * a + b1 * b + b2 * c;
+            rv += 0.5 * w * area_m * dot(coef_m * (r - pm), cross(nn, coef_n * (r - pn)));
+          }
+          continue;        // coinciding triangles: PV part 0
+        }
+        bool touch = false;
+        for (int u = 0; u < 3; ++u)
+          for (int v = 0; v < 3; ++v) touch = touch || (T[3 * trm + u] == T[3 * trn + v]);
+        Frame F;
+        make_frame(on, F);
+        const int nsub = touch ? 8 : 1, nt = nsub * nsub;
+        double acc = 0.0;
+        for (int t = 0; t < nt; ++t)
+          for (int q = 0; q < 7; ++q) {
+            double b0, b1, b2, w;
+            if (nsub == 1) radon7(q, b0, b1, b2, w);
+            else sub_point(nsub, t, q, b0, b1, b2, w);
+            const Vec3 r = b0 * a + b1 * b + b2 * c;
+            const Vec3 Q = k_q(F, r);
+            const Vec3 inner = (-coef_n * inv4pi) * cross(Q, r - pn);
+            acc += w * dot(coef_m * (r - pm), inner);
+          }
+        kv -= area_m * acc;
+      }
+    }
+    Kun[k] = kv;
+    Res[k] = rv;
+  }
+}
+
+__constant__ double c_gk_tab[3 * 2197];   // d_a G_s(h delta) for |delta_i| <= 6: [(dz+6)*169 + (dy+6)*13 + (dx+6)][a]
+
+// Warp per row: C_K = (Kun + Kun^T)/2 + Res - K_s,P, K_s,P[m,n] = -sum_{c,a,b}
+// eps_cab Lambda^c_m B^a_D Lambda^b_n, B^a_D[s,s'] = d_a G_s(h (s - s' - D)).
+__global__ void k_K_combine(int nb, int order, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                            const int32_t* __restrict__ anchor, const double* __restrict__ lam,
+                            const double* __restrict__ Kun, const double* __restrict__ Res,
+                            double* __restrict__ CK) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= nb) return;
+  const int m = (int)warp;
+  const int p = order + 1, p3 = p * p * p;
+  const double* lm = lam + (int64_t)m * p3 * 4;
+  for (int64_t k = rowptr[m] + lane; k < rowptr[m + 1]; k += 32) {
+    const int n = col[k];
+    int64_t lo = rowptr[n], hi = rowptr[n + 1] - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < m) lo = mid + 1; else hi = mid;
+    }
+    const double ks = 0.5 * (Kun[k] + Kun[lo]);
+    const int Dx = anchor[3 * n] - anchor[3 * m], Dy = anchor[3 * n + 1] - anchor[3 * m + 1],
+              Dz = anchor[3 * n + 2] - anchor[3 * m + 2];
+    const double* ln = lam + (int64_t)n * p3 * 4;
+    double kp = 0.0;
+    for (int s2 = 0; s2 < p3; ++s2) {
+      const int i2 = s2 % p, j2 = (s2 / p) % p, k2 = s2 / (p * p);
+      double u[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};   // u[a][c] = sum_s1 Lam^c_m[s1] B^a[s1, s2]
+      for (int s1 = 0; s1 < p3; ++s1) {
+        const int dx = s1 % p - i2 - Dx, dy = (s1 / p) % p - j2 - Dy, dz = s1 / (p * p) - k2 - Dz;
+        const double* g = c_gk_tab + 3 * ((dz + 6) * 169 + (dy + 6) * 13 + (dx + 6));
+        for (int a = 0; a < 3; ++a)
+          for (int c = 0; c < 3; ++c) u[a][c] += lm[s1 * 4 + c] * g[a];
+      }
+      // sum_{c,a,b} eps_cab u[a][c] Lam^b_n[s2]
+      const double l0 = ln[s2 * 4 + 0], l1 = ln[s2 * 4 + 1], l2 = ln[s2 * 4 + 2];
+      kp += u[1][0] * l2 - u[2][0] * l1     // c = x: (a,b) = (y,z) +, (z,y) -
+            + u[2][1] * l0 - u[0][1] * l2   // c = y: (z,x) +, (x,z) -
+            + u[0][2] * l1 - u[1][2] * l0;  // c = z: (x,y) +, (y,x) -
+    }
+    CK[k] = ks + Res[k] + kp;   // - K_s,P = + sum eps ...
+  }
+}
+
 void gauss_legendre(int q, double* x, double* w) {
   // nodes/weights on [0, 1]
   for (int i = 0; i < q; ++i) {
@@ -608,6 +771,34 @@ void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, 
     k_aim_fill<double2><<<(unsigned)blocks, threads, shm, s>>>((int)t.nb, t.order, k0, d.rowptr, d.col, d.anchor,
                                                                 d.side, d.lam, (double2*)DA, (double2*)DR);
   AIMX_CHECK_LAUNCH();
+}
+
+void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s) {
+  const int R = 2 * t.order + t.near_cells;
+  if (R > 6) throw Error(AIMX_E_GRID, "K precorrection offset table too small");
+  std::vector<double> tab(3 * 2197, 0.0);
+  for (int dz = -6; dz <= 6; ++dz)
+    for (int dy = -6; dy <= 6; ++dy)
+      for (int dx = -6; dx <= 6; ++dx) {
+        const double q = (double)(dx * dx + dy * dy + dz * dz);
+        if (q == 0.0) continue;
+        const double f = -1.0 / (4.0 * kPi * t.h * t.h * q * std::sqrt(q));   // d_a G_s = -delta_a / (4 pi h^2 |delta|^3)
+        double* g = tab.data() + 3 * ((dz + 6) * 169 + (dy + 6) * 13 + (dx + 6));
+        g[0] = f * dx; g[1] = f * dy; g[2] = f * dz;
+      }
+  AIMX_CUDA(cudaMemcpyToSymbolAsync(c_gk_tab, tab.data(), sizeof(double) * tab.size(), 0, cudaMemcpyHostToDevice, s));
+  const int64_t nnz = t.rowptr[t.nb];
+  double *Kun = nullptr, *Res = nullptr;
+  AIMX_CUDA(cudaMallocAsync(&Kun, (size_t)std::max<int64_t>(nnz, 1) * sizeof(double), s));
+  AIMX_CUDA(cudaMallocAsync(&Res, (size_t)std::max<int64_t>(nnz, 1) * sizeof(double), s));
+  const int threads = 128;
+  const int64_t blocks = (t.nb * 32 + threads - 1) / threads;
+  k_K_near_un<<<(unsigned)blocks, threads, 0, s>>>((int)t.nb, d.rowptr, d.col, d.side, d.T, d.tp, d.tm, Kun, Res);
+  AIMX_CHECK_LAUNCH();
+  k_K_combine<<<(unsigned)blocks, threads, 0, s>>>((int)t.nb, t.order, d.rowptr, d.col, d.anchor, d.lam, Kun, Res, CK);
+  AIMX_CHECK_LAUNCH();
+  AIMX_CUDA(cudaFreeAsync(Kun, s));
+  AIMX_CUDA(cudaFreeAsync(Res, s));
 }
 
 void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s) {

@@ -1,0 +1,30 @@
+"""NEXT #1 groundwork on the device: the static near part of the double-layer
+operator K (C_K = sym(K_s,PV) + residue - K_s,P, readings R23-R25) computed
+by the setup kernels in fp64, against the oracle (oracle/kop.py) on closed
+icospheres."""
+import numpy as np
+import pytest
+
+import aimx_inputs as inp
+from tests._parity import make_gpu_op, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("subdiv,n", [(1, (8, 8, 8)), (2, (16, 16, 16))])
+def test_K_static_vs_oracle(subdiv, n):
+    from oracle.aimx import AIMxOracle
+    from oracle.kop import K_precorrection_entries, residue_entries, static_K_entries
+    from oracle.static_near import symmetrize
+    m = inp.icosphere_mesh(subdiv, radius=0.5)
+    orc = AIMxOracle(m.vertices, m.triangles, n, static=False)
+    op = make_gpu_op(m, n, "c128")
+    rp, col = op.near_csr()
+    assert np.array_equal(rp, orc.rowptr) and np.array_equal(col, orc.col)
+    rows = np.repeat(np.arange(orc.N), np.diff(orc.rowptr))
+    ks = symmetrize(orc.rowptr, orc.col, static_K_entries(orc.V, orc.T, orc.rwg, rows, orc.col))
+    res = residue_entries(orc.V, orc.T, orc.rwg, rows, orc.col)
+    kp = K_precorrection_entries(orc.Lam, orc.A, rows, orc.col, orc.order, orc.grid.h)
+    ck = op.K_static()
+    assert rel_l2(ck, ks + res - kp) <= 1e-12
+    assert rel_l2(ck, ks + res) > 1e-6          # the precorrection is not negligible
