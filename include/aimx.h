@@ -249,7 +249,7 @@ aimx_status aimx_get_linear_entries(const aimx_ctx* ctx, int32_t* cols, double* 
  * sec:methods:K P:400-474, readings R23-R25): CK[nnz] (fp64, CSR order) =
  * sym(K_s,PV) + 1/2 int f_m . (n x f_n) - K_s,P, computed on the device on
  * demand (the K matvec itself is not built yet).  One-GPU contexts only. */
-aimx_status aimx_get_K_static(aimx_ctx* ctx, double* CK);
+aimx_status aimx_get_kop_static(aimx_ctx* ctx, double* CK);
 /* Projection weights (fp64) lam[N_b][4][(n+1)^3], channels (x, y, z, rho),
  * node s = i + (n+1)(j + (n+1) k). */
 aimx_status aimx_get_weights(const aimx_ctx* ctx, double* lam);

@@ -61,7 +61,7 @@ ABI_FUNCTIONS = {
     "aimx_get_linear_term": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "aimx_set_conventional": (C.c_int, [_P, C.c_int]),
     "aimx_get_aim_entries": (C.c_int, [_P, _P, _P]),
-    "aimx_get_K_static": (C.c_int, [_P, _P]),
+    "aimx_get_kop_static": (C.c_int, [_P, _P]),
     "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec_parts": (C.c_int, [_P, _P, _P, _P, _P]),
     "aimx_sweep": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_int32, _P]),
@@ -246,7 +246,7 @@ class AIMx:
         nnz = C.c_int64()
         _check(self.lib, self.lib.aimx_get_near_csr(self.ctx, None, None, C.byref(nnz)), self.ctx)
         ck = np.empty(nnz.value)
-        _check(self.lib, self.lib.aimx_get_K_static(self.ctx, _P(ck.ctypes.data)), self.ctx)
+        _check(self.lib, self.lib.aimx_get_kop_static(self.ctx, _P(ck.ctypes.data)), self.ctx)
         return ck
 
     def aim_entries(self):

@@ -169,7 +169,7 @@ void launch_precorrect(const Topology& t, SetupDev& d, cudaStream_t s);
 void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, void* DA, void* DR, cudaStream_t s);
 
 // ---------------------------------------------------------------- double-layer operator K (NEXT #1)
-// C_K = sym(K_s,PV) + residue - K_s,P on the near CSR pattern (fp64; oracle/kop.py,
+// C_K = sym(K_s,PV) + residue - K_s,P on the near CSR pattern (fp64; the oracle kop module,
 // readings R23-R25).  Needs d.side, d.T, d.tp, d.tm.
 void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s);
 

@@ -1829,7 +1829,7 @@ aimx_status aimx_get_linear_entries(const aimx_ctx* cc, int32_t* cols, double* C
   AIMX_API_END(c)
 }
 
-aimx_status aimx_get_K_static(aimx_ctx* c, double* CK) {
+aimx_status aimx_get_kop_static(aimx_ctx* c, double* CK) {
   if (!c || !CK) return AIMX_E_INVALID_ARG;
   AIMX_API_BEGIN
   if (c->slab) throw Error(AIMX_E_UNSUPPORTED, "one-GPU contexts only");

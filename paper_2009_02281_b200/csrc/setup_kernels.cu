@@ -516,7 +516,7 @@ __global__ void k_aim_fill(int nb, int order, double k0, const int64_t* __restri
 }
 
 // ---- the double-layer operator K, static near part (
-// oracle/kop.py, readings R23-R25): C_K = sym(K_s,PV) + residue - K_s,P.
+// the oracle kop module, readings R23-R25): C_K = sym(K_s,PV) + residue - K_s,P.
 // Q(r) = int_T (r - r')/R^3 dS' = sum_i m_i f2_i + n sgn(d) Omega (in-plane
 // points up to rounding are in-plane: the +-2 pi jump is the residue's).
 __device__ __forceinline__ Vec3 k_q(const Frame& F, Vec3 r) {
