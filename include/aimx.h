@@ -245,6 +245,17 @@ aimx_status aimx_get_static(const aimx_ctx* ctx, double* CA, double* Crho,
  * C^A_lin, C^rho_lin [N_b][5] as stored (compute precision, widened to fp64).
  * Any pointer may be NULL. */
 aimx_status aimx_get_linear_entries(const aimx_ctx* ctx, int32_t* cols, double* CA_lin, double* Crho_lin);
+/* Double-layer operator K (sec:methods:K P:400-474):
+ * aimx_set_kop(ctx, 1) builds its static near part C_K (below) and the static
+ * spectrum of F_s = 1/(4 pi r^3); every later aimx_set_frequency also forms
+ * F_hat(k0).  aimx_matvec_kop: y = Kmat x (reading R24: -int f_m . PV K[f_n]
+ * + the exterior residue), eq:KAIMx with the grid part through the even radial
+ * factor F of grad G = -r F: sum_ab eps_cab (d_a G (*) J_b) = -h [s x (F (*) J)
+ * - F (*) (s x J)] (two passes of the hot-path transforms), W^(K) = -P^T of
+ * the current channels, + C_K x.  One column, device vectors as aimx_matvec;
+ * AIMX_E_STATE when not enabled or no frequency bound; one-GPU contexts. */
+aimx_status aimx_set_kop(aimx_ctx* ctx, int enable);
+aimx_status aimx_matvec_kop(aimx_ctx* ctx, const void* x, void* y, void* stream);
 /* Double-layer operator K, static near part (SURVEY 8(f) NEXT #1 groundwork;
  * sec:methods:K P:400-474, readings R23-R25): CK[nnz] (fp64, CSR order) =
  * sym(K_s,PV) + 1/2 int f_m . (n x f_n) - K_s,P, computed on the device on

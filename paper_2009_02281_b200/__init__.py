@@ -62,6 +62,8 @@ ABI_FUNCTIONS = {
     "aimx_set_conventional": (C.c_int, [_P, C.c_int]),
     "aimx_get_aim_entries": (C.c_int, [_P, _P, _P]),
     "aimx_get_kop_static": (C.c_int, [_P, _P]),
+    "aimx_set_kop": (C.c_int, [_P, C.c_int]),
+    "aimx_matvec_kop": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec_parts": (C.c_int, [_P, _P, _P, _P, _P]),
     "aimx_sweep": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_int32, _P]),
@@ -239,6 +241,19 @@ class AIMx:
         """Conventional AIM mode: the near region regenerated by
         direct integration at every frequency (the method AIMx is compared with)."""
         _check(self.lib, self.lib.aimx_set_conventional(self.ctx, int(bool(on))), self.ctx)
+
+    def set_kop(self, on: bool = True):
+        """Enable the double-layer operator K (aimx_set_kop)."""
+        _check(self.lib, self.lib.aimx_set_kop(self.ctx, int(bool(on))), self.ctx)
+
+    def matvec_kop(self, x, y=None, stream=None):
+        """y = Kmat x at the bound frequency (aimx_matvec_kop)."""
+        torch = _torch()
+        if y is None:
+            y = torch.empty(self.N, dtype=self.cdtype, device=x.device)
+        _check(self.lib, self.lib.aimx_matvec_kop(self.ctx, self._vec(x, (self.N,)), self._vec(y, (self.N,)),
+                                                  self._s(stream)), self.ctx)
+        return y
 
     def K_static(self):
         """C_K of the double-layer operator on the near pattern (CSR order), fp64

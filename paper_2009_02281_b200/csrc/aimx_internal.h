@@ -172,6 +172,13 @@ void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, 
 // C_K = sym(K_s,PV) + residue - K_s,P on the near CSR pattern (fp64; the oracle kop module,
 // readings R23-R25).  Needs d.side, d.T, d.tp, d.tm.
 void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s);
+struct HotDev;
+// y = Kmat x (one column, bound frequency): two passes of the grid transforms
+// with the radial spectrum HF (slot 0), the curl combination, interpolation
+// with the fp64 weights lam, + C_K x (ck: compute precision, CSR order)
+void kop_matvec(bool f32, const HotDev& h, const void* x, void* y, const void* HF, void* phi1, void* phi2,
+                const double* lam, double hg, const int64_t* rowptr, const int32_t* col, const void* ck,
+                cudaStream_t s);
 
 // ---------------------------------------------------------------- linear-term modification
 // P:382-398 (sec:methods:aimx:acc): k0^2 G_lin, G_lin = -r/(8 pi) (eq:linterm
@@ -213,13 +220,15 @@ struct SpectrumPlan {
 void spectrum_plan_init(SpectrumPlan& sp, int batch, cudaStream_t s);
 void spectrum_plan_free(SpectrumPlan& sp);
 // H_hat octant (unnormalised) of the static kernel, fp64.
-void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s);
+// kind 0: the Green's function K = G (eq:hgf); 1: the radial factor F of
+// grad G = -r F (double-layer operator, NEXT #1)
+void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s, int kind = 0);
 // Per-frequency, B frequencies: out[b] = scale * (Hs + DFT3(K_d(k0[b]))) in the
 // compute precision (out stride noct).
 void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
-                          float2* out, cudaStream_t s);
+                          float2* out, cudaStream_t s, int kind = 0);
 void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs,
-                          double scale, double2* out, cudaStream_t s);
+                          double scale, double2* out, cudaStream_t s, int kind = 0);
 
 // ---------------------------------------------------------------- profiler
 // Per-stage CUDA-event timer (aimx_profile_*).

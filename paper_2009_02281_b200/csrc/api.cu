@@ -88,6 +88,14 @@ struct aimx_ctx {
   std::vector<MvGraph> graphs;
   MvGraph last_mv{nullptr, nullptr, nullptr, -1, 0.0, nullptr, 0};
   cudaStream_t cap = nullptr;   // capture stream
+  // double-layer operator K (aimx_set_kop, NEXT #1)
+  bool kop_on = false;
+  double2* HsF = nullptr;       // static spectrum of F_s = 1/(4 pi r^3), fp64
+  void* HsF_T = nullptr;        // ... compute precision (c64)
+  void* HF = nullptr;           // F_hat of the bound frequency (slot 0), scaled 1/M
+  void* kphi1 = nullptr;        // F (*) J and F (*) (s x J), phi layout
+  void* kphi2 = nullptr;
+  void* ck_T = nullptr;         // C_K (compute precision, CSR order)
   // conventional AIM mode (aimx_set_conventional): D(k0) on the near pattern
   bool aim_on = false;
   void* aimDA = nullptr;        // [nnz] compute precision complex
@@ -168,6 +176,11 @@ __global__ void k_pack_c(int64_t n, const int64_t* __restrict__ slot, const doub
   v.y = CR[i];
   *reinterpret_cast<T2*>(payload + slot[i]) = v;
 }
+__global__ void k_d2f_real(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (float)a[i];
+}
+
 __global__ void k_d2f(int64_t n, const double2* __restrict__ a, float2* __restrict__ b) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -831,8 +844,20 @@ void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s, void* out = nu
     spectrum_dynamic_f64(c->sp, B, k0, c->Hs, 1.0 / M, (double2*)out, s);
 }
 
+// F_hat(k0) of the double-layer operator into c->HF (slot 0)
+void kop_spectrum(aimx_ctx* c, double f, cudaStream_t s) {
+  double k0[1] = {2.0 * kPi * f / kC0};
+  const HotDev& h = c->hot;
+  const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
+  if (c->prec == AIMX_C64)
+    spectrum_dynamic_f32(c->sp, 1, k0, (const float2*)c->HsF_T, (float)(1.0 / M), (float2*)c->HF, s, 1);
+  else
+    spectrum_dynamic_f64(c->sp, 1, k0, c->HsF, 1.0 / M, (double2*)c->HF, s, 1);
+}
+
 void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
   spectra(c, 1, &f, s);
+  if (c->kop_on) kop_spectrum(c, f, s);
   c->f = f;
   c->k0 = 2.0 * kPi * f / kC0;
   c->omega = 2.0 * kPi * f;
@@ -1826,6 +1851,77 @@ aimx_status aimx_get_linear_entries(const aimx_ctx* cc, int32_t* cols, double* C
     if (CA_lin) CA_lin[i] = v[2 * i];
     if (Crho_lin) Crho_lin[i] = v[2 * i + 1];
   }
+  AIMX_API_END(c)
+}
+
+// double-layer operator K (NEXT #1): static near part, static F spectrum and
+// buffers, built once on the first enable
+static void build_kop(aimx_ctx* c) {
+  const Topology& t = c->topo;
+  ensure_side(c);
+  if (!c->sd.T) c->sd.T = dupload(c, t.T);
+  const int64_t nnz = t.rowptr[t.nb];
+  const bool f32 = c->prec == AIMX_C64;
+  const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
+  double* ck = dalloc<double>(c, nnz);
+  launch_K_static(t, c->sd, ck, c->stream);
+  if (f32) {
+    float* ckf = dalloc<float>(c, nnz);
+    k_d2f_real<<<nblk(nnz), 256, 0, c->stream>>>(nnz, ck, ckf);
+    AIMX_CHECK_LAUNCH();
+    AIMX_CUDA(cudaStreamSynchronize(c->stream));
+    dfree(c, ck, nnz * (int64_t)sizeof(double));
+    c->ck_T = ckf;
+  } else {
+    c->ck_T = ck;
+  }
+  const int64_t noct = (int64_t)(t.n[0] + 1) * (t.n[1] + 1) * (t.n[2] + 1);
+  c->HsF = dalloc<double2>(c, noct);
+  spectrum_static(c->sp, c->HsF, c->stream, 1);
+  if (f32) {
+    c->HsF_T = dalloc<float2>(c, noct);
+    k_d2f<<<nblk(noct), 256, 0, c->stream>>>(noct, c->HsF, (float2*)c->HsF_T);
+    AIMX_CHECK_LAUNCH();
+  } else {
+    c->HsF_T = c->HsF;
+  }
+  c->HF = dalloc<char>(c, noct * (int64_t)cs);
+  const int64_t nP = (int64_t)t.n[0] * t.n[1] * t.n[2] * 4;
+  c->kphi1 = zalloc<char>(c, nP * c->slots * (int64_t)cs + 64);
+  c->kphi2 = zalloc<char>(c, nP * c->slots * (int64_t)cs + 64);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+aimx_status aimx_set_kop(aimx_ctx* c, int enable) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (enable && c->slab) throw Error(AIMX_E_UNSUPPORTED, "the double-layer operator: one-GPU contexts only");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  if (enable && !c->HsF) build_kop(c);
+  c->kop_on = enable != 0;
+  if (c->kop_on && c->freq_set) {
+    kop_spectrum(c, c->f, c->stream);
+    AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
+  }
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_matvec_kop(aimx_ctx* c, const void* x, void* y, void* stream) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (!x || !y) throw Error(AIMX_E_INVALID_ARG, "null vector");
+  if (x == y) throw Error(AIMX_E_INVALID_ARG, "input and output alias");
+  if (!c->kop_on) throw Error(AIMX_E_STATE, "aimx_set_kop has not been enabled");
+  if (!c->freq_set) throw Error(AIMX_E_STATE, "aimx_set_frequency has not been called");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  cudaStream_t s = pick(c, stream);
+  if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
+  kop_matvec(c->prec == AIMX_C64, c->hot, x, y, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr,
+             c->sd.col, c->ck_T, s);
+  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
   AIMX_API_END(c)
 }
 

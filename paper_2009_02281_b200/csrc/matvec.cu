@@ -1264,6 +1264,100 @@ void hot_matvec(const HotDev& h, const void* x, void* y0, void* y1, const Combin
   hot_near<T>(h, x, y0, y1, c, s, prof);
 }
 
+// ---- the double-layer operator K: its grid part
+// through the EVEN radial factor F of grad G = -r F:
+//   sum_{a,b} eps_cab (d_a G (*) J_b) = -h [s x (F (*) J) - F (*) (s x J)]_c,
+// s the node coordinates in cells; two passes of the hot-path transforms with
+// the spectrum F_hat, then y_K = -sum_c W^c Phi_c + C_K x.
+// S := s x S on the occupied nodes (channel 3 -> 0), in place
+template <typename T>
+__global__ void k_cross_s(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= h.nocc) return;
+  const int lin = h.node_lin[q];
+  const T sx = (T)(lin % h.Nx), sy = (T)((lin / h.Nx) % h.Ny), sz = (T)(lin / (h.Nx * h.Ny));
+  T2* g = (T2*)h.S + ((int64_t)h.node_line[q] * h.Nx + lin % h.Nx) * 4;
+  const T2 jx = g[0], jy = g[1], jz = g[2];
+  g[0] = mk<T2>(sy * jz.x - sz * jy.x, sy * jz.y - sz * jy.y);
+  g[1] = mk<T2>(sz * jx.x - sx * jz.x, sz * jx.y - sx * jz.y);
+  g[2] = mk<T2>(sx * jy.x - sy * jx.x, sx * jy.y - sy * jx.y);
+  g[3] = mk<T2>(0, 0);
+}
+
+// thread per RWG: y = -sum_c sum_s Lambda^c[s] Phi_c(node), Phi = -hg [s x phi1 - phi2]
+// (phi layout [node][channel][slot], slot 0), then + C_K x (CSR, real)
+template <typename T>
+__global__ void k_kop_interp(HotDev h, const typename CT<T>::T2* __restrict__ phi1,
+                             const typename CT<T>::T2* __restrict__ phi2, const double* __restrict__ lam,
+                             double hg, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                             const T* __restrict__ ck, const typename CT<T>::T2* __restrict__ x,
+                             typename CT<T>::T2* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= h.nb) return;
+  const int p = h.p, p3 = h.p3, Nx = h.Nx, Ny = h.Ny;
+  const int64_t ns = (int64_t)h.batch * 4;
+  const int base = h.rwg_base[m];
+  double yr = 0.0, yi = 0.0;
+  for (int sl = 0; sl < p3; ++sl) {
+    const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
+    const int lin = base + i + Nx * (j + Ny * k);
+    const double* lw = lam + ((int64_t)m * p3 + sl) * 4;
+    if (lw[0] == 0.0 && lw[1] == 0.0 && lw[2] == 0.0) continue;
+    const double s0 = lin % Nx, s1 = (lin / Nx) % Ny, s2 = lin / (Nx * Ny);
+    const T2* a = phi1 + (int64_t)lin * ns;
+    const T2* b = phi2 + (int64_t)lin * ns;
+    const double ax = a[0].x, ay = a[h.batch].x, az = a[2 * h.batch].x;
+    const double axi = a[0].y, ayi = a[h.batch].y, azi = a[2 * h.batch].y;
+    // Phi = -hg (s x phi1 - phi2)
+    const double px = -hg * ((s1 * az - s2 * ay) - b[0].x), pxi = -hg * ((s1 * azi - s2 * ayi) - b[0].y);
+    const double py = -hg * ((s2 * ax - s0 * az) - b[h.batch].x), pyi = -hg * ((s2 * axi - s0 * azi) - b[h.batch].y);
+    const double pz = -hg * ((s0 * ay - s1 * ax) - b[2 * h.batch].x), pzi = -hg * ((s0 * ayi - s1 * axi) - b[2 * h.batch].y);
+    yr -= lw[0] * px + lw[1] * py + lw[2] * pz;
+    yi -= lw[0] * pxi + lw[1] * pyi + lw[2] * pzi;
+  }
+  for (int64_t e = rowptr[m]; e < rowptr[m + 1]; ++e) {
+    const T2 xv = x[col[e]];
+    yr += (double)ck[e] * xv.x;
+    yi += (double)ck[e] * xv.y;
+  }
+  y[m] = mk<T2>((T)yr, (T)yi);
+}
+
+template <typename T>
+void hot_kop(const HotDev& h0, const void* x, void* y, const void* HF, void* phi1, void* phi2, const double* lam,
+             double hg, const int64_t* rowptr, const int32_t* col, const void* ck, cudaStream_t s) {
+  using T2 = typename CT<T>::T2;
+  HotDev h = h0;
+  h.Hoct = const_cast<void*>(HF);
+  const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz;
+  run_gather<T>(h, x, h.nb, 1, s);   // S = P x (one column)
+  auto conv = [&](void* phi) {
+    h.phi = phi;
+    AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, 1, s)));
+    if (!run_yz_fused<T>(h, 1, s, nullptr)) {
+      AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, 1, s)));
+      AIMX_SWITCH_L(Lz, (run_z<T, L>(h, 1, s)));
+      AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, 1, s)));
+    }
+    AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, 1, s)));
+  };
+  conv(phi1);                                   // F (*) J
+  if (h.nocc > 0) {
+    launch_pdl(k_cross_s<T>, dim3((unsigned)((h.nocc + 255) / 256)), dim3(256), 0, s, h);
+    AIMX_CHECK_LAUNCH();
+  }
+  conv(phi2);                                   // F (*) (s x J)
+  launch_pdl(k_kop_interp<T>, dim3((unsigned)((h.nb + 127) / 128)), dim3(128), 0, s, h, (const T2*)phi1,
+             (const T2*)phi2, lam, hg, rowptr, col, (const T*)ck, (const T2*)x, (T2*)y);
+  AIMX_CHECK_LAUNCH();
+}
+
 // ---- slab-decomposed hot path (SlabRank): per rank S2 + x fwd on its rows,
 // exchange 0 (rows -> kx slabs), y fwd / z conv / y inv on its kx slab,
 // exchange 1 (kx slabs -> rows incl. the `order`-row halo), x inv of its
@@ -1459,6 +1553,12 @@ void hot_near_f32(const HotDev& h, const void* x, void* y0, void* y1, const Comb
 void hot_near_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s,
                   Profiler* prof) {
   hot_near<double>(h, x, y0, y1, c, s, prof);
+}
+void kop_matvec(bool f32, const HotDev& h, const void* x, void* y, const void* HF, void* phi1, void* phi2,
+                const double* lam, double hg, const int64_t* rowptr, const int32_t* col, const void* ck,
+                cudaStream_t s) {
+  if (f32) hot_kop<float>(h, x, y, HF, phi1, phi2, lam, hg, rowptr, col, ck, s);
+  else hot_kop<double>(h, x, y, HF, phi1, phi2, lam, hg, rowptr, col, ck, s);
 }
 void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof) {

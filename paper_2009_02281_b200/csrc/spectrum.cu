@@ -32,7 +32,10 @@ namespace {
 // Static samples: sample[(j (Nz+1) + l)(Nx+1) + i] = K_s(h sqrt(i^2 + j^2 + l^2)),
 // K_s = 1/(4 pi r) (eq:hgfs P:227), K_s(0) = 0 (eq:Hsmm P:321), 0 on wrap
 // slots; fp64.  (The dynamic samples are generated inside the x pass, ksample.)
-__global__ void k_sample_static(int Nx, int Ny, int Nz, int64_t noct, double h, double2* __restrict__ out) {
+// kind 1: F_s = 1/(4 pi r^3) (the radial factor of grad G_s = -r F_s; the
+// double-layer operator's grid form, NEXT #1), 0 at r = 0
+__global__ void k_sample_static(int Nx, int Ny, int Nz, int64_t noct, double h, double2* __restrict__ out,
+                                int kind) {
   pdl_wait();
   pdl_trigger();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -44,7 +47,10 @@ __global__ void k_sample_static(int Nx, int Ny, int Nz, int64_t noct, double h, 
   double re = 0.0;
   if (i < Nx && j < Ny && l < Nz) {
     int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
-    if (q > 0) re = 1.0 / (4.0 * kPi) / (h * sqrt((double)q));
+    if (q > 0) {
+      const double r = h * sqrt((double)q);
+      re = kind ? 1.0 / (4.0 * kPi * r * r * r) : 1.0 / (4.0 * kPi) / r;
+    }
   }
   out[idx] = make_double2(re, 0.0);
 }
@@ -70,9 +76,24 @@ template <typename S, int L, bool SMALL = false> struct EvGeom {
 // wrap slots; K_s (STATIC) or K_d(k0) in fp64, rounded to T.
 template <typename T, bool STATIC>
 __device__ __forceinline__ typename CT<T>::T2 ksample(int i, int j, int l, int Nx, int Ny, int Nz,
-                                                      double h, double k0) {
+                                                      double h, double k0, int kind = 0) {
   using T2 = typename CT<T>::T2;
   double re = 0.0, im = 0.0;
+  if (kind == 1) {   // F_d = ((1 + j x) e^{-j x} - 1)/(4 pi r^3), x = k0 r; 0 at r = 0 (fp64)
+    if (i < Nx && j < Ny && l < Nz) {
+      const int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
+      if (q > 0) {
+        const double r = h * sqrt((double)q), x = k0 * r;
+        double sh, ch, sx, cx;
+        sincos(0.5 * x, &sh, &ch);
+        sincos(x, &sx, &cx);
+        const double a = 1.0 / (4.0 * kPi * r * r * r);
+        re = (x * sx - 2.0 * sh * sh) * a;
+        im = (x * cx - sx) * a;
+      }
+    }
+    return mk<T2>((T)re, (T)im);
+  }
   if (i < Nx && j < Ny && l < Nz) {
     const int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
     const double inv4pi = 1.0 / (4.0 * kPi);
@@ -103,6 +124,7 @@ struct SampleArgs {
   int Nx, Ny, Nz;
   double h;
   double k0[kMaxBatch];
+  int kind;   // 0: K_d (eq:hgfd), 1: F_d (double-layer operator)
 };
 
 // MODE 0: read `in`; MODE 1: generate dynamic samples K_d (row pass only).
@@ -148,7 +170,7 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
     if constexpr (G::XB >= N1) {
       // each of the N1 samples once, staged in the line's exchange buffer
       if (act)
-        for (int n = t; n < N1; n += G::T) xb[n] = ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0);
+        for (int n = t; n < N1; n += G::T) xb[n] = ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0, sa.kind);
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < G::E; ++i) {
@@ -162,7 +184,7 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
       for (int i = 0; i < G::E; ++i) {
         int n = G::TL::in_index(t, i);
         n = n <= L / 2 ? n : L - n;
-        v[i] = act ? ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0) : mk<T2>(0, 0);
+        v[i] = act ? ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0, sa.kind) : mk<T2>(0, 0);
       }
     }
   } else {
@@ -376,26 +398,26 @@ void spectrum_plan_free(SpectrumPlan& sp) {
   sp = SpectrumPlan{};
 }
 
-void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s) {
+void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s, int kind) {
   launch_pdl(k_sample_static, dim3((unsigned)((sp.noct + 255) / 256)), dim3(256), 0, s, sp.Nx, sp.Ny, sp.Nz,
-             sp.noct, sp.h, (double2*)sp.work0);
+             sp.noct, sp.h, (double2*)sp.work0, kind);
   AIMX_CHECK_LAUNCH();
   dct3<double>(sp, 1, sp.tw64, sp.work0, sp.work1, out, nullptr, 1.0, s);
 }
 
 void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
-                          float2* out, cudaStream_t s) {
+                          float2* out, cudaStream_t s, int kind) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}, kind};
   for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
   // K_d samples generated inside the x pass (each sample once per line)
   dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s, &sa);
 }
 
 void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs, double scale,
-                          double2* out, cudaStream_t s) {
+                          double2* out, cudaStream_t s, int kind) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}};
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}, kind};
   for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
   // K_d samples generated inside the x pass (each sample once per line)
   dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s, &sa);

@@ -28,3 +28,29 @@ def test_K_static_vs_oracle(subdiv, n):
     ck = op.K_static()
     assert rel_l2(ck, ks + res - kp) <= 1e-12
     assert rel_l2(ck, ks + res) > 1e-6          # the precorrection is not negligible
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("subdiv,n", [(1, (8, 8, 8)), (2, (16, 16, 16))])
+def test_K_matvec_vs_oracle(prec, subdiv, n):
+    """aimx_matvec_kop (the grid part through the radial factor F, two passes
+    of the hot-path transforms) against the oracle's AIMx K (odd gradient
+    spectra) on closed icospheres."""
+    from oracle.aimx import AIMxOracle
+    from oracle.kop import AIMxK
+    from paper_2009_02281_b200 import AIMxError
+    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    m = inp.icosphere_mesh(subdiv, radius=0.5)
+    orc = AIMxOracle(m.vertices, m.triangles, n, static=False)
+    ak = AIMxK(orc)
+    op = make_gpu_op(m, n, prec)
+    x = np.random.default_rng(11).standard_normal(op.N) + 1j * np.random.default_rng(12).standard_normal(op.N)
+    with pytest.raises(AIMxError):
+        op.matvec_kop(to_gpu(x, prec))            # not enabled
+    op.set_kop(True)
+    for f in (50e6, 300e6):
+        op.set_frequency(f)
+        k0 = 2 * np.pi * f / 299792458.0
+        y = op.matvec_kop(to_gpu(x, prec)).cpu().numpy()
+        ref = ak.matvec(gpu_input_as_c128(x, prec), k0)
+        assert rel_l2(y, ref) <= TOL[prec], (f, rel_l2(y, ref))
