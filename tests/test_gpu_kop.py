@@ -54,3 +54,29 @@ def test_K_matvec_vs_oracle(prec, subdiv, n):
         y = op.matvec_kop(to_gpu(x, prec)).cpu().numpy()
         ref = ak.matvec(gpu_input_as_c128(x, prec), k0)
         assert rel_l2(y, ref) <= TOL[prec], (f, rel_l2(y, ref))
+
+
+@pytest.fixture(scope="module")
+def k3():
+    from oracle.aimx import AIMxOracle
+    from oracle.kop import AIMxK
+    m = inp.icosphere_mesh(3, radius=0.5)
+    orc = AIMxOracle(m.vertices, m.triangles, (32, 32, 32), static=False)
+    return m, AIMxK(orc)
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_K_matvec_long_transforms(prec, k3):
+    """1920 RWG on a 32^3 grid: the y / z transforms are too long for the fused
+    kernel and every z plane is occupied, so the two F passes run the separate
+    y passes and the TMA z pass."""
+    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    m, ak = k3
+    op = make_gpu_op(m, (32, 32, 32), prec)
+    op.set_kop(True)
+    x = np.random.default_rng(21).standard_normal(op.N) * (1 + 0.4j)
+    for f in (80e6, 400e6):
+        op.set_frequency(f)
+        y = op.matvec_kop(to_gpu(x, prec)).cpu().numpy()
+        ref = ak.matvec(gpu_input_as_c128(x, prec), 2 * np.pi * f / 299792458.0)
+        assert rel_l2(y, ref) <= TOL[prec], (f, rel_l2(y, ref))
