@@ -259,7 +259,7 @@ aimx_status aimx_matvec_kop(aimx_ctx* ctx, const void* x, void* y, void* stream)
 /* Double-layer operator K, static near part (SURVEY 8(f) NEXT #1 groundwork;
  * sec:methods:K P:400-474, readings R23-R25): CK[nnz] (fp64, CSR order) =
  * sym(K_s,PV) + 1/2 int f_m . (n x f_n) - K_s,P, computed on the device on
- * demand (the K matvec itself is not built yet).  One-GPU contexts only. */
+ * demand (introspection for the parity tests).  One-GPU contexts only. */
 aimx_status aimx_get_kop_static(aimx_ctx* ctx, double* CK);
 /* Projection weights (fp64) lam[N_b][4][(n+1)^3], channels (x, y, z, rho),
  * node s = i + (n+1)(j + (n+1) k). */
