@@ -29,7 +29,7 @@ label) step by step:
                     (eq:linterm P:363, eq:Lmatdecomplin P:386)
 * ``gmres``         restarted GMRES with the static diagonal preconditioner
 * ``kop``           AIMx for the double-layer operator K (eq:opK P:408,
-                    eq:KAIMx P:457; NEXT #1 groundwork, oracle only)
+                    eq:KAIMx P:457; NEXT #1)
 * ``aim``           the conventional AIM (per-frequency near region and
                     precorrection, eq:aimL P:190, eq:aimLP P:205)
 

@@ -1,7 +1,7 @@
 """The double-layer operator K and its AIMx form (oracle).  TEST INFRASTRUCTURE ONLY.
 
-SURVEY 8(f) NEXT #1 groundwork: the oracle side of AIMx for K (the device
-side is not built this round).
+SURVEY 8(f) NEXT #1: the oracle side of AIMx for K (the library's
+aimx_matvec_kop is checked against it, tests/test_gpu_kop.py).
 
 R25  the static PV entries use the analytic inner integral with the 7-point
      outer rule, subdivided 8 x 8 on triangle pairs that touch (the inner
