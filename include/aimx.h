@@ -255,6 +255,12 @@ aimx_status aimx_get_linear_entries(const aimx_ctx* ctx, int32_t* cols, double* 
  * the current channels, + C_K x.  One column, device vectors as aimx_matvec;
  * AIMX_E_STATE when not enabled or no frequency bound; one-GPU contexts. */
 aimx_status aimx_set_kop(aimx_ctx* ctx, int enable);
+/* CFIE (eq:CFIEdis P:422, closed PEC surfaces): enable != 0 makes every later
+ * combined matvec, sweep point and solve apply (-j w mu0 L - eta0 Kmat)
+ * (eta0 = mu0 c0; parts stay the L parts); sweeps and solves then run one
+ * frequency at a time.  Enables K (aimx_set_kop) if needed; exclusive with
+ * the conventional-AIM mode. */
+aimx_status aimx_set_cfie(aimx_ctx* ctx, int enable);
 aimx_status aimx_matvec_kop(aimx_ctx* ctx, const void* x, void* y, void* stream);
 /* Double-layer operator K, static near part (SURVEY 8(f) NEXT #1 groundwork;
  * sec:methods:K P:400-474, readings R23-R25): CK[nnz] (fp64, CSR order) =

@@ -63,6 +63,7 @@ ABI_FUNCTIONS = {
     "aimx_get_aim_entries": (C.c_int, [_P, _P, _P]),
     "aimx_get_kop_static": (C.c_int, [_P, _P]),
     "aimx_set_kop": (C.c_int, [_P, C.c_int]),
+    "aimx_set_cfie": (C.c_int, [_P, C.c_int]),
     "aimx_matvec_kop": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec_parts": (C.c_int, [_P, _P, _P, _P, _P]),
@@ -245,6 +246,10 @@ class AIMx:
     def set_kop(self, on: bool = True):
         """Enable the double-layer operator K (aimx_set_kop)."""
         _check(self.lib, self.lib.aimx_set_kop(self.ctx, int(bool(on))), self.ctx)
+
+    def set_cfie(self, on: bool = True):
+        """CFIE (eq:CFIEdis): matvec / sweep / solve apply -j w mu0 L - eta0 K."""
+        _check(self.lib, self.lib.aimx_set_cfie(self.ctx, int(bool(on))), self.ctx)
 
     def matvec_kop(self, x, y=None, stream=None):
         """y = Kmat x at the bound frequency (aimx_matvec_kop)."""

@@ -360,6 +360,7 @@ void gm_lincomb(bool f32, int nv, int B, int64_t N, const void* V, int64_t vstri
 void gm_colscale(bool f32, int B, int64_t N, const void* W, const double* sc, void* out, cudaStream_t s);
 void gm_colscale_rsqrt(bool f32, int B, int64_t N, const void* W, const double2* n2, void* out, cudaStream_t s);
 void gm_sub(bool f32, int64_t n, const void* a, const void* b, void* out, cudaStream_t s);
+void gm_axpy(bool f32, int64_t n, double a, const void* t, void* y, cudaStream_t s);   // y += a t
 void gm_take(int64_t n, const int64_t* idx, const double* src, double* d, cudaStream_t s);
 
 bool fft_length_supported(int L);

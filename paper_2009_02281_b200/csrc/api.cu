@@ -96,6 +96,8 @@ struct aimx_ctx {
   void* kphi1 = nullptr;        // F (*) J and F (*) (s x J), phi layout
   void* kphi2 = nullptr;
   void* ck_T = nullptr;         // C_K (compute precision, CSR order)
+  bool cfie_on = false;         // aimx_set_cfie: matvec / sweep / solve apply -j w mu0 L - eta0 K
+  void* ktmp = nullptr;         // [nb] K x
   // conventional AIM mode (aimx_set_conventional): D(k0) on the near pattern
   bool aim_on = false;
   void* aimDA = nullptr;        // [nnz] compute precision complex
@@ -918,6 +920,11 @@ void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaSt
     else hot_matvec_f64(c->hot, x, y0, y1, cb, q, &c->prof);
     if (c->aim_on)
       aim_spmv(c->prec == AIMX_C64, c->hot.nb, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, x, y0, y1, cb, q);
+    if (c->cfie_on && mode == 0) {   // eq:CFIEdis P:422: (-j w mu0 L - eta0 K) x
+      kop_matvec(c->prec == AIMX_C64, c->hot, x, c->ktmp, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h,
+                 c->sd.rowptr, c->sd.col, c->ck_T, q);
+      gm_axpy(c->prec == AIMX_C64, c->hot.nb, -kMu0 * kC0, c->ktmp, y0, q);
+    }
   };
   if (c->prof.on || std::getenv("AIMX_NO_GRAPH")) return eager(s);
   auto same = [&](const aimx_ctx::MvGraph& g) {
@@ -958,7 +965,7 @@ void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaSt
 
 // B frequency points: spectra into slots, then one batched matvec.
 void run_batch(aimx_ctx* c, int B, const double* f, const void* X, void* Y, cudaStream_t s) {
-  if (c->aim_on) {   // conventional AIM: near fill + matvec per frequency
+  if (c->aim_on || c->cfie_on) {   // conventional AIM / CFIE: per frequency
     const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
     for (int b = 0; b < B; ++b) {
       bind_frequency(c, f[b], s);
@@ -1228,10 +1235,19 @@ static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, ch
     if (B != 1) throw Error(AIMX_E_INTERNAL, "conventional AIM solve runs one frequency per batch");
     launch_aim_fill(c->topo, c->sd, 2.0 * kPi * f[0] / kC0, f32, c->aimDA, c->aimDR, s);
   }
+  if (c->cfie_on) {   // CFIE: this frequency's F spectrum
+    if (B != 1) throw Error(AIMX_E_INTERNAL, "CFIE solve runs one frequency per batch");
+    kop_spectrum(c, f[0], s);
+  }
   auto matvec = [&](const void* in, void* out) {
     if (f32) hot_matvec_f32(c->hot, in, out, nullptr, cb, s, &c->prof);
     else hot_matvec_f64(c->hot, in, out, nullptr, cb, s, &c->prof);
     if (c->aim_on) aim_spmv(f32, N, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, in, out, nullptr, cb, s);
+    if (c->cfie_on) {
+      kop_matvec(f32, c->hot, in, c->ktmp, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr,
+                 c->sd.col, c->ck_T, s);
+      gm_axpy(f32, N, -kMu0 * kC0, c->ktmp, out, s);
+    }
   };
   auto norms = [&](const void* A, std::vector<double>& out) {   // ||A_b||
     gm_dots(f32, 1, B, N, A, 0, A, ddots, s);
@@ -1385,7 +1401,7 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
   }
   const bool had = c->freq_set;
   const double f0 = c->f;
-  const int B = c->aim_on ? 1 : sweep_batch(c, 0, nf);   // conventional AIM: per-frequency near fill
+  const int B = (c->aim_on || c->cfie_on) ? 1 : sweep_batch(c, 0, nf);   // AIM / CFIE: one frequency at a time
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   for (int64_t i = 0; i < nf; i += B) {
     const int nb_ = (int)std::min<int64_t>(B, nf - i);
@@ -1485,6 +1501,7 @@ aimx_status aimx_set_conventional(aimx_ctx* c, int enable) {
   check_sticky(c);
   if (enable && c->slab) throw Error(AIMX_E_UNSUPPORTED, "conventional AIM mode: one-GPU contexts only");
   if (enable && c->lin_on) throw Error(AIMX_E_INVALID_ARG, "turn the linear-term modification off first");
+  if (enable && c->cfie_on) throw Error(AIMX_E_INVALID_ARG, "turn the CFIE off first");
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
   if (enable && !c->aimDA) {
     ensure_side(c);
@@ -1567,7 +1584,7 @@ static void sweep_impl(aimx_ctx* c, const std::vector<int64_t>& off, const doubl
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   const int64_t nbat = (int64_t)off.size() - 1;
   auto count = [&](int64_t i) { return (int)(off[i + 1] - off[i]); };
-  if (c->slab || nbat < 2 || !c->s2 || c->aim_on) {
+  if (c->slab || nbat < 2 || !c->s2 || c->aim_on || c->cfie_on) {
     for (int64_t i = 0; i < nbat; ++i) {
       if (before) before(i);
       run_batch(c, count(i), f + off[i], X + off[i] * vb, Y + off[i] * vb, s);
@@ -1896,6 +1913,7 @@ aimx_status aimx_set_kop(aimx_ctx* c, int enable) {
   if (!c) return AIMX_E_INVALID_ARG;
   AIMX_API_BEGIN
   if (enable && c->slab) throw Error(AIMX_E_UNSUPPORTED, "the double-layer operator: one-GPU contexts only");
+  if (!enable && c->cfie_on) throw Error(AIMX_E_INVALID_ARG, "turn the CFIE off first");
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
@@ -1905,6 +1923,28 @@ aimx_status aimx_set_kop(aimx_ctx* c, int enable) {
     kop_spectrum(c, c->f, c->stream);
     AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
   }
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_set_cfie(aimx_ctx* c, int enable) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (enable && c->slab) throw Error(AIMX_E_UNSUPPORTED, "CFIE: one-GPU contexts only");
+  if (enable && c->aim_on) throw Error(AIMX_E_INVALID_ARG, "turn the conventional AIM mode off first");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  if (enable) {
+    if (!c->HsF) build_kop(c);
+    if (!c->ktmp) c->ktmp = dalloc<char>(c, c->topo.nb * (int64_t)(c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2)));
+    if (!c->kop_on) {
+      c->kop_on = true;
+      if (c->freq_set) kop_spectrum(c, c->f, c->stream);
+    }
+  }
+  clear_graphs(c);
+  c->cfie_on = enable != 0;
+  AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
   AIMX_API_END(c)
 }
 

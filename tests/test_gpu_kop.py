@@ -80,3 +80,41 @@ def test_K_matvec_long_transforms(prec, k3):
         y = op.matvec_kop(to_gpu(x, prec)).cpu().numpy()
         ref = ak.matvec(gpu_input_as_c128(x, prec), 2 * np.pi * f / 299792458.0)
         assert rel_l2(y, ref) <= TOL[prec], (f, rel_l2(y, ref))
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_cfie_matvec_sweep_solve(prec):
+    """CFIE (eq:CFIEdis): matvec = Z x - eta0 Kmat x against the oracle's
+    parts; a sweep and a GMRES solve in CFIE mode, residuals under the oracle
+    CFIE operator."""
+    from oracle.aimx import AIMxOracle
+    from oracle.kop import AIMxK
+    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    m = inp.icosphere_mesh(2, radius=0.5)
+    n = (16, 16, 16)
+    orc = AIMxOracle(m.vertices, m.triangles, n)
+    ak = AIMxK(orc)
+    eta0 = 1.25663706212e-6 * 299792458.0
+
+    def cfie(x, f):
+        orc.set_frequency(f)
+        return orc.matvec(x) - eta0 * ak.matvec(x, orc.k0)
+    op = make_gpu_op(m, n, prec)
+    op.set_cfie(True)
+    x = np.random.default_rng(31).standard_normal(op.N) * (1 - 0.2j)
+    for f in (60e6, 250e6):
+        op.set_frequency(f)
+        y = op.matvec(to_gpu(x, prec)).cpu().numpy()
+        assert rel_l2(y, cfie(gpu_input_as_c128(x, prec), f)) <= TOL[prec]
+    freqs = np.array([80e6, 200e6, 320e6])
+    X = np.stack([np.random.default_rng(40 + i).standard_normal(op.N) + 0j for i in range(3)])
+    Y = op.sweep(freqs, to_gpu(X, prec)).cpu().numpy()
+    for i, f in enumerate(freqs):
+        assert rel_l2(Y[i], cfie(gpu_input_as_c128(X[i], prec), f)) <= TOL[prec]
+    tol = 1e-6 if prec == "c128" else 1e-4
+    Xs, its, rr = op.solve(freqs, to_gpu(X, prec), tol=tol, restart=30, maxiter=2000)
+    Xs = Xs.cpu().numpy()
+    for i, f in enumerate(freqs):
+        b = gpu_input_as_c128(X[i], prec)
+        res = np.linalg.norm(b - cfie(Xs[i], f)) / np.linalg.norm(b)
+        assert rr[i] <= tol * (1 + 1e-6) and res <= 5 * tol, (i, its[i], rr[i], res)
