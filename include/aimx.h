@@ -261,6 +261,18 @@ aimx_status aimx_set_kop(aimx_ctx* ctx, int enable);
  * frequency at a time.  Enables K (aimx_set_kop) if needed; exclusive with
  * the conventional-AIM mode. */
 aimx_status aimx_set_cfie(aimx_ctx* ctx, int enable);
+/* PMCHWT for a homogeneous dielectric body (cfg4's formulation; reading R27,
+ * AMB-17 -- the paper names PMCHWT but never states it): x = [J; M] and
+ * y = [y_E; y_H], device vectors of 2 N_b complex,
+ *   y_E = (Z0 + Z1) J - (K0 + K1) M,   y_H = (K0 + K1) J + (Z0/eta0^2 + Z1/eta1^2) M,
+ * medium 0 outside (k0 of the bound frequency), medium 1 inside (k1 = k0
+ * sqrt(eps_r), eta1 = eta0/sqrt(eps_r), mu_r = 1); Z_i = -j w mu0 (L_A(k_i) +
+ * k_i^-2 L_phi(k_i)) with the physical w; K_i the tested principal-value K
+ * (the exterior and interior residues cancel).  Both media share the static
+ * matrices (G_s is medium-free).  Needs aimx_set_kop's static part
+ * (AIMX_E_STATE otherwise); AIMX_E_INVALID_ARG in conventional-AIM or CFIE
+ * mode. */
+aimx_status aimx_matvec_pmchwt(aimx_ctx* ctx, double eps_r, const void* x, void* y, void* stream);
 aimx_status aimx_matvec_kop(aimx_ctx* ctx, const void* x, void* y, void* stream);
 /* Double-layer operator K, static near part (SURVEY 8(f) NEXT #1 groundwork;
  * sec:methods:K P:400-474, readings R23-R25): CK[nnz] (fp64, CSR order) =

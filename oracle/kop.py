@@ -359,7 +359,42 @@ class AIMxK:
         kp = K_precorrection_entries(op.Lam, op.A, rows, op.col, op.order, op.grid.h)
         import scipy.sparse as sp
         self.C = sp.csr_matrix((ks + res - kp, op.col, op.rowptr), shape=(op.N, op.N))
+        self.Cpv = sp.csr_matrix((ks - kp, op.col, op.rowptr), shape=(op.N, op.N))
 
-    def matvec(self, x, k0: float):
+    def matvec(self, x, k0: float, residue: bool = True):
         x = np.asarray(x, np.complex128)
-        return self.C @ x + grid_K(self.op, x, k0)
+        return (self.C if residue else self.Cpv) @ x + grid_K(self.op, x, k0)
+
+
+def pmchwt_matvec(op, ak: AIMxK, f_hz: float, eps_r: float, x):
+    """PMCHWT for a homogeneous dielectric body (
+    reading R27, AMB-17: the paper names PMCHWT, but never states
+    it): unknowns x = [J; M] (electric and magnetic surface currents), media
+    0 (outside, k0, eta0) and 1 (inside, k1 = k0 sqrt(eps_r), eta1 = eta0 /
+    sqrt(eps_r), mu_r = 1):
+        y_E = (Z0 + Z1) J - (K0 + K1) M
+        y_H = (K0 + K1) J + (Z0 / eta0^2 + Z1 / eta1^2) M
+    Z_i = -j w mu0 (L_A(k_i) + k_i^-2 L_phi(k_i)) (w the physical frequency),
+    K_i the tested PV operator (the exterior and interior residues cancel in
+    the sum).  The same static matrices serve both media (G_s is medium-free)."""
+    from .kernels import MU0, C0
+    x = np.asarray(x, np.complex128)
+    N = op.N
+    J, M = x[:N], x[N:]
+    w = 2 * np.pi * f_hz
+    eta0 = MU0 * C0
+    eta1 = eta0 / np.sqrt(eps_r)
+    out_E = np.zeros(N, complex)
+    out_H = np.zeros(N, complex)
+    Ksum_J = np.zeros(N, complex)
+    Ksum_M = np.zeros(N, complex)
+    for i, fi in enumerate((f_hz, f_hz * np.sqrt(eps_r))):
+        op.set_frequency(fi)
+        k = op.k0
+        zJ = (lambda a, r: -1j * w * MU0 * (a - r / (k * k)))(*op.parts(J))
+        zM = (lambda a, r: -1j * w * MU0 * (a - r / (k * k)))(*op.parts(M))
+        out_E += zJ
+        out_H += zM / (eta0 ** 2 if i == 0 else eta1 ** 2)
+        Ksum_J += ak.matvec(J, k, residue=False)
+        Ksum_M += ak.matvec(M, k, residue=False)
+    return np.concatenate([out_E - Ksum_M, out_H + Ksum_J])

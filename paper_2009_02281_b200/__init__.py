@@ -64,6 +64,7 @@ ABI_FUNCTIONS = {
     "aimx_get_kop_static": (C.c_int, [_P, _P]),
     "aimx_set_kop": (C.c_int, [_P, C.c_int]),
     "aimx_set_cfie": (C.c_int, [_P, C.c_int]),
+    "aimx_matvec_pmchwt": (C.c_int, [_P, C.c_double, _P, _P, _P]),
     "aimx_matvec_kop": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec_parts": (C.c_int, [_P, _P, _P, _P, _P]),
@@ -250,6 +251,15 @@ class AIMx:
     def set_cfie(self, on: bool = True):
         """CFIE (eq:CFIEdis): matvec / sweep / solve apply -j w mu0 L - eta0 K."""
         _check(self.lib, self.lib.aimx_set_cfie(self.ctx, int(bool(on))), self.ctx)
+
+    def matvec_pmchwt(self, eps_r: float, x, y=None, stream=None):
+        """PMCHWT [y_E; y_H] for x = [J; M] (2N), interior eps_r (aimx_matvec_pmchwt)."""
+        torch = _torch()
+        if y is None:
+            y = torch.empty(2 * self.N, dtype=self.cdtype, device=x.device)
+        _check(self.lib, self.lib.aimx_matvec_pmchwt(self.ctx, float(eps_r), self._vec(x, (2 * self.N,)),
+                                                     self._vec(y, (2 * self.N,)), self._s(stream)), self.ctx)
+        return y
 
     def matvec_kop(self, x, y=None, stream=None):
         """y = Kmat x at the bound frequency (aimx_matvec_kop)."""

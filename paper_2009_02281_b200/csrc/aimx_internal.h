@@ -171,7 +171,7 @@ void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, 
 // ---------------------------------------------------------------- double-layer operator K (NEXT #1)
 // C_K = sym(K_s,PV) + residue - K_s,P on the near CSR pattern (fp64; the oracle kop module,
 // readings R23-R25).  Needs d.side, d.T, d.tp, d.tm.
-void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s);
+void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s, double* CKpv = nullptr);
 struct HotDev;
 // y = Kmat x (one column, bound frequency): two passes of the grid transforms
 // with the radial spectrum HF (slot 0), the curl combination, interpolation
@@ -361,6 +361,7 @@ void gm_colscale(bool f32, int B, int64_t N, const void* W, const double* sc, vo
 void gm_colscale_rsqrt(bool f32, int B, int64_t N, const void* W, const double2* n2, void* out, cudaStream_t s);
 void gm_sub(bool f32, int64_t n, const void* a, const void* b, void* out, cudaStream_t s);
 void gm_axpy(bool f32, int64_t n, double a, const void* t, void* y, cudaStream_t s);   // y += a t
+void gm_caxpy(bool f32, int64_t n, double ar, double ai, const void* t, void* y, cudaStream_t s);   // y += (ar + j ai) t
 void gm_take(int64_t n, const int64_t* idx, const double* src, double* d, cudaStream_t s);
 
 bool fft_length_supported(int L);

@@ -98,6 +98,10 @@ struct aimx_ctx {
   void* ck_T = nullptr;         // C_K (compute precision, CSR order)
   bool cfie_on = false;         // aimx_set_cfie: matvec / sweep / solve apply -j w mu0 L - eta0 K
   void* ktmp = nullptr;         // [nb] K x
+  void* ckpv_T = nullptr;       // C_K without the residue (PMCHWT), compute precision
+  void* pm_H1 = nullptr;        // PMCHWT: spectra of the interior medium (H_hat, F_hat)
+  void* pm_HF1 = nullptr;
+  void* pm_t = nullptr;         // [3][nb] temporaries
   // conventional AIM mode (aimx_set_conventional): D(k0) on the near pattern
   bool aim_on = false;
   void* aimDA = nullptr;        // [nnz] compute precision complex
@@ -847,14 +851,15 @@ void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s, void* out = nu
 }
 
 // F_hat(k0) of the double-layer operator into c->HF (slot 0)
-void kop_spectrum(aimx_ctx* c, double f, cudaStream_t s) {
+void kop_spectrum(aimx_ctx* c, double f, cudaStream_t s, void* out = nullptr) {
+  if (!out) out = c->HF;
   double k0[1] = {2.0 * kPi * f / kC0};
   const HotDev& h = c->hot;
   const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
   if (c->prec == AIMX_C64)
-    spectrum_dynamic_f32(c->sp, 1, k0, (const float2*)c->HsF_T, (float)(1.0 / M), (float2*)c->HF, s, 1);
+    spectrum_dynamic_f32(c->sp, 1, k0, (const float2*)c->HsF_T, (float)(1.0 / M), (float2*)out, s, 1);
   else
-    spectrum_dynamic_f64(c->sp, 1, k0, c->HsF, 1.0 / M, (double2*)c->HF, s, 1);
+    spectrum_dynamic_f64(c->sp, 1, k0, c->HsF, 1.0 / M, (double2*)out, s, 1);
 }
 
 void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
@@ -1881,16 +1886,23 @@ static void build_kop(aimx_ctx* c) {
   const bool f32 = c->prec == AIMX_C64;
   const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
   double* ck = dalloc<double>(c, nnz);
-  launch_K_static(t, c->sd, ck, c->stream);
+  double* ckpv = dalloc<double>(c, nnz);
+  launch_K_static(t, c->sd, ck, c->stream, ckpv);
   if (f32) {
     float* ckf = dalloc<float>(c, nnz);
+    float* ckpvf = dalloc<float>(c, nnz);
     k_d2f_real<<<nblk(nnz), 256, 0, c->stream>>>(nnz, ck, ckf);
+    AIMX_CHECK_LAUNCH();
+    k_d2f_real<<<nblk(nnz), 256, 0, c->stream>>>(nnz, ckpv, ckpvf);
     AIMX_CHECK_LAUNCH();
     AIMX_CUDA(cudaStreamSynchronize(c->stream));
     dfree(c, ck, nnz * (int64_t)sizeof(double));
+    dfree(c, ckpv, nnz * (int64_t)sizeof(double));
     c->ck_T = ckf;
+    c->ckpv_T = ckpvf;
   } else {
     c->ck_T = ck;
+    c->ckpv_T = ckpv;
   }
   const int64_t noct = (int64_t)(t.n[0] + 1) * (t.n[1] + 1) * (t.n[2] + 1);
   c->HsF = dalloc<double2>(c, noct);
@@ -1961,6 +1973,73 @@ aimx_status aimx_matvec_kop(aimx_ctx* c, const void* x, void* y, void* stream) {
   if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
   kop_matvec(c->prec == AIMX_C64, c->hot, x, y, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr,
              c->sd.col, c->ck_T, s);
+  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  AIMX_API_END(c)
+}
+
+// PMCHWT (reading R27): x = [J; M], y = [y_E; y_H],
+//   y_E = (Z0 + Z1) J - (K0 + K1) M,  y_H = (K0 + K1) J + (Z0/eta0^2 + Z1/eta1^2) M,
+// medium 1 = the interior, k1 = k0 sqrt(eps_r), eta1 = eta0 / sqrt(eps_r); the
+// interior operators are the free-space ones at the frequency f sqrt(eps_r)
+// (same static matrices), the Z prefactor keeps the physical omega.
+aimx_status aimx_matvec_pmchwt(aimx_ctx* c, double eps_r, const void* x, void* y, void* stream) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (!x || !y || x == y) throw Error(AIMX_E_INVALID_ARG, "null or aliased vectors");
+  if (!(eps_r >= 1.0) || !std::isfinite(eps_r)) throw Error(AIMX_E_INVALID_ARG, "eps_r must be finite and >= 1");
+  if (!c->HsF) throw Error(AIMX_E_STATE, "aimx_set_kop has not been enabled");
+  if (!c->freq_set) throw Error(AIMX_E_STATE, "aimx_set_frequency has not been called");
+  if (c->aim_on || c->cfie_on) throw Error(AIMX_E_INVALID_ARG, "PMCHWT runs the AIMx operators (AIM / CFIE off)");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  cudaStream_t s = pick(c, stream);
+  if (s != c->stream) {
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
+  }
+  const bool f32 = c->prec == AIMX_C64;
+  const int64_t nb = c->hot.nb;
+  const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
+  const int64_t noct = (int64_t)(c->hot.Nx + 1) * (c->hot.Ny + 1) * (c->hot.Nz + 1);
+  if (!c->pm_H1) {
+    c->pm_H1 = dalloc<char>(c, noct * (int64_t)cs);
+    c->pm_HF1 = dalloc<char>(c, noct * (int64_t)cs);
+    c->pm_t = dalloc<char>(c, 3 * nb * (int64_t)cs);
+  }
+  if (!c->kop_on) kop_spectrum(c, c->f, s);   // F_hat(k0) (aimx_set_kop(0) left it stale)
+  const double f0 = c->f, f1 = c->f * std::sqrt(eps_r);
+  spectra(c, 1, &f1, s, c->pm_H1);
+  kop_spectrum(c, f1, s, c->pm_HF1);
+  char* tA = (char*)c->pm_t;
+  char* tP = tA + nb * cs;
+  char* tK = tP + nb * cs;
+  const char* J = (const char*)x;
+  const char* Mc = J + nb * cs;
+  char* yE = (char*)y;
+  char* yH = yE + nb * cs;
+  AIMX_CUDA(cudaMemsetAsync(y, 0, 2 * nb * cs, s));
+  const double w = 2.0 * kPi * f0, eta0 = kMu0 * kC0, eta1 = eta0 / std::sqrt(eps_r);
+  for (int i = 0; i < 2; ++i) {
+    const double fi = i ? f1 : f0, k = 2.0 * kPi * fi / kC0;
+    HotDev h = c->hot;
+    if (i) h.Hoct = c->pm_H1;
+    const void* HFi = i ? c->pm_HF1 : c->HF;
+    Combine cb = make_combine(1, &fi, 1, nb);   // parts: tA = y^A, tP = -y^rho
+    // Z = -j w mu0 (y^A - y^rho / k^2) = -j w mu0 (tA + tP / k^2)
+    const double a = -w * kMu0, b = -w * kMu0 / (k * k);   // imaginary coefficients
+    for (int src = 0; src < 2; ++src) {
+      const void* xs = src ? (const void*)Mc : (const void*)J;
+      if (f32) hot_matvec_f32(h, xs, tA, tP, cb, s, nullptr);
+      else hot_matvec_f64(h, xs, tA, tP, cb, s, nullptr);
+      const double sc = src ? 1.0 / ((i ? eta1 : eta0) * (i ? eta1 : eta0)) : 1.0;
+      char* yz = src ? yH : yE;
+      gm_caxpy(f32, nb, 0.0, a * sc, tA, yz, s);
+      gm_caxpy(f32, nb, 0.0, b * sc, tP, yz, s);
+      kop_matvec(f32, h, xs, tK, HFi, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr, c->sd.col,
+                 c->ckpv_T, s);
+      gm_axpy(f32, nb, src ? -1.0 : 1.0, tK, src ? yE : yH, s);   // y_E -= K M, y_H += K J
+    }
+  }
   AIMX_CUDA(cudaEventRecord(c->ev_use, s));
   AIMX_API_END(c)
 }

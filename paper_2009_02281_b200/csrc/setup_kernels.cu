@@ -640,7 +640,7 @@ __constant__ double c_gk_tab[3 * 2197];   // d_a G_s(h delta) for |delta_i| <= 6
 __global__ void k_K_combine(int nb, int order, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                             const int32_t* __restrict__ anchor, const double* __restrict__ lam,
                             const double* __restrict__ Kun, const double* __restrict__ Res,
-                            double* __restrict__ CK) {
+                            double* __restrict__ CK, double* __restrict__ CKpv) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (warp >= nb) return;
@@ -675,6 +675,7 @@ __global__ void k_K_combine(int nb, int order, const int64_t* __restrict__ rowpt
             + u[0][2] * l1 - u[1][2] * l0;  // c = z: (x,y) +, (y,x) -
     }
     CK[k] = ks + Res[k] + kp;   // - K_s,P = + sum eps ...
+    if (CKpv) CKpv[k] = ks + kp;   // principal value only (PMCHWT: the residues cancel)
   }
 }
 
@@ -773,7 +774,7 @@ void launch_aim_fill(const Topology& t, const SetupDev& d, double k0, bool f32, 
   AIMX_CHECK_LAUNCH();
 }
 
-void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s) {
+void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStream_t s, double* CKpv) {
   const int R = 2 * t.order + t.near_cells;
   if (R > 6) throw Error(AIMX_E_GRID, "K precorrection offset table too small");
   std::vector<double> tab(3 * 2197, 0.0);
@@ -795,7 +796,8 @@ void launch_K_static(const Topology& t, const SetupDev& d, double* CK, cudaStrea
   const int64_t blocks = (t.nb * 32 + threads - 1) / threads;
   k_K_near_un<<<(unsigned)blocks, threads, 0, s>>>((int)t.nb, d.rowptr, d.col, d.side, d.T, d.tp, d.tm, Kun, Res);
   AIMX_CHECK_LAUNCH();
-  k_K_combine<<<(unsigned)blocks, threads, 0, s>>>((int)t.nb, t.order, d.rowptr, d.col, d.anchor, d.lam, Kun, Res, CK);
+  k_K_combine<<<(unsigned)blocks, threads, 0, s>>>((int)t.nb, t.order, d.rowptr, d.col, d.anchor, d.lam, Kun, Res, CK,
+                                                    CKpv);
   AIMX_CHECK_LAUNCH();
   AIMX_CUDA(cudaFreeAsync(Kun, s));
   AIMX_CUDA(cudaFreeAsync(Res, s));

@@ -120,6 +120,17 @@ __global__ void k_axpy(int64_t n, double a, const T2* __restrict__ t, T2* __rest
   y[i] = mk<T2>(v.x + a * u.x, v.y + a * u.y);
 }
 
+// y += a t (a complex)
+template <typename T2>
+__global__ void k_caxpy(int64_t n, double ar, double ai, const T2* __restrict__ t, T2* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 u = to_d(t[i]), v = to_d(y[i]);
+  y[i] = mk<T2>(v.x + ar * u.x - ai * u.y, v.y + ar * u.y + ai * u.x);
+}
+
 // out = a - b
 template <typename T2>
 __global__ void k_sub(int64_t n, const T2* __restrict__ a, const T2* __restrict__ b, T2* __restrict__ out) {
@@ -177,6 +188,11 @@ void gm_colscale_rsqrt(bool f32, int B, int64_t N, const void* W, const double2*
 void gm_axpy(bool f32, int64_t n, double a, const void* t, void* y, cudaStream_t s) {
   if (f32) launch_pdl(k_axpy<float2>, dim3(nb256(n)), dim3(256), 0, s, n, a, (const float2*)t, (float2*)y);
   else launch_pdl(k_axpy<double2>, dim3(nb256(n)), dim3(256), 0, s, n, a, (const double2*)t, (double2*)y);
+  AIMX_CHECK_LAUNCH();
+}
+void gm_caxpy(bool f32, int64_t n, double ar, double ai, const void* t, void* y, cudaStream_t s) {
+  if (f32) launch_pdl(k_caxpy<float2>, dim3(nb256(n)), dim3(256), 0, s, n, ar, ai, (const float2*)t, (float2*)y);
+  else launch_pdl(k_caxpy<double2>, dim3(nb256(n)), dim3(256), 0, s, n, ar, ai, (const double2*)t, (double2*)y);
   AIMX_CHECK_LAUNCH();
 }
 void gm_sub(bool f32, int64_t n, const void* a, const void* b, void* out, cudaStream_t s) {

@@ -118,3 +118,27 @@ def test_cfie_matvec_sweep_solve(prec):
         b = gpu_input_as_c128(X[i], prec)
         res = np.linalg.norm(b - cfie(Xs[i], f)) / np.linalg.norm(b)
         assert rr[i] <= tol * (1 + 1e-6) and res <= 5 * tol, (i, its[i], rr[i], res)
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_pmchwt_vs_oracle(prec):
+    """PMCHWT (reading R27) for a dielectric sphere, eps_r = 4: the library's
+    composite of L and principal-value K in both media against the oracle's."""
+    from oracle.aimx import AIMxOracle
+    from oracle.kop import AIMxK, pmchwt_matvec
+    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    m = inp.icosphere_mesh(2, radius=0.25)
+    n = (16, 16, 16)
+    orc = AIMxOracle(m.vertices, m.triangles, n)
+    ak = AIMxK(orc)
+    op = make_gpu_op(m, n, prec)
+    op.set_kop(True)
+    x = np.random.default_rng(51).standard_normal(2 * op.N) * (1 + 0.3j)
+    x[op.N:] /= 376.73                       # M ~ eta0 J
+    for f in (100e6, 300e6):
+        op.set_frequency(f)
+        y = op.matvec_pmchwt(4.0, to_gpu(x, prec)).cpu().numpy()
+        ref = pmchwt_matvec(orc, ak, f, 4.0, gpu_input_as_c128(x, prec))
+        N = op.N
+        for sl in (slice(0, N), slice(N, 2 * N)):   # each equation on its own scale
+            assert rel_l2(y[sl], ref[sl]) <= TOL[prec], (f, sl, rel_l2(y[sl], ref[sl]))

@@ -171,3 +171,23 @@ def test_grid_K_through_the_radial_kernel(sph):
         k0 = 2 * np.pi * f / 299792458.0
         a, b = grid_K(op, x, k0), grid_K_radial(op, x, k0)
         assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(a)
+
+
+def test_pmchwt_equal_media_reduces_to_doubled_blocks(sph):
+    # eps_r = 1: both media are free space, so y_E = 2 Z J - 2 K_pv M and
+    # y_H = 2 K_pv J + 2 Z / eta0^2 M (reading R27; the residues cancel)
+    from oracle.kernels import C0, MU0
+    from oracle.kop import pmchwt_matvec
+    op = sph
+    ak = AIMxK(op)
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal(2 * op.N) + 1j * rng.standard_normal(2 * op.N)
+    f = 120e6
+    y = pmchwt_matvec(op, ak, f, 1.0, x)
+    op.set_frequency(f)
+    J, M = x[:op.N], x[op.N:]
+    eta0 = MU0 * C0
+    k0 = op.k0
+    Kj, Km = ak.matvec(J, k0, residue=False), ak.matvec(M, k0, residue=False)
+    assert np.linalg.norm(y[:op.N] - (2 * op.matvec(J) - 2 * Km)) <= 1e-12 * np.linalg.norm(y[:op.N])
+    assert np.linalg.norm(y[op.N:] - (2 * Kj + 2 * op.matvec(M) / eta0 ** 2)) <= 1e-12 * np.linalg.norm(y[op.N:])
