@@ -1287,8 +1287,9 @@ __global__ void k_cross_s(HotDev h) {
   g[3] = mk<T2>(0, 0);
 }
 
-// thread per RWG: y = -sum_c sum_s Lambda^c[s] Phi_c(node), Phi = -hg [s x phi1 - phi2]
-// (phi layout [node][channel][slot], slot 0), then + C_K x (CSR, real)
+// warp per RWG: y = -sum_c sum_s Lambda^c[s] Phi_c(node), Phi = -hg [s x phi1 - phi2]
+// (phi layout [node][channel][slot], slot 0; lanes over the stencil slots),
+// then + C_K x (lanes over the row's CSR entries); fixed-order shuffle sum
 template <typename T>
 __global__ void k_kop_interp(HotDev h, const typename CT<T>::T2* __restrict__ phi1,
                              const typename CT<T>::T2* __restrict__ phi2, const double* __restrict__ lam,
@@ -1298,35 +1299,40 @@ __global__ void k_kop_interp(HotDev h, const typename CT<T>::T2* __restrict__ ph
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (m >= h.nb) return;
   const int p = h.p, p3 = h.p3, Nx = h.Nx, Ny = h.Ny;
   const int64_t ns = (int64_t)h.batch * 4;
   const int base = h.rwg_base[m];
   double yr = 0.0, yi = 0.0;
-  for (int sl = 0; sl < p3; ++sl) {
-    const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
-    const int lin = base + i + Nx * (j + Ny * k);
+  for (int sl = lane; sl < p3; sl += 32) {
     const double* lw = lam + ((int64_t)m * p3 + sl) * 4;
     if (lw[0] == 0.0 && lw[1] == 0.0 && lw[2] == 0.0) continue;
+    const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
+    const int lin = base + i + Nx * (j + Ny * k);
     const double s0 = lin % Nx, s1 = (lin / Nx) % Ny, s2 = lin / (Nx * Ny);
     const T2* a = phi1 + (int64_t)lin * ns;
     const T2* b = phi2 + (int64_t)lin * ns;
     const double ax = a[0].x, ay = a[h.batch].x, az = a[2 * h.batch].x;
     const double axi = a[0].y, ayi = a[h.batch].y, azi = a[2 * h.batch].y;
-    // Phi = -hg (s x phi1 - phi2)
     const double px = -hg * ((s1 * az - s2 * ay) - b[0].x), pxi = -hg * ((s1 * azi - s2 * ayi) - b[0].y);
     const double py = -hg * ((s2 * ax - s0 * az) - b[h.batch].x), pyi = -hg * ((s2 * axi - s0 * azi) - b[h.batch].y);
     const double pz = -hg * ((s0 * ay - s1 * ax) - b[2 * h.batch].x), pzi = -hg * ((s0 * ayi - s1 * axi) - b[2 * h.batch].y);
     yr -= lw[0] * px + lw[1] * py + lw[2] * pz;
     yi -= lw[0] * pxi + lw[1] * pyi + lw[2] * pzi;
   }
-  for (int64_t e = rowptr[m]; e < rowptr[m + 1]; ++e) {
+  for (int64_t e = rowptr[m] + lane; e < rowptr[m + 1]; e += 32) {
     const T2 xv = x[col[e]];
     yr += (double)ck[e] * xv.x;
     yi += (double)ck[e] * xv.y;
   }
-  y[m] = mk<T2>((T)yr, (T)yi);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    yr += __shfl_xor_sync(0xffffffffu, yr, o);
+    yi += __shfl_xor_sync(0xffffffffu, yi, o);
+  }
+  if (lane == 0) y[m] = mk<T2>((T)yr, (T)yi);
 }
 
 template <typename T>
@@ -1353,7 +1359,7 @@ void hot_kop(const HotDev& h0, const void* x, void* y, const void* HF, void* phi
     AIMX_CHECK_LAUNCH();
   }
   conv(phi2);                                   // F (*) (s x J)
-  launch_pdl(k_kop_interp<T>, dim3((unsigned)((h.nb + 127) / 128)), dim3(128), 0, s, h, (const T2*)phi1,
+  launch_pdl(k_kop_interp<T>, dim3((unsigned)(((int64_t)h.nb * 32 + 255) / 256)), dim3(256), 0, s, h, (const T2*)phi1,
              (const T2*)phi2, lam, hg, rowptr, col, (const T*)ck, (const T2*)x, (T2*)y);
   AIMX_CHECK_LAUNCH();
 }
