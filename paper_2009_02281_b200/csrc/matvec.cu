@@ -1278,7 +1278,10 @@ __global__ void k_cross_s(HotDev h) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= h.nocc) return;
   const int lin = h.node_lin[q];
-  const T sx = (T)(lin % h.Nx), sy = (T)((lin / h.Nx) % h.Ny), sz = (T)(lin / (h.Nx * h.Ny));
+  // coordinates about the grid centre (any origin is exact; the centre halves
+  // |s| and with it the fp32 cancellation of s x (F * J) - F * (s x J))
+  const T sx = (T)(lin % h.Nx - h.Nx / 2), sy = (T)((lin / h.Nx) % h.Ny - h.Ny / 2),
+          sz = (T)(lin / (h.Nx * h.Ny) - h.Nz / 2);
   T2* g = (T2*)h.S + ((int64_t)h.node_line[q] * h.Nx + lin % h.Nx) * 4;
   const T2 jx = g[0], jy = g[1], jz = g[2];
   g[0] = mk<T2>(sy * jz.x - sz * jy.x, sy * jz.y - sz * jy.y);
@@ -1311,7 +1314,7 @@ __global__ void k_kop_interp(HotDev h, const typename CT<T>::T2* __restrict__ ph
     if (lw[0] == 0.0 && lw[1] == 0.0 && lw[2] == 0.0) continue;
     const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
     const int lin = base + i + Nx * (j + Ny * k);
-    const double s0 = lin % Nx, s1 = (lin / Nx) % Ny, s2 = lin / (Nx * Ny);
+    const double s0 = lin % Nx - Nx / 2, s1 = (lin / Nx) % Ny - Ny / 2, s2 = lin / (Nx * Ny) - h.Nz / 2;
     const T2* a = phi1 + (int64_t)lin * ns;
     const T2* b = phi2 + (int64_t)lin * ns;
     const double ax = a[0].x, ay = a[h.batch].x, az = a[2 * h.batch].x;
