@@ -370,7 +370,13 @@ void build_gather(aimx_ctx* c, HotDev& h, const NodeMap& m) {
   dfree(c, ent_slot, nent * (int64_t)sizeof(int32_t));
   const double avg = h.nocc > 0 ? (double)nent / h.nocc : 1.0;
   int G = 4;
-  while (G < 32 && 2 * G < avg) G *= 2;   // about two entries per lane: the shuffle reduction stays a small share
+  // four to eight entries per lane: loads in flight per lane hide the gather
+  // latency and the shuffle reduction stays a small share (measured: cfg3 G = 4
+  // 69 us, 8 73, 16 81, 32 106 for gather + x fwd)
+  // ... unless that leaves too few threads to fill the GPU (cfg2: 8448 nodes
+  // want 32 lanes each)
+  while (G < 32 && (8 * G <= avg || (int64_t)h.nocc * G < 148 * 2048)) G *= 2;
+  if (const char* e = std::getenv("AIMX_GATHER_G")) G = std::max(4, std::min(32, std::atoi(e)));   // experiments
   h.G = G;
 }
 
