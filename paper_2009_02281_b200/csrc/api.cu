@@ -476,7 +476,10 @@ int choose_slots(aimx_ctx* c) {
   const int64_t nA = Nz * Ny * 2 * Nx * 4, nB = Nz * 2 * Ny * 2 * Nx * 4, nP = Nx * Ny * Nz * 4;
   const int64_t noct = (Nx + 1) * (Ny + 1) * (Nz + 1);
   const int64_t per_freq = (int64_t)cs * (nS + 2 * nA + nB + nP + noct) + 2 * (int64_t)sizeof(double2) * noct;
-  int slots = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)(1536ll << 20) / per_freq));
+  // per-frequency grid buffers within 6 GB (of 180 GB): cfg3 gets 8 slots, its
+  // 16-point sweep +17% over 2 slots (measured 1566 / 1691 / 1827 / 1730
+  // freq-pts/s at 2 / 4 / 8 / 16)
+  int slots = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)(6144ll << 20) / per_freq));
   if (const char* e = std::getenv("AIMX_BATCH")) slots = std::max(1, std::min(kMaxBatch, std::atoi(e)));
   while (slots & (slots - 1)) slots &= slots - 1;   // power of two (batch buckets never exceed it)
   return slots;
