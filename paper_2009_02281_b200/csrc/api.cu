@@ -929,9 +929,13 @@ void clear_graphs(aimx_ctx* c) {
 void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaStream_t s) {
   Combine cb = make_combine(1, &c->f, mode, c->hot.nb);
   if (c->slab) return run_slab(c, x, y0, y1, cb, s);
+  // one column: the potentials compact ([node][channel], batch 1), so the
+  // interpolation's node rows are dense whatever the context's slot count
+  HotDev h1 = c->hot;
+  h1.batch = 1;
   auto eager = [&](cudaStream_t q) {
-    if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, x, y0, y1, cb, q, &c->prof);
-    else hot_matvec_f64(c->hot, x, y0, y1, cb, q, &c->prof);
+    if (c->prec == AIMX_C64) hot_matvec_f32(h1, x, y0, y1, cb, q, &c->prof);
+    else hot_matvec_f64(h1, x, y0, y1, cb, q, &c->prof);
     if (c->aim_on)
       aim_spmv(c->prec == AIMX_C64, c->hot.nb, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, x, y0, y1, cb, q);
     if (c->cfie_on && mode == 0) {   // eq:CFIEdis P:422: (-j w mu0 L - eta0 K) x
