@@ -1344,6 +1344,7 @@ void hot_kop(const HotDev& h0, const void* x, void* y, const void* HF, void* phi
   using T2 = typename CT<T>::T2;
   HotDev h = h0;
   h.Hoct = const_cast<void*>(HF);
+  h.batch = 1;   // one column: compact potentials ([node][channel])
   const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz;
   run_gather<T>(h, x, h.nb, 1, s);   // S = P x (one column)
   auto conv = [&](void* phi) {
