@@ -142,3 +142,42 @@ def test_pmchwt_vs_oracle(prec):
         N = op.N
         for sl in (slice(0, N), slice(N, 2 * N)):   # each equation on its own scale
             assert rel_l2(y[sl], ref[sl]) <= TOL[prec], (f, sl, rel_l2(y[sl], ref[sl]))
+
+
+def test_kop_api_edges():
+    """States and exclusions of the K / CFIE / PMCHWT calls."""
+    import torch
+    from paper_2009_02281_b200 import AIMxError
+    from tests._parity import to_gpu
+    m = inp.icosphere_mesh(1, radius=0.5)
+    op = make_gpu_op(m, (8, 8, 8), "c128")
+    x = to_gpu(np.ones(op.N), "c128")
+    x2 = to_gpu(np.ones(2 * op.N), "c128")
+    with pytest.raises(AIMxError):
+        op.matvec_pmchwt(4.0, x2)                  # K not built
+    op.set_kop(True)
+    with pytest.raises(AIMxError):
+        op.matvec_kop(x)                           # no frequency bound
+    op.set_frequency(100e6)
+    y = op.matvec_kop(x)
+    assert torch.isfinite(torch.view_as_real(y)).all()
+    with pytest.raises(AIMxError):
+        op.matvec_pmchwt(0.5, x2)                  # eps_r < 1
+    with pytest.raises(AIMxError):
+        op.matvec_kop(x, x)                        # aliasing
+    op.set_cfie(True)
+    with pytest.raises(AIMxError):
+        op.set_kop(False)                          # CFIE needs K
+    with pytest.raises(AIMxError):
+        op.set_conventional(True)                  # CFIE and conventional AIM are exclusive
+    with pytest.raises(AIMxError):
+        op.matvec_pmchwt(4.0, x2)                  # PMCHWT runs the AIMx operators
+    op.set_cfie(False)
+    yp = op.matvec_pmchwt(4.0, x2)
+    assert yp.shape[0] == 2 * op.N
+    # zero input -> zero output
+    z = op.matvec_kop(torch.zeros_like(x))
+    assert torch.count_nonzero(z) == 0
+    s = make_gpu_op(m, (8, 8, 8), "c128", slab=("emulate", 2))
+    with pytest.raises(AIMxError):
+        s.set_kop(True)
