@@ -181,6 +181,12 @@ aimx_status aimx_get_aim_entries(const aimx_ctx* ctx, double* DA, double* Drho);
  * x, y: device vectors of N_b complex numbers (see conventions). */
 aimx_status aimx_matvec(aimx_ctx* ctx, const void* x, void* y, void* stream);
 
+/* Several right-hand sides at the bound frequency: Y[i,:] = Z(k0) X[i,:] for
+ * i < nrhs (device [nrhs][N_b]), in device batches of the context's slots
+ * (the batched kernels, one spectrum for all columns).  AIMX_E_UNSUPPORTED
+ * for slab contexts and in conventional-AIM / CFIE mode. */
+aimx_status aimx_matvec_multi(aimx_ctx* ctx, int64_t nrhs, const void* X, void* Y, void* stream);
+
 /* Parts, unscaled: yA = L_A x = y^A, yPhi = L_phi x = -y^rho (the divergence is
  * moved to the testing function).  Either output may be NULL. */
 aimx_status aimx_matvec_parts(aimx_ctx* ctx, const void* x, void* yA, void* yPhi,

@@ -64,6 +64,7 @@ ABI_FUNCTIONS = {
     "aimx_get_kop_static": (C.c_int, [_P, _P]),
     "aimx_set_kop": (C.c_int, [_P, C.c_int]),
     "aimx_set_cfie": (C.c_int, [_P, C.c_int]),
+    "aimx_matvec_multi": (C.c_int, [_P, C.c_int64, _P, _P, _P]),
     "aimx_matvec_pmchwt": (C.c_int, [_P, C.c_double, _P, _P, _P]),
     "aimx_matvec_kop": (C.c_int, [_P, _P, _P, _P]),
     "aimx_matvec": (C.c_int, [_P, _P, _P, _P]),
@@ -301,6 +302,16 @@ class AIMx:
         _check(self.lib, self.lib.aimx_matvec(self.ctx, self._vec(x, (self.N,)),
                                               self._vec(y, (self.N,)), self._s(stream)), self.ctx)
         return y
+
+    def matvec_multi(self, X, Y=None, stream=None):
+        """Y[i] = Z(k0) X[i] for several right-hand sides at the bound frequency."""
+        torch = _torch()
+        n = X.shape[0]
+        if Y is None:
+            Y = torch.empty((n, self.N), dtype=self.cdtype, device=X.device)
+        _check(self.lib, self.lib.aimx_matvec_multi(self.ctx, n, self._vec(X, (n, self.N)), self._vec(Y, (n, self.N)),
+                                                    self._s(stream)), self.ctx)
+        return Y
 
     def matvec_parts(self, x, stream=None):
         torch = _torch()

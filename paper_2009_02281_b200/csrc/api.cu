@@ -1951,6 +1951,38 @@ aimx_status aimx_set_kop(aimx_ctx* c, int enable) {
   AIMX_API_END(c)
 }
 
+// Several right-hand sides at the bound frequency, in device batches of the
+// context's slots: the batched kernels with every column reading spectrum
+// slot 0 (slot stride 0), so one spectrum serves the whole batch.
+aimx_status aimx_matvec_multi(aimx_ctx* c, int64_t nrhs, const void* X, void* Y, void* stream) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (nrhs < 0 || (nrhs > 0 && (!X || !Y))) throw Error(AIMX_E_INVALID_ARG, "bad arguments");
+  if (nrhs > 0 && X == Y) throw Error(AIMX_E_INVALID_ARG, "input and output alias");
+  if (!c->freq_set) throw Error(AIMX_E_STATE, "aimx_set_frequency has not been called");
+  if (c->slab || c->aim_on || c->cfie_on)
+    throw Error(AIMX_E_UNSUPPORTED, "aimx_matvec_multi: one-GPU AIMx contexts (no AIM / CFIE mode)");
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  cudaStream_t s = pick(c, stream);
+  if (s != c->stream) {
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
+  }
+  const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
+  HotDev h = c->hot;
+  h.sH = 0;   // every column reads the bound spectrum (slot 0)
+  for (int64_t i = 0; i < nrhs; i += c->hot.batch) {
+    const int B = (int)std::min<int64_t>(c->hot.batch, nrhs - i);
+    std::vector<double> f(B, c->f);
+    Combine cb = make_combine(B, f.data(), 0, c->hot.nb);
+    if (c->prec == AIMX_C64) hot_matvec_f32(h, (const char*)X + i * vb, (char*)Y + i * vb, nullptr, cb, s, &c->prof);
+    else hot_matvec_f64(h, (const char*)X + i * vb, (char*)Y + i * vb, nullptr, cb, s, &c->prof);
+  }
+  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  AIMX_API_END(c)
+}
+
 aimx_status aimx_set_cfie(aimx_ctx* c, int enable) {
   if (!c) return AIMX_E_INVALID_ARG;
   AIMX_API_BEGIN

@@ -346,3 +346,21 @@ def test_planar_single_plane_z_pass(prec, world):
         oA, oR = orc.parts(gpu_input_as_c128(x, prec))
         assert rel_l2(yA.cpu().numpy(), oA) <= TOL[prec]
         assert rel_l2(yP.cpu().numpy(), -oR) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_matvec_multi_equals_single(prec):
+    """Several right-hand sides at one frequency (batched kernels, one spectrum
+    for all columns) against single matvecs, across a batch boundary, with the
+    linear term on too."""
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), prec)
+    S = op.stats()["batch_slots"]
+    n = S + 3
+    X = to_gpu(np.stack([inp.rhs_vector(1, 200 + i, op.N) for i in range(n)]), prec)
+    tol = 1e-6 if prec == "c64" else 1e-13
+    for lin in (False, True):
+        op.set_linear_term(lin)
+        op.set_frequency(210e6)
+        Y = op.matvec_multi(X).cpu().numpy()
+        for i in (0, S - 1, S, n - 1):
+            assert rel_l2(Y[i], op.matvec(X[i].contiguous()).cpu().numpy()) <= tol
