@@ -470,6 +470,9 @@ def run_aimx(a):
             "data": "synthetic (seeded meshes and complex-Gaussian x per frequency, aimx_inputs)",
             "config": {"workload": workload_desc(c, prec, nf), "config_index": a.config - 1,
                        "freq_pts_per_rank_per_step": nf,
+                       "batch_slots": st["batch_slots"],
+                       "device_batches": [min(st["batch_slots"], nf - i) for i in range(0, nf, st["batch_slots"])]
+                       if a.mode != "slab" else None,
                        "parallelism": f"slab-fft x{world}" if a.mode == "slab" else f"freq-shard x{world}",
                        "l2": "flushed between timed steps (256 MB write); inputs resident in HBM",
                        "setup_seconds": st["setup_seconds"], "linear_term": bool(a.linear_term)},
