@@ -920,6 +920,17 @@ void run_slab(aimx_ctx* c, const void* x, void* y0, void* y1, const Combine& cb,
   }
 }
 
+// HotDev for a B-column launch: the potentials laid out for the power-of-two
+// column bucket of B (the kernels' bucket; <= the slots), not for all slots,
+// so small batches read dense node rows
+HotDev batch_view(const aimx_ctx* c, int B) {
+  HotDev h = c->hot;
+  int b = 1;
+  while (b < B) b <<= 1;
+  h.batch = std::min(h.batch, b);
+  return h;
+}
+
 void clear_graphs(aimx_ctx* c) {
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   c->graphs.clear();
@@ -994,8 +1005,9 @@ void run_batch(aimx_ctx* c, int B, const double* f, const void* X, void* Y, cuda
   spectra(c, B, f, s);
   Combine cb = make_combine(B, f, 0, c->hot.nb);
   if (c->slab) return run_slab(c, X, Y, nullptr, cb, s);
-  if (c->prec == AIMX_C64) hot_matvec_f32(c->hot, X, Y, nullptr, cb, s, &c->prof);
-  else hot_matvec_f64(c->hot, X, Y, nullptr, cb, s, &c->prof);
+  const HotDev hb = batch_view(c, B);
+  if (c->prec == AIMX_C64) hot_matvec_f32(hb, X, Y, nullptr, cb, s, &c->prof);
+  else hot_matvec_f64(hb, X, Y, nullptr, cb, s, &c->prof);
 }
 
 aimx_status fail(aimx_ctx* c, const Error& e) {
@@ -1257,9 +1269,10 @@ static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, ch
     if (B != 1) throw Error(AIMX_E_INTERNAL, "CFIE solve runs one frequency per batch");
     kop_spectrum(c, f[0], s);
   }
+  const HotDev hsv = batch_view(c, B);
   auto matvec = [&](const void* in, void* out) {
-    if (f32) hot_matvec_f32(c->hot, in, out, nullptr, cb, s, &c->prof);
-    else hot_matvec_f64(c->hot, in, out, nullptr, cb, s, &c->prof);
+    if (f32) hot_matvec_f32(hsv, in, out, nullptr, cb, s, &c->prof);
+    else hot_matvec_f64(hsv, in, out, nullptr, cb, s, &c->prof);
     if (c->aim_on) aim_spmv(f32, N, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, in, out, nullptr, cb, s);
     if (c->cfie_on) {
       kop_matvec(f32, c->hot, in, c->ktmp, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr,
@@ -1634,7 +1647,7 @@ static void sweep_impl(aimx_ctx* c, const std::vector<int64_t>& off, const doubl
     if (i + 1 < nbat) spec(i + 1);
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_sp[i % 2], 0));
     if (before) before(i);
-    HotDev hh = c->hot;
+    HotDev hh = batch_view(c, count(i));
     hh.Hoct = c->HB[i % 2];
     hh.xt = c->XT[i % 2];
     Combine cb = make_combine(count(i), f + off[i], 0, c->hot.nb);
@@ -1970,10 +1983,10 @@ aimx_status aimx_matvec_multi(aimx_ctx* c, int64_t nrhs, const void* X, void* Y,
     AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
   }
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
-  HotDev h = c->hot;
-  h.sH = 0;   // every column reads the bound spectrum (slot 0)
   for (int64_t i = 0; i < nrhs; i += c->hot.batch) {
     const int B = (int)std::min<int64_t>(c->hot.batch, nrhs - i);
+    HotDev h = batch_view(c, B);
+    h.sH = 0;   // every column reads the bound spectrum (slot 0)
     std::vector<double> f(B, c->f);
     Combine cb = make_combine(B, f.data(), 0, c->hot.nb);
     if (c->prec == AIMX_C64) hot_matvec_f32(h, (const char*)X + i * vb, (char*)Y + i * vb, nullptr, cb, s, &c->prof);
