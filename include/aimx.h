@@ -225,7 +225,10 @@ aimx_status aimx_solve(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void
 
 /* The same sweep with X, Y in HOST memory (pinned or pageable): the library
  * stages each batch host->device and the results device->host on `stream`
- * and synchronises the stream before returning. */
+ * and synchronises the stream before returning.  With batch <= 0 the first
+ * device batch is 3/4 of the slots (its copy is shorter, the compute starts
+ * sooner), so results equal aimx_sweep's to rounding; with an explicit batch
+ * the batches, and the results bit for bit, are aimx_sweep's. */
 aimx_status aimx_sweep_host(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* X,
                             void* Y, int32_t batch, void* stream);
 

@@ -1685,10 +1685,13 @@ static int sweep_batch(const aimx_ctx* c, int32_t batch, int64_t nf) {
 // full slots with the remainder last (a short last batch also shortens the
 // host sweep's final device->host copy); AIMX_SWEEP_PLAN="s0,s1,..." sets the
 // leading batch sizes (experiments).
-static std::vector<int64_t> sweep_plan(const aimx_ctx* c, int32_t batch, int64_t nf) {
+static std::vector<int64_t> sweep_plan(const aimx_ctx* c, int32_t batch, int64_t nf, bool host = false) {
   const int64_t S = c->hot.batch;
   const int64_t B = batch > 0 ? std::max<int64_t>(1, std::min<int64_t>(batch, S)) : S;
   std::vector<int64_t> off{0};
+  // host buffers: a 3/4 first batch starts the compute after a shorter first
+  // copy (cfg2 100 points: 24, 32, 32, 12 -- 0.754 against 0.772 ms end to end)
+  if (host && batch <= 0 && nf > S && S >= 4 && !std::getenv("AIMX_SWEEP_PLAN")) off.push_back(3 * S / 4);
   if (batch <= 0)
     if (const char* e = std::getenv("AIMX_SWEEP_PLAN")) {
       for (const char* p = e; *p && off.back() < nf;) {
@@ -1737,7 +1740,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  const std::vector<int64_t> plan = sweep_plan(c, batch, nf);
+  const std::vector<int64_t> plan = sweep_plan(c, batch, nf, true);
   const int64_t nbat_all = (int64_t)plan.size() - 1;
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   // staging: chunks of whole batches within 1 GB (all of them for cfg1/cfg2), so

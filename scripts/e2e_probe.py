@@ -50,8 +50,9 @@ out = {
     "sweep_host_wall_ms": wall(lambda: op.sweep_host(freqs, Xh, Yh)),
     "bytes_each_way": int(Xh.numel() * 8),
 }
-for plan in ("25,25,25,25", "4,32,32,32", "4,32,32,28,4", "8,32,32,28", "2,32,32,32,2", "16,32,32,20",
-             "12,32,32,24"):
+plans = sys.argv[1].split(";") if len(sys.argv) > 1 else ["25,25,25,25", "4,32,32,32", "4,32,32,28,4",
+                                                          "8,32,32,28", "2,32,32,32,2", "16,32,32,20", "12,32,32,24"]
+for plan in plans:
     os.environ["AIMX_SWEEP_PLAN"] = plan
     out[f"host[{plan}]"] = wall(lambda: op.sweep_host(freqs, Xh, Yh), 20)
     out[f"dev[{plan}]"] = wall(lambda: op.sweep(freqs, X, Y), 20)

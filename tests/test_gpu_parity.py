@@ -275,7 +275,11 @@ def test_sweep_overlapped_near_equals_serial(prec, monkeypatch):
             monkeypatch.setenv("AIMX_NO_OVERLAP", "1")
             s = op.sweep(freqs, X, batch=b).clone()
             monkeypatch.delenv("AIMX_NO_OVERLAP")
-            assert torch.equal(a, s) and torch.equal(Yh, a.cpu())
+            assert torch.equal(a, s)
+            if b > 0:   # same batches: bit for bit
+                assert torch.equal(Yh, a.cpu())
+            else:       # the host sweep's shorter first batch: equal to rounding
+                assert rel_l2(Yh.numpy(), a.cpu().numpy()) <= (1e-6 if prec == "c64" else 1e-13)
 
 
 def test_sweep_plan_shapes():
