@@ -38,6 +38,8 @@ Every reading of a silent/ambiguous/garbled passage is listed in DESIGN.md
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against closed forms, brute force, invariants or
-the paper's printed values.  Parity unpinned: the SIGN of the residue term
-of ``kop`` (reading R24, exterior limit; nothing in the paper fixes it).
+the paper's printed values.  The sign of ``kop``'s residue term (reading R24)
+and the PMCHWT composition and medium scalings (R27) are pinned by physics
+in ``tests/test_oracle_kop_physics.py``: the field of a uniformly
+magnetised sphere and the extinction theorem for plane waves.
 """

@@ -30,8 +30,9 @@ Readings (DESIGN.md):
                (f_m is tangential, so f_m . (n (n . v) - v) = -f_m . v; the
                residue is n x H^+ = J/2 + n x PV K[J]).  n = outward normal
                (vertex order).  The residue sign follows this exterior-limit
-               reading; nothing in the paper pins it (parity unpinned for the
-               residue's sign; every other part is pinned).
+               reading.  It is pinned by the field of a uniformly magnetised
+               sphere (tests/test_oracle_kop_physics.py: Kmat x = +b/3 within
+               2%, the other sign gives -2b/3).
 
 AIMx for K, channel form: with the current channels g_b = P^b x (b = x, y, z),
     Phi_c = sum_{a,b} eps_{cab} (H_grad,a (*) g_b),   y_K = -sum_c W^c Phi_c + (K_s,NR - K_s,P) x,
@@ -376,7 +377,10 @@ def pmchwt_matvec(op, ak: AIMxK, f_hz: float, eps_r: float, x):
         y_H = (K0 + K1) J + (Z0 / eta0^2 + Z1 / eta1^2) M
     Z_i = -j w mu0 (L_A(k_i) + k_i^-2 L_phi(k_i)) (w the physical frequency),
     K_i the tested PV operator (the exterior and interior residues cancel in
-    the sum).  The same static matrices serve both media (G_s is medium-free)."""
+    the sum).  The same static matrices serve both media (G_s is medium-free).
+    M is n x E (so y_H is +int f . H_inc for the incident fields); the
+    composition and both media's scalings are pinned by the extinction
+    theorem (tests/test_oracle_kop_physics.py)."""
     from .kernels import MU0, C0
     x = np.asarray(x, np.complex128)
     N = op.N
