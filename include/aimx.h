@@ -111,6 +111,9 @@ typedef struct {
   int32_t near_group_rows;    /* R: rows per group of the near matrix's row-group layout */
   int32_t near_row_order;     /* 0: rows ordered by anchor linear index, 1: by anchor Morton code */
   int64_t near_union;         /* stored (column, group) entries; fill = nnz / (near_union * R) */
+  int32_t planar;             /* 1: one occupied z plane, S3 runs in its exact 2-D form with the
+                                 dz = 0 kernel slice (AIMX_NO_PLANAR=1 at setup keeps the 3-D path) */
+  int32_t reserved;
 } aimx_stats;
 
 /* S0 (the paper's "one-time static matrix-fill", tab:prof P:715): RWG basis,
@@ -292,7 +295,10 @@ aimx_status aimx_get_kop_static(aimx_ctx* ctx, double* CK);
  * node s = i + (n+1)(j + (n+1) k). */
 aimx_status aimx_get_weights(const aimx_ctx* ctx, double* lam);
 /* Spectrum octant, complex128 interleaved, index ((ky (N_z+1) + kz)(N_x+1) + kx):
- * which = 0 static H_hat_s, 1 the bound H_hat(k0) (unnormalised DFT). */
+ * which = 0 static H_hat_s, 1 the bound H_hat(k0) (unnormalised DFT).
+ * Planar contexts (aimx_stats.planar = 1): the 2-D spectrum of the dz = 0
+ * kernel slice, index (ky (N_x+1) + kx); it equals the 3-D octant summed over
+ * all 2 N_z values of kz, divided by 2 N_z. */
 aimx_status aimx_get_spectrum(const aimx_ctx* ctx, int which, double* out);
 
 /* ---- stage profiling (CUDA events recorded on the launching stream) ----

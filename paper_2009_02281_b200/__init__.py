@@ -50,7 +50,7 @@ class _Stats(C.Structure):
                 ("setup_seconds", C.c_double),
                 ("n", C.c_int32 * 3), ("order", C.c_int32), ("h", C.c_double),
                 ("origin", C.c_double * 3), ("near_group_rows", C.c_int32), ("near_row_order", C.c_int32),
-                ("near_union", C.c_int64)]
+                ("near_union", C.c_int64), ("planar", C.c_int32), ("reserved", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -223,11 +223,16 @@ class AIMx:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         return _P(s.cuda_stream)
 
+    def _dev(self):
+        return _torch().device("cuda", self.device)
+
     def _vec(self, x, shape):
         torch = _torch()
         if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == self.cdtype
                 and x.is_contiguous() and tuple(x.shape) == shape):
             raise ValueError(f"expected contiguous {self.cdtype} cuda tensor of shape {shape}")
+        if x.device.index != self.device:
+            raise ValueError(f"tensor on cuda:{x.device.index}, the context is on cuda:{self.device}")
         return _P(x.data_ptr())
 
     # ----------------------------------------------------------- hot path
@@ -257,7 +262,7 @@ class AIMx:
         """PMCHWT [y_E; y_H] for x = [J; M] (2N), interior eps_r (aimx_matvec_pmchwt)."""
         torch = _torch()
         if y is None:
-            y = torch.empty(2 * self.N, dtype=self.cdtype, device=x.device)
+            y = torch.empty(2 * self.N, dtype=self.cdtype, device=self._dev())
         _check(self.lib, self.lib.aimx_matvec_pmchwt(self.ctx, float(eps_r), self._vec(x, (2 * self.N,)),
                                                      self._vec(y, (2 * self.N,)), self._s(stream)), self.ctx)
         return y
@@ -266,7 +271,7 @@ class AIMx:
         """y = Kmat x at the bound frequency (aimx_matvec_kop)."""
         torch = _torch()
         if y is None:
-            y = torch.empty(self.N, dtype=self.cdtype, device=x.device)
+            y = torch.empty(self.N, dtype=self.cdtype, device=self._dev())
         _check(self.lib, self.lib.aimx_matvec_kop(self.ctx, self._vec(x, (self.N,)), self._vec(y, (self.N,)),
                                                   self._s(stream)), self.ctx)
         return y
@@ -298,7 +303,7 @@ class AIMx:
     def matvec(self, x, y=None, stream=None):
         torch = _torch()
         if y is None:
-            y = torch.empty(self.N, dtype=self.cdtype, device=x.device)
+            y = torch.empty(self.N, dtype=self.cdtype, device=self._dev())
         _check(self.lib, self.lib.aimx_matvec(self.ctx, self._vec(x, (self.N,)),
                                               self._vec(y, (self.N,)), self._s(stream)), self.ctx)
         return y
@@ -308,15 +313,15 @@ class AIMx:
         torch = _torch()
         n = X.shape[0]
         if Y is None:
-            Y = torch.empty((n, self.N), dtype=self.cdtype, device=X.device)
+            Y = torch.empty((n, self.N), dtype=self.cdtype, device=self._dev())
         _check(self.lib, self.lib.aimx_matvec_multi(self.ctx, n, self._vec(X, (n, self.N)), self._vec(Y, (n, self.N)),
                                                     self._s(stream)), self.ctx)
         return Y
 
     def matvec_parts(self, x, stream=None):
         torch = _torch()
-        yA = torch.empty(self.N, dtype=self.cdtype, device=x.device)
-        yP = torch.empty(self.N, dtype=self.cdtype, device=x.device)
+        yA = torch.empty(self.N, dtype=self.cdtype, device=self._dev())
+        yP = torch.empty(self.N, dtype=self.cdtype, device=self._dev())
         _check(self.lib, self.lib.aimx_matvec_parts(self.ctx, self._vec(x, (self.N,)),
                                                     self._vec(yA, (self.N,)),
                                                     self._vec(yP, (self.N,)), self._s(stream)),
@@ -328,7 +333,7 @@ class AIMx:
         f = np.ascontiguousarray(freqs, dtype=np.float64)
         nf = f.shape[0]
         if Y is None:
-            Y = torch.empty((nf, self.N), dtype=self.cdtype, device=X.device)
+            Y = torch.empty((nf, self.N), dtype=self.cdtype, device=self._dev())
         _check(self.lib, self.lib.aimx_sweep(self.ctx, nf, f.ctypes.data_as(C.POINTER(C.c_double)),
                                              self._vec(X, (nf, self.N)), self._vec(Y, (nf, self.N)),
                                              int(batch), self._s(stream)), self.ctx)
@@ -341,7 +346,7 @@ class AIMx:
         f = np.ascontiguousarray(freqs, dtype=np.float64)
         nf = f.shape[0]
         if X is None:
-            X = torch.empty((nf, self.N), dtype=self.cdtype, device=RHS.device)
+            X = torch.empty((nf, self.N), dtype=self.cdtype, device=self._dev())
         its = np.zeros(nf, np.int32)
         rr = np.zeros(nf, np.float64)
         _check(self.lib, self.lib.aimx_solve(self.ctx, nf, f.ctypes.data_as(C.POINTER(C.c_double)),
@@ -375,7 +380,7 @@ class AIMx:
                 "batch_slots": s.batch_slots, "setup_seconds": s.setup_seconds,
                 "n": tuple(s.n), "order": s.order, "h": s.h, "origin": tuple(s.origin),
                 "near_group_rows": s.near_group_rows, "near_row_order": s.near_row_order,
-                "near_union": s.near_union}
+                "near_union": s.near_union, "planar": bool(s.planar)}
 
     STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
 
@@ -445,6 +450,7 @@ class AIMx:
     def spectrum(self, which: int = 0):
         st = self.stats()
         nx, ny, nz = st["n"]
-        out = np.empty((ny + 1) * (nx + 1) * (nz + 1) * 2)
+        nz1 = 1 if st["planar"] else nz + 1   # planar: the dz = 0 slice's 2-D spectrum
+        out = np.empty((ny + 1) * (nx + 1) * nz1 * 2)
         _check(self.lib, self.lib.aimx_get_spectrum(self.ctx, int(which), _P(out.ctypes.data)), self.ctx)
-        return out.view(np.complex128).reshape(ny + 1, nz + 1, nx + 1)
+        return out.view(np.complex128).reshape(ny + 1, nz1, nx + 1)

@@ -208,7 +208,8 @@ constexpr int near_chw(bool f32, int slots) { return (f32 ? 32 : 16) / (slots >=
 // Octant layout (all spectra): index ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.
 struct SpectrumPlan {
   int Nx = 0, Ny = 0, Nz = 0;
-  int64_t noct = 0;           // (Nx+1)(Ny+1)(Nz+1)
+  int nz1 = 0;                // z samples: Nz+1, or 1 (planar: the dz = 0 slice, 2-D transform); 0 -> Nz+1
+  int64_t noct = 0;           // (Nx+1)(Ny+1) nz1
   double h = 0;
   int batch = 0;              // work buffers hold `batch` octants
   void* tw64[3] = {nullptr, nullptr, nullptr};   // fp64 twiddles, L = 2N per axis
@@ -284,6 +285,12 @@ struct HotDev {
   int32_t* line_id = nullptr;    // [nlines] y + Ny z
   int32_t* zplanes = nullptr;    // [nzocc]
   int zplane0 = 0;               // the first occupied z plane (the z pass's one-plane form)
+  // planar path (one occupied z plane, one-GPU contexts): bufA / bufC / phi hold
+  // that plane only (line ids y, node indices lin - phi_off), bufB is absent and
+  // S3 is x fwd -> y fwd * H_hat2 * y inv (k_yconv_plane) -> x inv with the
+  // 2-D spectrum of the dz = 0 kernel slice [ky][kx]
+  int planar = 0;
+  int64_t phi_off = 0;           // linear grid index of phi's node 0 (planar: z0 Nx Ny)
   uint8_t* line_occ = nullptr;   // [Ny*Nz]
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)

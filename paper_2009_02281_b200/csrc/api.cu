@@ -74,6 +74,7 @@ struct aimx_ctx {
   std::unique_ptr<SlabExchange> xchg;
   void* comm = nullptr;                    // ncclComm_t
   int slots = 0;
+  bool planar = false;          // one occupied z plane: the 2-D S3 path (HotDev::planar)
   void* Hoct = nullptr;         // bound spectra [slots][noct], compute precision, scaled 1/M
   // linear-term modification (aimx_set_linear_term), built on first use
   int32_t* lin_col = nullptr;   // [nb][kLinW] overlapping columns
@@ -345,7 +346,13 @@ void build_gather(aimx_ctx* c, HotDev& h, const NodeMap& m) {
   h.node_ptr = dupload(c, m.node_ptr);
   h.node_line = dupload(c, m.node_line);
   h.ent_rwg = dupload(c, m.ent_rwg);
-  h.line_id = dupload(c, m.line_id);
+  if (h.planar) {   // bufA / bufC hold the one occupied plane: line id = y
+    std::vector<int32_t> lid(m.line_id);
+    for (auto& v : lid) v -= m.zplanes[0] * t.n[1];
+    h.line_id = dupload(c, lid);
+  } else {
+    h.line_id = dupload(c, m.line_id);
+  }
   h.zplanes = dupload(c, m.zplanes);
   h.zplane0 = m.zplanes.empty() ? 0 : m.zplanes[0];
   h.line_occ = dupload(c, m.line_occ);
@@ -390,6 +397,8 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   h.rwg_base = dupload(c, base);
   NearGroups grp;
   build_near_groups(t, c->nz, grp, rows);
+  if (h.planar)   // phi holds the occupied plane only
+    for (auto& v : grp.wnode) v -= (int32_t)h.phi_off;
   if (grp.ptr.back() > (int64_t)INT32_MAX || grp.wptr.back() > (int64_t)INT32_MAX)
     throw Error(AIMX_E_GRID, "near matrix too large");
   h.R = grp.R;
@@ -473,9 +482,12 @@ int choose_slots(aimx_ctx* c) {
   const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
   const int64_t Nx = t.n[0], Ny = t.n[1], Nz = t.n[2];
   const int64_t nS = (int64_t)c->nodes.line_id.size() * Nx * 4;
-  const int64_t nA = Nz * Ny * 2 * Nx * 4, nB = Nz * 2 * Ny * 2 * Nx * 4, nP = Nx * Ny * Nz * 4;
-  const int64_t noct = (Nx + 1) * (Ny + 1) * (Nz + 1);
-  const int64_t per_freq = (int64_t)cs * (nS + 2 * nA + nB + nP + noct) + 2 * (int64_t)sizeof(double2) * noct;
+  const int64_t nz = c->planar ? 1 : Nz;   // planes held by bufA / bufC / phi
+  const int64_t nA = nz * Ny * 2 * Nx * 4, nB = c->planar ? 0 : Nz * 2 * Ny * 2 * Nx * 4, nP = Nx * Ny * nz * 4;
+  const int64_t noct = (Nx + 1) * (Ny + 1) * (c->planar ? 1 : Nz + 1);
+  // S, bufA, bufC, bufB, phi (double-buffered), the spectra (bound + 2 sweep
+  // buffers) and the spectrum plan's two fp64 work octants
+  const int64_t per_freq = (int64_t)cs * (nS + 2 * nA + nB + 2 * nP + 3 * noct) + 2 * (int64_t)sizeof(double2) * noct;
   // per-frequency grid buffers within 6 GB (of 180 GB): cfg3 gets 8 slots, its
   // 16-point sweep +17% over 2 slots (measured 1566 / 1691 / 1827 / 1730
   // freq-pts/s at 2 / 4 / 8 / 16)
@@ -494,9 +506,10 @@ template <typename P> P* zalloc(aimx_ctx* c, int64_t bytes) {
 // static spectrum (fp64, and its compute-precision copy) and the spectrum plan
 void setup_spectrum(aimx_ctx* c) {
   const Topology& t = c->topo;
-  const int64_t noct = (int64_t)(t.n[0] + 1) * (t.n[1] + 1) * (t.n[2] + 1);
   c->sp.Nx = t.n[0]; c->sp.Ny = t.n[1]; c->sp.Nz = t.n[2]; c->sp.h = t.h;
+  c->sp.nz1 = c->planar ? 1 : t.n[2] + 1;
   spectrum_plan_init(c->sp, c->slots, c->stream);
+  const int64_t noct = c->sp.noct;
   c->Hs = dalloc<double2>(c, noct);
   spectrum_static(c->sp, c->Hs, c->stream);
   if (c->prec == AIMX_C64) {
@@ -526,31 +539,38 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   const Topology& t = c->topo;
   HotDev& h = c->hot;
   hot_common(c, h);
+  // planar grids (one occupied z plane): the exact 2-D form of S3 (SURVEY
+  // 8(d) pruning); AIMX_NO_PLANAR=1 keeps the general 3-D path
+  c->planar = c->nodes.zplanes.size() == 1 && !std::getenv("AIMX_NO_PLANAR");
+  if (c->planar) {
+    h.planar = 1;
+    h.phi_off = (int64_t)c->nodes.zplanes[0] * h.Nx * h.Ny;
+  }
   const int slots = c->slots = choose_slots(c);
   build_gather(c, h, c->nodes);
   build_near(c, h, {});
   // ---- batch slots and grid buffers
   const size_t cs = c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2);
+  const int64_t nzb = c->planar ? 1 : h.Nz;   // planes held by bufA / bufC / phi
   const int64_t nS = (int64_t)h.nlines * h.Nx * 4;
-  const int64_t nA = (int64_t)h.Nz * h.Ny * 2 * h.Nx * 4;
-  const int64_t nB = (int64_t)h.Nz * 2 * h.Ny * 2 * h.Nx * 4;
-  const int64_t nP = (int64_t)h.Nx * h.Ny * h.Nz * 4;
-  const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
+  const int64_t nA = nzb * h.Ny * 2 * h.Nx * 4;
+  const int64_t nB = c->planar ? 0 : (int64_t)h.Nz * 2 * h.Ny * 2 * h.Nx * 4;
+  const int64_t nP = (int64_t)h.Nx * h.Ny * nzb * 4;
+  const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (c->planar ? 1 : h.Nz + 1);
   h.batch = slots;
   h.sS = nS; h.sA = nA; h.sB = nB; h.sP = nP; h.sH = noct;
   h.S = zalloc<char>(c, nS * slots * (int64_t)cs);
   h.bufA = zalloc<char>(c, nA * slots * (int64_t)cs);
-  h.bufB = zalloc<char>(c, nB * slots * (int64_t)cs);
+  h.bufB = nB ? zalloc<char>(c, nB * slots * (int64_t)cs) : nullptr;
   h.bufC = zalloc<char>(c, nA * slots * (int64_t)cs);
   h.phi = zalloc<char>(c, nP * slots * (int64_t)cs + 64);
   h.twx = make_twiddles(c, 2 * h.Nx);
   h.twy_tab = make_twiddles(c, 2 * h.Ny);
   h.twz_tab = make_twiddles(c, 2 * h.Nz);
-  attach_z_map(c, h);
+  if (!c->planar) attach_z_map(c, h);
   setup_spectrum(c);
   h.Hoct = c->Hoct;
   {
-    const int64_t noct = (int64_t)(h.Nx + 1) * (h.Ny + 1) * (h.Nz + 1);
     for (int k = 0; k < 2; ++k) c->HB[k] = dalloc<char>(c, noct * slots * (int64_t)cs);
     for (int k = 0; k < 2; ++k) c->XT[k] = dalloc<char>(c, (int64_t)t.nb * kMaxBatch * (int64_t)cs + 64);
     // stream priorities (experiments: AIMX_PRIO_S2 / AIMX_PRIO_S3, 0 = default, 1 = high, -1 = low)
@@ -563,6 +583,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     };
     AIMX_CUDA(cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking, prio("AIMX_PRIO_S2")));
     AIMX_CUDA(cudaStreamCreateWithPriority(&c->s3, cudaStreamNonBlocking, prio("AIMX_PRIO_S3")));
+    AIMX_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));   // CUDA-graph capture (run_matvec)
     AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
       AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_sp[k], cudaEventDisableTiming));
@@ -842,6 +863,13 @@ void do_setup_slab(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc
   finish_setup(c);
 }
 
+// Normalisation folded into the bound spectra: the inverse DFT's 1/M, M the
+// padded grid size (planar: the padded plane, 4 N_x N_y).
+double spectrum_scale(const aimx_ctx* c) {
+  const HotDev& h = c->hot;
+  return c->planar ? 1.0 / (4.0 * (double)h.Nx * h.Ny) : 1.0 / (8.0 * (double)h.Nx * h.Ny * h.Nz);
+}
+
 // S1 for B frequency points into spectrum slots 0..B-1.
 void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s, void* out = nullptr) {
   if (!out) out = c->Hoct;
@@ -850,25 +878,23 @@ void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s, void* out = nu
     if (!(f[b] > 0.0) || !std::isfinite(f[b])) throw Error(AIMX_E_INVALID_ARG, "frequency must be finite and > 0");
     k0[b] = 2.0 * kPi * f[b] / kC0;
   }
-  const HotDev& h = c->hot;
-  const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
+  const double sc1 = spectrum_scale(c);
   StageScope sc(&c->prof, 0, s);
   if (c->prec == AIMX_C64)
-    spectrum_dynamic_f32(c->sp, B, k0, (const float2*)c->Hs_T, (float)(1.0 / M), (float2*)out, s);
+    spectrum_dynamic_f32(c->sp, B, k0, (const float2*)c->Hs_T, (float)sc1, (float2*)out, s);
   else
-    spectrum_dynamic_f64(c->sp, B, k0, c->Hs, 1.0 / M, (double2*)out, s);
+    spectrum_dynamic_f64(c->sp, B, k0, c->Hs, sc1, (double2*)out, s);
 }
 
 // F_hat(k0) of the double-layer operator into c->HF (slot 0)
 void kop_spectrum(aimx_ctx* c, double f, cudaStream_t s, void* out = nullptr) {
   if (!out) out = c->HF;
   double k0[1] = {2.0 * kPi * f / kC0};
-  const HotDev& h = c->hot;
-  const double M = 8.0 * (double)h.Nx * h.Ny * h.Nz;
+  const double sc1 = spectrum_scale(c);
   if (c->prec == AIMX_C64)
-    spectrum_dynamic_f32(c->sp, 1, k0, (const float2*)c->HsF_T, (float)(1.0 / M), (float2*)out, s, 1);
+    spectrum_dynamic_f32(c->sp, 1, k0, (const float2*)c->HsF_T, (float)sc1, (float2*)out, s, 1);
   else
-    spectrum_dynamic_f64(c->sp, 1, k0, c->HsF, 1.0 / M, (double2*)out, s, 1);
+    spectrum_dynamic_f64(c->sp, 1, k0, c->HsF, sc1, (double2*)out, s, 1);
 }
 
 void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
@@ -968,7 +994,6 @@ void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaSt
   const bool repeat = same(c->last_mv);
   c->last_mv = {x, y0, y1, mode, c->f, nullptr, 0};
   if (!repeat) return eager(s);
-  if (!c->cap) AIMX_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
   const int64_t n0 = launch_counter();
   AIMX_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeRelaxed));
   cudaGraph_t graph = nullptr;
@@ -1022,6 +1047,29 @@ void check_sticky(aimx_ctx* c) {
 }
 
 cudaStream_t pick(aimx_ctx* c, void* s) { return s ? (cudaStream_t)s : c->stream; }
+
+// Stream ordering (include/aimx.h): every call that enqueues work waits, on
+// its stream, for the spectra it reads (ev_spec) and for the last call that
+// used the context's buffers on any stream (ev_use); when done it records
+// ev_use (and ev_spec if it rewrote the bound spectra) and, on a user stream,
+// makes the context stream wait for it.  So calls on different streams never
+// overlap on the shared buffers (S, bufA-C, phi, xt, the spectra).  A wait on
+// an event last recorded on the same stream costs nothing.
+void enter_stream(aimx_ctx* c, cudaStream_t s) {
+  AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
+  AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
+}
+void leave_stream(aimx_ctx* c, cudaStream_t s, bool spec_written = false) {
+  if (spec_written) AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
+  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
+}
+// host-side state changes (set_kop / cfie / linear term / conventional):
+// every call in flight on any stream has finished
+void quiesce(aimx_ctx* c) {
+  AIMX_CUDA(cudaEventSynchronize(c->ev_use));
+  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+}
 
 void destroy_impl(aimx_ctx* c) {
   if (!c) return;
@@ -1426,10 +1474,7 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  if (s != c->stream) {
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
-  }
+  enter_stream(c, s);
   const bool had = c->freq_set;
   const double f0 = c->f;
   const int B = (c->aim_on || c->cfie_on) ? 1 : sweep_batch(c, 0, nf);   // AIM / CFIE: one frequency at a time
@@ -1441,9 +1486,7 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
   }
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
-  AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
-  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
-  if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
+  leave_stream(c, s, true);
   AIMX_API_END(c)
 }
 
@@ -1465,9 +1508,9 @@ aimx_status aimx_set_frequency(aimx_ctx* c, double f_hz) {
   AIMX_API_BEGIN
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
-  AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
+  enter_stream(c, c->stream);
   bind_frequency(c, f_hz, c->stream);
-  AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
+  leave_stream(c, c->stream, true);
   AIMX_API_END(c)
 }
 
@@ -1511,7 +1554,7 @@ aimx_status aimx_set_linear_term(aimx_ctx* c, int enable) {
   AIMX_API_BEGIN
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
-  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  quiesce(c);
   if (enable && c->aim_on) throw Error(AIMX_E_INVALID_ARG, "the linear-term modification is an AIMx option (conventional AIM mode is on)");
   if (enable && !c->lin_col) build_linear(c);
   clear_graphs(c);
@@ -1533,7 +1576,7 @@ aimx_status aimx_set_conventional(aimx_ctx* c, int enable) {
   if (enable && c->slab) throw Error(AIMX_E_UNSUPPORTED, "conventional AIM mode: one-GPU contexts only");
   if (enable && c->lin_on) throw Error(AIMX_E_INVALID_ARG, "turn the linear-term modification off first");
   if (enable && c->cfie_on) throw Error(AIMX_E_INVALID_ARG, "turn the CFIE off first");
-  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  quiesce(c);
   if (enable && !c->aimDA) {
     ensure_side(c);
     const int64_t nnz = c->topo.rowptr[c->topo.nb];
@@ -1544,9 +1587,9 @@ aimx_status aimx_set_conventional(aimx_ctx* c, int enable) {
   clear_graphs(c);
   c->aim_on = enable != 0;
   if (c->aim_on && c->freq_set) {   // the bound frequency's near fill
-    AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
+    enter_stream(c, c->stream);
     launch_aim_fill(c->topo, c->sd, c->k0, c->prec == AIMX_C64, c->aimDA, c->aimDR, c->stream);
-    AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
+    leave_stream(c, c->stream, true);
   }
   AIMX_API_END(c)
 }
@@ -1590,9 +1633,9 @@ static aimx_status matvec_common(aimx_ctx* c, const void* x, void* y0, void* y1,
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
+  enter_stream(c, s);
   run_matvec(c, x, y0, y1, mode, s);
-  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  leave_stream(c, s);
   AIMX_API_END(c)
 }
 
@@ -1717,16 +1760,11 @@ aimx_status aimx_sweep(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
   cudaStream_t s = pick(c, stream);
   const bool had = c->freq_set;
   const double f0 = c->f;
-  if (s != c->stream) {
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
-  }
+  enter_stream(c, s);
   sweep_impl(c, sweep_plan(c, batch, nf), f_hz, (const char*)X, (char*)Y, s);
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
-  AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
-  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
-  if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(c->stream, c->ev_use, 0));
+  leave_stream(c, s, true);
   AIMX_API_END(c)
 }
 
@@ -1766,10 +1804,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   char* dY = dX + CH * vb;
   const bool had = c->freq_set;
   const double f0 = c->f;
-  if (s != c->stream) {
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
-  }
+  enter_stream(c, s);
   // per device batch: host->device copy on one copy stream, device->host on
   // another, ordered with the batch's compute by events, so both directions
   // overlap the other batches' compute
@@ -1809,8 +1844,7 @@ aimx_status aimx_sweep_host(aimx_ctx* c, int64_t nf, const double* f_hz, const v
   }
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
-  AIMX_CUDA(cudaEventRecord(c->ev_spec, s));
-  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  leave_stream(c, s, true);
   AIMX_CUDA(cudaStreamSynchronize(s));
   AIMX_API_END(c)
 }
@@ -1834,6 +1868,7 @@ aimx_status aimx_get_stats(const aimx_ctx* c, aimx_stats* o) {
   o->near_group_rows = c->near_R;
   o->near_row_order = c->near_order;
   o->near_union = c->near_union;
+  o->planar = c->planar ? 1 : 0;
   return AIMX_OK;
 }
 
@@ -1933,7 +1968,7 @@ static void build_kop(aimx_ctx* c) {
     c->ck_T = ck;
     c->ckpv_T = ckpv;
   }
-  const int64_t noct = (int64_t)(t.n[0] + 1) * (t.n[1] + 1) * (t.n[2] + 1);
+  const int64_t noct = c->sp.noct;
   c->HsF = dalloc<double2>(c, noct);
   spectrum_static(c->sp, c->HsF, c->stream, 1);
   if (f32) {
@@ -1944,9 +1979,9 @@ static void build_kop(aimx_ctx* c) {
     c->HsF_T = c->HsF;
   }
   c->HF = dalloc<char>(c, noct * (int64_t)cs);
-  const int64_t nP = (int64_t)t.n[0] * t.n[1] * t.n[2] * 4;
-  c->kphi1 = zalloc<char>(c, nP * c->slots * (int64_t)cs + 64);
-  c->kphi2 = zalloc<char>(c, nP * c->slots * (int64_t)cs + 64);
+  const int64_t nP = c->hot.sP;   // one column, compact potentials (batch 1)
+  c->kphi1 = zalloc<char>(c, nP * (int64_t)cs + 64);
+  c->kphi2 = zalloc<char>(c, nP * (int64_t)cs + 64);
   AIMX_CUDA(cudaStreamSynchronize(c->stream));
 }
 
@@ -1957,12 +1992,12 @@ aimx_status aimx_set_kop(aimx_ctx* c, int enable) {
   if (!enable && c->cfie_on) throw Error(AIMX_E_INVALID_ARG, "turn the CFIE off first");
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
-  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  quiesce(c);
   if (enable && !c->HsF) build_kop(c);
   c->kop_on = enable != 0;
   if (c->kop_on && c->freq_set) {
     kop_spectrum(c, c->f, c->stream);
-    AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
+    leave_stream(c, c->stream, true);
   }
   AIMX_API_END(c)
 }
@@ -1981,10 +2016,7 @@ aimx_status aimx_matvec_multi(aimx_ctx* c, int64_t nrhs, const void* X, void* Y,
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  if (s != c->stream) {
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
-  }
+  enter_stream(c, s);
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   for (int64_t i = 0; i < nrhs; i += c->hot.batch) {
     const int B = (int)std::min<int64_t>(c->hot.batch, nrhs - i);
@@ -1995,7 +2027,7 @@ aimx_status aimx_matvec_multi(aimx_ctx* c, int64_t nrhs, const void* X, void* Y,
     if (c->prec == AIMX_C64) hot_matvec_f32(h, (const char*)X + i * vb, (char*)Y + i * vb, nullptr, cb, s, &c->prof);
     else hot_matvec_f64(h, (const char*)X + i * vb, (char*)Y + i * vb, nullptr, cb, s, &c->prof);
   }
-  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  leave_stream(c, s);
   AIMX_API_END(c)
 }
 
@@ -2006,7 +2038,7 @@ aimx_status aimx_set_cfie(aimx_ctx* c, int enable) {
   if (enable && c->aim_on) throw Error(AIMX_E_INVALID_ARG, "turn the conventional AIM mode off first");
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
-  AIMX_CUDA(cudaStreamSynchronize(c->stream));
+  quiesce(c);
   if (enable) {
     if (!c->HsF) build_kop(c);
     if (!c->ktmp) c->ktmp = dalloc<char>(c, c->topo.nb * (int64_t)(c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2)));
@@ -2017,7 +2049,7 @@ aimx_status aimx_set_cfie(aimx_ctx* c, int enable) {
   }
   clear_graphs(c);
   c->cfie_on = enable != 0;
-  AIMX_CUDA(cudaEventRecord(c->ev_spec, c->stream));
+  leave_stream(c, c->stream, true);
   AIMX_API_END(c)
 }
 
@@ -2031,10 +2063,10 @@ aimx_status aimx_matvec_kop(aimx_ctx* c, const void* x, void* y, void* stream) {
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  if (s != c->stream) AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
+  enter_stream(c, s);
   kop_matvec(c->prec == AIMX_C64, c->hot, x, y, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr,
              c->sd.col, c->ck_T, s);
-  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  leave_stream(c, s);
   AIMX_API_END(c)
 }
 
@@ -2054,14 +2086,11 @@ aimx_status aimx_matvec_pmchwt(aimx_ctx* c, double eps_r, const void* x, void* y
   AIMX_CUDA(cudaSetDevice(c->device));
   check_sticky(c);
   cudaStream_t s = pick(c, stream);
-  if (s != c->stream) {
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_spec, 0));
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_use, 0));
-  }
+  enter_stream(c, s);
   const bool f32 = c->prec == AIMX_C64;
   const int64_t nb = c->hot.nb;
   const size_t cs = f32 ? sizeof(float2) : sizeof(double2);
-  const int64_t noct = (int64_t)(c->hot.Nx + 1) * (c->hot.Ny + 1) * (c->hot.Nz + 1);
+  const int64_t noct = c->sp.noct;
   if (!c->pm_H1) {
     c->pm_H1 = dalloc<char>(c, noct * (int64_t)cs);
     c->pm_HF1 = dalloc<char>(c, noct * (int64_t)cs);
@@ -2101,7 +2130,7 @@ aimx_status aimx_matvec_pmchwt(aimx_ctx* c, double eps_r, const void* x, void* y
       gm_axpy(f32, nb, src ? -1.0 : 1.0, tK, src ? yE : yH, s);   // y_E -= K M, y_H += K J
     }
   }
-  AIMX_CUDA(cudaEventRecord(c->ev_use, s));
+  leave_stream(c, s);
   AIMX_API_END(c)
 }
 
@@ -2152,7 +2181,7 @@ aimx_status aimx_get_spectrum(const aimx_ctx* cc, int which, double* out) {
   if (which == 0) {
     AIMX_CUDA(cudaMemcpy(out, c->Hs, n * sizeof(double2), cudaMemcpyDeviceToHost));
   } else {
-    const double M = 8.0 * (double)c->hot.Nx * c->hot.Ny * c->hot.Nz;
+    const double M = 1.0 / spectrum_scale(c);
     if (c->prec == AIMX_C64) {
       std::vector<float2> tmp(n);
       AIMX_CUDA(cudaMemcpy(tmp.data(), c->Hoct, n * sizeof(float2), cudaMemcpyDeviceToHost));

@@ -602,6 +602,65 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
   if (threadIdx.x == 0) bulk_wait0();
 }
 
+// ---- planar grids (h.planar, one occupied z plane z0): y fwd * H_hat2 * y inv
+// in one pass, bufA[y < Ny][col] -> bufC[y < Ny, occupied][col].  With all
+// sources and potentials on z0 the z transform pair collapses exactly and the
+// padded 3-D convolution is the padded 2-D one with the dz = 0 kernel slice,
+// whose spectrum H_hat2[ky][kx] (scaled by 1/(4 N_x N_y)) is generated per
+// frequency (spectrum.cu, planar plan).  The CTA's slab of H_hat2 (the octant
+// rows ky <= N_y of its CW/4 kx, mirrored on read) is staged in shared memory
+// while the forward transform runs.
+template <typename T, int L>
+__global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<T, L>;
+  const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
+  const int W = h.W, Nx = h.Nx, Ny = h.Ny;
+  const ColTile ct = col_tile<T, L>(line, W);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* tw = reinterpret_cast<T2*>(smem_raw);
+  T2* xb = tw + L + line * G::XB;
+  T2* hs = tw + L + (size_t)G::NL * G::XB;          // [ky <= Ny][kx - kx0]
+  const int nkx = ct.CW / 4, kx0 = h.kx0 + (blockIdx.x * ct.CW) / 4;
+  const int b = blockIdx.z;
+  const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = ((const T2*)h.twy_tab)[i];
+  for (int i = threadIdx.x; i < (L / 2 + 1) * nkx; i += blockDim.x) {
+    const int ky = i / nkx, kx = kx0 + i % nkx;
+    hs[i] = Hb[(int64_t)ky * (Nx + 1) + (kx <= Nx ? kx : 2 * Nx - kx)];
+  }
+  __syncthreads();
+  const bool act = ct.rsub == 0;   // one plane: the column tile's first row set only
+  const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
+  const uint8_t* __restrict__ occ = h.line_occ + (int64_t)h.zplane0 * Ny;
+  const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + col;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {   // y < Ny = L/2  <=>  n2 < R2/2; unoccupied rows are zero
+    const int y = G::TL::in_index(t, i);
+    v[i] = (act && i % G::R2 < G::R2 / 2 && occ[y]) ? in[(int64_t)y * W] : mk<T2>(0, 0);
+  }
+  fwd_fft<T2, L>(v, xb, tw, t);
+  {
+    const T2* hl = hs + (ct.w >> 2);
+#pragma unroll
+    for (int i = 0; i < G::E; ++i) {
+      const int ky = TwoLevel<G::R2, G::R1>::in_index(t, i);
+      v[i] = cmul(v[i], hl[(ky <= L / 2 ? ky : L - ky) * nkx]);
+    }
+  }
+  inv_fft_swapped<T2, L>(v, xb, tw, t);
+  if (!act) return;
+  T2* __restrict__ out = (T2*)h.bufC + b * h.sA + col;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {
+    const int y = G::TL::in_index(t, i);
+    if (i % G::R2 < G::R2 / 2 && occ[y]) out[(int64_t)y * W] = v[i];
+  }
+}
+
 // ---- fused y fwd -> (z fwd * H_hat * z inv) -> y inv for short y and z
 // transforms (2 N_y, 2 N_z <= 32): one CTA owns a tile of TW grid columns
 // (col = 4 kx + channel) and all (y, z) of them in shared memory, every line
@@ -1201,6 +1260,14 @@ void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combin
   else run_interp_r<T, 8>(h, x, y0, y1, c, s);
 }
 
+template <typename T, int L> void run_yconv_plane(const HotDev& h, int B, cudaStream_t s) {
+  constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)(L / 2 + 1) * (PassGeom<T, L>::NL / 4);
+  set_smem(k_yconv_plane<T, L>, sm);
+  dim3 g = col_grid<T, L>(h.W, 1, B);
+  launch_pdl(k_yconv_plane<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
+  AIMX_CHECK_LAUNCH();
+}
+
 // y fwd + z conv + y inv in one kernel when both transforms are short
 // (reported as stage 3, zconv)
 template <typename T, int LY, int LZ> void launch_yz(const HotDev& h, int B, cudaStream_t s) {
@@ -1228,11 +1295,27 @@ template <typename T> bool run_yz_fused(const HotDev& h, int B, cudaStream_t s, 
   return true;
 }
 
+// S3 between the x transforms: the planar y pass, the fused short y/z pass,
+// or y fwd / z conv / y inv (reported as stages 2, 3, 4; fused forms as 3)
+template <typename T>
+void grid_conv(const HotDev& h, int B, cudaStream_t s, Profiler* prof) {
+  const int Ly = 2 * h.Ny, Lz = 2 * h.Nz;
+  if (h.planar) {
+    StageScope sc(prof, 3, s);
+    AIMX_SWITCH_L(Ly, (run_yconv_plane<T, L>(h, B, s)));
+    return;
+  }
+  if (run_yz_fused<T>(h, B, s, prof)) return;
+  { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, B, s))); }
+  { StageScope sc(prof, 3, s); AIMX_SWITCH_L(Lz, (run_z<T, L>(h, B, s))); }
+  { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, B, s))); }
+}
+
 // S2 + S3 (+ x inverse): the grid part of a matvec, up to the potentials phi
 template <typename T>
 void hot_grid(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, Profiler* prof) {
   if (c.B < 1 || c.B > h.batch || c.B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "bad batch");
-  const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz, B = c.B;
+  const int Lx = 2 * h.Nx, B = c.B;
   {
     StageScope sc(prof, 1, s);
     if (!c.xt_ready) run_interleave<T>(h, x, c, s);   // xt: batch-interleaved columns (gather, S4+S5)
@@ -1240,11 +1323,7 @@ void hot_grid(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, 
     else run_gather_b<T>(h, B, s);
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, B, s)));
   }
-  if (!run_yz_fused<T>(h, B, s, prof)) {
-    { StageScope sc(prof, 2, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, B, s))); }
-    { StageScope sc(prof, 3, s); AIMX_SWITCH_L(Lz, (run_z<T, L>(h, B, s))); }
-    { StageScope sc(prof, 4, s); AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, B, s))); }
-  }
+  grid_conv<T>(h, B, s, prof);
   { StageScope sc(prof, 5, s); AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, B, s))); }
 }
 
@@ -1315,8 +1394,8 @@ __global__ void k_kop_interp(HotDev h, const typename CT<T>::T2* __restrict__ ph
     const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
     const int lin = base + i + Nx * (j + Ny * k);
     const double s0 = lin % Nx - Nx / 2, s1 = (lin / Nx) % Ny - Ny / 2, s2 = lin / (Nx * Ny) - h.Nz / 2;
-    const T2* a = phi1 + (int64_t)lin * ns;
-    const T2* b = phi2 + (int64_t)lin * ns;
+    const T2* a = phi1 + (int64_t)(lin - h.phi_off) * ns;
+    const T2* b = phi2 + (int64_t)(lin - h.phi_off) * ns;
     const double ax = a[0].x, ay = a[h.batch].x, az = a[2 * h.batch].x;
     const double axi = a[0].y, ayi = a[h.batch].y, azi = a[2 * h.batch].y;
     const double px = -hg * ((s1 * az - s2 * ay) - b[0].x), pxi = -hg * ((s1 * azi - s2 * ayi) - b[0].y);
@@ -1345,16 +1424,12 @@ void hot_kop(const HotDev& h0, const void* x, void* y, const void* HF, void* phi
   HotDev h = h0;
   h.Hoct = const_cast<void*>(HF);
   h.batch = 1;   // one column: compact potentials ([node][channel])
-  const int Lx = 2 * h.Nx, Ly = 2 * h.Ny, Lz = 2 * h.Nz;
+  const int Lx = 2 * h.Nx;
   run_gather<T>(h, x, h.nb, 1, s);   // S = P x (one column)
   auto conv = [&](void* phi) {
     h.phi = phi;
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, 1, s)));
-    if (!run_yz_fused<T>(h, 1, s, nullptr)) {
-      AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, 1, s)));
-      AIMX_SWITCH_L(Lz, (run_z<T, L>(h, 1, s)));
-      AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, 1, s)));
-    }
+    grid_conv<T>(h, 1, s, nullptr);
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, 1, s)));
   };
   conv(phi1);                                   // F (*) J

@@ -17,6 +17,11 @@
 // H_hat_s and scales by 1/M (the inverse-FFT normalisation is folded into the
 // spectrum).  B frequencies per launch.
 // Octant layout ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.
+// Planar grids (one occupied z plane, sp.nz1 = 1): only the dz = 0 slice of K
+// is sampled and transformed in 2-D, layout (ky (N_x+1) + kx); for sources and
+// potentials on one plane the padded 3-D convolution equals the padded 2-D
+// convolution with that slice (SURVEY 8(d) "exact algebraic pruning"), and
+// sum_kz H_hat3(kx, ky, kz) = 2 N_z H_hat2(kx, ky).
 #include <cmath>
 #include <vector>
 
@@ -34,7 +39,7 @@ namespace {
 // slots; fp64.  (The dynamic samples are generated inside the x pass, ksample.)
 // kind 1: F_s = 1/(4 pi r^3) (the radial factor of grad G_s = -r F_s; the
 // double-layer operator's grid form, NEXT #1), 0 at r = 0
-__global__ void k_sample_static(int Nx, int Ny, int Nz, int64_t noct, double h, double2* __restrict__ out,
+__global__ void k_sample_static(int Nx, int Ny, int Nz, int nz1, int64_t noct, double h, double2* __restrict__ out,
                                 int kind) {
   pdl_wait();
   pdl_trigger();
@@ -42,8 +47,8 @@ __global__ void k_sample_static(int Nx, int Ny, int Nz, int64_t noct, double h, 
   if (idx >= noct) return;
   int i = (int)(idx % (Nx + 1));
   int64_t r2 = idx / (Nx + 1);
-  int l = (int)(r2 % (Nz + 1));
-  int j = (int)(r2 / (Nz + 1));
+  int l = (int)(r2 % nz1);
+  int j = (int)(r2 / nz1);
   double re = 0.0;
   if (i < Nx && j < Ny && l < Nz) {
     int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
@@ -122,6 +127,7 @@ __device__ __forceinline__ typename CT<T>::T2 ksample(int i, int j, int l, int N
 
 struct SampleArgs {
   int Nx, Ny, Nz;
+  int nz1;    // z samples per (ky, kx): N_z + 1, or 1 for the planar (dz = 0) spectrum
   double h;
   double k0[kMaxBatch];
   int kind;   // 0: K_d (eq:hgfd), 1: F_d (double-layer operator)
@@ -165,7 +171,7 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
   T2 v[G::E];
   if constexpr (MODE == 1) {   // row pass over x: line lg = j (Nz+1) + l, element n = i
     const int64_t lg = (int64_t)blockIdx.x * G::NL + line;
-    const int jj = (int)(lg / (sa.Nz + 1)), ll = (int)(lg % (sa.Nz + 1));
+    const int jj = (int)(lg / sa.nz1), ll = (int)(lg % sa.nz1);
     const double k0 = sa.k0[blockIdx.z];
     if constexpr (G::XB >= N1) {
       // each of the N1 samples once, staged in the line's exchange buffer
@@ -352,8 +358,12 @@ bool evyz(const SpectrumPlan& sp, int B, const void* in, void* out, const void* 
 template <typename T>
 void dct3(SpectrumPlan& sp, int B, void** tw, void* a, void* b, void* out, const void* add, T scale,
           cudaStream_t s, const SampleArgs* gen = nullptr) {
-  const int64_t nx = sp.Nx + 1, ny = sp.Ny + 1, nz = sp.Nz + 1, no = sp.noct;
+  const int64_t nx = sp.Nx + 1, ny = sp.Ny + 1, nz = sp.nz1, no = sp.noct;
   even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s, gen);
+  if (sp.nz1 == 1) {   // planar: the dz = 0 slice, a 2-D transform (x rows, y cols)
+    even_cols<T>(2 * sp.Ny, 1, nx, no, B, b, out, tw[1], add, scale, s);
+    return;
+  }
   if (evyz<T>(sp, B, b, out, add, scale, s)) return;
   even_cols<T>(2 * sp.Nz, ny, nx, no, B, b, a, tw[2], nullptr, (T)1, s);
   even_cols<T>(2 * sp.Ny, 1, nz * nx, no, B, a, out, tw[1], add, scale, s);
@@ -382,7 +392,8 @@ void spectrum_plan_init(SpectrumPlan& sp, int batch, cudaStream_t s) {
   make(2 * sp.Nx, 0);
   make(2 * sp.Ny, 1);
   make(2 * sp.Nz, 2);
-  sp.noct = (int64_t)(sp.Nx + 1) * (sp.Ny + 1) * (sp.Nz + 1);
+  if (sp.nz1 <= 0) sp.nz1 = sp.Nz + 1;
+  sp.noct = (int64_t)(sp.Nx + 1) * (sp.Ny + 1) * sp.nz1;
   sp.batch = batch < 1 ? 1 : batch;
   AIMX_CUDA(cudaMalloc(&sp.work0, sizeof(double2) * sp.noct * sp.batch));
   AIMX_CUDA(cudaMalloc(&sp.work1, sizeof(double2) * sp.noct * sp.batch));
@@ -400,7 +411,7 @@ void spectrum_plan_free(SpectrumPlan& sp) {
 
 void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s, int kind) {
   launch_pdl(k_sample_static, dim3((unsigned)((sp.noct + 255) / 256)), dim3(256), 0, s, sp.Nx, sp.Ny, sp.Nz,
-             sp.noct, sp.h, (double2*)sp.work0, kind);
+             sp.nz1, sp.noct, sp.h, (double2*)sp.work0, kind);
   AIMX_CHECK_LAUNCH();
   dct3<double>(sp, 1, sp.tw64, sp.work0, sp.work1, out, nullptr, 1.0, s);
 }
@@ -408,7 +419,7 @@ void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s, int kind) {
 void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
                           float2* out, cudaStream_t s, int kind) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}, kind};
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.nz1, sp.h, {}, kind};
   for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
   // K_d samples generated inside the x pass (each sample once per line)
   dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s, &sa);
@@ -417,7 +428,7 @@ void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float
 void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs, double scale,
                           double2* out, cudaStream_t s, int kind) {
   if (B > sp.batch || B > kMaxBatch) throw Error(AIMX_E_INTERNAL, "spectrum batch too large");
-  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.h, {}, kind};
+  SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.nz1, sp.h, {}, kind};
   for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
   // K_d samples generated inside the x pass (each sample once per line)
   dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s, &sa);

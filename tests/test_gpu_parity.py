@@ -39,13 +39,22 @@ def test_cfg1_weights_and_static(gpu1, orc1):
         assert rel_l2(s[key], ref) <= 1e-12, key
 
 
+def _octant_ref(op, H):
+    """The oracle's padded spectrum H [2Nz, 2Ny, 2Nx] in the library's layout
+    [ky, kz, kx]: the octant, or for planar contexts the dz = 0 slice's 2-D
+    spectrum, sum over kz of H / (2 N_z) (the inverse z-DFT at dz = 0)."""
+    Nz2, Ny2, Nx2 = H.shape
+    Nx, Ny, Nz = Nx2 // 2, Ny2 // 2, Nz2 // 2
+    if op.stats()["planar"]:
+        H = H.sum(axis=0, keepdims=True) / Nz2
+        Nz = 0
+    return np.transpose(H[: Nz + 1, : Ny + 1, : Nx + 1], (1, 0, 2))
+
+
 def test_cfg1_static_spectrum(gpu1, orc1):
     op, prec = gpu1
-    Hs = op.spectrum(0)
-    Nx, Ny, Nz = orc1.grid.n
-    ref = orc1.Hs_hat[: Nz + 1, : Ny + 1, : Nx + 1]          # [kz, ky, kx]
-    ref = np.transpose(ref, (1, 0, 2))                      # -> [ky, kz, kx]
-    assert rel_l2(Hs, ref) <= 1e-13
+    assert op.stats()["planar"]          # the plate: one occupied z plane
+    assert rel_l2(op.spectrum(0), _octant_ref(op, orc1.Hs_hat)) <= 1e-13
 
 
 @pytest.mark.parametrize("fi", [0, 1])
@@ -54,10 +63,7 @@ def test_cfg1_matvec_parts_and_combined(gpu1, orc1, fi):
     f = 150e6 if fi == 0 else 37.5e6
     op.set_frequency(f)
     orc1.set_frequency(f)
-    Hd = op.spectrum(1)
-    Nx, Ny, Nz = orc1.grid.n
-    ref = np.transpose(orc1.H_hat[: Nz + 1, : Ny + 1, : Nx + 1], (1, 0, 2))
-    assert rel_l2(Hd, ref) <= (1e-13 if prec == "c128" else 1e-6)
+    assert rel_l2(op.spectrum(1), _octant_ref(op, orc1.H_hat)) <= (1e-13 if prec == "c128" else 1e-6)
     for i in range(3):
         x = inp.rhs_vector(1, i, op.N)
         xg = to_gpu(x, prec)
@@ -330,18 +336,23 @@ def test_matvec_graph_replay_bit_identical(prec, monkeypatch):
 
 
 @pytest.mark.parametrize("prec", ["c64", "c128"])
-@pytest.mark.parametrize("world", [1, 2])
-def test_planar_single_plane_z_pass(prec, world):
-    """A planar mesh occupies ONE z plane; on a grid whose y transform is too
-    long for the fused y/z kernel the z pass takes its one-plane form (a
-    multiply by the kernel's z-sum).  Against the oracle, single context and
-    emulated slab ranks (kx-slab offsets)."""
+@pytest.mark.parametrize("path", ["planar", "3d", "slab2"])
+def test_planar_single_plane_z_pass(prec, path, monkeypatch):
+    """A planar mesh occupies ONE z plane.  planar: the 2-D form of S3 (x fwd,
+    y fwd * H_hat2 * y inv with the dz = 0 kernel slice, x inv); 3d
+    (AIMX_NO_PLANAR=1) and slab2 (emulated slab ranks, kx-slab offsets): the
+    general path, whose z pass takes its one-plane form (a multiply by the
+    kernel's z-sum) on a grid whose y transform is too long for the fused y/z
+    kernel.  Each against the oracle."""
     from oracle.aimx import AIMxOracle
     m = inp.make_mesh(1)
     n = (16, 32, 4)
     orc = AIMxOracle(m.vertices, m.triangles, n)
-    op = make_gpu_op(m, n, prec, slab=None if world == 1 else ("emulate", world))
+    if path == "3d":
+        monkeypatch.setenv("AIMX_NO_PLANAR", "1")
+    op = make_gpu_op(m, n, prec, slab=None if path != "slab2" else ("emulate", 2))
     assert op.stats()["occupied_planes"] == 1
+    assert op.stats()["planar"] == (path == "planar")
     for f in (150e6, 600e6):
         op.set_frequency(f)
         orc.set_frequency(f)
@@ -368,3 +379,39 @@ def test_matvec_multi_equals_single(prec):
         Y = op.matvec_multi(X).cpu().numpy()
         for i in (0, S - 1, S, n - 1):
             assert rel_l2(Y[i], op.matvec(X[i].contiguous()).cpu().numpy()) <= tol
+
+
+def test_calls_on_several_streams_are_ordered():
+    """Calls on different streams share the context's buffers; the library
+    orders them with events (include/aimx.h).  Interleave matvecs, parts and
+    sweeps on two side streams and the default stream with no host sync in
+    between; every result must equal the serial one bit for bit."""
+    import torch
+    op = make_gpu_op(inp.make_mesh(2), (256, 16, 4), "c64")
+    c = inp.get_config(2)
+    xs = [to_gpu(inp.rhs_vector(2, 300 + i, op.N), "c64") for i in range(6)]
+    X = to_gpu(np.stack([inp.rhs_vector(2, 310 + i, op.N) for i in range(8)]), "c64")
+    op.set_frequency(c.freqs[3])
+    ref_mv = [op.matvec(x).clone() for x in xs]
+    ref_pa = [tuple(t.clone() for t in op.matvec_parts(x)) for x in xs[:2]]
+    ref_sw = op.sweep(c.freqs[:8], X).clone()
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for rep in range(3):
+        for i, x in enumerate(xs):
+            st = (sa, sb, torch.cuda.current_stream())[i % 3]
+            with torch.cuda.stream(st):
+                outs.append(("mv", i, op.matvec(x)))
+                if i < 2:
+                    outs.append(("pa", i, op.matvec_parts(x)))
+                if i == 3:
+                    outs.append(("sw", 0, op.sweep(c.freqs[:8], X)))
+    torch.cuda.synchronize()
+    for kind, i, v in outs:
+        if kind == "mv":
+            assert torch.equal(v, ref_mv[i])
+        elif kind == "pa":
+            assert all(torch.equal(a, b) for a, b in zip(v, ref_pa[i]))
+        else:
+            assert torch.equal(v, ref_sw)

@@ -28,6 +28,20 @@ def test_fft_convolution_equals_bruteforce_toeplitz(k0):
     assert np.max(np.abs(fft - bf)) <= 1e-12 * np.abs(bf).max()
 
 
+@pytest.mark.parametrize("n", [(512, 2, 2), (2, 512, 2)])
+def test_fft_convolution_1024_point_lines(n):
+    # the padded 1024-point lines of cfg5's grid (1024 x 1024 x 16), along x
+    # and along y, against the O(N^2) definition on a thin grid (2048 nodes)
+    h, k0 = 0.013, 3.1
+    rng = np.random.default_rng(5)
+    g = np.zeros((n[2], n[1], n[0]), complex)
+    m = rng.random(g.shape) < 0.3                      # sparse sources, as on a grid
+    g[m] = rng.standard_normal(m.sum()) + 1j * rng.standard_normal(m.sum())
+    fft = conv.convolve(conv.spectrum(n, h, k0), g)
+    bf = conv.convolve_bruteforce(g, h, lambda r: K.G(k0, r), -1j * k0 / (4 * np.pi))
+    assert np.max(np.abs(fft - bf)) <= 1e-12 * np.abs(bf).max()
+
+
 def test_unit_impulse_returns_kernel_samples():
     n = (6, 5, 4)
     h = 0.5
