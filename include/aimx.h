@@ -57,7 +57,11 @@ typedef enum {
   AIMX_E_OOM = 5,          /* device or host allocation failed */
   AIMX_E_CUDA = 6,         /* CUDA runtime error (message in aimx_last_error) */
   AIMX_E_UNSUPPORTED = 7,  /* grid length with no compiled FFT kernel (see aimx.h notes) */
-  AIMX_E_INTERNAL = 8
+  AIMX_E_INTERNAL = 8,
+  AIMX_E_NCCL = 9,         /* NCCL failure, or an asynchronous NCCL error found by polling: the
+                              communicator has been aborted (sticky for the context) */
+  AIMX_E_TIMEOUT = 10      /* aimx_sync: the work did not finish in time (NCCL contexts: the
+                              communicator has been aborted, e.g. a peer rank hung or died) */
 } aimx_status;
 
 typedef enum {
@@ -342,6 +346,16 @@ aimx_status aimx_slab_plan(const int32_t n[3], int32_t order, int32_t world, int
 aimx_status aimx_setup_slab(const aimx_mesh_desc* mesh, const aimx_grid_desc* grid, aimx_prec prec,
                             int device, int32_t rank, int32_t world, const uint8_t* nccl_id,
                             void* stream, aimx_ctx** out);
+/* Wait on the host until every call enqueued on the context (any stream)
+ * has finished, polling every 0.2 ms.  NCCL (slab) contexts also poll
+ * ncclCommGetAsyncError: an asynchronous NCCL error, or no completion within
+ * timeout_s seconds (<= 0: no limit), aborts the communicator
+ * (ncclCommAbort) so the rank cannot deadlock on a dead or hung peer, and
+ * returns AIMX_E_NCCL / AIMX_E_TIMEOUT; every later call on the context then
+ * returns AIMX_E_NCCL.  Every API call also polls the asynchronous error
+ * first. */
+aimx_status aimx_sync(aimx_ctx* ctx, double timeout_s);
+
 /* ncclGetUniqueId (NCCL loaded at run time; AIMX_E_UNSUPPORTED if absent). */
 aimx_status aimx_nccl_unique_id(uint8_t id[128]);
 

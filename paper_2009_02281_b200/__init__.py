@@ -92,6 +92,7 @@ ABI_FUNCTIONS = {
     "aimx_setup_slab": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Grid), C.c_int, C.c_int, C.c_int32,
                                   C.c_int32, _P, _P, C.POINTER(_P)]),
     "aimx_nccl_unique_id": (C.c_int, [_P]),
+    "aimx_sync": (C.c_int, [_P, C.c_double]),
     "aimx_save_static": (C.c_int, [_P, C.c_char_p]),
     "aimx_solve": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_double, C.c_int32, C.c_int32,
                              C.POINTER(C.c_int32), C.POINTER(C.c_double), _P]),
@@ -206,6 +207,12 @@ class AIMx:
     def save_static(self, path: str):
         """Write the static matrices (aimx_save_static) for AIMx(..., static_cache=path)."""
         _check(self.lib, self.lib.aimx_save_static(self.ctx, os.fsencode(path)), self.ctx)
+
+    def sync(self, timeout_s: float = 0.0):
+        """Wait for every call enqueued on the context (aimx_sync); NCCL
+        contexts abort their communicator on an asynchronous NCCL error or
+        after timeout_s seconds (> 0) and raise."""
+        _check(self.lib, self.lib.aimx_sync(self.ctx, float(timeout_s)), self.ctx)
 
     def close(self):
         if getattr(self, "ctx", None):

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/aimx.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace aimx {
 
@@ -124,13 +125,17 @@ struct NearChunks {
   std::vector<unsigned char> payload;
   std::vector<int64_t> uoff_c;     // [U] payload byte offset of union entry u's C pairs
   std::vector<int64_t> uoff_w;     // [Uw] ... of the W weights
-  std::vector<int64_t> gfirst;     // [ngrp+1] first chunk of each group
+  std::vector<int64_t> gfirst;     // [ngrp] first chunk of each group
+  int64_t nchunk = 0;
   std::vector<double> cost;        // [ngrp] work estimate
 };
-// cs = bytes of one complex (= one real pair) in the compute precision
-void build_near_chunks(const NearGroups& g, int chw, int chc, int cs, NearChunks& ck);
-// chunk ranges (whole groups) per CTA
-std::vector<int32_t> near_partition(const NearChunks& ck, int64_t ngrp, int ncta);
+// cs = bytes of one complex (= one real pair) in the compute precision; the
+// chunks follow the groups in `order` (a permutation of 0..ngrp-1)
+void build_near_chunks(const NearGroups& g, int chw, int chc, int cs, NearChunks& ck,
+                       const std::vector<int64_t>& order);
+// the S4+S5 kernel's group order for `ncta` CTAs: CTA k's groups are
+// order[cta_begin[k] .. cta_begin[k+1]) (k, k + ncta, k + 2 ncta, ...)
+std::vector<int64_t> near_round_order(int64_t ngrp, int ncta, std::vector<int64_t>& cta_begin);
 
 // ---------------------------------------------------------------- device setup (fp64)
 struct SetupDev {
@@ -248,16 +253,23 @@ struct Profiler {
   ~Profiler();
 };
 
+// A hot-path stage: an NVTX range on the host thread (named like bench.py's
+// stages; visible to nsys / ncu --nvtx, a no-op without a tool attached)
+// and, when the profiler is on for it, CUDA events around its launches.
+constexpr const char* kStageNames[8] = {"aimx:spectrum", "aimx:proj_xfft", "aimx:yfwd", "aimx:zconv",
+                                        "aimx:yinv", "aimx:xinv", "aimx:interp_near", "aimx:other"};
 struct StageScope {
   Profiler* p;
   int stage;
   cudaStream_t s;
   cudaEvent_t a = nullptr;
   StageScope(Profiler* p_, int st, cudaStream_t s_) : p(p_), stage(st), s(s_) {
+    nvtxRangePushA(kStageNames[stage & 7]);
     if (p && p->on && ((p->mask >> stage) & 1)) p->begin(stage, s, a);
   }
   ~StageScope() {
     if (a) p->end(stage, s, a);
+    nvtxRangePop();
   }
 };
 

@@ -12,6 +12,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda.h>
@@ -73,6 +74,7 @@ struct aimx_ctx {
   std::vector<SlabRank> slabs;             // emulation: all ranks; NCCL: this rank
   std::unique_ptr<SlabExchange> xchg;
   void* comm = nullptr;                    // ncclComm_t
+  bool nccl_dead = false;                  // the communicator was aborted (sticky AIMX_E_NCCL)
   int slots = 0;
   bool planar = false;          // one occupied z plane: the 2-D S3 path (HotDev::planar)
   void* Hoct = nullptr;         // bound spectra [slots][noct], compute precision, scaled 1/M
@@ -410,7 +412,10 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   const bool f32 = c->prec == AIMX_C64;
   const int cs = f32 ? 8 : 16;
   if (c->slots <= 0) throw Error(AIMX_E_INTERNAL, "batch slots not chosen before the near layout");
-  build_near_chunks(grp, near_chw(f32, c->slots), near_chc(f32, c->slots), cs, ck);
+  std::vector<int64_t> cta_begin;
+  const int ncta = near_ctas_per_sm(f32, false, grp.R) * nsm;   // one wave of resident CTAs
+  const std::vector<int64_t> order = near_round_order(grp.ngrp, ncta, cta_begin);
+  build_near_chunks(grp, near_chw(f32, c->slots), near_chc(f32, c->slots), cs, ck, order);
   // value slot (u R + r) -> payload byte offset
   for (auto& v : grp.slot)
     if (v >= 0) v = ck.uoff_c[v / grp.R] + (v % grp.R) * cs;
@@ -420,14 +425,15 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   int64_t* wslot = dupload(c, grp.wslot);
   h.payload = dupload(c, ck.payload);
   h.chunks = dupload(c, ck.chunks);
-  double waves = 1.0;   // CTAs per resident slot (experiments: AIMX_NEAR_WAVES)
-  if (const char* e = std::getenv("AIMX_NEAR_WAVES")) waves = std::max(0.25, std::atof(e));
-  std::vector<int32_t> cp = near_partition(ck, grp.ngrp, (int)(waves * near_ctas_per_sm(f32, false, grp.R) * nsm));
+  // chunk range of each CTA (its groups are contiguous in `order`)
+  std::vector<int32_t> cp(cta_begin.size());
+  for (size_t k = 0; k + 1 < cta_begin.size(); ++k)
+    cp[k] = cta_begin[k] < grp.ngrp ? (int32_t)ck.gfirst[order[cta_begin[k]]] : (int32_t)ck.nchunk;
+  cp.back() = (int32_t)ck.nchunk;
   h.cta_ptr = dupload(c, cp);
   h.near_ctas = (int)cp.size() - 1;
-  cp = near_partition(ck, grp.ngrp, near_ctas_per_sm(f32, true, grp.R) * nsm);
-  h.cta_ptr1 = dupload(c, cp);
-  h.near_ctas1 = (int)cp.size() - 1;
+  h.cta_ptr1 = h.cta_ptr;   // single-column launches: the same order and CTAs
+  h.near_ctas1 = h.near_ctas;
   const SetupDev& d = c->sd;
   if (f32) {
     k_lam_to<float4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (float4*)nullptr, h.payload);
@@ -610,6 +616,8 @@ struct NcclApi {
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclGetErrorString) errorString = nullptr;
+  decltype(&ncclCommGetAsyncError) getAsyncError = nullptr;
+  decltype(&ncclCommAbort) commAbort = nullptr;
 };
 NcclApi& nccl() {
   static NcclApi api;
@@ -629,6 +637,8 @@ NcclApi& nccl() {
     api.groupEnd = (decltype(api.groupEnd))dlsym(api.lib, "ncclGroupEnd");
     api.allReduce = (decltype(api.allReduce))dlsym(api.lib, "ncclAllReduce");
     api.errorString = (decltype(api.errorString))dlsym(api.lib, "ncclGetErrorString");
+    api.getAsyncError = (decltype(api.getAsyncError))dlsym(api.lib, "ncclCommGetAsyncError");
+    api.commAbort = (decltype(api.commAbort))dlsym(api.lib, "ncclCommAbort");
   });
   if (!api.lib || !api.getUniqueId || !api.commInitRank || !api.send || !api.recv || !api.groupStart ||
       !api.groupEnd || !api.allReduce)
@@ -639,7 +649,7 @@ NcclApi& nccl() {
   do {                                                                                         \
     ncclResult_t r_ = (call);                                                                  \
     if (r_ != ncclSuccess)                                                                     \
-      throw Error(AIMX_E_CUDA, std::string("NCCL: ") + (nccl().errorString ? nccl().errorString(r_) : "error")); \
+      throw Error(AIMX_E_NCCL, std::string("NCCL: ") + (nccl().errorString ? nccl().errorString(r_) : "error")); \
   } while (0)
 
 // Exchange geometry.  Step 0 (rows -> kx slabs): rank p sends rank q the
@@ -1040,10 +1050,36 @@ aimx_status fail(aimx_ctx* c, const Error& e) {
   return e.code;
 }
 
+// abort the context's NCCL communicator (a hung or failed peer must not
+// deadlock this rank); later calls return AIMX_E_NCCL
+void nccl_abort(aimx_ctx* c, const std::string& why) {
+  if (c->comm && !c->nccl_dead) {
+    NcclApi& api = nccl();
+    if (api.commAbort) api.commAbort((ncclComm_t)c->comm);
+    c->comm = nullptr;
+  }
+  c->nccl_dead = true;
+  c->last_error = why;
+}
+
+// asynchronous NCCL error of the context's communicator, if any
+void poll_nccl(aimx_ctx* c) {
+  if (c->nccl_dead) throw Error(AIMX_E_NCCL, "the NCCL communicator was aborted");
+  if (!c->comm) return;
+  NcclApi& api = nccl();
+  if (!api.getAsyncError) return;
+  ncclResult_t r = ncclSuccess;
+  if (api.getAsyncError((ncclComm_t)c->comm, &r) != ncclSuccess || (r != ncclSuccess && r != ncclInProgress)) {
+    const std::string why = std::string("NCCL asynchronous error: ") + (api.errorString ? api.errorString(r) : "?");
+    nccl_abort(c, why);
+    throw Error(AIMX_E_NCCL, why);
+  }
+}
+
 void check_sticky(aimx_ctx* c) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw Error(AIMX_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
-  (void)c;
+  poll_nccl(c);
 }
 
 cudaStream_t pick(aimx_ctx* c, void* s) { return s ? (cudaStream_t)s : c->stream; }
@@ -1487,6 +1523,29 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
   leave_stream(c, s, true);
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_sync(aimx_ctx* c, double timeout_s) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  AIMX_CUDA(cudaEventRecord(c->ev_use, c->stream));   // ev_use: the context stream waits for every user stream
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(c->ev_use);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) AIMX_CUDA(q);
+    poll_nccl(c);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_s > 0 && el > timeout_s) {
+      const std::string why = "aimx_sync: no completion within " + std::to_string(timeout_s) + " s";
+      if (c->comm) nccl_abort(c, why + " (NCCL communicator aborted)");
+      throw Error(AIMX_E_TIMEOUT, why);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
   AIMX_API_END(c)
 }
 
@@ -2238,6 +2297,8 @@ const char* aimx_status_string(aimx_status s) {
     case AIMX_E_OOM: return "out of memory";
     case AIMX_E_CUDA: return "CUDA error";
     case AIMX_E_UNSUPPORTED: return "unsupported configuration";
+    case AIMX_E_NCCL: return "NCCL error (communicator aborted)";
+    case AIMX_E_TIMEOUT: return "timed out";
     case AIMX_E_INTERNAL: return "internal error";
   }
   return "unknown status";

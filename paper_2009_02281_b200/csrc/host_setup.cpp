@@ -478,10 +478,13 @@ void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, N
   }
 }
 
-void build_near_chunks(const NearGroups& ng, int chw, int chc, int cs, NearChunks& ck) {
-  // chunk list in group order: the group's W (interpolation) chunks, then its
-  // C (near) chunks; every group gets at least one chunk (its epilogue).
+void build_near_chunks(const NearGroups& ng, int chw, int chc, int cs, NearChunks& ck,
+                       const std::vector<int64_t>& order) {
+  // chunk list in `order` (all groups, each once): the group's W
+  // (interpolation) chunks, then its C (near) chunks; every group gets at
+  // least one chunk (its epilogue).
   const int R = ng.R;
+  if ((int64_t)order.size() != ng.ngrp) throw Error(AIMX_E_INTERNAL, "near group order");
   ck.chunks.clear();
   ck.gfirst.assign(ng.ngrp + 1, 0);
   ck.cost.assign(ng.ngrp, 0.0);
@@ -490,7 +493,8 @@ void build_near_chunks(const NearGroups& ng, int chw, int chc, int cs, NearChunk
   int64_t off = 0;   // payload bytes so far
   std::vector<int64_t> poff;
   auto pad16 = [](int64_t x) { return (x + 15) & ~(int64_t)15; };
-  for (int64_t g = 0; g < ng.ngrp; ++g) {
+  for (int64_t gi = 0; gi < ng.ngrp; ++gi) {
+    const int64_t g = order[gi];
     ck.gfirst[g] = (int64_t)ck.chunks.size() / 4;
     const int64_t n0 = ck.chunks.size();
     for (int kind = 0; kind < 2; ++kind) {
@@ -514,7 +518,7 @@ void build_near_chunks(const NearGroups& ng, int chw, int chc, int cs, NearChunk
     ck.chunks[ck.chunks.size() - 3] |= 4;            // last chunk of the group
     ck.cost[g] = 4.0 * (ng.wptr[g + 1] - ng.wptr[g]) + (ng.ptr[g + 1] - ng.ptr[g]) + 32.0;
   }
-  ck.gfirst[ng.ngrp] = (int64_t)ck.chunks.size() / 4;
+  ck.nchunk = (int64_t)ck.chunks.size() / 4;
   if (off / 16 > (int64_t)INT32_MAX) throw Error(AIMX_E_GRID, "near matrix payload too large");
   // payload: per chunk [coefficients | row indices (16-byte padded) | descriptor of chunk + kNearD]
   const int64_t nchunk = (int64_t)ck.chunks.size() / 4;
@@ -537,20 +541,25 @@ void build_near_chunks(const NearGroups& ng, int chw, int chc, int cs, NearChunk
   for (int64_t c = 0; c < nchunk; ++c) ck.chunks[4 * c + 2] = (int32_t)(poff[c] / 16);
 }
 
-std::vector<int32_t> near_partition(const NearChunks& ck, int64_t ngrp, int ncta) {
-  // contiguous group ranges per CTA, balanced by cost
+std::vector<int64_t> near_round_order(int64_t ngrp, int ncta, std::vector<int64_t>& cta_begin) {
+  // Groups are spatially ordered (anchor Morton code or linear index), so a
+  // run of consecutive groups shares most of its stencil nodes and near
+  // columns.  Round r = groups [r ncta, (r + 1) ncta); CTA k takes the k-th
+  // group of every round.  All CTAs advance through the rounds together, so
+  // the gathered rows in use at any time (x: B columns per RWG, phi: 4 B per
+  // node) are one round's neighbourhood and stay in L2, whatever B is; with
+  // contiguous per-CTA ranges the CTAs would touch the whole grid at once
+  // (cfg5 at 32 columns: 2.3 GB of DRAM reads against 1.2 GB of coefficients).
   ncta = (int)std::max<int64_t>(1, std::min<int64_t>(ncta, ngrp));
-  double total = 0;
-  for (double c : ck.cost) total += c;
-  std::vector<int32_t> cta_ptr(ncta + 1, 0);
-  int64_t g = 0;
-  double acc = 0;
+  std::vector<int64_t> order;
+  order.reserve(ngrp);
+  cta_begin.assign(ncta + 1, 0);
   for (int k = 0; k < ncta; ++k) {
-    const double target = total * (k + 1) / ncta;
-    while (g < ngrp && (acc + 0.5 * ck.cost[g] <= target || k == ncta - 1)) acc += ck.cost[g++];
-    cta_ptr[k + 1] = (int32_t)ck.gfirst[g];
+    cta_begin[k] = (int64_t)order.size();
+    for (int64_t g = k; g < ngrp; g += ncta) order.push_back(g);
   }
-  return cta_ptr;
+  cta_begin[ncta] = ngrp;
+  return order;
 }
 
 

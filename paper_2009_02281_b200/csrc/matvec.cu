@@ -291,6 +291,51 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   }
 }
 
+// ---- x inverse, batched (B >= 4): the CTA's 16 lines are the 4 channels x
+// 4 consecutive slots of one line, so both sides move whole 32-byte sectors:
+// each read covers the 4 channels of a slot's point (bufC[slot][line][kx][c]),
+// each write 4 consecutive slots of a channel (phi[node][c][slot]).  With the
+// per-slot mapping of k_xinv every phi write was a lone 8-byte piece of a
+// sector (cfg5, 32 columns: 766 us, issue 7%).
+template <typename T, int L> struct XinvB {
+  static constexpr int T_ = TwoLevel<Fac<L>::R1, Fac<L>::R2>::T;
+  static constexpr int NL = 16, NT = NL * T_;
+  static constexpr int XB = PassGeom<T, L>::XB;
+  static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (L + (size_t)NL * XB);
+};
+template <typename T, int L>
+__global__ void __launch_bounds__(XinvB<T, L>::NT) k_xinv_b(HotDev h, int B) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<T, L>;
+  using X = XinvB<T, L>;
+  const int line = threadIdx.x % X::NL, t = threadIdx.x / X::NL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* tw = reinterpret_cast<T2*>(smem_raw);
+  T2* xb = tw + L + line * X::XB;
+  for (int i = threadIdx.x; i < L; i += X::NT) tw[i] = ((const T2*)h.twx)[i];
+  __syncthreads();
+  const int r = blockIdx.x, c = line & 3, b = blockIdx.y * 4 + (line >> 2);
+  const bool act = b < B;
+  const int lid = h.line_id[r];
+  const T2* __restrict__ in = (const T2*)h.bufC + (int64_t)(act ? b : 0) * h.sA + (int64_t)lid * L * 4 + c;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * 4] : mk<T2>(0, 0);
+  inv_fft<T2, L>(v, xb, tw, t);
+  if (!act) return;
+  const int Nx = h.Nx;
+  const int64_t ns = (int64_t)h.batch * 4;   // phi node stride (complex): [node][channel][slot]
+  const int plid = h.phi_line ? h.phi_line[r] : lid;
+  T2* __restrict__ out = (T2*)h.phi + (int64_t)c * h.batch + b + (int64_t)plid * Nx * ns;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {   // x < Nx  <=>  k1 < R1/2 in D(R2,R1)
+    const int x = TwoLevel<G::R2, G::R1>::in_index(t, i);
+    if (i % G::R1 < (G::R1 + 1) / 2 && x < Nx) out[x * ns] = v[i];
+  }
+}
+
 // Column passes: CTA = NL lines = (rows per CTA) x (column tile CW).
 struct ColTile {
   int w, rsub, CW, RPC;
@@ -631,16 +676,18 @@ __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
     const int ky = i / nkx, kx = kx0 + i % nkx;
     hs[i] = Hb[(int64_t)ky * (Nx + 1) + (kx <= Nx ? kx : 2 * Nx - kx)];
   }
+  uint8_t* occ = reinterpret_cast<uint8_t*>(hs + (L / 2 + 1) * nkx);   // the plane's occupied rows
+  for (int y = threadIdx.x; y < Ny; y += blockDim.x) occ[y] = h.line_occ[(int64_t)h.zplane0 * Ny + y];
   __syncthreads();
   const bool act = ct.rsub == 0;   // one plane: the column tile's first row set only
   const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
-  const uint8_t* __restrict__ occ = h.line_occ + (int64_t)h.zplane0 * Ny;
+  // per-element offsets in 32 bits (one slot's plane: Ny W < 2^31)
   const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + col;
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {   // y < Ny = L/2  <=>  n2 < R2/2; unoccupied rows are zero
     const int y = G::TL::in_index(t, i);
-    v[i] = (act && i % G::R2 < G::R2 / 2 && occ[y]) ? in[(int64_t)y * W] : mk<T2>(0, 0);
+    v[i] = (act && i % G::R2 < G::R2 / 2 && occ[y]) ? in[y * W] : mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   {
@@ -657,7 +704,7 @@ __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {
     const int y = G::TL::in_index(t, i);
-    if (i % G::R2 < G::R2 / 2 && occ[y]) out[(int64_t)y * W] = v[i];
+    if (i % G::R2 < G::R2 / 2 && occ[y]) out[y * W] = v[i];
   }
 }
 
@@ -781,9 +828,10 @@ template <typename T, int R, int BB, bool PARTS> struct NearCfg {
   static constexpr int NBUF = NPC > 4 * NPW ? NPC : 4 * NPW;   // row loads in flight per lane
   static constexpr int NA = (PARTS ? 2 : 1) * R * V;  // complex accumulators: [part][r][v]
   static constexpr int NV = 2 * NA;                   // as reals
-  // partial sums: per lane (NG > 4) or, after a shuffle reduction over the
-  // warp's NG lane groups, per (warp, lane of group 0)
-  static constexpr bool SHFL = NG <= 4;
+  // partial sums per (warp, lane of group 0), after a shuffle reduction over
+  // the warp's NG lane groups (small shared footprint: 5 CTAs per SM fit at
+  // every column count)
+  static constexpr bool SHFL = true;
   static constexpr size_t REDB = (size_t)(SHFL ? (NT / 32) * LG : NT) * (NV + 1) * sizeof(T);
   static constexpr size_t OFF_RED = (size_t)NDS * STB;
   static constexpr size_t OFF_DESC = (OFF_RED + REDB + 15) / 16 * 16;
@@ -1040,9 +1088,18 @@ void run_x_geom(const HotDev& h, bool inv, int B, cudaStream_t s) {
   }
   AIMX_CHECK_LAUNCH();
 }
-// x passes: below two waves of default CTAs, one x row per (smaller) CTA
+// x passes: below two waves of default CTAs, one x row per (smaller) CTA;
+// batched inverse passes (B >= 4, lines of 64+ points) group 4 slots per CTA
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
+  if (h.nlines <= 0) return;
+  if (inv && B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024) {
+    using X = XinvB<T, L>;
+    set_smem(k_xinv_b<T, L>, X::SMEM);
+    launch_pdl(k_xinv_b<T, L>, dim3((unsigned)h.nlines, (unsigned)((B + 3) / 4)), dim3(X::NT), X::SMEM, s, h, B);
+    AIMX_CHECK_LAUNCH();
+    return;
+  }
   constexpr int RPC = PassGeom<T, L>::NL / 4;
   if ((int64_t)(h.nlines + RPC - 1) / RPC * B < 2 * 148) run_x_geom<T, L, true>(h, inv, B, s);
   else run_x_geom<T, L, false>(h, inv, B, s);
@@ -1261,7 +1318,8 @@ void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combin
 }
 
 template <typename T, int L> void run_yconv_plane(const HotDev& h, int B, cudaStream_t s) {
-  constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)(L / 2 + 1) * (PassGeom<T, L>::NL / 4);
+  constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)(L / 2 + 1) * (PassGeom<T, L>::NL / 4)
+                        + L / 2;   // + the occupied-row flags
   set_smem(k_yconv_plane<T, L>, sm);
   dim3 g = col_grid<T, L>(h.W, 1, B);
   launch_pdl(k_yconv_plane<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);

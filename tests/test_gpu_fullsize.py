@@ -11,10 +11,10 @@ from tests._parity import TOL, check_structure, gpu_input_as_c128, make_gpu_op, 
 pytestmark = pytest.mark.gpu
 
 
-def _fullsize(cfg, prec, freqs, nrows):
+def _fullsize(cfg, prec, freqs, nrows, orc=None):
     from oracle.aimx import from_config
     c = inp.get_config(cfg)
-    orc = from_config(cfg, static=False)
+    orc = orc if orc is not None else from_config(cfg, static=False)
     op = make_gpu_op(inp.make_mesh(cfg), c.grid_n, prec)
     check_structure(op, orc)
     lam = op.weights()
@@ -83,3 +83,39 @@ def test_cfg2_bench_sweep_vs_oracle_rows():
         a = np.array([gA[m] + ca @ x[cols] for m, (cols, ca, cr) in zip(rows, sr)])
         r = np.array([gR[m] + cr @ x[cols] for m, (cols, ca, cr) in zip(rows, sr)])
         assert rel_l2(Y[i][rows], orc.combine(a, r)) <= TOL["c64"]
+
+
+@pytest.fixture(scope="module")
+def orc5():
+    from oracle.aimx import from_config
+    return from_config(5, static=False)        # grid part on the full 1024 x 1024 x 16 padded grid
+
+
+def test_cfg5_fullsize_c64(orc5):
+    """cfg5 (401,088 RWG, 78.4 M near pairs, 1024-point x and y lines, the
+    planar S3 path): RWG table, anchors and near CSR bit-exact over the whole
+    problem; weights; C on 48 seeded rows; L_A x, L_phi x and Z x on those rows
+    at the first and last frequency."""
+    c = inp.get_config(5)
+    op = _fullsize(5, "c64", [c.freqs[0], c.freqs[-1]], 48, orc=orc5)
+    assert op.stats()["planar"]
+
+
+def test_cfg5_bench_sweep_vs_oracle_rows(orc5):
+    """bench.py's launch configuration (cfg5, c64, the 64-point sweep in two
+    device batches of 32 points, 32-column kernels) against the oracle on
+    seeded sampled rows at the first / last points of both batches."""
+    c = inp.get_config(5)
+    op = make_gpu_op(inp.make_mesh(5), c.grid_n, "c64")
+    assert op.stats()["batch_slots"] == 32
+    X = np.stack([inp.rhs_vector(5, i, op.N) for i in range(len(c.freqs))])
+    Y = op.sweep(c.freqs, to_gpu(X, "c64")).cpu().numpy()
+    rows = np.sort(np.random.default_rng(55).choice(op.N, 48, replace=False))
+    sr = orc5.static_rows(rows)
+    for i in (0, 31, 32, 63):
+        orc5.set_frequency(c.freqs[i])
+        x = gpu_input_as_c128(X[i], "c64")
+        gA, gR = orc5.grid_parts(x)
+        a = np.array([gA[m] + ca @ x[cols] for m, (cols, ca, cr) in zip(rows, sr)])
+        r = np.array([gR[m] + cr @ x[cols] for m, (cols, ca, cr) in zip(rows, sr)])
+        assert rel_l2(Y[i][rows], orc5.combine(a, r)) <= TOL["c64"]
