@@ -185,6 +185,9 @@ __device__ __forceinline__ void load_tw(T2* s_tw, const T2* __restrict__ g_tw, i
     case 256: { constexpr int L = 256; CALL; } break;                  \
     case 512: { constexpr int L = 512; CALL; } break;                  \
     case 1024: { constexpr int L = 1024; CALL; } break;                \
+    case 48: { constexpr int L = 48; CALL; } break;                    \
+    case 96: { constexpr int L = 96; CALL; } break;                    \
+    case 192: { constexpr int L = 192; CALL; } break;                  \
     default: throw Error(AIMX_E_UNSUPPORTED, "FFT length not compiled"); \
   }
 

