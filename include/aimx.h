@@ -117,7 +117,8 @@ typedef struct {
   int64_t near_union;         /* stored (column, group) entries; fill = nnz / (near_union * R) */
   int32_t planar;             /* 1: one occupied z plane, S3 runs in its exact 2-D form with the
                                  dz = 0 kernel slice (AIMX_NO_PLANAR=1 at setup keeps the 3-D path) */
-  int32_t reserved;
+  int32_t kop_grad;           /* 1: the double-layer operator K runs through the gradient-of-kernel
+                                 spectra (set after aimx_set_kop; 0: the radial form or not built) */
 } aimx_stats;
 
 /* S0 (the paper's "one-time static matrix-fill", tab:prof P:715): RWG basis,

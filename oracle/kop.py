@@ -402,3 +402,53 @@ def pmchwt_matvec(op, ak: AIMxK, f_hz: float, eps_r: float, x):
         Ksum_J += ak.matvec(J, k, residue=False)
         Ksum_M += ak.matvec(M, k, residue=False)
     return np.concatenate([out_E - Ksum_M, out_H + Ksum_J])
+
+
+# ---------------------------------------------------------------- sampled rows (full-size parity)
+def static_K_rows(op, rows):
+    """C_K on the near columns of the given rows, entry by entry: the
+    symmetrised PV part (both orientations, reading R25), + residue, - K_s,P.
+    Returns a list of (row, cols, C_K row, C_K row without the residue)."""
+    out = []
+    for m in rows:
+        cols = op.col[op.rowptr[m]:op.rowptr[m + 1]]
+        mm = np.full(cols.shape, m)
+        pv = 0.5 * (static_K_entries(op.V, op.T, op.rwg, mm, cols) + static_K_entries(op.V, op.T, op.rwg, cols, mm))
+        res = residue_entries(op.V, op.T, op.rwg, mm, cols)
+        kp = K_precorrection_entries(op.Lam, op.A, mm, cols, op.order, op.grid.h)
+        out.append((m, cols, pv + res - kp, pv - kp))
+    return out
+
+
+def kop_rows(op, krows, x, k0: float, residue: bool = True):
+    """(Kmat x) on the rows of krows (= static_K_rows(op, rows)): AIMxK.matvec
+    with the grid part on the full grid and C_K only on those rows."""
+    x = np.asarray(x, np.complex128)
+    g = grid_K(op, x, k0)
+    return np.array([g[m] + (ck if residue else cpv) @ x[cols] for m, cols, ck, cpv in krows])
+
+
+def pmchwt_rows(op, krows, f_hz: float, eps_r: float, x):
+    """pmchwt_matvec on the rows of krows (y_E rows, y_H rows), with the L
+    parts from op.matvec_rows (the oracle's row-wise near part) and K from
+    kop_rows; the same composition and scalings (reading R27)."""
+    from .kernels import MU0, C0
+    x = np.asarray(x, np.complex128)
+    N = op.N
+    J, M = x[:N], x[N:]
+    rows = [m for m, _, _, _ in krows]
+    w = 2 * np.pi * f_hz
+    eta0 = MU0 * C0
+    eta1 = eta0 / np.sqrt(eps_r)
+    yE = np.zeros(len(rows), complex)
+    yH = np.zeros(len(rows), complex)
+    for i, fi in enumerate((f_hz, f_hz * np.sqrt(eps_r))):
+        op.set_frequency(fi)
+        k = op.k0
+        aJ, rJ, _ = op.matvec_rows(J, rows)
+        aM, rM, _ = op.matvec_rows(M, rows)
+        yE += -1j * w * MU0 * (aJ - rJ / (k * k))
+        yH += -1j * w * MU0 * (aM - rM / (k * k)) / (eta0 ** 2 if i == 0 else eta1 ** 2)
+        yE -= kop_rows(op, krows, M, k, residue=False)
+        yH += kop_rows(op, krows, J, k, residue=False)
+    return yE, yH

@@ -181,9 +181,14 @@ struct HotDev;
 // y = Kmat x (one column, bound frequency): two passes of the grid transforms
 // with the radial spectrum HF (slot 0), the curl combination, interpolation
 // with the fp64 weights lam, + C_K x (ck: compute precision, CSR order)
+// grad: the gradient-of-kernel form (HF = the three spectra d_a G_hat [3][noct],
+// phi1 the potentials, phi2 unused), else the radial form (HF = F_hat)
 void kop_matvec(bool f32, const HotDev& h, const void* x, void* y, const void* HF, void* phi1, void* phi2,
                 const double* lam, double hg, const int64_t* rowptr, const int32_t* col, const void* ck,
-                cudaStream_t s);
+                cudaStream_t s, bool grad = false);
+// the gradient form runs on this context's grid (not planar; a fused short y/z
+// pass or the TMA z pass)
+bool kop_grad_supported(bool f32, const HotDev& h);
 
 // ---------------------------------------------------------------- linear-term modification
 // P:382-398 (sec:methods:aimx:acc): k0^2 G_lin, G_lin = -r/(8 pi) (eq:linterm

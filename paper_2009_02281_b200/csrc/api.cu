@@ -93,8 +93,10 @@ struct aimx_ctx {
   cudaStream_t cap = nullptr;   // capture stream
   // double-layer operator K (aimx_set_kop, NEXT #1)
   bool kop_on = false;
-  double2* HsF = nullptr;       // static spectrum of F_s = 1/(4 pi r^3), fp64
+  double2* HsF = nullptr;       // static spectra of K's grid part, fp64: the gradient form's
+                                // d_a G_s (a = x, y, z; [3][noct]) or the radial F_s = 1/(4 pi r^3)
   void* HsF_T = nullptr;        // ... compute precision (c64)
+  bool kgrad = false;           // K through the gradient-of-kernel spectra (else the radial form)
   void* HF = nullptr;           // F_hat of the bound frequency (slot 0), scaled 1/M
   void* kphi1 = nullptr;        // F (*) J and F (*) (s x J), phi layout
   void* kphi2 = nullptr;
@@ -896,15 +898,21 @@ void spectra(aimx_ctx* c, int B, const double* f, cudaStream_t s, void* out = nu
     spectrum_dynamic_f64(c->sp, B, k0, c->Hs, sc1, (double2*)out, s);
 }
 
-// F_hat(k0) of the double-layer operator into c->HF (slot 0)
+// K's spectra at f into c->HF: the three gradient spectra d_a G_hat(k0)
+// ([3][noct], kinds 2-4, odd along a), or the radial F_hat(k0) (kind 1)
 void kop_spectrum(aimx_ctx* c, double f, cudaStream_t s, void* out = nullptr) {
   if (!out) out = c->HF;
   double k0[1] = {2.0 * kPi * f / kC0};
   const double sc1 = spectrum_scale(c);
-  if (c->prec == AIMX_C64)
-    spectrum_dynamic_f32(c->sp, 1, k0, (const float2*)c->HsF_T, (float)sc1, (float2*)out, s, 1);
-  else
-    spectrum_dynamic_f64(c->sp, 1, k0, c->HsF, sc1, (double2*)out, s, 1);
+  const int64_t noct = c->sp.noct;
+  for (int a = 0; a < (c->kgrad ? 3 : 1); ++a) {
+    const int kind = c->kgrad ? 2 + a : 1;
+    if (c->prec == AIMX_C64)
+      spectrum_dynamic_f32(c->sp, 1, k0, (const float2*)c->HsF_T + a * noct, (float)sc1,
+                           (float2*)out + a * noct, s, kind);
+    else
+      spectrum_dynamic_f64(c->sp, 1, k0, c->HsF + a * noct, sc1, (double2*)out + a * noct, s, kind);
+  }
 }
 
 void bind_frequency(aimx_ctx* c, double f, cudaStream_t s) {
@@ -987,7 +995,7 @@ void run_matvec(aimx_ctx* c, const void* x, void* y0, void* y1, int mode, cudaSt
       aim_spmv(c->prec == AIMX_C64, c->hot.nb, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, x, y0, y1, cb, q);
     if (c->cfie_on && mode == 0) {   // eq:CFIEdis P:422: (-j w mu0 L - eta0 K) x
       kop_matvec(c->prec == AIMX_C64, c->hot, x, c->ktmp, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h,
-                 c->sd.rowptr, c->sd.col, c->ck_T, q);
+                 c->sd.rowptr, c->sd.col, c->ck_T, q, c->kgrad);
       gm_axpy(c->prec == AIMX_C64, c->hot.nb, -kMu0 * kC0, c->ktmp, y0, q);
     }
   };
@@ -1360,7 +1368,7 @@ static void solve_batch(aimx_ctx* c, int B, const double* f, const char* RHS, ch
     if (c->aim_on) aim_spmv(f32, N, c->sd.rowptr, c->sd.col, c->aimDA, c->aimDR, in, out, nullptr, cb, s);
     if (c->cfie_on) {
       kop_matvec(f32, c->hot, in, c->ktmp, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr,
-                 c->sd.col, c->ck_T, s);
+                 c->sd.col, c->ck_T, s, c->kgrad);
       gm_axpy(f32, N, -kMu0 * kC0, c->ktmp, out, s);
     }
   };
@@ -1928,6 +1936,7 @@ aimx_status aimx_get_stats(const aimx_ctx* c, aimx_stats* o) {
   o->near_row_order = c->near_order;
   o->near_union = c->near_union;
   o->planar = c->planar ? 1 : 0;
+  o->kop_grad = c->HsF && c->kgrad ? 1 : 0;
   return AIMX_OK;
 }
 
@@ -2027,17 +2036,21 @@ static void build_kop(aimx_ctx* c) {
     c->ck_T = ck;
     c->ckpv_T = ckpv;
   }
+  // the gradient-of-kernel form where the grid passes support its spectral
+  // cross product (AIMX_K_RADIAL=1 or an unsupported grid: the radial form)
+  c->kgrad = kop_grad_supported(f32, c->hot) && !std::getenv("AIMX_K_RADIAL");
+  const int ns = c->kgrad ? 3 : 1;
   const int64_t noct = c->sp.noct;
-  c->HsF = dalloc<double2>(c, noct);
-  spectrum_static(c->sp, c->HsF, c->stream, 1);
+  c->HsF = dalloc<double2>(c, ns * noct);
+  for (int a = 0; a < ns; ++a) spectrum_static(c->sp, c->HsF + a * noct, c->stream, c->kgrad ? 2 + a : 1);
   if (f32) {
-    c->HsF_T = dalloc<float2>(c, noct);
-    k_d2f<<<nblk(noct), 256, 0, c->stream>>>(noct, c->HsF, (float2*)c->HsF_T);
+    c->HsF_T = dalloc<float2>(c, ns * noct);
+    k_d2f<<<nblk(ns * noct), 256, 0, c->stream>>>(ns * noct, c->HsF, (float2*)c->HsF_T);
     AIMX_CHECK_LAUNCH();
   } else {
     c->HsF_T = c->HsF;
   }
-  c->HF = dalloc<char>(c, noct * (int64_t)cs);
+  c->HF = dalloc<char>(c, ns * noct * (int64_t)cs);
   const int64_t nP = c->hot.sP;   // one column, compact potentials (batch 1)
   c->kphi1 = zalloc<char>(c, nP * (int64_t)cs + 64);
   c->kphi2 = zalloc<char>(c, nP * (int64_t)cs + 64);
@@ -2124,7 +2137,7 @@ aimx_status aimx_matvec_kop(aimx_ctx* c, const void* x, void* y, void* stream) {
   cudaStream_t s = pick(c, stream);
   enter_stream(c, s);
   kop_matvec(c->prec == AIMX_C64, c->hot, x, y, c->HF, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr,
-             c->sd.col, c->ck_T, s);
+             c->sd.col, c->ck_T, s, c->kgrad);
   leave_stream(c, s);
   AIMX_API_END(c)
 }
@@ -2152,7 +2165,7 @@ aimx_status aimx_matvec_pmchwt(aimx_ctx* c, double eps_r, const void* x, void* y
   const int64_t noct = c->sp.noct;
   if (!c->pm_H1) {
     c->pm_H1 = dalloc<char>(c, noct * (int64_t)cs);
-    c->pm_HF1 = dalloc<char>(c, noct * (int64_t)cs);
+    c->pm_HF1 = dalloc<char>(c, (c->kgrad ? 3 : 1) * noct * (int64_t)cs);
     c->pm_t = dalloc<char>(c, 3 * nb * (int64_t)cs);
   }
   if (!c->kop_on) kop_spectrum(c, c->f, s);   // F_hat(k0) (aimx_set_kop(0) left it stale)
@@ -2185,7 +2198,7 @@ aimx_status aimx_matvec_pmchwt(aimx_ctx* c, double eps_r, const void* x, void* y
       gm_caxpy(f32, nb, 0.0, a * sc, tA, yz, s);
       gm_caxpy(f32, nb, 0.0, b * sc, tP, yz, s);
       kop_matvec(f32, h, xs, tK, HFi, c->kphi1, c->kphi2, c->sd.lam, c->topo.h, c->sd.rowptr, c->sd.col,
-                 c->ckpv_T, s);
+                 c->ckpv_T, s, c->kgrad);
       gm_axpy(f32, nb, src ? -1.0 : 1.0, tK, src ? yE : yH, s);   // y_E -= K M, y_H += K J
     }
   }

@@ -258,7 +258,7 @@ template <int R1, int R2> struct TwoLevel {
   static constexpr int L = R1 * R2;
   static constexpr int T = R1 < R2 ? R1 : R2;   // threads per line
   static constexpr int E = L / T;               // complex values per thread
-  static constexpr int XB = (R1 > R2 ? R1 : R2) * ((R1 > R2 ? R1 : R2) + 1);   // exchange elements
+  static constexpr int XB = R2 * (R1 + 1);   // exchange elements: [k2 < R2][n1 < R1], row stride R1 + 1
   // element index held in slot i under the input distribution D(R1,R2)
   static __device__ __forceinline__ int in_index(int t, int i) {
     return t + T * (i / R2) + R1 * (i % R2);

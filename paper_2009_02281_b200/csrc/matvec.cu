@@ -526,13 +526,17 @@ template <typename S, int L> struct ZGeom {
   static constexpr int XB = PassGeom<S, L>::XB;
   static constexpr int NL = sizeof(S) == 4 ? 16 : 8, NT = NL * T;   // (measured on cfg3)
 };
-template <typename T, int L> struct ZTma {
+// CURL (the double-layer operator's grid part, eq:KAIMx): three spectra (the
+// gradient components d_a G), a [kz][column] exchange of the channels
+template <typename T, int L, bool CURL = false> struct ZTma {
   using G = ZGeom<T, L>;
   static constexpr int CW = G::NL;   // columns per CTA (one ky row per step)
-  static constexpr size_t OFF_HS = sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB);
+  static constexpr int NS = CURL ? 3 : 1;   // spectra
+  static constexpr size_t XCH = CURL ? sizeof(typename CT<T>::T2) * (size_t)L * CW : 0;   // channel exchange
+  static constexpr size_t OFF_HS = sizeof(typename CT<T>::T2) * (L + (size_t)G::NL * G::XB) + XCH;
   static constexpr int KZ = L / 2 + 1;   // stored kz (the octant; kz > L/2 mirrors on read)
-  static constexpr int NPF = (KZ * (CW / 4) + G::NT - 1) / G::NT;   // slab elements per thread
-  static constexpr size_t HSB = sizeof(typename CT<T>::T2) * (size_t)KZ * CW / 4;   // one slab
+  static constexpr int NPF = (KZ * (CW / 4) + G::NT - 1) / G::NT;   // slab elements per thread and spectrum
+  static constexpr size_t HSB = sizeof(typename CT<T>::T2) * (size_t)NS * KZ * CW / 4;   // one slab
   static constexpr size_t OFF_IN = (OFF_HS + 2 * HSB + 127) / 128 * 128;   // TMA: 128-byte aligned
   __host__ __device__ static size_t inb(int Nz) { return sizeof(typename CT<T>::T2) * (size_t)Nz * CW; }
   // input ring depth: 3 (two row sets in flight) when two CTAs still fit an SM
@@ -540,13 +544,13 @@ template <typename T, int L> struct ZTma {
   __host__ __device__ static size_t smem(int Nz) { return OFF_IN + nbuf(Nz) * inb(Nz) + 24 + 128; }
 };
 
-template <typename T, int L>
+template <typename T, int L, bool CURL = false>
 __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zconv_tma(HotDev h, const __grid_constant__ CUtensorMap tm) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = ZGeom<T, L>;
-  using Z = ZTma<T, L>;
+  using Z = ZTma<T, L, CURL>;
   constexpr int NPF = Z::NPF, CW = Z::CW, C0S = sizeof(T2) / 8;   // tensor elements per complex
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   __builtin_assume(t < G::T);
@@ -554,14 +558,16 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
   const int b = blockIdx.z;
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   unsigned char* smem_raw = (unsigned char*)(((uintptr_t)smem_dyn + 127) & ~(uintptr_t)127);
-  T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][kz <= Nz][kx - kx0]
+  T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][NS][kz <= Nz][kx - kx0]
   const int NB = Z::nbuf(Nz);
   T2* inb = reinterpret_cast<T2*>(smem_raw + Z::OFF_IN);                       // [NB][z][CW]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Z::OFF_IN + NB * Z::inb(Nz));
   constexpr int nkx = CW / 4;
   const int kx0 = h.kx0 + (blockIdx.x * CW) / 4;
-  constexpr int nslab = Z::KZ * nkx;   // the slab stores kz = 0..Nz (Nz = L/2 here)
+  constexpr int nslab1 = Z::KZ * nkx;   // one spectrum's slab: kz = 0..Nz (Nz = L/2 here)
+  constexpr int nslab = Z::NS * nslab1;
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
+  const int64_t noct = (int64_t)(Nx + 1) * (Ny + 1) * (Nz + 1);   // spectrum stride (CURL: d_x, d_y, d_z G)
   const int64_t kystride = (int64_t)(Nz + 1) * (Nx + 1);
   int64_t poff[NPF];
   {
@@ -578,10 +584,13 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
   auto prefetch = [&](int ky, int buf) {
     const int kyf = ky <= Ny ? ky : Ny2 - ky;
 #pragma unroll
-    for (int k = 0; k < NPF; ++k) {
-      const int idx = threadIdx.x + k * G::NT;
-      if (idx < nslab) cp_async(hs + buf * nslab + idx, Hb + (int64_t)kyf * kystride + poff[k]);
-    }
+    for (int a = 0; a < Z::NS; ++a)
+#pragma unroll
+      for (int k = 0; k < NPF; ++k) {
+        const int idx = threadIdx.x + k * G::NT;
+        if (idx < nslab1)
+          cp_async(hs + buf * nslab + a * nslab1 + idx, Hb + a * noct + (int64_t)kyf * kystride + poff[k]);
+      }
     asm volatile("cp.async.commit_group;\n" ::);
   };
   const int col0 = blockIdx.x * CW, rs0 = blockIdx.y * ZROWS;
@@ -620,10 +629,37 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
       v[i] = (i % G::R2 < G::R2 / 2) ? ib[z * CW + line] : mk<T2>(0, 0);
     }
     fwd_fft<T2, L>(v, xb, tw, t);
+    if constexpr (CURL) {   // this thread's z spectrum of its column, to the channel exchange
+      T2* xs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS - Z::XCH);   // [kz][column]
+#pragma unroll
+      for (int i = 0; i < G::E; ++i) xs[TwoLevel<G::R2, G::R1>::in_index(t, i) * CW + line] = v[i];
+    }
     if (it + 1 < nrs) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
-    {  // spectrum multiply (slab in shared memory, 1/M folded into H)
+    if constexpr (CURL) {
+      // Phi_c = (G_hat x J_hat)_c = sum_ab eps_cab G_hat_a J_hat_b at this (kx, ky, kz);
+      // G_hat_a is odd along a: its octant value changes sign past N_a
+      const T2* xs = reinterpret_cast<const T2*>(smem_raw + Z::OFF_HS - Z::XCH);
+      const int c = line & 3, c0 = line & ~3;
+      const int kx = kx0 + (line >> 2);
+      const T sx = kx > Nx ? T(-1) : T(1), sy = ky > Ny ? T(-1) : T(1);
+      const T2* hl = hs + buf * nslab + (line >> 2);
+#pragma unroll
+      for (int i = 0; i < G::E; ++i) {
+        const int kz = TwoLevel<G::R2, G::R1>::in_index(t, i);
+        const int kzf = kz <= L / 2 ? kz : L - kz;
+        const T sz = kz > L / 2 ? T(-1) : T(1);
+        const T2 jx = xs[kz * CW + c0], jy = xs[kz * CW + c0 + 1], jz = xs[kz * CW + c0 + 2];
+        const T2 gx0 = hl[kzf * nkx], gy0 = hl[nslab1 + kzf * nkx], gz0 = hl[2 * nslab1 + kzf * nkx];
+        const T2 gx = mk<T2>(sx * gx0.x, sx * gx0.y), gy = mk<T2>(sy * gy0.x, sy * gy0.y),
+                 gz = mk<T2>(sz * gz0.x, sz * gz0.y);
+        if (c == 0) v[i] = csub(cmul(gy, jz), cmul(gz, jy));
+        else if (c == 1) v[i] = csub(cmul(gz, jx), cmul(gx, jz));
+        else if (c == 2) v[i] = csub(cmul(gx, jy), cmul(gy, jx));
+        else v[i] = mk<T2>(0, 0);
+      }
+    } else {  // spectrum multiply (slab in shared memory, 1/M folded into H)
       const T2* hl = hs + buf * nslab + (line >> 2);
 #pragma unroll
       for (int i = 0; i < G::E; ++i) {
@@ -720,7 +756,7 @@ template <typename T, int LY, int LZ> struct YZGeom {
   static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (size_t)(LZ / 2) * LY * TW;
 };
 
-template <typename T, int LY, int LZ>
+template <typename T, int LY, int LZ, bool CURL = false>
 __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 4 : 2) k_yzconv(HotDev h) {
   pdl_wait();
   pdl_trigger();
@@ -749,6 +785,50 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 4 : 2) k_yzconv(HotDev h
   __syncthreads();
   // phase 2: z forward, spectrum multiply, z inverse (z < Nz kept)
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
+  if constexpr (CURL) {
+    // per (ky, kx): the three current channels' z lines, Phi = G_hat x J_hat
+    // (G_hat_a odd along a: sign change past N_a), channel 3 -> 0
+    const int64_t noct = (int64_t)(Nx + 1) * (Ny + 1) * (Nz + 1);
+    for (int it = threadIdx.x; it < LY * (TW / 4); it += NT) {
+      const int ky = it / (TW / 4), w0 = 4 * (it % (TW / 4));
+      const int kx = h.kx0 + ((col0 + w0) >> 2);
+      const int kxf = kx <= Nx ? kx : 2 * Nx - kx, kyf = ky <= Ny ? ky : 2 * Ny - ky;
+      const T sx = kx > Nx ? T(-1) : T(1), sy = ky > Ny ? T(-1) : T(1);
+      T2 J[3][LZ];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int z = 0; z < LZ; ++z) J[c][z] = z < Nz ? S[(z * LY + ky) * TW + w0 + c] : mk<T2>(0, 0);
+        dftr<T2, LZ, false>(J[c]);
+      }
+      const T2* hl = Hb + (int64_t)kyf * (Nz + 1) * (Nx + 1) + kxf;
+#pragma unroll
+      for (int kz = 0; kz < LZ; ++kz) {
+        const int kzf = kz <= Nz ? kz : 2 * Nz - kz;
+        const T sz = kz > Nz ? T(-1) : T(1);
+        const T2 a0 = hl[(int64_t)kzf * (Nx + 1)], a1 = hl[noct + (int64_t)kzf * (Nx + 1)],
+                 a2 = hl[2 * noct + (int64_t)kzf * (Nx + 1)];
+        const T2 gx = mk<T2>(sx * a0.x, sx * a0.y), gy = mk<T2>(sy * a1.x, sy * a1.y),
+                 gz = mk<T2>(sz * a2.x, sz * a2.y);
+        const T2 px = csub(cmul(gy, J[2][kz]), cmul(gz, J[1][kz]));
+        const T2 py = csub(cmul(gz, J[0][kz]), cmul(gx, J[2][kz]));
+        const T2 pz = csub(cmul(gx, J[1][kz]), cmul(gy, J[0][kz]));
+        J[0][kz] = px;
+        J[1][kz] = py;
+        J[2][kz] = pz;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        dftr<T2, LZ, true>(J[c]);
+#pragma unroll
+        for (int z = 0; z < LZ; ++z)
+          if (z < Nz) S[(z * LY + ky) * TW + w0 + c] = J[c][z];
+      }
+#pragma unroll
+      for (int z = 0; z < LZ; ++z)
+        if (z < Nz) S[(z * LY + ky) * TW + w0 + 3] = mk<T2>(0, 0);
+    }
+  } else
   for (int it = threadIdx.x; it < LY * TW; it += NT) {
     const int ky = it / TW, w = it % TW;
     const int kx = h.kx0 + ((col0 + w) >> 2);
@@ -1327,30 +1407,49 @@ template <typename T, int L> void run_yconv_plane(const HotDev& h, int B, cudaSt
 }
 
 // y fwd + z conv + y inv in one kernel when both transforms are short
-// (reported as stage 3, zconv)
-template <typename T, int LY, int LZ> void launch_yz(const HotDev& h, int B, cudaStream_t s) {
+// (reported as stage 3, zconv); CURL: the double-layer operator's spectral
+// cross product (three gradient spectra) in place of the multiply
+template <typename T, int LY, int LZ, bool CURL = false> void launch_yz(const HotDev& h, int B, cudaStream_t s) {
   using G = YZGeom<T, LY, LZ>;
-  set_smem(k_yzconv<T, LY, LZ>, G::SMEM);
+  set_smem(k_yzconv<T, LY, LZ, CURL>, G::SMEM);
   dim3 g((unsigned)(h.W / G::TW), (unsigned)B);
-  launch_pdl(k_yzconv<T, LY, LZ>, dim3(g), dim3(G::NT), G::SMEM, s, h);
+  launch_pdl(k_yzconv<T, LY, LZ, CURL>, dim3(g), dim3(G::NT), G::SMEM, s, h);
   AIMX_CHECK_LAUNCH();
 }
-template <typename T> bool run_yz_fused(const HotDev& h, int B, cudaStream_t s, Profiler* prof) {
+// CURL keeps three z lines per thread in registers: short z transforms only
+template <typename T> constexpr int curl_fused_max_lz() { return sizeof(T) == 4 ? 16 : 8; }
+template <typename T, bool CURL = false> bool run_yz_fused(const HotDev& h, int B, cudaStream_t s, Profiler* prof) {
   const int Ly = 2 * h.Ny, Lz = 2 * h.Nz;
   if (Ly > 32 || Lz > 32 || h.W % YZGeom<T, 8, 8>::TW != 0 || Ly * Lz > 512) return false;
+  if (CURL && Lz > curl_fused_max_lz<T>()) return false;
   StageScope sc(prof, 3, s);
   switch (Ly * 64 + Lz) {
-    case 8 * 64 + 8: launch_yz<T, 8, 8>(h, B, s); break;
-    case 16 * 64 + 8: launch_yz<T, 16, 8>(h, B, s); break;
-    case 32 * 64 + 8: launch_yz<T, 32, 8>(h, B, s); break;
-    case 8 * 64 + 16: launch_yz<T, 8, 16>(h, B, s); break;
-    case 16 * 64 + 16: launch_yz<T, 16, 16>(h, B, s); break;
-    case 32 * 64 + 16: launch_yz<T, 32, 16>(h, B, s); break;
-    case 8 * 64 + 32: launch_yz<T, 8, 32>(h, B, s); break;
-    case 16 * 64 + 32: launch_yz<T, 16, 32>(h, B, s); break;
+    case 8 * 64 + 8: launch_yz<T, 8, 8, CURL>(h, B, s); break;
+    case 16 * 64 + 8: launch_yz<T, 16, 8, CURL>(h, B, s); break;
+    case 32 * 64 + 8: launch_yz<T, 32, 8, CURL>(h, B, s); break;
+    case 8 * 64 + 16: if constexpr (!CURL || curl_fused_max_lz<T>() >= 16) launch_yz<T, 8, 16, CURL>(h, B, s); break;
+    case 16 * 64 + 16: if constexpr (!CURL || curl_fused_max_lz<T>() >= 16) launch_yz<T, 16, 16, CURL>(h, B, s); break;
+    case 32 * 64 + 16: if constexpr (!CURL || curl_fused_max_lz<T>() >= 16) launch_yz<T, 32, 16, CURL>(h, B, s); break;
+    case 8 * 64 + 32: if constexpr (!CURL) launch_yz<T, 8, 32>(h, B, s); break;
+    case 16 * 64 + 32: if constexpr (!CURL) launch_yz<T, 16, 32>(h, B, s); break;
     default: return false;
   }
   return true;
+}
+
+// the z pass of the double-layer operator: TMA z pass with the spectral cross product
+template <typename T, int L> void run_z_curl(const HotDev& h, cudaStream_t s) {
+  using Z = ZTma<T, L, true>;
+  const size_t zs = Z::smem(h.Nz);
+  set_smem(k_zconv_tma<T, L, true>, zs);
+  dim3 gt((unsigned)(h.W / Z::CW), (unsigned)((2 * h.Ny + ZROWS - 1) / ZROWS), 1u);
+  launch_pdl(k_zconv_tma<T, L, true>, gt, dim3(ZGeom<T, L>::NT), zs, s, h, *(const CUtensorMap*)h.tmB);
+  AIMX_CHECK_LAUNCH();
+}
+template <typename T> bool z_curl_tma_ok(const HotDev& h) {
+  int nl = 0;
+  AIMX_SWITCH_L(2 * h.Nz, (nl = ZGeom<T, L>::NL));
+  return h.tmB && h.nzocc == h.Nz && h.W >= nl && h.Nz <= 256;
 }
 
 // S3 between the x transforms: the planar y pass, the fused short y/z pass,
@@ -1498,6 +1597,88 @@ void hot_kop(const HotDev& h0, const void* x, void* y, const void* HF, void* phi
   conv(phi2);                                   // F (*) (s x J)
   launch_pdl(k_kop_interp<T>, dim3((unsigned)(((int64_t)h.nb * 32 + 255) / 256)), dim3(256), 0, s, h, (const T2*)phi1,
              (const T2*)phi2, lam, hg, rowptr, col, (const T*)ck, (const T2*)x, (T2*)y);
+  AIMX_CHECK_LAUNCH();
+}
+
+// ---- the double-layer operator K through the gradient-of-kernel spectra
+// (eq:KAIMx P:457, BASELINE cfg4 "K via gradient-of-kernel spectra"):
+// Phi_c = sum_{a,b} eps_cab (d_a G (*) J_b) is ONE forward transform of the
+// current channels, the spectral cross product Phi_hat = G_hat x J_hat with
+// the three odd gradient spectra (octants, sign change past N_a along a) in
+// the z pass, and ONE inverse transform; then y_K = -sum_c W^c Phi_c + C_K x.
+// No cancellation: every term is the same size as the result, so c64 keeps
+// its accuracy on flat faces (the radial form s x (F * J) - F * (s x J)
+// cancels there).
+template <typename T> bool kop_grad_ok(const HotDev& h) {
+  if (h.planar) return false;
+  const int Ly = 2 * h.Ny, Lz = 2 * h.Nz;
+  const bool fused = Ly <= 32 && Lz <= curl_fused_max_lz<T>() && h.W % YZGeom<T, 8, 8>::TW == 0 &&
+                     Ly * Lz <= 512 && Ly >= 8;
+  return fused || z_curl_tma_ok<T>(h);
+}
+
+template <typename T>
+void grid_conv_curl(const HotDev& h, cudaStream_t s) {
+  if (run_yz_fused<T, true>(h, 1, s, nullptr)) return;
+  const int Ly = 2 * h.Ny, Lz = 2 * h.Nz;
+  AIMX_SWITCH_L(Ly, (run_y<T, L>(h, false, 1, s)));
+  AIMX_SWITCH_L(Lz, (run_z_curl<T, L>(h, s)));
+  AIMX_SWITCH_L(Ly, (run_y<T, L>(h, true, 1, s)));
+}
+
+// warp per RWG: y = -sum_{c in xyz} sum_s Lambda^c[s] Phi_c(node) + C_K x
+// (phi: [node][channel], one column; fixed-order shuffle sum)
+template <typename T>
+__global__ void k_kop_interp_grad(HotDev h, const typename CT<T>::T2* __restrict__ phi,
+                                  const double* __restrict__ lam, const int64_t* __restrict__ rowptr,
+                                  const int32_t* __restrict__ col, const T* __restrict__ ck,
+                                  const typename CT<T>::T2* __restrict__ x, typename CT<T>::T2* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  const int lane = threadIdx.x & 31;
+  const int m = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (m >= h.nb) return;
+  const int p = h.p, p3 = h.p3, Nx = h.Nx, Ny = h.Ny;
+  const int base = h.rwg_base[m];
+  double yr = 0.0, yi = 0.0;
+  for (int sl = lane; sl < p3; sl += 32) {
+    const double* lw = lam + ((int64_t)m * p3 + sl) * 4;
+    if (lw[0] == 0.0 && lw[1] == 0.0 && lw[2] == 0.0) continue;
+    const int i = sl % p, j = (sl / p) % p, k = sl / (p * p);
+    const int64_t lin = base + i + Nx * (j + Ny * k);
+    const T2* a = phi + (lin - h.phi_off) * 4;
+    yr -= lw[0] * (double)a[0].x + lw[1] * (double)a[1].x + lw[2] * (double)a[2].x;
+    yi -= lw[0] * (double)a[0].y + lw[1] * (double)a[1].y + lw[2] * (double)a[2].y;
+  }
+  for (int64_t e = rowptr[m] + lane; e < rowptr[m + 1]; e += 32) {
+    const T2 xv = x[col[e]];
+    yr += (double)ck[e] * xv.x;
+    yi += (double)ck[e] * xv.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    yr += __shfl_xor_sync(0xffffffffu, yr, o);
+    yi += __shfl_xor_sync(0xffffffffu, yi, o);
+  }
+  if (lane == 0) y[m] = mk<T2>((T)yr, (T)yi);
+}
+
+template <typename T>
+void hot_kop_grad(const HotDev& h0, const void* x, void* y, const void* HG, void* phi, const double* lam,
+                  const int64_t* rowptr, const int32_t* col, const void* ck, cudaStream_t s) {
+  using T2 = typename CT<T>::T2;
+  HotDev h = h0;
+  h.Hoct = const_cast<void*>(HG);   // [3][noct]: d_x G, d_y G, d_z G
+  h.batch = 1;                      // one column: compact potentials ([node][channel])
+  h.phi = phi;
+  const int Lx = 2 * h.Nx;
+  run_gather<T>(h, x, h.nb, 1, s);                 // J = P x (the rho channel is carried, unused)
+  AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, 1, s)));
+  grid_conv_curl<T>(h, s);
+  AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, 1, s)));
+  launch_pdl(k_kop_interp_grad<T>, dim3((unsigned)(((int64_t)h.nb * 32 + 255) / 256)), dim3(256), 0, s, h,
+             (const T2*)phi, lam, rowptr, col, (const T*)ck, (const T2*)x, (T2*)y);
   AIMX_CHECK_LAUNCH();
 }
 
@@ -1702,10 +1883,16 @@ void hot_near_f64(const HotDev& h, const void* x, void* y0, void* y1, const Comb
 }
 void kop_matvec(bool f32, const HotDev& h, const void* x, void* y, const void* HF, void* phi1, void* phi2,
                 const double* lam, double hg, const int64_t* rowptr, const int32_t* col, const void* ck,
-                cudaStream_t s) {
+                cudaStream_t s, bool grad) {
+  if (grad) {   // HF: the three gradient spectra [3][noct]
+    if (f32) hot_kop_grad<float>(h, x, y, HF, phi1, lam, rowptr, col, ck, s);
+    else hot_kop_grad<double>(h, x, y, HF, phi1, lam, rowptr, col, ck, s);
+    return;
+  }
   if (f32) hot_kop<float>(h, x, y, HF, phi1, phi2, lam, hg, rowptr, col, ck, s);
   else hot_kop<double>(h, x, y, HF, phi1, phi2, lam, hg, rowptr, col, ck, s);
 }
+bool kop_grad_supported(bool f32, const HotDev& h) { return f32 ? kop_grad_ok<float>(h) : kop_grad_ok<double>(h); }
 void hot_matvec_f64(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c,
                     cudaStream_t s, Profiler* prof) {
   hot_matvec<double>(h, x, y0, y1, c, s, prof);

@@ -38,7 +38,9 @@ namespace {
 // K_s = 1/(4 pi r) (eq:hgfs P:227), K_s(0) = 0 (eq:Hsmm P:321), 0 on wrap
 // slots; fp64.  (The dynamic samples are generated inside the x pass, ksample.)
 // kind 1: F_s = 1/(4 pi r^3) (the radial factor of grad G_s = -r F_s; the
-// double-layer operator's grid form, NEXT #1), 0 at r = 0
+// double-layer operator's grid form, NEXT #1), 0 at r = 0; kinds 2, 3, 4:
+// d_a G_s = -r_a F_s, a = x, y, z (the gradient-of-kernel spectra of eq:KAIMx,
+// odd along a), 0 at r = 0 (reading R23)
 __global__ void k_sample_static(int Nx, int Ny, int Nz, int nz1, int64_t noct, double h, double2* __restrict__ out,
                                 int kind) {
   pdl_wait();
@@ -55,6 +57,7 @@ __global__ void k_sample_static(int Nx, int Ny, int Nz, int nz1, int64_t noct, d
     if (q > 0) {
       const double r = h * sqrt((double)q);
       re = kind ? 1.0 / (4.0 * kPi * r * r * r) : 1.0 / (4.0 * kPi) / r;
+      if (kind >= 2) re *= -h * (double)(kind == 2 ? i : (kind == 3 ? j : l));
     }
   }
   out[idx] = make_double2(re, 0.0);
@@ -84,7 +87,8 @@ __device__ __forceinline__ typename CT<T>::T2 ksample(int i, int j, int l, int N
                                                       double h, double k0, int kind = 0) {
   using T2 = typename CT<T>::T2;
   double re = 0.0, im = 0.0;
-  if (kind == 1) {   // F_d = ((1 + j x) e^{-j x} - 1)/(4 pi r^3), x = k0 r; 0 at r = 0 (fp64)
+  if (kind >= 1) {   // F_d = ((1 + j x) e^{-j x} - 1)/(4 pi r^3), x = k0 r; 0 at r = 0 (fp64);
+                     // kinds 2-4: d_a G_d = -r_a F_d (a = kind - 2), odd along a
     if (i < Nx && j < Ny && l < Nz) {
       const int64_t q = (int64_t)i * i + (int64_t)j * j + (int64_t)l * l;
       if (q > 0) {
@@ -95,6 +99,11 @@ __device__ __forceinline__ typename CT<T>::T2 ksample(int i, int j, int l, int N
         const double a = 1.0 / (4.0 * kPi * r * r * r);
         re = (x * sx - 2.0 * sh * sh) * a;
         im = (x * cx - sx) * a;
+        if (kind >= 2) {
+          const double ra = -h * (double)(kind == 2 ? i : (kind == 3 ? j : l));
+          re *= ra;
+          im *= ra;
+        }
       }
     }
     return mk<T2>((T)re, (T)im);
@@ -130,11 +139,13 @@ struct SampleArgs {
   int nz1;    // z samples per (ky, kx): N_z + 1, or 1 for the planar (dz = 0) spectrum
   double h;
   double k0[kMaxBatch];
-  int kind;   // 0: K_d (eq:hgfd), 1: F_d (double-layer operator)
+  int kind;   // 0: K_d (eq:hgfd), 1: F_d (double-layer operator), 2-4: d_a G_d (a = x, y, z)
 };
 
 // MODE 0: read `in`; MODE 1: generate dynamic samples K_d (row pass only).
-template <typename T, int L, bool ROW, int MODE = 0, bool SMALL = false>
+// ODD: odd extension v[2N - i] = -v[i] (the DST-I of a kernel odd along this
+// axis: the gradient components d_a G along a), else even.
+template <typename T, int L, bool ROW, int MODE = 0, bool SMALL = false, bool ODD = false>
 __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int64_t noct,
                                               const typename CT<T>::T2* __restrict__ in,
                                               typename CT<T>::T2* __restrict__ out,
@@ -181,24 +192,30 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
 #pragma unroll
       for (int i = 0; i < G::E; ++i) {
         int n = G::TL::in_index(t, i);
+        const bool neg = ODD && n > L / 2;
         n = n <= L / 2 ? n : L - n;
-        v[i] = act ? xb[n] : mk<T2>(0, 0);
+        const T2 u = act ? xb[n] : mk<T2>(0, 0);
+        v[i] = neg ? mk<T2>(-u.x, -u.y) : u;
       }
       __syncthreads();
     } else {
 #pragma unroll
       for (int i = 0; i < G::E; ++i) {
         int n = G::TL::in_index(t, i);
+        const bool neg = ODD && n > L / 2;
         n = n <= L / 2 ? n : L - n;
-        v[i] = act ? ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0, sa.kind) : mk<T2>(0, 0);
+        const T2 u = act ? ksample<T, false>(n, jj, ll, sa.Nx, sa.Ny, sa.Nz, sa.h, k0, sa.kind) : mk<T2>(0, 0);
+        v[i] = neg ? mk<T2>(-u.x, -u.y) : u;
       }
     }
   } else {
 #pragma unroll
     for (int i = 0; i < G::E; ++i) {
       int n = G::TL::in_index(t, i);
+      const bool neg = ODD && n > L / 2;
       n = n <= L / 2 ? n : L - n;
-      v[i] = act ? in[base + n * stride] : mk<T2>(0, 0);
+      const T2 u = act ? in[base + n * stride] : mk<T2>(0, 0);
+      v[i] = neg ? mk<T2>(-u.x, -u.y) : u;
     }
   }
   fft2<T2, G::R1, G::R2, false>(v, xb, tw, t);
@@ -226,7 +243,7 @@ template <class K> void set_smem(K kernel, size_t bytes) {
 // CTAs of a pass with the default geometry; below two waves use SMALL CTAs
 template <typename T, int L> bool use_small(int64_t ctas_default) { return ctas_default < 2 * 148; }
 
-template <typename T, int L, bool SMALL>
+template <typename T, int L, bool SMALL, bool ODD>
 void even_rows_geom(int64_t nlines, int64_t noct, int B, const void* in, void* out, const void* tw, cudaStream_t s,
                     const SampleArgs* gen) {
   using T2 = typename CT<T>::T2;
@@ -234,12 +251,12 @@ void even_rows_geom(int64_t nlines, int64_t noct, int B, const void* in, void* o
   const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
   dim3 g((unsigned)((nlines + G::NL - 1) / G::NL), 1, (unsigned)B);
   if (gen) {
-    set_smem(k_even<T, L, true, 1, SMALL>, sm);
-    launch_pdl(k_even<T, L, true, 1, SMALL>, g, dim3(G::NT), sm, s, nlines, (int64_t)1, noct, (const T2*)nullptr,
-               (T2*)out, (const T2*)tw, (const T2*)nullptr, (T)1, *gen);
+    set_smem(k_even<T, L, true, 1, SMALL, ODD>, sm);
+    launch_pdl(k_even<T, L, true, 1, SMALL, ODD>, g, dim3(G::NT), sm, s, nlines, (int64_t)1, noct,
+               (const T2*)nullptr, (T2*)out, (const T2*)tw, (const T2*)nullptr, (T)1, *gen);
   } else {
-    set_smem(k_even<T, L, true, 0, SMALL>, sm);
-    launch_pdl(k_even<T, L, true, 0, SMALL>, g, dim3(G::NT), sm, s, nlines, (int64_t)1, noct, (const T2*)in,
+    set_smem(k_even<T, L, true, 0, SMALL, ODD>, sm);
+    launch_pdl(k_even<T, L, true, 0, SMALL, ODD>, g, dim3(G::NT), sm, s, nlines, (int64_t)1, noct, (const T2*)in,
                (T2*)out, (const T2*)tw, (const T2*)nullptr, (T)1, SampleArgs{});
   }
   AIMX_CHECK_LAUNCH();
@@ -248,44 +265,52 @@ void even_rows_geom(int64_t nlines, int64_t noct, int B, const void* in, void* o
 // x rows (contiguous lines); gen: the dynamic samples are generated in the pass
 template <typename T>
 void even_rows(int L, int64_t nlines, int64_t noct, int B, const void* in, void* out, const void* tw,
-               cudaStream_t s, const SampleArgs* gen = nullptr) {
+               cudaStream_t s, const SampleArgs* gen = nullptr, bool odd = false) {
   AIMX_SWITCH_L(L, ({
-    if (use_small<T, L>((nlines + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * B))
-      even_rows_geom<T, L, true>(nlines, noct, B, in, out, tw, s, gen);
-    else
-      even_rows_geom<T, L, false>(nlines, noct, B, in, out, tw, s, gen);
+    const bool sm = use_small<T, L>((nlines + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * B);
+    if (odd) {
+      if (sm) even_rows_geom<T, L, true, true>(nlines, noct, B, in, out, tw, s, gen);
+      else even_rows_geom<T, L, false, true>(nlines, noct, B, in, out, tw, s, gen);
+    } else {
+      if (sm) even_rows_geom<T, L, true, false>(nlines, noct, B, in, out, tw, s, gen);
+      else even_rows_geom<T, L, false, false>(nlines, noct, B, in, out, tw, s, gen);
+    }
   }));
+}
+
+template <typename T, int L, bool SMALL, bool ODD>
+void even_cols_geom(int64_t outer, int64_t inner, int64_t noct, int B, const void* in, void* out, const void* tw,
+                    const void* add, T scale, cudaStream_t s) {
+  using T2 = typename CT<T>::T2;
+  using G = EvGeom<T, L, SMALL>;
+  const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
+  set_smem(k_even<T, L, false, 0, SMALL, ODD>, sm);
+  dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
+  launch_pdl(k_even<T, L, false, 0, SMALL, ODD>, g, dim3(G::NT), sm, s, 0, inner, noct, (const T2*)in, (T2*)out,
+             (const T2*)tw, (const T2*)add, scale, SampleArgs{});
+  AIMX_CHECK_LAUNCH();
 }
 
 template <typename T>
 void even_cols(int L, int64_t outer, int64_t inner, int64_t noct, int B, const void* in, void* out,
-               const void* tw, const void* add, T scale, cudaStream_t s) {
-  using T2 = typename CT<T>::T2;
+               const void* tw, const void* add, T scale, cudaStream_t s, bool odd = false) {
   AIMX_SWITCH_L(L, ({
-    if (use_small<T, L>((inner + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * outer * B)) {
-      using G = EvGeom<T, L, true>;
-      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
-      set_smem(k_even<T, L, false, 0, true>, sm);
-      dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
-      launch_pdl(k_even<T, L, false, 0, true>, g, dim3(G::NT), sm, s, 0, inner, noct, (const T2*)in, (T2*)out,
-                                                        (const T2*)tw, (const T2*)add, scale, SampleArgs{});
+    const bool sm = use_small<T, L>((inner + EvGeom<T, L>::NL - 1) / EvGeom<T, L>::NL * outer * B);
+    if (odd) {
+      if (sm) even_cols_geom<T, L, true, true>(outer, inner, noct, B, in, out, tw, add, scale, s);
+      else even_cols_geom<T, L, false, true>(outer, inner, noct, B, in, out, tw, add, scale, s);
     } else {
-      using G = EvGeom<T, L>;
-      const size_t sm = sizeof(T2) * (L + (size_t)G::NL * G::XB);
-      set_smem(k_even<T, L, false>, sm);
-      dim3 g((unsigned)((inner + G::NL - 1) / G::NL), (unsigned)outer, (unsigned)B);
-      launch_pdl(k_even<T, L, false>, g, dim3(G::NT), sm, s, 0, inner, noct, (const T2*)in, (T2*)out, (const T2*)tw,
-                                               (const T2*)add, scale, SampleArgs{});
+      if (sm) even_cols_geom<T, L, true, false>(outer, inner, noct, B, in, out, tw, add, scale, s);
+      else even_cols_geom<T, L, false, false>(outer, inner, noct, B, in, out, tw, add, scale, s);
     }
   }));
-  AIMX_CHECK_LAUNCH();
 }
 
 // z then y even-extension transforms of the octant for short z / y lengths
 // (2 N_z, 2 N_y <= 32): a CTA owns TW consecutive kx and all their (ky, kz)
 // in shared memory; each line transform is one thread's register DFT; the
 // epilogue out = scale (v + add) is fused.
-template <typename T, int LY, int LZ>
+template <typename T, int LY, int LZ, bool ODDY = false, bool ODDZ = false>
 __global__ void __launch_bounds__(128) k_evyz(int Nx, int Ny, int Nz, int64_t noct,
                                               const typename CT<T>::T2* __restrict__ in,
                                               typename CT<T>::T2* __restrict__ out,
@@ -308,7 +333,10 @@ __global__ void __launch_bounds__(128) k_evyz(int Nx, int Ny, int Nz, int64_t no
     const int w = it % TW, ky = it / TW;
     T2 v[LZ];
 #pragma unroll
-    for (int n = 0; n < LZ; ++n) v[n] = S[(ky * nz1 + (n <= LZ / 2 ? n : LZ - n)) * TW + w];
+    for (int n = 0; n < LZ; ++n) {
+      const T2 u = S[(ky * nz1 + (n <= LZ / 2 ? n : LZ - n)) * TW + w];
+      v[n] = (ODDZ && n > LZ / 2) ? mk<T2>(-u.x, -u.y) : u;
+    }
     dftr<T2, LZ, false>(v);
 #pragma unroll
     for (int k = 0; k <= LZ / 2; ++k) S[(ky * nz1 + k) * TW + w] = v[k];
@@ -319,7 +347,10 @@ __global__ void __launch_bounds__(128) k_evyz(int Nx, int Ny, int Nz, int64_t no
     if (kx >= nx1) continue;
     T2 v[LY];
 #pragma unroll
-    for (int n = 0; n < LY; ++n) v[n] = S[((n <= LY / 2 ? n : LY - n) * nz1 + kz) * TW + w];
+    for (int n = 0; n < LY; ++n) {
+      const T2 u = S[((n <= LY / 2 ? n : LY - n) * nz1 + kz) * TW + w];
+      v[n] = (ODDY && n > LY / 2) ? mk<T2>(-u.x, -u.y) : u;
+    }
     dftr<T2, LY, false>(v);
 #pragma unroll
     for (int k = 0; k <= LY / 2; ++k) {
@@ -330,44 +361,57 @@ __global__ void __launch_bounds__(128) k_evyz(int Nx, int Ny, int Nz, int64_t no
   }
 }
 
-template <typename T, int LY, int LZ>
+template <typename T, int LY, int LZ, bool ODDY, bool ODDZ>
 void launch_evyz(const SpectrumPlan& sp, int B, const void* in, void* out, const void* add, T scale, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   const size_t sm = sizeof(T2) * (size_t)(sp.Ny + 1) * (sp.Nz + 1) * 32;
-  set_smem(k_evyz<T, LY, LZ>, sm);
-  launch_pdl(k_evyz<T, LY, LZ>, dim3((unsigned)((sp.Nx + 1 + 31) / 32), (unsigned)B), dim3(128), sm, s, sp.Nx,
-             sp.Ny, sp.Nz, sp.noct, (const T2*)in, (T2*)out, (const T2*)add, scale);
+  set_smem(k_evyz<T, LY, LZ, ODDY, ODDZ>, sm);
+  launch_pdl(k_evyz<T, LY, LZ, ODDY, ODDZ>, dim3((unsigned)((sp.Nx + 1 + 31) / 32), (unsigned)B), dim3(128), sm, s,
+             sp.Nx, sp.Ny, sp.Nz, sp.noct, (const T2*)in, (T2*)out, (const T2*)add, scale);
   AIMX_CHECK_LAUNCH();
 }
 
+template <typename T, int LY, int LZ>
+void launch_evyz_p(const SpectrumPlan& sp, int B, const void* in, void* out, const void* add, T scale, cudaStream_t s,
+                   int odd) {
+  if (odd == 1) launch_evyz<T, LY, LZ, true, false>(sp, B, in, out, add, scale, s);
+  else if (odd == 2) launch_evyz<T, LY, LZ, false, true>(sp, B, in, out, add, scale, s);
+  else launch_evyz<T, LY, LZ, false, false>(sp, B, in, out, add, scale, s);
+}
+
+// odd: the axis (1 = y, 2 = z) along which the kernel is odd, else -1
 template <typename T>
-bool evyz(const SpectrumPlan& sp, int B, const void* in, void* out, const void* add, T scale, cudaStream_t s) {
+bool evyz(const SpectrumPlan& sp, int B, const void* in, void* out, const void* add, T scale, cudaStream_t s,
+          int odd) {
   switch (2 * sp.Ny * 64 + 2 * sp.Nz) {
-    case 8 * 64 + 8: launch_evyz<T, 8, 8>(sp, B, in, out, add, scale, s); return true;
-    case 16 * 64 + 8: launch_evyz<T, 16, 8>(sp, B, in, out, add, scale, s); return true;
-    case 32 * 64 + 8: launch_evyz<T, 32, 8>(sp, B, in, out, add, scale, s); return true;
-    case 8 * 64 + 16: launch_evyz<T, 8, 16>(sp, B, in, out, add, scale, s); return true;
-    case 16 * 64 + 16: launch_evyz<T, 16, 16>(sp, B, in, out, add, scale, s); return true;
-    case 32 * 64 + 16: launch_evyz<T, 32, 16>(sp, B, in, out, add, scale, s); return true;
-    case 16 * 64 + 32: launch_evyz<T, 16, 32>(sp, B, in, out, add, scale, s); return true;
+    case 8 * 64 + 8: launch_evyz_p<T, 8, 8>(sp, B, in, out, add, scale, s, odd); return true;
+    case 16 * 64 + 8: launch_evyz_p<T, 16, 8>(sp, B, in, out, add, scale, s, odd); return true;
+    case 32 * 64 + 8: launch_evyz_p<T, 32, 8>(sp, B, in, out, add, scale, s, odd); return true;
+    case 8 * 64 + 16: launch_evyz_p<T, 8, 16>(sp, B, in, out, add, scale, s, odd); return true;
+    case 16 * 64 + 16: launch_evyz_p<T, 16, 16>(sp, B, in, out, add, scale, s, odd); return true;
+    case 32 * 64 + 16: launch_evyz_p<T, 32, 16>(sp, B, in, out, add, scale, s, odd); return true;
+    case 16 * 64 + 32: launch_evyz_p<T, 16, 32>(sp, B, in, out, add, scale, s, odd); return true;
     default: return false;
   }
 }
 
-// 3-D even-extension transform on the octant [B][y][z][x]: x rows, z cols, y cols.
+// 3-D even-extension transform on the octant [B][y][z][x]: x rows, z cols, y
+// cols; `odd` (0 x, 1 y, 2 z, -1 none): the axis with the odd extension
 template <typename T>
 void dct3(SpectrumPlan& sp, int B, void** tw, void* a, void* b, void* out, const void* add, T scale,
-          cudaStream_t s, const SampleArgs* gen = nullptr) {
+          cudaStream_t s, const SampleArgs* gen = nullptr, int odd = -1) {
   const int64_t nx = sp.Nx + 1, ny = sp.Ny + 1, nz = sp.nz1, no = sp.noct;
-  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s, gen);
+  even_rows<T>(2 * sp.Nx, ny * nz, no, B, a, b, tw[0], s, gen, odd == 0);
   if (sp.nz1 == 1) {   // planar: the dz = 0 slice, a 2-D transform (x rows, y cols)
-    even_cols<T>(2 * sp.Ny, 1, nx, no, B, b, out, tw[1], add, scale, s);
+    even_cols<T>(2 * sp.Ny, 1, nx, no, B, b, out, tw[1], add, scale, s, odd == 1);
     return;
   }
-  if (evyz<T>(sp, B, b, out, add, scale, s)) return;
-  even_cols<T>(2 * sp.Nz, ny, nx, no, B, b, a, tw[2], nullptr, (T)1, s);
-  even_cols<T>(2 * sp.Ny, 1, nz * nx, no, B, a, out, tw[1], add, scale, s);
+  if (evyz<T>(sp, B, b, out, add, scale, s, odd)) return;
+  even_cols<T>(2 * sp.Nz, ny, nx, no, B, b, a, tw[2], nullptr, (T)1, s, odd == 2);
+  even_cols<T>(2 * sp.Ny, 1, nz * nx, no, B, a, out, tw[1], add, scale, s, odd == 1);
 }
+
+int odd_axis(int kind) { return kind >= 2 ? kind - 2 : -1; }
 
 }  // namespace
 
@@ -413,7 +457,7 @@ void spectrum_static(SpectrumPlan& sp, double2* out, cudaStream_t s, int kind) {
   launch_pdl(k_sample_static, dim3((unsigned)((sp.noct + 255) / 256)), dim3(256), 0, s, sp.Nx, sp.Ny, sp.Nz,
              sp.nz1, sp.noct, sp.h, (double2*)sp.work0, kind);
   AIMX_CHECK_LAUNCH();
-  dct3<double>(sp, 1, sp.tw64, sp.work0, sp.work1, out, nullptr, 1.0, s);
+  dct3<double>(sp, 1, sp.tw64, sp.work0, sp.work1, out, nullptr, 1.0, s, nullptr, odd_axis(kind));
 }
 
 void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float2* Hs, float scale,
@@ -422,7 +466,7 @@ void spectrum_dynamic_f32(SpectrumPlan& sp, int B, const double* k0, const float
   SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.nz1, sp.h, {}, kind};
   for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
   // K_d samples generated inside the x pass (each sample once per line)
-  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s, &sa);
+  dct3<float>(sp, B, sp.tw32, sp.work0, sp.work1, out, Hs, scale, s, &sa, odd_axis(kind));
 }
 
 void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const double2* Hs, double scale,
@@ -431,7 +475,7 @@ void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const doubl
   SampleArgs sa{sp.Nx, sp.Ny, sp.Nz, sp.nz1, sp.h, {}, kind};
   for (int b = 0; b < B; ++b) sa.k0[b] = k0[b];
   // K_d samples generated inside the x pass (each sample once per line)
-  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s, &sa);
+  dct3<double>(sp, B, sp.tw64, sp.work0, sp.work1, out, Hs, scale, s, &sa, odd_axis(kind));
 }
 
 }  // namespace aimx

@@ -30,16 +30,21 @@ def test_K_static_vs_oracle(subdiv, n):
     assert rel_l2(ck, ks + res) > 1e-6          # the precorrection is not negligible
 
 
+@pytest.mark.parametrize("form", ["grad", "radial"])
 @pytest.mark.parametrize("prec", ["c128", "c64"])
-@pytest.mark.parametrize("subdiv,n", [(1, (8, 8, 8)), (2, (16, 16, 16))])
-def test_K_matvec_vs_oracle(prec, subdiv, n):
-    """aimx_matvec_kop (the grid part through the radial factor F, two passes
-    of the hot-path transforms) against the oracle's AIMx K (odd gradient
-    spectra) on closed icospheres."""
+@pytest.mark.parametrize("subdiv,n", [(1, (8, 8, 8)), (2, (16, 16, 16)), (2, (24, 24, 24))])
+def test_K_matvec_vs_oracle(prec, subdiv, n, form, monkeypatch):
+    """aimx_matvec_kop against the oracle's AIMx K (odd gradient spectra) on
+    closed icospheres.  grad: the device's gradient-of-kernel form (one
+    forward / inverse transform pair, the spectral cross product in the fused
+    short y/z pass (8^3 c64) or the TMA z pass; 24^3: padded 48, radix 3);
+    radial (AIMX_K_RADIAL=1): the radial factor F, two passes."""
     from oracle.aimx import AIMxOracle
     from oracle.kop import AIMxK
     from paper_2009_02281_b200 import AIMxError
     from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    if form == "radial":
+        monkeypatch.setenv("AIMX_K_RADIAL", "1")
     m = inp.icosphere_mesh(subdiv, radius=0.5)
     orc = AIMxOracle(m.vertices, m.triangles, n, static=False)
     ak = AIMxK(orc)
@@ -48,6 +53,7 @@ def test_K_matvec_vs_oracle(prec, subdiv, n):
     with pytest.raises(AIMxError):
         op.matvec_kop(to_gpu(x, prec))            # not enabled
     op.set_kop(True)
+    assert op.stats()["kop_grad"] == (form == "grad")
     for f in (50e6, 300e6):
         op.set_frequency(f)
         k0 = 2 * np.pi * f / 299792458.0
@@ -181,3 +187,56 @@ def test_kop_api_edges():
     s = make_gpu_op(m, (8, 8, 8), "c128", slab=("emulate", 2))
     with pytest.raises(AIMxError):
         s.set_kop(True)
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_pmchwt_flat_faced_cube_vs_oracle(prec):
+    """PMCHWT (eps_r = 4) on a cube (flat faces, cfg4's body at a small size,
+    grid 24^3 padded 48): with the gradient-of-kernel spectra the c64 path
+    meets the north_star bar on both equations (the radial form's fp32
+    cancellation on flat faces missed it: 2.8e-5 on the H rows)."""
+    from oracle.aimx import AIMxOracle
+    from oracle.kop import AIMxK, pmchwt_matvec
+    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    m = inp.box_mesh(8, 8, 8, (0.0, 0.0, 0.0), (0.5, 0.5, 0.5))
+    n = (24, 24, 24)
+    orc = AIMxOracle(m.vertices, m.triangles, n)
+    ak = AIMxK(orc)
+    op = make_gpu_op(m, n, prec)
+    op.set_kop(True)
+    assert op.stats()["kop_grad"]
+    x = np.random.default_rng(61).standard_normal(2 * op.N) * (1 - 0.4j)
+    x[op.N:] /= 376.73
+    for f in (100e6, 400e6):
+        op.set_frequency(f)
+        y = op.matvec_pmchwt(4.0, to_gpu(x, prec)).cpu().numpy()
+        ref = pmchwt_matvec(orc, ak, f, 4.0, gpu_input_as_c128(x, prec))
+        for sl in (slice(0, op.N), slice(op.N, 2 * op.N)):
+            assert rel_l2(y[sl], ref[sl]) <= TOL[prec], (f, sl, rel_l2(y[sl], ref[sl]))
+
+
+def test_cfg4_pmchwt_fullsize_c64():
+    """cfg4 as BASELINE.json names it: the dielectric cube (eps_r = 4, 0.5 m,
+    60,552 RWG -> 121,104 unknowns [J; M]), grid 96^3 (padded 192: radix 3),
+    K via the gradient-of-kernel spectra, c64.  The PMCHWT matvec against the
+    oracle on 24 seeded rows of each equation (the oracle's grid parts on the
+    full grid, its near parts row by row) at the first and last frequency."""
+    from oracle.aimx import from_config
+    from oracle.kop import pmchwt_rows, static_K_rows
+    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    c = inp.get_config(4)
+    orc = from_config(4, static=False)
+    op = make_gpu_op(inp.make_mesh(4), c.grid_n, "c64")
+    op.set_kop(True)
+    assert op.stats()["kop_grad"] and op.N == 60552
+    rows = np.sort(np.random.default_rng(44).choice(op.N, 24, replace=False))
+    kr = static_K_rows(orc, rows)
+    rng = np.random.default_rng(45)
+    x = (rng.standard_normal(2 * op.N) + 1j * rng.standard_normal(2 * op.N))
+    x[op.N:] /= 376.73
+    for f in (c.freqs[0], c.freqs[-1]):
+        op.set_frequency(f)
+        y = op.matvec_pmchwt(4.0, to_gpu(x, "c64")).cpu().numpy()
+        yE, yH = pmchwt_rows(orc, kr, f, 4.0, gpu_input_as_c128(x, "c64"))
+        assert rel_l2(y[rows], yE) <= TOL["c64"]
+        assert rel_l2(y[op.N + rows], yH) <= TOL["c64"]

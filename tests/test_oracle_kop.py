@@ -191,3 +191,24 @@ def test_pmchwt_equal_media_reduces_to_doubled_blocks(sph):
     Kj, Km = ak.matvec(J, k0, residue=False), ak.matvec(M, k0, residue=False)
     assert np.linalg.norm(y[:op.N] - (2 * op.matvec(J) - 2 * Km)) <= 1e-12 * np.linalg.norm(y[:op.N])
     assert np.linalg.norm(y[op.N:] - (2 * Kj + 2 * op.matvec(M) / eta0 ** 2)) <= 1e-12 * np.linalg.norm(y[op.N:])
+
+
+def test_rows_variants_equal_the_full_operators(sph):
+    # the sampled-row forms used by the full-size GPU parity tests (cfg4):
+    # C_K row by row and the grid part on the full grid give the same rows
+    from oracle.kop import kop_rows, pmchwt_matvec, pmchwt_rows, static_K_rows
+    op = sph
+    ak = AIMxK(op)
+    rows = np.array([0, 7, 33, op.N - 1])
+    kr = static_K_rows(op, rows)
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal(op.N) + 1j * rng.standard_normal(op.N)
+    k0 = 2 * np.pi * 120e6 / 299792458.0
+    for res in (True, False):
+        full = ak.matvec(x, k0, residue=res)
+        assert np.linalg.norm(kop_rows(op, kr, x, k0, residue=res) - full[rows]) <= 1e-12 * np.linalg.norm(full[rows])
+    x2 = rng.standard_normal(2 * op.N) + 1j * rng.standard_normal(2 * op.N)
+    y = pmchwt_matvec(op, ak, 120e6, 4.0, x2)
+    yE, yH = pmchwt_rows(op, kr, 120e6, 4.0, x2)
+    assert np.linalg.norm(yE - y[rows]) <= 1e-12 * np.linalg.norm(y[rows])
+    assert np.linalg.norm(yH - y[op.N + rows]) <= 1e-12 * np.linalg.norm(y[op.N + rows])
