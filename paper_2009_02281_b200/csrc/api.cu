@@ -496,10 +496,10 @@ int choose_slots(aimx_ctx* c) {
   // S, bufA, bufC, bufB, phi (double-buffered), the spectra (bound + 2 sweep
   // buffers) and the spectrum plan's two fp64 work octants
   const int64_t per_freq = (int64_t)cs * (nS + 2 * nA + nB + 2 * nP + 3 * noct) + 2 * (int64_t)sizeof(double2) * noct;
-  // per-frequency grid buffers within 6 GB (of 180 GB): cfg3 gets 8 slots, its
-  // 16-point sweep +17% over 2 slots (measured 1566 / 1691 / 1827 / 1730
-  // freq-pts/s at 2 / 4 / 8 / 16)
-  int slots = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)(6144ll << 20) / per_freq));
+  // per-frequency grid buffers within 12 GB (of 180 GB): cfg3 gets 8 slots, its
+  // 16-point sweep +17% over 2 slots (round 1: 1566 / 1691 / 1827 / 1730
+  // freq-pts/s at 2 / 4 / 8 / 16); planar cfg5 32
+  int slots = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)(12288ll << 20) / per_freq));
   if (const char* e = std::getenv("AIMX_BATCH")) slots = std::max(1, std::min(kMaxBatch, std::atoi(e)));
   while (slots & (slots - 1)) slots &= slots - 1;   // power of two (batch buckets never exceed it)
   return slots;

@@ -340,10 +340,18 @@ __global__ void __launch_bounds__(XinvB<T, L>::NT) k_xinv_b(HotDev h, int B) {
 struct ColTile {
   int w, rsub, CW, RPC;
 };
+// column tile width: the largest power of two <= NL that divides W (W = 8 N_x,
+// or 4 x the kx slab: a multiple of 8; radix-3 grids such as N_x = 24 give W
+// = 192, not a multiple of the 128 lines of a length-48 pass)
+__host__ __device__ __forceinline__ int col_width(int W, int NL) {
+  int cw = NL < W ? NL : W;
+  while (cw > 8 && W % cw) cw >>= 1;
+  return cw;
+}
 template <typename T, int L> __device__ __forceinline__ ColTile col_tile(int line, int W) {
   constexpr int NL = PassGeom<T, L>::NL;
   ColTile ct;
-  ct.CW = NL < W ? NL : W;
+  ct.CW = col_width(W, NL);
   ct.RPC = NL / ct.CW;
   ct.w = line % ct.CW;
   ct.rsub = line / ct.CW;
@@ -1187,7 +1195,7 @@ void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
 
 template <typename T, int L> dim3 col_grid(int W, int rows, int B) {
   constexpr int NL = PassGeom<T, L>::NL;
-  const int CW = NL < W ? NL : W;
+  const int CW = col_width(W, NL);
   const int RPC = NL / CW;
   return dim3((unsigned)(W / CW), (unsigned)((rows + RPC - 1) / RPC), (unsigned)B);
 }
@@ -1249,7 +1257,7 @@ void run_z(const HotDev& h, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L>() + 2 * sizeof(typename CT<T>::T2) * (size_t)PassGeom<T, L>::NL * L / 4;
   dim3 g = col_grid<T, L>(h.W, 2 * h.Ny, B);
   g.y = (g.y + ZROWS - 1) / ZROWS;   // row sets per CTA
-  if (h.tmB && h.nzocc == h.Nz && h.W >= ZGeom<T, L>::NL && h.Nz <= 256) {
+  if (h.tmB && h.nzocc == h.Nz && h.W >= ZGeom<T, L>::NL && h.W % ZGeom<T, L>::NL == 0 && h.Nz <= 256) {
     using Z = ZTma<T, L>;
     const size_t zs = Z::smem(h.Nz);
     set_smem(k_zconv_tma<T, L>, zs);
@@ -1449,7 +1457,7 @@ template <typename T, int L> void run_z_curl(const HotDev& h, cudaStream_t s) {
 template <typename T> bool z_curl_tma_ok(const HotDev& h) {
   int nl = 0;
   AIMX_SWITCH_L(2 * h.Nz, (nl = ZGeom<T, L>::NL));
-  return h.tmB && h.nzocc == h.Nz && h.W >= nl && h.Nz <= 256;
+  return h.tmB && h.nzocc == h.Nz && h.W >= nl && h.W % nl == 0 && h.Nz <= 256;
 }
 
 // S3 between the x transforms: the planar y pass, the fused short y/z pass,

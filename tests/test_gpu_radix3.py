@@ -18,10 +18,13 @@ CASES = [
     ("box", (24, 48, 96)),      # x 48, y 96, z 192 (TMA z pass, separate y passes)
     ("box", (96, 24, 24)),      # x 192, y / z 48
     ("plate", (96, 48, 4)),     # planar: x 192, planar y pass 96
+    ("sphere", (24, 24, 24)),   # 48 on every axis, W = 192 not a multiple of the pass's 128 lines
 ]
 
 
 def _mesh(kind, n):
+    if kind == "sphere":
+        return inp.icosphere_mesh(2, radius=0.5)
     if kind == "plate":
         return inp.plate_mesh(40, 20, 1.0, 0.5)
     ext = np.array(n, float) / max(n) * 0.9          # box filling the grid
