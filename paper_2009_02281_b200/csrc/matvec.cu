@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
 // one is used); within a chunk each group issues its x-row loads 8 at a time
 // before the arithmetic (packed FFMA2 in fp32).
 template <typename T, int BB>
-__global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
-                                                  int B) {
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
+                                                     int B) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(256) k_gather_b(HotDev h, const typename CT<T>
   constexpr int V = sizeof(T2) == 8 ? 2 : 1;
   constexpr int LG = BB / V, NG = 32 / LG;
   constexpr int PER = 32 / NG;             // entries of a chunk per group
-  constexpr int QB = PER < 8 ? PER : 8;    // loads in flight per batch
+  // loads in flight per batch: 4 (3 CTAs of 256 threads per SM; with 8 the
+  // registers allowed 2 and the gather was latency bound at 22% occupancy)
+  constexpr int QB = PER < 4 ? PER : 4;
   using VT = typename std::conditional<V == 2, float4, double2>::type;
   const int lane = threadIdx.x & 31;
   const int b0 = (lane % LG) * V, g = lane / LG;
