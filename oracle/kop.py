@@ -281,8 +281,9 @@ def grid_K(op, x, k0: float):
     import scipy.fft as sfft
     Nx, Ny, Nz = op.grid.n
     g = np.stack([(op.P[b] @ x).reshape(Nz, Ny, Nx) for b in range(3)])
-    G = sfft.fftn(g, s=(2 * Nz, 2 * Ny, 2 * Nx), axes=(-3, -2, -1))
-    Hh = sfft.fftn(gradient_kernel_samples(op.grid.n, op.grid.h, k0), axes=(-3, -2, -1))
+    from .convolution import WORKERS
+    G = sfft.fftn(g, s=(2 * Nz, 2 * Ny, 2 * Nx), axes=(-3, -2, -1), workers=WORKERS)
+    Hh = sfft.fftn(gradient_kernel_samples(op.grid.n, op.grid.h, k0), axes=(-3, -2, -1), workers=WORKERS)
     y = np.zeros(op.N, np.complex128)
     for c in range(3):
         acc = np.zeros_like(G[0])
@@ -290,7 +291,7 @@ def grid_K(op, x, k0: float):
             for b in range(3):
                 if EPS3[c, a, b] != 0.0:
                     acc += EPS3[c, a, b] * Hh[a] * G[b]
-        phi = sfft.ifftn(acc)[:Nz, :Ny, :Nx]
+        phi = sfft.ifftn(acc, workers=WORKERS)[:Nz, :Ny, :Nx]
         y -= op.P[c].T @ phi.ravel()
     return y
 

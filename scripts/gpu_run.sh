@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 TAG=${TAG:-run}
 python -m paper_2009_02281_b200.build > gpurun_out/${TAG}_build.log 2>&1 || { echo build failed; exit 1; }
 if [ -n "${TESTS:-}" ]; then
-  timeout ${TTIME:-1500} python -m pytest $TESTS -m gpu -x -q ${K:+-k "$K"} > gpurun_out/${TAG}_pytest.log 2>&1
+  timeout ${TTIME:-1500} python -m pytest $TESTS -m gpu -x -q --durations=30 ${K:+-k "$K"} > gpurun_out/${TAG}_pytest.log 2>&1
   echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
 fi
 for c in ${BENCH:-}; do

@@ -1,7 +1,7 @@
-"""cfg4's formulation on the B200: the dielectric cube (eps_r = 4, side 0.5 m,
-40,368 triangles, 60,552 RWG per current) with PMCHWT (aimx_matvec_pmchwt).
-BASELINE's 96^3 grid needs the FFT length 192, which the library does not
-support, so the grid is 128^3 (the next supported size, a finer grid): setup
+"""cfg4 on the B200: the dielectric cube (eps_r = 4, side 0.5 m, 40,368
+triangles, 60,552 RWG per current) with PMCHWT (aimx_matvec_pmchwt) on
+BASELINE's 96^3 grid (padded 192, radix 3), K through the gradient-of-kernel
+spectra (and the radial form with AIMX_K_RADIAL=1 for comparison): setup
 time, PMCHWT matvec time, and c64 against c128.  JSON line."""
 import json
 import os
@@ -17,21 +17,24 @@ import aimx_inputs as inp  # noqa: E402
 from paper_2009_02281_b200 import AIMx  # noqa: E402
 
 m = inp.make_mesh(4)
-n = (128, 128, 128)
+n = (96, 96, 96)
 f = 350e6                       # mid-band of cfg4's 100-600 MHz
 out = {"mesh": "cfg4 cube", "grid": list(n), "eps_r": 4.0, "f_hz": f}
 res = {}
-for prec in ("c64", "c128"):
+for prec in ("c64", "c128", "c64_radial"):
+    if prec == "c64_radial":
+        os.environ["AIMX_K_RADIAL"] = "1"
     t0 = time.perf_counter()
-    op = AIMx(m.vertices, m.triangles, n, prec=prec)
+    op = AIMx(m.vertices, m.triangles, n, prec=prec[:3] if prec != "c128" else "c128")
     op.set_kop(True)
+    out[f"{prec}_kop_grad"] = op.stats()["kop_grad"]
     torch.cuda.synchronize()
     out[f"{prec}_setup_s"] = time.perf_counter() - t0
     N = op.N
     rng = np.random.default_rng(4)
     x = rng.standard_normal(2 * N) + 1j * rng.standard_normal(2 * N)
     x[N:] /= 376.73
-    dt = torch.complex64 if prec == "c64" else torch.complex128
+    dt = torch.complex128 if prec == "c128" else torch.complex64
     xg = torch.as_tensor(x).to(dt).cuda()
     op.set_frequency(f)
     y = op.matvec_pmchwt(4.0, xg)
@@ -50,6 +53,7 @@ for prec in ("c64", "c128"):
     torch.cuda.empty_cache()
 N = out["N_rwg"]
 for name, sl in (("E", slice(0, N)), ("H", slice(N, 2 * N))):
-    out[f"c64_vs_c128_relL2_{name}"] = float(np.linalg.norm(res["c64"][sl] - res["c128"][sl]) /
-                                             np.linalg.norm(res["c128"][sl]))
+    for k in ("c64", "c64_radial"):
+        out[f"{k}_vs_c128_relL2_{name}"] = float(np.linalg.norm(res[k][sl] - res["c128"][sl]) /
+                                                 np.linalg.norm(res["c128"][sl]))
 print(json.dumps(out))

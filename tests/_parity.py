@@ -45,3 +45,15 @@ def check_structure(op_gpu, op_orc):
     st = op_gpu.stats()
     assert st["h"] == op_orc.grid.h
     assert np.array_equal(np.array(st["origin"]), op_orc.grid.origin)
+
+
+_ORC = {}
+
+
+def oracle_config(cfg: int):
+    """The oracle of a config with its grid part only (static=False), built
+    once per test session (cfg5 takes ~40 s) and shared by the full-size tests."""
+    if cfg not in _ORC:
+        from oracle.aimx import from_config
+        _ORC[cfg] = from_config(cfg, static=False)
+    return _ORC[cfg]

@@ -6,15 +6,14 @@ import numpy as np
 import pytest
 
 import aimx_inputs as inp
-from tests._parity import TOL, check_structure, gpu_input_as_c128, make_gpu_op, rel_l2, to_gpu
+from tests._parity import TOL, check_structure, gpu_input_as_c128, make_gpu_op, oracle_config, rel_l2, to_gpu
 
 pytestmark = pytest.mark.gpu
 
 
 def _fullsize(cfg, prec, freqs, nrows, orc=None):
-    from oracle.aimx import from_config
     c = inp.get_config(cfg)
-    orc = orc if orc is not None else from_config(cfg, static=False)
+    orc = orc if orc is not None else oracle_config(cfg)
     op = make_gpu_op(inp.make_mesh(cfg), c.grid_n, prec)
     check_structure(op, orc)
     lam = op.weights()
@@ -69,11 +68,10 @@ def test_cfg2_bench_sweep_vs_oracle_rows():
     """bench.py's launch configuration (cfg2, c64, the 100-point sweep in
     device batches of 32, 32, 32 and 4 points, 32- and 4-column kernels)
     against the oracle on seeded sampled rows."""
-    from oracle.aimx import from_config
     c = inp.get_config(2)
     op = make_gpu_op(inp.make_mesh(2), c.grid_n, "c64")
     assert op.stats()["batch_slots"] == 32      # 100 points -> device batches 32, 32, 32, 4
-    orc = from_config(2, static=False)
+    orc = oracle_config(2)
     X = np.stack([inp.rhs_vector(2, i, op.N) for i in range(len(c.freqs))])
     Y = op.sweep(c.freqs, to_gpu(X, "c64")).cpu().numpy()
     rows = np.sort(np.random.default_rng(22).choice(op.N, 32, replace=False))
@@ -89,8 +87,7 @@ def test_cfg2_bench_sweep_vs_oracle_rows():
 
 @pytest.fixture(scope="module")
 def orc5():
-    from oracle.aimx import from_config
-    return from_config(5, static=False)        # grid part on the full 1024 x 1024 x 16 padded grid
+    return oracle_config(5)        # grid part on the full 1024 x 1024 x 16 padded grid
 
 
 def test_cfg5_fullsize_c64(orc5):

@@ -30,6 +30,9 @@ def test_K_static_vs_oracle(subdiv, n):
     assert rel_l2(ck, ks + res) > 1e-6          # the precorrection is not negligible
 
 
+_KORC = {}   # oracle K per (icosphere, grid), shared by precisions and forms
+
+
 @pytest.mark.parametrize("form", ["grad", "radial"])
 @pytest.mark.parametrize("prec", ["c128", "c64"])
 @pytest.mark.parametrize("subdiv,n", [(1, (8, 8, 8)), (2, (16, 16, 16)), (2, (24, 24, 24))])
@@ -46,8 +49,10 @@ def test_K_matvec_vs_oracle(prec, subdiv, n, form, monkeypatch):
     if form == "radial":
         monkeypatch.setenv("AIMX_K_RADIAL", "1")
     m = inp.icosphere_mesh(subdiv, radius=0.5)
-    orc = AIMxOracle(m.vertices, m.triangles, n, static=False)
-    ak = AIMxK(orc)
+    if (subdiv, n) not in _KORC:
+        orc = AIMxOracle(m.vertices, m.triangles, n, static=False)
+        _KORC[(subdiv, n)] = (orc, AIMxK(orc))
+    orc, ak = _KORC[(subdiv, n)]
     op = make_gpu_op(m, n, prec)
     x = np.random.default_rng(11).standard_normal(op.N) + 1j * np.random.default_rng(12).standard_normal(op.N)
     with pytest.raises(AIMxError):
@@ -221,11 +226,10 @@ def test_cfg4_pmchwt_fullsize_c64():
     K via the gradient-of-kernel spectra, c64.  The PMCHWT matvec against the
     oracle on 24 seeded rows of each equation (the oracle's grid parts on the
     full grid, its near parts row by row) at the first and last frequency."""
-    from oracle.aimx import from_config
     from oracle.kop import pmchwt_rows, static_K_rows
-    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    from tests._parity import TOL, gpu_input_as_c128, oracle_config, to_gpu
     c = inp.get_config(4)
-    orc = from_config(4, static=False)
+    orc = oracle_config(4)
     op = make_gpu_op(inp.make_mesh(4), c.grid_n, "c64")
     op.set_kop(True)
     assert op.stats()["kop_grad"] and op.N == 60552
