@@ -415,7 +415,10 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   const int cs = f32 ? 8 : 16;
   if (c->slots <= 0) throw Error(AIMX_E_INTERNAL, "batch slots not chosen before the near layout");
   std::vector<int64_t> cta_begin;
-  const int ncta = near_ctas_per_sm(f32, false, grp.R) * nsm;   // one wave of resident CTAs
+  // one wave of resident CTAs (AIMX_NEAR_SMS: spread over fewer SMs, experiments)
+  int nsm_near = nsm;
+  if (const char* e = std::getenv("AIMX_NEAR_SMS")) nsm_near = std::max(1, std::min(nsm, std::atoi(e)));
+  const int ncta = near_ctas_per_sm(f32, false, grp.R) * nsm_near;
   const std::vector<int64_t> order = near_round_order(grp.ngrp, ncta, cta_begin);
   build_near_chunks(grp, near_chw(f32, c->slots), near_chc(f32, c->slots), cs, ck, order);
   // value slot (u R + r) -> payload byte offset

@@ -101,6 +101,7 @@ def full(path, out, jpath=None, key=None):
 
 def stage_of(k):
     for pat, st in (("k_interp_near", "interp_near"), ("k_zconv", "zconv"), ("k_yzconv", "zconv"),
+                    ("k_yconv_plane", "zconv"), ("k_gather_b", "proj_xfft"), ("k_xfwd", "proj_xfft"),
                     ("k_yfwd", "yfwd"), ("k_yinv", "yinv"), ("k_xinv", "xinv")):
         if pat in k:
             return st

@@ -71,16 +71,16 @@ def test_K_matvec_vs_oracle(prec, subdiv, n, form, monkeypatch):
 def k3():
     from oracle.aimx import AIMxOracle
     from oracle.kop import AIMxK
-    m = inp.icosphere_mesh(3, radius=0.5)
+    m = inp.icosphere_mesh(2, radius=0.5)
     orc = AIMxOracle(m.vertices, m.triangles, (32, 32, 32), static=False)
     return m, AIMxK(orc)
 
 
 @pytest.mark.parametrize("prec", ["c128", "c64"])
 def test_K_matvec_long_transforms(prec, k3):
-    """1920 RWG on a 32^3 grid: the y / z transforms are too long for the fused
-    kernel and every z plane is occupied, so the two F passes run the separate
-    y passes and the TMA z pass."""
+    """A 32^3 grid: the y / z transforms are too long for the fused kernel and
+    every z plane is occupied, so K runs the separate y passes and the TMA z
+    pass (with the spectral cross product)."""
     from tests._parity import TOL, gpu_input_as_c128, to_gpu
     m, ak = k3
     op = make_gpu_op(m, (32, 32, 32), prec)
@@ -205,8 +205,10 @@ def test_pmchwt_flat_faced_cube_vs_oracle(prec):
     from tests._parity import TOL, gpu_input_as_c128, to_gpu
     m = inp.box_mesh(8, 8, 8, (0.0, 0.0, 0.0), (0.5, 0.5, 0.5))
     n = (24, 24, 24)
-    orc = AIMxOracle(m.vertices, m.triangles, n)
-    ak = AIMxK(orc)
+    if "cube" not in _KORC:
+        orc = AIMxOracle(m.vertices, m.triangles, n)
+        _KORC["cube"] = (orc, AIMxK(orc))
+    orc, ak = _KORC["cube"]
     op = make_gpu_op(m, n, prec)
     op.set_kop(True)
     assert op.stats()["kop_grad"]
