@@ -30,10 +30,16 @@
  *   see aimx_get_rwg).  Input and output must not alias.
  * - `stream` is a cudaStream_t passed as void*; NULL means the context's own
  *   stream (the one given to aimx_setup).  Work is enqueued asynchronously:
- *   no host synchronisation and no allocation happens in aimx_matvec /
- *   aimx_matvec_parts / aimx_sweep.  A context owns one set of work buffers,
- *   so calls on one context must not run concurrently on different streams
- *   (the library orders them with events; it is not thread-safe).
+ *   no host synchronisation and no buffer allocation happens in aimx_matvec /
+ *   aimx_matvec_parts / aimx_sweep, with one exception: the second call of
+ *   aimx_matvec / aimx_matvec_parts with the same (x, y, mode, frequency)
+ *   captures its launch sequence and instantiates a CUDA graph (driver
+ *   memory for the graph; at most 8 are kept; AIMX_NO_GRAPH=1 disables it),
+ *   which later identical calls replay.  aimx_matvec_pmchwt allocates its
+ *   interior-medium spectra on its first call.  A context owns one set of
+ *   work buffers: calls on different streams are ordered by the library with
+ *   events (each waits for the previous call on any stream), never run
+ *   concurrently on those buffers; a context is not thread-safe.
  * - Asynchronous CUDA faults surface as AIMX_E_CUDA on the next call.
  * - Independent contexts are independent (one per GPU / process in the
  *   multi-GPU frequency-sharded sweep).

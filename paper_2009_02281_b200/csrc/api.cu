@@ -200,6 +200,12 @@ __global__ void k_d2f(int64_t n, const double2* __restrict__ a, float2* __restri
 
 unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+// flag = 1 if any weight of channel c is non-zero (lam [n][4], fp64)
+__global__ void k_chan_nonzero(int64_t n, const double* __restrict__ lam, int c, int* flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && lam[4 * i + c] != 0.0) atomicOr(flag, 1);
+}
+
 void* make_twiddles(aimx_ctx* c, int L) {
   // exp(-2 pi i m / L) with exact octant reduction, computed in fp64
   std::vector<double> re(L), im(L);
@@ -556,6 +562,18 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
   if (c->planar) {
     h.planar = 1;
     h.phi_off = (int64_t)c->nodes.zplanes[0] * h.Nx * h.Ny;
+    // a mesh in a z plane has f_z = 0, so Lambda^z is exactly zero: the z
+    // channel of the grid is never transformed (reading R12)
+    int* flag = dalloc<int>(c, 1);
+    AIMX_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    const int64_t nw = (int64_t)t.nb * t.p3;
+    k_chan_nonzero<<<nblk(nw), 256, 0, c->stream>>>(nw, c->sd.lam, 2, flag);
+    AIMX_CHECK_LAUNCH();
+    int hf = 1;
+    AIMX_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    AIMX_CUDA(cudaStreamSynchronize(c->stream));
+    dfree(c, flag, (int64_t)sizeof(int));
+    h.zch = hf == 0 && !std::getenv("AIMX_NO_ZSKIP") ? 1 : 0;
   }
   const int slots = c->slots = choose_slots(c);
   build_gather(c, h, c->nodes);

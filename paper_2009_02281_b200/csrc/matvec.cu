@@ -293,32 +293,36 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   }
 }
 
-// ---- x inverse, batched (B >= 4): the CTA's 16 lines are the 4 channels x
-// 4 consecutive slots of one line, so both sides move whole 32-byte sectors:
-// each read covers the 4 channels of a slot's point (bufC[slot][line][kx][c]),
-// each write 4 consecutive slots of a channel (phi[node][c][slot]).  With the
-// per-slot mapping of k_xinv every phi write was a lone 8-byte piece of a
-// sector (cfg5, 32 columns: 766 us, issue 7%).
-template <typename T, int L> struct XinvB {
+// ---- x passes, batched (B >= 4): the CTA's lines are the NCH channels x 4
+// consecutive slots of one grid line, so both sides move whole 32-byte
+// sectors: each read or write of the grid rows covers the channels of a
+// slot's point ([slot][line][x][c]), each write of phi 4 consecutive slots of
+// a channel ([node][c][slot]).  With the per-slot mapping of k_xinv every phi
+// write was a lone 8-byte piece of a sector (cfg5, 32 columns: 766 us, issue
+// 7%).  NCH = 3: the z channel is identically zero (a planar mesh in a z
+// plane: f_z = 0, so Lambda^z = 0 exactly; reading R12) and is never
+// transformed -- a quarter of the x passes' work.
+template <int NCH> __device__ __forceinline__ int xch(int i) { return NCH == 4 ? i : (i == 2 ? 3 : i); }
+template <typename T, int L, int NCH = 4> struct XinvB {
   static constexpr int T_ = TwoLevel<Fac<L>::R1, Fac<L>::R2>::T;
-  static constexpr int NL = 16, NT = NL * T_;
+  static constexpr int NL = 4 * NCH, NT = NL * T_;
   static constexpr int XB = PassGeom<T, L>::XB;
   static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (L + (size_t)NL * XB);
 };
-template <typename T, int L>
-__global__ void __launch_bounds__(XinvB<T, L>::NT) k_xinv_b(HotDev h, int B) {
+template <typename T, int L, int NCH>
+__global__ void __launch_bounds__(XinvB<T, L, NCH>::NT) k_xinv_b(HotDev h, int B) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
-  using X = XinvB<T, L>;
+  using X = XinvB<T, L, NCH>;
   const int line = threadIdx.x % X::NL, t = threadIdx.x / X::NL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* tw = reinterpret_cast<T2*>(smem_raw);
   T2* xb = tw + L + line * X::XB;
   for (int i = threadIdx.x; i < L; i += X::NT) tw[i] = ((const T2*)h.twx)[i];
   __syncthreads();
-  const int r = blockIdx.x, c = line & 3, b = blockIdx.y * 4 + (line >> 2);
+  const int r = blockIdx.x, c = xch<NCH>(line % NCH), b = blockIdx.y * 4 + line / NCH;
   const bool act = b < B;
   const int lid = h.line_id[r];
   const T2* __restrict__ in = (const T2*)h.bufC + (int64_t)(act ? b : 0) * h.sA + (int64_t)lid * L * 4 + c;
@@ -336,6 +340,37 @@ __global__ void __launch_bounds__(XinvB<T, L>::NT) k_xinv_b(HotDev h, int B) {
     const int x = TwoLevel<G::R2, G::R1>::in_index(t, i);
     if (i % G::R1 < (G::R1 + 1) / 2 && x < Nx) out[x * ns] = v[i];
   }
+}
+
+// x forward, batched: occupied lines of S (x < Nx, zero padded) -> bufA[slot][line_id][kx][c]
+template <typename T, int L, int NCH>
+__global__ void __launch_bounds__(XinvB<T, L, NCH>::NT) k_xfwd_b(HotDev h, int B) {
+  pdl_wait();
+  pdl_trigger();
+  using T2 = typename CT<T>::T2;
+  using G = PassGeom<T, L>;
+  using X = XinvB<T, L, NCH>;
+  const int line = threadIdx.x % X::NL, t = threadIdx.x / X::NL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* tw = reinterpret_cast<T2*>(smem_raw);
+  T2* xb = tw + L + line * X::XB;
+  for (int i = threadIdx.x; i < L; i += X::NT) tw[i] = ((const T2*)h.twx)[i];
+  __syncthreads();
+  const int r = blockIdx.x, c = xch<NCH>(line % NCH), b = blockIdx.y * 4 + line / NCH;
+  const bool act = b < B;
+  const int Nx = h.Nx;
+  const T2* __restrict__ in = (const T2*)h.S + (int64_t)(act ? b : 0) * h.sS + (int64_t)r * Nx * 4 + c;
+  T2 v[G::E];
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) {   // x < Nx = L/2  <=>  n2 < R2/2
+    const int x = G::TL::in_index(t, i);
+    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * 4] : mk<T2>(0, 0);
+  }
+  fwd_fft<T2, L>(v, xb, tw, t);
+  if (!act) return;
+  T2* __restrict__ out = (T2*)h.bufA + (int64_t)b * h.sA + (int64_t)h.line_id[r] * L * 4 + c;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i) out[TwoLevel<G::R2, G::R1>::in_index(t, i) * 4] = v[i];
 }
 
 // Column passes: CTA = NL lines = (rows per CTA) x (column tile CW).
@@ -701,7 +736,9 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
 // frequency (spectrum.cu, planar plan).  The CTA's slab of H_hat2 (the octant
 // rows ky <= N_y of its CW/4 kx, mirrored on read) is staged in shared memory
 // while the forward transform runs.
-template <typename T, int L>
+// SKIPZ (h.zch): the z channel is identically zero; the CTA's column tile
+// enumerates only the active columns 4 kx + {0, 1, 3} (three quarters of the work)
+template <typename T, int L, bool SKIPZ = false>
 __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
   pdl_wait();
   pdl_trigger();
@@ -709,12 +746,15 @@ __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   const int W = h.W, Nx = h.Nx, Ny = h.Ny;
-  const ColTile ct = col_tile<T, L>(line, W);
+  const int Wa = SKIPZ ? 3 * (W / 4) : W;            // active columns
+  const ColTile ct = col_tile<T, L>(line, Wa);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* tw = reinterpret_cast<T2*>(smem_raw);
   T2* xb = tw + L + line * G::XB;
   T2* hs = tw + L + (size_t)G::NL * G::XB;          // [ky <= Ny][kx - kx0]
-  const int nkx = ct.CW / 4, kx0 = h.kx0 + (blockIdx.x * ct.CW) / 4;
+  const int ja = blockIdx.x * ct.CW;                 // first active column of the tile
+  const int kx0 = h.kx0 + (SKIPZ ? ja / 3 : ja / 4);
+  const int nkx = SKIPZ ? (ja + ct.CW - 1) / 3 - ja / 3 + 1 : ct.CW / 4;
   const int b = blockIdx.z;
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
   for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = ((const T2*)h.twy_tab)[i];
@@ -726,7 +766,9 @@ __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
   for (int y = threadIdx.x; y < Ny; y += blockDim.x) occ[y] = h.line_occ[(int64_t)h.zplane0 * Ny + y];
   __syncthreads();
   const bool act = ct.rsub == 0;   // one plane: the column tile's first row set only
-  const int64_t col = (int64_t)blockIdx.x * ct.CW + ct.w;
+  const int jc = ja + ct.w;                          // active column -> grid column 4 kx + c
+  const int64_t col = SKIPZ ? 4 * (jc / 3) + xch<3>(jc % 3) : jc;
+  const int kxl = SKIPZ ? jc / 3 - ja / 3 : ct.w >> 2;
   // per-element offsets in 32 bits (one slot's plane: Ny W < 2^31)
   const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + col;
   T2 v[G::E];
@@ -737,7 +779,7 @@ __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   {
-    const T2* hl = hs + (ct.w >> 2);
+    const T2* hl = hs + kxl;
 #pragma unroll
     for (int i = 0; i < G::E; ++i) {
       const int ky = TwoLevel<G::R2, G::R1>::in_index(t, i);
@@ -1178,16 +1220,28 @@ void run_x_geom(const HotDev& h, bool inv, int B, cudaStream_t s) {
   }
   AIMX_CHECK_LAUNCH();
 }
+template <typename T, int L, int NCH>
+void run_x_b(const HotDev& h, bool inv, int B, cudaStream_t s) {
+  using X = XinvB<T, L, NCH>;
+  const dim3 g((unsigned)h.nlines, (unsigned)((B + 3) / 4));
+  if (inv) {
+    set_smem(k_xinv_b<T, L, NCH>, X::SMEM);
+    launch_pdl(k_xinv_b<T, L, NCH>, g, dim3(X::NT), X::SMEM, s, h, B);
+  } else {
+    set_smem(k_xfwd_b<T, L, NCH>, X::SMEM);
+    launch_pdl(k_xfwd_b<T, L, NCH>, g, dim3(X::NT), X::SMEM, s, h, B);
+  }
+  AIMX_CHECK_LAUNCH();
+}
+
 // x passes: below two waves of default CTAs, one x row per (smaller) CTA;
 // batched inverse passes (B >= 4, lines of 64+ points) group 4 slots per CTA
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   if (h.nlines <= 0) return;
-  if (inv && B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024) {
-    using X = XinvB<T, L>;
-    set_smem(k_xinv_b<T, L>, X::SMEM);
-    launch_pdl(k_xinv_b<T, L>, dim3((unsigned)h.nlines, (unsigned)((B + 3) / 4)), dim3(X::NT), X::SMEM, s, h, B);
-    AIMX_CHECK_LAUNCH();
+  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || h.zch)) {
+    if (h.zch) run_x_b<T, L, 3>(h, inv, B, s);
+    else run_x_b<T, L, 4>(h, inv, B, s);
     return;
   }
   constexpr int RPC = PassGeom<T, L>::NL / 4;
@@ -1408,11 +1462,16 @@ void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combin
 }
 
 template <typename T, int L> void run_yconv_plane(const HotDev& h, int B, cudaStream_t s) {
-  constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)(L / 2 + 1) * (PassGeom<T, L>::NL / 4)
-                        + L / 2;   // + the occupied-row flags
-  set_smem(k_yconv_plane<T, L>, sm);
-  dim3 g = col_grid<T, L>(h.W, 1, B);
-  launch_pdl(k_yconv_plane<T, L>, g, dim3(PassGeom<T, L>::NT), sm, s, h);
+  // the slab: kx of the tile's columns (SKIPZ: CW/3 + 2 at most), + the occupied-row flags
+  constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)(L / 2 + 1) * (PassGeom<T, L>::NL / 3 + 2)
+                        + L / 2;
+  if (h.zch) {
+    set_smem(k_yconv_plane<T, L, true>, sm);
+    launch_pdl(k_yconv_plane<T, L, true>, col_grid<T, L>(3 * (h.W / 4), 1, B), dim3(PassGeom<T, L>::NT), sm, s, h);
+  } else {
+    set_smem(k_yconv_plane<T, L>, sm);
+    launch_pdl(k_yconv_plane<T, L>, col_grid<T, L>(h.W, 1, B), dim3(PassGeom<T, L>::NT), sm, s, h);
+  }
   AIMX_CHECK_LAUNCH();
 }
 
@@ -1591,6 +1650,7 @@ void hot_kop(const HotDev& h0, const void* x, void* y, const void* HF, void* phi
   HotDev h = h0;
   h.Hoct = const_cast<void*>(HF);
   h.batch = 1;   // one column: compact potentials ([node][channel])
+  h.zch = 0;     // s x J has a z component on planar meshes
   const int Lx = 2 * h.Nx;
   run_gather<T>(h, x, h.nb, 1, s);   // S = P x (one column)
   auto conv = [&](void* phi) {

@@ -415,3 +415,24 @@ def test_calls_on_several_streams_are_ordered():
             assert all(torch.equal(a, b) for a, b in zip(v, ref_pa[i]))
         else:
             assert torch.equal(v, ref_sw)
+
+
+def test_planar_z_channel_skip_is_exact(monkeypatch):
+    """A planar mesh (z = 0) has Lambda^z = 0 exactly, so the batched x passes
+    and the planar y pass skip the z channel (three of four channels
+    transformed); the results equal the four-channel run bit for bit."""
+    import torch
+    m = inp.patch_array_mesh(2, 2, 30e-3, 40e-3, 50e-3, 12, 16)
+    n = (64, 64, 4)
+    freqs = np.linspace(2e9, 6e9, 8)
+    X = to_gpu(np.stack([inp.rhs_vector(5, 400 + i, 1) * np.ones(1) for i in range(1)]), "c64")
+    outs = []
+    for skip in (True, False):
+        if not skip:
+            monkeypatch.setenv("AIMX_NO_ZSKIP", "1")
+        op = make_gpu_op(m, n, "c64")
+        assert op.stats()["planar"]
+        X = to_gpu(np.stack([inp.rhs_vector(5, 400 + i, op.N) for i in range(8)]), "c64")
+        outs.append(op.sweep(freqs, X).clone())
+        op.close()
+    assert torch.equal(outs[0], outs[1])
