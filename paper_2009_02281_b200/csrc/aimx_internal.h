@@ -308,8 +308,9 @@ struct HotDev {
   // 2-D spectrum of the dz = 0 kernel slice [ky][kx]
   int planar = 0;
   int64_t phi_off = 0;           // linear grid index of phi's node 0 (planar: z0 Nx Ny)
-  int zch = 0;                   // 1: the z channel is identically zero (Lambda^z = 0 exactly): the
-                                 // batched x passes and the planar y pass skip it
+  int zch = 0;                   // the z channel is identically zero (Lambda^z = 0 exactly); bits:
+                                 // 1 the batched x inverse, 2 the batched x forward, 4 the planar
+                                 // y pass, 8 the S4+S5 gathers skip it
   uint8_t* line_occ = nullptr;   // [Ny*Nz]
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)

@@ -573,7 +573,12 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     AIMX_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     AIMX_CUDA(cudaStreamSynchronize(c->stream));
     dfree(c, flag, (int64_t)sizeof(int));
-    h.zch = hf == 0 && !std::getenv("AIMX_NO_ZSKIP") ? 1 : 0;
+    // measured on cfg5 (32 columns): the x inverse (3 of 4 channel lines) and
+    // the S4+S5 potential gathers gain; the x forward and the planar y pass,
+    // whose active columns no longer fill whole sectors, lose (AIMX_ZSKIP_MASK)
+    int mask = 1 | 8;
+    if (const char* e = std::getenv("AIMX_ZSKIP_MASK")) mask = std::atoi(e) & 15;
+    h.zch = hf == 0 && !std::getenv("AIMX_NO_ZSKIP") ? mask : 0;
   }
   const int slots = c->slots = choose_slots(c);
   build_gather(c, h, c->nodes);

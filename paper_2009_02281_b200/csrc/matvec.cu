@@ -1008,6 +1008,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
   const int64_t ns = (int64_t)h.batch * 4;        // phi node stride (complex): [node][channel][slot]
   const T2* __restrict__ phi = (const T2*)h.phi + b0;
   const T2* __restrict__ xr = xt + b0;
+  const bool zch = (h.zch & 8) != 0;
   T be[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) be[v] = PARTS ? T(0) : (T)cb.beta[b0 + v];   // 0 for b >= B
@@ -1061,7 +1062,8 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
         if (e < d.w) {
           const T2* pr = phi + (int64_t)ix[e] * ns;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) buf[4 * i + c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
+          for (int c = 0; c < 4; ++c)   // zch: phi_z and Lambda^z are zero, its row is not gathered
+            if (c != 2 || !zch) buf[4 * i + c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
         }
       }
     }
@@ -1121,7 +1123,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
           T2& a = acc[r * V + v];
           axpy(a, w.x, pv[0][v]);
           axpy(a, w.y, pv[1][v]);
-          axpy(a, w.z, pv[2][v]);
+          if (!zch) axpy(a, w.z, pv[2][v]);
           if constexpr (PARTS) axpy(acc[(R + r) * V + v], w.w, pv[3][v]);
           else axpy(a, -be[v] * w.w, pv[3][v]);
         }
@@ -1239,8 +1241,9 @@ void run_x_b(const HotDev& h, bool inv, int B, cudaStream_t s) {
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   if (h.nlines <= 0) return;
-  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || h.zch)) {
-    if (h.zch) run_x_b<T, L, 3>(h, inv, B, s);
+  const int zbit = inv ? 1 : 2;
+  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || (h.zch & zbit))) {
+    if (h.zch & zbit) run_x_b<T, L, 3>(h, inv, B, s);
     else run_x_b<T, L, 4>(h, inv, B, s);
     return;
   }
@@ -1465,7 +1468,7 @@ template <typename T, int L> void run_yconv_plane(const HotDev& h, int B, cudaSt
   // the slab: kx of the tile's columns (SKIPZ: CW/3 + 2 at most), + the occupied-row flags
   constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)(L / 2 + 1) * (PassGeom<T, L>::NL / 3 + 2)
                         + L / 2;
-  if (h.zch) {
+  if (h.zch & 4) {
     set_smem(k_yconv_plane<T, L, true>, sm);
     launch_pdl(k_yconv_plane<T, L, true>, col_grid<T, L>(3 * (h.W / 4), 1, B), dim3(PassGeom<T, L>::NT), sm, s, h);
   } else {

@@ -425,7 +425,6 @@ def test_planar_z_channel_skip_is_exact(monkeypatch):
     m = inp.patch_array_mesh(2, 2, 30e-3, 40e-3, 50e-3, 12, 16)
     n = (64, 64, 4)
     freqs = np.linspace(2e9, 6e9, 8)
-    X = to_gpu(np.stack([inp.rhs_vector(5, 400 + i, 1) * np.ones(1) for i in range(1)]), "c64")
     outs = []
     for skip in (True, False):
         if not skip:
