@@ -466,6 +466,28 @@ def run_aimx(a):
     m = sweep_measure(op, c, prec, freqs, X, Y, flush, a.steps, a.warmup, barrier, a.sustained_seconds, world)
     tmax = m["tmax"]
     value = nf_job * a.steps / (tmax / 1e3)
+    weak = None
+    if world > 1 and a.mode == "shard" and a.scaling == "strong":
+        # second line: weak scaling (every rank sweeps the whole list; the
+        # batching per rank stays that of one GPU)
+        fw, iw = rank_freqs(c, rank, world, "weak")
+        Xw = torch.from_numpy(inp.rhs_matrix(a.config, op.N, iw)).to(cdt).cuda()
+        Yw = torch.empty_like(Xw)
+        for _ in range(a.warmup):
+            op.sweep(fw, Xw, Yw)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            flush.zero_()
+            op.sweep(fw, Xw, Yw)
+        e1.record()
+        torch.cuda.synchronize()
+        tw = max_over_ranks(e0.elapsed_time(e1))
+        weak = {"value": len(fw) * world * a.steps / (tw / 1e3), "unit": UNIT, "freq_pts_per_rank": len(fw),
+                "note": "every rank sweeps the config's whole list (flush included in the timed region)"}
+        del Xw, Yw
     plan = [min(st["batch_slots"], nf - i) for i in range(0, nf, st["batch_slots"])] if a.mode != "slab" else None
     cols = max(plan) if plan else 1
     roofline, stages, sb = roofline_of(st, prec, m["prof_all"], m["prof"], m["dom"], cols, a.config)
@@ -565,6 +587,7 @@ def run_aimx(a):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nf * vec_bytes,
                     "d2h_bytes_per_step": nf * vec_bytes},
             "gpu_launches": m["kernels_timed"],
+            "weak_scaling": weak,
             "roofline": roofline,
             "step_hbm": {"algorithmic_bytes": step_bytes, "GBps": step_bytes / (tmax / a.steps * 1e-3) / 1e9,
                          "frac": step_bytes / (tmax / a.steps * 1e-3) / 1e9 / roofline["peak"],

@@ -310,7 +310,7 @@ template <typename T, int L, int NCH = 4> struct XinvB {
   static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (L + (size_t)NL * XB);
 };
 template <typename T, int L, int NCH>
-__global__ void __launch_bounds__(XinvB<T, L, NCH>::NT) k_xinv_b(HotDev h, int B) {
+__global__ void __launch_bounds__(XinvB<T, L, NCH>::NT, (sizeof(T) == 4 && NCH == 3) ? 2 : 1) k_xinv_b(HotDev h, int B) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
