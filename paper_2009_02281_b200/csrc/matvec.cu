@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
 // SKIPZ (h.zch): the z channel is identically zero; the CTA's column tile
 // enumerates only the active columns 4 kx + {0, 1, 3} (three quarters of the work)
 template <typename T, int L, bool SKIPZ = false>
-__global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
+__global__ void __launch_bounds__(256, 2) k_yconv_plane(HotDev h) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
@@ -771,11 +771,18 @@ __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
   const int kxl = SKIPZ ? jc / 3 - ja / 3 : ct.w >> 2;
   // per-element offsets in 32 bits (one slot's plane: Ny W < 2^31)
   const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + col;
+  // this thread's occupied rows as a bit mask (the loads and the stores use
+  // the same rows): one shared-memory byte read per row, once
+  static_assert(G::E <= 64, "row mask");
+  uint64_t om = 0;
+#pragma unroll
+  for (int i = 0; i < G::E; ++i)
+    if (i % G::R2 < G::R2 / 2 && occ[G::TL::in_index(t, i)]) om |= 1ull << i;
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {   // y < Ny = L/2  <=>  n2 < R2/2; unoccupied rows are zero
     const int y = G::TL::in_index(t, i);
-    v[i] = (act && i % G::R2 < G::R2 / 2 && occ[y]) ? in[y * W] : mk<T2>(0, 0);
+    v[i] = (act && ((om >> i) & 1)) ? in[y * W] : mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   {
@@ -790,10 +797,8 @@ __global__ void __launch_bounds__(256) k_yconv_plane(HotDev h) {
   if (!act) return;
   T2* __restrict__ out = (T2*)h.bufC + b * h.sA + col;
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) {
-    const int y = G::TL::in_index(t, i);
-    if (i % G::R2 < G::R2 / 2 && occ[y]) out[y * W] = v[i];
-  }
+  for (int i = 0; i < G::E; ++i)
+    if ((om >> i) & 1) out[G::TL::in_index(t, i) * W] = v[i];
 }
 
 // ---- fused y fwd -> (z fwd * H_hat * z inv) -> y inv for short y and z
