@@ -198,7 +198,8 @@ def stage_bytes(st: dict, prec: str, B: int = 1, fused_yz: bool = False) -> dict
     nent = st["projection_entries"]
     planar = bool(st.get("planar"))
     noct = (Nx + 1) * (Ny + 1) * (1 if planar else Nz + 1)
-    row = 2 * Nx * 4 * s                    # one padded x-line, 4 channels
+    nc = st.get("grid_channels", 4)         # 3 on planar grids (the z channel is identically zero)
+    row = 2 * Nx * nc * s                   # one padded x-line, nc channels
     out = {
         "spectrum": noct * s + B * noct * s,                        # read H_hat_s, write H_hat per column
         "proj_xfft": nent * (4 + 4 * r) + 8 * nocc + B * (s * nb + nl * row),
@@ -206,11 +207,11 @@ def stage_bytes(st: dict, prec: str, B: int = 1, fused_yz: bool = False) -> dict
         "zconv": B * ((nz_ * Ny * row + nl * row + noct * s) if (fused_yz or planar)
                       else (2 * nz_ * 2 * Ny * row + noct * s)),
         "yinv": B * (nz_ * 2 * Ny * row + nl * row),
-        "xinv": B * (nl * row + nl * Nx * 4 * s),
+        "xinv": B * (nl * row + nl * Nx * nc * s),
         # S4 + S5: Lambda (RWG-major) and its index, the near matrix (CSR model:
         # column index + (C_A, C_rho)) and its row pointer, per column x, phi, y
         "interp_near": nb * p3 * 4 * r + 4 * nb + nnz * (4 + 2 * r) + 4 * (nb + 1)
-                       + B * (nocc * 4 * s + 2 * s * nb),
+                       + B * (nocc * nc * s + 2 * s * nb),
     }
     if planar:
         out["zconv"] = B * (2 * nl * row + noct * s)

@@ -125,6 +125,9 @@ typedef struct {
                                  dz = 0 kernel slice (AIMX_NO_PLANAR=1 at setup keeps the 3-D path) */
   int32_t kop_grad;           /* 1: the double-layer operator K runs through the gradient-of-kernel
                                  spectra (set after aimx_set_kop; 0: the radial form or not built) */
+  int32_t grid_channels;      /* channels of the grid passes: 4 (x, y, z, rho), or 3 on planar grids
+                                 whose Lambda^z is exactly zero (AIMX_NO_ZSKIP=1 keeps 4) */
+  int32_t reserved;
 } aimx_stats;
 
 /* S0 (the paper's "one-time static matrix-fill", tab:prof P:715): RWG basis,

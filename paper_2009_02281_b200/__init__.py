@@ -50,7 +50,8 @@ class _Stats(C.Structure):
                 ("setup_seconds", C.c_double),
                 ("n", C.c_int32 * 3), ("order", C.c_int32), ("h", C.c_double),
                 ("origin", C.c_double * 3), ("near_group_rows", C.c_int32), ("near_row_order", C.c_int32),
-                ("near_union", C.c_int64), ("planar", C.c_int32), ("kop_grad", C.c_int32)]
+                ("near_union", C.c_int64), ("planar", C.c_int32), ("kop_grad", C.c_int32),
+                ("grid_channels", C.c_int32), ("reserved", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -388,7 +389,7 @@ class AIMx:
                 "n": tuple(s.n), "order": s.order, "h": s.h, "origin": tuple(s.origin),
                 "near_group_rows": s.near_group_rows, "near_row_order": s.near_row_order,
                 "near_union": s.near_union, "planar": bool(s.planar),
-                "kop_grad": bool(s.kop_grad)}
+                "kop_grad": bool(s.kop_grad), "grid_channels": s.grid_channels}
 
     STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
 

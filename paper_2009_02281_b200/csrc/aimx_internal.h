@@ -308,9 +308,9 @@ struct HotDev {
   // 2-D spectrum of the dz = 0 kernel slice [ky][kx]
   int planar = 0;
   int64_t phi_off = 0;           // linear grid index of phi's node 0 (planar: z0 Nx Ny)
-  int zch = 0;                   // the z channel is identically zero (Lambda^z = 0 exactly); bits:
-                                 // 1 the batched x inverse, 2 the batched x forward, 4 the planar
-                                 // y pass, 8 the S4+S5 gathers skip it
+  int nc = 4;                    // channels stored in S / bufA / bufC / phi: 4 (x, y, z, rho), or 3
+                                 // (x, y, rho) on planar grids, where Lambda^z = 0 exactly (R12)
+  void* S4 = nullptr;            // nc = 3: a 4-channel S for the double-layer operator's passes
   uint8_t* line_occ = nullptr;   // [Ny*Nz]
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)

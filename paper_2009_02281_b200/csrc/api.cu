@@ -573,12 +573,12 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     AIMX_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     AIMX_CUDA(cudaStreamSynchronize(c->stream));
     dfree(c, flag, (int64_t)sizeof(int));
-    // measured on cfg5 (32 columns): the x inverse (3 of 4 channel lines) and
-    // the S4+S5 potential gathers gain; the x forward and the planar y pass,
-    // whose active columns no longer fill whole sectors, lose (AIMX_ZSKIP_MASK)
-    int mask = 1 | 8;
-    if (const char* e = std::getenv("AIMX_ZSKIP_MASK")) mask = std::atoi(e) & 15;
-    h.zch = hf == 0 && !std::getenv("AIMX_NO_ZSKIP") ? mask : 0;
+    // and the grid buffers store 3 channels (x, y, rho): a quarter less of
+    // every grid pass and of the potential gathers
+    if (hf == 0 && !std::getenv("AIMX_NO_ZSKIP")) {
+      h.nc = 3;
+      h.W = 2 * h.Nx * 3;
+    }
   }
   const int slots = c->slots = choose_slots(c);
   build_gather(c, h, c->nodes);
@@ -1963,6 +1963,7 @@ aimx_status aimx_get_stats(const aimx_ctx* c, aimx_stats* o) {
   o->near_union = c->near_union;
   o->planar = c->planar ? 1 : 0;
   o->kop_grad = c->HsF && c->kgrad ? 1 : 0;
+  o->grid_channels = c->hot.nc;
   return AIMX_OK;
 }
 
@@ -2077,6 +2078,8 @@ static void build_kop(aimx_ctx* c) {
     c->HsF_T = c->HsF;
   }
   c->HF = dalloc<char>(c, ns * noct * (int64_t)cs);
+  if (c->hot.nc != 4 && !c->hot.S4)   // K's passes keep 4 channels (s x J has a z part)
+    c->hot.S4 = zalloc<char>(c, (int64_t)c->hot.nlines * c->hot.Nx * 4 * (int64_t)cs);
   const int64_t nP = c->hot.sP;   // one column, compact potentials (batch 1)
   c->kphi1 = zalloc<char>(c, nP * (int64_t)cs + 64);
   c->kphi2 = zalloc<char>(c, nP * (int64_t)cs + 64);

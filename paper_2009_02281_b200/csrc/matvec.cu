@@ -72,9 +72,11 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
     a2.x += __shfl_xor_sync(0xffffffffu, a2.x, o); a2.y += __shfl_xor_sync(0xffffffffu, a2.y, o);
     a3.x += __shfl_xor_sync(0xffffffffu, a3.x, o); a3.y += __shfl_xor_sync(0xffffffffu, a3.y, o);
   }
-  if (act && gl == 0) {
-    T2* dst = (T2*)h.S + b * h.sS + ((int64_t)h.node_line[q] * h.Nx + h.node_lin[q] % h.Nx) * 4;
-    dst[0] = a0; dst[1] = a1; dst[2] = a2; dst[3] = a3;
+  if (act && gl == 0) {   // nc = 3: the channels (x, y, rho) of a planar grid
+    T2* dst = (T2*)h.S + b * h.sS + ((int64_t)h.node_line[q] * h.Nx + h.node_lin[q] % h.Nx) * h.nc;
+    dst[0] = a0; dst[1] = a1;
+    if (h.nc == 4) { dst[2] = a2; dst[3] = a3; }
+    else dst[2] = a3;
   }
 }
 
@@ -170,13 +172,16 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev
         a[v][c].y += __shfl_xor_sync(0xffffffffu, a[v][c].y, o);
       }
   if (g == 0) {
-    const int64_t off = ((int64_t)h.node_line[q] * h.Nx + h.node_lin[q] % h.Nx) * 4;
+    const int nc = h.nc;
+    const int64_t off = ((int64_t)h.node_line[q] * h.Nx + h.node_lin[q] % h.Nx) * nc;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int b = b0 + v;
       if (b < B) {
         T2* dst = (T2*)h.S + b * h.sS + off;
-        dst[0] = a[v][0]; dst[1] = a[v][1]; dst[2] = a[v][2]; dst[3] = a[v][3];
+        dst[0] = a[v][0]; dst[1] = a[v][1];
+        if (nc == 4) { dst[2] = a[v][2]; dst[3] = a[v][3]; }
+        else dst[2] = a[v][3];
       }
     }
   }
@@ -243,22 +248,22 @@ __global__ void __launch_bounds__(256) k_xfwd(HotDev h) {
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
   pass_prologue<T, L, SMALL>(tw, xb, (const T2*)h.twx, line);
-  const int b = blockIdx.y;
-  const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
+  const int b = blockIdx.y, nc = h.nc;   // lines = (grid line r, channel c < nc), c fastest
+  const int gline = blockIdx.x * G::NL + line, r = gline / nc, c = gline - r * nc;
   const bool act = r < h.nlines;
   const int Nx = h.Nx;
-  const T2* __restrict__ in = (const T2*)h.S + b * h.sS + (int64_t)r * Nx * 4 + c;
+  const T2* __restrict__ in = (const T2*)h.S + b * h.sS + (int64_t)(act ? r : 0) * Nx * nc + c;
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {   // x < Nx = L/2  <=>  n2 < R2/2
     const int x = G::TL::in_index(t, i);
-    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * 4] : mk<T2>(0, 0);
+    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * nc] : mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
-  T2* __restrict__ out = (T2*)h.bufA + b * h.sA + (int64_t)h.line_id[r] * L * 4 + c;
+  T2* __restrict__ out = (T2*)h.bufA + b * h.sA + (int64_t)h.line_id[r] * L * nc + c;
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) out[TwoLevel<G::R2, G::R1>::in_index(t, i) * 4] = v[i];
+  for (int i = 0; i < G::E; ++i) out[TwoLevel<G::R2, G::R1>::in_index(t, i) * nc] = v[i];
 }
 
 // ---- x inverse: bufC[line_id][kx][c] -> phi[line][x < Nx][c]
@@ -271,11 +276,11 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
   pass_prologue<T, L, SMALL>(tw, xb, (const T2*)h.twx, line);
-  const int b = blockIdx.y;
-  const int r = blockIdx.x * (G::NL / 4) + (line >> 2), c = line & 3;
+  const int b = blockIdx.y, nc = h.nc;
+  const int gline = blockIdx.x * G::NL + line, r = gline / nc, c = gline - r * nc;
   const bool act = r < h.nlines;
   const int lid = act ? h.line_id[r] : 0;
-  const T2* __restrict__ in = (const T2*)h.bufC + b * h.sA + (int64_t)lid * L * 4 + c;
+  const T2* __restrict__ in = (const T2*)h.bufC + b * h.sA + (int64_t)lid * L * nc + c;
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * 4] : mk<T2>(0, 0);
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   if (!act) return;
   const int Nx = h.Nx;
   // phi layout [node][channel][slot] (slots = batch, complex)
-  const int64_t ns = (int64_t)h.batch * 4;   // node stride
+  const int64_t ns = (int64_t)h.batch * nc;   // node stride
   const int plid = h.phi_line ? (act ? h.phi_line[r] : 0) : lid;   // line of phi (global grid)
   T2* __restrict__ out = (T2*)h.phi + (int64_t)c * h.batch + b + (int64_t)plid * Nx * ns;
 #pragma unroll
@@ -299,10 +304,7 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
 // slot's point ([slot][line][x][c]), each write of phi 4 consecutive slots of
 // a channel ([node][c][slot]).  With the per-slot mapping of k_xinv every phi
 // write was a lone 8-byte piece of a sector (cfg5, 32 columns: 766 us, issue
-// 7%).  NCH = 3: the z channel is identically zero (a planar mesh in a z
-// plane: f_z = 0, so Lambda^z = 0 exactly; reading R12) and is never
-// transformed -- a quarter of the x passes' work.
-template <int NCH> __device__ __forceinline__ int xch(int i) { return NCH == 4 ? i : (i == 2 ? 3 : i); }
+// 7%).  NCH = the stored channels: 4, or 3 on a planar grid (h.nc).
 template <typename T, int L, int NCH = 4> struct XinvB {
   static constexpr int T_ = TwoLevel<Fac<L>::R1, Fac<L>::R2>::T;
   static constexpr int NL = 4 * NCH, NT = NL * T_;
@@ -322,17 +324,17 @@ __global__ void __launch_bounds__(XinvB<T, L, NCH>::NT, (sizeof(T) == 4 && NCH =
   T2* xb = tw + L + line * X::XB;
   for (int i = threadIdx.x; i < L; i += X::NT) tw[i] = ((const T2*)h.twx)[i];
   __syncthreads();
-  const int r = blockIdx.x, c = xch<NCH>(line % NCH), b = blockIdx.y * 4 + line / NCH;
+  const int r = blockIdx.x, c = line % NCH, b = blockIdx.y * 4 + line / NCH;
   const bool act = b < B;
   const int lid = h.line_id[r];
-  const T2* __restrict__ in = (const T2*)h.bufC + (int64_t)(act ? b : 0) * h.sA + (int64_t)lid * L * 4 + c;
+  const T2* __restrict__ in = (const T2*)h.bufC + (int64_t)(act ? b : 0) * h.sA + (int64_t)lid * L * NCH + c;
   T2 v[G::E];
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * 4] : mk<T2>(0, 0);
+  for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * NCH] : mk<T2>(0, 0);
   inv_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   const int Nx = h.Nx;
-  const int64_t ns = (int64_t)h.batch * 4;   // phi node stride (complex): [node][channel][slot]
+  const int64_t ns = (int64_t)h.batch * NCH;   // phi node stride (complex): [node][channel][slot]
   const int plid = h.phi_line ? h.phi_line[r] : lid;
   T2* __restrict__ out = (T2*)h.phi + (int64_t)c * h.batch + b + (int64_t)plid * Nx * ns;
 #pragma unroll
@@ -356,21 +358,21 @@ __global__ void __launch_bounds__(XinvB<T, L, NCH>::NT) k_xfwd_b(HotDev h, int B
   T2* xb = tw + L + line * X::XB;
   for (int i = threadIdx.x; i < L; i += X::NT) tw[i] = ((const T2*)h.twx)[i];
   __syncthreads();
-  const int r = blockIdx.x, c = xch<NCH>(line % NCH), b = blockIdx.y * 4 + line / NCH;
+  const int r = blockIdx.x, c = line % NCH, b = blockIdx.y * 4 + line / NCH;
   const bool act = b < B;
   const int Nx = h.Nx;
-  const T2* __restrict__ in = (const T2*)h.S + (int64_t)(act ? b : 0) * h.sS + (int64_t)r * Nx * 4 + c;
+  const T2* __restrict__ in = (const T2*)h.S + (int64_t)(act ? b : 0) * h.sS + (int64_t)r * Nx * NCH + c;
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) {   // x < Nx = L/2  <=>  n2 < R2/2
     const int x = G::TL::in_index(t, i);
-    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * 4] : mk<T2>(0, 0);
+    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * NCH] : mk<T2>(0, 0);
   }
   fwd_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
-  T2* __restrict__ out = (T2*)h.bufA + (int64_t)b * h.sA + (int64_t)h.line_id[r] * L * 4 + c;
+  T2* __restrict__ out = (T2*)h.bufA + (int64_t)b * h.sA + (int64_t)h.line_id[r] * L * NCH + c;
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) out[TwoLevel<G::R2, G::R1>::in_index(t, i) * 4] = v[i];
+  for (int i = 0; i < G::E; ++i) out[TwoLevel<G::R2, G::R1>::in_index(t, i) * NCH] = v[i];
 }
 
 // Column passes: CTA = NL lines = (rows per CTA) x (column tile CW).
@@ -736,25 +738,23 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
 // frequency (spectrum.cu, planar plan).  The CTA's slab of H_hat2 (the octant
 // rows ky <= N_y of its CW/4 kx, mirrored on read) is staged in shared memory
 // while the forward transform runs.
-// SKIPZ (h.zch): the z channel is identically zero; the CTA's column tile
-// enumerates only the active columns 4 kx + {0, 1, 3} (three quarters of the work)
-template <typename T, int L, bool SKIPZ = false>
+// Columns col = nc kx + c (h.nc = 3 on planar grids: channels x, y, rho).
+template <typename T, int L>
 __global__ void __launch_bounds__(256, 2) k_yconv_plane(HotDev h) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
-  const int W = h.W, Nx = h.Nx, Ny = h.Ny;
-  const int Wa = SKIPZ ? 3 * (W / 4) : W;            // active columns
-  const ColTile ct = col_tile<T, L>(line, Wa);
+  const int W = h.W, Nx = h.Nx, Ny = h.Ny, nc = h.nc;
+  const ColTile ct = col_tile<T, L>(line, W);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* tw = reinterpret_cast<T2*>(smem_raw);
   T2* xb = tw + L + line * G::XB;
   T2* hs = tw + L + (size_t)G::NL * G::XB;          // [ky <= Ny][kx - kx0]
-  const int ja = blockIdx.x * ct.CW;                 // first active column of the tile
-  const int kx0 = h.kx0 + (SKIPZ ? ja / 3 : ja / 4);
-  const int nkx = SKIPZ ? (ja + ct.CW - 1) / 3 - ja / 3 + 1 : ct.CW / 4;
+  const int ja = blockIdx.x * ct.CW;                 // first column of the tile
+  const int kx0 = h.kx0 + ja / nc;
+  const int nkx = (ja + ct.CW - 1) / nc - ja / nc + 1;
   const int b = blockIdx.z;
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
   for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = ((const T2*)h.twy_tab)[i];
@@ -766,9 +766,8 @@ __global__ void __launch_bounds__(256, 2) k_yconv_plane(HotDev h) {
   for (int y = threadIdx.x; y < Ny; y += blockDim.x) occ[y] = h.line_occ[(int64_t)h.zplane0 * Ny + y];
   __syncthreads();
   const bool act = ct.rsub == 0;   // one plane: the column tile's first row set only
-  const int jc = ja + ct.w;                          // active column -> grid column 4 kx + c
-  const int64_t col = SKIPZ ? 4 * (jc / 3) + xch<3>(jc % 3) : jc;
-  const int kxl = SKIPZ ? jc / 3 - ja / 3 : ct.w >> 2;
+  const int64_t col = ja + ct.w;
+  const int kxl = (ja + ct.w) / nc - ja / nc;
   // per-element offsets in 32 bits (one slot's plane: Ny W < 2^31)
   const T2* __restrict__ in = (const T2*)h.bufA + b * h.sA + col;
   // this thread's occupied rows as a bit mask (the loads and the stores use
@@ -1010,10 +1009,10 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
   const int c0 = cta_ptr[blockIdx.x], nch = cta_ptr[blockIdx.x + 1] - c0;
   if (nch <= 0) return;
   const int4* __restrict__ chunks = reinterpret_cast<const int4*>(h.chunks) + c0;
-  const int64_t ns = (int64_t)h.batch * 4;        // phi node stride (complex): [node][channel][slot]
+  const int nc = h.nc;                            // stored channels: 4, or 3 (x, y, rho) on planar grids
+  const int64_t ns = (int64_t)h.batch * nc;       // phi node stride (complex): [node][channel][slot]
   const T2* __restrict__ phi = (const T2*)h.phi + b0;
   const T2* __restrict__ xr = xt + b0;
-  const bool zch = (h.zch & 8) != 0;
   T be[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) be[v] = PARTS ? T(0) : (T)cb.beta[b0 + v];   // 0 for b >= B
@@ -1067,8 +1066,8 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
         if (e < d.w) {
           const T2* pr = phi + (int64_t)ix[e] * ns;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)   // zch: phi_z and Lambda^z are zero, its row is not gathered
-            if (c != 2 || !zch) buf[4 * i + c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
+          for (int c = 0; c < 4; ++c)   // nc = 3: phi_z is not stored (Lambda^z = 0), slot 2 holds rho
+            if (c < nc) buf[4 * i + c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
         }
       }
     }
@@ -1119,7 +1118,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
       const T4* __restrict__ wf = (const T4*)stg + e * R;
       T2 pv[4][V];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) unpack<T2, V>(buf[4 * i + c], pv[c]);
+      for (int c = 0; c < 4; ++c) unpack<T2, V>(buf[4 * i + (c == 3 && nc == 3 ? 2 : c)], pv[c]);   // rho
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const T4 w = wf[r];
@@ -1128,7 +1127,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
           T2& a = acc[r * V + v];
           axpy(a, w.x, pv[0][v]);
           axpy(a, w.y, pv[1][v]);
-          if (!zch) axpy(a, w.z, pv[2][v]);
+          if (nc == 4) axpy(a, w.z, pv[2][v]);
           if constexpr (PARTS) axpy(acc[(R + r) * V + v], w.w, pv[3][v]);
           else axpy(a, -be[v] * w.w, pv[3][v]);
         }
@@ -1216,8 +1215,8 @@ void run_gather(const HotDev& h, const void* x, int64_t xstride, int B, cudaStre
 template <typename T, int L, bool SMALL>
 void run_x_geom(const HotDev& h, bool inv, int B, cudaStream_t s) {
   constexpr size_t sm = pass_smem<T, L, SMALL>();
-  constexpr int RPC = PassGeom<T, L, SMALL>::NL / 4;
-  dim3 g((unsigned)((h.nlines + RPC - 1) / RPC), (unsigned)B);
+  constexpr int NL = PassGeom<T, L, SMALL>::NL;
+  dim3 g((unsigned)(((int64_t)h.nlines * h.nc + NL - 1) / NL), (unsigned)B);
   if (!inv) {
     set_smem(k_xfwd<T, L, SMALL>, sm);
     launch_pdl(k_xfwd<T, L, SMALL>, g, dim3(PassGeom<T, L, SMALL>::NT), sm, s, h);
@@ -1246,14 +1245,13 @@ void run_x_b(const HotDev& h, bool inv, int B, cudaStream_t s) {
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   if (h.nlines <= 0) return;
-  const int zbit = inv ? 1 : 2;
-  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || (h.zch & zbit))) {
-    if (h.zch & zbit) run_x_b<T, L, 3>(h, inv, B, s);
+  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || h.nc == 3)) {
+    if (h.nc == 3) run_x_b<T, L, 3>(h, inv, B, s);
     else run_x_b<T, L, 4>(h, inv, B, s);
     return;
   }
-  constexpr int RPC = PassGeom<T, L>::NL / 4;
-  if ((int64_t)(h.nlines + RPC - 1) / RPC * B < 2 * 148) run_x_geom<T, L, true>(h, inv, B, s);
+  constexpr int NL = PassGeom<T, L>::NL;
+  if (((int64_t)h.nlines * h.nc + NL - 1) / NL * B < 2 * 148) run_x_geom<T, L, true>(h, inv, B, s);
   else run_x_geom<T, L, false>(h, inv, B, s);
 }
 
@@ -1470,16 +1468,11 @@ void run_interp(const HotDev& h, const void* x, void* y0, void* y1, const Combin
 }
 
 template <typename T, int L> void run_yconv_plane(const HotDev& h, int B, cudaStream_t s) {
-  // the slab: kx of the tile's columns (SKIPZ: CW/3 + 2 at most), + the occupied-row flags
+  // the slab: kx of the tile's columns (CW/3 + 2 at most), + the occupied-row flags
   constexpr size_t sm = pass_smem<T, L>() + sizeof(typename CT<T>::T2) * (size_t)(L / 2 + 1) * (PassGeom<T, L>::NL / 3 + 2)
                         + L / 2;
-  if (h.zch & 4) {
-    set_smem(k_yconv_plane<T, L, true>, sm);
-    launch_pdl(k_yconv_plane<T, L, true>, col_grid<T, L>(3 * (h.W / 4), 1, B), dim3(PassGeom<T, L>::NT), sm, s, h);
-  } else {
-    set_smem(k_yconv_plane<T, L>, sm);
-    launch_pdl(k_yconv_plane<T, L>, col_grid<T, L>(h.W, 1, B), dim3(PassGeom<T, L>::NT), sm, s, h);
-  }
+  set_smem(k_yconv_plane<T, L>, sm);
+  launch_pdl(k_yconv_plane<T, L>, col_grid<T, L>(h.W, 1, B), dim3(PassGeom<T, L>::NT), sm, s, h);
   AIMX_CHECK_LAUNCH();
 }
 
@@ -1658,7 +1651,11 @@ void hot_kop(const HotDev& h0, const void* x, void* y, const void* HF, void* phi
   HotDev h = h0;
   h.Hoct = const_cast<void*>(HF);
   h.batch = 1;   // one column: compact potentials ([node][channel])
-  h.zch = 0;     // s x J has a z component on planar meshes
+  if (h.nc != 4) {   // s x J has a z component on planar meshes: K keeps 4 channels, its own S
+    h.nc = 4;
+    h.W = 8 * h.Nx;
+    h.S = h.S4;
+  }
   const int Lx = 2 * h.Nx;
   run_gather<T>(h, x, h.nb, 1, s);   // S = P x (one column)
   auto conv = [&](void* phi) {

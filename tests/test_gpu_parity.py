@@ -418,9 +418,9 @@ def test_calls_on_several_streams_are_ordered():
 
 
 def test_planar_z_channel_skip_is_exact(monkeypatch):
-    """A planar mesh (z = 0) has Lambda^z = 0 exactly, so the batched x passes
-    and the planar y pass skip the z channel (three of four channels
-    transformed); the results equal the four-channel run bit for bit."""
+    """A planar mesh (z = 0) has Lambda^z = 0 exactly, so the grid passes
+    store and transform three channels (x, y, rho); the results equal the
+    four-channel run (AIMX_NO_ZSKIP=1) bit for bit, single-column and sweep."""
     import torch
     m = inp.patch_array_mesh(2, 2, 30e-3, 40e-3, 50e-3, 12, 16)
     n = (64, 64, 4)
@@ -430,8 +430,11 @@ def test_planar_z_channel_skip_is_exact(monkeypatch):
         if not skip:
             monkeypatch.setenv("AIMX_NO_ZSKIP", "1")
         op = make_gpu_op(m, n, "c64")
-        assert op.stats()["planar"]
+        assert op.stats()["planar"] and op.stats()["grid_channels"] == (3 if skip else 4)
         X = to_gpu(np.stack([inp.rhs_vector(5, 400 + i, op.N) for i in range(8)]), "c64")
-        outs.append(op.sweep(freqs, X).clone())
+        Y = op.sweep(freqs, X).clone()
+        op.set_frequency(freqs[3])
+        outs.append((Y, op.matvec(X[3].contiguous()).clone()) + tuple(t.clone() for t in op.matvec_parts(X[3].contiguous())))
         op.close()
-    assert torch.equal(outs[0], outs[1])
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
