@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   const T2* __restrict__ in = (const T2*)h.bufC + b * h.sA + (int64_t)lid * L * nc + c;
   T2 v[G::E];
 #pragma unroll
-  for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * 4] : mk<T2>(0, 0);
+  for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * nc] : mk<T2>(0, 0);
   inv_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   const int Nx = h.Nx;

@@ -246,3 +246,30 @@ def test_cfg4_pmchwt_fullsize_c64():
         yE, yH = pmchwt_rows(orc, kr, f, 4.0, gpu_input_as_c128(x, "c64"))
         assert rel_l2(y[rows], yE) <= TOL["c64"]
         assert rel_l2(y[op.N + rows], yH) <= TOL["c64"]
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_K_on_planar_grid_vs_oracle(prec):
+    """K on a planar mesh (cfg1's plate): the EFIE passes of the context store
+    3 channels (Lambda^z = 0), K's radial passes 4 (s x J has a z part) in their
+    own buffers; K and then the EFIE matvec against the oracle."""
+    from oracle.aimx import AIMxOracle
+    from oracle.kop import AIMxK
+    from tests._parity import TOL, gpu_input_as_c128, to_gpu
+    m = inp.make_mesh(1)
+    n = (16, 16, 4)
+    orc = AIMxOracle(m.vertices, m.triangles, n)
+    ak = AIMxK(orc)
+    op = make_gpu_op(m, n, prec)
+    op.set_kop(True)
+    st = op.stats()
+    assert st["planar"] and st["grid_channels"] == 3 and not st["kop_grad"]
+    x = np.random.default_rng(31).standard_normal(op.N) * (1 - 0.2j)
+    f = 150e6
+    op.set_frequency(f)
+    orc.set_frequency(f)
+    xo = gpu_input_as_c128(x, prec)
+    y = op.matvec_kop(to_gpu(x, prec)).cpu().numpy()
+    assert rel_l2(y, ak.matvec(xo, 2 * np.pi * f / 299792458.0)) <= TOL[prec]
+    z = op.matvec(to_gpu(x, prec)).cpu().numpy()
+    assert rel_l2(z, orc.matvec(xo)) <= TOL[prec]
