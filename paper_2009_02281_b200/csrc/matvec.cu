@@ -27,6 +27,7 @@
 // Pruning (exact, reading R12): lines/planes with no occupied node are never
 // transformed; their data are identically zero and are never read as input.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "aimx_internal.h"
@@ -1245,7 +1246,8 @@ void run_x_b(const HotDev& h, bool inv, int B, cudaStream_t s) {
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   if (h.nlines <= 0) return;
-  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || h.nc == 3)) {
+  static const bool fwd_b = !std::getenv("AIMX_NO_XFWD_B");   // experiments
+  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || (h.nc == 3 && fwd_b))) {
     if (h.nc == 3) run_x_b<T, L, 3>(h, inv, B, s);
     else run_x_b<T, L, 4>(h, inv, B, s);
     return;
