@@ -135,7 +135,7 @@ void build_near_chunks(const NearGroups& g, int chw, int chc, int cs, NearChunks
                        const std::vector<int64_t>& order);
 // the S4+S5 kernel's group order for `ncta` CTAs: CTA k's groups are
 // order[cta_begin[k] .. cta_begin[k+1]) (k, k + ncta, k + 2 ncta, ...)
-std::vector<int64_t> near_round_order(int64_t ngrp, int ncta, std::vector<int64_t>& cta_begin, int nsm = 0);
+std::vector<int64_t> near_round_order(int64_t ngrp, int ncta, std::vector<int64_t>& cta_begin);
 
 // ---------------------------------------------------------------- device setup (fp64)
 struct SetupDev {

@@ -425,8 +425,7 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   int nsm_near = nsm;
   if (const char* e = std::getenv("AIMX_NEAR_SMS")) nsm_near = std::max(1, std::min(nsm, std::atoi(e)));
   const int ncta = near_ctas_per_sm(f32, false, grp.R) * nsm_near;
-  const std::vector<int64_t> order =
-      near_round_order(grp.ngrp, ncta, cta_begin, std::getenv("AIMX_NEAR_SMGROUP") ? nsm_near : 0);
+  const std::vector<int64_t> order = near_round_order(grp.ngrp, ncta, cta_begin);
   build_near_chunks(grp, near_chw(f32, c->slots), near_chc(f32, c->slots), cs, ck, order);
   // value slot (u R + r) -> payload byte offset
   for (auto& v : grp.slot)

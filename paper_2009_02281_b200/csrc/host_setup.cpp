@@ -541,7 +541,7 @@ void build_near_chunks(const NearGroups& ng, int chw, int chc, int cs, NearChunk
   for (int64_t c = 0; c < nchunk; ++c) ck.chunks[4 * c + 2] = (int32_t)(poff[c] / 16);
 }
 
-std::vector<int64_t> near_round_order(int64_t ngrp, int ncta, std::vector<int64_t>& cta_begin, int nsm) {
+std::vector<int64_t> near_round_order(int64_t ngrp, int ncta, std::vector<int64_t>& cta_begin) {
   // Groups are spatially ordered (anchor Morton code or linear index), so a
   // run of consecutive groups shares most of its stencil nodes and near
   // columns.  Round r = groups [r ncta, (r + 1) ncta); CTA k takes the k-th
@@ -554,14 +554,9 @@ std::vector<int64_t> near_round_order(int64_t ngrp, int ncta, std::vector<int64_
   std::vector<int64_t> order;
   order.reserve(ngrp);
   cta_begin.assign(ncta + 1, 0);
-  // nsm > 0: the CTAs co-resident on one SM (blocks s, s + nsm, s + 2 nsm, ...
-  // under the usual round-robin dispatch) take consecutive groups of a round,
-  // so the rows they share can also hit in that SM's L1
-  const int per = nsm > 0 ? std::max(1, ncta / nsm) : 1;
   for (int k = 0; k < ncta; ++k) {
     cta_begin[k] = (int64_t)order.size();
-    const int slot = nsm > 0 && ncta % nsm == 0 ? (k % nsm) * per + k / nsm : k;
-    for (int64_t g = slot; g < ngrp; g += ncta) order.push_back(g);
+    for (int64_t g = k; g < ngrp; g += ncta) order.push_back(g);
   }
   cta_begin[ncta] = ngrp;
   return order;

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(256) k_xinv(HotDev h) {
   }
 }
 
-// ---- x passes, batched (B >= 4): the CTA's lines are the NCH channels x 4
+// ---- x inverse, batched (B >= 4): the CTA's lines are the NCH channels x 4
 // consecutive slots of one grid line, so both sides move whole 32-byte
 // sectors: each read or write of the grid rows covers the channels of a
 // slot's point ([slot][line][x][c]), each write of phi 4 consecutive slots of
@@ -343,37 +343,6 @@ __global__ void __launch_bounds__(XinvB<T, L, NCH>::NT, (sizeof(T) == 4 && NCH =
     const int x = TwoLevel<G::R2, G::R1>::in_index(t, i);
     if (i % G::R1 < (G::R1 + 1) / 2 && x < Nx) out[x * ns] = v[i];
   }
-}
-
-// x forward, batched: occupied lines of S (x < Nx, zero padded) -> bufA[slot][line_id][kx][c]
-template <typename T, int L, int NCH>
-__global__ void __launch_bounds__(XinvB<T, L, NCH>::NT) k_xfwd_b(HotDev h, int B) {
-  pdl_wait();
-  pdl_trigger();
-  using T2 = typename CT<T>::T2;
-  using G = PassGeom<T, L>;
-  using X = XinvB<T, L, NCH>;
-  const int line = threadIdx.x % X::NL, t = threadIdx.x / X::NL;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* tw = reinterpret_cast<T2*>(smem_raw);
-  T2* xb = tw + L + line * X::XB;
-  for (int i = threadIdx.x; i < L; i += X::NT) tw[i] = ((const T2*)h.twx)[i];
-  __syncthreads();
-  const int r = blockIdx.x, c = line % NCH, b = blockIdx.y * 4 + line / NCH;
-  const bool act = b < B;
-  const int Nx = h.Nx;
-  const T2* __restrict__ in = (const T2*)h.S + (int64_t)(act ? b : 0) * h.sS + (int64_t)r * Nx * NCH + c;
-  T2 v[G::E];
-#pragma unroll
-  for (int i = 0; i < G::E; ++i) {   // x < Nx = L/2  <=>  n2 < R2/2
-    const int x = G::TL::in_index(t, i);
-    v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * NCH] : mk<T2>(0, 0);
-  }
-  fwd_fft<T2, L>(v, xb, tw, t);
-  if (!act) return;
-  T2* __restrict__ out = (T2*)h.bufA + (int64_t)b * h.sA + (int64_t)h.line_id[r] * L * NCH + c;
-#pragma unroll
-  for (int i = 0; i < G::E; ++i) out[TwoLevel<G::R2, G::R1>::in_index(t, i) * NCH] = v[i];
 }
 
 // Column passes: CTA = NL lines = (rows per CTA) x (column tile CW).
@@ -1228,16 +1197,10 @@ void run_x_geom(const HotDev& h, bool inv, int B, cudaStream_t s) {
   AIMX_CHECK_LAUNCH();
 }
 template <typename T, int L, int NCH>
-void run_x_b(const HotDev& h, bool inv, int B, cudaStream_t s) {
+void run_x_b(const HotDev& h, int B, cudaStream_t s) {
   using X = XinvB<T, L, NCH>;
-  const dim3 g((unsigned)h.nlines, (unsigned)((B + 3) / 4));
-  if (inv) {
-    set_smem(k_xinv_b<T, L, NCH>, X::SMEM);
-    launch_pdl(k_xinv_b<T, L, NCH>, g, dim3(X::NT), X::SMEM, s, h, B);
-  } else {
-    set_smem(k_xfwd_b<T, L, NCH>, X::SMEM);
-    launch_pdl(k_xfwd_b<T, L, NCH>, g, dim3(X::NT), X::SMEM, s, h, B);
-  }
+  set_smem(k_xinv_b<T, L, NCH>, X::SMEM);
+  launch_pdl(k_xinv_b<T, L, NCH>, dim3((unsigned)h.nlines, (unsigned)((B + 3) / 4)), dim3(X::NT), X::SMEM, s, h, B);
   AIMX_CHECK_LAUNCH();
 }
 
@@ -1246,10 +1209,12 @@ void run_x_b(const HotDev& h, bool inv, int B, cudaStream_t s) {
 template <typename T, int L>
 void run_x(const HotDev& h, bool inv, int B, cudaStream_t s) {
   if (h.nlines <= 0) return;
-  static const bool fwd_b = !std::getenv("AIMX_NO_XFWD_B");   // experiments
-  if (B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024 && (inv || (h.nc == 3 && fwd_b))) {
-    if (h.nc == 3) run_x_b<T, L, 3>(h, inv, B, s);
-    else run_x_b<T, L, 4>(h, inv, B, s);
+  // batched inverse: 4 slots per CTA (the forward pass's per-slot CTAs already
+  // read and write whole runs of channels; a batched forward measured slower:
+  // cfg5 188 against 159 us)
+  if (inv && B >= 4 && L >= 64 && h.batch % 4 == 0 && XinvB<T, L>::SMEM <= 220 * 1024) {
+    if (h.nc == 3) run_x_b<T, L, 3>(h, B, s);
+    else run_x_b<T, L, 4>(h, B, s);
     return;
   }
   constexpr int NL = PassGeom<T, L>::NL;
@@ -1337,17 +1302,27 @@ void run_z(const HotDev& h, int B, cudaStream_t s) {
   AIMX_CHECK_LAUNCH();
 }
 
-// xt[n * BB + b] = x[b * xstride + n] (zero for b >= B)
+// xt[n * BB + b] = x[b * xstride + n] (zero for b >= B): a transpose through a
+// shared-memory tile of kIlN rows, so both the column reads (kIlN consecutive
+// n of a column) and the interleaved writes (kIlN * BB contiguous) coalesce
+constexpr int kIlN = 64;
 template <typename T>
-__global__ void k_interleave(int nb, int B, int BB, const typename CT<T>::T2* __restrict__ x,
-                             int64_t xstride, typename CT<T>::T2* __restrict__ xt) {
+__global__ void __launch_bounds__(256) k_interleave(int nb, int B, int BB, const typename CT<T>::T2* __restrict__ x,
+                                                    int64_t xstride, typename CT<T>::T2* __restrict__ xt) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename CT<T>::T2;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nb * BB) return;
-  const int n = (int)(i / BB), b = (int)(i - (int64_t)n * BB);
-  xt[i] = b < B ? x[b * xstride + n] : mk<T2>(0, 0);
+  __shared__ T2 tile[kMaxBatch][kIlN + 1];
+  const int n0 = blockIdx.x * kIlN;
+  for (int idx = threadIdx.x; idx < BB * kIlN; idx += blockDim.x) {
+    const int b = idx / kIlN, j = idx - b * kIlN;
+    tile[b][j] = (b < B && n0 + j < nb) ? x[b * xstride + n0 + j] : mk<T2>(0, 0);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < BB * kIlN; idx += blockDim.x) {
+    const int j = idx / BB, b = idx - j * BB;
+    if (n0 + j < nb) xt[(int64_t)(n0 + j) * BB + b] = tile[b][j];
+  }
 }
 
 template <int BB> constexpr int bucket_ok() { return BB; }
@@ -1357,9 +1332,8 @@ template <typename T>
 void run_interleave(const HotDev& h, const void* x, const Combine& c, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   const int BB = batch_bucket(c.B);
-  const int64_t n = (int64_t)h.nb * BB;
-  launch_pdl(k_interleave<T>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, h.nb, c.B, BB, (const T2*)x, c.xstride,
-                                                              (T2*)h.xt);
+  launch_pdl(k_interleave<T>, dim3((unsigned)((h.nb + kIlN - 1) / kIlN)), dim3(256), 0, s, h.nb, c.B, BB, (const T2*)x,
+             c.xstride, (T2*)h.xt);
   AIMX_CHECK_LAUNCH();
 }
 

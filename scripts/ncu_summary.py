@@ -25,7 +25,7 @@ def short(name):
     return name[:70]
 
 
-SETUP = ("k_static_near", "k_precorrect", "k_weights", "k_rwg_sides", "k_lam_to", "k_pack_c", "k_ent_w",
+SETUP = ("k_chan_nonzero", "k_take", "k_static_near", "k_precorrect", "k_weights", "k_rwg_sides", "k_lam_to", "k_pack_c", "k_ent_w",
          "k_aim_fill", "k_lin_entries", "k_sample_static", "k_d2f", "k_self", "k_diag")
 
 
