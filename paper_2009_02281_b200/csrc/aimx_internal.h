@@ -207,17 +207,12 @@ void launch_lin_entries(const Topology& t, const SetupDev& d, const int32_t* col
 constexpr int kMaxBatch = 32;
 
 // CTAs per SM of the S4+S5 kernel (its register budget, __launch_bounds__)
-// (bb: the kernel's column bucket; 16 and 32 columns keep two register
-// buffers of gathered rows for the software pipeline: 4 CTAs per SM in fp32)
-constexpr int near_ctas_per_sm(bool f32, bool single, int R = 8, int bb = 1) {
-  return R >= 16 ? 3 : (f32 ? (bb >= 16 ? 4 : 5) : 4);
-}
+constexpr int near_ctas_per_sm(bool f32, bool single, int R = 8) { return R >= 16 ? 3 : (f32 ? 5 : 4); }
 // S4+S5 chunk lengths (entries) in the payload: C chunks 1024 / s, W chunks
-// 256 / s, divided by 2 (16 slots) or 4 (32 slots): the wide kernels keep two
-// register buffers of gathered rows (software pipeline) in the same registers
-constexpr int near_chunk_div(int cols) { return cols >= 32 ? 4 : (cols >= 16 ? 2 : 1); }
-constexpr int near_chc(bool f32, int slots) { return (f32 ? 128 : 64) / near_chunk_div(slots); }
-constexpr int near_chw(bool f32, int slots) { return (f32 ? 32 : 16) / near_chunk_div(slots); }
+// 256 / s, halved when the context holds 32 batch slots (the 32-column kernel
+// keeps the same registers per lane)
+constexpr int near_chc(bool f32, int slots) { return (f32 ? 128 : 64) / (slots >= 32 ? 2 : 1); }
+constexpr int near_chw(bool f32, int slots) { return (f32 ? 32 : 16) / (slots >= 32 ? 2 : 1); }
 
 // ---------------------------------------------------------------- spectrum
 // Octant layout (all spectra): index ((ky (N_z+1) + kz) (N_x+1) + kx), x fastest.

@@ -424,8 +424,7 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   // one wave of resident CTAs (AIMX_NEAR_SMS: spread over fewer SMs, experiments)
   int nsm_near = nsm;
   if (const char* e = std::getenv("AIMX_NEAR_SMS")) nsm_near = std::max(1, std::min(nsm, std::atoi(e)));
-  // the widest column bucket the context launches (its slots) sets the CTAs per SM
-  const int ncta = near_ctas_per_sm(f32, false, grp.R, c->slots) * nsm_near;
+  const int ncta = near_ctas_per_sm(f32, false, grp.R) * nsm_near;
   const std::vector<int64_t> order = near_round_order(grp.ngrp, ncta, cta_begin);
   build_near_chunks(grp, near_chw(f32, c->slots), near_chc(f32, c->slots), cs, ck, order);
   // value slot (u R + r) -> payload byte offset

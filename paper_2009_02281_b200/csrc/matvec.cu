@@ -921,12 +921,12 @@ template <typename T, int R, int BB, bool PARTS> struct NearCfg {
   using T2 = typename CT<T>::T2;
   static constexpr int NT = 128;                      // threads per CTA
   static constexpr int S = (int)sizeof(T2);           // complex bytes
-  // entries per C / W chunk (at most; near_chc / near_chw of the context's slots <= BB)
-  static constexpr int CHC = 1024 / S / near_chunk_div(BB), CHW = 256 / S / near_chunk_div(BB);
+  // entries per C / W chunk (at most; near_chc / near_chw, halved for 32 columns)
+  static constexpr int CHC = (BB >= 32 ? 512 : 1024) / S, CHW = (BB >= 32 ? 128 : 256) / S;
   static constexpr int COEFB = CHC * R * S;           // coefficient bytes (C: R pairs; W: R real4 = 2 S per entry)
   static constexpr int STB = COEFB + CHC * 4 + 16;    // stage: one chunk payload (NearChunks)
   static constexpr int D = kNearD;                    // pipeline depth (chunks)
-  static constexpr int NDS = D + 2, NDD = D + 2;      // stage / descriptor slots (software pipeline)
+  static constexpr int NDS = D + 1, NDD = D + 1;      // stage / descriptor slots
   static constexpr int V = (S == 8 && BB >= 2) ? 2 : 1;
   static constexpr int LG = BB / V, NG = 32 / LG, NLG = (NT / 32) * NG;
   static constexpr int NPC = (CHC + NLG - 1) / NLG;   // C entries per lane group per chunk
@@ -956,7 +956,7 @@ __device__ __forceinline__ void unpack(const typename VecT<T2, V>::type& u, T2* 
 }
 
 template <typename T, int R, int BB, bool PARTS>
-__global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1, R, BB))
+__global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1, R))
     k_interp_near(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      typename CT<T>::T2* __restrict__ y0,
                                                      typename CT<T>::T2* __restrict__ y1, Combine cb) {
@@ -1012,18 +1012,12 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
     for (int j = 0; j < D && j < nch; ++j) issue(j, chunks[j]);
   __syncthreads();
 
-  // Software pipeline: the gathered rows of chunk k + 1 (x rows or potential
-  // rows, from L2) are loaded into the second register buffer while chunk k
-  // is computed, so the L2 latency overlaps the arithmetic.  Stages: chunk k
-  // (computing), k + 1 (its indices read), k + 2 .. k + D (in flight): NDS =
-  // D + 2 (the bulk copy of chunk k + 1 + D refills chunk k - 1's stage).
-  VT buf2[2 * K::NBUF];   // two register buffers: [0, NBUF) and [NBUF, 2 NBUF) (compile-time offsets)
-  auto fetch = [&](auto OFF, int k, int4& d, const unsigned char*& stg) {
-    VT* buf = buf2 + decltype(OFF)::value;
+  VT buf[K::NBUF];
+  for (int k = 0; k < nch; ++k) {
     // chunk k's payload (with the descriptor of chunk k + D) has landed
     mbar_wait(bar + k % K::NDS, (uint32_t)(k / K::NDS) & 1u);
-    d = sdesc[k % K::NDD];
-    stg = sdata + (k % K::NDS) * K::STB;
+    const int4 d = sdesc[k % K::NDD];
+    const unsigned char* stg = sdata + (k % K::NDS) * K::STB;
     const int* ix = reinterpret_cast<const int*>(stg + coef_bytes(d));
     if (tid == 0 && k + D < nch)
       issue(k + D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
@@ -1047,9 +1041,6 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
         }
       }
     }
-  };
-  auto compute = [&](auto OFF, const int4& d, const unsigned char* stg) {
-    const VT* buf = buf2 + decltype(OFF)::value;
     if (d.y & 1) {   // near correction: pairs [e][R]
       const T2* __restrict__ cf = (const T2*)stg;
 #pragma unroll
@@ -1167,20 +1158,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
         }
       }
     }
-  };
-  using O0 = std::integral_constant<int, 0>;
-  using O1 = std::integral_constant<int, K::NBUF>;
-  int4 da, db;
-  const unsigned char *sa, *sb;
-  fetch(O0{}, 0, da, sa);
-  for (int k = 0; k < nch; k += 2) {
-    if (k + 1 < nch) fetch(O1{}, k + 1, db, sb);
-    compute(O0{}, da, sa);
     __syncthreads();   // stage and descriptor slots of chunk k are refilled next
-    if (k + 1 >= nch) break;
-    if (k + 2 < nch) fetch(O0{}, k + 2, da, sa);
-    compute(O1{}, db, sb);
-    __syncthreads();
   }
 }
 
