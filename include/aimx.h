@@ -249,6 +249,13 @@ aimx_status aimx_solve(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void
 aimx_status aimx_sweep_host(aimx_ctx* ctx, int64_t nf, const double* f_hz, const void* X,
                             void* Y, int32_t batch, void* stream);
 
+/* Per-frequency status of a sweep's (or a solve's) result: status[i] (HOST,
+ * int32[nf]) = 0 when every element of Y[i,:] is finite, 1 when Y[i,:] holds a
+ * NaN or an infinity (e.g. a frequency whose inputs overflowed).  Y: device
+ * [nf][N_b] as written by aimx_sweep / aimx_solve; one device pass over Y on
+ * `stream`, then a host synchronisation of `stream`. */
+aimx_status aimx_sweep_status(aimx_ctx* ctx, int64_t nf, const void* Y, int32_t* status, void* stream);
+
 /* ---- introspection (parity tests; all host buffers, caller-allocated) ---- */
 int64_t aimx_num_unknowns(const aimx_ctx* ctx);
 aimx_status aimx_get_stats(const aimx_ctx* ctx, aimx_stats* out);

@@ -94,6 +94,7 @@ ABI_FUNCTIONS = {
                                   C.c_int32, _P, _P, C.POINTER(_P)]),
     "aimx_nccl_unique_id": (C.c_int, [_P]),
     "aimx_sync": (C.c_int, [_P, C.c_double]),
+    "aimx_sweep_status": (C.c_int, [_P, C.c_int64, _P, _P, _P]),
     "aimx_save_static": (C.c_int, [_P, C.c_char_p]),
     "aimx_solve": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double), _P, _P, C.c_double, C.c_int32, C.c_int32,
                              C.POINTER(C.c_int32), C.POINTER(C.c_double), _P]),
@@ -363,6 +364,15 @@ class AIMx:
                                              its.ctypes.data_as(C.POINTER(C.c_int32)),
                                              rr.ctypes.data_as(C.POINTER(C.c_double)), self._s(stream)), self.ctx)
         return X, its, rr
+
+    def sweep_status(self, Y, stream=None):
+        """Per-frequency status of a sweep / solve result Y [nf, N] (device):
+        0 = all finite, 1 = a NaN or infinity (aimx_sweep_status)."""
+        nf = int(Y.shape[0])
+        st = np.zeros(nf, dtype=np.int32)
+        _check(self.lib, self.lib.aimx_sweep_status(self.ctx, nf, self._vec(Y, (nf, self.N)),
+                                                    _P(st.ctypes.data), self._s(stream)), self.ctx)
+        return st
 
     def sweep_host(self, freqs, X, Y, batch: int = 0, stream=None):
         """X, Y: host (CPU) torch tensors [nf, N] (pinned for best speed)."""

@@ -200,6 +200,14 @@ __global__ void k_d2f(int64_t n, const double2* __restrict__ a, float2* __restri
 
 unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+// flag[i] = 1 if column i of Y ([nf][n] complex, as reals) holds a non-finite value
+template <typename R>
+__global__ void k_nonfinite(int64_t n2, int64_t nf, const R* __restrict__ Y, int32_t* flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n2 * nf) return;
+  if (!isfinite(Y[i])) flag[i / n2] = 1;   // benign race: every writer stores 1
+}
+
 // flag = 1 if any weight of channel c is non-zero (lam [n][4], fp64)
 __global__ void k_chan_nonzero(int64_t n, const double* __restrict__ lam, int c, int* flag) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1557,6 +1565,29 @@ aimx_status aimx_solve(aimx_ctx* c, int64_t nf, const double* f_hz, const void* 
   if (had) bind_frequency(c, f0, s);
   else c->freq_set = false;
   leave_stream(c, s, true);
+  AIMX_API_END(c)
+}
+
+aimx_status aimx_sweep_status(aimx_ctx* c, int64_t nf, const void* Y, int32_t* status, void* stream) {
+  if (!c) return AIMX_E_INVALID_ARG;
+  AIMX_API_BEGIN
+  if (nf < 0 || (nf > 0 && (!Y || !status))) throw Error(AIMX_E_INVALID_ARG, "bad status arguments");
+  if (nf == 0) return AIMX_OK;
+  AIMX_CUDA(cudaSetDevice(c->device));
+  check_sticky(c);
+  cudaStream_t s = pick(c, stream);
+  int32_t* flag = nullptr;
+  AIMX_CUDA(cudaMallocAsync((void**)&flag, nf * sizeof(int32_t), s));
+  AIMX_CUDA(cudaMemsetAsync(flag, 0, nf * sizeof(int32_t), s));
+  const int64_t n2 = 2 * c->topo.nb;
+  if (c->prec == AIMX_C64)
+    k_nonfinite<float><<<nblk(n2 * nf), 256, 0, s>>>(n2, nf, (const float*)Y, flag);
+  else
+    k_nonfinite<double><<<nblk(n2 * nf), 256, 0, s>>>(n2, nf, (const double*)Y, flag);
+  AIMX_CHECK_LAUNCH();
+  AIMX_CUDA(cudaMemcpyAsync(status, flag, nf * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  AIMX_CUDA(cudaFreeAsync(flag, s));
+  AIMX_CUDA(cudaStreamSynchronize(s));
   AIMX_API_END(c)
 }
 

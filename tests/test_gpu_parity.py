@@ -438,3 +438,16 @@ def test_planar_z_channel_skip_is_exact(monkeypatch):
         op.close()
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+
+
+def test_sweep_status_flags_nonfinite_columns():
+    """aimx_sweep_status: 0 for finite sweep outputs, 1 for a column with a NaN."""
+    import torch
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), "c64")
+    X = to_gpu(np.stack([inp.rhs_vector(1, 500 + i, op.N) for i in range(4)]), "c64")
+    Y = op.sweep([1e8, 2e8, 3e8, 4e8], X)
+    assert np.array_equal(op.sweep_status(Y), [0, 0, 0, 0])
+    X[2, 5] = float("nan")
+    Y = op.sweep([1e8, 2e8, 3e8, 4e8], X)
+    assert np.array_equal(op.sweep_status(Y), [0, 0, 1, 0])
+    assert torch.isfinite(torch.view_as_real(Y[[0, 1, 3]])).all()
