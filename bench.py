@@ -635,8 +635,8 @@ def run_secondary(cfg: int, prec: str, a, flush, barrier) -> dict:
                          "reps": m["sustained_reps"], "seconds": m["sustained_ms"] / 1e3},
            "fft_stage_hbm": {"bytes": fft_bytes, "ms": fft_ms,
                              "frac": fft_bytes / (fft_ms * 1e-3) / 1e9 / measured_peaks()[0],
-                             "note": "y/z/x-inverse passes (the x forward pass is fused with the S2 gather "
-                                     "in proj_xfft); profiled step"}}
+                             "note": "y/z/x-inverse passes (the x forward pass is timed with the S2 gather "
+                                     "as proj_xfft); profiled step"}}
     op.close()
     del X, Y
     torch.cuda.empty_cache()
