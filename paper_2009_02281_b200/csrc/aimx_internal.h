@@ -311,6 +311,8 @@ struct HotDev {
   int nc = 4;                    // channels stored in S / bufA / bufC / phi: 4 (x, y, z, rho), or 3
                                  // (x, y, rho) on planar grids, where Lambda^z = 0 exactly (R12)
   void* S4 = nullptr;            // nc = 3: a 4-channel S for the double-layer operator's passes
+  cudaEvent_t spec_ready = nullptr;   // HOST handle: the launch stream waits on it before the
+                                      // spectrum multiply (sweep pipeline), or null
   uint8_t* line_occ = nullptr;   // [Ny*Nz]
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)

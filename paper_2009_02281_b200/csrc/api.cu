@@ -47,6 +47,7 @@ struct aimx_ctx {
   cudaStream_t sc[2] = {nullptr, nullptr};   // host sweep copy streams (H2D, D2H)
   std::vector<cudaEvent_t> ev_io;
   cudaEvent_t ev_start = nullptr, ev_sp[2] = {nullptr, nullptr}, ev_mv[2] = {nullptr, nullptr};
+  cudaEvent_t ev_xt[2] = {nullptr, nullptr};   // the batch's interleaved columns are ready
   // sweep pipeline, S4+S5 of batch i on s3 while the grid part of batch i+1 runs:
   cudaStream_t s3 = nullptr;
   cudaEvent_t ev_grid[2] = {nullptr, nullptr};
@@ -629,6 +630,7 @@ void do_setup(aimx_ctx* c, const aimx_mesh_desc* mesh, const aimx_grid_desc* gri
     AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
       AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_sp[k], cudaEventDisableTiming));
+      AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_xt[k], cudaEventDisableTiming));
       AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_mv[k], cudaEventDisableTiming));
       AIMX_CUDA(cudaEventCreateWithFlags(&c->ev_grid[k], cudaEventDisableTiming));
     }
@@ -1180,7 +1182,8 @@ void destroy_impl(aimx_ctx* c) {
       cudaStreamDestroy(c->sc[k]);
     }
   for (cudaEvent_t e : c->ev_io) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_start, c->ev_sp[0], c->ev_sp[1], c->ev_mv[0], c->ev_mv[1], c->ev_grid[0], c->ev_grid[1]})
+  for (cudaEvent_t e : {c->ev_start, c->ev_sp[0], c->ev_sp[1], c->ev_mv[0], c->ev_mv[1], c->ev_grid[0], c->ev_grid[1],
+                        c->ev_xt[0], c->ev_xt[1]})
     if (e) cudaEventDestroy(e);
   delete c;
 }
@@ -1792,17 +1795,21 @@ static void sweep_impl(aimx_ctx* c, const std::vector<int64_t>& off, const doubl
   }
   AIMX_CUDA(cudaEventRecord(c->ev_start, s));
   AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_start, 0));
-  // side stream, per batch: its spectra and its interleaved columns (xt),
-  // double-buffered; `before` (the host sweep's copy) gates the columns
+  // side stream, per batch: its interleaved columns (xt), then its spectra,
+  // double-buffered; `before` (the host sweep's copy) gates the columns.  The
+  // batch's gather and x transform wait only for its columns (ev_xt), its
+  // spectrum multiply for its spectra (ev_sp; HotDev::spec_ready), so the
+  // first batch's spectra overlap its projection
   auto spec = [&](int64_t i) {
     if (i >= 2) AIMX_CUDA(cudaStreamWaitEvent(c->s2, c->ev_mv[i % 2], 0));   // matvec i-2 read these buffers
-    spectra(c, count(i), f + off[i], c->s2, c->HB[i % 2]);
     HotDev hh = c->hot;
     hh.xt = c->XT[i % 2];
     Combine cb = make_combine(count(i), f + off[i], 0, c->hot.nb);
     if (before_side) before_side(i, c->s2);
     if (c->prec == AIMX_C64) interleave_f32(hh, X + off[i] * vb, cb, c->s2);
     else interleave_f64(hh, X + off[i] * vb, cb, c->s2);
+    AIMX_CUDA(cudaEventRecord(c->ev_xt[i % 2], c->s2));
+    spectra(c, count(i), f + off[i], c->s2, c->HB[i % 2]);
     AIMX_CUDA(cudaEventRecord(c->ev_sp[i % 2], c->s2));
   };
   // overlap: the grid part of batch i+1 (stream s) runs while S4+S5 of batch
@@ -1812,9 +1819,10 @@ static void sweep_impl(aimx_ctx* c, const std::vector<int64_t>& off, const doubl
   spec(0);
   for (int64_t i = 0; i < nbat; ++i) {
     if (i + 1 < nbat) spec(i + 1);
-    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_sp[i % 2], 0));
+    AIMX_CUDA(cudaStreamWaitEvent(s, c->ev_xt[i % 2], 0));
     if (before) before(i);
     HotDev hh = batch_view(c, count(i));
+    hh.spec_ready = c->ev_sp[i % 2];
     hh.Hoct = c->HB[i % 2];
     hh.xt = c->XT[i % 2];
     Combine cb = make_combine(count(i), f + off[i], 0, c->hot.nb);

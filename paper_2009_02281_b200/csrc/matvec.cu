@@ -1526,6 +1526,7 @@ void hot_grid(const HotDev& h, const void* x, const Combine& c, cudaStream_t s, 
     else run_gather_b<T>(h, B, s);
     AIMX_SWITCH_L(Lx, (run_x<T, L>(h, false, B, s)));
   }
+  if (h.spec_ready) AIMX_CUDA(cudaStreamWaitEvent(s, h.spec_ready, 0));   // the batch's spectra
   grid_conv<T>(h, B, s, prof);
   { StageScope sc(prof, 5, s); AIMX_SWITCH_L(Lx, (run_x<T, L>(h, true, B, s))); }
 }
