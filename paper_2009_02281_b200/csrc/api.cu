@@ -433,7 +433,9 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   // one wave of resident CTAs (AIMX_NEAR_SMS: spread over fewer SMs, experiments)
   int nsm_near = nsm;
   if (const char* e = std::getenv("AIMX_NEAR_SMS")) nsm_near = std::max(1, std::min(nsm, std::atoi(e)));
-  const int ncta = near_ctas_per_sm(f32, false, grp.R) * nsm_near;
+  int per_sm = near_ctas_per_sm(f32, false, grp.R);   // AIMX_NEAR_PER_SM: fewer (experiments)
+  if (const char* e = std::getenv("AIMX_NEAR_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+  const int ncta = per_sm * nsm_near;
   const std::vector<int64_t> order = near_round_order(grp.ngrp, ncta, cta_begin);
   build_near_chunks(grp, near_chw(f32, c->slots), near_chc(f32, c->slots), cs, ck, order);
   // value slot (u R + r) -> payload byte offset

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
 // one is used); within a chunk each group issues its x-row loads 8 at a time
 // before the arithmetic (packed FFMA2 in fp32).
 template <typename T, int BB>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 2) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      int B) {
   pdl_wait();
   pdl_trigger();
