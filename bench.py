@@ -357,7 +357,10 @@ def sweep_measure(op, c, prec, freqs, X, Y, flush, steps, warmup, barrier, susta
         flush.zero_()
         op.sweep(freqs, X, Y)
     torch.cuda.synchronize()
-    op.profile_enable(True)
+    # stage breakdown on one stream (each stage's own device time; the
+    # pipelined sweep overlaps a batch's spectra and S4+S5 with the next
+    # batch's grid stages, which would charge one stage for another's work)
+    op.profile_enable(True, serial=True)
     flush.zero_()
     op.sweep(freqs, X, Y)
     prof_all = op.profile_read()
@@ -413,13 +416,19 @@ def roofline_of(st, prec, prof_all, prof, dom, cols_per_launch, cfg):
                      "GBps": sb[k] / (avg * 1e-3) / 1e9, "share": ms / step_stage_ms}
     dms, dn = prof[dom]
     ach = sb[dom] / (dms / dn * 1e-3) / 1e9
+    sms, sn = prof_all[dom]
     tr = traffic.get(dom)
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": tr.get("bytes") if isinstance(tr, dict) else tr,
                 "traffic_source": (tr.get("source") if isinstance(tr, dict) else
                                    ("profiles/ncu_traffic.json" if tr is not None else None)),
                 "kernel": dom, "peak_source": peak_src, "algorithmic_bytes_per_launch": sb[dom],
-                "columns_per_launch": cols_per_launch, "ms_per_launch": dms / dn, "launches_timed": dn}
+                "columns_per_launch": cols_per_launch, "ms_per_launch": dms / dn, "launches_timed": dn,
+                "ms_per_launch_serial": sms / sn,
+                "frac_serial": sb[dom] / (sms / sn * 1e-3) / 1e9 / peak,
+                "note": "achieved/frac: the kernel's launches bracketed live in the timed (pipelined) steps, "
+                        "where it shares the GPU with the next batch's grid stages; *_serial: the same "
+                        "launches in the one-stream breakdown step (its own time)"}
     return roofline, stages, sb
 
 
@@ -595,8 +604,8 @@ def run_aimx(a):
                          "note": "sum over every launch of the step of its stage's algorithmic bytes "
                                  "(stage_bytes) over the step's device time"},
             "stages": stages,
-            "stages_note": "one extra untimed step with every stage bracketed by CUDA events (stages of "
-                           "overlapping streams share the GPU, so their times overstate their own cost)",
+            "stages_note": "one extra untimed step with every stage bracketed by CUDA events, its device "
+                           "batches on one stream (AIMX_PROFILE_SERIAL), so each stage's time is its own",
             "fft_conv_vs_cufft": fft_vs_cufft,
             "secondary": secondary,
             "cpu_baseline": cpu,

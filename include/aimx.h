@@ -337,7 +337,11 @@ aimx_status aimx_profile_read(aimx_ctx* ctx, double* ms, int64_t* launches, int6
 /* Which stages are bracketed while profiling is on (bit i = stage i; default
  * all).  Each bracket is a pair of events on the stream, which also ends the
  * overlap of consecutive kernels' launches (programmatic dependent launch)
- * at that point, so a timed run brackets only the stage it reports. */
+ * at that point, so a timed run brackets only the stage it reports.
+ * AIMX_PROFILE_SERIAL in the mask: while profiling is on, sweeps run their
+ * device batches on one stream (no overlap of one batch's spectra or S4+S5
+ * with the next batch's grid stages), so each stage's time is its own. */
+#define AIMX_PROFILE_SERIAL 0x80
 aimx_status aimx_profile_stages(aimx_ctx* ctx, int32_t mask);
 
 /* ---- slab-decomposed FFT (multi-GPU for the largest grid) ----

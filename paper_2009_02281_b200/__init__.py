@@ -403,9 +403,11 @@ class AIMx:
 
     STAGES = ("spectrum", "proj_xfft", "yfwd", "zconv", "yinv", "xinv", "interp_near")
 
-    def profile_enable(self, on: bool = True, stages=None):
-        """stages: names (AIMx.STAGES) to bracket with events; None = all."""
+    def profile_enable(self, on: bool = True, stages=None, serial: bool = False):
+        """stages: names (AIMx.STAGES) to bracket with events; None = all.
+        serial: sweeps run their batches on one stream (each stage's own time)."""
         mask = 0x7F if stages is None else sum(1 << self.STAGES.index(k) for k in stages)
+        mask |= 0x80 if serial else 0
         _check(self.lib, self.lib.aimx_profile_stages(self.ctx, int(mask)), self.ctx)
         _check(self.lib, self.lib.aimx_profile_enable(self.ctx, int(bool(on))), self.ctx)
 

@@ -246,6 +246,7 @@ void spectrum_dynamic_f64(SpectrumPlan& sp, int B, const double* k0, const doubl
 struct Profiler {
   bool on = false;
   int mask = 0x7f;             // stages bracketed while on (bit i = stage i)
+  bool serial = false;         // sweeps on one stream while on (AIMX_PROFILE_SERIAL)
   std::vector<cudaEvent_t> pool;
   struct Rec { int stage; cudaEvent_t a, b; };
   std::vector<Rec> pending;

@@ -1787,7 +1787,7 @@ static void sweep_impl(aimx_ctx* c, const std::vector<int64_t>& off, const doubl
   const size_t vb = (size_t)c->hot.nb * (c->prec == AIMX_C64 ? sizeof(float2) : sizeof(double2));
   const int64_t nbat = (int64_t)off.size() - 1;
   auto count = [&](int64_t i) { return (int)(off[i + 1] - off[i]); };
-  if (c->slab || nbat < 2 || !c->s2 || c->aim_on || c->cfie_on) {
+  if (c->slab || nbat < 2 || !c->s2 || c->aim_on || c->cfie_on || (c->prof.on && c->prof.serial)) {
     for (int64_t i = 0; i < nbat; ++i) {
       if (before) before(i);
       run_batch(c, count(i), f + off[i], X + off[i] * vb, Y + off[i] * vb, s);
@@ -2349,6 +2349,7 @@ aimx_status aimx_profile_enable(aimx_ctx* c, int on) {
 aimx_status aimx_profile_stages(aimx_ctx* c, int32_t mask) {
   if (!c) return AIMX_E_INVALID_ARG;
   c->prof.mask = mask & 0x7f;
+  c->prof.serial = (mask & AIMX_PROFILE_SERIAL) != 0;
   return AIMX_OK;
 }
 
