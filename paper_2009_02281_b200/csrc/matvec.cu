@@ -198,9 +198,13 @@ template <typename S, int L, bool SMALL = false> struct PassGeom {
   using TL = TwoLevel<R1, R2>;
   static constexpr int T = TL::T, E = TL::E;
   // per-line exchange stride: bank-spread so that the lines and threads of a
-  // warp hit distinct 8-byte slots (stride = 1 mod 16, or 4 mod 16 when a
-  // warp holds 8 lines x 4 threads)
-  static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? 4 : 1) : 0;
+  // half-warp (one shared-memory wavefront of 8-byte accesses: 16 lanes) hit
+  // distinct 8-byte slots: a half-warp holds NL lines x 16/NL threads, so the
+  // stride is 16/NL mod 16 -- 1 for 16 lines (T = 16), 2 for 8 lines (T = 32,
+  // 256 threads), 4 for 4 lines (T = 32, SMALL: 128 threads).  (4 for 8 lines
+  // put lines l and l + 4 on one slot: ncu counted 12.6 M excess store and
+  // 13 M excess load wavefronts in the cfg5 planar y pass, 30% of its stalls.)
+  static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? (SMALL ? 4 : 2) : 1) : 0;
   static constexpr size_t BYTES256 = sizeof(typename CT<S>::T2) * (size_t)(256 / T) * XB;
   // threads per CTA; SMALL: one x row (4 channel lines) per CTA when rows are few
   static constexpr int NT = SMALL ? (4 * T > 64 ? 4 * T : 64) : (BYTES256 > 200 * 1024 ? 128 : 256);
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !SMALL) ? 3 : 1) k_xin
 template <typename T, int L, int NCH = 4> struct XinvB {
   static constexpr int T_ = TwoLevel<Fac<L>::R1, Fac<L>::R2>::T;
   static constexpr int NL = 4 * NCH, NT = NL * T_;
-  static constexpr int XB = PassGeom<T, L>::XB;
+  static constexpr int XB = PassGeom<T, L>::XB;   // (3 mod 16 for the 12-line CTA measured 199 -> 207 us on cfg5)
   static constexpr size_t SMEM = sizeof(typename CT<T>::T2) * (L + (size_t)NL * XB);
 };
 template <typename T, int L, int NCH>
@@ -574,7 +578,10 @@ __global__ void __launch_bounds__(ZGeom<T, L>::NT, sizeof(T) == 4 ? 2 : 2) k_zco
   const int Nx = h.Nx, Ny = h.Ny, Nz = h.Nz, Ny2 = 2 * h.Ny;
   const int b = blockIdx.z;
   extern __shared__ __align__(128) unsigned char smem_dyn[];
-  unsigned char* smem_raw = (unsigned char*)(((uintptr_t)smem_dyn + 127) & ~(uintptr_t)127);
+  // 128-byte aligned base by pointer arithmetic on the shared array (an
+  // integer round trip would lose the address space: generic LD/ST for every
+  // exchange and slab access, measured as 42% of the stall samples)
+  unsigned char* smem_raw = smem_dyn + ((128u - (smem_u32(smem_dyn) & 127u)) & 127u);
   T2* hs = reinterpret_cast<T2*>(smem_raw + Z::OFF_HS);                        // [2][NS][kz <= Nz][kx - kx0]
   const int NB = Z::nbuf(Nz);
   T2* inb = reinterpret_cast<T2*>(smem_raw + Z::OFF_IN);                       // [NB][z][CW]
