@@ -85,8 +85,19 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
 // warp per occupied node, groups of BB/V lanes stride its entries (each entry's
 // weights and RWG index read once for all columns), lanes cover columns.  The
 // entries come in coalesced chunks of 32 (the next chunk's loaded while this
-// one is used); within a chunk each group issues its x-row loads 8 at a time
-// before the arithmetic (packed FFMA2 in fp32).
+// one is used).  A chunk's x rows go global -> shared by cp.async, all of
+// them at once (each lane copies the 16-byte pieces it later reads, so only
+// its own copies are waited on), then the arithmetic reads them back (packed
+// FFMA2 in fp32).  Staging the rows in registers allowed 4 loads in flight
+// per lane at 3 CTAs per SM: four dependent L2 round trips per chunk, 45% of
+// the stall samples.
+template <typename T, int BB> struct GatherB {
+  static constexpr int V = sizeof(T) == 4 ? 2 : 1;
+  static constexpr int LG = BB / V, NG = 32 / LG;
+  static constexpr int PER = 32 / NG;   // entries of a chunk per group
+  static constexpr int PS = PER < 16 ? PER : 16;   // ... in flight at once (64 KB of pieces per CTA at most)
+  static constexpr size_t SMEM = (size_t)(256 / 32) * PS * 32 * 16;   // [warp][entry][lane] 16-byte pieces
+};
 template <typename T, int BB>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      int B) {
@@ -94,14 +105,12 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev
   pdl_trigger();
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
-  constexpr int V = sizeof(T2) == 8 ? 2 : 1;
-  constexpr int LG = BB / V, NG = 32 / LG;
-  constexpr int PER = 32 / NG;             // entries of a chunk per group
-  // loads in flight per batch: 4 (3 CTAs of 256 threads per SM; with 8 the
-  // registers allowed 2 and the gather was latency bound at 22% occupancy)
-  constexpr int QB = PER < 4 ? PER : 4;
+  using GB = GatherB<T, BB>;
+  constexpr int V = GB::V, LG = GB::LG, NG = GB::NG, PER = GB::PER, PS = GB::PS;
   using VT = typename std::conditional<V == 2, float4, double2>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
+  VT* const ub = reinterpret_cast<VT*>(smem_raw) + (threadIdx.x >> 5) * PS * 32 + lane;   // this lane's pieces
   const int b0 = (lane % LG) * V, g = lane / LG;
   const int q = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (q >= h.nocc) return;
@@ -128,37 +137,44 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev
       nw = ew[nx];
     }
 #pragma unroll
-    for (int jb = 0; jb < PER; jb += QB) {
-      if (jb * NG >= cnt) break;   // warp-uniform: no entry of this batch exists
-      VT u[QB];
-      T4 w[QB];
+    for (int j0 = 0; j0 < PER; j0 += PS) {
+    if (j0 * NG >= cnt) break;
+    // this group's entries jb NG + g of the chunk: their x rows, PS in flight
 #pragma unroll
-      for (int qq = 0; qq < QB; ++qq) {
-        const int src = (jb + qq) * NG + g;   // entries past the node carry zero weights
-        w[qq].x = __shfl_sync(0xffffffffu, myw.x, src);
-        w[qq].y = __shfl_sync(0xffffffffu, myw.y, src);
-        w[qq].z = __shfl_sync(0xffffffffu, myw.z, src);
-        w[qq].w = __shfl_sync(0xffffffffu, myw.w, src);
-        const int rr = __shfl_sync(0xffffffffu, myr, src);
-        u[qq] = *(const VT*)(xt + (int64_t)rr * BB + b0);
+    for (int jj = 0; jj < PS; ++jj) {
+      const int jb = j0 + jj;
+      if (jb * NG >= cnt) break;   // warp-uniform: no entry from here on
+      const int rr = __shfl_sync(0xffffffffu, myr, jb * NG + g);   // entries past the node: row 0, zero weights
+      cp_async(ub + jj * 32, (const VT*)(xt + (int64_t)rr * BB + b0));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+    for (int jj = 0; jj < PS; ++jj) {
+      const int jb = j0 + jj;
+      if (jb * NG >= cnt) break;
+      const int src = jb * NG + g;
+      T4 w;
+      w.x = __shfl_sync(0xffffffffu, myw.x, src);
+      w.y = __shfl_sync(0xffffffffu, myw.y, src);
+      w.z = __shfl_sync(0xffffffffu, myw.z, src);
+      w.w = __shfl_sync(0xffffffffu, myw.w, src);
+      const VT u = ub[jj * 32];
+      T2 xv[V];
+      if constexpr (V == 2) {
+        xv[0] = mk<T2>(u.x, u.y);
+        xv[1] = mk<T2>(u.z, u.w);
+      } else {
+        xv[0] = u;
       }
 #pragma unroll
-      for (int qq = 0; qq < QB; ++qq) {
-        T2 xv[V];
-        if constexpr (V == 2) {
-          xv[0] = mk<T2>(u[qq].x, u[qq].y);
-          xv[1] = mk<T2>(u[qq].z, u[qq].w);
-        } else {
-          xv[0] = u[qq];
-        }
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          axpy(a[v][0], w[qq].x, xv[v]);
-          axpy(a[v][1], w[qq].y, xv[v]);
-          axpy(a[v][2], w[qq].z, xv[v]);
-          axpy(a[v][3], w[qq].w, xv[v]);
-        }
+      for (int v = 0; v < V; ++v) {
+        axpy(a[v][0], w.x, xv[v]);
+        axpy(a[v][1], w.y, xv[v]);
+        axpy(a[v][2], w.z, xv[v]);
+        axpy(a[v][3], w.w, xv[v]);
       }
+    }
     }
     myr = nr;
     myw = nw;
@@ -226,7 +242,10 @@ __device__ __forceinline__ void inv_fft(T2* v, T2* xb, const T2* tw, int t) {
   fft2<T2, Fac<L>::R1, Fac<L>::R2, true>(v, xb, tw, t);
 }
 
-template <typename T, int L, bool SMALL = false>
+// ASYNC: the twiddle table goes global -> shared by cp.async (one commit
+// group) so its latency overlaps the pass's input loads; the kernel calls
+// pass_ready() after issuing them, before the first transform.
+template <typename T, int L, bool SMALL = false, bool ASYNC = false>
 __device__ __forceinline__ void pass_prologue(typename CT<T>::T2*& tw, typename CT<T>::T2*& xb,
                                               const typename CT<T>::T2* __restrict__ gtw, int line) {
   using T2 = typename CT<T>::T2;
@@ -234,7 +253,17 @@ __device__ __forceinline__ void pass_prologue(typename CT<T>::T2*& tw, typename 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   tw = reinterpret_cast<T2*>(smem_raw);
   xb = tw + L + line * G::XB;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = gtw[i];
+  if constexpr (ASYNC) {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async(tw + i, gtw + i);
+    asm volatile("cp.async.commit_group;\n" ::);
+  } else {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = gtw[i];
+    __syncthreads();
+  }
+}
+// every cp.async of this thread landed, and every thread's (block barrier)
+__device__ __forceinline__ void pass_ready() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
 }
 
@@ -252,7 +281,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !SMALL) ? 3 : 1) k_xfw
   using G = PassGeom<T, L, SMALL>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T, L, SMALL>(tw, xb, (const T2*)h.twx, line);
+  pass_prologue<T, L, SMALL, true>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y, nc = h.nc;   // lines = (grid line r, channel c < nc), c fastest
   const int gline = blockIdx.x * G::NL + line, r = gline / nc, c = gline - r * nc;
   const bool act = r < h.nlines;
@@ -264,6 +293,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !SMALL) ? 3 : 1) k_xfw
     const int x = G::TL::in_index(t, i);
     v[i] = (act && i % G::R2 < G::R2 / 2) ? in[x * nc] : mk<T2>(0, 0);
   }
+  pass_ready();
   fwd_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   T2* __restrict__ out = (T2*)h.bufA + b * h.sA + (int64_t)h.line_id[r] * L * nc + c;
@@ -280,7 +310,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !SMALL) ? 3 : 1) k_xin
   using G = PassGeom<T, L, SMALL>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T, L, SMALL>(tw, xb, (const T2*)h.twx, line);
+  pass_prologue<T, L, SMALL, true>(tw, xb, (const T2*)h.twx, line);
   const int b = blockIdx.y, nc = h.nc;
   const int gline = blockIdx.x * G::NL + line, r = gline / nc, c = gline - r * nc;
   const bool act = r < h.nlines;
@@ -289,6 +319,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 && !SMALL) ? 3 : 1) k_xin
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * nc] : mk<T2>(0, 0);
+  pass_ready();
   inv_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   const int Nx = h.Nx;
@@ -327,8 +358,7 @@ __global__ void __launch_bounds__(XinvB<T, L, NCH>::NT, (sizeof(T) == 4 && NCH =
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* tw = reinterpret_cast<T2*>(smem_raw);
   T2* xb = tw + L + line * X::XB;
-  for (int i = threadIdx.x; i < L; i += X::NT) tw[i] = ((const T2*)h.twx)[i];
-  __syncthreads();
+  for (int i = threadIdx.x; i < L; i += X::NT) cp_async(tw + i, (const T2*)h.twx + i);   // lands behind the input loads
   const int r = blockIdx.x, c = line % NCH, b = blockIdx.y * 4 + line / NCH;
   const bool act = b < B;
   const int lid = h.line_id[r];
@@ -336,6 +366,7 @@ __global__ void __launch_bounds__(XinvB<T, L, NCH>::NT, (sizeof(T) == 4 && NCH =
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) v[i] = act ? in[G::TL::in_index(t, i) * NCH] : mk<T2>(0, 0);
+  pass_ready();
   inv_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   const int Nx = h.Nx;
@@ -380,7 +411,7 @@ __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T, L>(tw, xb, (const T2*)h.twy_tab, line);
+  pass_prologue<T, L, false, true>(tw, xb, (const T2*)h.twy_tab, line);
   const int W = h.W, Ny = h.Ny;
   const ColTile ct = col_tile<T, L>(line, W);
   const int zi = blockIdx.y * ct.RPC + ct.rsub;
@@ -395,6 +426,7 @@ __global__ void __launch_bounds__(256) k_yfwd(HotDev h) {
     const int y = G::TL::in_index(t, i);
     v[i] = (act && i % G::R2 < G::R2 / 2) ? in[(int64_t)y * W] : mk<T2>(0, 0);
   }
+  pass_ready();
   fwd_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   T2* __restrict__ out = (T2*)h.bufB + b * h.sB + (int64_t)z * L * W + col;
@@ -411,7 +443,7 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
   using G = PassGeom<T, L>;
   const int line = threadIdx.x % G::NL, t = threadIdx.x / G::NL;
   T2 *tw, *xb;
-  pass_prologue<T, L>(tw, xb, (const T2*)h.twy_tab, line);
+  pass_prologue<T, L, false, true>(tw, xb, (const T2*)h.twy_tab, line);
   const int W = h.W, Ny = h.Ny;
   const ColTile ct = col_tile<T, L>(line, W);
   const int zi = blockIdx.y * ct.RPC + ct.rsub;
@@ -423,6 +455,7 @@ __global__ void __launch_bounds__(256) k_yinv(HotDev h) {
   T2 v[G::E];
 #pragma unroll
   for (int i = 0; i < G::E; ++i) v[i] = act ? in[(int64_t)G::TL::in_index(t, i) * W] : mk<T2>(0, 0);
+  pass_ready();
   inv_fft<T2, L>(v, xb, tw, t);
   if (!act) return;
   T2* __restrict__ out = (T2*)h.bufC + b * h.sA + (int64_t)z * Ny * W + col;
@@ -734,13 +767,18 @@ __global__ void __launch_bounds__(256, 2) k_yconv_plane(HotDev h) {
   const int nkx = (ja + ct.CW - 1) / nc - ja / nc + 1;
   const int b = blockIdx.z;
   const T2* __restrict__ Hb = (const T2*)h.Hoct + b * h.sH;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = ((const T2*)h.twy_tab)[i];
+  // the plane's occupied rows (they gate the loads) by plain loads; the
+  // twiddles and the H_hat2 slab by cp.async (two commit groups), landing
+  // behind the input loads and the forward transform respectively
+  uint8_t* occ = reinterpret_cast<uint8_t*>(hs + (L / 2 + 1) * nkx);
+  for (int y = threadIdx.x; y < Ny; y += blockDim.x) occ[y] = h.line_occ[(int64_t)h.zplane0 * Ny + y];
+  for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async(tw + i, (const T2*)h.twy_tab + i);
+  asm volatile("cp.async.commit_group;\n" ::);
   for (int i = threadIdx.x; i < (L / 2 + 1) * nkx; i += blockDim.x) {
     const int ky = i / nkx, kx = kx0 + i % nkx;
-    hs[i] = Hb[(int64_t)ky * (Nx + 1) + (kx <= Nx ? kx : 2 * Nx - kx)];
+    cp_async(hs + i, Hb + (int64_t)ky * (Nx + 1) + (kx <= Nx ? kx : 2 * Nx - kx));
   }
-  uint8_t* occ = reinterpret_cast<uint8_t*>(hs + (L / 2 + 1) * nkx);   // the plane's occupied rows
-  for (int y = threadIdx.x; y < Ny; y += blockDim.x) occ[y] = h.line_occ[(int64_t)h.zplane0 * Ny + y];
+  asm volatile("cp.async.commit_group;\n" ::);
   __syncthreads();
   const bool act = ct.rsub == 0;   // one plane: the column tile's first row set only
   const int64_t col = ja + ct.w;
@@ -760,7 +798,11 @@ __global__ void __launch_bounds__(256, 2) k_yconv_plane(HotDev h) {
     const int y = G::TL::in_index(t, i);
     v[i] = (act && ((om >> i) & 1)) ? in[y * W] : mk<T2>(0, 0);
   }
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // the twiddles
+  __syncthreads();
   fwd_fft<T2, L>(v, xb, tw, t);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // the slab
+  __syncthreads();
   {
     const T2* hl = hs + kxl;
 #pragma unroll
@@ -1344,17 +1386,22 @@ void run_interleave(const HotDev& h, const void* x, const Combine& c, cudaStream
   AIMX_CHECK_LAUNCH();
 }
 
+template <typename T, int BB>
+void run_gather_bk(const HotDev& h, dim3 g, const typename CT<T>::T2* xt, int B, cudaStream_t s) {
+  set_smem(k_gather_b<T, BB>, GatherB<T, BB>::SMEM);
+  launch_pdl(k_gather_b<T, BB>, g, dim3(256), GatherB<T, BB>::SMEM, s, h, xt, B);
+}
 template <typename T>
 void run_gather_b(const HotDev& h, int B, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   const unsigned g = (unsigned)(((int64_t)h.nocc * 32 + 255) / 256);
   const T2* xt = (const T2*)h.xt;
   switch (batch_bucket(B)) {
-    case 2: launch_pdl(k_gather_b<T, 2>, dim3(g), dim3(256), 0, s, h, xt, B); break;
-    case 4: launch_pdl(k_gather_b<T, 4>, dim3(g), dim3(256), 0, s, h, xt, B); break;
-    case 8: launch_pdl(k_gather_b<T, 8>, dim3(g), dim3(256), 0, s, h, xt, B); break;
-    case 16: launch_pdl(k_gather_b<T, 16>, dim3(g), dim3(256), 0, s, h, xt, B); break;
-    default: launch_pdl(k_gather_b<T, 32>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    case 2: run_gather_bk<T, 2>(h, g, xt, B, s); break;
+    case 4: run_gather_bk<T, 4>(h, g, xt, B, s); break;
+    case 8: run_gather_bk<T, 8>(h, g, xt, B, s); break;
+    case 16: run_gather_bk<T, 16>(h, g, xt, B, s); break;
+    default: run_gather_bk<T, 32>(h, g, xt, B, s); break;
   }
   AIMX_CHECK_LAUNCH();
 }
