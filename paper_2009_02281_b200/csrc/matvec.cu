@@ -85,19 +85,8 @@ __global__ void __launch_bounds__(256) k_gather(HotDev h, const typename CT<T>::
 // warp per occupied node, groups of BB/V lanes stride its entries (each entry's
 // weights and RWG index read once for all columns), lanes cover columns.  The
 // entries come in coalesced chunks of 32 (the next chunk's loaded while this
-// one is used).  A chunk's x rows go global -> shared by cp.async, all of
-// them at once (each lane copies the 16-byte pieces it later reads, so only
-// its own copies are waited on), then the arithmetic reads them back (packed
-// FFMA2 in fp32).  Staging the rows in registers allowed 4 loads in flight
-// per lane at 3 CTAs per SM: four dependent L2 round trips per chunk, 45% of
-// the stall samples.
-template <typename T, int BB> struct GatherB {
-  static constexpr int V = sizeof(T) == 4 ? 2 : 1;
-  static constexpr int LG = BB / V, NG = 32 / LG;
-  static constexpr int PER = 32 / NG;   // entries of a chunk per group
-  static constexpr int PS = PER < 16 ? PER : 16;   // ... in flight at once (64 KB of pieces per CTA at most)
-  static constexpr size_t SMEM = (size_t)(256 / 32) * PS * 32 * 16;   // [warp][entry][lane] 16-byte pieces
-};
+// one is used); within a chunk each group issues its x-row loads 8 at a time
+// before the arithmetic (packed FFMA2 in fp32).
 template <typename T, int BB>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev h, const typename CT<T>::T2* __restrict__ xt,
                                                      int B) {
@@ -105,12 +94,14 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev
   pdl_trigger();
   using T2 = typename CT<T>::T2;
   using T4 = typename CT<T>::T4;
-  using GB = GatherB<T, BB>;
-  constexpr int V = GB::V, LG = GB::LG, NG = GB::NG, PER = GB::PER, PS = GB::PS;
+  constexpr int V = sizeof(T2) == 8 ? 2 : 1;
+  constexpr int LG = BB / V, NG = 32 / LG;
+  constexpr int PER = 32 / NG;             // entries of a chunk per group
+  // loads in flight per batch: 4 (3 CTAs of 256 threads per SM; with 8 the
+  // registers allowed 2 and the gather was latency bound at 22% occupancy)
+  constexpr int QB = PER < 4 ? PER : 4;
   using VT = typename std::conditional<V == 2, float4, double2>::type;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  VT* const ub = reinterpret_cast<VT*>(smem_raw) + (threadIdx.x >> 5) * PS * 32 + lane;   // this lane's pieces
   const int b0 = (lane % LG) * V, g = lane / LG;
   const int q = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (q >= h.nocc) return;
@@ -137,44 +128,37 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) k_gather_b(HotDev
       nw = ew[nx];
     }
 #pragma unroll
-    for (int j0 = 0; j0 < PER; j0 += PS) {
-    if (j0 * NG >= cnt) break;
-    // this group's entries jb NG + g of the chunk: their x rows, PS in flight
+    for (int jb = 0; jb < PER; jb += QB) {
+      if (jb * NG >= cnt) break;   // warp-uniform: no entry of this batch exists
+      VT u[QB];
+      T4 w[QB];
 #pragma unroll
-    for (int jj = 0; jj < PS; ++jj) {
-      const int jb = j0 + jj;
-      if (jb * NG >= cnt) break;   // warp-uniform: no entry from here on
-      const int rr = __shfl_sync(0xffffffffu, myr, jb * NG + g);   // entries past the node: row 0, zero weights
-      cp_async(ub + jj * 32, (const VT*)(xt + (int64_t)rr * BB + b0));
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-#pragma unroll
-    for (int jj = 0; jj < PS; ++jj) {
-      const int jb = j0 + jj;
-      if (jb * NG >= cnt) break;
-      const int src = jb * NG + g;
-      T4 w;
-      w.x = __shfl_sync(0xffffffffu, myw.x, src);
-      w.y = __shfl_sync(0xffffffffu, myw.y, src);
-      w.z = __shfl_sync(0xffffffffu, myw.z, src);
-      w.w = __shfl_sync(0xffffffffu, myw.w, src);
-      const VT u = ub[jj * 32];
-      T2 xv[V];
-      if constexpr (V == 2) {
-        xv[0] = mk<T2>(u.x, u.y);
-        xv[1] = mk<T2>(u.z, u.w);
-      } else {
-        xv[0] = u;
+      for (int qq = 0; qq < QB; ++qq) {
+        const int src = (jb + qq) * NG + g;   // entries past the node carry zero weights
+        w[qq].x = __shfl_sync(0xffffffffu, myw.x, src);
+        w[qq].y = __shfl_sync(0xffffffffu, myw.y, src);
+        w[qq].z = __shfl_sync(0xffffffffu, myw.z, src);
+        w[qq].w = __shfl_sync(0xffffffffu, myw.w, src);
+        const int rr = __shfl_sync(0xffffffffu, myr, src);
+        u[qq] = *(const VT*)(xt + (int64_t)rr * BB + b0);
       }
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        axpy(a[v][0], w.x, xv[v]);
-        axpy(a[v][1], w.y, xv[v]);
-        axpy(a[v][2], w.z, xv[v]);
-        axpy(a[v][3], w.w, xv[v]);
+      for (int qq = 0; qq < QB; ++qq) {
+        T2 xv[V];
+        if constexpr (V == 2) {
+          xv[0] = mk<T2>(u[qq].x, u[qq].y);
+          xv[1] = mk<T2>(u[qq].z, u[qq].w);
+        } else {
+          xv[0] = u[qq];
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          axpy(a[v][0], w[qq].x, xv[v]);
+          axpy(a[v][1], w[qq].y, xv[v]);
+          axpy(a[v][2], w[qq].z, xv[v]);
+          axpy(a[v][3], w[qq].w, xv[v]);
+        }
       }
-    }
     }
     myr = nr;
     myw = nw;
@@ -1386,22 +1370,17 @@ void run_interleave(const HotDev& h, const void* x, const Combine& c, cudaStream
   AIMX_CHECK_LAUNCH();
 }
 
-template <typename T, int BB>
-void run_gather_bk(const HotDev& h, dim3 g, const typename CT<T>::T2* xt, int B, cudaStream_t s) {
-  set_smem(k_gather_b<T, BB>, GatherB<T, BB>::SMEM);
-  launch_pdl(k_gather_b<T, BB>, g, dim3(256), GatherB<T, BB>::SMEM, s, h, xt, B);
-}
 template <typename T>
 void run_gather_b(const HotDev& h, int B, cudaStream_t s) {
   using T2 = typename CT<T>::T2;
   const unsigned g = (unsigned)(((int64_t)h.nocc * 32 + 255) / 256);
   const T2* xt = (const T2*)h.xt;
   switch (batch_bucket(B)) {
-    case 2: run_gather_bk<T, 2>(h, g, xt, B, s); break;
-    case 4: run_gather_bk<T, 4>(h, g, xt, B, s); break;
-    case 8: run_gather_bk<T, 8>(h, g, xt, B, s); break;
-    case 16: run_gather_bk<T, 16>(h, g, xt, B, s); break;
-    default: run_gather_bk<T, 32>(h, g, xt, B, s); break;
+    case 2: launch_pdl(k_gather_b<T, 2>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    case 4: launch_pdl(k_gather_b<T, 4>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    case 8: launch_pdl(k_gather_b<T, 8>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    case 16: launch_pdl(k_gather_b<T, 16>, dim3(g), dim3(256), 0, s, h, xt, B); break;
+    default: launch_pdl(k_gather_b<T, 32>, dim3(g), dim3(256), 0, s, h, xt, B); break;
   }
   AIMX_CHECK_LAUNCH();
 }
