@@ -363,8 +363,14 @@ void build_near_groups(const Topology& t, const std::vector<uint8_t>& nz_slot, N
   const char* eR = std::getenv("AIMX_NEAR_R");
   const char* eK = std::getenv("AIMX_NEAR_ORDER");
   std::vector<int32_t> perm[2] = {row_order(t, 0, rows), row_order(t, 1, rows)};
+  // every anchor in one z plane (planar meshes, cfg5): the linear order, a
+  // band of grid rows per round of groups, measured faster than Morton order
+  // (cfg5, 32 columns: S4+S5 0.783 -> 0.748 ms in the serial stage profile,
+  // bench step 3.93 -> 3.87 ms)
+  bool one_plane = true;
+  for (int64_t e = 1; e < t.nb && one_plane; ++e) one_plane = t.anchor[3 * e + 2] == t.anchor[2];
   for (int kind = 0; kind < 2; ++kind) {
-    if (eK && std::atoi(eK) != kind) continue;
+    if (eK ? std::atoi(eK) != kind : (one_plane && kind == 1)) continue;
     for (int R : {4, 8, 16}) {
       if (eR ? std::atoi(eR) != R : R == 16) continue;   // 16: opt-in (AIMX_NEAR_R=16)
       const int64_t ngrp = (nb + R - 1) / R;

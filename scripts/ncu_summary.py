@@ -87,7 +87,8 @@ def full(path, out, jpath=None, key=None):
             j = json.load(open(jpath))
         except FileNotFoundError:
             j = {}
-        ent = j.setdefault(key, {})
+        ent = {}   # per stage: the sum over its kernels (proj_xfft = gather + x forward)
+        j[key] = ent
         for d in recs:
             def num(m):
                 v = float(str(d.get(m, "0")).replace(",", ""))
@@ -95,7 +96,7 @@ def full(path, out, jpath=None, key=None):
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             stage = stage_of(d["kernel"])
             if stage:
-                ent[stage] = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+                ent[stage] = ent.get(stage, 0.0) + num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
         json.dump(j, open(jpath, "w"), indent=1)
 
 
