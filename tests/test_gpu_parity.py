@@ -451,3 +451,41 @@ def test_sweep_status_flags_nonfinite_columns():
     Y = op.sweep([1e8, 2e8, 3e8, 4e8], X)
     assert np.array_equal(op.sweep_status(Y), [0, 0, 1, 0])
     assert torch.isfinite(torch.view_as_real(Y[[0, 1, 3]])).all()
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_profiled_serial_sweep_equals_pipelined(prec):
+    """bench.py's stage breakdown runs a sweep with every stage bracketed by
+    events and its device batches on one stream (AIMX_PROFILE_SERIAL): the
+    same kernels on the same batches, so bit-identical to the pipelined sweep;
+    every stage of the S1-S5 path is bracketed at least once per batch."""
+    import torch
+    op = make_gpu_op(inp.make_mesh(1), (16, 16, 4), prec)
+    freqs = np.linspace(30e6, 450e6, 37)
+    X = to_gpu(np.stack([inp.rhs_vector(1, 90 + i, op.N) for i in range(37)]), prec)
+    a = op.sweep(freqs, X, batch=8).clone()
+    op.profile_enable(True, serial=True)
+    s = op.sweep(freqs, X, batch=8).clone()
+    prof = op.profile_read()
+    op.profile_enable(False)
+    assert torch.equal(a, s)
+    nbat = (37 + 7) // 8
+    assert prof["spectrum"][1] >= nbat and prof["interp_near"][1] >= nbat
+    assert prof["kernels"] > 0 and all(ms >= 0 for ms, n in (prof[k] for k in op.STAGES))
+
+
+def test_planar_mesh_near_rows_in_linear_order(monkeypatch):
+    """One-plane meshes group the near rows in linear anchor order (measured
+    faster than Morton on cfg5); AIMX_NEAR_ORDER still overrides, and both
+    layouts give the same operator to rounding."""
+    m = inp.make_mesh(1)
+    op = make_gpu_op(m, (16, 16, 4), "c128")
+    assert op.stats()["near_row_order"] == 0
+    monkeypatch.setenv("AIMX_NEAR_ORDER", "1")
+    op1 = make_gpu_op(m, (16, 16, 4), "c128")
+    monkeypatch.delenv("AIMX_NEAR_ORDER")
+    assert op1.stats()["near_row_order"] == 1
+    x = to_gpu(inp.rhs_vector(1, 3, op.N), "c128")
+    op.set_frequency(150e6)
+    op1.set_frequency(150e6)
+    assert rel_l2(op.matvec(x).cpu().numpy(), op1.matvec(x).cpu().numpy()) <= 1e-13
