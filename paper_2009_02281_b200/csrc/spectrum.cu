@@ -73,7 +73,10 @@ template <typename S, int L, bool SMALL = false> struct EvGeom {
   static constexpr int R1 = Fac<L>::R1, R2 = Fac<L>::R2;
   using TL = TwoLevel<R1, R2>;
   static constexpr int T = TL::T, E = TL::E;
-  static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? 4 : 1) : 0;
+  // exchange stride: 16/NL mod 16 (a half-warp of the line-fastest column
+  // mapping holds NL lines x 16/NL threads; the row mapping puts a line in
+  // one warp and is conflict-free at any stride), as matvec.cu's PassGeom
+  static constexpr int XB = R1 > 1 ? ((TL::XB + 15) / 16) * 16 + (T == 32 ? (SMALL ? 8 : 2) : 1) : 0;
   static constexpr size_t BYTES256 = sizeof(typename CT<S>::T2) * (size_t)(256 / T) * XB;
   // SMALL: 64-thread CTAs when there are few lines (more CTAs in flight)
   static constexpr int NT = SMALL ? (T > 64 ? T : 64) : (BYTES256 > 200 * 1024 ? 128 : 256);
@@ -162,8 +165,9 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* tw = reinterpret_cast<T2*>(smem_raw);
   T2* xb = tw + L + line * G::XB;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = twg[i];
-  __syncthreads();
+  // the twiddle table lands behind the samples' loads (waited on before the transform)
+  for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async(tw + i, twg + i);
+  asm volatile("cp.async.commit_group;\n" ::);
   const int64_t boff = (int64_t)blockIdx.z * noct;
   // line -> base offset and element stride
   int64_t base, stride;
@@ -218,6 +222,8 @@ __global__ void __launch_bounds__(256) k_even(int64_t nlines, int64_t inner, int
       v[i] = neg ? mk<T2>(-u.x, -u.y) : u;
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
   fft2<T2, G::R1, G::R2, false>(v, xb, tw, t);
   if (!act) return;
 #pragma unroll
