@@ -1195,6 +1195,242 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
   }
 }
 
+// S4+S5 on the tensor cores (c64 batched launches, BB = 8/16/32 columns).
+// The same chunk payload and TMA ring as k_interp_near; per row group the
+// contraction is done as  D^T[2BB x 2R] += X^T[2BB x K] . C^T[K x 2R]  with
+// mma.sync m16n8k8 tf32 (legacy tensor path, operands straight from the
+// registers the gather loads into -- no shared-memory staging):
+//   M = the 2BB real components of the batch (MT = BB/8 m16 tiles),
+//   N = C chunks: two n8 tiles, the group's R = 8 rows of the A part (C^A)
+//       and of the rho part (C^rho); W chunks: one n8 tile, the rho channel
+//       entering A as -beta_b phi^rho (beta_b is a per-M-row scale), so the
+//       tile accumulates Lambda^x,y,z . phi^x,y,z - beta_b Lambda^rho . phi^rho,
+//   K = C chunk: the chunk's union entries (8 per k-step);
+//       W chunk: (entry, channel) pairs (2 entries x 4 channels per k-step).
+// fp32 accuracy by the 3-term split  a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi
+// (a_hi = a truncated to tf32, a_lo = a - a_hi exact; the dropped a_lo b_lo
+// and the truncation of a_lo, b_lo to tf32 are ~2^-20 relative).
+// M mapping: lane (g = lane/4, t = lane%4) loads the 2MT contiguous reals
+// q = 2MT g + 2j + h of its gathered rows (one or two 16-byte loads); tile j's
+// fragment row g is q with h = 0 (the real part of column MT g + j), row
+// g + 8 is h = 1 (its imaginary part).  The accumulator fragment then holds,
+// for column b = MT g + j and rows r = 2t, 2t + 1, both parts (n tiles 0, 1)
+// re and im in one lane, so the combine y = j alpha_b (y^A - beta_b y^rho)
+// (eq:EFIEAIMx P:288) needs no shuffles; the four warps' partial sums are
+// added in a fixed order through shared memory at the group's last chunk.
+template <int MT> struct NearMma {
+  static constexpr int NT = 128, R = 8, BB = 8 * MT;
+  static constexpr int CHC = 128, CHW = 32;                 // largest chunk lengths (entries) at c64
+  static constexpr int D = kNearD, NDS = D + 1, NDD = D + 1;
+  static constexpr int STB = CHC * R * 8 + CHC * 4 + 16;    // stage: one chunk payload
+  static constexpr int KB = 2;                              // k-steps per warp batch (loads in flight)
+  static constexpr size_t OFF_RED = (size_t)NDS * STB;
+  static constexpr size_t REDB = (size_t)4 * 32 * (4 * MT + 1) * sizeof(float);   // [warp][lane][2 rows][MT][re, im]
+  static constexpr size_t OFF_DESC = (OFF_RED + REDB + 15) / 16 * 16;
+  static constexpr size_t OFF_BAR = OFF_DESC + NDD * 16;
+  static constexpr size_t OFF_NBE = OFF_BAR + NDS * 8;      // [BB] -beta_b
+  static constexpr size_t SMEM = OFF_NBE + BB * 4;
+};
+
+// a -> (hi, lo) with hi + lo = a exactly, hi a tf32 (truncated: one LOP3;
+// cvt.rna.tf32.f32 expands to five instructions on sm_100a), |lo| < 2^-10 |a|
+__device__ __forceinline__ void tf32_split(float a, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(a) & 0xffffe000u;
+  lo = __float_as_uint(a - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// the lane's 2MT contiguous reals of a gathered row (zero when !ok)
+template <int MT> struct RowV { float v[2 * MT]; };
+template <int MT>
+__device__ __forceinline__ RowV<MT> load_row(const float* p, bool ok) {
+  RowV<MT> r;
+  if constexpr (MT == 4) {
+    float4 u0 = make_float4(0.f, 0.f, 0.f, 0.f), u1 = u0;
+    if (ok) { u0 = __ldg((const float4*)p); u1 = __ldg((const float4*)p + 1); }
+    r.v[0] = u0.x; r.v[1] = u0.y; r.v[2] = u0.z; r.v[3] = u0.w;
+    r.v[4] = u1.x; r.v[5] = u1.y; r.v[6] = u1.z; r.v[7] = u1.w;
+  } else if constexpr (MT == 2) {
+    float4 u0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) u0 = __ldg((const float4*)p);
+    r.v[0] = u0.x; r.v[1] = u0.y; r.v[2] = u0.z; r.v[3] = u0.w;
+  } else {
+    float2 u0 = make_float2(0.f, 0.f);
+    if (ok) u0 = __ldg((const float2*)p);
+    r.v[0] = u0.x; r.v[1] = u0.y;
+  }
+  return r;
+}
+
+template <int MT>
+__global__ void __launch_bounds__(128, 5) k_interp_near_mma(HotDev h, const float2* __restrict__ xt, float2* __restrict__ y0,
+                                                           Combine cb) {
+  pdl_wait();
+  pdl_trigger();
+  using K = NearMma<MT>;
+  constexpr int R = K::R, BB = K::BB, KB = K::KB;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* const sdata = smem;
+  float* const red = reinterpret_cast<float*>(smem + K::OFF_RED);
+  int4* const sdesc = reinterpret_cast<int4*>(smem + K::OFF_DESC);
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = h.cta_ptr[blockIdx.x], nch = h.cta_ptr[blockIdx.x + 1] - c0;
+  if (nch <= 0) return;
+  const int4* __restrict__ chunks = reinterpret_cast<const int4*>(h.chunks) + c0;
+  const int nc = h.nc;
+  const int64_t ns = (int64_t)h.batch * nc;                       // phi node stride (complex)
+  const float* __restrict__ xr = reinterpret_cast<const float*>(xt) + 2 * MT * g;
+  const float* __restrict__ phr = reinterpret_cast<const float*>(h.phi) + 2 * MT * g;
+  // W chunks: this lane's channel t (x, y, z, rho) -> stored channel, or none
+  // (planar grids store x, y, rho: Lambda^z = 0 and phi^z is not kept)
+  const int wch = (nc == 3) ? (t == 3 ? 2 : (t == 2 ? -1 : t)) : t;
+  float* const nbe = reinterpret_cast<float*>(smem + K::OFF_NBE) + MT * g;   // -beta of the lane's columns MT g + j
+  if (tid < BB) reinterpret_cast<float*>(smem + K::OFF_NBE)[tid] = -(float)cb.beta[tid];
+  float acc[MT][2][4];
+#pragma unroll
+  for (int j = 0; j < MT; ++j)
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[j][p][i] = 0.f;
+
+  auto coef_bytes = [&](const int4& d) -> int { return d.w * R * ((d.y & 1) ? 8 : 16); };
+  auto issue = [&](int j, const int4& d) {
+    uint64_t* bj = bar + j % K::NDS;
+    const uint32_t bytes = (uint32_t)(coef_bytes(d) + ((4 * d.w + 15) & ~15) + 16);
+    sdesc[j % K::NDD] = d;
+    mbar_arrive_expect_tx(bj, bytes);
+    bulk_g2s(sdata + (j % K::NDS) * K::STB, h.payload + (int64_t)d.z * 16, bytes, bj);
+  };
+  if (tid < K::NDS) mbar_init(bar + tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  if (tid == 0)
+    for (int j = 0; j < K::D && j < nch; ++j) issue(j, chunks[j]);
+  __syncthreads();
+
+  for (int k = 0; k < nch; ++k) {
+    mbar_wait(bar + k % K::NDS, (uint32_t)(k / K::NDS) & 1u);
+    const int4 d = sdesc[k % K::NDD];
+    const unsigned char* stg = sdata + (k % K::NDS) * K::STB;
+    const int* ix = reinterpret_cast<const int*>(stg + coef_bytes(d));
+    if (tid == 0 && k + K::D < nch)
+      issue(k + K::D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
+    const bool isC = d.y & 1;
+    const int epk = isC ? 8 : 2;                           // entries per k-step
+    const int nks = (d.w + epk - 1) / epk, elast = d.w - 1;
+    for (int ks0 = wib; ks0 < nks; ks0 += 4 * KB) {
+      // gathered rows of KB k-steps, all loads before any use (k = t and t + 4).
+      // Entries past the chunk load a valid row (the last entry's) against a
+      // zero coefficient, so no load is predicated.
+      RowV<MT> ra[KB][2];
+      float bA[KB][2], bR[KB][2];
+      if (isC) {
+#pragma unroll
+        for (int q = 0; q < KB; ++q)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int e = (ks0 + 4 * q) * 8 + t + 4 * hh;
+            const int ec = min(e, elast);
+            ra[q][hh] = load_row<MT>(xr + (int64_t)ix[ec] * (2 * BB), true);
+            const float2 cv = reinterpret_cast<const float2*>(stg)[ec * R + g];
+            bA[q][hh] = e <= elast ? cv.x : 0.f;
+            bR[q][hh] = e <= elast ? cv.y : 0.f;
+          }
+      } else {
+#pragma unroll
+        for (int q = 0; q < KB; ++q)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int e = (ks0 + 4 * q) * 2 + hh;
+            const int ec = min(e, elast);
+            // planar grids: the absent z channel (t = 2) reads channel 0 against
+            // a zero weight
+            ra[q][hh] = load_row<MT>(phr + ((int64_t)ix[ec] * ns + (int64_t)max(wch, 0) * h.batch) * 2, true);
+            // the rho channel enters as -beta_b phi^rho (beta_b scales M rows), so
+            // one n tile carries y^A - beta y^rho of the W part
+            if (t == 3)
+#pragma unroll
+              for (int j = 0; j < MT; ++j) {
+                ra[q][hh].v[2 * j] *= nbe[j];
+                ra[q][hh].v[2 * j + 1] *= nbe[j];
+              }
+            const float w = reinterpret_cast<const float*>(stg)[(ec * R + g) * 4 + t];
+            bA[q][hh] = (e <= elast && wch >= 0) ? w : 0.f;
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        if (ks0 + 4 * q >= nks) break;   // warp-uniform
+        uint32_t bh[2][2], bl[2][2];   // [part][k half]
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          tf32_split(bA[q][hh], bh[0][hh], bl[0][hh]);
+          if (isC) tf32_split(bR[q][hh], bh[1][hh], bl[1][hh]);
+        }
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+          uint32_t ah[4], al[4];
+          tf32_split(ra[q][0].v[2 * j], ah[0], al[0]);       // (row g,     k = t)
+          tf32_split(ra[q][0].v[2 * j + 1], ah[1], al[1]);   // (row g + 8, k = t)
+          tf32_split(ra[q][1].v[2 * j], ah[2], al[2]);       // (row g,     k = t + 4)
+          tf32_split(ra[q][1].v[2 * j + 1], ah[3], al[3]);   // (row g + 8, k = t + 4)
+          mma_tf32(acc[j][0], al, bh[0][0], bh[0][1]);
+          mma_tf32(acc[j][0], ah, bl[0][0], bl[0][1]);
+          mma_tf32(acc[j][0], ah, bh[0][0], bh[0][1]);
+          if (isC) {   // W chunks: one n tile (rho folded into A)
+            mma_tf32(acc[j][1], al, bh[1][0], bh[1][1]);
+            mma_tf32(acc[j][1], ah, bl[1][0], bl[1][1]);
+            mma_tf32(acc[j][1], ah, bh[1][0], bh[1][1]);
+          }
+        }
+      }
+    }
+    if (d.y & 4) {   // last chunk of group d.x: combine, fixed-order reduction over the warps, store
+      // lane's outputs: column b = MT g + j, row r = 2t + hh; y^A - beta_b y^rho
+      float* rw = red + (wib * 32 + lane) * (4 * MT + 1);
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          rw[(hh * MT + j) * 2] = acc[j][0][hh] + nbe[j] * acc[j][1][hh];             // re (fragment row g)
+          rw[(hh * MT + j) * 2 + 1] = acc[j][0][2 + hh] + nbe[j] * acc[j][1][2 + hh];   // im (fragment row g + 8)
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[j][p][i] = 0.f;
+      }
+      __syncthreads();
+      const int32_t* gr = h.grp_rows + (int64_t)d.x * R;
+      // 32 lanes x 2 rows x MT columns complex outputs
+      for (int o = tid; o < 32 * 2 * MT; o += K::NT) {
+        const int ln = o / (2 * MT), jj = o % (2 * MT);   // jj = hh MT + j
+        float re = 0.f, im = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float* src = red + (w * 32 + ln) * (4 * MT + 1) + 2 * jj;
+          re += src[0];
+          im += src[1];
+        }
+        const int hh = jj / MT, j = jj % MT;
+        const int b = MT * (ln >> 2) + j, r = 2 * (ln & 3) + hh;
+        const int m = gr[r];
+        if (m >= 0 && b < cb.B) {   // (j alpha) u: re = -alpha u.im, im = alpha u.re
+          const float al = (float)cb.alpha_im[b];
+          y0[(int64_t)b * cb.ystride + m] = make_float2(-al * im, al * re);
+        }
+      }
+    }
+    __syncthreads();   // stage, descriptor and reduction slots are reused next
+  }
+}
+
 // ------------------------------------------------------------------ dispatch
 template <class K> void set_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024)
@@ -1395,6 +1631,15 @@ void launch_interp(const HotDev& h, const void* xt, void* y0, void* y1, const Co
   AIMX_CHECK_LAUNCH();
 }
 
+template <int MT>
+void launch_interp_mma(const HotDev& h, void* y0, const Combine& c, cudaStream_t s) {
+  using K = NearMma<MT>;
+  set_smem(k_interp_near_mma<MT>, K::SMEM);
+  launch_pdl(k_interp_near_mma<MT>, dim3((unsigned)h.near_ctas), dim3(K::NT), K::SMEM, s, h, (const float2*)h.xt,
+             (float2*)y0, c);
+  AIMX_CHECK_LAUNCH();
+}
+
 template <typename T, int R>
 void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   (void)x;
@@ -1404,6 +1649,20 @@ void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Comb
     return;
   }
   if (c.mode != 0) throw Error(AIMX_E_INTERNAL, "batched parts not supported");
+  if constexpr (sizeof(T) == 4 && R == 8) {   // c64, 8 to 32 columns: the tensor-core kernel (opt-in)
+    // opt-in (AIMX_NEAR_MMA=1, read per call): measured slower than the FMA
+    // kernel on B200 (legacy HMMA issue rate, 3-term split)
+    const char* mm = std::getenv("AIMX_NEAR_MMA");
+    const int bb = batch_bucket(c.B);
+    if (mm && mm[0] == '1' && bb >= 8) {
+      switch (bb) {
+        case 8: launch_interp_mma<1>(h, y0, c, s); break;
+        case 16: launch_interp_mma<2>(h, y0, c, s); break;
+        default: launch_interp_mma<4>(h, y0, c, s); break;
+      }
+      return;
+    }
+  }
   switch (batch_bucket(c.B)) {   // xt: interleaved by run_interleave earlier in the matvec
     case 2: launch_interp<T, R, 2, false>(h, h.xt, y0, y1, c, s); break;
     case 4: launch_interp<T, R, 4, false>(h, h.xt, y0, y1, c, s); break;
