@@ -433,6 +433,10 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   // one wave of resident CTAs (AIMX_NEAR_SMS: spread over fewer SMs, experiments)
   int nsm_near = nsm;
   if (const char* e = std::getenv("AIMX_NEAR_SMS")) nsm_near = std::max(1, std::min(nsm, std::atoi(e)));
+  // AIMX_NEAR_MMA=1: batched c64 launches on the legacy tensor path (measured
+  // slower; the same chunk layout and 5 CTAs per SM)
+  const char* mm = std::getenv("AIMX_NEAR_MMA");
+  h.near_mma = (f32 && grp.R == 8 && mm && mm[0] == '1') ? 1 : 0;
   int per_sm = near_ctas_per_sm(f32, false, grp.R);   // AIMX_NEAR_PER_SM: fewer (experiments)
   if (const char* e = std::getenv("AIMX_NEAR_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
   const int ncta = per_sm * nsm_near;

@@ -1322,8 +1322,7 @@ __global__ void __launch_bounds__(128, 5) k_interp_near_mma(HotDev h, const floa
     if (tid == 0 && k + K::D < nch)
       issue(k + K::D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
     const bool isC = d.y & 1;
-    const int epk = isC ? 8 : 2;                           // entries per k-step
-    const int nks = (d.w + epk - 1) / epk, elast = d.w - 1;
+    const int nks = isC ? (d.w + 7) >> 3 : (d.w + 1) >> 1, elast = d.w - 1;   // k-steps: 8 / 2 entries
     for (int ks0 = wib; ks0 < nks; ks0 += 4 * KB) {
       // gathered rows of KB k-steps, all loads before any use (k = t and t + 4).
       // Entries past the chunk load a valid row (the last entry's) against a
@@ -1650,11 +1649,10 @@ void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Comb
   }
   if (c.mode != 0) throw Error(AIMX_E_INTERNAL, "batched parts not supported");
   if constexpr (sizeof(T) == 4 && R == 8) {   // c64, 8 to 32 columns: the tensor-core kernel (opt-in)
-    // opt-in (AIMX_NEAR_MMA=1, read per call): measured slower than the FMA
-    // kernel on B200 (legacy HMMA issue rate, 3-term split)
-    const char* mm = std::getenv("AIMX_NEAR_MMA");
+    // opt-in (AIMX_NEAR_MMA=1 at setup): measured slower than the FMA kernel on
+    // B200 (legacy HMMA issue rate, 3-term split)
     const int bb = batch_bucket(c.B);
-    if (mm && mm[0] == '1' && bb >= 8) {
+    if (h.near_mma && bb >= 8) {
       switch (bb) {
         case 8: launch_interp_mma<1>(h, y0, c, s); break;
         case 16: launch_interp_mma<2>(h, y0, c, s); break;

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _mma_on(monkeypatch):
-    monkeypatch.setenv("AIMX_NEAR_MMA", "1")   # read by the library per call
+    monkeypatch.setenv("AIMX_NEAR_MMA", "1")   # read by the library at setup
 
 
 def _sweep_vs_oracle(mesh, n, freqs, batches, seed):
