@@ -1,4 +1,5 @@
-"""Where the end-to-end sweep (aimx_sweep_host) spends its time on cfg2:
+"""Where the end-to-end sweep (aimx_sweep_host) spends its time on cfg
+$E2E_CFG (default 2):
 copies alone (H2D, D2H, both), the device-resident sweep, and the host sweep
 wall time, each averaged over a few repetitions.  Prints one JSON line."""
 import json
@@ -14,11 +15,12 @@ import torch  # noqa: E402
 import aimx_inputs as inp  # noqa: E402
 from paper_2009_02281_b200 import AIMx  # noqa: E402
 
-c = inp.get_config(2)
-m = inp.make_mesh(2)
-op = AIMx(m.vertices, m.triangles, c.grid_n, prec="c64")
+CFG = int(os.environ.get("E2E_CFG", "2"))
+c = inp.get_config(CFG)
+m = inp.make_mesh(CFG)
+op = AIMx(m.vertices, m.triangles, c.grid_n, order=c.order, near_cells=c.near_cells, prec="c64")
 freqs = c.freqs
-Xh = torch.from_numpy(inp.rhs_matrix(2, op.N, np.arange(len(freqs)))).to(torch.complex64).pin_memory()
+Xh = torch.from_numpy(inp.rhs_matrix(CFG, op.N, np.arange(len(freqs)))).to(torch.complex64).pin_memory()
 Yh = torch.empty_like(Xh).pin_memory()
 X = Xh.cuda()
 Y = torch.empty_like(X)
