@@ -259,9 +259,19 @@ class DirectK:
 
 
 # ---------------------------------------------------------------- AIMx for K
-def gradient_kernel_samples(n: tuple, h: float, k0: float | None):
+def gH00_literal(k0: float) -> complex:
+    """eq:gH00 as printed: (-j k0)^2 / (4 pi 2!).  It is the coefficient
+    of rhat in the r -> 0 limit of grad G_d (eq:ghgftaylor P:429), not a value
+    of the vector kernel; the default reading R23 uses 0 (the average over
+    +-rhat).  Kept behind gh00="literal" (AMB-16)."""
+    return (-1j * k0) ** 2 / (FOUR_PI * 2.0)
+
+
+def gradient_kernel_samples(n: tuple, h: float, k0: float | None, gh00: str = "zero"):
     """H_grad,a on the padded grid [2Nz, 2Ny, 2Nx] (wrap slot 0, R10): d_a G at
-    r = h * offset (k0 None: the static kernel).  Returns [3, ...] (a = x, y, z)."""
+    r = h * offset (k0 None: the static kernel).  Returns [3, ...] (a = x, y, z).
+    gh00: self term H_grad,a(0): "zero" (R23), or "literal" (eq:gH00's scalar in
+    every component)."""
     offs = []
     wrap = []
     for N in (n[2], n[1], n[0]):
@@ -273,17 +283,22 @@ def gradient_kernel_samples(n: tuple, h: float, k0: float | None):
     rv = h * np.stack([ox, oy, oz], axis=-1).astype(np.float64)
     g = grad_G_s(rv) if k0 is None else grad_G(k0, rv)
     g[wz | wy | wx] = 0.0
+    if gh00 == "literal" and k0 is not None:
+        g[0, 0, 0, :] = gH00_literal(k0)
+    elif gh00 != "zero":
+        raise ValueError(f"gh00 must be 'zero' or 'literal', not {gh00!r}")
     return np.moveaxis(g, -1, 0)
 
 
-def grid_K(op, x, k0: float):
-    """-sum_c W^c sum_{a,b} eps_cab (H_grad,a (*) P^b x) on the op's grid."""
+def grid_K(op, x, k0: float, gh00: str = "zero"):
+    """-sum_c W^c sum_{a,b} eps_cab (H_grad,a (*) P^b x) on the op's grid
+    (gh00: the self-term reading, see gradient_kernel_samples)."""
     import scipy.fft as sfft
     Nx, Ny, Nz = op.grid.n
     g = np.stack([(op.P[b] @ x).reshape(Nz, Ny, Nx) for b in range(3)])
     from .convolution import WORKERS
     G = sfft.fftn(g, s=(2 * Nz, 2 * Ny, 2 * Nx), axes=(-3, -2, -1), workers=WORKERS)
-    Hh = sfft.fftn(gradient_kernel_samples(op.grid.n, op.grid.h, k0), axes=(-3, -2, -1), workers=WORKERS)
+    Hh = sfft.fftn(gradient_kernel_samples(op.grid.n, op.grid.h, k0, gh00), axes=(-3, -2, -1), workers=WORKERS)
     y = np.zeros(op.N, np.complex128)
     for c in range(3):
         acc = np.zeros_like(G[0])

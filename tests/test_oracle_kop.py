@@ -10,15 +10,19 @@ SURVEY 8(f) NEXT #1 groundwork, oracle only this round).
 * the residue term: antisymmetric, zero on the diagonal;
 * K_s,P against the dense definition with explicit grid matrices;
 * the grid convolution against the dense O(N_g^2) sum;
-* AIMx K against the dense direct K on a closed icosphere (rel-L2 <= 1e-2).
+* AIMx K against the dense direct K on a closed icosphere (rel-L2 <= 1e-2);
+* eq:gH00's printed scalar is the coefficient of rhat in the r -> 0 limit of
+  grad G_d (so the vector self term is direction dependent and its +-rhat
+  average, reading R23's 0, is the symmetric value); the gh00="literal" flag
+  changes the grid K by exactly the self term's contribution.
 """
 import numpy as np
 import pytest
 
 import aimx_inputs as inp
 from oracle.kernels import G
-from oracle.kop import (EPS3, AIMxK, DirectK, K_precorrection_entries, grad_G, grad_G_d, grad_G_s, grid_K,
-                        residue_entries, static_K_entries, triangle_Q)
+from oracle.kop import (EPS3, AIMxK, DirectK, K_precorrection_entries, gH00_literal, grad_G, grad_G_d, grad_G_s,
+                        grid_K, residue_entries, static_K_entries, triangle_Q)
 
 
 @pytest.fixture(scope="module")
@@ -212,3 +216,41 @@ def test_rows_variants_equal_the_full_operators(sph):
     yE, yH = pmchwt_rows(op, kr, 120e6, 4.0, x2)
     assert np.linalg.norm(yE - y[rows]) <= 1e-12 * np.linalg.norm(y[rows])
     assert np.linalg.norm(yH - y[op.N + rows]) <= 1e-12 * np.linalg.norm(y[op.N + rows])
+
+
+@pytest.mark.parametrize("k0", [1.0, 7.5])
+def test_gH00_printed_scalar_is_the_rhat_coefficient_of_the_limit(k0):
+    """eq:gH00: (-j k0)^2 / (4 pi 2!) = lim_{r->0} grad G_d . rhat for
+    every direction (eq:ghgftaylor's second term), while grad G_d itself tends
+    to that scalar times rhat: opposite directions give opposite vectors, so
+    the only direction-free value is their average, 0 (reading R23)."""
+    s = gH00_literal(k0)
+    assert np.isclose(s, -k0 * k0 / (8 * np.pi), rtol=1e-15, atol=0)
+    rng = np.random.default_rng(5)
+    for _ in range(5):
+        rhat = rng.standard_normal(3)
+        rhat /= np.linalg.norm(rhat)
+        for eps in (1e-4, 1e-5):
+            g = grad_G_d(k0, eps * rhat)
+            assert np.allclose(g, s * rhat, rtol=10 * (k0 * eps), atol=0)
+            gm = grad_G_d(k0, -eps * rhat)
+            assert np.allclose(0.5 * (g + gm), 0.0, atol=abs(s) * 10 * (k0 * eps))
+
+
+def test_grid_K_literal_gH00_flag_adds_exactly_the_self_term(sph):
+    """gh00="literal" puts eq:gH00's scalar in every component of H_grad(0):
+    Phi_c gains s sum_{a,b} eps_cab g_b, so y changes by
+    -sum_c P_c^T (s sum_{a,b} eps_cab P_b x)."""
+    op = sph
+    k0 = 2 * np.pi * 3e8 / 299792458.0
+    x = np.random.default_rng(9).standard_normal(op.N) * (1 - 0.25j)
+    d = grid_K(op, x, k0, gh00="literal") - grid_K(op, x, k0)
+    s = gH00_literal(k0)
+    gb = [op.P[b] @ x for b in range(3)]
+    ref = np.zeros(op.N, complex)
+    for c in range(3):
+        phi = sum(EPS3[c, a, b] * s * gb[b] for a in range(3) for b in range(3) if EPS3[c, a, b])
+        ref -= op.P[c].T @ phi
+    assert np.linalg.norm(d - ref) <= 1e-10 * np.linalg.norm(ref)
+    with pytest.raises(ValueError):
+        grid_K(op, x, k0, gh00="half")
