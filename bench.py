@@ -429,6 +429,23 @@ def roofline_of(st, prec, prof_all, prof, dom, cols_per_launch, cfg):
                 "note": "achieved/frac: the kernel's launches bracketed live in the timed (pipelined) steps, "
                         "where it shares the GPU with the next batch's grid stages; *_serial: the same "
                         "launches in the one-stream breakdown step (its own time)"}
+    if dom == "interp_near":
+        # S4+S5 is bound by the FP32 pipe, not by HBM (DESIGN 7): the same
+        # launch against the FP32 FMA peak, 148 SMs x 128 lanes x 2 flop x
+        # clocks.max.sm 1965 MHz (B200_PROFILING.md unit counts and clock).
+        # Algorithmic flops per column: a near pair is 2 real coefficients x a
+        # complex x (4 real FMA), a stencil node of a testing function nc real
+        # weights x a complex potential (2 nc real FMA).
+        nc = st.get("grid_channels", 4)
+        p3 = (st["order"] + 1) ** 3
+        fl = 2.0 * cols_per_launch * (4 * st["nnz"] + 2 * nc * st["num_unknowns"] * p3)
+        pk = 148 * 128 * 2 * 1.965e9 / 1e12
+        roofline["alu"] = {"bound": "alu", "unit": "TFLOP/s", "peak": pk,
+                           "algorithmic_flops_per_launch": fl,
+                           "achieved": fl / (dms / dn * 1e-3) / 1e12,
+                           "frac": fl / (dms / dn * 1e-3) / 1e12 / pk,
+                           "frac_serial": fl / (sms / sn * 1e-3) / 1e12 / pk,
+                           "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1965 MHz (guide)"}
     return roofline, stages, sb
 
 
