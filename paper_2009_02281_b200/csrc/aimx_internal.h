@@ -318,6 +318,7 @@ struct HotDev {
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)
   int R = 8;                     // rows per group
+  int near1_old = 0;            // 1: single-column c64 launches keep the entry-per-lane kernel (AIMX_NEAR1_OLD=1 at setup; A/B)
   int near_mma = 0;              // 1: batched c64 launches take the tensor-core kernel (AIMX_NEAR_MMA=1 at setup)
   int ngrp = 0;
   int32_t* grp_rows = nullptr;   // [ngrp][R]

@@ -1045,22 +1045,16 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
     for (int j = 0; j < D && j < nch; ++j) issue(j, chunks[j]);
   __syncthreads();
 
-  VT buf[K::NBUF];
-  for (int k = 0; k < nch; ++k) {
-    // chunk k's payload (with the descriptor of chunk k + D) has landed
-    mbar_wait(bar + k % K::NDS, (uint32_t)(k / K::NDS) & 1u);
-    const int4 d = sdesc[k % K::NDD];
-    const unsigned char* stg = sdata + (k % K::NDS) * K::STB;
+  // gathered rows of a landed chunk into registers (all loads issued before any
+  // use): C: x rows of entries lgid + i NLG; W: the 4 channel rows of entries
+  // lgid + i NLG
+  auto gather = [&](const int4& d, const unsigned char* stg, VT* b) {
     const int* ix = reinterpret_cast<const int*>(stg + coef_bytes(d));
-    if (tid == 0 && k + D < nch)
-      issue(k + D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
-    // gathered rows into registers (all loads issued before any use): C: x rows
-    // of entries lgid + i NLG; W: the 4 channel rows of entries lgid + i NLG
     if (d.y & 1) {
 #pragma unroll
       for (int i = 0; i < K::NPC; ++i) {
         const int e = lgid + i * NLG;
-        if (e < d.w) buf[i] = __ldg((const VT*)(xr + (int64_t)ix[e] * BB));
+        if (e < d.w) b[i] = __ldg((const VT*)(xr + (int64_t)ix[e] * BB));
       }
     } else {
 #pragma unroll
@@ -1070,9 +1064,37 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
           const T2* pr = phi + (int64_t)ix[e] * ns;
 #pragma unroll
           for (int c = 0; c < 4; ++c)   // nc = 3: phi_z is not stored (Lambda^z = 0), slot 2 holds rho
-            if (c < nc) buf[4 * i + c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
+            if (c < nc) b[4 * i + c] = __ldg((const VT*)(pr + (int64_t)c * h.batch));
         }
       }
+    }
+  };
+  // Single column (few registers per lane): the rows of chunk k + 1 are
+  // gathered while chunk k computes, so their L2 latency is off the per-chunk
+  // chain (wait -> indices -> gather -> arithmetic -> block barrier).
+  constexpr bool PRE = BB == 1;
+  VT buf[K::NBUF];
+  [[maybe_unused]] VT nbuf[PRE ? K::NBUF : 1];
+  if constexpr (PRE) {
+    mbar_wait(bar, 0u);
+    gather(sdesc[0], sdata, nbuf);
+  }
+  for (int k = 0; k < nch; ++k) {
+    // chunk k's payload (with the descriptor of chunk k + D) has landed
+    if constexpr (!PRE) mbar_wait(bar + k % K::NDS, (uint32_t)(k / K::NDS) & 1u);
+    const int4 d = sdesc[k % K::NDD];
+    const unsigned char* stg = sdata + (k % K::NDS) * K::STB;
+    if (tid == 0 && k + D < nch)
+      issue(k + D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
+    if constexpr (PRE) {
+#pragma unroll
+      for (int i = 0; i < K::NBUF; ++i) buf[i] = nbuf[i];
+      if (k + 1 < nch) {
+        mbar_wait(bar + (k + 1) % K::NDS, (uint32_t)((k + 1) / K::NDS) & 1u);
+        gather(sdesc[(k + 1) % K::NDD], sdata + ((k + 1) % K::NDS) * K::STB, nbuf);
+      }
+    } else {
+      gather(d, stg, buf);
     }
     if (d.y & 1) {   // near correction: pairs [e][R]
       const T2* __restrict__ cf = (const T2*)stg;
@@ -1187,6 +1209,191 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
             T* yy = reinterpret_cast<T*>(y0 + (int64_t)b * cb.ystride + m);
             if (comp == 0) yy[1] = al * sum;
             else yy[0] = -al * sum;
+          }
+        }
+      }
+    }
+    __syncthreads();   // stage and descriptor slots of chunk k are refilled next
+  }
+}
+
+// S4+S5, ONE column, c64, R = 8 rows per group (the single matvec of a GMRES
+// iteration: HBM-bound on the coefficient stream).  The same chunk payload
+// and TMA ring as k_interp_near, but the lanes split an entry's rows instead
+// of taking one entry each: C chunks: 4 lanes per entry, lane q reads the
+// 16-byte word of rows 2q, 2q+1 ((C_A, C_rho) pairs); W chunks: 8 lanes per
+// entry, lane r reads row r's real4 weight.  Consecutive lanes read consecutive
+// 16-byte words of the stage, so the shared-memory reads are conflict-free
+// (one entry per lane strides them by 64 / 128 bytes: 4- / 8-way conflicts,
+// the shared pipe at 65% and the limiter, profiles/r2h_near1.md), every
+// thread has work on the short chunks of 32-slot contexts, and a group ends
+// with 16 shuffles per lane instead of 80.  The gathered x / potential values
+// of chunk k + 1 load while chunk k computes.
+template <bool PARTS>
+__global__ void __launch_bounds__(128, 5)
+    k_interp_near1(HotDev h, const float2* __restrict__ xt, float2* __restrict__ y0, float2* __restrict__ y1,
+                   Combine cb) {
+  pdl_wait();
+  pdl_trigger();
+  using K = NearCfg<float, 8, 1, PARTS>;
+  constexpr int R = 8, NT = K::NT, D = K::D, NP = PARTS ? 2 : 1;
+  constexpr int PC = K::CHC / 32;   // C passes: 32 entries per pass
+  constexpr int PW = K::CHW / 16;   // W passes: 16 entries per pass
+  constexpr int NB = PC > 4 * PW ? PC : 4 * PW;
+  static_assert(K::CHC % 32 == 0 && K::CHW % 16 == 0 && NT == 128, "lane mapping");
+  static_assert(K::REDB >= (size_t)(NT / 32) * NP * R * sizeof(float2), "partial sums");
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* const sdata = smem;                                         // [NDS][STB]
+  float2* const red = reinterpret_cast<float2*>(smem + K::OFF_RED);          // [warp][part][R]
+  int4* const sdesc = reinterpret_cast<int4*>(smem + K::OFF_DESC);           // [NDD]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);      // [NDS]
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  const int c0 = h.cta_ptr1[blockIdx.x], nch = h.cta_ptr1[blockIdx.x + 1] - c0;
+  if (nch <= 0) return;
+  const int4* __restrict__ chunks = reinterpret_cast<const int4*>(h.chunks) + c0;
+  const int nc = h.nc;                            // stored channels: 4, or 3 (x, y, rho) on planar grids
+  const int64_t ns = (int64_t)h.batch * nc;       // phi node stride (complex): [node][channel][slot]
+  const float2* __restrict__ phi = (const float2*)h.phi;
+  const float be = PARTS ? 0.f : (float)cb.beta[0];
+
+  auto coef_bytes = [&](const int4& d) -> int { return d.w * R * ((d.y & 1) ? 8 : 16); };
+  auto issue = [&](int j, const int4& d) {   // as in k_interp_near
+    uint64_t* bj = bar + j % K::NDS;
+    const uint32_t bytes = (uint32_t)(coef_bytes(d) + ((4 * d.w + 15) & ~15) + 16);
+    sdesc[j % K::NDD] = d;
+    mbar_arrive_expect_tx(bj, bytes);
+    bulk_g2s(sdata + (j % K::NDS) * K::STB, h.payload + (int64_t)d.z * 16, bytes, bj);
+  };
+  if (tid < K::NDS) mbar_init(bar + tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  if (tid == 0)
+    for (int j = 0; j < D && j < nch; ++j) issue(j, chunks[j]);
+  __syncthreads();
+
+  const int ec = tid >> 2, qc = tid & 3;   // C: entry of pass 0, row pair
+  const int ew = tid >> 3, rw = tid & 7;   // W: entry of pass 0, row
+  auto gather = [&](const int4& d, const unsigned char* stg, float2* b) {
+    const int* ix = reinterpret_cast<const int*>(stg + coef_bytes(d));
+    if (d.y & 1) {
+#pragma unroll
+      for (int i = 0; i < PC; ++i) {
+        const int e = ec + 32 * i;
+        if (e < d.w) b[i] = __ldg(xt + ix[e]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < PW; ++i) {
+        const int e = ew + 16 * i;
+        if (e < d.w) {
+          const float2* pr = phi + (int64_t)ix[e] * ns;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)   // nc = 3: phi_z is not stored (Lambda^z = 0), slot 2 holds rho
+            if (c < nc) b[4 * i + c] = __ldg(pr + (int64_t)c * h.batch);
+        }
+      }
+    }
+  };
+
+  float2 aC[2 * NP], aW[NP];   // C: [part][row 2 qc + j]; W: [part] of row rw
+#pragma unroll
+  for (int j = 0; j < 2 * NP; ++j) aC[j] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < NP; ++j) aW[j] = make_float2(0.f, 0.f);
+  float2 buf[NB], nbuf[NB];
+  mbar_wait(bar, 0u);
+  gather(sdesc[0], sdata, nbuf);
+  for (int k = 0; k < nch; ++k) {
+    const int4 d = sdesc[k % K::NDD];
+    const unsigned char* stg = sdata + (k % K::NDS) * K::STB;
+    if (tid == 0 && k + D < nch)
+      issue(k + D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
+#pragma unroll
+    for (int i = 0; i < NB; ++i) buf[i] = nbuf[i];
+    if (k + 1 < nch) {
+      mbar_wait(bar + (k + 1) % K::NDS, (uint32_t)((k + 1) / K::NDS) & 1u);
+      gather(sdesc[(k + 1) % K::NDD], sdata + ((k + 1) % K::NDS) * K::STB, nbuf);
+    }
+    if (d.y & 1) {   // near correction: [e][R] (C_A, C_rho) pairs
+      const float4* __restrict__ cf = reinterpret_cast<const float4*>(stg);
+#pragma unroll
+      for (int i = 0; i < PC; ++i) {
+        const int e = ec + 32 * i;
+        if (e >= d.w) break;
+        const float4 f = cf[e * 4 + qc];
+        const float2 x = buf[i];
+        if constexpr (PARTS) {
+          axpy(aC[0], f.x, x);
+          axpy(aC[2], f.y, x);
+          axpy(aC[1], f.z, x);
+          axpy(aC[3], f.w, x);
+        } else {
+          axpy(aC[0], f.x - be * f.y, x);
+          axpy(aC[1], f.z - be * f.w, x);
+        }
+      }
+    } else {         // interpolation: [e][R] real4 weights
+      const float4* __restrict__ wf = reinterpret_cast<const float4*>(stg);
+#pragma unroll
+      for (int i = 0; i < PW; ++i) {
+        const int e = ew + 16 * i;
+        if (e >= d.w) break;
+        const float4 w = wf[e * 8 + rw];
+        axpy(aW[0], w.x, buf[4 * i]);
+        axpy(aW[0], w.y, buf[4 * i + 1]);
+        if (nc == 4) axpy(aW[0], w.z, buf[4 * i + 2]);
+        const float2 rho = nc == 4 ? buf[4 * i + 3] : buf[4 * i + 2];
+        if constexpr (PARTS) axpy(aW[1], w.w, rho);
+        else axpy(aW[0], -be * w.w, rho);
+      }
+    }
+    if (d.y & 4) {   // last chunk of group d.x: fixed-order reduction + combine
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < 2 * NP; ++j) {
+          aC[j].x += __shfl_xor_sync(0xffffffffu, aC[j].x, o);
+          aC[j].y += __shfl_xor_sync(0xffffffffu, aC[j].y, o);
+        }
+#pragma unroll
+      for (int o = 8; o < 32; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          aW[j].x += __shfl_xor_sync(0xffffffffu, aW[j].x, o);
+          aW[j].y += __shfl_xor_sync(0xffffffffu, aW[j].y, o);
+        }
+      // row r = lane (< 8): its C sums sit in lanes with qc = r >> 1, slot r & 1
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const int src = (lane >> 1) & 3;
+        const float a0x = __shfl_sync(0xffffffffu, aC[2 * p].x, src), a0y = __shfl_sync(0xffffffffu, aC[2 * p].y, src);
+        const float a1x = __shfl_sync(0xffffffffu, aC[2 * p + 1].x, src), a1y = __shfl_sync(0xffffffffu, aC[2 * p + 1].y, src);
+        if (lane < R)
+          red[(wib * NP + p) * R + lane] =
+              make_float2(aW[p].x + ((lane & 1) ? a1x : a0x), aW[p].y + ((lane & 1) ? a1y : a0y));
+      }
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) aC[j] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) aW[j] = make_float2(0.f, 0.f);
+      __syncthreads();
+      if (tid < NP * R) {
+        const int p = tid / R, r = tid % R;
+        float2 sum = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) {
+          const float2 v = red[(w * NP + p) * R + r];
+          sum.x += v.x;
+          sum.y += v.y;
+        }
+        const int m = h.grp_rows[(int64_t)d.x * R + r];
+        if (m >= 0) {
+          if constexpr (PARTS) {
+            float2* y = p ? y1 : y0;
+            if (y) y[m] = p ? make_float2(-sum.x, -sum.y) : sum;
+          } else {   // (j alpha) u: re = -alpha u.im, im = alpha u.re
+            const float al = (float)cb.alpha_im[0];
+            y0[m] = make_float2(-al * sum.y, al * sum.x);
           }
         }
       }
@@ -1643,6 +1850,23 @@ template <typename T, int R>
 void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Combine& c, cudaStream_t s) {
   (void)x;
   if (c.B == 1) {   // single column, staged in xt by run_interleave
+    if constexpr (sizeof(T) == 4 && R == 8) {   // c64: rows split over lanes
+      if (!h.near1_old) {
+        using K = NearCfg<float, 8, 1, false>;
+        using KP = NearCfg<float, 8, 1, true>;
+        if (c.mode == 1) {
+          set_smem(k_interp_near1<true>, KP::SMEM);
+          launch_pdl(k_interp_near1<true>, dim3((unsigned)h.near_ctas1), dim3(KP::NT), KP::SMEM, s, h,
+                     (const float2*)h.xt, (float2*)y0, (float2*)y1, c);
+        } else {
+          set_smem(k_interp_near1<false>, K::SMEM);
+          launch_pdl(k_interp_near1<false>, dim3((unsigned)h.near_ctas1), dim3(K::NT), K::SMEM, s, h,
+                     (const float2*)h.xt, (float2*)y0, (float2*)y1, c);
+        }
+        AIMX_CHECK_LAUNCH();
+        return;
+      }
+    }
     if (c.mode == 1) launch_interp<T, R, 1, true>(h, h.xt, y0, y1, c, s);
     else launch_interp<T, R, 1, false>(h, h.xt, y0, y1, c, s);
     return;
