@@ -318,6 +318,7 @@ struct HotDev {
   uint8_t* zocc = nullptr;       // [Nz] plane occupied
   // near matrix C = L_s,NR - L_s,P in row-group form (NearGroups)
   int R = 8;                     // rows per group
+  int near_half = 0;            // 1: the payload's chunks are half length (32-slot contexts: near_chc / near_chw)
   int near1_old = 0;            // 1: single-column c64 launches keep the entry-per-lane kernel (AIMX_NEAR1_OLD=1 at setup; A/B)
   int near_mma = 0;              // 1: batched c64 launches take the tensor-core kernel (AIMX_NEAR_MMA=1 at setup)
   int ngrp = 0;

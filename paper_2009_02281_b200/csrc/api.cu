@@ -437,6 +437,7 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   // slower; the same chunk layout and 5 CTAs per SM)
   const char* mm = std::getenv("AIMX_NEAR_MMA");
   h.near_mma = (f32 && grp.R == 8 && mm && mm[0] == '1') ? 1 : 0;
+  h.near_half = c->slots >= 32 ? 1 : 0;
   { const char* o1 = getenv("AIMX_NEAR1_OLD"); h.near1_old = (o1 && o1[0] == '1') ? 1 : 0; }
   int per_sm = near_ctas_per_sm(f32, false, grp.R);   // AIMX_NEAR_PER_SM: fewer (experiments)
   if (const char* e = std::getenv("AIMX_NEAR_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));

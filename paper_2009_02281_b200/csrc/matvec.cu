@@ -1229,7 +1229,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
 // thread has work on the short chunks of 32-slot contexts, and a group ends
 // with 16 shuffles per lane instead of 80.  The gathered x / potential values
 // of chunk k + 1 load while chunk k computes.
-template <bool PARTS>
+template <bool PARTS, bool HALF>
 __global__ void __launch_bounds__(128, 5)
     k_interp_near1(HotDev h, const float2* __restrict__ xt, float2* __restrict__ y0, float2* __restrict__ y1,
                    Combine cb) {
@@ -1237,8 +1237,10 @@ __global__ void __launch_bounds__(128, 5)
   pdl_trigger();
   using K = NearCfg<float, 8, 1, PARTS>;
   constexpr int R = 8, NT = K::NT, D = K::D, NP = PARTS ? 2 : 1;
-  constexpr int PC = K::CHC / 32;   // C passes: 32 entries per pass
-  constexpr int PW = K::CHW / 16;   // W passes: 16 entries per pass
+  // HALF: the context holds 32 batch slots, its payload chunks are half length
+  // (near_chc / near_chw)
+  constexpr int PC = K::CHC / 32 / (HALF ? 2 : 1);   // C passes: 32 entries per pass
+  constexpr int PW = K::CHW / 16 / (HALF ? 2 : 1);   // W passes: 16 entries per pass
   constexpr int NB = PC > 4 * PW ? PC : 4 * PW;
   static_assert(K::CHC % 32 == 0 && K::CHW % 16 == 0 && NT == 128, "lane mapping");
   static_assert(K::REDB >= (size_t)(NT / 32) * NP * R * sizeof(float2), "partial sums");
@@ -1300,6 +1302,8 @@ __global__ void __launch_bounds__(128, 5)
   for (int j = 0; j < 2 * NP; ++j) aC[j] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int j = 0; j < NP; ++j) aW[j] = make_float2(0.f, 0.f);
+  // (swapping two register buffers in a loop unrolled by two instead of the
+  // copy was measured slower: cfg3 0.091 -> 0.099 ms)
   float2 buf[NB], nbuf[NB];
   mbar_wait(bar, 0u);
   gather(sdesc[0], sdata, nbuf);
@@ -1854,15 +1858,14 @@ void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Comb
       if (!h.near1_old) {
         using K = NearCfg<float, 8, 1, false>;
         using KP = NearCfg<float, 8, 1, true>;
-        if (c.mode == 1) {
-          set_smem(k_interp_near1<true>, KP::SMEM);
-          launch_pdl(k_interp_near1<true>, dim3((unsigned)h.near_ctas1), dim3(KP::NT), KP::SMEM, s, h,
-                     (const float2*)h.xt, (float2*)y0, (float2*)y1, c);
-        } else {
-          set_smem(k_interp_near1<false>, K::SMEM);
-          launch_pdl(k_interp_near1<false>, dim3((unsigned)h.near_ctas1), dim3(K::NT), K::SMEM, s, h,
-                     (const float2*)h.xt, (float2*)y0, (float2*)y1, c);
-        }
+        auto go = [&](auto kern, size_t smem) {
+          set_smem(kern, smem);
+          launch_pdl(kern, dim3((unsigned)h.near_ctas1), dim3(K::NT), smem, s, h, (const float2*)h.xt, (float2*)y0,
+                     (float2*)y1, c);
+        };
+        const bool half = h.near_half != 0;   // near_chc / near_chw of this context's payload
+        if (c.mode == 1) half ? go(k_interp_near1<true, true>, KP::SMEM) : go(k_interp_near1<true, false>, KP::SMEM);
+        else half ? go(k_interp_near1<false, true>, K::SMEM) : go(k_interp_near1<false, false>, K::SMEM);
         AIMX_CHECK_LAUNCH();
         return;
       }
