@@ -208,6 +208,8 @@ constexpr int kMaxBatch = 32;
 
 // CTAs per SM of the S4+S5 kernel (its register budget, __launch_bounds__)
 constexpr int near_ctas_per_sm(bool f32, bool single, int R = 8) { return R >= 16 ? 3 : (f32 ? 5 : 4); }
+// CTAs per SM of the single-column c64 kernel (k_interp_near1; HALF: half-length chunks, 64 registers)
+constexpr int near1_ctas_per_sm(bool half) { return half ? 8 : 5; }
 // S4+S5 chunk lengths (entries) in the payload: C chunks 1024 / s, W chunks
 // 256 / s, halved when the context holds 32 batch slots (the 32-column kernel
 // keeps the same registers per lane)

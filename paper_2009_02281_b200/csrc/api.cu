@@ -462,6 +462,23 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
   h.near_ctas = (int)cp.size() - 1;
   h.cta_ptr1 = h.cta_ptr;   // single-column launches: the same order and CTAs
   h.near_ctas1 = h.near_ctas;
+  if (f32 && grp.R == 8 && h.near_half && !h.near1_old && !std::getenv("AIMX_NEAR_PER_SM")) {
+    // k_interp_near1 keeps 8 CTAs per SM resident on half-length chunks: the
+    // same chunk stream cut into that many contiguous ranges of whole groups
+    // with equal chunk counts
+    const int n1 = near1_ctas_per_sm(true) * nsm_near;
+    std::vector<int32_t> gb((size_t)grp.ngrp + 1);   // first chunk of each group in payload order
+    for (int64_t i = 0; i < grp.ngrp; ++i) gb[(size_t)i] = (int32_t)ck.gfirst[order[(size_t)i]];
+    gb.back() = (int32_t)ck.nchunk;
+    if (!std::is_sorted(gb.begin(), gb.end())) throw Error(AIMX_E_INTERNAL, "near chunks not in group order");
+    std::vector<int32_t> cp1((size_t)n1 + 1);
+    for (int j = 0; j <= n1; ++j) {
+      const int32_t target = (int32_t)((int64_t)ck.nchunk * j / n1);
+      cp1[(size_t)j] = *std::lower_bound(gb.begin(), gb.end(), target);
+    }
+    h.cta_ptr1 = dupload(c, cp1);
+    h.near_ctas1 = n1;
+  }
   const SetupDev& d = c->sd;
   if (f32) {
     k_lam_to<float4><<<nblk(nb * p3), 256, 0, c->stream>>>(nb * p3, wslot, d.lam, (float4*)nullptr, h.payload);

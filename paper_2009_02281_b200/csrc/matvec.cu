@@ -1217,6 +1217,18 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
   }
 }
 
+// shared-memory layout of k_interp_near1: NearCfg<float, 8, 1, PARTS>'s with the
+// stage sized for the context's chunk length (HALF: 8 CTAs per SM fit)
+template <bool PARTS, bool HALF> struct Near1Smem {
+  using K = NearCfg<float, 8, 1, PARTS>;
+  static constexpr int CH = K::CHC / (HALF ? 2 : 1);
+  static constexpr int STB = CH * 8 * 8 + CH * 4 + 16;
+  static constexpr size_t OFF_RED = (size_t)K::NDS * STB;
+  static constexpr size_t OFF_DESC = (OFF_RED + K::REDB + 15) / 16 * 16;
+  static constexpr size_t OFF_BAR = OFF_DESC + K::NDD * 16;
+  static constexpr size_t SMEM = OFF_BAR + K::NDS * 8;
+};
+
 // S4+S5, ONE column, c64, R = 8 rows per group (the single matvec of a GMRES
 // iteration: HBM-bound on the coefficient stream).  The same chunk payload
 // and TMA ring as k_interp_near, but the lanes split an entry's rows instead
@@ -1230,7 +1242,7 @@ __global__ void __launch_bounds__(128, near_ctas_per_sm(sizeof(T) == 4, BB == 1,
 // with 16 shuffles per lane instead of 80.  The gathered x / potential values
 // of chunk k + 1 load while chunk k computes.
 template <bool PARTS, bool HALF>
-__global__ void __launch_bounds__(128, 5)
+__global__ void __launch_bounds__(128, near1_ctas_per_sm(HALF))
     k_interp_near1(HotDev h, const float2* __restrict__ xt, float2* __restrict__ y0, float2* __restrict__ y1,
                    Combine cb) {
   pdl_wait();
@@ -1242,13 +1254,15 @@ __global__ void __launch_bounds__(128, 5)
   constexpr int PC = K::CHC / 32 / (HALF ? 2 : 1);   // C passes: 32 entries per pass
   constexpr int PW = K::CHW / 16 / (HALF ? 2 : 1);   // W passes: 16 entries per pass
   constexpr int NB = PC > 4 * PW ? PC : 4 * PW;
+  using SM = Near1Smem<PARTS, HALF>;
+  constexpr int STB = SM::STB;   // stage: one (half-length) chunk payload
   static_assert(K::CHC % 32 == 0 && K::CHW % 16 == 0 && NT == 128, "lane mapping");
   static_assert(K::REDB >= (size_t)(NT / 32) * NP * R * sizeof(float2), "partial sums");
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* const sdata = smem;                                         // [NDS][STB]
-  float2* const red = reinterpret_cast<float2*>(smem + K::OFF_RED);          // [warp][part][R]
-  int4* const sdesc = reinterpret_cast<int4*>(smem + K::OFF_DESC);           // [NDD]
-  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);      // [NDS]
+  float2* const red = reinterpret_cast<float2*>(smem + SM::OFF_RED);          // [warp][part][R]
+  int4* const sdesc = reinterpret_cast<int4*>(smem + SM::OFF_DESC);           // [NDD]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);      // [NDS]
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int c0 = h.cta_ptr1[blockIdx.x], nch = h.cta_ptr1[blockIdx.x + 1] - c0;
   if (nch <= 0) return;
@@ -1264,7 +1278,7 @@ __global__ void __launch_bounds__(128, 5)
     const uint32_t bytes = (uint32_t)(coef_bytes(d) + ((4 * d.w + 15) & ~15) + 16);
     sdesc[j % K::NDD] = d;
     mbar_arrive_expect_tx(bj, bytes);
-    bulk_g2s(sdata + (j % K::NDS) * K::STB, h.payload + (int64_t)d.z * 16, bytes, bj);
+    bulk_g2s(sdata + (j % K::NDS) * STB, h.payload + (int64_t)d.z * 16, bytes, bj);
   };
   if (tid < K::NDS) mbar_init(bar + tid, 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1309,14 +1323,14 @@ __global__ void __launch_bounds__(128, 5)
   gather(sdesc[0], sdata, nbuf);
   for (int k = 0; k < nch; ++k) {
     const int4 d = sdesc[k % K::NDD];
-    const unsigned char* stg = sdata + (k % K::NDS) * K::STB;
+    const unsigned char* stg = sdata + (k % K::NDS) * STB;
     if (tid == 0 && k + D < nch)
       issue(k + D, *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15)));
 #pragma unroll
     for (int i = 0; i < NB; ++i) buf[i] = nbuf[i];
     if (k + 1 < nch) {
       mbar_wait(bar + (k + 1) % K::NDS, (uint32_t)((k + 1) / K::NDS) & 1u);
-      gather(sdesc[(k + 1) % K::NDD], sdata + ((k + 1) % K::NDS) * K::STB, nbuf);
+      gather(sdesc[(k + 1) % K::NDD], sdata + ((k + 1) % K::NDS) * STB, nbuf);
     }
     if (d.y & 1) {   // near correction: [e][R] (C_A, C_rho) pairs
       const float4* __restrict__ cf = reinterpret_cast<const float4*>(stg);
@@ -1856,16 +1870,18 @@ void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Comb
   if (c.B == 1) {   // single column, staged in xt by run_interleave
     if constexpr (sizeof(T) == 4 && R == 8) {   // c64: rows split over lanes
       if (!h.near1_old) {
-        using K = NearCfg<float, 8, 1, false>;
-        using KP = NearCfg<float, 8, 1, true>;
         auto go = [&](auto kern, size_t smem) {
           set_smem(kern, smem);
-          launch_pdl(kern, dim3((unsigned)h.near_ctas1), dim3(K::NT), smem, s, h, (const float2*)h.xt, (float2*)y0,
+          launch_pdl(kern, dim3((unsigned)h.near_ctas1), dim3(128), smem, s, h, (const float2*)h.xt, (float2*)y0,
                      (float2*)y1, c);
         };
-        const bool half = h.near_half != 0;   // near_chc / near_chw of this context's payload
-        if (c.mode == 1) half ? go(k_interp_near1<true, true>, KP::SMEM) : go(k_interp_near1<true, false>, KP::SMEM);
-        else half ? go(k_interp_near1<false, true>, K::SMEM) : go(k_interp_near1<false, false>, K::SMEM);
+        if (h.near_half) {   // near_chc / near_chw of this context's payload
+          if (c.mode == 1) go(k_interp_near1<true, true>, Near1Smem<true, true>::SMEM);
+          else go(k_interp_near1<false, true>, Near1Smem<false, true>::SMEM);
+        } else {
+          if (c.mode == 1) go(k_interp_near1<true, false>, Near1Smem<true, false>::SMEM);
+          else go(k_interp_near1<false, false>, Near1Smem<false, false>::SMEM);
+        }
         AIMX_CHECK_LAUNCH();
         return;
       }
