@@ -541,6 +541,29 @@ def run_aimx(a):
     torch.cuda.synchronize()
     mv_ms = e0.elapsed_time(e1) / nmv
     matvec_per_s = (1 if a.mode == "slab" else world) * 1e3 / max_over_ranks(mv_ms)
+    # the single-column matvec is HBM-bound on the near-matrix stream: its
+    # S4+S5 launch (k_interp_near1 in c64) against the copy peak, from the
+    # library's stage profiler over 20 more matvecs (untimed above)
+    matvec_roofline = None
+    if a.mode != "slab":
+        op.profile_enable(True)
+        for _ in range(20):
+            op.matvec(x0, y0)
+        torch.cuda.synchronize()
+        pr1 = op.profile_read()
+        op.profile_enable(False)
+        sb1 = stage_bytes(st, prec, 1)
+        n_ms, n_n = pr1["interp_near"]
+        if n_n > 0:
+            mv_stage_ms = sum(v[0] for k, v in pr1.items() if k != "kernels")
+            matvec_roofline = {"bound": "hbm", "kernel": "interp_near (single column)", "unit": "GB/s",
+                               "algorithmic_bytes_per_launch": sb1["interp_near"],
+                               "ms_per_launch": n_ms / n_n, "launches_timed": n_n,
+                               "achieved": sb1["interp_near"] / (n_ms / n_n * 1e-3) / 1e9,
+                               "peak": roofline["peak"],
+                               "frac": sb1["interp_near"] / (n_ms / n_n * 1e-3) / 1e9 / roofline["peak"],
+                               "share_of_matvec": n_ms / mv_stage_ms if mv_stage_ms > 0 else None,
+                               "ms_per_matvec": mv_ms}
 
     # end to end: the same sweep through the C ABI with HOST buffers (pinned)
     Xp = Xh.pin_memory()
@@ -607,7 +630,7 @@ def run_aimx(a):
                        "parallelism": f"slab-fft x{world}" if a.mode == "slab" else f"freq-shard x{world}",
                        "l2": "flushed between timed steps (256 MB write); inputs resident in HBM",
                        "setup_seconds": st["setup_seconds"], "linear_term": bool(a.linear_term)},
-            "matvec_per_s": matvec_per_s,
+            "matvec_per_s": matvec_per_s, "matvec_roofline": matvec_roofline,
             "sustained": {"value": sus, "unit": UNIT, "reps": m["sustained_reps"],
                           "seconds": m["sustained_ms"] / 1e3,
                           "note": "back-to-back sweeps without the L2 flush (inputs exceed L2)"},
