@@ -330,6 +330,8 @@ struct HotDev {
   int32_t* chunks = nullptr;     // [nchunk][4] NearChunks work list
   int32_t* cta_ptr = nullptr;    // [near_ctas+1] whole-group chunk ranges per CTA (batched launches)
   int near_ctas = 0;
+  int32_t* warp_ptr1 = nullptr;  // [near_warps1+1] chunk ranges of whole groups per WARP (k_interp_near1w), or null
+  int near_warps1 = 0;
   int32_t* cta_ptr1 = nullptr;   // [near_ctas1+1] the same for single-column launches
   int near_ctas1 = 0;
   // grid buffers (complex, 4 channels innermost), `batch` slots each

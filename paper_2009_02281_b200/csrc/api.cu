@@ -478,6 +478,19 @@ void build_near(aimx_ctx* c, HotDev& h, const std::vector<int32_t>& rows) {
     }
     h.cta_ptr1 = dupload(c, cp1);
     h.near_ctas1 = n1;
+    // k_interp_near1w: one range per warp, 4 CTAs of 4 warps per SM
+    // (AIMX_NEAR1_WARP=0: keep the CTA-per-range kernel, A/B)
+    const char* w1 = std::getenv("AIMX_NEAR1_WARP");
+    if (!(w1 && w1[0] == '0')) {
+      const int nw = 16 * nsm_near;
+      std::vector<int32_t> wp((size_t)nw + 1);
+      for (int j = 0; j <= nw; ++j) {
+        const int32_t target = (int32_t)((int64_t)ck.nchunk * j / nw);
+        wp[(size_t)j] = *std::lower_bound(gb.begin(), gb.end(), target);
+      }
+      h.warp_ptr1 = dupload(c, wp);
+      h.near_warps1 = nw;
+    }
   }
   const SetupDev& d = c->sd;
   if (f32) {

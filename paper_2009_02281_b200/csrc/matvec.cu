@@ -1420,6 +1420,170 @@ __global__ void __launch_bounds__(128, near1_ctas_per_sm(HALF))
   }
 }
 
+// S4+S5, ONE column, c64, R = 8, 32-slot contexts (half-length chunks): the
+// warp-private form of k_interp_near1.  Each WARP walks its own contiguous
+// range of whole groups (warp_ptr1) through its own 3-stage TMA ring and
+// mbarriers: no block barrier anywhere, a group ends inside the warp (shuffles,
+// lanes 0..7 store the 8 rows), and the per-chunk bookkeeping (wait,
+// descriptor, refill) is paid once per chunk instead of once per warp and
+// chunk.  A stage is refilled (chunk k + D, whose descriptor rides in chunk
+// k's payload) right after the warp has consumed it.  Lanes: C chunks 4 lanes
+// per entry (lane q: rows 2q, 2q+1), 8 entries per pass; W chunks 8 lanes per
+// entry (lane r: row r), 4 entries per pass; a chunk's gathers are all issued
+// before its arithmetic.
+struct Near1W {
+  static constexpr int NT = 128, NW = NT / 32, PER_SM = 4;
+  static constexpr int CH = 64, CW = 16;                 // near_chc / near_chw at 32 slots
+  static constexpr int STB = CH * 8 * 8 + CH * 4 + 16;   // one chunk payload
+  static constexpr int NS = kNearD;                      // stages per warp
+  static constexpr size_t OFF_DESC = (size_t)NW * NS * STB;
+  static constexpr size_t OFF_BAR = OFF_DESC + (size_t)NW * NS * 16;
+  static constexpr size_t SMEM = OFF_BAR + (size_t)NW * NS * 8;
+};
+
+template <bool PARTS>
+__global__ void __launch_bounds__(Near1W::NT, Near1W::PER_SM)
+    k_interp_near1w(HotDev h, const float2* __restrict__ xt, float2* __restrict__ y0, float2* __restrict__ y1,
+                    Combine cb) {
+  pdl_wait();
+  pdl_trigger();
+  using K = Near1W;
+  constexpr int R = 8, D = kNearD, NS = K::NS, STB = K::STB, NP = PARTS ? 2 : 1;
+  constexpr int PC = K::CH / 8, PW = K::CW / 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* const sdata = smem + (size_t)wib * NS * STB;                         // [NS][STB]
+  int4* const sdesc = reinterpret_cast<int4*>(smem + K::OFF_DESC) + wib * NS;         // [NS]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR) + wib * NS;    // [NS]
+  const int wid = blockIdx.x * K::NW + wib;
+  const int c0 = h.warp_ptr1[wid], nch = h.warp_ptr1[wid + 1] - c0;
+  if (nch <= 0) return;
+  const int4* __restrict__ chunks = reinterpret_cast<const int4*>(h.chunks) + c0;
+  const int nc = h.nc;
+  const int64_t ns = (int64_t)h.batch * nc;
+  const float2* __restrict__ phi = (const float2*)h.phi;
+  const float be = PARTS ? 0.f : (float)cb.beta[0];
+  const float al = (float)cb.alpha_im[0];
+
+  auto coef_bytes = [&](const int4& d) -> int { return d.w * R * ((d.y & 1) ? 8 : 16); };
+  auto issue = [&](int j, const int4& d) {   // lane 0
+    uint64_t* bj = bar + j % NS;
+    const uint32_t bytes = (uint32_t)(coef_bytes(d) + ((4 * d.w + 15) & ~15) + 16);
+    sdesc[j % NS] = d;
+    mbar_arrive_expect_tx(bj, bytes);
+    bulk_g2s(sdata + (j % NS) * STB, h.payload + (int64_t)d.z * 16, bytes, bj);
+  };
+  if (lane == 0) {
+    for (int j = 0; j < NS; ++j) mbar_init(bar + j, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int j = 0; j < D && j < nch; ++j) issue(j, chunks[j]);
+  }
+  __syncwarp();
+
+  const int ec = lane >> 2, qc = lane & 3;   // C: entry of pass 0, row pair
+  const int ew = lane >> 3, rw = lane & 7;   // W: entry of pass 0, row
+  float2 aC[2 * NP], aW[NP];
+#pragma unroll
+  for (int j = 0; j < 2 * NP; ++j) aC[j] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < NP; ++j) aW[j] = make_float2(0.f, 0.f);
+
+  for (int k = 0; k < nch; ++k) {
+    mbar_wait(bar + k % NS, (uint32_t)(k / NS) & 1u);
+    const int4 d = sdesc[k % NS];
+    const unsigned char* stg = sdata + (k % NS) * STB;
+    const int* ix = reinterpret_cast<const int*>(stg + coef_bytes(d));
+    const int4 dn = *reinterpret_cast<const int4*>(stg + coef_bytes(d) + ((4 * d.w + 15) & ~15));
+    if (d.y & 1) {   // near correction: [e][R] (C_A, C_rho) pairs
+      const float4* __restrict__ cf = reinterpret_cast<const float4*>(stg);
+      float2 b[PC];
+#pragma unroll
+      for (int i = 0; i < PC; ++i) {
+        const int e = ec + 8 * i;
+        if (e < d.w) b[i] = __ldg(xt + ix[e]);
+      }
+#pragma unroll
+      for (int i = 0; i < PC; ++i) {
+        const int e = ec + 8 * i;
+        if (e >= d.w) break;
+        const float4 f = cf[e * 4 + qc];
+        if constexpr (PARTS) {
+          axpy(aC[0], f.x, b[i]);
+          axpy(aC[2], f.y, b[i]);
+          axpy(aC[1], f.z, b[i]);
+          axpy(aC[3], f.w, b[i]);
+        } else {
+          axpy(aC[0], f.x - be * f.y, b[i]);
+          axpy(aC[1], f.z - be * f.w, b[i]);
+        }
+      }
+    } else {         // interpolation: [e][R] real4 weights
+      const float4* __restrict__ wf = reinterpret_cast<const float4*>(stg);
+      float2 b[4 * PW];
+#pragma unroll
+      for (int i = 0; i < PW; ++i) {
+        const int e = ew + 4 * i;
+        if (e < d.w) {
+          const float2* pr = phi + (int64_t)ix[e] * ns;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)   // nc = 3: slot 2 holds rho
+            if (c < nc) b[4 * i + c] = __ldg(pr + (int64_t)c * h.batch);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < PW; ++i) {
+        const int e = ew + 4 * i;
+        if (e >= d.w) break;
+        const float4 w = wf[e * 8 + rw];
+        axpy(aW[0], w.x, b[4 * i]);
+        axpy(aW[0], w.y, b[4 * i + 1]);
+        if (nc == 4) axpy(aW[0], w.z, b[4 * i + 2]);
+        const float2 rho = nc == 4 ? b[4 * i + 3] : b[4 * i + 2];
+        if constexpr (PARTS) axpy(aW[1], w.w, rho);
+        else axpy(aW[0], -be * w.w, rho);
+      }
+    }
+    if (d.y & 4) {   // last chunk of group d.x: reduce inside the warp, combine, store
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < 2 * NP; ++j) {
+          aC[j].x += __shfl_xor_sync(0xffffffffu, aC[j].x, o);
+          aC[j].y += __shfl_xor_sync(0xffffffffu, aC[j].y, o);
+        }
+#pragma unroll
+      for (int o = 8; o < 32; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          aW[j].x += __shfl_xor_sync(0xffffffffu, aW[j].x, o);
+          aW[j].y += __shfl_xor_sync(0xffffffffu, aW[j].y, o);
+        }
+      const int m = lane < R ? h.grp_rows[(int64_t)d.x * R + lane] : -1;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {   // row r = lane (< 8): its C sums sit in lane r >> 1, slot r & 1
+        const int src = (lane >> 1) & 3;
+        const float a0x = __shfl_sync(0xffffffffu, aC[2 * p].x, src), a0y = __shfl_sync(0xffffffffu, aC[2 * p].y, src);
+        const float a1x = __shfl_sync(0xffffffffu, aC[2 * p + 1].x, src), a1y = __shfl_sync(0xffffffffu, aC[2 * p + 1].y, src);
+        const float2 sum = make_float2(aW[p].x + ((lane & 1) ? a1x : a0x), aW[p].y + ((lane & 1) ? a1y : a0y));
+        if (m >= 0) {
+          if constexpr (PARTS) {
+            float2* y = p ? y1 : y0;
+            if (y) y[m] = p ? make_float2(-sum.x, -sum.y) : sum;
+          } else {   // (j alpha) u: re = -alpha u.im, im = alpha u.re
+            y0[m] = make_float2(-al * sum.y, al * sum.x);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) aC[j] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) aW[j] = make_float2(0.f, 0.f);
+    }
+    __syncwarp();   // every lane is done with stage k % NS: refill it
+    if (lane == 0 && k + D < nch) issue(k + D, dn);
+  }
+}
+
 // S4+S5 on the tensor cores (c64 batched launches, BB = 8/16/32 columns).
 // The same chunk payload and TMA ring as k_interp_near; per row group the
 // contraction is done as  D^T[2BB x 2R] += X^T[2BB x K] . C^T[K x 2R]  with
@@ -1875,6 +2039,17 @@ void run_interp_r(const HotDev& h, const void* x, void* y0, void* y1, const Comb
           launch_pdl(kern, dim3((unsigned)h.near_ctas1), dim3(128), smem, s, h, (const float2*)h.xt, (float2*)y0,
                      (float2*)y1, c);
         };
+        if (h.near_half && h.warp_ptr1) {   // warp-private rings (32-slot contexts)
+          auto gow = [&](auto kern) {
+            set_smem(kern, Near1W::SMEM);
+            launch_pdl(kern, dim3((unsigned)(h.near_warps1 / Near1W::NW)), dim3(Near1W::NT), Near1W::SMEM, s, h,
+                       (const float2*)h.xt, (float2*)y0, (float2*)y1, c);
+          };
+          if (c.mode == 1) gow(k_interp_near1w<true>);
+          else gow(k_interp_near1w<false>);
+          AIMX_CHECK_LAUNCH();
+          return;
+        }
         if (h.near_half) {   // near_chc / near_chw of this context's payload
           if (c.mode == 1) go(k_interp_near1<true, true>, Near1Smem<true, true>::SMEM);
           else go(k_interp_near1<false, true>, Near1Smem<false, true>::SMEM);

@@ -1,5 +1,5 @@
-"""GPU parity of the single-column S4+S5 kernel (k_interp_near1: c64, lanes
-split an entry's rows; eq:LAIMx P:283, eq:EFIEAIMx P:288, W = P^T P:198)
+"""GPU parity of the single-column S4+S5 kernel (k_interp_near1 and its warp-private form
+k_interp_near1w: c64, lanes split an entry's rows; eq:LAIMx P:283, eq:EFIEAIMx P:288, W = P^T P:198)
 against the fp64 oracle, in both of its chunk-length variants (32-slot
 contexts: half-length chunks, 8 CTAs per SM; fewer slots: full-length chunks),
 on a planar mesh (3 stored channels) and a closed mesh (4 channels), combined
@@ -23,12 +23,15 @@ MESHES = {
 }
 
 
-@pytest.mark.parametrize("slots", [32, 8])
+# (slots, AIMX_NEAR1_WARP): 32 slots -> the warp-private form k_interp_near1w
+# (default) or the CTA form k_interp_near1<., HALF>; 8 slots -> k_interp_near1
+@pytest.mark.parametrize("slots,warp", [(32, "1"), (32, "0"), (8, "1")])
 @pytest.mark.parametrize("which", ["planar", "closed"])
-def test_near1_matvec_vs_oracle_and_old_kernel(which, slots, monkeypatch):
+def test_near1_matvec_vs_oracle_and_old_kernel(which, slots, warp, monkeypatch):
     from oracle.aimx import AIMxOracle
     mesh, n = MESHES[which]()
     monkeypatch.setenv("AIMX_BATCH", str(slots))      # read by the library at setup
+    monkeypatch.setenv("AIMX_NEAR1_WARP", warp)
     op = make_gpu_op(mesh, n, "c64")
     assert op.stats()["batch_slots"] == slots
     monkeypatch.setenv("AIMX_NEAR1_OLD", "1")
