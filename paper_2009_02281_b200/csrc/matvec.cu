@@ -1436,6 +1436,7 @@ struct Near1W {
   static constexpr int CH = 64, CW = 16;                 // near_chc / near_chw at 32 slots
   static constexpr int STB = CH * 8 * 8 + CH * 4 + 16;   // one chunk payload
   static constexpr int NS = kNearD;                      // stages per warp
+  static_assert(CH == near_chc(true, 32) && CW == near_chw(true, 32), "chunk lengths of 32-slot c64 contexts");
   static constexpr size_t OFF_DESC = (size_t)NW * NS * STB;
   static constexpr size_t OFF_BAR = OFF_DESC + (size_t)NW * NS * 16;
   static constexpr size_t SMEM = OFF_BAR + (size_t)NW * NS * 8;
